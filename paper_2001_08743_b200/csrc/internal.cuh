@@ -1,0 +1,207 @@
+// Internal definitions shared by the libktune_cuda translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ktune_cuda.h"
+
+namespace kt {
+
+constexpr int kMaxKnobs = 32;   // device kernels keep one config in registers/smem
+constexpr int kMaxRuleOps = 64; // postfix program length passed by value
+constexpr int kMaxK = 64;       // k-means clusters (sweep is [8, 64))
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define KT_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      ::kt::fail(e_ == cudaErrorMemoryAllocation ? KTUNE_ERR_NOMEM : KTUNE_ERR_CUDA,      \
+                 std::string(#call) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+
+// Device buffer owned by a context workspace slot (grow-only).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      KT_CUDA(cudaMalloc(&p, need < 256 ? 256 : need));
+      bytes = need < 256 ? 256 : need;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      bytes = 0;
+      KT_CUDA(cudaMallocHost(&p, need < 4096 ? 4096 : need));
+      bytes = need < 4096 ? 4096 : need;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+enum WsSlot {
+  WS_IN0, WS_IN1, WS_IN2, WS_OUT0, WS_OUT1, WS_OUT2, WS_OUT3, WS_OUT4,
+  WS_D2, WS_D2B, WS_ASSIGN, WS_ASSIGN2, WS_MEMBERS, WS_BLOCK, WS_BLOCK2, WS_CENT, WS_CENT2,
+  WS_SCRATCH, WS_SCRATCH2, WS_KPP, WS_SNAP, WS_VALID, WS_TASKS, WS_BEST_ASSIGN, WS_BEST_D2,
+  WS_PREV_ASSIGN, WS_PREV_D2, WS_NUM_SLOTS
+};
+
+}  // namespace kt
+
+struct ktune_ctx {
+  int device = 0;
+  int rank = 0;
+  int world = 1;
+  void* nccl = nullptr;  // ncclComm_t
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  int64_t opt_force_exact = 0;
+  int64_t opt_kmeans_mode = 0;
+  int64_t stats[16] = {0};
+  kt::DevBuf ws[kt::WS_NUM_SLOTS];
+  kt::HostBuf pinned[4];
+  void* dev(int slot, size_t bytes) { return ws[slot].get(bytes); }
+  void* host(int slot, size_t bytes) { return pinned[slot].get(bytes); }
+  void count_launch(int n = 1) { stats[KTUNE_STAT_LAUNCHES] += n; }
+};
+
+// Device-side view of a design space, passed to kernels by value.
+struct KtSpaceParams {
+  int32_t D;
+  int32_t nops;
+  int32_t card[kt::kMaxKnobs];
+  int32_t lut_off[kt::kMaxKnobs + 1];  // offsets into the feature LUT (sum of cards)
+  int32_t val_off[kt::kMaxKnobs + 1];  // offsets into the knob values
+  const double* lut;                   // feature LUT: idx / (card - 1) (0 for card 1)
+  const int64_t* values;               // knob values (validity rule operands)
+  int32_t op_code[kt::kMaxRuleOps];
+  int64_t op_arg[kt::kMaxRuleOps];
+};
+
+struct ktune_space {
+  ktune_ctx* ctx = nullptr;
+  int D = 0;
+  std::vector<int32_t> card;
+  std::vector<int64_t> values;
+  std::vector<int64_t> val_off;
+  std::vector<ktune_rule_op> ops;
+  std::vector<double> lut;  // host copy of the feature LUT
+  unsigned __int128 size = 0;
+  double* d_lut = nullptr;
+  int64_t* d_values = nullptr;
+  KtSpaceParams params{};
+  int lut_total = 0;
+  bool validate(const int32_t* idx) const;
+};
+
+// Complete-tree layout of a GBT ensemble.
+struct ktune_gbt {
+  ktune_ctx* ctx = nullptr;
+  int num_trees = 0;
+  int num_features = 0;
+  int depth = 0;          // padded depth of every tree (complete binary trees)
+  double base = 0.0;
+  double lr = 0.0;
+  bool has_space = false;
+  int D = 0;
+  int idx_card_max = 0;
+  // device arrays
+  uint32_t* d_inode_idx = nullptr;  // [T][2^depth - 1] (feature << 16) | idx threshold
+  double* d_inode_thr = nullptr;    // [T][2^depth - 1] fp64 thresholds (feature path)
+  int32_t* d_inode_feat = nullptr;  // [T][2^depth - 1]
+  double* d_leaf = nullptr;         // [T][2^depth]
+  // generic pointer-walk layout when depth > kMaxCompleteDepth
+  int32_t* d_offsets = nullptr;
+  ktune_tree_node* d_nodes = nullptr;
+  bool complete = true;
+};
+
+struct ktune_ac {
+  ktune_ctx* ctx = nullptr;
+  int n = 0, h = 0, g = 0;
+  int64_t num_params = 0;
+  double* d_params = nullptr;
+  std::vector<double> host_params;
+};
+
+namespace kt {
+
+// ---------------------------------------------------------------- helpers
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int sm_count(ktune_ctx* ctx);
+
+// Copy host->device (when !device) through pinned staging, returns device ptr.
+const void* stage_in(ktune_ctx* ctx, int slot, const void* src, size_t bytes, bool device);
+void* out_buf(ktune_ctx* ctx, int slot, void* dst, size_t bytes, bool device);
+void stage_out(ktune_ctx* ctx, void* dst, const void* dev, size_t bytes, bool device);
+
+void check_launch(ktune_ctx* ctx, const char* what, int n = 1);
+void allreduce_sum(ktune_ctx* ctx, void* buf, size_t count, bool is_double);
+void allgather(ktune_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank);
+
+}  // namespace kt
+
+void kt_nccl_destroy(ktune_ctx* ctx);
+
+namespace kt {
+
+}  // namespace kt
+
+// Run `body` converting exceptions to status codes.
+template <class F>
+int kt_guard(ktune_ctx* ctx, F&& body) {
+  try {
+    body();
+    return KTUNE_OK;
+  } catch (const kt::Error& e) {
+    if (ctx) ctx->last_error = e.what();
+    extern thread_local std::string kt_tls_error;
+    kt_tls_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->last_error = "host allocation failed";
+    return KTUNE_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    extern thread_local std::string kt_tls_error;
+    kt_tls_error = e.what();
+    return KTUNE_ERR_BACKEND;
+  }
+}

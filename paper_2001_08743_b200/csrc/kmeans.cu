@@ -1,0 +1,1123 @@
+// K3-K6: k-means for Adaptive Sampling (sampling.cpp:39-175, 202-235, 409-452).
+//
+// Exactness contract:
+//  * per-point squared distances are computed exactly as the reference
+//    (strided Eigen rows => sequential over knobs, no FMA), so every
+//    assignment and every d2 value is bit-identical;
+//  * centroids are the reference's exact-order sums: members of each cluster
+//    are gathered in ascending point order (stable counting sort) and one
+//    thread per (cluster, knob) accumulates them sequentially (mode A);
+//  * order-sensitive REDUCTIONS that only feed decisions (the kmeans++ total
+//    and cumulative scan, restart selection, the sweep's break test) are
+//    computed in parallel with a rigorous error bound; a decision whose
+//    outcome is not certified by the bound is re-decided by an exact
+//    sequential chain that reproduces the reference order bit-for-bit.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "device.cuh"
+#include "internal.cuh"
+
+namespace {
+
+constexpr int kChunk = 1024;  // points per block-sum chunk (kmeans++ / loss)
+constexpr int kBT = 256;      // threads per block for point kernels
+constexpr double kU = 1.1102230246251565e-16;  // 2^-53
+
+template <class IdxT>
+__device__ __forceinline__ double feat(const KtSpaceParams& sp, const double* lut_s, const IdxT* p, int d) {
+  return lut_s[sp.lut_off[d] + (int)p[d]];
+}
+
+// Sequential squared distance.
+template <class IdxT>
+__device__ __forceinline__ double row_d2(const KtSpaceParams& sp, const double* lut, const IdxT* p,
+                                         const double* c, int D) {
+  double t = kt::dsub(feat(sp, lut, p, 0), c[0]);
+  double s = kt::dmul(t, t);
+  for (int d = 1; d < D; ++d) {
+    t = kt::dsub(feat(sp, lut, p, d), c[d]);
+    s = kt::dadd(s, kt::dmul(t, t));
+  }
+  return s;
+}
+
+// Block reduction (sum) of a double in deterministic tree order.
+__device__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) v = kt::dadd(v, __shfl_down_sync(0xffffffff, v, o));
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  if (w == 0) {
+    v = lane < nw ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = kt::dadd(v, __shfl_down_sync(0xffffffff, v, o));
+  }
+  __syncthreads();
+  return v;  // valid in thread 0
+}
+
+// Load the feature LUT into shared memory.
+__device__ const double* stage_lut(const KtSpaceParams& sp, double* s_lut, int lut_total) {
+  for (int i = threadIdx.x; i < lut_total; i += blockDim.x) s_lut[i] = sp.lut[i];
+  return s_lut;
+}
+
+// ------------------------------------------------------------------ kmeans++ (K5)
+struct KppState {
+  uint64_t rng;
+  int64_t pick;
+  int32_t fallbacks;
+  int32_t pad;
+};
+
+// d2[i] = (first ? v : min(d2[i], v)), v = |p_i - centroid c|^2, plus chunk sums.
+template <class IdxT>
+__global__ void __launch_bounds__(kBT) kpp_d2_kernel(KtSpaceParams sp, int lut_total,
+                                                     const IdxT* __restrict__ pts, int64_t N,
+                                                     const KppState* __restrict__ st,
+                                                     double* __restrict__ cent, int c, int first,
+                                                     double* __restrict__ d2,
+                                                     double* __restrict__ chunk_sum) {
+  extern __shared__ double sdyn[];
+  __shared__ double red[32];
+  __shared__ double cs[kt::kMaxKnobs];
+  const double* lut = stage_lut(sp, sdyn, lut_total);
+  const int D = sp.D;
+  const int64_t pick = st->pick;
+  if (threadIdx.x < D) {
+    const double v = lut[sp.lut_off[threadIdx.x] + (int)pts[pick * D + threadIdx.x]];
+    cs[threadIdx.x] = v;
+    if (blockIdx.x == 0) cent[c * D + threadIdx.x] = v;
+  }
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  double part = 0.0;
+  for (int j = 0; j < kChunk / kBT; ++j) {
+    const int64_t i = base + j * kBT + threadIdx.x;
+    if (i < N) {
+      const double v = row_d2(sp, lut, pts + i * D, cs, D);
+      double o = v;
+      if (!first) {
+        const double old = d2[i];
+        o = v < old ? v : old;  // std::min(d2, v) (sampling.cpp:92)
+      }
+      d2[i] = o;
+      part = kt::dadd(part, o);
+    }
+  }
+  const double s = block_sum(part, red);
+  if (threadIdx.x == 0) chunk_sum[blockIdx.x] = s;
+}
+
+__device__ __forceinline__ double gamma_bound(double terms) { return terms * kU * 1.0625; }
+
+// Exact reference order for the kmeans++ total (Eigen contiguous sum, A.3) and
+// cumulative scan (sampling.cpp:74-88). Run by thread 0..3 of one block.
+__device__ void kpp_exact(const double* __restrict__ d2, int64_t N, uint64_t& rng, double* lanes,
+                          int64_t* pick_out) {
+  const int t = threadIdx.x;
+  const int64_t aligned2 = (N / 4) * 4, aligned = (N / 2) * 2;
+  if (t < 4 && aligned > 2) {
+    double s = d2[t];
+    for (int64_t i = 4 + t; i < aligned2; i += 4) s = kt::dadd(s, d2[i]);
+    lanes[t] = s;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double total;
+    if (aligned == 0) {
+      total = d2[0];
+      for (int64_t i = 1; i < N; ++i) total = kt::dadd(total, d2[i]);
+    } else {
+      double a0 = d2[0], a1 = d2[1];
+      if (aligned > 2) {
+        a0 = kt::dadd(lanes[0], lanes[2]);
+        a1 = kt::dadd(lanes[1], lanes[3]);
+        if (aligned > aligned2) {
+          a0 = kt::dadd(a0, d2[aligned2]);
+          a1 = kt::dadd(a1, d2[aligned2 + 1]);
+        }
+      }
+      total = kt::dadd(a0, a1);
+      for (int64_t i = aligned; i < N; ++i) total = kt::dadd(total, d2[i]);
+    }
+    int64_t pick;
+    if (total <= 0.0) {
+      pick = (int64_t)kt::rng_below(rng, (uint64_t)N);
+    } else {
+      const double r = kt::dmul(kt::rng_uniform01(rng), total);
+      double cum = 0.0;
+      pick = N - 1;
+      for (int64_t i = 0; i < N; ++i) {
+        cum = kt::dadd(cum, d2[i]);
+        if (cum > r) {
+          pick = i;
+          break;
+        }
+      }
+    }
+    *pick_out = pick;
+  }
+  __syncthreads();
+}
+
+// One CTA of 1024 threads: decide the next kmeans++ pick.
+// mode 0: first pick (below(N)); mode 1: D^2 sampling; force_exact: always chain.
+__global__ void __launch_bounds__(1024) kpp_select_kernel(const double* __restrict__ d2,
+                                                          const double* __restrict__ chunk_sum,
+                                                          int64_t N, KppState* st, int mode,
+                                                          int force_exact,
+                                                          double* __restrict__ scratch) {
+  __shared__ double red[32];
+  __shared__ double lanes[4];
+  __shared__ double sh_u, sh_tot;
+  __shared__ int sh_branch;  // 0 below, 1 sample
+  __shared__ unsigned long long sh_ib, sh_ia;
+  __shared__ int sh_bfirst, sh_bsecond;
+  __shared__ int64_t sh_pick;
+  const int tid = threadIdx.x;
+  uint64_t rng = st->rng;
+  if (mode == 0) {
+    if (tid == 0) {
+      st->pick = (int64_t)kt::rng_below(rng, (uint64_t)N);
+      st->rng = rng;
+    }
+    return;
+  }
+  const int64_t nch = (N + kChunk - 1) / kChunk;
+  // total estimate + positivity (d2 >= 0, so total_ref > 0 iff some d2 > 0)
+  double part = 0.0;
+  for (int64_t b = tid; b < nch; b += blockDim.x) part = kt::dadd(part, chunk_sum[b]);
+  const double tot = block_sum(part, red);
+  if (tid == 0) {
+    sh_tot = tot;
+    // Any positive d2 <=> every chunk sum of non-negatives is 0 otherwise.
+    sh_branch = tot > 0.0 ? 1 : 0;
+    if (!force_exact) {
+      if (sh_branch == 0) {
+        st->pick = (int64_t)kt::rng_below(rng, (uint64_t)N);
+        st->rng = rng;
+      } else {
+        sh_u = kt::rng_uniform01(rng);
+        st->rng = rng;
+      }
+    }
+  }
+  __syncthreads();
+  if (force_exact) {
+    kpp_exact(d2, N, rng, lanes, &sh_pick);
+    if (tid == 0) {
+      st->pick = sh_pick;
+      st->rng = rng;
+      st->fallbacks += 1;
+    }
+    return;
+  }
+  if (sh_branch == 0) return;
+  const double u = sh_u, T = sh_tot;
+  const double lgN = (double)(64 - __clzll((unsigned long long)N)) + 16.0;
+  const double eT = gamma_bound((double)(N / 4) + lgN) * T;
+  const double r_est = kt::dmul(u, T);
+  const double r_err = kt::dadd(kt::dmul(u, eT), gamma_bound(4.0) * r_est);
+  const double r_lo = kt::dsub(r_est, r_err), r_hi = kt::dadd(r_est, r_err);
+  // chunk exclusive prefix (sequential per 1024-chunk slice, tree-free and
+  // simple: thread 0 scans up to nch chunk sums into scratch)
+  if (tid == 0) {
+    double p = 0.0;
+    for (int64_t b = 0; b < nch; ++b) {
+      scratch[b] = p;
+      p = kt::dadd(p, chunk_sum[b]);
+    }
+    sh_bfirst = -1;
+    sh_bsecond = -1;
+    sh_ib = ~0ull;
+    sh_ia = ~0ull;
+  }
+  __syncthreads();
+  // locate chunks: b_first = first chunk whose max (C_i + e_i) may exceed r_lo,
+  // b_second = first chunk whose end certainly exceeds r_hi.
+  for (int64_t b0 = 0; b0 < nch; b0 += blockDim.x) {
+    const int64_t b = b0 + tid;
+    if (b < nch) {
+      const double hi_val = kt::dadd(scratch[b], chunk_sum[b]);
+      const double e = gamma_bound((double)std::min<int64_t>(N, (b + 1) * kChunk) + lgN + 16.0) * hi_val;
+      if (kt::dadd(hi_val, e) > r_lo) atomicMin(&sh_ib, (unsigned long long)b);
+      if (kt::dsub(hi_val, e) > r_hi) atomicMin(&sh_ia, (unsigned long long)b);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    sh_bfirst = sh_ib == ~0ull ? -1 : (int)sh_ib;
+    sh_bsecond = sh_ia == ~0ull ? -1 : (int)sh_ia;
+    sh_ib = ~0ull;
+    sh_ia = ~0ull;
+  }
+  __syncthreads();
+  const int bfirst = sh_bfirst, bsecond = sh_bsecond;
+  bool certified = false;
+  int64_t pick = N - 1;
+  if (bfirst < 0) {
+    certified = true;  // cum never exceeds r: default N-1 (sampling.cpp:81)
+  } else if (bsecond < 0 || bsecond - bfirst <= 1) {
+    const int blast = bsecond < 0 ? bfirst : bsecond;
+    for (int b = bfirst; b <= blast; ++b) {
+      const int64_t i = (int64_t)b * kChunk + tid;
+      double v = i < N ? d2[i] : 0.0;
+      // inclusive block scan (Hillis-Steele through shared memory)
+      __shared__ double sc[1024];
+      sc[tid] = v;
+      __syncthreads();
+      for (int o = 1; o < 1024; o <<= 1) {
+        const double add = tid >= o ? sc[tid - o] : 0.0;
+        __syncthreads();
+        sc[tid] = kt::dadd(sc[tid], add);
+        __syncthreads();
+      }
+      if (i < N) {
+        const double C = kt::dadd(scratch[b], sc[tid]);
+        const double e = gamma_bound((double)(i + 1) + lgN + 16.0) * C;
+        if (kt::dadd(C, e) > r_lo) atomicMin(&sh_ib, (unsigned long long)i);
+        if (kt::dsub(C, e) > r_hi) atomicMin(&sh_ia, (unsigned long long)i);
+      }
+      __syncthreads();
+    }
+    if (sh_ia != ~0ull && sh_ib == sh_ia) {
+      certified = true;
+      pick = (int64_t)sh_ia;
+    }
+  }
+  if (certified) {
+    if (tid == 0) st->pick = pick;
+    return;
+  }
+  // exact fallback: re-run the reference order (rng state rewound to before
+  // the uniform01 draw: the branch is identical, the draw is repeated).
+  uint64_t r0 = st[0].rng;  // already advanced by one draw
+  r0 -= 0x9E3779B97F4A7C15ULL;
+  kpp_exact(d2, N, r0, lanes, &sh_pick);
+  if (tid == 0) {
+    st->pick = sh_pick;
+    st->rng = r0;
+    st->fallbacks += 1;
+  }
+}
+
+// ------------------------------------------------------------------ assign (K3)
+// Exact argmin over centroids (strict <, lowest index wins ties,
+// sampling.cpp:39-54); writes d2 of the chosen centroid, the number of
+// changed assignments and per-chunk loss partial sums.
+template <class IdxT>
+__global__ void __launch_bounds__(kBT) assign_kernel(KtSpaceParams sp, int lut_total,
+                                                     const IdxT* __restrict__ pts, int64_t N,
+                                                     const double* __restrict__ cent, int k,
+                                                     const int32_t* __restrict__ prev,
+                                                     int32_t* __restrict__ asg,
+                                                     double* __restrict__ d2,
+                                                     double* __restrict__ chunk_sum,
+                                                     unsigned long long* __restrict__ changed) {
+  extern __shared__ double sdyn[];
+  __shared__ double red[32];
+  const int D = sp.D;
+  double* s_cent = sdyn;
+  double* s_lut = sdyn + k * D;
+  for (int i = threadIdx.x; i < k * D; i += blockDim.x) s_cent[i] = cent[i];
+  const double* lut = stage_lut(sp, s_lut, lut_total);
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  double part = 0.0;
+  int nchg = 0;
+  for (int j = 0; j < kChunk / kBT; ++j) {
+    const int64_t i = base + j * kBT + threadIdx.x;
+    if (i < N) {
+      double x[kt::kMaxKnobs];
+      for (int d = 0; d < D; ++d) x[d] = feat(sp, lut, pts + i * D, d);
+      double best = INFINITY;
+      int bc = 0;
+      for (int c = 0; c < k; ++c) {
+        const double* cc = s_cent + c * D;
+        double t = kt::dsub(x[0], cc[0]);
+        double s = kt::dmul(t, t);
+        for (int d = 1; d < D; ++d) {
+          t = kt::dsub(x[d], cc[d]);
+          s = kt::dadd(s, kt::dmul(t, t));
+        }
+        if (s < best) {
+          best = s;
+          bc = c;
+        }
+      }
+      asg[i] = bc;
+      d2[i] = best;
+      part = kt::dadd(part, best);
+      if (prev && prev[i] != bc) ++nchg;
+    }
+  }
+  const double s = block_sum(part, red);
+  if (threadIdx.x == 0) chunk_sum[blockIdx.x] = s;
+  if (prev) {
+    for (int o = 16; o > 0; o >>= 1) nchg += __shfl_down_sync(0xffffffff, nchg, o);
+    if ((threadIdx.x & 31) == 0 && nchg) atomicAdd(changed, (unsigned long long)nchg);
+  }
+}
+
+// ------------------------------------------------------------------ centroid update (K4)
+// Stable counting sort of point ids by cluster (ascending point order inside
+// each cluster), then one thread per (cluster, knob) sums its members' features
+// in that order (sampling.cpp:110-121).
+__global__ void __launch_bounds__(kBT) hist_kernel(const int32_t* __restrict__ asg, int64_t N, int k,
+                                                   int32_t* __restrict__ blockcounts) {
+  __shared__ int cnt[kt::kMaxK];
+  for (int c = threadIdx.x; c < k; c += blockDim.x) cnt[c] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  for (int j = threadIdx.x; j < kChunk; j += blockDim.x) {
+    const int64_t i = base + j;
+    if (i < N) atomicAdd(&cnt[asg[i]], 1);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) blockcounts[(int64_t)blockIdx.x * k + c] = cnt[c];
+}
+
+// Exclusive scan over blocks per cluster; cluster totals and starts.
+__global__ void scan_counts_kernel(int32_t* __restrict__ blockcounts, int64_t nblocks, int k,
+                                   int32_t* __restrict__ counts, int32_t* __restrict__ cstart) {
+  const int c = threadIdx.x;
+  __shared__ int tot[kt::kMaxK];
+  if (c < k) {
+    int run = 0;
+    for (int64_t b = 0; b < nblocks; ++b) {
+      const int v = blockcounts[b * k + c];
+      blockcounts[b * k + c] = run;
+      run += v;
+    }
+    tot[c] = run;
+    counts[c] = run;
+  }
+  __syncthreads();
+  if (c == 0) {
+    int s = 0;
+    for (int j = 0; j < k; ++j) {
+      cstart[j] = s;
+      s += tot[j];
+    }
+  }
+}
+
+// Stable scatter: warp w of the block owns points [base + w*128, base + (w+1)*128).
+__global__ void __launch_bounds__(kBT) scatter_kernel(const int32_t* __restrict__ asg, int64_t N, int k,
+                                                      const int32_t* __restrict__ blockoffs,
+                                                      const int32_t* __restrict__ cstart,
+                                                      int32_t* __restrict__ members) {
+  constexpr int kWarps = kBT / 32;
+  constexpr int kPerWarp = kChunk / kWarps;  // 128 points = 4 rounds of 32
+  __shared__ int wcnt[kWarps][kt::kMaxK];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = lane; c < k; c += 32) wcnt[w][c] = 0;
+  __syncwarp();
+  const int64_t wbase = (int64_t)blockIdx.x * kChunk + w * kPerWarp;
+  // pass 1: per-warp histogram
+  for (int r = 0; r < kPerWarp / 32; ++r) {
+    const int64_t i = wbase + r * 32 + lane;
+    if (i < N) atomicAdd(&wcnt[w][asg[i]], 1);
+  }
+  __syncthreads();
+  // exclusive prefix over warps per cluster
+  if (threadIdx.x < k) {
+    const int c = threadIdx.x;
+    int run = 0;
+    for (int ww = 0; ww < kWarps; ++ww) {
+      const int v = wcnt[ww][c];
+      wcnt[ww][c] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  // pass 2: ranks in point order
+  for (int r = 0; r < kPerWarp / 32; ++r) {
+    const int64_t i = wbase + r * 32 + lane;
+    const bool ok = i < N;
+    const int c = ok ? asg[i] : -1 - lane;
+    const unsigned m = __match_any_sync(0xffffffff, c);
+    const int before = __popc(m & ((1u << lane) - 1));
+    if (ok) {
+      const int pos = cstart[c] + blockoffs[(int64_t)blockIdx.x * k + c] + wcnt[w][c] + before;
+      members[pos] = (int32_t)i;
+    }
+    __syncwarp();
+    if (ok && before == 0) wcnt[w][c] += __popc(m);
+    __syncwarp();
+  }
+}
+
+template <class IdxT>
+__global__ void chain_kernel(KtSpaceParams sp, const IdxT* __restrict__ pts,
+                             const int32_t* __restrict__ members,
+                             const int32_t* __restrict__ counts, const int32_t* __restrict__ cstart,
+                             int k, double* __restrict__ cent) {
+  const int D = sp.D;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= k * D) return;
+  const int c = tid / D, d = tid % D;
+  const int n = counts[c];
+  if (n == 0) return;  // empty cluster: handled by reseed
+  const int32_t* mem = members + cstart[c];
+  const double* lut = sp.lut + sp.lut_off[d];
+  double s = 0.0;  // MatrixXd::Zero then += (sampling.cpp:110,114)
+  int j = 0;
+  for (; j + 8 <= n; j += 8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldg(lut + (int)pts[(int64_t)mem[j + q] * D + d]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s = kt::dadd(s, v[q]);
+  }
+  for (; j < n; ++j) s = kt::dadd(s, __ldg(lut + (int)pts[(int64_t)mem[j] * D + d]));
+  cent[c * D + d] = kt::ddiv(s, (double)n);
+}
+
+// Empty clusters (sampling.cpp:122-136): in cluster order, the unclaimed
+// point farthest from its OLD centroid (strict >, first index on ties).
+template <class IdxT>
+__global__ void __launch_bounds__(1024) reseed_kernel(KtSpaceParams sp,
+                                                      const IdxT* __restrict__ pts, int64_t N,
+                                                      const int32_t* __restrict__ counts, int k,
+                                                      const double* __restrict__ d2_old,
+                                                      double* __restrict__ cent,
+                                                      int32_t* __restrict__ nempty) {
+  __shared__ int64_t claimed[kt::kMaxK];
+  __shared__ int nclaimed;
+  __shared__ double bv[32];
+  __shared__ int64_t bi[32];
+  const int D = sp.D;
+  if (threadIdx.x == 0) nclaimed = 0;
+  __syncthreads();
+  for (int c = 0; c < k; ++c) {
+    if (counts[c] > 0) continue;
+    double best = -1.0;
+    int64_t besti = 0;
+    bool have = false;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+      bool cl = false;
+      for (int q = 0; q < nclaimed; ++q) cl |= claimed[q] == i;
+      if (cl) continue;
+      const double v = d2_old[i];
+      if (!have || v > best) {  // per-thread indices ascend, so first max kept
+        best = v;
+        besti = i;
+        have = true;
+      }
+    }
+    if (!have) {
+      best = -INFINITY;
+      besti = INT64_MAX;
+    }
+    // (value desc, index asc) reduction
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffff, best, o);
+      const int64_t oi = __shfl_down_sync(0xffffffff, besti, o);
+      if (ov > best || (ov == best && oi < besti)) {
+        best = ov;
+        besti = oi;
+      }
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+      bv[w] = best;
+      bi[w] = besti;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = bv[0];
+      int64_t ii = bi[0];
+      for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+        if (bv[q] > b || (bv[q] == b && bi[q] < ii)) {
+          b = bv[q];
+          ii = bi[q];
+        }
+      // worst starts at -1.0 with strict >: all d2 >= 0, the first unclaimed point qualifies
+      claimed[nclaimed++] = ii;
+      for (int d = 0; d < D; ++d) cent[c * D + d] = sp.lut[sp.lut_off[d] + (int)pts[ii * D + d]];
+      atomicAdd(nempty, 1);
+    }
+    __syncthreads();
+  }
+}
+
+// Exact sequential loss chain over the per-point d2 of a run (sampling.cpp:56-63).
+__global__ void loss_chain_kernel(const double* __restrict__ d2, int64_t N, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  int64_t i = 0;
+  for (; i + 8 <= N; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = d2[i + q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s = kt::dadd(s, v[q]);
+  }
+  for (; i < N; ++i) s = kt::dadd(s, d2[i]);
+  *out = s;
+}
+
+__global__ void sum_chunks_kernel(const double* __restrict__ cs, int64_t n, double* out) {
+  __shared__ double red[32];
+  double p = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) p = kt::dadd(p, cs[i]);
+  const double s = block_sum(p, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void count_diff_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ b,
+                                  int64_t N, unsigned long long* out) {
+  int c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    c += a[i] != b[i];
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffff, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+// ------------------------------------------------------------------ snap (K6)
+// Eigen contiguous squaredNorm over D.
+__device__ double eigen_sqnorm_diff(const double* x, const double* c, int n) {
+  auto f = [&](int i) {
+    const double t = kt::dsub(x[i], c[i]);
+    return kt::dmul(t, t);
+  };
+  const int a2 = (n / 4) * 4, a = (n / 2) * 2;
+  if (a == 0) {
+    double s = f(0);
+    for (int i = 1; i < n; ++i) s = kt::dadd(s, f(i));
+    return s;
+  }
+  double p0 = f(0), p1 = f(1);
+  if (a > 2) {
+    double q0 = f(2), q1 = f(3);
+    for (int i = 4; i < a2; i += 4) {
+      p0 = kt::dadd(p0, f(i));
+      p1 = kt::dadd(p1, f(i + 1));
+      q0 = kt::dadd(q0, f(i + 2));
+      q1 = kt::dadd(q1, f(i + 3));
+    }
+    p0 = kt::dadd(p0, q0);
+    p1 = kt::dadd(p1, q1);
+    if (a > a2) {
+      p0 = kt::dadd(p0, f(a2));
+      p1 = kt::dadd(p1, f(a2 + 1));
+    }
+  }
+  double s = kt::dadd(p0, p1);
+  for (int i = a; i < n; ++i) s = kt::dadd(s, f(i));
+  return s;
+}
+
+// Rounding (sampling.cpp:209-214) + validity; flags[c] = 1 when a fallback is needed.
+__global__ void snap_round_kernel(KtSpaceParams sp, const double* __restrict__ cent, int k,
+                                  int32_t* __restrict__ out, int32_t* __restrict__ need) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  const int D = sp.D;
+  for (int d = 0; d < D; ++d) {
+    const int card = sp.card[d];
+    int v = (int)floor(kt::dadd(kt::dmul(cent[c * D + d], (double)(card - 1)), 0.5));
+    v = v < 0 ? 0 : (v > card - 1 ? card - 1 : v);
+    out[c * D + d] = v;
+  }
+  const int32_t* row = out + c * D;
+  need[c] = kt::rule_eval(sp, [&](int d) { return (int)row[d]; }) ? 0 : 1;
+}
+
+struct SnapKey {
+  unsigned long long hi;  // (invalid << 63) | (d2 bits >> 1) -- d2 >= 0 so bit 63 is 0
+  unsigned long long lo;  // (d2 bit 0 << 63) | id >> 1 ... packed below
+};
+
+// Per (centroid, block): best (invalid, d2, id) candidate; lexicographic min.
+template <class IdxT>
+__global__ void __launch_bounds__(kBT) snap_fallback_kernel(KtSpaceParams sp, int lut_total,
+                                                            const double* __restrict__ cent,
+                                                            const int32_t* __restrict__ need,
+                                                            const IdxT* __restrict__ cand,
+                                                            const uint64_t* __restrict__ ids,
+                                                            int64_t N,
+                                                            unsigned long long* __restrict__ part) {
+  extern __shared__ double sdyn[];
+  const int c = blockIdx.y;
+  const int D = sp.D;
+  unsigned long long* outp = part + ((int64_t)c * gridDim.x + blockIdx.x) * 3;
+  if (!need[c]) {
+    if (threadIdx.x == 0) outp[0] = outp[1] = outp[2] = ~0ull;
+    return;
+  }
+  const double* lut = stage_lut(sp, sdyn, lut_total);
+  __shared__ double cc[kt::kMaxKnobs];
+  if (threadIdx.x < D) cc[threadIdx.x] = cent[c * D + threadIdx.x];
+  __syncthreads();
+  unsigned long long b0 = ~0ull, b1 = ~0ull, b2 = ~0ull;  // (invalid, d2 bits, id)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const IdxT* row = cand + i * D;
+    const bool valid = kt::rule_eval(sp, [&](int d) { return (int)row[d]; });
+    double x[kt::kMaxKnobs];
+    for (int d = 0; d < D; ++d) x[d] = lut[sp.lut_off[d] + (int)row[d]];
+    const double d2 = eigen_sqnorm_diff(x, cc, D);
+    const unsigned long long k0 = valid ? 0ull : 1ull;
+    const unsigned long long k1 = (unsigned long long)__double_as_longlong(d2);
+    const unsigned long long k2 = ids[i];
+    if (k0 < b0 || (k0 == b0 && (k1 < b1 || (k1 == b1 && k2 < b2)))) {
+      b0 = k0;
+      b1 = k1;
+      b2 = k2;
+    }
+  }
+  __shared__ unsigned long long s0[kBT], s1[kBT], s2[kBT];
+  s0[threadIdx.x] = b0;
+  s1[threadIdx.x] = b1;
+  s2[threadIdx.x] = b2;
+  __syncthreads();
+  for (int o = kBT / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const int q = threadIdx.x + o;
+      if (s0[q] < s0[threadIdx.x] ||
+          (s0[q] == s0[threadIdx.x] && (s1[q] < s1[threadIdx.x] || (s1[q] == s1[threadIdx.x] && s2[q] < s2[threadIdx.x])))) {
+        s0[threadIdx.x] = s0[q];
+        s1[threadIdx.x] = s1[q];
+        s2[threadIdx.x] = s2[q];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    outp[0] = s0[0];
+    outp[1] = s1[0];
+    outp[2] = s2[0];
+  }
+}
+
+template <class IdxT>
+__global__ void snap_reduce_kernel(KtSpaceParams sp, const int32_t* __restrict__ need,
+                                   const unsigned long long* __restrict__ part, int nblk,
+                                   const IdxT* __restrict__ cand, const uint64_t* __restrict__ ids,
+                                   int64_t N, int32_t* __restrict__ out) {
+  const int c = blockIdx.x;
+  if (!need[c] || threadIdx.x != 0) return;
+  const unsigned long long* p = part + (int64_t)c * nblk * 3;
+  unsigned long long b0 = ~0ull, b1 = ~0ull, b2 = ~0ull;
+  for (int q = 0; q < nblk; ++q) {
+    const unsigned long long k0 = p[3 * q], k1 = p[3 * q + 1], k2 = p[3 * q + 2];
+    if (k0 < b0 || (k0 == b0 && (k1 < b1 || (k1 == b1 && k2 < b2)))) {
+      b0 = k0;
+      b1 = k1;
+      b2 = k2;
+    }
+  }
+  if (b0 == ~0ull) return;  // no candidates: keep the rounding (sampling.cpp:233)
+  // ids are unique (CandidateSet is deduplicated): find the row with id b2
+  for (int64_t i = 0; i < N; ++i)
+    if (ids[i] == b2) {
+      for (int d = 0; d < sp.D; ++d) out[c * sp.D + d] = (int32_t)cand[i * sp.D + d];
+      return;
+    }
+}
+
+// ------------------------------------------------------------------ host orchestration
+struct Run {
+  // device
+  double* cent;      // k x D
+  int32_t* asg;
+  double* d2;
+  double loss_est;   // parallel estimate
+  double loss_exact; // NaN unless computed
+  std::vector<double> iter_losses;
+};
+
+template <class IdxT>
+struct KMeans {
+  ktune_ctx* ctx;
+  const ktune_space* sp;
+  const IdxT* pts;  // device
+  int64_t N;
+  int D;
+  int lut_total;
+  int64_t nchunks;
+  size_t lut_smem;
+  // workspace
+  double* d2;         // kmeans++ d2
+  double* chunk;      // chunk sums
+  double* scratch;    // chunk prefix
+  KppState* kst;
+  int32_t* asg_a;     // current assignment
+  int32_t* asg_b;     // next assignment
+  double* d2_a;       // per-point d2 of current assignment
+  double* d2_b;
+  int32_t* members;
+  int32_t* blockcounts;
+  int32_t* counts;    // [k] + cstart [k] + nempty
+  double* cent_a;
+  double* cent_b;
+  unsigned long long* ull;  // [0] changed, [1] diff
+  double* dscal;      // [0] loss sum, [1] exact loss
+  // best-of-restarts and previous-k best (for exact fallbacks)
+  int32_t* best_asg;
+  double* best_d2;
+  double* best_cent;
+  int32_t* prev_asg;
+  double* prev_d2;
+
+  void setup(ktune_ctx* c, const ktune_space* s, const IdxT* p, int64_t n) {
+    ctx = c;
+    sp = s;
+    pts = p;
+    N = n;
+    D = s->D;
+    lut_total = s->lut_total;
+    nchunks = kt::ceil_div(N, kChunk);
+    lut_smem = sizeof(double) * lut_total;
+    d2 = (double*)ctx->dev(kt::WS_D2, sizeof(double) * N);
+    chunk = (double*)ctx->dev(kt::WS_BLOCK, sizeof(double) * nchunks);
+    scratch = (double*)ctx->dev(kt::WS_BLOCK2, sizeof(double) * nchunks);
+    kst = (KppState*)ctx->dev(kt::WS_KPP, sizeof(KppState));
+    asg_a = (int32_t*)ctx->dev(kt::WS_ASSIGN, sizeof(int32_t) * N);
+    asg_b = (int32_t*)ctx->dev(kt::WS_ASSIGN2, sizeof(int32_t) * N);
+    d2_a = (double*)ctx->dev(kt::WS_D2B, sizeof(double) * N * 2);
+    d2_b = d2_a + N;
+    members = (int32_t*)ctx->dev(kt::WS_MEMBERS, sizeof(int32_t) * N);
+    blockcounts = (int32_t*)ctx->dev(kt::WS_SCRATCH, sizeof(int32_t) * nchunks * kt::kMaxK);
+    counts = (int32_t*)ctx->dev(kt::WS_SCRATCH2, sizeof(int32_t) * (2 * kt::kMaxK + 8));
+    cent_a = (double*)ctx->dev(kt::WS_CENT, sizeof(double) * kt::kMaxK * D * 3);
+    cent_b = cent_a + kt::kMaxK * D;
+    best_cent = cent_b + kt::kMaxK * D;
+    ull = (unsigned long long*)ctx->dev(kt::WS_VALID, 64);
+    dscal = (double*)ctx->dev(kt::WS_SNAP, 64);
+    best_asg = (int32_t*)ctx->dev(kt::WS_BEST_ASSIGN, sizeof(int32_t) * N);
+    best_d2 = (double*)ctx->dev(kt::WS_BEST_D2, sizeof(double) * N);
+    prev_asg = (int32_t*)ctx->dev(kt::WS_PREV_ASSIGN, sizeof(int32_t) * N);
+    prev_d2 = (double*)ctx->dev(kt::WS_PREV_D2, sizeof(double) * N);
+  }
+
+  cudaStream_t s() const { return ctx->stream; }
+  int grid_pts() const { return (int)nchunks; }
+
+  void kmeanspp(int k, uint64_t rng_seed) {
+    KppState h{rng_seed, 0, 0, 0};
+    KT_CUDA(cudaMemcpyAsync(kst, &h, sizeof(h), cudaMemcpyHostToDevice, s()));
+    kpp_select_kernel<<<1, 1024, 0, s()>>>(d2, chunk, N, kst, 0, 0, scratch);
+    kt::check_launch(ctx, "kpp_select");
+    const size_t smem = lut_smem;
+    for (int c = 0; c < k; ++c) {
+      kpp_d2_kernel<IdxT><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, kst, cent_a, c,
+                                                          c == 0 ? 1 : 0, d2, chunk);
+      kt::check_launch(ctx, "kpp_d2");
+      if (c + 1 < k) {
+        kpp_select_kernel<<<1, 1024, 0, s()>>>(d2, chunk, N, kst, 1, (int)ctx->opt_force_exact, scratch);
+        kt::check_launch(ctx, "kpp_select");
+        ctx->stats[KTUNE_STAT_KPP_PICKS] += 1;
+      }
+    }
+  }
+
+  // assignment against cent; returns loss estimate; changed count if prev != null
+  double assign(const double* cent, int k, const int32_t* prev, int32_t* asg, double* dd,
+                unsigned long long* changed_out) {
+    KT_CUDA(cudaMemsetAsync(ull, 0, 16, s()));
+    const size_t smem = sizeof(double) * (k * D) + lut_smem;
+    assign_kernel<IdxT><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent, k, prev, asg,
+                                                        dd, chunk, ull);
+    kt::check_launch(ctx, "assign");
+    sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk, nchunks, dscal);
+    kt::check_launch(ctx, "sum_chunks");
+    struct {
+      double loss;
+      unsigned long long changed;
+    } h;
+    KT_CUDA(cudaMemcpyAsync(&h.loss, dscal, 8, cudaMemcpyDeviceToHost, s()));
+    KT_CUDA(cudaMemcpyAsync(&h.changed, ull, 8, cudaMemcpyDeviceToHost, s()));
+    KT_CUDA(cudaStreamSynchronize(s()));
+    if (changed_out) *changed_out = h.changed;
+    return h.loss;
+  }
+
+  void update_centroids(int k, const int32_t* asg, const double* d2_old, double* next) {
+    hist_kernel<<<grid_pts(), kBT, 0, s()>>>(asg, N, k, blockcounts);
+    scan_counts_kernel<<<1, 64, 0, s()>>>(blockcounts, nchunks, k, counts, counts + kt::kMaxK);
+    scatter_kernel<<<grid_pts(), kBT, 0, s()>>>(asg, N, k, blockcounts, counts + kt::kMaxK, members);
+    const int th = 128;
+    chain_kernel<IdxT><<<(int)kt::ceil_div(k * D, th), th, 0, s()>>>(sp->params, pts, members, counts,
+                                                                      counts + kt::kMaxK, k, next);
+    KT_CUDA(cudaMemsetAsync(counts + 2 * kt::kMaxK, 0, 4, s()));
+    reseed_kernel<IdxT><<<1, 1024, 0, s()>>>(sp->params, pts, N, counts, k, d2_old, next,
+                                             counts + 2 * kt::kMaxK);
+    kt::check_launch(ctx, "centroid update", 5);
+  }
+
+  double exact_loss(const double* dd) {
+    loss_chain_kernel<<<1, 32, 0, s()>>>(dd, N, dscal + 1);
+    kt::check_launch(ctx, "loss_chain");
+    double v;
+    KT_CUDA(cudaMemcpyAsync(&v, dscal + 1, 8, cudaMemcpyDeviceToHost, s()));
+    KT_CUDA(cudaStreamSynchronize(s()));
+    return v;
+  }
+
+  double loss_err(double L) const { return (double)(N + 80) * kU * 1.0625 * L; }
+
+  bool same_assign(const int32_t* a, const int32_t* b) {
+    KT_CUDA(cudaMemsetAsync(ull + 1, 0, 8, s()));
+    count_diff_kernel<<<std::min<int64_t>(kt::ceil_div(N, 256), 1024), 256, 0, s()>>>(a, b, N, ull + 1);
+    kt::check_launch(ctx, "count_diff");
+    unsigned long long v;
+    KT_CUDA(cudaMemcpyAsync(&v, ull + 1, 8, cudaMemcpyDeviceToHost, s()));
+    KT_CUDA(cudaStreamSynchronize(s()));
+    return v == 0;
+  }
+
+  // Lloyd from kmeans++ (sampling.cpp:98-153). Result left in (cent_a, asg_a, d2_a).
+  double lloyd(int k, uint64_t rng_seed, int max_iters, std::vector<double>& iter_losses) {
+    kmeanspp(k, rng_seed);
+    double loss = assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);
+    iter_losses.assign(1, loss);
+    for (int it = 0; it < max_iters; ++it) {
+      update_centroids(k, asg_a, d2_a, cent_b);
+      unsigned long long changed = 0;
+      const double nl = assign(cent_b, k, asg_a, asg_b, d2_b, &changed);
+      ctx->stats[KTUNE_STAT_LLOYD_ITERS] += 1;
+      if (nl > loss + 1e-9 + loss_err(loss) + loss_err(nl))
+        kt::fail(KTUNE_ERR_LOGIC, "kmeans: Lloyd loss increased, which should be impossible");
+      std::swap(cent_a, cent_b);
+      std::swap(asg_a, asg_b);
+      std::swap(d2_a, d2_b);
+      loss = nl;
+      iter_losses.push_back(nl);
+      if (changed == 0) break;
+    }
+    return loss;
+  }
+
+  // Certified strict "a < b" on reference losses; exact chains when undecided.
+  bool less_loss(double La, const double* d2a, const int32_t* asga, double& La_exact, double Lb,
+                 const double* d2b, const int32_t* asgb, double& Lb_exact) {
+    if (!ctx->opt_force_exact) {
+      const double ea = loss_err(La), eb = loss_err(Lb);
+      if (La + ea < Lb - eb) return true;
+      if (La - ea >= Lb + eb) return false;
+      if (same_assign(asga, asgb)) return false;  // same partition => identical reference losses
+    }
+    ctx->stats[KTUNE_STAT_DECISION_FALLBACKS] += 1;
+    if (std::isnan(La_exact)) La_exact = exact_loss(d2a);
+    if (std::isnan(Lb_exact)) Lb_exact = exact_loss(d2b);
+    return La_exact < Lb_exact;
+  }
+
+  struct Result {
+    double loss, loss_exact;
+    std::vector<double> iter_losses;
+  };
+
+  // kmeans_run (sampling.cpp:157-175): best of restarts into best_* buffers.
+  Result run(int k, uint64_t seed, int max_iters, int restarts) {
+    Result best{0.0, NAN, {}};
+    bool have = false;
+    for (int r = 0; r < std::max(1, restarts); ++r) {
+      std::vector<double> il;
+      const double L = lloyd(k, kt::seed_combine(seed, (uint64_t)r), max_iters, il);
+      double Lx = NAN;
+      bool take = !have;
+      if (have) take = less_loss(L, d2_a, asg_a, Lx, best.loss, best_d2, best_asg, best.loss_exact);
+      if (take) {
+        have = true;
+        best.loss = L;
+        best.loss_exact = Lx;
+        best.iter_losses = il;
+        KT_CUDA(cudaMemcpyAsync(best_asg, asg_a, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s()));
+        KT_CUDA(cudaMemcpyAsync(best_d2, d2_a, sizeof(double) * N, cudaMemcpyDeviceToDevice, s()));
+        KT_CUDA(cudaMemcpyAsync(best_cent, cent_a, sizeof(double) * k * D, cudaMemcpyDeviceToDevice, s()));
+      }
+    }
+    return best;
+  }
+};
+
+template <class IdxT>
+void snap_device(ktune_ctx* ctx, const ktune_space* sp, const double* d_cent, int k,
+                 const IdxT* d_cand, const uint64_t* d_ids, int64_t N, int32_t* d_out) {
+  int32_t* need = (int32_t*)ctx->dev(kt::WS_OUT4, sizeof(int32_t) * kt::kMaxK);
+  snap_round_kernel<<<1, 64, 0, ctx->stream>>>(sp->params, d_cent, k, d_out, need);
+  kt::check_launch(ctx, "snap_round");
+  if (N <= 0) return;
+  const int nblk = (int)std::min<int64_t>(kt::ceil_div(N, kBT), 256);
+  unsigned long long* part = (unsigned long long*)ctx->dev(kt::WS_OUT3, sizeof(unsigned long long) * 3 * nblk * k);
+  dim3 grid(nblk, k);
+  snap_fallback_kernel<IdxT><<<grid, kBT, sizeof(double) * sp->lut_total, ctx->stream>>>(
+      sp->params, sp->lut_total, d_cent, need, d_cand, d_ids, N, part);
+  snap_reduce_kernel<IdxT><<<k, 32, 0, ctx->stream>>>(sp->params, need, part, nblk, d_cand, d_ids, N, d_out);
+  kt::check_launch(ctx, "snap", 2);
+}
+
+void check_lut(const ktune_space* sp) {
+  if ((size_t)sp->lut_total * 8 + kt::kMaxK * kt::kMaxKnobs * 8 > 200 * 1024)
+    kt::fail(KTUNE_ERR_CONFIG, "k-means: feature table too large for shared memory");
+}
+
+template <class IdxT>
+void kmeans_impl(ktune_ctx* ctx, const ktune_space* space, const void* idx, int64_t N, int k,
+                 uint64_t seed, int max_iters, int restarts, ktune_kmeans_out* out, bool dev) {
+  const int D = space->D;
+  const IdxT* d_pts = (const IdxT*)kt::stage_in(ctx, kt::WS_IN0, idx, sizeof(IdxT) * N * D, dev);
+  KMeans<IdxT> km;
+  km.setup(ctx, space, d_pts, N);
+  auto res = km.run(k, seed, max_iters, restarts);
+  const double loss = std::isnan(res.loss_exact) ? res.loss : res.loss_exact;
+  if (dev) {
+    if (out->centroids) KT_CUDA(cudaMemcpyAsync(out->centroids, km.best_cent, sizeof(double) * k * D, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (out->assignments) KT_CUDA(cudaMemcpyAsync(out->assignments, km.best_asg, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (out->l2_loss) KT_CUDA(cudaMemcpyAsync(out->l2_loss, &loss, 8, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    if (out->centroids) KT_CUDA(cudaMemcpyAsync(out->centroids, km.best_cent, sizeof(double) * k * D, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->assignments) KT_CUDA(cudaMemcpyAsync(out->assignments, km.best_asg, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, ctx->stream));
+    if (out->l2_loss) *out->l2_loss = loss;
+  }
+  if (out->iteration_losses) {
+    for (size_t i = 0; i < res.iter_losses.size(); ++i) out->iteration_losses[i] = res.iter_losses[i];
+    if (!res.iter_losses.empty() && !std::isnan(res.loss_exact))
+      out->iteration_losses[res.iter_losses.size() - 1] = res.loss_exact;
+  }
+  if (out->num_losses) *out->num_losses = (int32_t)res.iter_losses.size();
+  KT_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+template <class IdxT>
+void sweep_impl(ktune_ctx* ctx, const ktune_space* space, const void* idx, const uint64_t* ids,
+                int64_t N, const ktune_sampling_params* p, uint64_t rng_seed, ktune_sweep_out* out,
+                bool dev) {
+  const int D = space->D;
+  const IdxT* d_pts = (const IdxT*)kt::stage_in(ctx, kt::WS_IN0, idx, sizeof(IdxT) * N * D, dev);
+  const uint64_t* d_ids = (const uint64_t*)kt::stage_in(ctx, kt::WS_IN1, ids, sizeof(uint64_t) * N, dev);
+  KMeans<IdxT> km;
+  km.setup(ctx, space, d_pts, N);
+  const int k_lo = (int)std::min<int64_t>(p->k_min, N);
+  const int k_hi = (int)std::min<int64_t>(p->k_max_exclusive - 1, N);
+  double prev = INFINITY, prev_exact = NAN;
+  bool have_prev = false;
+  int chosen = k_lo;
+  double chosen_loss = 0.0;
+  std::vector<double> klosses;
+  double* d_chosen_cent = (double*)ctx->dev(kt::WS_OUT2, sizeof(double) * kt::kMaxK * D);
+  for (int k = k_lo; k <= k_hi; ++k) {
+    auto res = km.run(k, kt::seed_combine(rng_seed, (uint64_t)k), p->max_iters, p->restarts);
+    chosen = k;
+    chosen_loss = std::isnan(res.loss_exact) ? res.loss : res.loss_exact;
+    KT_CUDA(cudaMemcpyAsync(d_chosen_cent, km.best_cent, sizeof(double) * k * D, cudaMemcpyDeviceToDevice, ctx->stream));
+    // break test: threshold * L_k >= L_{k-1} (sampling.cpp:444)
+    bool brk = false;
+    if (have_prev) {
+      double Lk = res.loss, Lp = prev;
+      bool decided = false;
+      if (!ctx->opt_force_exact) {
+        const double ek = km.loss_err(Lk), ep = km.loss_err(Lp);
+        if (p->threshold * (Lk - ek) * (1 - 4 * kU) >= (Lp + ep) * (1 + 4 * kU)) {
+          brk = true;
+          decided = true;
+        } else if (p->threshold * (Lk + ek) * (1 + 4 * kU) < (Lp - ep) * (1 - 4 * kU)) {
+          brk = false;
+          decided = true;
+        }
+      }
+      if (!decided) {
+        ctx->stats[KTUNE_STAT_DECISION_FALLBACKS] += 1;
+        if (std::isnan(res.loss_exact)) res.loss_exact = km.exact_loss(km.best_d2);
+        if (std::isnan(prev_exact)) prev_exact = km.exact_loss(km.prev_d2);
+        brk = p->threshold * res.loss_exact >= prev_exact;
+        chosen_loss = res.loss_exact;
+      }
+    }
+    klosses.push_back(chosen_loss);
+    if (brk) break;
+    prev = res.loss;
+    prev_exact = res.loss_exact;
+    have_prev = true;
+    KT_CUDA(cudaMemcpyAsync(km.prev_d2, km.best_d2, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  // snap the chosen centroids (sampling.cpp:448-452)
+  int32_t* d_snap = (int32_t*)ctx->dev(kt::WS_OUT1, sizeof(int32_t) * kt::kMaxK * D);
+  snap_device<IdxT>(ctx, space, d_chosen_cent, chosen, d_pts, d_ids, N, d_snap);
+  const auto kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (out->centroids) KT_CUDA(cudaMemcpyAsync(out->centroids, d_chosen_cent, sizeof(double) * chosen * D, kind, ctx->stream));
+  if (out->assignments) KT_CUDA(cudaMemcpyAsync(out->assignments, km.best_asg, sizeof(int32_t) * N, kind, ctx->stream));
+  if (out->snapped) KT_CUDA(cudaMemcpyAsync(out->snapped, d_snap, sizeof(int32_t) * chosen * D, kind, ctx->stream));
+  KT_CUDA(cudaStreamSynchronize(ctx->stream));
+  *out->k = chosen;
+  if (out->l2_loss) *out->l2_loss = chosen_loss;
+  if (out->k_losses)
+    for (size_t i = 0; i < klosses.size(); ++i) out->k_losses[i] = klosses[i];
+  if (out->num_k) *out->num_k = (int32_t)klosses.size();
+}
+
+}  // namespace
+
+extern "C" {
+
+int ktune_kmeans_run(ktune_ctx* ctx, const ktune_space* space, const void* idx, int idx_bytes,
+                     int64_t N, int k, uint64_t seed, int max_iters, int restarts,
+                     ktune_kmeans_out* out, int flags) {
+  return kt_guard(ctx, [&] {
+    if (N == 0) kt::fail(KTUNE_ERR_CONFIG, "kmeans: empty point set");
+    if (k < 1 || k > N)
+      kt::fail(KTUNE_ERR_CONFIG, "kmeans: k=" + std::to_string(k) + " out of range for " + std::to_string(N) + " points");
+    if (k > kt::kMaxK) kt::fail(KTUNE_ERR_CONFIG, "kmeans: k > 64 unsupported on the device path");
+    if (idx_bytes != 1 && idx_bytes != 2) kt::fail(KTUNE_ERR_CONFIG, "idx_bytes must be 1 or 2");
+    if (N > INT32_MAX) kt::fail(KTUNE_ERR_CONFIG, "kmeans: at most 2^31-1 points");
+    if (max_iters < 0) max_iters = 0;
+    check_lut(space);
+    cudaSetDevice(ctx->device);
+    if (idx_bytes == 1)
+      kmeans_impl<uint8_t>(ctx, space, idx, N, k, seed, max_iters, restarts, out, flags & KTUNE_F_DEVICE);
+    else
+      kmeans_impl<uint16_t>(ctx, space, idx, N, k, seed, max_iters, restarts, out, flags & KTUNE_F_DEVICE);
+  });
+}
+
+int ktune_adaptive_sweep(ktune_ctx* ctx, const ktune_space* space, const void* idx, int idx_bytes,
+                         const uint64_t* ids, int64_t N, const ktune_sampling_params* p,
+                         uint64_t rng_seed, ktune_sweep_out* out, int flags) {
+  return kt_guard(ctx, [&] {
+    if (N == 0) kt::fail(KTUNE_ERR_CONFIG, "adaptive_sample: empty candidate set");
+    if (p->k_min >= p->k_max_exclusive || p->k_min < 1)
+      kt::fail(KTUNE_ERR_CONFIG, "adaptive_sample: need 1 <= k_min < k_max_exclusive");
+    if (p->threshold <= 1.0) kt::fail(KTUNE_ERR_CONFIG, "adaptive_sample: threshold must exceed 1");
+    if (p->k_max_exclusive - 1 > kt::kMaxK) kt::fail(KTUNE_ERR_CONFIG, "adaptive_sample: k > 64 unsupported on the device path");
+    if (idx_bytes != 1 && idx_bytes != 2) kt::fail(KTUNE_ERR_CONFIG, "idx_bytes must be 1 or 2");
+    if (N > INT32_MAX) kt::fail(KTUNE_ERR_CONFIG, "adaptive_sample: at most 2^31-1 candidates");
+    check_lut(space);
+    cudaSetDevice(ctx->device);
+    if (idx_bytes == 1)
+      sweep_impl<uint8_t>(ctx, space, idx, ids, N, p, rng_seed, out, flags & KTUNE_F_DEVICE);
+    else
+      sweep_impl<uint16_t>(ctx, space, idx, ids, N, p, rng_seed, out, flags & KTUNE_F_DEVICE);
+  });
+}
+
+int ktune_snap(ktune_ctx* ctx, const ktune_space* space, const double* centroids, int k,
+               const void* cand_idx, int idx_bytes, const uint64_t* cand_ids, int64_t N,
+               int32_t* out_idx, int flags) {
+  return kt_guard(ctx, [&] {
+    if (k < 0 || k > kt::kMaxK) kt::fail(KTUNE_ERR_CONFIG, "snap: 0 <= k <= 64");
+    if (k == 0) return;
+    if (idx_bytes != 1 && idx_bytes != 2) kt::fail(KTUNE_ERR_CONFIG, "idx_bytes must be 1 or 2");
+    const bool dev = flags & KTUNE_F_DEVICE;
+    const int D = space->D;
+    const double* d_c = (const double*)kt::stage_in(ctx, kt::WS_IN2, centroids, sizeof(double) * k * D, dev);
+    const void* d_cand = kt::stage_in(ctx, kt::WS_IN0, cand_idx, (size_t)idx_bytes * N * D, dev);
+    const uint64_t* d_ids = (const uint64_t*)kt::stage_in(ctx, kt::WS_IN1, cand_ids, sizeof(uint64_t) * N, dev);
+    int32_t* d_out = (int32_t*)kt::out_buf(ctx, kt::WS_OUT0, out_idx, sizeof(int32_t) * k * D, dev);
+    if (idx_bytes == 1)
+      snap_device<uint8_t>(ctx, space, d_c, k, (const uint8_t*)d_cand, d_ids, N, d_out);
+    else
+      snap_device<uint16_t>(ctx, space, d_c, k, (const uint16_t*)d_cand, d_ids, N, d_out);
+    kt::stage_out(ctx, out_idx, d_out, sizeof(int32_t) * k * D, dev);
+    if (!dev) KT_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

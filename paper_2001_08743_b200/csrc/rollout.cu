@@ -1,0 +1,492 @@
+// K2: persistent batched rollout (run_episodes) and the
+// ActorCritic forward (actor_critic.hpp:43).
+//
+// Exact fp64 path: every dot product, tanh/exp/log and the sampling compare
+// evaluates exactly as the oracle restatement does, so
+// actions, configurations, log-probabilities and values are bit-identical.
+//
+// Layout: one CTA of 128 threads owns a tile of 32 episodes for all T steps;
+// the configurations stay resident in shared memory for the whole episode
+// and the actor-critic parameters (fp64, ~175 KB at n=16) are staged into
+// shared memory once per CTA. Per step:
+//   0: x[i][c] = idx/(card-1)
+//   A: h0[j][c] = tanh(W0 x + b0)            thread = hidden unit j
+//   B: hp/hv[u][c] = tanh(W h0 + b)           thread = head unit u, 8 configs per weight load
+//   C: logits[a][c], value[c]                 thread = (config, logit) items
+//   D: per (config, knob) log-softmax, counter-RNG draw, saturating move
+//   E: joint log-probability, trajectory writes
+#include <algorithm>
+
+#include "device.cuh"
+#include "internal.cuh"
+
+namespace {
+
+constexpr int kTile = 32;      // episodes per CTA
+constexpr int kThreads = 128;  // threads per CTA
+
+struct AcOff {
+  int w0, b0, wp1, bp1, wp2, bp2, wv1, bv1, wv2, bv2, total;
+};
+
+__host__ __device__ inline AcOff ac_layout(int n, int h, int g) {
+  AcOff o;
+  o.w0 = 0;
+  o.b0 = o.w0 + h * n;
+  o.wp1 = o.b0 + h;
+  o.bp1 = o.wp1 + g * h;
+  o.wp2 = o.bp1 + g;
+  o.bp2 = o.wp2 + 3 * n * g;
+  o.wv1 = o.bp2 + 3 * n;
+  o.bv1 = o.wv1 + g * h;
+  o.wv2 = o.bv1 + g;
+  o.bv2 = o.wv2 + g;
+  o.total = o.bv2 + 1;
+  return o;
+}
+
+struct RolloutTask {
+  KtSpaceParams sp;
+  const double* params;  // device, flat layout
+  int n, h, g;
+  int T;
+  int64_t E;
+  int64_t episode_offset;
+  uint64_t seed;
+  const uint16_t* init_idx;
+  uint16_t* idx;
+  int8_t* actions;
+  double* logp;
+  double* value;
+};
+
+struct CtaWork {
+  int task;
+  int64_t first;  // first episode (task-local) of this CTA's tile
+};
+
+// Shared-memory carve-up (in doubles): params | act [max(h,2g)][32] | buf [3n][32] | val[32]
+// then uint16 cfg [32][n].
+__host__ __device__ inline size_t rollout_smem_bytes(int n, int h, int g, bool smem_params) {
+  const AcOff o = ac_layout(n, h, g);
+  const int act = (h > 2 * g ? h : 2 * g) * kTile;
+  size_t d = (smem_params ? (size_t)o.total : 0) + act + (size_t)3 * n * kTile + kTile;
+  return d * 8 + (size_t)kTile * n * 2 + 16;
+}
+
+// One forward pass over the 32 states held in buf[i][c] (phase A..C).
+// Leaves logits in buf[a][c] and values in val[c]; act holds hp/hv.
+__device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n, int h, int g,
+                             double* act, double* buf, double* val) {
+  const int tid = threadIdx.x;
+  // ---- A: h0 = tanh(W0 x + b0), W0 column-major (h x n)
+  for (int j = tid; j < h; j += kThreads) {
+    double w[kt::kMaxKnobs];
+#pragma unroll
+    for (int i = 0; i < kt::kMaxKnobs; ++i) w[i] = i < n ? P[o.w0 + i * h + j] : 0.0;
+    const double b = P[o.b0 + j];
+    for (int c = 0; c < kTile; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < kt::kMaxKnobs; ++i)
+        if (i < n) acc = kt::dadd(acc, kt::dmul(w[i], buf[i * kTile + c]));
+      act[j * kTile + c] = kt::kt_tanh(kt::dadd(acc, b));
+    }
+  }
+  __syncthreads();
+  // ---- B: hp = tanh(Wp1 h0 + bp1) (u < g), hv = tanh(Wv1 h0 + bv1) (u >= g)
+  double res[kTile];
+  const int u = tid;
+  const bool active = u < 2 * g;
+  if (active) {
+    const int wbase = u < g ? o.wp1 + u : o.wv1 + (u - g);
+    const double b = u < g ? P[o.bp1 + u] : P[o.bv1 + (u - g)];
+#pragma unroll
+    for (int cb = 0; cb < kTile; cb += 8) {
+      double acc[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) acc[r] = 0.0;
+      for (int i = 0; i < h; ++i) {
+        const double w = P[wbase + i * g];
+        const double2* hrow = reinterpret_cast<const double2*>(act + i * kTile + cb);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const double2 v = hrow[r];
+          acc[2 * r] = kt::dadd(acc[2 * r], kt::dmul(w, v.x));
+          acc[2 * r + 1] = kt::dadd(acc[2 * r + 1], kt::dmul(w, v.y));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) res[cb + r] = kt::kt_tanh(kt::dadd(acc[r], b));
+    }
+  }
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int c = 0; c < kTile; ++c) act[u * kTile + c] = res[c];
+  }
+  __syncthreads();
+  // ---- C: logits[a][c] = Wp2 hp + bp2 (Wp2 column-major 3n x g); value = wv2 . hv + bv2
+  const int na = 3 * n + 1;
+  for (int item = tid; item < na * kTile; item += kThreads) {
+    const int c = item / na, a = item % na;
+    double acc = 0.0;
+    if (a < 3 * n) {
+      for (int j = 0; j < g; ++j) acc = kt::dadd(acc, kt::dmul(P[o.wp2 + j * 3 * n + a], act[j * kTile + c]));
+      buf[a * kTile + c] = kt::dadd(acc, P[o.bp2 + a]);
+    } else {
+      for (int j = 0; j < g; ++j) acc = kt::dadd(acc, kt::dmul(P[o.wv2 + j], act[(g + j) * kTile + c]));
+      val[c] = kt::dadd(acc, P[o.bv2]);
+    }
+  }
+  __syncthreads();
+}
+
+// Per-knob log-softmax over {dec, stay, inc} (actor_critic.hpp:13-14).
+struct Knob3 {
+  double lp[3], p[3];
+};
+__device__ __forceinline__ Knob3 softmax3(double l0, double l1, double l2) {
+  double m = l0;
+  if (l1 > m) m = l1;
+  if (l2 > m) m = l2;
+  const double e0 = kt::kt_exp(kt::dsub(l0, m)), e1 = kt::kt_exp(kt::dsub(l1, m)),
+               e2 = kt::kt_exp(kt::dsub(l2, m));
+  const double s = kt::dadd(kt::dadd(e0, e1), e2);
+  const double lse = kt::dadd(m, kt::kt_log(s));
+  Knob3 r;
+  r.lp[0] = kt::dsub(l0, lse);
+  r.lp[1] = kt::dsub(l1, lse);
+  r.lp[2] = kt::dsub(l2, lse);
+  r.p[0] = kt::ddiv(e0, s);
+  r.p[1] = kt::ddiv(e1, s);
+  r.p[2] = kt::ddiv(e2, s);
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+rollout_kernel(const RolloutTask* __restrict__ tasks, const CtaWork* __restrict__ work,
+               int smem_params) {
+  extern __shared__ __align__(16) double sm[];
+  const CtaWork wk = work[blockIdx.x];
+  const RolloutTask& tk = tasks[wk.task];
+  const int n = tk.n, h = tk.h, g = tk.g, T = tk.T;
+  const AcOff o = ac_layout(n, h, g);
+  const double* P = tk.params;
+  double* p_s = sm;
+  if (smem_params) {
+    for (int i = threadIdx.x; i < o.total; i += kThreads) p_s[i] = P[i];
+    P = p_s;
+  }
+  double* act = sm + (smem_params ? o.total : 0);
+  double* buf = act + (h > 2 * g ? h : 2 * g) * kTile;
+  double* val = buf + 3 * n * kTile;
+  uint16_t* cfg = reinterpret_cast<uint16_t*>(val + kTile);
+  const int tid = threadIdx.x;
+  const int64_t E = tk.E;
+  // load initial configurations, write trajectory row 0
+  for (int item = tid; item < kTile * n; item += kThreads) {
+    const int c = item / n, d = item % n;
+    const int64_t e = wk.first + c;
+    uint16_t v = 0;
+    if (e < E) {
+      v = tk.init_idx[e * n + d];
+      tk.idx[(e * (T + 1)) * n + d] = v;
+    }
+    cfg[c * n + d] = v;
+  }
+  __syncthreads();
+  for (int t = 0; t < T; ++t) {
+    // ---- 0: features x = idx / (card - 1) (design_space.cpp:195-197)
+    for (int item = tid; item < kTile * n; item += kThreads) {
+      const int c = item / n, d = item % n;
+      const int card = tk.sp.card[d];
+      buf[d * kTile + c] = card > 1 ? kt::ddiv((double)cfg[c * n + d], (double)(card - 1)) : 0.0;
+    }
+    __syncthreads();
+    forward_tile(P, o, n, h, g, act, buf, val);
+    // ---- D: sample per knob, saturating update
+    for (int item = tid; item < kTile * n; item += kThreads) {
+      const int c = item / n, d = item % n;
+      const int64_t e = wk.first + c;
+      const Knob3 k3 = softmax3(buf[(3 * d) * kTile + c], buf[(3 * d + 1) * kTile + c],
+                                buf[(3 * d + 2) * kTile + c]);
+      const uint64_t ge = (uint64_t)(tk.episode_offset + e);
+      const double u = kt::hash01(tk.seed, (ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n + (uint64_t)d);
+      const int a = u < k3.p[0] ? 0 : (u < kt::dadd(k3.p[0], k3.p[1]) ? 1 : 2);
+      int v = (int)cfg[c * n + d] + (a - 1);
+      const int card = tk.sp.card[d];
+      v = v < 0 ? 0 : (v > card - 1 ? card - 1 : v);
+      cfg[c * n + d] = (uint16_t)v;
+      buf[(3 * d) * kTile + c] = k3.lp[a];
+      if (e < E) {
+        if (tk.actions) tk.actions[(e * T + t) * n + d] = (int8_t)(a - 1);
+        tk.idx[(e * (T + 1) + t + 1) * n + d] = (uint16_t)v;
+      }
+    }
+    __syncthreads();
+    // ---- E: joint log-probability in knob order, value
+    if (tid < kTile) {
+      const int64_t e = wk.first + tid;
+      if (e < E) {
+        double lp = 0.0;
+        for (int d = 0; d < n; ++d) lp = kt::dadd(lp, buf[(3 * d) * kTile + tid]);
+        if (tk.logp) tk.logp[e * T + t] = lp;
+        if (tk.value) tk.value[e * T + t] = val[tid];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ActorCritic::forward over arbitrary fp64 states.
+__global__ void __launch_bounds__(kThreads, 1)
+ac_forward_kernel(const double* __restrict__ params, int n, int h, int g,
+                  const double* __restrict__ states, int64_t B, double* __restrict__ log_probs,
+                  double* __restrict__ probs, double* __restrict__ values, int smem_params) {
+  extern __shared__ __align__(16) double sm[];
+  const AcOff o = ac_layout(n, h, g);
+  const double* P = params;
+  if (smem_params) {
+    for (int i = threadIdx.x; i < o.total; i += kThreads) sm[i] = params[i];
+    P = sm;
+  }
+  double* act = sm + (smem_params ? o.total : 0);
+  double* buf = act + (h > 2 * g ? h : 2 * g) * kTile;
+  double* val = buf + 3 * n * kTile;
+  const int tid = threadIdx.x;
+  for (int64_t first = (int64_t)blockIdx.x * kTile; first < B; first += (int64_t)gridDim.x * kTile) {
+    __syncthreads();
+    for (int item = tid; item < kTile * n; item += kThreads) {
+      const int c = item / n, d = item % n;
+      buf[d * kTile + c] = first + c < B ? states[(first + c) * n + d] : 0.0;
+    }
+    __syncthreads();
+    forward_tile(P, o, n, h, g, act, buf, val);
+    for (int item = tid; item < kTile * n; item += kThreads) {
+      const int c = item / n, d = item % n;
+      const int64_t b = first + c;
+      if (b >= B) continue;
+      const Knob3 k3 = softmax3(buf[(3 * d) * kTile + c], buf[(3 * d + 1) * kTile + c],
+                                buf[(3 * d + 2) * kTile + c]);
+      for (int a = 0; a < 3; ++a) {
+        if (log_probs) log_probs[b * 3 * n + 3 * d + a] = k3.lp[a];
+        if (probs) probs[b * 3 * n + 3 * d + a] = k3.p[a];
+      }
+    }
+    if (values && tid < kTile && first + tid < B) values[first + tid] = val[tid];
+  }
+}
+
+__global__ void debug_math_kernel(int op, const double* __restrict__ x, int64_t n,
+                                  double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = op == 0 ? kt::kt_exp(x[i]) : (op == 1 ? kt::kt_log(x[i]) : kt::kt_tanh(x[i]));
+}
+
+bool fits_smem(int n, int h, int g) { return rollout_smem_bytes(n, h, g, true) <= 227 * 1024; }
+
+void check_dims(int n, int h, int g) {
+  if (n < 1 || n > kt::kMaxKnobs) kt::fail(KTUNE_ERR_CONFIG, "actor-critic: 1 <= num_knobs <= 32 on the device path");
+  if (h < 1 || g < 1 || 2 * g > kThreads || h > 1024)
+    kt::fail(KTUNE_ERR_CONFIG, "actor-critic: device path needs head_hidden <= 64 and hidden_dim <= 1024");
+}
+
+}  // namespace
+
+namespace kt {
+void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_idx, int idx_bytes,
+                            int64_t B, double* d_out);
+}
+
+extern "C" {
+
+int64_t ktune_ac_num_params(int n, int h, int g) { return ac_layout(n, h, g).total; }
+
+int ktune_ac_init_params(int n, int h, int g, uint64_t seed, double* p) {
+  // Pinned init: one Rng(seed) stream; weights in flat-layout
+  // order as normal()/sqrt(fan_in) (Box-Muller, rng.hpp:78-83); biases 0.
+  return kt_guard(nullptr, [&] {
+    const AcOff o = ac_layout(n, h, g);
+    std::fill(p, p + o.total, 0.0);
+    uint64_t st = seed;
+    auto normal = [&]() {
+      double u1 = (double)(kt::rng_next(st) >> 11) * 0x1.0p-53;
+      const double u2 = (double)(kt::rng_next(st) >> 11) * 0x1.0p-53;
+      if (u1 <= 0.0) u1 = 0x1.0p-53;
+      return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925286766559 * u2);
+    };
+    const double s0 = 1.0 / std::sqrt((double)n), s1 = 1.0 / std::sqrt((double)h),
+                 s2 = 1.0 / std::sqrt((double)g);
+    for (int i = o.w0; i < o.b0; ++i) p[i] = normal() * s0;
+    for (int i = o.wp1; i < o.bp1; ++i) p[i] = normal() * s1;
+    for (int i = o.wp2; i < o.bp2; ++i) p[i] = normal() * s2;
+    for (int i = o.wv1; i < o.bv1; ++i) p[i] = normal() * s1;
+    for (int i = o.wv2; i < o.bv2; ++i) p[i] = normal() * s2;
+  });
+}
+
+int ktune_ac_create(ktune_ctx* ctx, int n, int h, int g, const double* flat, ktune_ac** out) {
+  return kt_guard(ctx, [&] {
+    check_dims(n, h, g);
+    auto* a = new ktune_ac();
+    a->ctx = ctx;
+    a->n = n;
+    a->h = h;
+    a->g = g;
+    a->num_params = ac_layout(n, h, g).total;
+    a->host_params.assign(flat, flat + a->num_params);
+    cudaSetDevice(ctx->device);
+    KT_CUDA(cudaMalloc(&a->d_params, sizeof(double) * a->num_params));
+    KT_CUDA(cudaMemcpy(a->d_params, flat, sizeof(double) * a->num_params, cudaMemcpyHostToDevice));
+    *out = a;
+  });
+}
+
+int ktune_ac_destroy(ktune_ac* a) {
+  if (!a) return KTUNE_OK;
+  cudaFree(a->d_params);
+  delete a;
+  return KTUNE_OK;
+}
+
+int ktune_ac_forward(ktune_ctx* ctx, const ktune_ac* ac, const double* states, int64_t B,
+                     double* log_probs, double* probs, double* values, int flags) {
+  return kt_guard(ctx, [&] {
+    if (B < 0) kt::fail(KTUNE_ERR_CONFIG, "negative batch");
+    if (B == 0) return;
+    const bool dev = flags & KTUNE_F_DEVICE;
+    const int n = ac->n;
+    const double* d_s = (const double*)kt::stage_in(ctx, kt::WS_IN0, states, sizeof(double) * B * n, dev);
+    double* d_lp = log_probs ? (double*)kt::out_buf(ctx, kt::WS_OUT0, log_probs, sizeof(double) * B * 3 * n, dev) : nullptr;
+    double* d_p = probs ? (double*)kt::out_buf(ctx, kt::WS_OUT1, probs, sizeof(double) * B * 3 * n, dev) : nullptr;
+    double* d_v = values ? (double*)kt::out_buf(ctx, kt::WS_OUT2, values, sizeof(double) * B, dev) : nullptr;
+    const bool sp = fits_smem(n, ac->h, ac->g);
+    const size_t smem = rollout_smem_bytes(n, ac->h, ac->g, sp);
+    KT_CUDA(cudaFuncSetAttribute(ac_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = (int)std::min<int64_t>(kt::ceil_div(B, kTile), kt::sm_count(ctx));
+    ac_forward_kernel<<<grid, kThreads, smem, ctx->stream>>>(ac->d_params, n, ac->h, ac->g, d_s, B, d_lp,
+                                                             d_p, d_v, sp ? 1 : 0);
+    kt::check_launch(ctx, "ac_forward");
+    if (d_lp) kt::stage_out(ctx, log_probs, d_lp, sizeof(double) * B * 3 * n, dev);
+    if (d_p) kt::stage_out(ctx, probs, d_p, sizeof(double) * B * 3 * n, dev);
+    if (d_v) kt::stage_out(ctx, values, d_v, sizeof(double) * B, dev);
+    if (!dev) KT_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ktune_debug_math(ktune_ctx* ctx, int op, const double* x, int64_t n, double* out) {
+  return kt_guard(ctx, [&] {
+    if (n <= 0) return;
+    const double* d_x = (const double*)kt::stage_in(ctx, kt::WS_IN0, x, sizeof(double) * n, false);
+    double* d_o = (double*)kt::out_buf(ctx, kt::WS_OUT0, out, sizeof(double) * n, false);
+    debug_math_kernel<<<(int)std::min<int64_t>(kt::ceil_div(n, 256), 4096), 256, 0, ctx->stream>>>(op, d_x, n, d_o);
+    kt::check_launch(ctx, "debug_math");
+    kt::stage_out(ctx, out, d_o, sizeof(double) * n, false);
+    KT_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks, int32_t T,
+                  int flags) {
+  return kt_guard(ctx, [&] {
+    if (num_tasks < 0 || T < 0) kt::fail(KTUNE_ERR_CONFIG, "rollout: bad task count or steps");
+    if (num_tasks == 0) return;
+    const bool dev = flags & KTUNE_F_DEVICE;
+    std::vector<RolloutTask> dt(num_tasks);
+    std::vector<CtaWork> work;
+    // device buffers for host-pointer calls
+    struct HostIo {
+      const uint16_t* d_init;
+      uint16_t* d_idx;
+      int8_t* d_act;
+      double* d_logp;
+      double* d_val;
+      double* d_score;
+    };
+    std::vector<HostIo> io(num_tasks);
+    std::vector<void*> temp;
+    auto alloc = [&](size_t bytes) {
+      void* p = nullptr;
+      KT_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
+      temp.push_back(p);
+      return p;
+    };
+    bool smem_params = true;
+    for (int k = 0; k < num_tasks; ++k) {
+      const ktune_rollout_task& t = tasks[k];
+      if (!t.space || !t.ac) kt::fail(KTUNE_ERR_CONFIG, "rollout: task needs a space and an agent");
+      if (t.ac->n != t.space->D) kt::fail(KTUNE_ERR_CONFIG, "rollout: agent/space knob count mismatch");
+      if (t.gbt && t.gbt->num_features != t.space->D) kt::fail(KTUNE_ERR_CONFIG, "rollout: cost model/space mismatch");
+      if (t.num_episodes < 0 || !t.idx) kt::fail(KTUNE_ERR_CONFIG, "rollout: bad episode count or missing idx output");
+      smem_params = smem_params && fits_smem(t.ac->n, t.ac->h, t.ac->g);
+      const int n = t.ac->n;
+      const int64_t E = t.num_episodes;
+      HostIo& h = io[k];
+      if (dev) {
+        h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score};
+      } else {
+        h.d_init = (const uint16_t*)alloc(std::max<size_t>(2, (size_t)E * n * 2));
+        KT_CUDA(cudaMemcpyAsync((void*)h.d_init, t.init_idx, (size_t)E * n * 2, cudaMemcpyHostToDevice, ctx->stream));
+        h.d_idx = (uint16_t*)alloc(std::max<size_t>(2, (size_t)E * (T + 1) * n * 2));
+        h.d_act = t.actions ? (int8_t*)alloc(std::max<size_t>(1, (size_t)E * T * n)) : nullptr;
+        h.d_logp = t.logp ? (double*)alloc(std::max<size_t>(8, (size_t)E * T * 8)) : nullptr;
+        h.d_val = t.value ? (double*)alloc(std::max<size_t>(8, (size_t)E * T * 8)) : nullptr;
+        h.d_score = t.score ? (double*)alloc(std::max<size_t>(8, (size_t)E * (T + 1) * 8)) : nullptr;
+      }
+      RolloutTask& r = dt[k];
+      r.sp = t.space->params;
+      r.params = t.ac->d_params;
+      r.n = n;
+      r.h = t.ac->h;
+      r.g = t.ac->g;
+      r.T = T;
+      r.E = E;
+      r.episode_offset = t.episode_offset;
+      r.seed = t.explore_seed;
+      r.init_idx = h.d_init;
+      r.idx = h.d_idx;
+      r.actions = h.d_act;
+      r.logp = h.d_logp;
+      r.value = h.d_val;
+      for (int64_t f = 0; f < E; f += kTile) work.push_back({k, f});
+    }
+    // one launch config for all tasks: smem sized for the largest task
+    size_t smem = 0;
+    for (int k = 0; k < num_tasks; ++k)
+      smem = std::max(smem, rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, smem_params));
+    if (smem > 227 * 1024) kt::fail(KTUNE_ERR_CONFIG, "rollout: agent too large for shared memory");
+    if (!work.empty()) {
+      RolloutTask* d_tasks = (RolloutTask*)alloc(sizeof(RolloutTask) * num_tasks);
+      CtaWork* d_work = (CtaWork*)alloc(sizeof(CtaWork) * work.size());
+      KT_CUDA(cudaMemcpyAsync(d_tasks, dt.data(), sizeof(RolloutTask) * num_tasks, cudaMemcpyHostToDevice, ctx->stream));
+      KT_CUDA(cudaMemcpyAsync(d_work, work.data(), sizeof(CtaWork) * work.size(), cudaMemcpyHostToDevice, ctx->stream));
+      KT_CUDA(cudaFuncSetAttribute(rollout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      rollout_kernel<<<(unsigned)work.size(), kThreads, smem, ctx->stream>>>(d_tasks, d_work, smem_params ? 1 : 0);
+      kt::check_launch(ctx, "rollout");
+    }
+    // cost-model scores of every visited configuration (K1 over the trajectory)
+    for (int k = 0; k < num_tasks; ++k) {
+      const ktune_rollout_task& t = tasks[k];
+      if (t.gbt && io[k].d_score && t.num_episodes > 0)
+        kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx, 2, t.num_episodes * (int64_t)(T + 1), io[k].d_score);
+    }
+    if (!dev) {
+      for (int k = 0; k < num_tasks; ++k) {
+        const ktune_rollout_task& t = tasks[k];
+        const int64_t E = t.num_episodes;
+        const int n = t.ac->n;
+        const HostIo& h = io[k];
+        KT_CUDA(cudaMemcpyAsync(t.idx, h.d_idx, (size_t)E * (T + 1) * n * 2, cudaMemcpyDeviceToHost, ctx->stream));
+        if (t.actions) KT_CUDA(cudaMemcpyAsync(t.actions, h.d_act, (size_t)E * T * n, cudaMemcpyDeviceToHost, ctx->stream));
+        if (t.logp) KT_CUDA(cudaMemcpyAsync(t.logp, h.d_logp, (size_t)E * T * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (t.value) KT_CUDA(cudaMemcpyAsync(t.value, h.d_val, (size_t)E * T * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        if (t.score && t.gbt) KT_CUDA(cudaMemcpyAsync(t.score, h.d_score, (size_t)E * (T + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+      }
+    }
+    for (void* p : temp) KT_CUDA(cudaFreeAsync(p, ctx->stream));
+    if (!dev) KT_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

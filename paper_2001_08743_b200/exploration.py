@@ -1,0 +1,178 @@
+"""Adaptive Exploration on the GPU: ActorCritic (actor_critic.hpp:18-64) and
+run_episodes through the persistent rollout kernel (K2).
+
+Builder-pinned details (no reference code exists for this module):
+DESIGN.md §5 — flat parameter layout of actor_critic.hpp:52-53 with
+column-major matrices, seeded init, fp64 forward with the portable
+tanh/exp/log, counter-based RNG u(e,t,d) = hash01(stream_seed(root,"explore"),
+(e*T+t)*D+d) keyed by the GLOBAL episode id e, inverse-CDF sampling,
+saturating apply, every episode runs exactly T steps.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+from .context import Context, Space, default_context, ptr_of
+from .cost_model import DeviceGbt
+from .errors import ConfigError
+from .spaces import stream_seed
+
+
+def num_parameters(n: int, h: int = 128, g: int = 64) -> int:
+    return int(L.lib().ktune_ac_num_params(n, h, g))
+
+
+def init_parameters(n: int, h: int = 128, g: int = 64, seed: int = 0) -> np.ndarray:
+    p = np.zeros(num_parameters(n, h, g), np.float64)
+    L.check(L.lib().ktune_ac_init_params(n, h, g, seed, p.ctypes.data_as(C.c_void_p)))
+    return p
+
+
+class ActorCritic:
+    """ktune::ActorCritic (actor_critic.hpp:18-64); forward runs on the GPU."""
+
+    def __init__(self, num_knobs: int, hidden_dim: int = 128, head_hidden: int = 64, seed: int = 0,
+                 params: Optional[np.ndarray] = None, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.n, self.h, self.g = num_knobs, hidden_dim, head_hidden
+        self.params = (np.ascontiguousarray(params, np.float64).copy() if params is not None
+                       else init_parameters(num_knobs, hidden_dim, head_hidden, seed))
+        if len(self.params) != num_parameters(num_knobs, hidden_dim, head_hidden):
+            raise ConfigError("actor-critic: parameter vector has the wrong length")
+        self.h_dev = None
+        self._upload()
+
+    def _upload(self):
+        if self.h_dev is not None:
+            L.lib().ktune_ac_destroy(self.h_dev)
+        h = C.c_void_p()
+        self.ctx.check(L.lib().ktune_ac_create(self.ctx.h, self.n, self.h, self.g,
+                                               self.params.ctypes.data_as(C.c_void_p), C.byref(h)))
+        self.h_dev = h
+
+    def set_parameters(self, params: np.ndarray) -> None:
+        self.params = np.ascontiguousarray(params, np.float64).copy()
+        self._upload()
+
+    @property
+    def num_parameters(self) -> int:
+        return len(self.params)
+
+    def forward(self, states):
+        """Returns dict(log_probs B x 3n, probs B x 3n, values B) (actor_critic.hpp:30-43)."""
+        S = np.ascontiguousarray(states, np.float64).reshape(-1, self.n)
+        B = len(S)
+        lp = np.zeros((B, 3 * self.n))
+        pr = np.zeros((B, 3 * self.n))
+        v = np.zeros(B)
+        if B:
+            self.ctx.check(L.lib().ktune_ac_forward(self.ctx.h, self.h_dev, S.ctypes.data_as(C.c_void_p), B,
+                                                    lp.ctypes.data_as(C.c_void_p), pr.ctypes.data_as(C.c_void_p),
+                                                    v.ctypes.data_as(C.c_void_p), 0))
+        return dict(log_probs=lp, probs=pr, values=v)
+
+    def __del__(self):
+        try:
+            if self.h_dev is not None:
+                L.lib().ktune_ac_destroy(self.h_dev)
+        except Exception:
+            pass
+
+
+@dataclass
+class RolloutTask:
+    """One workload of a grouped rollout launch."""
+    space: Space
+    agent: ActorCritic
+    cost_model: Optional[DeviceGbt]
+    init_idx: object          # E x D (numpy int / CUDA uint16 tensor)
+    episode_offset: int = 0   # global id of the first episode (RNG key; sharding)
+    root_seed: int = 0        # explore seed = stream_seed(root_seed, "explore")
+    want_trajectory: bool = True
+
+
+def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Context] = None,
+                       device_out: bool = False):
+    """Grouped run_episodes over several workloads in ONE persistent-kernel launch.
+
+    Host arrays in/out by default; with CUDA-tensor init_idx and device_out=True
+    everything stays on the device (torch tensors) and the call is stream-ordered.
+    Returns per task dict(idx E x (T+1) x D uint16, score E x (T+1), actions
+    E x T x D int8, logp E x T, value E x T).
+    """
+    ctx = ctx or tasks[0].space.ctx
+    arr = (L.RolloutTaskC * len(tasks))()
+    outs = []
+    keep = []
+    dev = False
+    for i, t in enumerate(tasks):
+        D = t.space.D
+        if t.agent.n != D:
+            raise ConfigError("rollout: agent/space knob count mismatch")
+        dev = hasattr(t.init_idx, "is_cuda") and t.init_idx.is_cuda
+        if dev:
+            import torch
+            init = t.init_idx.to(torch.uint16).contiguous() if t.init_idx.dtype != torch.uint16 else t.init_idx.contiguous()
+            E = init.shape[0]
+            mk = lambda shape, dt: torch.empty(shape, dtype=dt, device=init.device)
+            o = dict(idx=mk((E, T + 1, D), torch.uint16),
+                     score=mk((E, T + 1), torch.float64) if t.cost_model is not None else None,
+                     actions=mk((E, T, D), torch.int8) if t.want_trajectory else None,
+                     logp=mk((E, T), torch.float64) if t.want_trajectory else None,
+                     value=mk((E, T), torch.float64) if t.want_trajectory else None)
+            pp = lambda a: None if a is None else C.c_void_p(a.data_ptr())
+            init_p = C.c_void_p(init.data_ptr())
+            keep.append(init)
+        else:
+            init = np.ascontiguousarray(t.init_idx, np.uint16).reshape(-1, D)
+            E = len(init)
+            o = dict(idx=np.zeros((E, T + 1, D), np.uint16),
+                     score=np.zeros((E, T + 1)) if t.cost_model is not None else None,
+                     actions=np.zeros((E, T, D), np.int8) if t.want_trajectory else None,
+                     logp=np.zeros((E, T)) if t.want_trajectory else None,
+                     value=np.zeros((E, T)) if t.want_trajectory else None)
+            pp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
+            init_p = init.ctypes.data_as(C.c_void_p)
+            keep.append(init)
+        a = arr[i]
+        a.space = t.space.h
+        a.ac = t.agent.h_dev
+        a.gbt = t.cost_model.h if t.cost_model is not None else None
+        a.num_episodes = E
+        a.episode_offset = t.episode_offset
+        a.explore_seed = stream_seed(t.root_seed, "explore")
+        a.init_idx = init_p
+        a.idx = pp(o["idx"])
+        a.score = pp(o["score"])
+        a.actions = pp(o["actions"])
+        a.logp = pp(o["logp"])
+        a.value = pp(o["value"])
+        outs.append(o)
+    ctx.check(L.lib().ktune_rollout(ctx.h, len(tasks), arr, T, L.F_DEVICE if dev else 0))
+    return outs
+
+
+def run_episodes(space: Space, cost_model: Optional[DeviceGbt], agent: ActorCritic, init_idx, T: int,
+                 root_seed: int = 0, episode_offset: int = 0):
+    """run_episodes(space, cost_model, net, params, initial_configs, rng).
+
+    Returns (candidates, trajectory): candidates is a CandidateSet over every
+    visited configuration Θ_0..Θ_T of every episode with its predicted
+    fitness; trajectory holds actions, log-probabilities, values and the
+    per-step rewards r_t = pred(Θ_{t+1}) - pred(Θ_t).
+    """
+    from .sampling import make_candidate_set
+    o = run_episodes_batch([RolloutTask(space, agent, cost_model, init_idx, episode_offset, root_seed)], T)[0]
+    E = o["idx"].shape[0]
+    flat = o["idx"].reshape(-1, space.D).astype(np.int32)
+    score = o["score"].reshape(-1) if o["score"] is not None else np.zeros(len(flat))
+    cands = make_candidate_set(space, flat, score)
+    traj = dict(o)
+    if o["score"] is not None:
+        traj["reward"] = o["score"][:, 1:] - o["score"][:, :-1]
+    return cands, traj

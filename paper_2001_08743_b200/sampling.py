@@ -1,0 +1,189 @@
+"""Adaptive Sampling (sampling.hpp:16-80) on the GPU: kmeans_run (K3-K5),
+the threshold k-sweep, centroid snapping (K6) and the host sample synthesis.
+
+`clusterer(...)` returns a callable with the reference `Clusterer` signature
+(sampling.hpp:44-46) so the GPU k-means drops into code written against it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib as L
+from .context import Context, Space, ptr_of
+from .errors import ConfigError
+
+
+@dataclass
+class SamplingParams:  # sampling.hpp:16-23
+    threshold: float = 2.5
+    k_min: int = 8
+    k_max_exclusive: int = 64
+    greedy_batch: int = 64
+    kmeans_max_iters: int = 100
+    kmeans_restarts: int = 3
+
+    def c(self) -> L.SamplingParamsC:
+        return L.SamplingParamsC(self.threshold, self.k_min, self.k_max_exclusive,
+                                 self.kmeans_max_iters, self.kmeans_restarts)
+
+
+@dataclass
+class ClusterResult:  # sampling.hpp:27-32
+    centroids: np.ndarray
+    assignments: np.ndarray
+    l2_loss: float
+    iteration_losses: List[float] = field(default_factory=list)
+
+
+@dataclass
+class CandidateSet:  # candidates.hpp:20-27 (structure-of-arrays)
+    idx: np.ndarray          # N x D int32 configurations, ranked
+    ids: np.ndarray          # N uint64 ordinals
+    predicted: np.ndarray    # N float64
+
+    def __len__(self):
+        return len(self.ids)
+
+    def empty(self) -> bool:
+        return len(self.ids) == 0
+
+
+def make_candidate_set(space: Space, idx, predicted, ids=None) -> CandidateSet:
+    """make_candidate_set (sampling.cpp:16-31): dedup by id (first wins), rank by (pred desc, id asc)."""
+    idx = np.ascontiguousarray(idx, np.int32).reshape(-1, space.D)
+    pred = np.ascontiguousarray(predicted, np.float64).reshape(-1)
+    ids = space.id_of(idx) if ids is None else np.ascontiguousarray(ids, np.uint64)
+    rows = np.zeros(len(ids), np.int64)
+    m = C.c_int64()
+    space.ctx.check(L.lib().ktune_make_candidate_set(space.ctx.h, ids.ctypes.data_as(C.c_void_p),
+                                                     pred.ctypes.data_as(C.c_void_p), len(ids),
+                                                     rows.ctypes.data_as(C.c_void_p), C.byref(m)))
+    rows = rows[:m.value]
+    return CandidateSet(idx[rows], ids[rows], pred[rows])
+
+
+def _packed(space: Space, idx):
+    if hasattr(idx, "is_cuda") and idx.is_cuda:
+        return idx, True
+    return np.ascontiguousarray(idx, dtype=space.idx_dtype).reshape(-1, space.D), False
+
+
+def kmeans_run(space: Space, idx, k: int, seed: int, max_iters: int = 100, restarts: int = 3) -> ClusterResult:
+    """kmeans_run (sampling.cpp:157-175) over lattice points given as knob indices."""
+    arr, dev = _packed(space, idx)
+    N = (arr.numel() if dev else arr.size) // space.D
+    cen = np.zeros((max(k, 1), space.D), np.float64)
+    asg = np.zeros(N, np.int32)
+    loss = C.c_double()
+    il = np.zeros(max_iters + 1, np.float64)
+    nl = C.c_int32()
+    out = L.KmeansOutC(cen.ctypes.data_as(C.c_void_p), asg.ctypes.data_as(C.c_void_p),
+                       C.cast(C.pointer(loss), C.c_void_p), il.ctypes.data_as(C.c_void_p),
+                       C.cast(C.pointer(nl), C.c_void_p))
+    p = C.c_void_p(arr.data_ptr()) if dev else arr.ctypes.data_as(C.c_void_p)
+    if dev:  # device points, host outputs: stage through host result buffers
+        raise ConfigError("kmeans_run: pass host arrays (device-resident use goes through adaptive_sweep)")
+    space.ctx.check(L.lib().ktune_kmeans_run(space.ctx.h, space.h, p, space.index_bytes, N, k, seed,
+                                             max_iters, restarts, C.byref(out), 0))
+    return ClusterResult(cen[:k], asg, loss.value, list(il[:nl.value]))
+
+
+def clusterer(space: Space, params: SamplingParams = SamplingParams()):
+    """A `Clusterer` (sampling.hpp:44-46): (points as knob-index rows, k, seed) -> ClusterResult."""
+    def run(points_idx, k: int, seed: int) -> ClusterResult:
+        return kmeans_run(space, points_idx, k, seed, params.kmeans_max_iters, params.kmeans_restarts)
+    return run
+
+
+@dataclass
+class SweepResult:
+    k: int
+    centroids: np.ndarray
+    assignments: np.ndarray
+    l2_loss: float
+    k_losses: List[float]
+    snapped: np.ndarray
+
+
+def adaptive_sweep(space: Space, cands: CandidateSet, params: SamplingParams = SamplingParams(),
+                   rng_seed: int = 0) -> SweepResult:
+    """The k-sweep of adaptive_sample (sampling.cpp:436-446) + snap (:448-452), on the GPU."""
+    arr, _ = _packed(space, cands.idx)
+    ids = np.ascontiguousarray(cands.ids, np.uint64)
+    N = len(ids)
+    kmax = max(1, params.k_max_exclusive)
+    k = C.c_int32()
+    cen = np.zeros((kmax, space.D))
+    asg = np.zeros(N, np.int32)
+    loss = C.c_double()
+    kl = np.zeros(kmax)
+    nk = C.c_int32()
+    snap = np.zeros((kmax, space.D), np.int32)
+    out = L.SweepOutC(C.cast(C.pointer(k), C.c_void_p), cen.ctypes.data_as(C.c_void_p),
+                      asg.ctypes.data_as(C.c_void_p), C.cast(C.pointer(loss), C.c_void_p),
+                      kl.ctypes.data_as(C.c_void_p), C.cast(C.pointer(nk), C.c_void_p),
+                      snap.ctypes.data_as(C.c_void_p))
+    pc = params.c()
+    space.ctx.check(L.lib().ktune_adaptive_sweep(space.ctx.h, space.h, arr.ctypes.data_as(C.c_void_p),
+                                                 space.index_bytes, ids.ctypes.data_as(C.c_void_p), N,
+                                                 C.byref(pc), rng_seed, C.byref(out), 0))
+    kk = k.value
+    return SweepResult(kk, cen[:kk], asg, loss.value, list(kl[:nk.value]), snap[:kk])
+
+
+def snap_centroid(space: Space, centroids, cands: CandidateSet) -> np.ndarray:
+    """snap_centroid (sampling.cpp:202-235) for one centroid (D,) or a batch (k x D)."""
+    cen = np.ascontiguousarray(centroids, np.float64)
+    single = cen.ndim == 1
+    cen = cen.reshape(-1, space.D)
+    k = len(cen)
+    arr, _ = _packed(space, cands.idx)
+    ids = np.ascontiguousarray(cands.ids, np.uint64)
+    out = np.zeros((k, space.D), np.int32)
+    space.ctx.check(L.lib().ktune_snap(space.ctx.h, space.h, cen.ctypes.data_as(C.c_void_p), k,
+                                       arr.ctypes.data_as(C.c_void_p), space.index_bytes,
+                                       ids.ctypes.data_as(C.c_void_p), len(ids),
+                                       out.ctypes.data_as(C.c_void_p), 0))
+    return out[0] if single else out
+
+
+def adaptive_sample(space: Space, cands: CandidateSet, visited, params: SamplingParams = SamplingParams(),
+                    rng_seed: int = 0) -> np.ndarray:
+    """adaptive_sample (sampling.cpp:409-461): returns the configurations to measure (k x D)."""
+    if cands.empty():
+        raise ConfigError("adaptive_sample: empty candidate set")
+    idx = np.ascontiguousarray(cands.idx, np.int32)
+    ids = np.ascontiguousarray(cands.ids, np.uint64)
+    vis = np.ascontiguousarray(np.fromiter(visited, np.uint64) if not isinstance(visited, np.ndarray)
+                               else visited, np.uint64)
+    out = np.zeros((max(1, params.k_max_exclusive), space.D), np.int32)
+    cnt = C.c_int32()
+    pc = params.c()
+    space.ctx.check(L.lib().ktune_adaptive_sample(space.ctx.h, space.h, idx.ctypes.data_as(C.c_void_p),
+                                                  ids.ctypes.data_as(C.c_void_p), len(ids),
+                                                  vis.ctypes.data_as(C.c_void_p), len(vis), C.byref(pc),
+                                                  rng_seed, out.ctypes.data_as(C.c_void_p), C.byref(cnt)))
+    return out[:cnt.value]
+
+
+def synthesize_sample(space: Space, cands: CandidateSet, visited, rng_state: int):
+    """synthesize_sample (sampling.cpp:379-403); returns (config, advanced rng state)."""
+    idx = np.ascontiguousarray(cands.idx, np.int32)
+    vis = np.ascontiguousarray(np.fromiter(visited, np.uint64) if not isinstance(visited, np.ndarray)
+                               else visited, np.uint64)
+    st = C.c_uint64(rng_state)
+    out = np.zeros(space.D, np.int32)
+    L.check(L.lib().ktune_synthesize_sample(space.h, idx.ctypes.data_as(C.c_void_p), len(idx),
+                                            vis.ctypes.data_as(C.c_void_p), len(vis), C.byref(st),
+                                            out.ctypes.data_as(C.c_void_p)), space.ctx.h)
+    return out, st.value
+
+
+def greedy_select(cands: CandidateSet, batch: int) -> np.ndarray:
+    """greedy_select (sampling.cpp:181-196): CandidateSet is already ranked (pred desc, id asc)."""
+    order = np.lexsort((cands.ids, -cands.predicted))
+    return cands.idx[order[:max(0, batch)]]

