@@ -1,0 +1,368 @@
+#!/usr/bin/env python3
+"""Headline benchmark: candidate configs scored/sec (rollout + cost model), with
+the k-means ms/iter secondary metric, on B200.
+
+Workload (BASELINE.json configs[1]): ResNet-18, all 12 tuning tasks, 4096
+episodes (configs/step) per task, T = 500 episode steps, one grouped launch of
+the persistent rollout kernel + GBT scoring of every visited configuration.
+One bench "step" = one run_episodes pass over all 12 tasks; the unit is one
+config-step (actor-critic forward + per-knob sampling + saturating update +
+cost-model score of the new configuration).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1: launched by torchrun, one rank per GPU; every rank runs its own 12 x 4096
+episodes with globally offset episode ids (weak scaling, no data-path
+collective); the time is the max over ranks.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOP_PER_CONFIG_STEP = lambda n, h=128, g=64: 2 * (h * n + 2 * h * g + 3 * n * g + g)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def build_tasks(args, rank):
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.workloads import make_tasks
+    spaces = S.resnet18_tasks()[: args.tasks]
+    return make_tasks(spaces, args.episodes, seed=args.seed + 7919 * rank)
+
+
+def cpu_sample(specs, models, agents_params, args, threads):
+    """Oracle (CPU restatement; the rollout has no reference code) on a bounded sample."""
+    from oracle import pyoracle as O
+    from paper_2001_08743_b200.spaces import stream_seed
+    E, T = args.cpu_episodes, args.cpu_T
+    t0 = time.perf_counter()
+    n = 0
+    for spec, m, p in zip(specs, models, agents_params):
+        osp = O.OSpace(spec.space)
+        og = O.Gbt(m.base_prediction, m.learning_rate, m.num_features, m.offsets, m.feature, m.left, m.right,
+                   m.threshold, m.value, m.training_sse)
+        O.run_episodes(osp, og, 128, 64, p, spec.init_idx[:E], T, 0, stream_seed(spec.seed, "explore"),
+                       threads=threads, want_traj=True)
+        n += E * T
+    dt = time.perf_counter() - t0
+    return n / dt, f"{len(specs)} tasks x {E} episodes x {T} steps ({n} config-steps) in {dt:.2f}s"
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2001_08743_b200.cost_model import fit_gbt
+    from paper_2001_08743_b200.exploration import init_parameters
+    from paper_2001_08743_b200.workloads import encode
+    specs = build_tasks(args, 0)
+    models = [fit_gbt(encode(s.space, s.train_idx), s.train_y, seed=s.seed) for s in specs]
+    params = [init_parameters(s.space.num_knobs, 128, 64, s.seed) for s in specs]
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, sample = cpu_sample(specs, models, params, args, threads)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {"metric": "candidate configs scored/sec (rollout+cost model)", "value": value,
+            "unit": "config-steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * (args.cpu_episodes * args.cpu_T * len(specs)) / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded AutoTVM-style ResNet-18 conv spaces, SyntheticBackend-fitted GBT)",
+            "config": {"workload": "resnet18-12tasks-rollout (CPU sample)", "tasks": len(specs),
+                       "episodes_per_task": args.cpu_episodes, "T": args.cpu_T},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "config-steps/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "config-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def kmeans_secondary(ctx, args):
+    """k-means sampling ms/iter: AlexNet conv2 space (uint16 indices), 1M candidates."""
+    import torch
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep, kmeans_run
+    from paper_2001_08743_b200.workloads import random_configs
+    sp = S.alexnet_tasks()[1]
+    ds = Space(sp, ctx)
+    idx = random_configs(sp, args.kmeans_n, 123)
+    ids = ds.id_of(idx)
+    _, first = np.unique(ids, return_index=True)
+    idx = idx[np.sort(first)]
+    ctx.reset_stats()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = kmeans_run(ds, idx, 8, 11, restarts=1)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    iters = len(r.iteration_losses) - 1
+    assign_ns = ctx.stat(L.STAT_ASSIGN_NS)
+    assign_calls = max(1, ctx.stat(L.STAT_ASSIGN_CALLS))
+    # full adaptive_sample sweep + snap (default threshold 2.5)
+    t1 = time.perf_counter()
+    sw = adaptive_sweep(ds, CandidateSet(idx, ids[np.sort(first)], np.zeros(len(idx))), SamplingParams(), 5)
+    dsw = time.perf_counter() - t1
+    N = len(idx)
+    bytes_pt = sp.num_knobs * 2 + 4 + 4 + 8  # idx + assignment write + prev read + d2 write
+    a_ms = assign_ns / assign_calls / 1e6
+    return {"metric": "k-means sampling ms/iter", "value": 1e3 * dt / max(1, iters), "unit": "ms/iter",
+            "workload": f"alexnet.c2 space (u16), N={N}, k=8, 1 restart", "lloyd_iters": iters,
+            "kmeans_run_ms": 1e3 * dt, "adaptive_sample_ms": 1e3 * dsw, "sweep_k": sw.k,
+            "assign_kernel_ms": a_ms,
+            "assign_roofline": {"bound": "hbm", "achieved": N * bytes_pt / (a_ms * 1e-3) / 1e9, "unit": "GB/s"}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tasks", type=int, default=12)
+    ap.add_argument("--episodes", type=int, default=4096)
+    ap.add_argument("--T", type=int, default=500)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-episodes", type=int, default=64)
+    ap.add_argument("--cpu-T", type=int, default=200)
+    ap.add_argument("--kmeans-n", type=int, default=1 << 20)
+    ap.add_argument("--no-kmeans", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.context import Context, Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
+    from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
+    from paper_2001_08743_b200.workloads import encode
+
+    ctx = Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    specs = build_tasks(args, rank)
+    models = [fit_gbt(encode(s.space, s.train_idx), s.train_y, seed=s.seed) for s in specs]
+    spaces = [Space(s.space, ctx) for s in specs]
+    gbts = [DeviceGbt(m, d) for m, d in zip(models, spaces)]
+    agents = [ActorCritic(s.space.num_knobs, 128, 64, seed=s.seed, ctx=ctx) for s in specs]
+    E, T = args.episodes, args.T
+    inits_dev = [torch.from_numpy(s.init_idx.astype(np.uint16)).cuda() for s in specs]
+    tasks = [RolloutTask(d, a, g, init, episode_offset=rank * E, root_seed=s.seed)
+             for s, d, a, g, init in zip(specs, spaces, agents, gbts, inits_dev)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    for _ in range(args.warmup):
+        run_episodes_batch(tasks, T, ctx)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    ctx.set_option(L.OPT_PROFILE, 1)
+    ctx.reset_stats()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            flush.zero_()
+            outs = run_episodes_batch(tasks, T, ctx)
+        end.record(stream)
+        barrier()
+    ms = start.elapsed_time(end)
+    launches = ctx.stat(L.STAT_LAUNCHES)
+    roll_ns, roll_calls = ctx.stat(L.STAT_ROLLOUT_NS), ctx.stat(L.STAT_ROLLOUT_CALLS)
+    gbt_ns, gbt_calls = ctx.stat(L.STAT_GBT_NS), ctx.stat(L.STAT_GBT_CALLS)
+    ctx.set_option(L.OPT_PROFILE, 0)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    units_per_step = world * len(specs) * E * T
+    value = units_per_step * args.steps / (ms * 1e-3)
+    n_knobs = specs[0].space.num_knobs
+    flop = FLOP_PER_CONFIG_STEP(n_knobs)
+    roll_s = roll_ns / max(1, roll_calls) * 1e-9
+    peaks, peak_src = load_peaks()
+    achieved = len(specs) * E * T * flop / roll_s / 1e12
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "rollout_ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pinned = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()
+        host_init = [pinned(s.init_idx.shape, torch.int16).view(np.uint16) for s in specs]
+        for h, s in zip(host_init, specs):
+            h[:] = s.init_idx
+        D = n_knobs
+        host_out = [dict(idx=pinned((E, T + 1, D), torch.int16).view(np.uint16),
+                         score=pinned((E, T + 1), torch.float64), actions=pinned((E, T, D), torch.int8),
+                         logp=pinned((E, T), torch.float64), value=pinned((E, T), torch.float64)) for _ in specs]
+        htasks = [RolloutTask(d, a, g, hi, episode_offset=rank * E, root_seed=s.seed)
+                  for s, d, a, g, hi in zip(specs, spaces, agents, gbts, host_init)]
+        ctx.set_stream(None)
+        run_episodes_batch(htasks, T, ctx, host_out=host_out)  # warm
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            run_episodes_batch(htasks, T, ctx, host_out=host_out)
+        barrier()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            dt = float(t.item())
+        bi = sum(h.nbytes for h in host_init)
+        bo = sum(sum(v.nbytes for v in o.values()) for o in host_out)
+        e2e = {"value": units_per_step * args.steps / dt, "unit": "config-steps/s", "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo}
+        ctx.set_stream(stream.cuda_stream)
+
+    kmeans = None
+    if not args.no_kmeans and rank == 0:
+        try:
+            kmeans = kmeans_secondary(ctx, args)
+        except Exception as ex:  # reported, not hidden
+            kmeans = {"error": repr(ex)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from paper_2001_08743_b200.exploration import init_parameters
+        params = [a.params for a in agents]
+        threads = os.cpu_count() or 1
+        v, sample = cpu_sample(specs, models, params, args, threads)
+        cpu = {"value": v, "unit": "config-steps/s", "cores": threads, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": "candidate configs scored/sec (rollout+cost model)",
+            "value": value, "unit": "config-steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded AutoTVM-style ResNet-18 conv spaces, SyntheticBackend-fitted GBT, seeded agent)",
+            "config": {"workload": "resnet18-12tasks-rollout (BASELINE configs[1])", "tasks": len(specs),
+                       "episodes_per_task_per_gpu": E, "T": T, "knobs": n_knobs, "hidden": [128, 64],
+                       "gbt": "50 trees depth<=4", "path": "exact fp64 (bit-exact with the oracle)",
+                       "l2": "256 MB buffer written between timed steps; outputs 1.2 GB/step > L2",
+                       "parallelism": f"dp{world} (episodes sharded, no collective)"},
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "rollout_kernel",
+                         "kernel_ms": roll_s * 1e3, "flop_per_config_step": flop,
+                         "peak_source": f"{peak_src} bf16_tflops_sustained",
+                         "note": "exact path runs on the FP64 pipe (SIMT, no FMA); tensor-pipe fraction reported against bf16 as BASELINE.md asks"},
+            "gbt_kernel_ms_per_step": gbt_ns / max(1, gbt_calls) * 1e-6 * len(specs),
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "secondary": kmeans,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

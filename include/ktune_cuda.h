@@ -70,7 +70,8 @@ int ktune_ctx_synchronize(ktune_ctx* ctx);
 
 enum ktune_option {
   KTUNE_OPT_FORCE_EXACT = 1, /* 1: k-means decisions always via the exact-order fallback chains */
-  KTUNE_OPT_KMEANS_MODE = 2  /* 0 auto, 1 exact-order centroids (mode A), 2 certified integer centroids (mode B) */
+  KTUNE_OPT_KMEANS_MODE = 2, /* 0 auto, 1 exact-order centroids (mode A), 2 certified integer centroids (mode B) */
+  KTUNE_OPT_PROFILE = 3      /* 1: bracket the hot kernels with CUDA events on their stream (KTUNE_STAT_*_NS) */
 };
 int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value);
 
@@ -81,7 +82,13 @@ enum ktune_stat {
   KTUNE_STAT_ASSIGN_FALLBACKS = 4,  /* Lloyd iterations that needed exact-order centroids (mode B) */
   KTUNE_STAT_SNAP_CHAINS = 5,       /* centroid coordinates recomputed by exact-order chains for snapping */
   KTUNE_STAT_LLOYD_ITERS = 6,
-  KTUNE_STAT_KPP_PICKS = 7
+  KTUNE_STAT_KPP_PICKS = 7,
+  KTUNE_STAT_ROLLOUT_NS = 8,        /* summed device time of rollout_kernel launches (KTUNE_OPT_PROFILE) */
+  KTUNE_STAT_ROLLOUT_CALLS = 9,
+  KTUNE_STAT_GBT_NS = 10,           /* summed device time of gbt_predict_idx launches */
+  KTUNE_STAT_GBT_CALLS = 11,
+  KTUNE_STAT_ASSIGN_NS = 12,        /* summed device time of k-means assign launches */
+  KTUNE_STAT_ASSIGN_CALLS = 13
 };
 int ktune_ctx_stat(ktune_ctx* ctx, int stat, int64_t* value);
 int ktune_ctx_reset_stats(ktune_ctx* ctx);

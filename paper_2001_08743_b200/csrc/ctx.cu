@@ -40,6 +40,19 @@ void check_launch(ktune_ctx* ctx, const char* what, int n) {
   ctx->count_launch(n);
 }
 
+void resolve_timings(ktune_ctx* ctx) {
+  for (auto& t : ctx->pending) {
+    cudaEventSynchronize(t.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    ctx->stats[t.stat_ns] += (int64_t)((double)ms * 1e6);
+    ctx->stats[t.stat_ns + 1] += 1;
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  ctx->pending.clear();
+}
+
 }  // namespace kt
 
 // ============================================================ rule compiler
@@ -260,6 +273,7 @@ int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value) {
   return kt_guard(ctx, [&] {
     if (option == KTUNE_OPT_FORCE_EXACT) ctx->opt_force_exact = value;
     else if (option == KTUNE_OPT_KMEANS_MODE) ctx->opt_kmeans_mode = value;
+    else if (option == KTUNE_OPT_PROFILE) ctx->opt_profile = value;
     else kt::fail(KTUNE_ERR_CONFIG, "unknown option");
   });
 }
@@ -267,12 +281,16 @@ int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value) {
 int ktune_ctx_stat(ktune_ctx* ctx, int stat, int64_t* value) {
   return kt_guard(ctx, [&] {
     if (stat < 0 || stat >= 16) kt::fail(KTUNE_ERR_CONFIG, "unknown stat");
+    kt::resolve_timings(ctx);
     *value = ctx->stats[stat];
   });
 }
 
 int ktune_ctx_reset_stats(ktune_ctx* ctx) {
-  return kt_guard(ctx, [&] { std::fill(std::begin(ctx->stats), std::end(ctx->stats), 0); });
+  return kt_guard(ctx, [&] {
+    kt::resolve_timings(ctx);
+    std::fill(std::begin(ctx->stats), std::end(ctx->stats), 0);
+  });
 }
 
 // ------------------------------------------------------------ design space

@@ -268,6 +268,7 @@ void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_id
   const int per_sm = use_smem ? std::max(1, (int)((220 * 1024) / smem)) : 4;
   const int64_t want = ceil_div(B, threads);
   const int grid = (int)std::min<int64_t>(want, (int64_t)sm_count(ctx) * std::min(per_sm, 8));
+  kt::ProfScope prof(ctx, KTUNE_STAT_GBT_NS);
   if (idx_bytes == 1) {
     auto k = gbt_predict_idx_kernel<uint8_t>;
     KT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

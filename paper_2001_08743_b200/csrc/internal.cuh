@@ -93,7 +93,13 @@ struct ktune_ctx {
   std::string last_error;
   int64_t opt_force_exact = 0;
   int64_t opt_kmeans_mode = 0;
+  int64_t opt_profile = 0;
   int64_t stats[16] = {0};
+  struct PendingTiming {
+    cudaEvent_t a, b;
+    int stat_ns;
+  };
+  std::vector<PendingTiming> pending;  // resolved lazily by ktune_ctx_stat
   kt::DevBuf ws[kt::WS_NUM_SLOTS];
   kt::HostBuf pinned[4];
   void* dev(int slot, size_t bytes) { return ws[slot].get(bytes); }
@@ -179,6 +185,27 @@ void allgather(ktune_ctx* ctx, const void* send, void* recv, size_t bytes_per_ra
 }  // namespace kt
 
 void kt_nccl_destroy(ktune_ctx* ctx);
+
+namespace kt {
+// Brackets one launch with CUDA events on ctx->stream when KTUNE_OPT_PROFILE is set.
+struct ProfScope {
+  ktune_ctx* ctx;
+  int stat_ns;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(ktune_ctx* c, int s) : ctx(c), stat_ns(s) {
+    if (!ctx->opt_profile) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, ctx->stream);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, ctx->stream);
+    ctx->pending.push_back({a, b, stat_ns});
+  }
+};
+void resolve_timings(ktune_ctx* ctx);
+}  // namespace kt
 
 namespace kt {
 

@@ -823,6 +823,7 @@ struct KMeans {
                 unsigned long long* changed_out) {
     KT_CUDA(cudaMemsetAsync(ull, 0, 16, s()));
     const size_t smem = sizeof(double) * (k * D) + lut_smem;
+    kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
     assign_kernel<IdxT><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent, k, prev, asg,
                                                         dd, chunk, ull);
     kt::check_launch(ctx, "assign");

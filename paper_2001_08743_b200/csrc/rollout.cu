@@ -70,7 +70,7 @@ struct CtaWork {
 __host__ __device__ inline size_t rollout_smem_bytes(int n, int h, int g, bool smem_params) {
   const AcOff o = ac_layout(n, h, g);
   const int act = (h > 2 * g ? h : 2 * g) * kTile;
-  size_t d = (smem_params ? (size_t)o.total : 0) + act + (size_t)3 * n * kTile + kTile;
+  size_t d = (smem_params ? (size_t)((o.total + 1) & ~1) : 0) + act + (size_t)3 * n * kTile + kTile;
   return d * 8 + (size_t)kTile * n * 2 + 16;
 }
 
@@ -178,7 +178,7 @@ rollout_kernel(const RolloutTask* __restrict__ tasks, const CtaWork* __restrict_
     for (int i = threadIdx.x; i < o.total; i += kThreads) p_s[i] = P[i];
     P = p_s;
   }
-  double* act = sm + (smem_params ? o.total : 0);
+  double* act = sm + (smem_params ? ((o.total + 1) & ~1) : 0);  // 16-byte aligned (double2 loads)
   double* buf = act + (h > 2 * g ? h : 2 * g) * kTile;
   double* val = buf + 3 * n * kTile;
   uint16_t* cfg = reinterpret_cast<uint16_t*>(val + kTile);
@@ -251,7 +251,7 @@ ac_forward_kernel(const double* __restrict__ params, int n, int h, int g,
     for (int i = threadIdx.x; i < o.total; i += kThreads) sm[i] = params[i];
     P = sm;
   }
-  double* act = sm + (smem_params ? o.total : 0);
+  double* act = sm + (smem_params ? ((o.total + 1) & ~1) : 0);  // 16-byte aligned (double2 loads)
   double* buf = act + (h > 2 * g ? h : 2 * g) * kTile;
   double* val = buf + 3 * n * kTile;
   const int tid = threadIdx.x;
@@ -462,6 +462,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       KT_CUDA(cudaMemcpyAsync(d_tasks, dt.data(), sizeof(RolloutTask) * num_tasks, cudaMemcpyHostToDevice, ctx->stream));
       KT_CUDA(cudaMemcpyAsync(d_work, work.data(), sizeof(CtaWork) * work.size(), cudaMemcpyHostToDevice, ctx->stream));
       KT_CUDA(cudaFuncSetAttribute(rollout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
       rollout_kernel<<<(unsigned)work.size(), kThreads, smem, ctx->stream>>>(d_tasks, d_work, smem_params ? 1 : 0);
       kt::check_launch(ctx, "rollout");
     }

@@ -97,7 +97,7 @@ class RolloutTask:
 
 
 def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Context] = None,
-                       device_out: bool = False):
+                       device_out: bool = False, host_out: Optional[list] = None):
     """Grouped run_episodes over several workloads in ONE persistent-kernel launch.
 
     Host arrays in/out by default; with CUDA-tensor init_idx and device_out=True
@@ -131,11 +131,14 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
         else:
             init = np.ascontiguousarray(t.init_idx, np.uint16).reshape(-1, D)
             E = len(init)
-            o = dict(idx=np.zeros((E, T + 1, D), np.uint16),
-                     score=np.zeros((E, T + 1)) if t.cost_model is not None else None,
-                     actions=np.zeros((E, T, D), np.int8) if t.want_trajectory else None,
-                     logp=np.zeros((E, T)) if t.want_trajectory else None,
-                     value=np.zeros((E, T)) if t.want_trajectory else None)
+            if host_out is not None:  # caller-provided (e.g. pinned) host buffers
+                o = host_out[i]
+            else:
+                o = dict(idx=np.zeros((E, T + 1, D), np.uint16),
+                         score=np.zeros((E, T + 1)) if t.cost_model is not None else None,
+                         actions=np.zeros((E, T, D), np.int8) if t.want_trajectory else None,
+                         logp=np.zeros((E, T)) if t.want_trajectory else None,
+                         value=np.zeros((E, T)) if t.want_trajectory else None)
             pp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
             init_p = init.ctypes.data_as(C.c_void_p)
             keep.append(init)
