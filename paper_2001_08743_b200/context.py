@@ -52,9 +52,13 @@ class Context:
         L.check(rc, self.h)
 
     def set_stream(self, stream) -> None:
-        """Bind to an external cudaStream_t (int handle or torch.cuda.Stream); None = own stream."""
-        handle = None if stream is None else int(getattr(stream, "cuda_stream", stream))
-        self.check(L.lib().ktune_ctx_set_stream(self.h, C.c_void_p(handle) if handle else None))
+        """Bind to an external cudaStream_t (int handle or torch.cuda.Stream); None = own stream.
+        Handle 0 (torch's default stream) maps to cudaStreamLegacy."""
+        if stream is None:
+            self.check(L.lib().ktune_ctx_set_stream(self.h, None))
+            return
+        handle = int(getattr(stream, "cuda_stream", stream))
+        self.check(L.lib().ktune_ctx_set_stream(self.h, C.c_void_p(handle if handle else 0x1)))
 
     def synchronize(self) -> None:
         self.check(L.lib().ktune_ctx_synchronize(self.h))

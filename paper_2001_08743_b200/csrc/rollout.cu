@@ -22,8 +22,10 @@
 
 namespace {
 
-constexpr int kTile = 32;      // episodes per CTA
-constexpr int kThreads = 128;  // threads per CTA
+constexpr int kTile = 32;      // episodes per CTA (one per lane)
+constexpr int kThreads = 512;  // 16 warps per CTA; every phase maps lane <-> episode
+constexpr int kWarps = kThreads / 32;
+constexpr int kUnits = 8;      // hidden units per thread per pass (independent fp64 chains)
 
 struct AcOff {
   int w0, b0, wp1, bp1, wp2, bp2, wv1, bv1, wv2, bv2, total;
@@ -65,78 +67,84 @@ struct CtaWork {
   int64_t first;  // first episode (task-local) of this CTA's tile
 };
 
-// Shared-memory carve-up (in doubles): params | act [max(h,2g)][32] | buf [3n][32] | val[32]
-// then uint16 cfg [32][n].
+// Shared-memory carve-up (doubles): params (even-padded) | act [max(h,2g)][32] |
+// buf [3n][32] | val [32] | then uint16 cfg [n][32] | int32 card [n].
 __host__ __device__ inline size_t rollout_smem_bytes(int n, int h, int g, bool smem_params) {
   const AcOff o = ac_layout(n, h, g);
   const int act = (h > 2 * g ? h : 2 * g) * kTile;
   size_t d = (smem_params ? (size_t)((o.total + 1) & ~1) : 0) + act + (size_t)3 * n * kTile + kTile;
-  return d * 8 + (size_t)kTile * n * 2 + 16;
+  return d * 8 + (size_t)kTile * n * 2 + (size_t)n * 4 + 16;
 }
 
-// One forward pass over the 32 states held in buf[i][c] (phase A..C).
-// Leaves logits in buf[a][c] and values in val[c]; act holds hp/hv.
+// One exact fp64 forward pass over the 32 states held in buf[i][c] (lane = c).
+// Leaves logits in buf[a][c], values in val[c]; act ends up holding hp/hv.
+// Weight reads are warp-uniform (broadcast), activation reads lane-contiguous.
 __device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n, int h, int g,
                              double* act, double* buf, double* val) {
-  const int tid = threadIdx.x;
-  // ---- A: h0 = tanh(W0 x + b0), W0 column-major (h x n)
-  for (int j = tid; j < h; j += kThreads) {
-    double w[kt::kMaxKnobs];
+  const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // ---- A: h0[j][c] = tanh(sum_i W0(j,i) x[i][c] + b0[j]);  W0 column-major (h x n)
+  for (int ub = w * kUnits; ub < h; ub += kWarps * kUnits) {
+    double acc[kUnits];
 #pragma unroll
-    for (int i = 0; i < kt::kMaxKnobs; ++i) w[i] = i < n ? P[o.w0 + i * h + j] : 0.0;
-    const double b = P[o.b0 + j];
-    for (int c = 0; c < kTile; ++c) {
-      double acc = 0.0;
+    for (int r = 0; r < kUnits; ++r) acc[r] = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double x = buf[i * kTile + c];
+      const double* wr = P + o.w0 + i * h + ub;
 #pragma unroll
-      for (int i = 0; i < kt::kMaxKnobs; ++i)
-        if (i < n) acc = kt::dadd(acc, kt::dmul(w[i], buf[i * kTile + c]));
-      act[j * kTile + c] = kt::kt_tanh(kt::dadd(acc, b));
+      for (int r = 0; r < kUnits; ++r) acc[r] = kt::dadd(acc[r], kt::dmul(wr[r], x));
     }
+#pragma unroll
+    for (int r = 0; r < kUnits; ++r) act[(ub + r) * kTile + c] = kt::kt_tanh(kt::dadd(acc[r], P[o.b0 + ub + r]));
   }
   __syncthreads();
-  // ---- B: hp = tanh(Wp1 h0 + bp1) (u < g), hv = tanh(Wv1 h0 + bv1) (u >= g)
-  double res[kTile];
-  const int u = tid;
-  const bool active = u < 2 * g;
-  if (active) {
-    const int wbase = u < g ? o.wp1 + u : o.wv1 + (u - g);
-    const double b = u < g ? P[o.bp1 + u] : P[o.bv1 + (u - g)];
+  // ---- B: units u < g: hp = tanh(Wp1 h0 + bp1); g <= u < 2g: hv = tanh(Wv1 h0 + bv1)
+  double res[2][kUnits];
 #pragma unroll
-    for (int cb = 0; cb < kTile; cb += 8) {
-      double acc[8];
+  for (int pass = 0; pass < 2; ++pass) {
+    const int ub = w * kUnits + pass * kWarps * kUnits;
+    if (ub >= 2 * g) break;
+    const double* wb = ub < g ? P + o.wp1 + ub : P + o.wv1 + (ub - g);
+    const double* bb = ub < g ? P + o.bp1 + ub : P + o.bv1 + (ub - g);
+    double acc[kUnits];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) acc[r] = 0.0;
-      for (int i = 0; i < h; ++i) {
-        const double w = P[wbase + i * g];
-        const double2* hrow = reinterpret_cast<const double2*>(act + i * kTile + cb);
+    for (int r = 0; r < kUnits; ++r) acc[r] = 0.0;
+    for (int i = 0; i < h; ++i) {
+      const double x = act[i * kTile + c];
+      const double* wr = wb + i * g;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const double2 v = hrow[r];
-          acc[2 * r] = kt::dadd(acc[2 * r], kt::dmul(w, v.x));
-          acc[2 * r + 1] = kt::dadd(acc[2 * r + 1], kt::dmul(w, v.y));
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 8; ++r) res[cb + r] = kt::kt_tanh(kt::dadd(acc[r], b));
+      for (int r = 0; r < kUnits; ++r) acc[r] = kt::dadd(acc[r], kt::dmul(wr[r], x));
     }
-  }
-  __syncthreads();
-  if (active) {
 #pragma unroll
-    for (int c = 0; c < kTile; ++c) act[u * kTile + c] = res[c];
+    for (int r = 0; r < kUnits; ++r) res[pass][r] = kt::kt_tanh(kt::dadd(acc[r], bb[r]));
   }
   __syncthreads();
-  // ---- C: logits[a][c] = Wp2 hp + bp2 (Wp2 column-major 3n x g); value = wv2 . hv + bv2
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    const int ub = w * kUnits + pass * kWarps * kUnits;
+    if (ub >= 2 * g) break;
+#pragma unroll
+    for (int r = 0; r < kUnits; ++r) act[(ub + r) * kTile + c] = res[pass][r];
+  }
+  __syncthreads();
+  // ---- C: logits (Wp2 column-major 3n x g) and value; up to 4 items per warp interleaved
   const int na = 3 * n + 1;
-  for (int item = tid; item < na * kTile; item += kThreads) {
-    const int c = item / na, a = item % na;
-    double acc = 0.0;
-    if (a < 3 * n) {
-      for (int j = 0; j < g; ++j) acc = kt::dadd(acc, kt::dmul(P[o.wp2 + j * 3 * n + a], act[j * kTile + c]));
-      buf[a * kTile + c] = kt::dadd(acc, P[o.bp2 + a]);
-    } else {
-      for (int j = 0; j < g; ++j) acc = kt::dadd(acc, kt::dmul(P[o.wv2 + j], act[(g + j) * kTile + c]));
-      val[c] = kt::dadd(acc, P[o.bv2]);
+  for (int a0 = w; a0 < na; a0 += 4 * kWarps) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = 0; j < g; ++j) {
+      const double hpj = act[j * kTile + c];
+      const double hvj = act[(g + j) * kTile + c];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int a = a0 + q * kWarps;
+        if (a < 3 * n) acc[q] = kt::dadd(acc[q], kt::dmul(P[o.wp2 + j * 3 * n + a], hpj));
+        else if (a == 3 * n) acc[q] = kt::dadd(acc[q], kt::dmul(P[o.wv2 + j], hvj));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int a = a0 + q * kWarps;
+      if (a < 3 * n) buf[a * kTile + c] = kt::dadd(acc[q], P[o.bp2 + a]);
+      else if (a == 3 * n) val[c] = kt::dadd(acc[q], P[o.bv2]);
     }
   }
   __syncthreads();
@@ -169,71 +177,71 @@ rollout_kernel(const RolloutTask* __restrict__ tasks, const CtaWork* __restrict_
                int smem_params) {
   extern __shared__ __align__(16) double sm[];
   const CtaWork wk = work[blockIdx.x];
-  const RolloutTask& tk = tasks[wk.task];
-  const int n = tk.n, h = tk.h, g = tk.g, T = tk.T;
+  const RolloutTask* tkp = tasks + wk.task;
+  const int n = tkp->n, h = tkp->h, g = tkp->g, T = tkp->T;
+  const int64_t E = tkp->E, eoff = tkp->episode_offset;
+  const uint64_t seed = tkp->seed;
+  uint16_t* __restrict__ out_idx = tkp->idx;
+  int8_t* __restrict__ out_act = tkp->actions;
+  double* __restrict__ out_logp = tkp->logp;
+  double* __restrict__ out_val = tkp->value;
   const AcOff o = ac_layout(n, h, g);
-  const double* P = tk.params;
-  double* p_s = sm;
+  const double* P = tkp->params;
   if (smem_params) {
-    for (int i = threadIdx.x; i < o.total; i += kThreads) p_s[i] = P[i];
-    P = p_s;
+    for (int i = threadIdx.x; i < o.total; i += kThreads) sm[i] = P[i];
+    P = sm;
   }
-  double* act = sm + (smem_params ? ((o.total + 1) & ~1) : 0);  // 16-byte aligned (double2 loads)
+  double* act = sm + (smem_params ? ((o.total + 1) & ~1) : 0);
   double* buf = act + (h > 2 * g ? h : 2 * g) * kTile;
   double* val = buf + 3 * n * kTile;
-  uint16_t* cfg = reinterpret_cast<uint16_t*>(val + kTile);
-  const int tid = threadIdx.x;
-  const int64_t E = tk.E;
-  // load initial configurations, write trajectory row 0
-  for (int item = tid; item < kTile * n; item += kThreads) {
-    const int c = item / n, d = item % n;
-    const int64_t e = wk.first + c;
+  uint16_t* cfg = reinterpret_cast<uint16_t*>(val + kTile);  // [d][c]
+  int* card = reinterpret_cast<int*>(cfg + n * kTile);
+  const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e = wk.first + c;
+  const bool live = e < E;
+  if (threadIdx.x < n) card[threadIdx.x] = tkp->sp.card[threadIdx.x];
+  // initial configurations (trajectory row 0)
+  for (int d = w; d < n; d += kWarps) {
     uint16_t v = 0;
-    if (e < E) {
-      v = tk.init_idx[e * n + d];
-      tk.idx[(e * (T + 1)) * n + d] = v;
+    if (live) {
+      v = tkp->init_idx[e * n + d];
+      out_idx[(e * (T + 1)) * n + d] = v;
     }
-    cfg[c * n + d] = v;
+    cfg[d * kTile + c] = v;
   }
   __syncthreads();
   for (int t = 0; t < T; ++t) {
     // ---- 0: features x = idx / (card - 1) (design_space.cpp:195-197)
-    for (int item = tid; item < kTile * n; item += kThreads) {
-      const int c = item / n, d = item % n;
-      const int card = tk.sp.card[d];
-      buf[d * kTile + c] = card > 1 ? kt::ddiv((double)cfg[c * n + d], (double)(card - 1)) : 0.0;
+    for (int d = w; d < n; d += kWarps) {
+      const int cd = card[d];
+      buf[d * kTile + c] = cd > 1 ? kt::ddiv((double)cfg[d * kTile + c], (double)(cd - 1)) : 0.0;
     }
     __syncthreads();
     forward_tile(P, o, n, h, g, act, buf, val);
-    // ---- D: sample per knob, saturating update
-    for (int item = tid; item < kTile * n; item += kThreads) {
-      const int c = item / n, d = item % n;
-      const int64_t e = wk.first + c;
+    // ---- D: per knob: log-softmax, counter-RNG draw, inverse CDF, saturating move
+    for (int d = w; d < n; d += kWarps) {
       const Knob3 k3 = softmax3(buf[(3 * d) * kTile + c], buf[(3 * d + 1) * kTile + c],
                                 buf[(3 * d + 2) * kTile + c]);
-      const uint64_t ge = (uint64_t)(tk.episode_offset + e);
-      const double u = kt::hash01(tk.seed, (ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n + (uint64_t)d);
+      const uint64_t ge = (uint64_t)(eoff + e);
+      const double u = kt::hash01(seed, (ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n + (uint64_t)d);
       const int a = u < k3.p[0] ? 0 : (u < kt::dadd(k3.p[0], k3.p[1]) ? 1 : 2);
-      int v = (int)cfg[c * n + d] + (a - 1);
-      const int card = tk.sp.card[d];
-      v = v < 0 ? 0 : (v > card - 1 ? card - 1 : v);
-      cfg[c * n + d] = (uint16_t)v;
-      buf[(3 * d) * kTile + c] = k3.lp[a];
-      if (e < E) {
-        if (tk.actions) tk.actions[(e * T + t) * n + d] = (int8_t)(a - 1);
-        tk.idx[(e * (T + 1) + t + 1) * n + d] = (uint16_t)v;
+      int v = (int)cfg[d * kTile + c] + (a - 1);
+      const int cd = card[d];
+      v = v < 0 ? 0 : (v > cd - 1 ? cd - 1 : v);
+      cfg[d * kTile + c] = (uint16_t)v;
+      buf[(3 * d) * kTile + c] = a == 0 ? k3.lp[0] : (a == 1 ? k3.lp[1] : k3.lp[2]);
+      if (live) {
+        if (out_act) out_act[(e * T + t) * n + d] = (int8_t)(a - 1);
+        out_idx[(e * (T + 1) + t + 1) * n + d] = (uint16_t)v;
       }
     }
     __syncthreads();
     // ---- E: joint log-probability in knob order, value
-    if (tid < kTile) {
-      const int64_t e = wk.first + tid;
-      if (e < E) {
-        double lp = 0.0;
-        for (int d = 0; d < n; ++d) lp = kt::dadd(lp, buf[(3 * d) * kTile + tid]);
-        if (tk.logp) tk.logp[e * T + t] = lp;
-        if (tk.value) tk.value[e * T + t] = val[tid];
-      }
+    if (w == 0 && live) {
+      double lp = 0.0;
+      for (int d = 0; d < n; ++d) lp = kt::dadd(lp, buf[(3 * d) * kTile + c]);
+      if (out_logp) out_logp[e * T + t] = lp;
+      if (out_val) out_val[e * T + t] = val[c];
     }
     __syncthreads();
   }
@@ -264,7 +272,7 @@ ac_forward_kernel(const double* __restrict__ params, int n, int h, int g,
     __syncthreads();
     forward_tile(P, o, n, h, g, act, buf, val);
     for (int item = tid; item < kTile * n; item += kThreads) {
-      const int c = item / n, d = item % n;
+      const int c = item % kTile, d = item / kTile;
       const int64_t b = first + c;
       if (b >= B) continue;
       const Knob3 k3 = softmax3(buf[(3 * d) * kTile + c], buf[(3 * d + 1) * kTile + c],
@@ -288,8 +296,9 @@ bool fits_smem(int n, int h, int g) { return rollout_smem_bytes(n, h, g, true) <
 
 void check_dims(int n, int h, int g) {
   if (n < 1 || n > kt::kMaxKnobs) kt::fail(KTUNE_ERR_CONFIG, "actor-critic: 1 <= num_knobs <= 32 on the device path");
-  if (h < 1 || g < 1 || 2 * g > kThreads || h > 1024)
-    kt::fail(KTUNE_ERR_CONFIG, "actor-critic: device path needs head_hidden <= 64 and hidden_dim <= 1024");
+  if (h < 8 || g < 8 || h % 8 || g % 8 || 2 * g > 2 * kWarps * kUnits || h > 1024)
+    kt::fail(KTUNE_ERR_CONFIG, "actor-critic: device path needs hidden_dim, head_hidden multiples of 8, "
+                               "head_hidden <= 128, hidden_dim <= 1024");
 }
 
 }  // namespace
