@@ -171,6 +171,51 @@ __device__ inline double kt_tanh(double x) {
   return dadd(x, z);
 }
 
+// Branch-free evaluation of kt_tanh for SIMT lanes with mixed |x| (same
+// operations as kt_tanh on every input, so bit-identical): both the rational
+// branch and the exp branch are evaluated and selected. For |x| >= 0.625 the
+// exp argument 2|x| lies in [1.25, 709.78], where kt_exp always takes the
+// reduction path with 2 <= k <= 1024, so that path is inlined without its
+// range checks.
+__device__ __forceinline__ double kt_tanh_bf(double x) {
+  const double ln2HI = 6.93147180369123816490e-01;
+  const double ln2LO = 1.90821492927058770002e-10;
+  const double invln2 = 1.44269504088896338700e+00;
+  const double P1 = 1.66666666666666019037e-01;
+  const double P2 = -2.77777777770155933842e-03;
+  const double P3 = 6.61375632143793436117e-05;
+  const double P4 = -1.65339022054652515390e-06;
+  const double P5 = 4.13813679705723846039e-08;
+  const double Q0 = 1.12811678491632931402E2, Q1 = 2.23548839060100448583E3,
+               Q2 = 4.84406305325125486048E3;
+  const double T0 = -9.64399179425052238628E-1, T1 = -9.92877231001918586564E1,
+               T2 = -1.61468768441708447952E3;
+  const double z = fabs(x);
+  // exp branch on ze = clamp(z, 0.625, 354.89...) (identity where it is selected)
+  const double ze = fmin(fmax(z, 0.625), 354.891356446691998);
+  const double xx = dadd(ze, ze);
+  const int k = (int)dadd(dmul(invln2, xx), 0.5);
+  const double t = (double)k;
+  const double hi = dsub(xx, dmul(t, ln2HI));
+  const double lo = dmul(t, ln2LO);
+  const double r = dsub(hi, lo);
+  const double tt = dmul(r, r);
+  const double poly = dadd(P1, dmul(tt, dadd(P2, dmul(tt, dadd(P3, dmul(tt, dadd(P4, dmul(tt, P5))))))));
+  const double c = dsub(r, dmul(tt, poly));
+  const double y = dsub(1.0, dsub(dsub(lo, ddiv(dmul(r, c), dsub(2.0, c))), hi));
+  const double s = bitsd(dbits(y) + ((uint64_t)(int64_t)k << 52));
+  double ze_t = dsub(1.0, ddiv(2.0, dadd(s, 1.0)));
+  ze_t = x < 0.0 ? -ze_t : ze_t;
+  // rational branch
+  const double s2 = dmul(x, x);
+  const double p = dadd(dmul(dadd(dmul(T0, s2), T1), s2), T2);
+  const double q = dadd(dmul(dadd(dmul(dadd(s2, Q0), s2), Q1), s2), Q2);
+  const double zp = dadd(x, dmul(dmul(x, s2), ddiv(p, q)));
+  double res = z >= 0.625 ? ze_t : zp;
+  res = z > 354.891356446691998 ? (x > 0.0 ? 1.0 : -1.0) : res;
+  return x == 0.0 ? x : res;
+}
+
 // ---------------------------------------------------------------- validity.cpp:162-204
 template <class IdxAt>
 __device__ inline bool rule_eval(const KtSpaceParams& sp, IdxAt idx_at) {

@@ -78,7 +78,19 @@ __host__ __device__ inline size_t rollout_smem_bytes(int n, int h, int g, bool s
 
 // One exact fp64 forward pass over the 32 states held in buf[i][c] (lane = c).
 // Leaves logits in buf[a][c], values in val[c]; act ends up holding hp/hv.
-// Weight reads are warp-uniform (broadcast), activation reads lane-contiguous.
+// Weight reads are warp-uniform (broadcast, 16-byte), activation reads
+// lane-contiguous (conflict-free). P is shared memory when the parameter block
+// fits, else global (read-only path).
+__device__ __forceinline__ void load8(const double* p, double (&w)[kUnits]) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int r = 0; r < kUnits / 2; ++r) {
+    const double2 v = q[r];
+    w[2 * r] = v.x;
+    w[2 * r + 1] = v.y;
+  }
+}
+
 __device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n, int h, int g,
                              double* act, double* buf, double* val) {
   const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -89,12 +101,15 @@ __device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n
     for (int r = 0; r < kUnits; ++r) acc[r] = 0.0;
     for (int i = 0; i < n; ++i) {
       const double x = buf[i * kTile + c];
-      const double* wr = P + o.w0 + i * h + ub;
+      double wr[kUnits];
+      load8(P + o.w0 + i * h + ub, wr);
 #pragma unroll
       for (int r = 0; r < kUnits; ++r) acc[r] = kt::dadd(acc[r], kt::dmul(wr[r], x));
     }
+    double b[kUnits];
+    load8(P + o.b0 + ub, b);
 #pragma unroll
-    for (int r = 0; r < kUnits; ++r) act[(ub + r) * kTile + c] = kt::kt_tanh(kt::dadd(acc[r], P[o.b0 + ub + r]));
+    for (int r = 0; r < kUnits; ++r) act[(ub + r) * kTile + c] = kt::kt_tanh_bf(kt::dadd(acc[r], b[r]));
   }
   __syncthreads();
   // ---- B: units u < g: hp = tanh(Wp1 h0 + bp1); g <= u < 2g: hv = tanh(Wv1 h0 + bv1)
@@ -104,18 +119,21 @@ __device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n
     const int ub = w * kUnits + pass * kWarps * kUnits;
     if (ub >= 2 * g) break;
     const double* wb = ub < g ? P + o.wp1 + ub : P + o.wv1 + (ub - g);
-    const double* bb = ub < g ? P + o.bp1 + ub : P + o.bv1 + (ub - g);
     double acc[kUnits];
 #pragma unroll
     for (int r = 0; r < kUnits; ++r) acc[r] = 0.0;
+#pragma unroll 2
     for (int i = 0; i < h; ++i) {
       const double x = act[i * kTile + c];
-      const double* wr = wb + i * g;
+      double wr[kUnits];
+      load8(wb + i * g, wr);
 #pragma unroll
       for (int r = 0; r < kUnits; ++r) acc[r] = kt::dadd(acc[r], kt::dmul(wr[r], x));
     }
+    double b[kUnits];
+    load8(ub < g ? P + o.bp1 + ub : P + o.bv1 + (ub - g), b);
 #pragma unroll
-    for (int r = 0; r < kUnits; ++r) res[pass][r] = kt::kt_tanh(kt::dadd(acc[r], bb[r]));
+    for (int r = 0; r < kUnits; ++r) res[pass][r] = kt::kt_tanh_bf(kt::dadd(acc[r], b[r]));
   }
   __syncthreads();
 #pragma unroll
@@ -126,19 +144,26 @@ __device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n
     for (int r = 0; r < kUnits; ++r) act[(ub + r) * kTile + c] = res[pass][r];
   }
   __syncthreads();
-  // ---- C: logits (Wp2 column-major 3n x g) and value; up to 4 items per warp interleaved
+  // ---- C: logits (Wp2 column-major 3n x g) and value, 4 interleaved items per
+  // warp. Item a < 3n reads Wp2 row a against hp; a == 3n reads wv2 against hv;
+  // items beyond 3n are computed on row 0 and discarded (no branch in the loop).
   const int na = 3 * n + 1;
   for (int a0 = w; a0 < na; a0 += 4 * kWarps) {
+    const double* wp[4];
+    int ws[4];
+    const double* hrow[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int a = a0 + q * kWarps;
+      const bool is_val = a == 3 * n;
+      wp[q] = is_val ? P + o.wv2 : P + o.wp2 + (a < 3 * n ? a : 0);
+      ws[q] = is_val ? 1 : 3 * n;
+      hrow[q] = act + (is_val ? g : 0) * kTile + c;
+    }
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = 0; j < g; ++j) {
-      const double hpj = act[j * kTile + c];
-      const double hvj = act[(g + j) * kTile + c];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int a = a0 + q * kWarps;
-        if (a < 3 * n) acc[q] = kt::dadd(acc[q], kt::dmul(P[o.wp2 + j * 3 * n + a], hpj));
-        else if (a == 3 * n) acc[q] = kt::dadd(acc[q], kt::dmul(P[o.wv2 + j], hvj));
-      }
+      for (int q = 0; q < 4; ++q) acc[q] = kt::dadd(acc[q], kt::dmul(wp[q][j * ws[q]], hrow[q][j * kTile]));
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -172,9 +197,10 @@ __device__ __forceinline__ Knob3 softmax3(double l0, double l1, double l2) {
   return r;
 }
 
+template <bool SP>
 __global__ void __launch_bounds__(kThreads, 1)
-rollout_kernel(const RolloutTask* __restrict__ tasks, const CtaWork* __restrict__ work,
-               int smem_params) {
+rollout_kernel(const RolloutTask* __restrict__ tasks, const CtaWork* __restrict__ work) {
+  constexpr bool smem_params = SP;
   extern __shared__ __align__(16) double sm[];
   const CtaWork wk = work[blockIdx.x];
   const RolloutTask* tkp = tasks + wk.task;
@@ -187,7 +213,7 @@ rollout_kernel(const RolloutTask* __restrict__ tasks, const CtaWork* __restrict_
   double* __restrict__ out_val = tkp->value;
   const AcOff o = ac_layout(n, h, g);
   const double* P = tkp->params;
-  if (smem_params) {
+  if (SP) {
     for (int i = threadIdx.x; i < o.total; i += kThreads) sm[i] = P[i];
     P = sm;
   }
@@ -470,9 +496,10 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       CtaWork* d_work = (CtaWork*)alloc(sizeof(CtaWork) * work.size());
       KT_CUDA(cudaMemcpyAsync(d_tasks, dt.data(), sizeof(RolloutTask) * num_tasks, cudaMemcpyHostToDevice, ctx->stream));
       KT_CUDA(cudaMemcpyAsync(d_work, work.data(), sizeof(CtaWork) * work.size(), cudaMemcpyHostToDevice, ctx->stream));
-      KT_CUDA(cudaFuncSetAttribute(rollout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      auto kern = smem_params ? rollout_kernel<true> : rollout_kernel<false>;
+      KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
-      rollout_kernel<<<(unsigned)work.size(), kThreads, smem, ctx->stream>>>(d_tasks, d_work, smem_params ? 1 : 0);
+      kern<<<(unsigned)work.size(), kThreads, smem, ctx->stream>>>(d_tasks, d_work);
       kt::check_launch(ctx, "rollout");
     }
     // cost-model scores of every visited configuration (K1 over the trajectory)
