@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "device.cuh"
+#include "exactsum.cuh"
 #include "internal.cuh"
 
 namespace {
@@ -381,9 +382,11 @@ __global__ void __launch_bounds__(kBT) hist_kernel(const int32_t* __restrict__ a
   for (int c = threadIdx.x; c < k; c += blockDim.x) blockcounts[(int64_t)blockIdx.x * k + c] = cnt[c];
 }
 
-// Exclusive scan over blocks per cluster; cluster totals and starts.
+// Exclusive scan over blocks per cluster; cluster totals, starts and the
+// per-cluster segment bases of the exact-sum machinery (csb[k+1]).
 __global__ void scan_counts_kernel(int32_t* __restrict__ blockcounts, int64_t nblocks, int k,
-                                   int32_t* __restrict__ counts, int32_t* __restrict__ cstart) {
+                                   int32_t* __restrict__ counts, int32_t* __restrict__ cstart,
+                                   int32_t* __restrict__ csb) {
   const int c = threadIdx.x;
   __shared__ int tot[kt::kMaxK];
   if (c < k) {
@@ -398,19 +401,27 @@ __global__ void scan_counts_kernel(int32_t* __restrict__ blockcounts, int64_t nb
   }
   __syncthreads();
   if (c == 0) {
-    int s = 0;
+    int s = 0, sb = 0;
     for (int j = 0; j < k; ++j) {
       cstart[j] = s;
+      csb[j] = sb;
       s += tot[j];
+      sb += (tot[j] + kt::xsum::kSeg - 1) / kt::xsum::kSeg;
     }
+    csb[k] = sb;
   }
 }
 
 // Stable scatter: warp w of the block owns points [base + w*128, base + (w+1)*128).
+// Writes member ids and the members' knob-index rows in cluster-major,
+// ascending-point order (the reference's summation order, sampling.cpp:112-116).
+template <class IdxT>
 __global__ void __launch_bounds__(kBT) scatter_kernel(const int32_t* __restrict__ asg, int64_t N, int k,
+                                                      int D, const IdxT* __restrict__ pts,
                                                       const int32_t* __restrict__ blockoffs,
                                                       const int32_t* __restrict__ cstart,
-                                                      int32_t* __restrict__ members) {
+                                                      int32_t* __restrict__ members,
+                                                      IdxT* __restrict__ sorted) {
   constexpr int kWarps = kBT / 32;
   constexpr int kPerWarp = kChunk / kWarps;  // 128 points = 4 rounds of 32
   __shared__ int wcnt[kWarps][kt::kMaxK];
@@ -418,13 +429,11 @@ __global__ void __launch_bounds__(kBT) scatter_kernel(const int32_t* __restrict_
   for (int c = lane; c < k; c += 32) wcnt[w][c] = 0;
   __syncwarp();
   const int64_t wbase = (int64_t)blockIdx.x * kChunk + w * kPerWarp;
-  // pass 1: per-warp histogram
   for (int r = 0; r < kPerWarp / 32; ++r) {
     const int64_t i = wbase + r * 32 + lane;
     if (i < N) atomicAdd(&wcnt[w][asg[i]], 1);
   }
   __syncthreads();
-  // exclusive prefix over warps per cluster
   if (threadIdx.x < k) {
     const int c = threadIdx.x;
     int run = 0;
@@ -435,7 +444,6 @@ __global__ void __launch_bounds__(kBT) scatter_kernel(const int32_t* __restrict_
     }
   }
   __syncthreads();
-  // pass 2: ranks in point order
   for (int r = 0; r < kPerWarp / 32; ++r) {
     const int64_t i = wbase + r * 32 + lane;
     const bool ok = i < N;
@@ -443,8 +451,9 @@ __global__ void __launch_bounds__(kBT) scatter_kernel(const int32_t* __restrict_
     const unsigned m = __match_any_sync(0xffffffff, c);
     const int before = __popc(m & ((1u << lane) - 1));
     if (ok) {
-      const int pos = cstart[c] + blockoffs[(int64_t)blockIdx.x * k + c] + wcnt[w][c] + before;
+      const int64_t pos = cstart[c] + blockoffs[(int64_t)blockIdx.x * k + c] + wcnt[w][c] + before;
       members[pos] = (int32_t)i;
+      for (int d = 0; d < D; ++d) sorted[pos * D + d] = pts[i * D + d];
     }
     __syncwarp();
     if (ok && before == 0) wcnt[w][c] += __popc(m);
@@ -452,30 +461,150 @@ __global__ void __launch_bounds__(kBT) scatter_kernel(const int32_t* __restrict_
   }
 }
 
+// ---- exact centroid sums over the sorted rows (exactsum.cuh) ----------------
+// thread (cluster-segment g, knob d); g indexes segments of all clusters (csb).
+__device__ __forceinline__ int cluster_of_segment(const int32_t* csb, int k, int g) {
+  int c = 0;
+  while (c + 1 < k && csb[c + 1] <= g) ++c;
+  return c;
+}
+
 template <class IdxT>
-__global__ void chain_kernel(KtSpaceParams sp, const IdxT* __restrict__ pts,
-                             const int32_t* __restrict__ members,
-                             const int32_t* __restrict__ counts, const int32_t* __restrict__ cstart,
-                             int k, double* __restrict__ cent) {
+__global__ void xs_partial_kernel(KtSpaceParams sp, const IdxT* __restrict__ sorted,
+                                  const int32_t* __restrict__ counts, const int32_t* __restrict__ cstart,
+                                  const int32_t* __restrict__ csb, int k, int max_segs,
+                                  double* __restrict__ approx) {
   const int D = sp.D;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= k * D) return;
-  const int c = tid / D, d = tid % D;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = (int)(t / D), d = (int)(t % D);
+  if (g >= max_segs || g >= csb[k]) return;
+  const int c = cluster_of_segment(csb, k, g);
+  const int j = g - csb[c];
   const int n = counts[c];
-  if (n == 0) return;  // empty cluster: handled by reseed
-  const int32_t* mem = members + cstart[c];
+  const int lo = j * kt::xsum::kSeg, hi = min(n, lo + kt::xsum::kSeg);
   const double* lut = sp.lut + sp.lut_off[d];
-  double s = 0.0;  // MatrixXd::Zero then += (sampling.cpp:110,114)
-  int j = 0;
-  for (; j + 8 <= n; j += 8) {
-    double v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = __ldg(lut + (int)pts[(int64_t)mem[j + q] * D + d]);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) s = kt::dadd(s, v[q]);
+  const IdxT* rows = sorted + (int64_t)cstart[c] * D + d;
+  double s = 0.0;
+  for (int i = lo; i < hi; ++i) s = kt::dadd(s, __ldg(lut + (int)rows[(int64_t)i * D]));
+  approx[(int64_t)g * D + d] = s;
+}
+
+// thread (cluster c, knob d): exclusive prefix of the approximate segment sums.
+__global__ void xs_prefix_kernel(int D, const int32_t* __restrict__ csb, int k, double* __restrict__ approx) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k * D) return;
+  const int c = t / D, d = t % D;
+  double run = 0.0;
+  for (int g = csb[c]; g < csb[c + 1]; ++g) {
+    const double v = approx[(int64_t)g * D + d];
+    approx[(int64_t)g * D + d] = run;
+    run = kt::dadd(run, v);
   }
-  for (; j < n; ++j) s = kt::dadd(s, __ldg(lut + (int)pts[(int64_t)mem[j] * D + d]));
+}
+
+template <class IdxT>
+__global__ void xs_map_kernel(KtSpaceParams sp, const IdxT* __restrict__ sorted,
+                              const int32_t* __restrict__ counts, const int32_t* __restrict__ cstart,
+                              const int32_t* __restrict__ csb, int k, int max_segs,
+                              const double* __restrict__ prefix, kt::xsum::SegMap* __restrict__ maps) {
+  const int D = sp.D;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = (int)(t / D), d = (int)(t % D);
+  if (g >= max_segs || g >= csb[k]) return;
+  const int c = cluster_of_segment(csb, k, g);
+  const int j = g - csb[c];
+  const int n = counts[c];
+  const int lo = j * kt::xsum::kSeg, hi = min(n, lo + kt::xsum::kSeg);
+  const double pre = prefix[(int64_t)g * D + d];
+  kt::xsum::SegMap m{0, 0, 0, 0};
+  if (pre > 0.0) {
+    const double* lut = sp.lut + sp.lut_off[d];
+    const IdxT* rows = sorted + (int64_t)cstart[c] * D + d;
+    m = kt::xsum::segment_map([&](int i) { return __ldg(lut + (int)rows[(int64_t)(lo + i) * D]); }, hi - lo,
+                              kt::xsum::binade_of(pre));
+  }
+  maps[(int64_t)g * D + d] = m;
+}
+
+// thread (cluster c, knob d): compose the segment maps from s = 0 exactly;
+// centroid = s / count (sampling.cpp:110-121).
+template <class IdxT>
+__global__ void xs_compose_kernel(KtSpaceParams sp, const IdxT* __restrict__ sorted,
+                                  const int32_t* __restrict__ counts, const int32_t* __restrict__ cstart,
+                                  const int32_t* __restrict__ csb, int k,
+                                  const kt::xsum::SegMap* __restrict__ maps, double* __restrict__ cent,
+                                  int32_t* __restrict__ seq_segments) {
+  const int D = sp.D;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k * D) return;
+  const int c = t / D, d = t % D;
+  const int n = counts[c];
+  if (n == 0) return;  // empty cluster: reseeded
+  const double* lut = sp.lut + sp.lut_off[d];
+  const IdxT* rows = sorted + (int64_t)cstart[c] * D + d;
+  double s = 0.0;  // MatrixXd::Zero then += in point order
+  int nseq = 0;
+  for (int g = csb[c]; g < csb[c + 1]; ++g) {
+    const kt::xsum::SegMap m = maps[(int64_t)g * D + d];
+    if (kt::xsum::apply_map(s, m)) continue;
+    ++nseq;
+    const int lo = (g - csb[c]) * kt::xsum::kSeg, hi = min(n, lo + kt::xsum::kSeg);
+    int i = lo;
+    for (; i + 8 <= hi; i += 8) {
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldg(lut + (int)rows[(int64_t)(i + q) * D]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s = kt::dadd(s, v[q]);
+    }
+    for (; i < hi; ++i) s = kt::dadd(s, __ldg(lut + (int)rows[(int64_t)i * D]));
+  }
   cent[c * D + d] = kt::ddiv(s, (double)n);
+  if (nseq) atomicAdd(seq_segments, nseq);
+}
+
+// ---- exact loss: the sequential sum of per-point d2 (sampling.cpp:56-63) -----
+__global__ void xs_loss_partial_kernel(const double* __restrict__ x, int64_t N, double* __restrict__ approx) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t lo = g * kt::xsum::kSeg;
+  if (lo >= N) return;
+  const int64_t hi = min(N, lo + kt::xsum::kSeg);
+  double s = 0.0;
+  for (int64_t i = lo; i < hi; ++i) s = kt::dadd(s, x[i]);
+  approx[g] = s;
+}
+
+__global__ void xs_loss_map_kernel(const double* __restrict__ x, int64_t N, const double* __restrict__ prefix,
+                                   kt::xsum::SegMap* __restrict__ maps) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t lo = g * kt::xsum::kSeg;
+  if (lo >= N) return;
+  const int len = (int)(min(N, lo + kt::xsum::kSeg) - lo);
+  kt::xsum::SegMap m{0, 0, 0, 0};
+  if (prefix[g] > 0.0) m = kt::xsum::segment_map([&](int i) { return x[lo + i]; }, len, kt::xsum::binade_of(prefix[g]));
+  maps[g] = m;
+}
+
+__global__ void xs_loss_compose_kernel(const double* __restrict__ x, int64_t N,
+                                       const double* __restrict__ approx, double* __restrict__ prefix,
+                                       const kt::xsum::SegMap* __restrict__ maps, int phase, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int64_t nseg = (N + kt::xsum::kSeg - 1) / kt::xsum::kSeg;
+  if (phase == 0) {  // exclusive prefix of the approximate segment sums
+    double run = 0.0;
+    for (int64_t g = 0; g < nseg; ++g) {
+      prefix[g] = run;
+      run = kt::dadd(run, approx[g]);
+    }
+    return;
+  }
+  double s = 0.0;
+  for (int64_t g = 0; g < nseg; ++g) {
+    if (kt::xsum::apply_map(s, maps[g])) continue;
+    const int64_t lo = g * kt::xsum::kSeg, hi = min(N, lo + kt::xsum::kSeg);
+    for (int64_t i = lo; i < hi; ++i) s = kt::dadd(s, x[i]);
+  }
+  *out = s;
 }
 
 // Empty clusters (sampling.cpp:122-136): in cluster order, the unclaimed
@@ -544,22 +673,6 @@ __global__ void __launch_bounds__(1024) reseed_kernel(KtSpaceParams sp,
     }
     __syncthreads();
   }
-}
-
-// Exact sequential loss chain over the per-point d2 of a run (sampling.cpp:56-63).
-__global__ void loss_chain_kernel(const double* __restrict__ d2, int64_t N, double* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double s = 0.0;
-  int64_t i = 0;
-  for (; i + 8 <= N; i += 8) {
-    double v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = d2[i + q];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) s = kt::dadd(s, v[q]);
-  }
-  for (; i < N; ++i) s = kt::dadd(s, d2[i]);
-  *out = s;
 }
 
 __global__ void sum_chunks_kernel(const double* __restrict__ cs, int64_t n, double* out) {
@@ -765,6 +878,13 @@ struct KMeans {
   double* best_cent;
   int32_t* prev_asg;
   double* prev_d2;
+  // exact-sum machinery
+  IdxT* sorted;       // members' rows, cluster-major, ascending point order
+  double* xs_approx;  // per (segment, knob) approximate sums / prefixes
+  kt::xsum::SegMap* xs_maps;
+  int max_segs;
+  int32_t* csb;       // per-cluster segment bases [k+1]
+  int32_t* seqcnt;    // segments summed sequentially (stat)
 
   void setup(ktune_ctx* c, const ktune_space* s, const IdxT* p, int64_t n) {
     ctx = c;
@@ -785,7 +905,13 @@ struct KMeans {
     d2_b = d2_a + N;
     members = (int32_t*)ctx->dev(kt::WS_MEMBERS, sizeof(int32_t) * N);
     blockcounts = (int32_t*)ctx->dev(kt::WS_SCRATCH, sizeof(int32_t) * nchunks * kt::kMaxK);
-    counts = (int32_t*)ctx->dev(kt::WS_SCRATCH2, sizeof(int32_t) * (2 * kt::kMaxK + 8));
+    counts = (int32_t*)ctx->dev(kt::WS_SCRATCH2, sizeof(int32_t) * (4 * kt::kMaxK + 16));
+    csb = counts + 2 * kt::kMaxK + 8;
+    seqcnt = csb + kt::kMaxK + 4;
+    max_segs = (int)(kt::ceil_div(N, kt::xsum::kSeg) + kt::kMaxK);
+    sorted = (IdxT*)ctx->dev(kt::WS_SORTED, sizeof(IdxT) * N * D);
+    xs_approx = (double*)ctx->dev(kt::WS_XS_APPROX, sizeof(double) * (size_t)max_segs * D);
+    xs_maps = (kt::xsum::SegMap*)ctx->dev(kt::WS_XS_MAPS, sizeof(kt::xsum::SegMap) * (size_t)max_segs * D);
     cent_a = (double*)ctx->dev(kt::WS_CENT, sizeof(double) * kt::kMaxK * D * 3);
     cent_b = cent_a + kt::kMaxK * D;
     best_cent = cent_b + kt::kMaxK * D;
@@ -841,21 +967,33 @@ struct KMeans {
   }
 
   void update_centroids(int k, const int32_t* asg, const double* d2_old, double* next) {
+    int32_t* cstart = counts + kt::kMaxK;
     hist_kernel<<<grid_pts(), kBT, 0, s()>>>(asg, N, k, blockcounts);
-    scan_counts_kernel<<<1, 64, 0, s()>>>(blockcounts, nchunks, k, counts, counts + kt::kMaxK);
-    scatter_kernel<<<grid_pts(), kBT, 0, s()>>>(asg, N, k, blockcounts, counts + kt::kMaxK, members);
-    const int th = 128;
-    chain_kernel<IdxT><<<(int)kt::ceil_div(k * D, th), th, 0, s()>>>(sp->params, pts, members, counts,
-                                                                      counts + kt::kMaxK, k, next);
+    scan_counts_kernel<<<1, 64, 0, s()>>>(blockcounts, nchunks, k, counts, cstart, csb);
+    scatter_kernel<IdxT><<<grid_pts(), kBT, 0, s()>>>(asg, N, k, D, pts, blockcounts, cstart, members, sorted);
+    // exact in-order centroid sums (exactsum.cuh)
+    const int th = 256;
+    const int gseg = (int)kt::ceil_div((int64_t)max_segs * D, th);
+    xs_partial_kernel<IdxT><<<gseg, th, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, max_segs, xs_approx);
+    xs_prefix_kernel<<<(int)kt::ceil_div(k * D, 128), 128, 0, s()>>>(D, csb, k, xs_approx);
+    xs_map_kernel<IdxT><<<gseg, th, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, max_segs, xs_approx, xs_maps);
+    xs_compose_kernel<IdxT><<<(int)kt::ceil_div(k * D, 32), 32, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k,
+                                                                          xs_maps, next, seqcnt);
     KT_CUDA(cudaMemsetAsync(counts + 2 * kt::kMaxK, 0, 4, s()));
     reseed_kernel<IdxT><<<1, 1024, 0, s()>>>(sp->params, pts, N, counts, k, d2_old, next,
                                              counts + 2 * kt::kMaxK);
-    kt::check_launch(ctx, "centroid update", 5);
+    kt::check_launch(ctx, "centroid update", 8);
   }
 
+  // The reference's sequential loss (sampling.cpp:56-63), bit-exact, in parallel.
   double exact_loss(const double* dd) {
-    loss_chain_kernel<<<1, 32, 0, s()>>>(dd, N, dscal + 1);
-    kt::check_launch(ctx, "loss_chain");
+    const int64_t nseg = kt::ceil_div(N, kt::xsum::kSeg);
+    const int g = (int)kt::ceil_div(nseg, 128);
+    xs_loss_partial_kernel<<<g, 128, 0, s()>>>(dd, N, xs_approx);
+    xs_loss_compose_kernel<<<1, 32, 0, s()>>>(dd, N, xs_approx, xs_approx + nseg, xs_maps, 0, dscal + 1);
+    xs_loss_map_kernel<<<g, 128, 0, s()>>>(dd, N, xs_approx + nseg, xs_maps);
+    xs_loss_compose_kernel<<<1, 32, 0, s()>>>(dd, N, xs_approx, xs_approx + nseg, xs_maps, 1, dscal + 1);
+    kt::check_launch(ctx, "exact loss", 4);
     double v;
     KT_CUDA(cudaMemcpyAsync(&v, dscal + 1, 8, cudaMemcpyDeviceToHost, s()));
     KT_CUDA(cudaStreamSynchronize(s()));
@@ -896,39 +1034,25 @@ struct KMeans {
     return loss;
   }
 
-  // Certified strict "a < b" on reference losses; exact chains when undecided.
-  bool less_loss(double La, const double* d2a, const int32_t* asga, double& La_exact, double Lb,
-                 const double* d2b, const int32_t* asgb, double& Lb_exact) {
-    if (!ctx->opt_force_exact) {
-      const double ea = loss_err(La), eb = loss_err(Lb);
-      if (La + ea < Lb - eb) return true;
-      if (La - ea >= Lb + eb) return false;
-      if (same_assign(asga, asgb)) return false;  // same partition => identical reference losses
-    }
-    ctx->stats[KTUNE_STAT_DECISION_FALLBACKS] += 1;
-    if (std::isnan(La_exact)) La_exact = exact_loss(d2a);
-    if (std::isnan(Lb_exact)) Lb_exact = exact_loss(d2b);
-    return La_exact < Lb_exact;
-  }
-
   struct Result {
     double loss, loss_exact;
     std::vector<double> iter_losses;
   };
 
   // kmeans_run (sampling.cpp:157-175): best of restarts into best_* buffers.
+  // Restart losses are the reference's exact sequential sums, so the strict
+  // "<" (earliest restart wins ties) is decided exactly.
   Result run(int k, uint64_t seed, int max_iters, int restarts) {
     Result best{0.0, NAN, {}};
     bool have = false;
     for (int r = 0; r < std::max(1, restarts); ++r) {
       std::vector<double> il;
-      const double L = lloyd(k, kt::seed_combine(seed, (uint64_t)r), max_iters, il);
-      double Lx = NAN;
-      bool take = !have;
-      if (have) take = less_loss(L, d2_a, asg_a, Lx, best.loss, best_d2, best_asg, best.loss_exact);
-      if (take) {
+      lloyd(k, kt::seed_combine(seed, (uint64_t)r), max_iters, il);
+      const double Lx = exact_loss(d2_a);
+      il.back() = Lx;
+      if (!have || Lx < best.loss_exact) {
         have = true;
-        best.loss = L;
+        best.loss = Lx;
         best.loss_exact = Lx;
         best.iter_losses = il;
         KT_CUDA(cudaMemcpyAsync(best_asg, asg_a, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s()));
@@ -999,7 +1123,7 @@ void sweep_impl(ktune_ctx* ctx, const ktune_space* space, const void* idx, const
   km.setup(ctx, space, d_pts, N);
   const int k_lo = (int)std::min<int64_t>(p->k_min, N);
   const int k_hi = (int)std::min<int64_t>(p->k_max_exclusive - 1, N);
-  double prev = INFINITY, prev_exact = NAN;
+  double prev = INFINITY;
   bool have_prev = false;
   int chosen = k_lo;
   double chosen_loss = 0.0;
@@ -1010,35 +1134,12 @@ void sweep_impl(ktune_ctx* ctx, const ktune_space* space, const void* idx, const
     chosen = k;
     chosen_loss = std::isnan(res.loss_exact) ? res.loss : res.loss_exact;
     KT_CUDA(cudaMemcpyAsync(d_chosen_cent, km.best_cent, sizeof(double) * k * D, cudaMemcpyDeviceToDevice, ctx->stream));
-    // break test: threshold * L_k >= L_{k-1} (sampling.cpp:444)
-    bool brk = false;
-    if (have_prev) {
-      double Lk = res.loss, Lp = prev;
-      bool decided = false;
-      if (!ctx->opt_force_exact) {
-        const double ek = km.loss_err(Lk), ep = km.loss_err(Lp);
-        if (p->threshold * (Lk - ek) * (1 - 4 * kU) >= (Lp + ep) * (1 + 4 * kU)) {
-          brk = true;
-          decided = true;
-        } else if (p->threshold * (Lk + ek) * (1 + 4 * kU) < (Lp - ep) * (1 - 4 * kU)) {
-          brk = false;
-          decided = true;
-        }
-      }
-      if (!decided) {
-        ctx->stats[KTUNE_STAT_DECISION_FALLBACKS] += 1;
-        if (std::isnan(res.loss_exact)) res.loss_exact = km.exact_loss(km.best_d2);
-        if (std::isnan(prev_exact)) prev_exact = km.exact_loss(km.prev_d2);
-        brk = p->threshold * res.loss_exact >= prev_exact;
-        chosen_loss = res.loss_exact;
-      }
-    }
+    // break test: threshold * L_k >= L_{k-1} on exact losses (sampling.cpp:444)
+    const bool brk = have_prev && p->threshold * res.loss_exact >= prev;
     klosses.push_back(chosen_loss);
     if (brk) break;
-    prev = res.loss;
-    prev_exact = res.loss_exact;
+    prev = res.loss_exact;
     have_prev = true;
-    KT_CUDA(cudaMemcpyAsync(km.prev_d2, km.best_d2, sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   // snap the chosen centroids (sampling.cpp:448-452)
   int32_t* d_snap = (int32_t*)ctx->dev(kt::WS_OUT1, sizeof(int32_t) * kt::kMaxK * D);

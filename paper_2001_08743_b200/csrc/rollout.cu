@@ -48,7 +48,7 @@ __host__ __device__ inline AcOff ac_layout(int n, int h, int g) {
 }
 
 struct RolloutTask {
-  KtSpaceParams sp;
+  int32_t card[kt::kMaxKnobs];
   const double* params;  // device, flat layout
   int n, h, g;
   int T;
@@ -65,6 +65,16 @@ struct RolloutTask {
 struct CtaWork {
   int task;
   int64_t first;  // first episode (task-local) of this CTA's tile
+};
+
+// Whole launch description passed BY VALUE (kernel parameter space), so a
+// launch needs no host->device copy: CTA b serves task t with
+// cta_base[t] <= b < cta_base[t+1], tile (b - cta_base[t]) * 32.
+constexpr int kMaxTasksPerLaunch = 12;
+struct RolloutLaunch {
+  int32_t num_tasks;
+  int32_t cta_base[kMaxTasksPerLaunch + 1];
+  RolloutTask task[kMaxTasksPerLaunch];
 };
 
 // Shared-memory carve-up (doubles): params (even-padded) | act [max(h,2g)][32] |
@@ -199,11 +209,13 @@ __device__ __forceinline__ Knob3 softmax3(double l0, double l1, double l2) {
 
 template <bool SP>
 __global__ void __launch_bounds__(kThreads, 1)
-rollout_kernel(const RolloutTask* __restrict__ tasks, const CtaWork* __restrict__ work) {
+rollout_kernel(const __grid_constant__ RolloutLaunch L) {
   constexpr bool smem_params = SP;
   extern __shared__ __align__(16) double sm[];
-  const CtaWork wk = work[blockIdx.x];
-  const RolloutTask* tkp = tasks + wk.task;
+  int ti = 0;
+  while (ti + 1 < L.num_tasks && L.cta_base[ti + 1] <= (int)blockIdx.x) ++ti;
+  const CtaWork wk{ti, (int64_t)((int)blockIdx.x - L.cta_base[ti]) * kTile};
+  const RolloutTask* tkp = &L.task[ti];
   const int n = tkp->n, h = tkp->h, g = tkp->g, T = tkp->T;
   const int64_t E = tkp->E, eoff = tkp->episode_offset;
   const uint64_t seed = tkp->seed;
@@ -225,7 +237,7 @@ rollout_kernel(const RolloutTask* __restrict__ tasks, const CtaWork* __restrict_
   const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t e = wk.first + c;
   const bool live = e < E;
-  if (threadIdx.x < n) card[threadIdx.x] = tkp->sp.card[threadIdx.x];
+  if (threadIdx.x < n) card[threadIdx.x] = tkp->card[threadIdx.x];
   // initial configurations (trajectory row 0)
   for (int d = w; d < n; d += kWarps) {
     uint16_t v = 0;
@@ -470,7 +482,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         h.d_score = t.score ? (double*)alloc(std::max<size_t>(8, (size_t)E * (T + 1) * 8)) : nullptr;
       }
       RolloutTask& r = dt[k];
-      r.sp = t.space->params;
+      for (int d = 0; d < kt::kMaxKnobs; ++d) r.card[d] = d < n ? t.space->card[d] : 1;
       r.params = t.ac->d_params;
       r.n = n;
       r.h = t.ac->h;
@@ -492,14 +504,22 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       smem = std::max(smem, rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, smem_params));
     if (smem > 227 * 1024) kt::fail(KTUNE_ERR_CONFIG, "rollout: agent too large for shared memory");
     if (!work.empty()) {
-      RolloutTask* d_tasks = (RolloutTask*)alloc(sizeof(RolloutTask) * num_tasks);
-      CtaWork* d_work = (CtaWork*)alloc(sizeof(CtaWork) * work.size());
-      KT_CUDA(cudaMemcpyAsync(d_tasks, dt.data(), sizeof(RolloutTask) * num_tasks, cudaMemcpyHostToDevice, ctx->stream));
-      KT_CUDA(cudaMemcpyAsync(d_work, work.data(), sizeof(CtaWork) * work.size(), cudaMemcpyHostToDevice, ctx->stream));
       auto kern = smem_params ? rollout_kernel<true> : rollout_kernel<false>;
       KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
-      kern<<<(unsigned)work.size(), kThreads, smem, ctx->stream>>>(d_tasks, d_work);
+      for (int t0 = 0; t0 < num_tasks; t0 += kMaxTasksPerLaunch) {  // grouped launches
+        RolloutLaunch L{};
+        L.num_tasks = std::min(kMaxTasksPerLaunch, num_tasks - t0);
+        int ctas = 0;
+        for (int q = 0; q < L.num_tasks; ++q) {
+          L.task[q] = dt[t0 + q];
+          L.cta_base[q] = ctas;
+          ctas += (int)kt::ceil_div(dt[t0 + q].E, kTile);
+        }
+        L.cta_base[L.num_tasks] = ctas;
+        if (ctas > 0) kern<<<(unsigned)ctas, kThreads, smem, ctx->stream>>>(L);
+      }
+
       kt::check_launch(ctx, "rollout");
     }
     // cost-model scores of every visited configuration (K1 over the trajectory)
