@@ -88,7 +88,9 @@ enum ktune_stat {
   KTUNE_STAT_GBT_NS = 10,           /* summed device time of gbt_predict_idx launches */
   KTUNE_STAT_GBT_CALLS = 11,
   KTUNE_STAT_ASSIGN_NS = 12,        /* summed device time of k-means assign launches */
-  KTUNE_STAT_ASSIGN_CALLS = 13
+  KTUNE_STAT_ASSIGN_CALLS = 13,
+  KTUNE_STAT_XS_SEQUENTIAL = 14,    /* exact-sum segments summed sequentially (binade crossings) */
+  KTUNE_STAT_XS_SEGMENTS = 15       /* exact-sum segments in total */
 };
 int ktune_ctx_stat(ktune_ctx* ctx, int stat, int64_t* value);
 int ktune_ctx_reset_stats(ktune_ctx* ctx);

@@ -19,7 +19,8 @@ F_DEVICE = 1
 OPT_FORCE_EXACT, OPT_KMEANS_MODE, OPT_PROFILE = 1, 2, 3
 STAT_LAUNCHES, STAT_KPP_FALLBACKS, STAT_DECISION_FALLBACKS, STAT_ASSIGN_FALLBACKS, \
     STAT_SNAP_CHAINS, STAT_LLOYD_ITERS, STAT_KPP_PICKS, STAT_ROLLOUT_NS, STAT_ROLLOUT_CALLS, \
-    STAT_GBT_NS, STAT_GBT_CALLS, STAT_ASSIGN_NS, STAT_ASSIGN_CALLS = range(1, 14)
+    STAT_GBT_NS, STAT_GBT_CALLS, STAT_ASSIGN_NS, STAT_ASSIGN_CALLS, STAT_XS_SEQUENTIAL, \
+    STAT_XS_SEGMENTS = range(1, 16)
 
 P = C.c_void_p
 i32 = C.c_int32

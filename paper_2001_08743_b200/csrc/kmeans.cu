@@ -526,7 +526,49 @@ __global__ void xs_map_kernel(KtSpaceParams sp, const IdxT* __restrict__ sorted,
   maps[(int64_t)g * D + d] = m;
 }
 
-// thread (cluster c, knob d): compose the segment maps from s = 0 exactly;
+// Warp-cooperative exact chain over one segment: every lane holds the same
+// running sum (uniform control flow); lanes fetch 32 elements at a time and
+// the chain consumes them in order through shuffles.
+template <class At>
+__device__ __forceinline__ double warp_seq_segment(double s, At at, int lo, int hi) {
+  const int lane = threadIdx.x & 31;
+  for (int i0 = lo; i0 < hi; i0 += 32) {
+    const int i = i0 + lane;
+    const double v = i < hi ? at(i) : 0.0;
+    const int m = min(32, hi - i0);
+    for (int q = 0; q < m; ++q) s = kt::dadd(s, __shfl_sync(0xffffffff, v, q));
+  }
+  return s;
+}
+
+// Warp-cooperative composition of a chain's segment maps (maps prefetched 32 at a time).
+template <class At, class MapAt>
+__device__ __forceinline__ double warp_compose(At at, MapAt map_at, int nseg, int n, int* nseq_out) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;  // MatrixXd::Zero / loss = 0.0 then += in order
+  int nseq = 0;
+  for (int g0 = 0; g0 < nseg; g0 += 32) {
+    kt::xsum::SegMap mine{0, 0, 0, 0};
+    if (g0 + lane < nseg) mine = map_at(g0 + lane);
+    const int mcount = min(32, nseg - g0);
+    for (int q = 0; q < mcount; ++q) {
+      kt::xsum::SegMap m;
+      m.F0 = __shfl_sync(0xffffffff, mine.F0, q);
+      m.F1 = __shfl_sync(0xffffffff, mine.F1, q);
+      m.e = __shfl_sync(0xffffffff, mine.e, q);
+      m.ok = __shfl_sync(0xffffffff, mine.ok, q);
+      if (kt::xsum::apply_map(s, m)) continue;
+      const int g = g0 + q;
+      const int lo = g * kt::xsum::kSeg, hi = min(n, lo + kt::xsum::kSeg);
+      ++nseq;
+      s = warp_seq_segment(s, at, lo, hi);
+    }
+  }
+  *nseq_out = nseq;
+  return s;
+}
+
+// warp per (cluster c, knob d): compose the segment maps from s = 0 exactly;
 // centroid = s / count (sampling.cpp:110-121).
 template <class IdxT>
 __global__ void xs_compose_kernel(KtSpaceParams sp, const IdxT* __restrict__ sorted,
@@ -535,32 +577,21 @@ __global__ void xs_compose_kernel(KtSpaceParams sp, const IdxT* __restrict__ sor
                                   const kt::xsum::SegMap* __restrict__ maps, double* __restrict__ cent,
                                   int32_t* __restrict__ seq_segments) {
   const int D = sp.D;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (t >= k * D) return;
   const int c = t / D, d = t % D;
   const int n = counts[c];
   if (n == 0) return;  // empty cluster: reseeded
   const double* lut = sp.lut + sp.lut_off[d];
   const IdxT* rows = sorted + (int64_t)cstart[c] * D + d;
-  double s = 0.0;  // MatrixXd::Zero then += in point order
+  const int gb = csb[c], nseg = csb[c + 1] - csb[c];
   int nseq = 0;
-  for (int g = csb[c]; g < csb[c + 1]; ++g) {
-    const kt::xsum::SegMap m = maps[(int64_t)g * D + d];
-    if (kt::xsum::apply_map(s, m)) continue;
-    ++nseq;
-    const int lo = (g - csb[c]) * kt::xsum::kSeg, hi = min(n, lo + kt::xsum::kSeg);
-    int i = lo;
-    for (; i + 8 <= hi; i += 8) {
-      double v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = __ldg(lut + (int)rows[(int64_t)(i + q) * D]);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s = kt::dadd(s, v[q]);
-    }
-    for (; i < hi; ++i) s = kt::dadd(s, __ldg(lut + (int)rows[(int64_t)i * D]));
+  const double s = warp_compose([&](int i) { return __ldg(lut + (int)rows[(int64_t)i * D]); },
+                                [&](int g) { return maps[(int64_t)(gb + g) * D + d]; }, nseg, n, &nseq);
+  if ((threadIdx.x & 31) == 0) {
+    cent[c * D + d] = kt::ddiv(s, (double)n);
+    if (nseq) atomicAdd(seq_segments, nseq);
   }
-  cent[c * D + d] = kt::ddiv(s, (double)n);
-  if (nseq) atomicAdd(seq_segments, nseq);
 }
 
 // ---- exact loss: the sequential sum of per-point d2 (sampling.cpp:56-63) -----
@@ -588,9 +619,10 @@ __global__ void xs_loss_map_kernel(const double* __restrict__ x, int64_t N, cons
 __global__ void xs_loss_compose_kernel(const double* __restrict__ x, int64_t N,
                                        const double* __restrict__ approx, double* __restrict__ prefix,
                                        const kt::xsum::SegMap* __restrict__ maps, int phase, double* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
   const int64_t nseg = (N + kt::xsum::kSeg - 1) / kt::xsum::kSeg;
   if (phase == 0) {  // exclusive prefix of the approximate segment sums
+    if (threadIdx.x != 0) return;
     double run = 0.0;
     for (int64_t g = 0; g < nseg; ++g) {
       prefix[g] = run;
@@ -598,13 +630,9 @@ __global__ void xs_loss_compose_kernel(const double* __restrict__ x, int64_t N,
     }
     return;
   }
-  double s = 0.0;
-  for (int64_t g = 0; g < nseg; ++g) {
-    if (kt::xsum::apply_map(s, maps[g])) continue;
-    const int64_t lo = g * kt::xsum::kSeg, hi = min(N, lo + kt::xsum::kSeg);
-    for (int64_t i = lo; i < hi; ++i) s = kt::dadd(s, x[i]);
-  }
-  *out = s;
+  int nseq = 0;
+  const double s = warp_compose([&](int i) { return x[i]; }, [&](int g) { return maps[g]; }, (int)nseg, (int)N, &nseq);
+  if (threadIdx.x == 0) *out = s;
 }
 
 // Empty clusters (sampling.cpp:122-136): in cluster order, the unclaimed
@@ -912,6 +940,7 @@ struct KMeans {
     sorted = (IdxT*)ctx->dev(kt::WS_SORTED, sizeof(IdxT) * N * D);
     xs_approx = (double*)ctx->dev(kt::WS_XS_APPROX, sizeof(double) * (size_t)max_segs * D);
     xs_maps = (kt::xsum::SegMap*)ctx->dev(kt::WS_XS_MAPS, sizeof(kt::xsum::SegMap) * (size_t)max_segs * D);
+    KT_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (4 * kt::kMaxK + 16), ctx->stream));
     cent_a = (double*)ctx->dev(kt::WS_CENT, sizeof(double) * kt::kMaxK * D * 3);
     cent_b = cent_a + kt::kMaxK * D;
     best_cent = cent_b + kt::kMaxK * D;
@@ -958,10 +987,18 @@ struct KMeans {
     struct {
       double loss;
       unsigned long long changed;
+      int32_t seq, segs;
     } h;
     KT_CUDA(cudaMemcpyAsync(&h.loss, dscal, 8, cudaMemcpyDeviceToHost, s()));
     KT_CUDA(cudaMemcpyAsync(&h.changed, ull, 8, cudaMemcpyDeviceToHost, s()));
+    KT_CUDA(cudaMemcpyAsync(&h.seq, seqcnt, 4, cudaMemcpyDeviceToHost, s()));
+    KT_CUDA(cudaMemcpyAsync(&h.segs, csb + k, 4, cudaMemcpyDeviceToHost, s()));
+    KT_CUDA(cudaMemsetAsync(seqcnt, 0, 4, s()));
     KT_CUDA(cudaStreamSynchronize(s()));
+    if (prev) {
+      ctx->stats[KTUNE_STAT_XS_SEQUENTIAL] += h.seq;
+      ctx->stats[KTUNE_STAT_XS_SEGMENTS] += (int64_t)h.segs * D;
+    }
     if (changed_out) *changed_out = h.changed;
     return h.loss;
   }
@@ -977,7 +1014,7 @@ struct KMeans {
     xs_partial_kernel<IdxT><<<gseg, th, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, max_segs, xs_approx);
     xs_prefix_kernel<<<(int)kt::ceil_div(k * D, 128), 128, 0, s()>>>(D, csb, k, xs_approx);
     xs_map_kernel<IdxT><<<gseg, th, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, max_segs, xs_approx, xs_maps);
-    xs_compose_kernel<IdxT><<<(int)kt::ceil_div(k * D, 32), 32, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k,
+    xs_compose_kernel<IdxT><<<(int)kt::ceil_div(k * D * 32, 128), 128, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k,
                                                                           xs_maps, next, seqcnt);
     KT_CUDA(cudaMemsetAsync(counts + 2 * kt::kMaxK, 0, 4, s()));
     reseed_kernel<IdxT><<<1, 1024, 0, s()>>>(sp->params, pts, N, counts, k, d2_old, next,
