@@ -30,13 +30,22 @@
 namespace kt {
 namespace xsum {
 
-constexpr int kSeg = 512;  // elements per segment
+constexpr int kSeg = 256;  // elements per segment
 
 struct SegMap {
   uint64_t F0, F1;  // increments of m (units of U) for even / odd start parity
   int32_t e;        // binade the map assumes (unbiased exponent of the running sum)
-  int32_t ok;       // 0: must be summed sequentially
+  int32_t ok;       // 0: must be summed sequentially; 1: valid in binade e;
+                    // 2: identity (every element is +0: s + 0 == s for any s >= 0)
 };
+
+// Identity map if every element of the segment is zero.
+template <class At>
+__device__ SegMap zero_segment_map(At at, int len) {
+  for (int i = 0; i < len; ++i)
+    if (at(i) != 0.0) return SegMap{0, 0, 0, 0};
+  return SegMap{0, 0, 0, 2};
+}
 
 __device__ __forceinline__ int binade_of(double s) {
   return (int)((__double_as_longlong(s) >> 52) & 0x7FF) - 1023;
@@ -84,6 +93,7 @@ __device__ SegMap segment_map(At at, int len, int e) {
 // Apply a segment map to the exact running value s if valid; returns false
 // when the caller must sum the segment sequentially.
 __device__ __forceinline__ bool apply_map(double& s, const SegMap& m) {
+  if (m.ok == 2) return true;
   if (!m.ok || !(s > 0.0)) return false;
   const uint64_t b = (uint64_t)__double_as_longlong(s);
   const int e = (int)((b >> 52) & 0x7FF) - 1023;

@@ -60,6 +60,42 @@ __device__ double block_sum(double v, double* red) {
   return v;  // valid in thread 0
 }
 
+// One warp: in-place exclusive prefix of a[0..n) (stride `stride`), 32 at a time.
+// Only feeds approximations / certified bounds, so the tree order is fine.
+__device__ double warp_exclusive_scan(double* a, int64_t n, int64_t stride) {
+  const int lane = threadIdx.x & 31;
+  double carry = 0.0;
+  for (int64_t i0 = 0; i0 < n; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const double v = i < n ? a[i * stride] : 0.0;
+    double x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffff, x, o);
+      if (lane >= o) x = kt::dadd(x, y);
+    }
+    if (i < n) a[i * stride] = kt::dadd(carry, kt::dsub(x, v));
+    carry = kt::dadd(carry, __shfl_sync(0xffffffff, x, 31));
+  }
+  return carry;
+}
+
+__device__ int warp_exclusive_scan_int(int32_t* a, int64_t n, int64_t stride) {
+  const int lane = threadIdx.x & 31;
+  int carry = 0;
+  for (int64_t i0 = 0; i0 < n; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const int v = i < n ? a[i * stride] : 0;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffff, x, o);
+      if (lane >= o) x += y;
+    }
+    if (i < n) a[i * stride] = carry + x - v;
+    carry += __shfl_sync(0xffffffff, x, 31);
+  }
+  return carry;
+}
+
 // Load the feature LUT into shared memory.
 __device__ const double* stage_lut(const KtSpaceParams& sp, double* s_lut, int lut_total) {
   for (int i = threadIdx.x; i < lut_total; i += blockDim.x) s_lut[i] = sp.lut[i];
@@ -219,19 +255,20 @@ __global__ void __launch_bounds__(1024) kpp_select_kernel(const double* __restri
   }
   if (sh_branch == 0) return;
   const double u = sh_u, T = sh_tot;
-  const double lgN = (double)(64 - __clzll((unsigned long long)N)) + 16.0;
+  // slack for the tree/warp-scan order of the estimates (per-chunk tree + carry over nch/32 warps)
+  const double lgN = (double)(64 - __clzll((unsigned long long)N)) + 24.0 + (double)(nch / 32);
   const double eT = gamma_bound((double)(N / 4) + lgN) * T;
   const double r_est = kt::dmul(u, T);
   const double r_err = kt::dadd(kt::dmul(u, eT), gamma_bound(4.0) * r_est);
   const double r_lo = kt::dsub(r_est, r_err), r_hi = kt::dadd(r_est, r_err);
   // chunk exclusive prefix (sequential per 1024-chunk slice, tree-free and
   // simple: thread 0 scans up to nch chunk sums into scratch)
+  if (tid < 32) {
+    for (int64_t b = tid; b < nch; b += 32) scratch[b] = chunk_sum[b];
+    __syncwarp();
+    warp_exclusive_scan(scratch, nch, 1);
+  }
   if (tid == 0) {
-    double p = 0.0;
-    for (int64_t b = 0; b < nch; ++b) {
-      scratch[b] = p;
-      p = kt::dadd(p, chunk_sum[b]);
-    }
     sh_bfirst = -1;
     sh_bsecond = -1;
     sh_ib = ~0ull;
@@ -387,25 +424,22 @@ __global__ void __launch_bounds__(kBT) hist_kernel(const int32_t* __restrict__ a
 __global__ void scan_counts_kernel(int32_t* __restrict__ blockcounts, int64_t nblocks, int k,
                                    int32_t* __restrict__ counts, int32_t* __restrict__ cstart,
                                    int32_t* __restrict__ csb) {
-  const int c = threadIdx.x;
   __shared__ int tot[kt::kMaxK];
-  if (c < k) {
-    int run = 0;
-    for (int64_t b = 0; b < nblocks; ++b) {
-      const int v = blockcounts[b * k + c];
-      blockcounts[b * k + c] = run;
-      run += v;
+  const int w = threadIdx.x >> 5;  // warp per cluster
+  for (int c = w; c < k; c += blockDim.x >> 5) {
+    const int t = warp_exclusive_scan_int(blockcounts + c, nblocks, k);
+    if ((threadIdx.x & 31) == 0) {
+      tot[c] = t;
+      counts[c] = t;
     }
-    tot[c] = run;
-    counts[c] = run;
   }
   __syncthreads();
-  if (c == 0) {
-    int s = 0, sb = 0;
+  if (threadIdx.x == 0) {
+    int sum = 0, sb = 0;
     for (int j = 0; j < k; ++j) {
-      cstart[j] = s;
+      cstart[j] = sum;
       csb[j] = sb;
-      s += tot[j];
+      sum += tot[j];
       sb += (tot[j] + kt::xsum::kSeg - 1) / kt::xsum::kSeg;
     }
     csb[k] = sb;
@@ -489,17 +523,12 @@ __global__ void xs_partial_kernel(KtSpaceParams sp, const IdxT* __restrict__ sor
   approx[(int64_t)g * D + d] = s;
 }
 
-// thread (cluster c, knob d): exclusive prefix of the approximate segment sums.
+// warp per (cluster c, knob d): exclusive prefix of the approximate segment sums.
 __global__ void xs_prefix_kernel(int D, const int32_t* __restrict__ csb, int k, double* __restrict__ approx) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (t >= k * D) return;
   const int c = t / D, d = t % D;
-  double run = 0.0;
-  for (int g = csb[c]; g < csb[c + 1]; ++g) {
-    const double v = approx[(int64_t)g * D + d];
-    approx[(int64_t)g * D + d] = run;
-    run = kt::dadd(run, v);
-  }
+  warp_exclusive_scan(approx + (int64_t)csb[c] * D + d, csb[c + 1] - csb[c], D);
 }
 
 template <class IdxT>
@@ -516,13 +545,11 @@ __global__ void xs_map_kernel(KtSpaceParams sp, const IdxT* __restrict__ sorted,
   const int n = counts[c];
   const int lo = j * kt::xsum::kSeg, hi = min(n, lo + kt::xsum::kSeg);
   const double pre = prefix[(int64_t)g * D + d];
-  kt::xsum::SegMap m{0, 0, 0, 0};
-  if (pre > 0.0) {
-    const double* lut = sp.lut + sp.lut_off[d];
-    const IdxT* rows = sorted + (int64_t)cstart[c] * D + d;
-    m = kt::xsum::segment_map([&](int i) { return __ldg(lut + (int)rows[(int64_t)(lo + i) * D]); }, hi - lo,
-                              kt::xsum::binade_of(pre));
-  }
+  const double* lut = sp.lut + sp.lut_off[d];
+  const IdxT* rows = sorted + (int64_t)cstart[c] * D + d;
+  auto at = [&](int i) { return __ldg(lut + (int)rows[(int64_t)(lo + i) * D]); };
+  const kt::xsum::SegMap m = pre > 0.0 ? kt::xsum::segment_map(at, hi - lo, kt::xsum::binade_of(pre))
+                                       : kt::xsum::zero_segment_map(at, hi - lo);
   maps[(int64_t)g * D + d] = m;
 }
 
@@ -532,11 +559,29 @@ __global__ void xs_map_kernel(KtSpaceParams sp, const IdxT* __restrict__ sorted,
 template <class At>
 __device__ __forceinline__ double warp_seq_segment(double s, At at, int lo, int hi) {
   const int lane = threadIdx.x & 31;
-  for (int i0 = lo; i0 < hi; i0 += 32) {
-    const int i = i0 + lane;
-    const double v = i < hi ? at(i) : 0.0;
-    const int m = min(32, hi - i0);
-    for (int q = 0; q < m; ++q) s = kt::dadd(s, __shfl_sync(0xffffffff, v, q));
+  constexpr int kAhead = 4;  // batches in flight: the loads overlap the chain
+  double v[kAhead];
+#pragma unroll
+  for (int b = 0; b < kAhead; ++b) {
+    const int i = lo + b * 32 + lane;
+    v[b] = i < hi ? at(i) : 0.0;
+  }
+  for (int i0 = lo; i0 < hi; i0 += 32 * kAhead) {
+#pragma unroll
+    for (int b = 0; b < kAhead; ++b) {
+      const int base = i0 + b * 32;
+      const double cur = v[b];
+      const int nx = base + kAhead * 32 + lane;  // refill this slot for the next round
+      v[b] = nx < hi ? at(nx) : 0.0;
+      if (base < hi) {
+        if (hi - base >= 32) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) s = kt::dadd(s, __shfl_sync(0xffffffff, cur, q));
+        } else {
+          for (int q = 0; q < hi - base; ++q) s = kt::dadd(s, __shfl_sync(0xffffffff, cur, q));
+        }
+      }
+    }
   }
   return s;
 }
@@ -551,6 +596,32 @@ __device__ __forceinline__ double warp_compose(At at, MapAt map_at, int nseg, in
     kt::xsum::SegMap mine{0, 0, 0, 0};
     if (g0 + lane < nseg) mine = map_at(g0 + lane);
     const int mcount = min(32, nseg - g0);
+    // Fast path: all maps of this batch valid for one binade -> compose the
+    // 32 maps with a warp scan (m -> m + F(m mod 2) is closed under
+    // composition) and apply the whole batch in one step.
+    const unsigned real = __ballot_sync(0xffffffff, lane < mcount && mine.ok != 2);  // non-identity maps
+    if (real == 0) continue;  // whole batch is identity (all-zero segments)
+    const int e0 = __shfl_sync(0xffffffff, mine.e, __ffs(real) - 1);
+    const bool uniform = __all_sync(0xffffffff, lane >= mcount || mine.ok == 2 || (mine.ok == 1 && mine.e == e0));
+    if (uniform && s > 0.0) {
+      uint64_t c0 = mine.F0, c1 = mine.F1;  // inclusive composition f_0 .. f_lane
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t p0 = __shfl_up_sync(0xffffffff, c0, off);
+        const uint64_t p1 = __shfl_up_sync(0xffffffff, c1, off);
+        if (lane >= off) {  // earlier maps (p) then mine (c)
+          const uint64_t n0 = p0 + ((p0 & 1u) ? c1 : c0);
+          const uint64_t n1 = p1 + (((1u + p1) & 1u) ? c1 : c0);
+          c0 = n0;
+          c1 = n1;
+        }
+      }
+      kt::xsum::SegMap all;
+      all.F0 = __shfl_sync(0xffffffff, c0, mcount - 1);
+      all.F1 = __shfl_sync(0xffffffff, c1, mcount - 1);
+      all.e = e0;
+      all.ok = all.F0 < (1ull << 53) && all.F1 < (1ull << 53);
+      if (kt::xsum::apply_map(s, all)) continue;
+    }
     for (int q = 0; q < mcount; ++q) {
       kt::xsum::SegMap m;
       m.F0 = __shfl_sync(0xffffffff, mine.F0, q);
@@ -611,9 +682,9 @@ __global__ void xs_loss_map_kernel(const double* __restrict__ x, int64_t N, cons
   const int64_t lo = g * kt::xsum::kSeg;
   if (lo >= N) return;
   const int len = (int)(min(N, lo + kt::xsum::kSeg) - lo);
-  kt::xsum::SegMap m{0, 0, 0, 0};
-  if (prefix[g] > 0.0) m = kt::xsum::segment_map([&](int i) { return x[lo + i]; }, len, kt::xsum::binade_of(prefix[g]));
-  maps[g] = m;
+  auto at = [&](int i) { return x[lo + i]; };
+  maps[g] = prefix[g] > 0.0 ? kt::xsum::segment_map(at, len, kt::xsum::binade_of(prefix[g]))
+                            : kt::xsum::zero_segment_map(at, len);
 }
 
 __global__ void xs_loss_compose_kernel(const double* __restrict__ x, int64_t N,
@@ -622,12 +693,9 @@ __global__ void xs_loss_compose_kernel(const double* __restrict__ x, int64_t N,
   if (blockIdx.x != 0 || threadIdx.x >= 32) return;
   const int64_t nseg = (N + kt::xsum::kSeg - 1) / kt::xsum::kSeg;
   if (phase == 0) {  // exclusive prefix of the approximate segment sums
-    if (threadIdx.x != 0) return;
-    double run = 0.0;
-    for (int64_t g = 0; g < nseg; ++g) {
-      prefix[g] = run;
-      run = kt::dadd(run, approx[g]);
-    }
+    for (int64_t g = threadIdx.x; g < nseg; g += 32) prefix[g] = approx[g];
+    __syncwarp();
+    warp_exclusive_scan(prefix, nseg, 1);
     return;
   }
   int nseq = 0;
@@ -1006,13 +1074,13 @@ struct KMeans {
   void update_centroids(int k, const int32_t* asg, const double* d2_old, double* next) {
     int32_t* cstart = counts + kt::kMaxK;
     hist_kernel<<<grid_pts(), kBT, 0, s()>>>(asg, N, k, blockcounts);
-    scan_counts_kernel<<<1, 64, 0, s()>>>(blockcounts, nchunks, k, counts, cstart, csb);
+    scan_counts_kernel<<<1, 1024, 0, s()>>>(blockcounts, nchunks, k, counts, cstart, csb);
     scatter_kernel<IdxT><<<grid_pts(), kBT, 0, s()>>>(asg, N, k, D, pts, blockcounts, cstart, members, sorted);
     // exact in-order centroid sums (exactsum.cuh)
     const int th = 256;
     const int gseg = (int)kt::ceil_div((int64_t)max_segs * D, th);
     xs_partial_kernel<IdxT><<<gseg, th, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, max_segs, xs_approx);
-    xs_prefix_kernel<<<(int)kt::ceil_div(k * D, 128), 128, 0, s()>>>(D, csb, k, xs_approx);
+    xs_prefix_kernel<<<(int)kt::ceil_div(k * D * 32, 128), 128, 0, s()>>>(D, csb, k, xs_approx);
     xs_map_kernel<IdxT><<<gseg, th, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, max_segs, xs_approx, xs_maps);
     xs_compose_kernel<IdxT><<<(int)kt::ceil_div(k * D * 32, 128), 128, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k,
                                                                           xs_maps, next, seqcnt);

@@ -17,6 +17,7 @@ def seg_map(xs, e):
         if f0 >= 2**53 or f1 >= 2**53: return None
     return (f0, f1, e)
 def apply(s, m):
+    if m == "zero": return s
     if m is None or not s > 0: return None
     b = bits(s); e = ((b >> 52) & 0x7FF) - 1023
     if e != m[2] or ((b >> 52) & 0x7FF) == 0: return None
@@ -28,7 +29,8 @@ def exact(xs):
     segs = [xs[i:i+SEG] for i in range(0, len(xs), SEG)]
     approx = [sum(sg) for sg in segs]; pre = []; run = 0.0
     for a in approx: pre.append(run); run += a
-    maps = [seg_map(sg, binade(p)) if p > 0 else None for sg, p in zip(segs, pre)]
+    maps = [seg_map(sg, binade(p)) if p > 0 else ("zero" if all(x == 0 for x in sg) else None)
+            for sg, p in zip(segs, pre)]
     s = 0.0; nseq = 0
     for sg, m in zip(segs, maps):
         r = apply(s, m)
