@@ -99,6 +99,13 @@ int ktune_ctx_create_dist(int device, int rank, int world, const void* nccl_id, 
     ctx->world = world;
     KT_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
+    // keep stream-ordered allocations cached across calls (host-pointer paths
+    // allocate trajectory-sized buffers per call)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     if (world > 1) {
       if (!nccl_id) kt::fail(KTUNE_ERR_CONFIG, "world > 1 needs an ncclUniqueId");
       ncclUniqueId id;
