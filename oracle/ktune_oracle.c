@@ -350,26 +350,26 @@ static double ac_forward_one(int n, int h, int g, const double* p, const double*
   const ac_off o = ac_layout(n, h, g);
   for (int j = 0; j < h; ++j) {
     double acc = 0.0;
-    for (int i = 0; i < n; ++i) acc = acc + p[o.w0 + (int64_t)i * h + j] * x[i];
+    for (int i = 0; i < n; ++i) acc = fma(p[o.w0 + (int64_t)i * h + j], x[i], acc);
     h0[j] = ko_tanh(acc + p[o.b0 + j]);
   }
   for (int j = 0; j < g; ++j) {
     double acc = 0.0;
-    for (int i = 0; i < h; ++i) acc = acc + p[o.wp1 + (int64_t)i * g + j] * h0[i];
+    for (int i = 0; i < h; ++i) acc = fma(p[o.wp1 + (int64_t)i * g + j], h0[i], acc);
     hp[j] = ko_tanh(acc + p[o.bp1 + j]);
   }
   for (int a = 0; a < 3 * n; ++a) {
     double acc = 0.0;
-    for (int j = 0; j < g; ++j) acc = acc + p[o.wp2 + (int64_t)j * 3 * n + a] * hp[j];
+    for (int j = 0; j < g; ++j) acc = fma(p[o.wp2 + (int64_t)j * 3 * n + a], hp[j], acc);
     logits[a] = acc + p[o.bp2 + a];
   }
   for (int j = 0; j < g; ++j) {
     double acc = 0.0;
-    for (int i = 0; i < h; ++i) acc = acc + p[o.wv1 + (int64_t)i * g + j] * h0[i];
+    for (int i = 0; i < h; ++i) acc = fma(p[o.wv1 + (int64_t)i * g + j], h0[i], acc);
     hv[j] = ko_tanh(acc + p[o.bv1 + j]);
   }
   double v = 0.0;
-  for (int j = 0; j < g; ++j) v = v + p[o.wv2 + j] * hv[j];
+  for (int j = 0; j < g; ++j) v = fma(p[o.wv2 + j], hv[j], v);
   v = v + p[o.bv2];
   /* per-knob log-softmax over {dec, stay, inc} (actor_critic.hpp:13-14) */
   for (int d = 0; d < n; ++d) {

@@ -114,7 +114,7 @@ __device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n
       double wr[kUnits];
       load8(P + o.w0 + i * h + ub, wr);
 #pragma unroll
-      for (int r = 0; r < kUnits; ++r) acc[r] = kt::dadd(acc[r], kt::dmul(wr[r], x));
+      for (int r = 0; r < kUnits; ++r) acc[r] = __fma_rn(wr[r], x, acc[r]);
     }
     double b[kUnits];
     load8(P + o.b0 + ub, b);
@@ -138,7 +138,7 @@ __device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n
       double wr[kUnits];
       load8(wb + i * g, wr);
 #pragma unroll
-      for (int r = 0; r < kUnits; ++r) acc[r] = kt::dadd(acc[r], kt::dmul(wr[r], x));
+      for (int r = 0; r < kUnits; ++r) acc[r] = __fma_rn(wr[r], x, acc[r]);
     }
     double b[kUnits];
     load8(ub < g ? P + o.bp1 + ub : P + o.bv1 + (ub - g), b);
@@ -173,7 +173,7 @@ __device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = 0; j < g; ++j) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = kt::dadd(acc[q], kt::dmul(wp[q][j * ws[q]], hrow[q][j * kTile]));
+      for (int q = 0; q < 4; ++q) acc[q] = __fma_rn(wp[q][j * ws[q]], hrow[q][j * kTile], acc[q]);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
