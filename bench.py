@@ -277,8 +277,13 @@ def main():
              for s, d, a, g, init in zip(specs, spaces, agents, gbts, inits_dev)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
+    D0 = specs[0].space.num_knobs
+    mkd = lambda shape, dt: torch.empty(shape, dtype=dt, device="cuda")
+    dev_out = [dict(idx=mkd((E, T + 1, D0), torch.uint16), score=mkd((E, T + 1), torch.float64),
+                    actions=mkd((E, T, D0), torch.int8), logp=mkd((E, T), torch.float64),
+                    value=mkd((E, T), torch.float64)) for _ in specs]  # persistent trajectory buffers
     for _ in range(args.warmup):
-        run_episodes_batch(tasks, T, ctx)
+        run_episodes_batch(tasks, T, ctx, host_out=dev_out)
     torch.cuda.synchronize()
 
     def barrier():
@@ -294,7 +299,7 @@ def main():
         start.record(stream)
         for _ in range(args.steps):
             flush.zero_()
-            outs = run_episodes_batch(tasks, T, ctx)
+            run_episodes_batch(tasks, T, ctx, host_out=dev_out)
         end.record(stream)
         barrier()
     ms = start.elapsed_time(end)

@@ -22,7 +22,6 @@
 
 namespace {
 
-constexpr int kTile = 32;      // episodes per CTA (one per lane)
 constexpr int kThreads = 512;  // 16 warps per CTA; every phase maps lane <-> episode
 constexpr int kWarps = kThreads / 32;
 constexpr int kUnits = 8;      // hidden units per thread per pass (independent fp64 chains)
@@ -62,14 +61,9 @@ struct RolloutTask {
   double* value;
 };
 
-struct CtaWork {
-  int task;
-  int64_t first;  // first episode (task-local) of this CTA's tile
-};
-
 // Whole launch description passed BY VALUE (kernel parameter space), so a
 // launch needs no host->device copy: CTA b serves task t with
-// cta_base[t] <= b < cta_base[t+1], tile (b - cta_base[t]) * 32.
+// cta_base[t] <= b < cta_base[t+1].
 constexpr int kMaxTasksPerLaunch = 12;
 struct RolloutLaunch {
   int32_t num_tasks;
@@ -77,20 +71,21 @@ struct RolloutLaunch {
   RolloutTask task[kMaxTasksPerLaunch];
 };
 
-// Shared-memory carve-up (doubles): params (even-padded) | act [max(h,2g)][32] |
-// buf [3n][32] | val [32] | then uint16 cfg [n][32] | int32 card [n].
-__host__ __device__ inline size_t rollout_smem_bytes(int n, int h, int g, bool smem_params) {
-  const AcOff o = ac_layout(n, h, g);
-  const int act = (h > 2 * g ? h : 2 * g) * kTile;
-  size_t d = (smem_params ? (size_t)((o.total + 1) & ~1) : 0) + act + (size_t)3 * n * kTile + kTile;
-  return d * 8 + (size_t)kTile * n * 2 + (size_t)n * 4 + 16;
+__host__ __device__ inline int act_rows(int n, int h, int g) {
+  int r = h > 2 * g ? h : 2 * g;
+  return r > 3 * n ? r : 3 * n;  // logits alias the activation rows after layer 2
 }
 
-// One exact fp64 forward pass over the 32 states held in buf[i][c] (lane = c).
-// Leaves logits in buf[a][c], values in val[c]; act ends up holding hp/hv.
-// Weight reads are warp-uniform (broadcast, 16-byte), activation reads
-// lane-contiguous (conflict-free). P is shared memory when the parameter block
-// fits, else global (read-only path).
+// Shared-memory carve-up (doubles): params (even-padded) | act [rows][tile] |
+// x [n][tile] | val [tile] | then uint16 cfg [n][tile] | int32 card [n].
+__host__ __device__ inline size_t rollout_smem_bytes(int n, int h, int g, bool smem_params, int cpl) {
+  const AcOff o = ac_layout(n, h, g);
+  const int tile = 32 * cpl;
+  size_t d = (smem_params ? (size_t)((o.total + 1) & ~1) : 0) + (size_t)act_rows(n, h, g) * tile +
+             (size_t)n * tile + tile;
+  return d * 8 + (size_t)tile * n * 2 + (size_t)n * 4 + 16;
+}
+
 __device__ __forceinline__ void load8(const double* p, double (&w)[kUnits]) {
   const double2* q = reinterpret_cast<const double2*>(p);
 #pragma unroll
@@ -101,85 +96,134 @@ __device__ __forceinline__ void load8(const double* p, double (&w)[kUnits]) {
   }
 }
 
+// One exact forward pass over the tile's states held in x[i][e] (e = lane + 32q).
+// Leaves logits in act[a][e] (aliasing the hidden activations), values in val[e].
+// Weight reads are warp-uniform 16-byte broadcasts feeding 32*CPL FMAs each;
+// activation reads are lane-contiguous (conflict-free).
+template <int CPL>
 __device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n, int h, int g,
-                             double* act, double* buf, double* val) {
+                             double* act, const double* x, double* val) {
+  constexpr int tile = 32 * CPL;
   const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // ---- A: h0[j][c] = tanh(sum_i W0(j,i) x[i][c] + b0[j]);  W0 column-major (h x n)
+  // ---- A: h0[j][e] = tanh(sum_i fma(W0(j,i), x[i][e]) + b0[j]);  W0 column-major (h x n)
   for (int ub = w * kUnits; ub < h; ub += kWarps * kUnits) {
-    double acc[kUnits];
+    double acc[CPL][kUnits];
 #pragma unroll
-    for (int r = 0; r < kUnits; ++r) acc[r] = 0.0;
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int r = 0; r < kUnits; ++r) acc[q][r] = 0.0;
     for (int i = 0; i < n; ++i) {
-      const double x = buf[i * kTile + c];
       double wr[kUnits];
       load8(P + o.w0 + i * h + ub, wr);
 #pragma unroll
-      for (int r = 0; r < kUnits; ++r) acc[r] = __fma_rn(wr[r], x, acc[r]);
+      for (int q = 0; q < CPL; ++q) {
+        const double xv = x[i * tile + c + 32 * q];
+#pragma unroll
+        for (int r = 0; r < kUnits; ++r) acc[q][r] = __fma_rn(wr[r], xv, acc[q][r]);
+      }
     }
     double b[kUnits];
     load8(P + o.b0 + ub, b);
 #pragma unroll
-    for (int r = 0; r < kUnits; ++r) act[(ub + r) * kTile + c] = kt::kt_tanh_bf(kt::dadd(acc[r], b[r]));
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int r = 0; r < kUnits; ++r)
+        act[(ub + r) * tile + c + 32 * q] = kt::kt_tanh_bf(kt::dadd(acc[q][r], b[r]));
   }
   __syncthreads();
   // ---- B: units u < g: hp = tanh(Wp1 h0 + bp1); g <= u < 2g: hv = tanh(Wv1 h0 + bv1)
-  double res[2][kUnits];
+  constexpr int kPasses = CPL == 1 ? 2 : 1;  // 2g <= 256 (CPL 1) or <= 128 (CPL 2)
+  double res[kPasses][CPL][kUnits];
 #pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
+  for (int pass = 0; pass < kPasses; ++pass) {
     const int ub = w * kUnits + pass * kWarps * kUnits;
     if (ub >= 2 * g) break;
     const double* wb = ub < g ? P + o.wp1 + ub : P + o.wv1 + (ub - g);
-    double acc[kUnits];
+    double acc[CPL][kUnits];
 #pragma unroll
-    for (int r = 0; r < kUnits; ++r) acc[r] = 0.0;
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int r = 0; r < kUnits; ++r) acc[q][r] = 0.0;
 #pragma unroll 2
     for (int i = 0; i < h; ++i) {
-      const double x = act[i * kTile + c];
       double wr[kUnits];
       load8(wb + i * g, wr);
 #pragma unroll
-      for (int r = 0; r < kUnits; ++r) acc[r] = __fma_rn(wr[r], x, acc[r]);
+      for (int q = 0; q < CPL; ++q) {
+        const double xv = act[i * tile + c + 32 * q];
+#pragma unroll
+        for (int r = 0; r < kUnits; ++r) acc[q][r] = __fma_rn(wr[r], xv, acc[q][r]);
+      }
     }
     double b[kUnits];
     load8(ub < g ? P + o.bp1 + ub : P + o.bv1 + (ub - g), b);
 #pragma unroll
-    for (int r = 0; r < kUnits; ++r) res[pass][r] = kt::kt_tanh_bf(kt::dadd(acc[r], b[r]));
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int r = 0; r < kUnits; ++r) res[pass][q][r] = kt::kt_tanh_bf(kt::dadd(acc[q][r], b[r]));
   }
   __syncthreads();
 #pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
+  for (int pass = 0; pass < kPasses; ++pass) {
     const int ub = w * kUnits + pass * kWarps * kUnits;
     if (ub >= 2 * g) break;
 #pragma unroll
-    for (int r = 0; r < kUnits; ++r) act[(ub + r) * kTile + c] = res[pass][r];
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int r = 0; r < kUnits; ++r) act[(ub + r) * tile + c + 32 * q] = res[pass][q][r];
   }
   __syncthreads();
-  // ---- C: logits (Wp2 column-major 3n x g) and value, 4 interleaved items per
-  // warp. Item a < 3n reads Wp2 row a against hp; a == 3n reads wv2 against hv;
-  // items beyond 3n are computed on row 0 and discarded (no branch in the loop).
+  // ---- C: logits (Wp2 column-major 3n x g) and value; items a = w + 16j, up to
+  // 8 per warp (n <= 32), held in registers until every hp/hv read is done,
+  // then written over the activation rows.
   const int na = 3 * n + 1;
-  for (int a0 = w; a0 < na; a0 += 4 * kWarps) {
+  double outv[2][4][CPL];
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    const int a0 = w + pass * 4 * kWarps;
+    if (a0 >= na) break;
     const double* wp[4];
     int ws[4];
     const double* hrow[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int a = a0 + q * kWarps;
+    for (int k = 0; k < 4; ++k) {
+      const int a = a0 + k * kWarps;
       const bool is_val = a == 3 * n;
-      wp[q] = is_val ? P + o.wv2 : P + o.wp2 + (a < 3 * n ? a : 0);
-      ws[q] = is_val ? 1 : 3 * n;
-      hrow[q] = act + (is_val ? g : 0) * kTile + c;
+      wp[k] = is_val ? P + o.wv2 : P + o.wp2 + (a < 3 * n ? a : 0);
+      ws[k] = is_val ? 1 : 3 * n;
+      hrow[k] = act + (is_val ? g : 0) * tile + c;
     }
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double acc[4][CPL];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) acc[k][q] = 0.0;
     for (int j = 0; j < g; ++j) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = __fma_rn(wp[q][j * ws[q]], hrow[q][j * kTile], acc[q]);
+      for (int k = 0; k < 4; ++k) {
+        const double wv = wp[k][j * ws[k]];
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) acc[k][q] = __fma_rn(wv, hrow[k][j * tile + 32 * q], acc[k][q]);
+      }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int a = a0 + q * kWarps;
-      if (a < 3 * n) buf[a * kTile + c] = kt::dadd(acc[q], P[o.bp2 + a]);
-      else if (a == 3 * n) val[c] = kt::dadd(acc[q], P[o.bv2]);
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) outv[pass][k][q] = acc[k][q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    const int a0 = w + pass * 4 * kWarps;
+    if (a0 >= na) break;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int a = a0 + k * kWarps;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        if (a < 3 * n) act[a * tile + c + 32 * q] = kt::dadd(outv[pass][k][q], P[o.bp2 + a]);
+        else if (a == 3 * n) val[c + 32 * q] = kt::dadd(outv[pass][k][q], P[o.bv2]);
+      }
     }
   }
   __syncthreads();
@@ -207,14 +251,13 @@ __device__ __forceinline__ Knob3 softmax3(double l0, double l1, double l2) {
   return r;
 }
 
-template <bool SP>
-__global__ void __launch_bounds__(kThreads, 1)
-rollout_kernel(const __grid_constant__ RolloutLaunch L) {
-  constexpr bool smem_params = SP;
+template <bool SP, int CPL>
+__global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_constant__ RolloutLaunch L) {
+  constexpr int tile = 32 * CPL;
   extern __shared__ __align__(16) double sm[];
   int ti = 0;
   while (ti + 1 < L.num_tasks && L.cta_base[ti + 1] <= (int)blockIdx.x) ++ti;
-  const CtaWork wk{ti, (int64_t)((int)blockIdx.x - L.cta_base[ti]) * kTile};
+  const int64_t first = (int64_t)((int)blockIdx.x - L.cta_base[ti]) * tile;
   const RolloutTask* tkp = &L.task[ti];
   const int n = tkp->n, h = tkp->h, g = tkp->g, T = tkp->T;
   const int64_t E = tkp->E, eoff = tkp->episode_offset;
@@ -229,67 +272,82 @@ rollout_kernel(const __grid_constant__ RolloutLaunch L) {
     for (int i = threadIdx.x; i < o.total; i += kThreads) sm[i] = P[i];
     P = sm;
   }
-  double* act = sm + (smem_params ? ((o.total + 1) & ~1) : 0);
-  double* buf = act + (h > 2 * g ? h : 2 * g) * kTile;
-  double* val = buf + 3 * n * kTile;
-  uint16_t* cfg = reinterpret_cast<uint16_t*>(val + kTile);  // [d][c]
-  int* card = reinterpret_cast<int*>(cfg + n * kTile);
+  double* act = sm + (SP ? ((o.total + 1) & ~1) : 0);  // 16-byte aligned (double2 loads)
+  double* xb = act + act_rows(n, h, g) * tile;
+  double* val = xb + n * tile;
+  uint16_t* cfg = reinterpret_cast<uint16_t*>(val + tile);  // [d][e]
+  int* card = reinterpret_cast<int*>(cfg + n * tile);
   const int c = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t e = wk.first + c;
-  const bool live = e < E;
   if (threadIdx.x < n) card[threadIdx.x] = tkp->card[threadIdx.x];
   // initial configurations (trajectory row 0)
-  for (int d = w; d < n; d += kWarps) {
-    uint16_t v = 0;
-    if (live) {
-      v = tkp->init_idx[e * n + d];
-      out_idx[(e * (T + 1)) * n + d] = v;
+  for (int d = w; d < n; d += kWarps)
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int64_t e = first + c + 32 * q;
+      uint16_t v = 0;
+      if (e < E) {
+        v = tkp->init_idx[e * n + d];
+        out_idx[(e * (T + 1)) * n + d] = v;
+      }
+      cfg[d * tile + c + 32 * q] = v;
     }
-    cfg[d * kTile + c] = v;
-  }
   __syncthreads();
   for (int t = 0; t < T; ++t) {
     // ---- 0: features x = idx / (card - 1) (design_space.cpp:195-197)
     for (int d = w; d < n; d += kWarps) {
       const int cd = card[d];
-      buf[d * kTile + c] = cd > 1 ? kt::ddiv((double)cfg[d * kTile + c], (double)(cd - 1)) : 0.0;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int e = c + 32 * q;
+        xb[d * tile + e] = cd > 1 ? kt::ddiv((double)cfg[d * tile + e], (double)(cd - 1)) : 0.0;
+      }
     }
     __syncthreads();
-    forward_tile(P, o, n, h, g, act, buf, val);
+    forward_tile<CPL>(P, o, n, h, g, act, xb, val);
     // ---- D: per knob: log-softmax, counter-RNG draw, inverse CDF, saturating move
     for (int d = w; d < n; d += kWarps) {
-      const Knob3 k3 = softmax3(buf[(3 * d) * kTile + c], buf[(3 * d + 1) * kTile + c],
-                                buf[(3 * d + 2) * kTile + c]);
-      const uint64_t ge = (uint64_t)(eoff + e);
-      const double u = kt::hash01(seed, (ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n + (uint64_t)d);
-      const int a = u < k3.p[0] ? 0 : (u < kt::dadd(k3.p[0], k3.p[1]) ? 1 : 2);
-      int v = (int)cfg[d * kTile + c] + (a - 1);
       const int cd = card[d];
-      v = v < 0 ? 0 : (v > cd - 1 ? cd - 1 : v);
-      cfg[d * kTile + c] = (uint16_t)v;
-      buf[(3 * d) * kTile + c] = a == 0 ? k3.lp[0] : (a == 1 ? k3.lp[1] : k3.lp[2]);
-      if (live) {
-        if (out_act) out_act[(e * T + t) * n + d] = (int8_t)(a - 1);
-        out_idx[(e * (T + 1) + t + 1) * n + d] = (uint16_t)v;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const int el = c + 32 * q;
+        const int64_t e = first + el;
+        const Knob3 k3 = softmax3(act[(3 * d) * tile + el], act[(3 * d + 1) * tile + el],
+                                  act[(3 * d + 2) * tile + el]);
+        const uint64_t ge = (uint64_t)(eoff + e);
+        const double u = kt::hash01(seed, (ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n + (uint64_t)d);
+        const int a = u < k3.p[0] ? 0 : (u < kt::dadd(k3.p[0], k3.p[1]) ? 1 : 2);
+        int v = (int)cfg[d * tile + el] + (a - 1);
+        v = v < 0 ? 0 : (v > cd - 1 ? cd - 1 : v);
+        cfg[d * tile + el] = (uint16_t)v;
+        act[(3 * d) * tile + el] = a == 0 ? k3.lp[0] : (a == 1 ? k3.lp[1] : k3.lp[2]);
+        if (e < E) {
+          if (out_act) out_act[(e * T + t) * n + d] = (int8_t)(a - 1);
+          out_idx[(e * (T + 1) + t + 1) * n + d] = (uint16_t)v;
+        }
       }
     }
     __syncthreads();
     // ---- E: joint log-probability in knob order, value
-    if (w == 0 && live) {
-      double lp = 0.0;
-      for (int d = 0; d < n; ++d) lp = kt::dadd(lp, buf[(3 * d) * kTile + c]);
-      if (out_logp) out_logp[e * T + t] = lp;
-      if (out_val) out_val[e * T + t] = val[c];
+    if (w < CPL) {
+      const int el = c + 32 * w;
+      const int64_t e = first + el;
+      if (e < E) {
+        double lp = 0.0;
+        for (int d = 0; d < n; ++d) lp = kt::dadd(lp, act[(3 * d) * tile + el]);
+        if (out_logp) out_logp[e * T + t] = lp;
+        if (out_val) out_val[e * T + t] = val[el];
+      }
     }
     __syncthreads();
   }
 }
 
-// ActorCritic::forward over arbitrary fp64 states.
+// ActorCritic::forward over arbitrary fp64 states (32-state tiles).
 __global__ void __launch_bounds__(kThreads, 1)
 ac_forward_kernel(const double* __restrict__ params, int n, int h, int g,
                   const double* __restrict__ states, int64_t B, double* __restrict__ log_probs,
                   double* __restrict__ probs, double* __restrict__ values, int smem_params) {
+  constexpr int tile = 32;
   extern __shared__ __align__(16) double sm[];
   const AcOff o = ac_layout(n, h, g);
   const double* P = params;
@@ -297,30 +355,29 @@ ac_forward_kernel(const double* __restrict__ params, int n, int h, int g,
     for (int i = threadIdx.x; i < o.total; i += kThreads) sm[i] = params[i];
     P = sm;
   }
-  double* act = sm + (smem_params ? ((o.total + 1) & ~1) : 0);  // 16-byte aligned (double2 loads)
-  double* buf = act + (h > 2 * g ? h : 2 * g) * kTile;
-  double* val = buf + 3 * n * kTile;
+  double* act = sm + (smem_params ? ((o.total + 1) & ~1) : 0);
+  double* xb = act + act_rows(n, h, g) * tile;
+  double* val = xb + n * tile;
   const int tid = threadIdx.x;
-  for (int64_t first = (int64_t)blockIdx.x * kTile; first < B; first += (int64_t)gridDim.x * kTile) {
+  for (int64_t first = (int64_t)blockIdx.x * tile; first < B; first += (int64_t)gridDim.x * tile) {
     __syncthreads();
-    for (int item = tid; item < kTile * n; item += kThreads) {
+    for (int item = tid; item < tile * n; item += kThreads) {
       const int c = item / n, d = item % n;
-      buf[d * kTile + c] = first + c < B ? states[(first + c) * n + d] : 0.0;
+      xb[d * tile + c] = first + c < B ? states[(first + c) * n + d] : 0.0;
     }
     __syncthreads();
-    forward_tile(P, o, n, h, g, act, buf, val);
-    for (int item = tid; item < kTile * n; item += kThreads) {
-      const int c = item % kTile, d = item / kTile;
+    forward_tile<1>(P, o, n, h, g, act, xb, val);
+    for (int item = tid; item < tile * n; item += kThreads) {
+      const int c = item % tile, d = item / tile;
       const int64_t b = first + c;
       if (b >= B) continue;
-      const Knob3 k3 = softmax3(buf[(3 * d) * kTile + c], buf[(3 * d + 1) * kTile + c],
-                                buf[(3 * d + 2) * kTile + c]);
+      const Knob3 k3 = softmax3(act[(3 * d) * tile + c], act[(3 * d + 1) * tile + c], act[(3 * d + 2) * tile + c]);
       for (int a = 0; a < 3; ++a) {
         if (log_probs) log_probs[b * 3 * n + 3 * d + a] = k3.lp[a];
         if (probs) probs[b * 3 * n + 3 * d + a] = k3.p[a];
       }
     }
-    if (values && tid < kTile && first + tid < B) values[first + tid] = val[tid];
+    if (values && tid < tile && first + tid < B) values[first + tid] = val[tid];
   }
 }
 
@@ -330,7 +387,8 @@ __global__ void debug_math_kernel(int op, const double* __restrict__ x, int64_t 
     out[i] = op == 0 ? kt::kt_exp(x[i]) : (op == 1 ? kt::kt_log(x[i]) : kt::kt_tanh(x[i]));
 }
 
-bool fits_smem(int n, int h, int g) { return rollout_smem_bytes(n, h, g, true) <= 227 * 1024; }
+bool fits_smem(int n, int h, int g, int cpl = 1) { return rollout_smem_bytes(n, h, g, true, cpl) <= 227 * 1024; }
+
 
 void check_dims(int n, int h, int g) {
   if (n < 1 || n > kt::kMaxKnobs) kt::fail(KTUNE_ERR_CONFIG, "actor-critic: 1 <= num_knobs <= 32 on the device path");
@@ -409,9 +467,9 @@ int ktune_ac_forward(ktune_ctx* ctx, const ktune_ac* ac, const double* states, i
     double* d_p = probs ? (double*)kt::out_buf(ctx, kt::WS_OUT1, probs, sizeof(double) * B * 3 * n, dev) : nullptr;
     double* d_v = values ? (double*)kt::out_buf(ctx, kt::WS_OUT2, values, sizeof(double) * B, dev) : nullptr;
     const bool sp = fits_smem(n, ac->h, ac->g);
-    const size_t smem = rollout_smem_bytes(n, ac->h, ac->g, sp);
+    const size_t smem = rollout_smem_bytes(n, ac->h, ac->g, sp, 1);
     KT_CUDA(cudaFuncSetAttribute(ac_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int grid = (int)std::min<int64_t>(kt::ceil_div(B, kTile), kt::sm_count(ctx));
+    const int grid = (int)std::min<int64_t>(kt::ceil_div(B, 32), kt::sm_count(ctx));
     ac_forward_kernel<<<grid, kThreads, smem, ctx->stream>>>(ac->d_params, n, ac->h, ac->g, d_s, B, d_lp,
                                                              d_p, d_v, sp ? 1 : 0);
     kt::check_launch(ctx, "ac_forward");
@@ -441,7 +499,6 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     if (num_tasks == 0) return;
     const bool dev = flags & KTUNE_F_DEVICE;
     std::vector<RolloutTask> dt(num_tasks);
-    std::vector<CtaWork> work;
     // device buffers for host-pointer calls
     struct HostIo {
       const uint16_t* d_init;
@@ -496,15 +553,20 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       r.actions = h.d_act;
       r.logp = h.d_logp;
       r.value = h.d_val;
-      for (int64_t f = 0; f < E; f += kTile) work.push_back({k, f});
     }
-    // one launch config for all tasks: smem sized for the largest task
+    // one launch config for all tasks: smem sized for the largest task; 64-episode
+    // tiles (2 per lane) when they fit, else 32
+    int cpl = 2;
+    for (int k = 0; k < num_tasks; ++k)
+      if (!smem_params || rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, true, 2) > 227 * 1024 || 2 * dt[k].g > 128)
+        cpl = 1;
     size_t smem = 0;
     for (int k = 0; k < num_tasks; ++k)
-      smem = std::max(smem, rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, smem_params));
+      smem = std::max(smem, rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, smem_params, cpl));
     if (smem > 227 * 1024) kt::fail(KTUNE_ERR_CONFIG, "rollout: agent too large for shared memory");
-    if (!work.empty()) {
-      auto kern = smem_params ? rollout_kernel<true> : rollout_kernel<false>;
+    {
+      auto kern = smem_params ? (cpl == 2 ? rollout_kernel<true, 2> : rollout_kernel<true, 1>)
+                              : rollout_kernel<false, 1>;
       KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
       for (int t0 = 0; t0 < num_tasks; t0 += kMaxTasksPerLaunch) {  // grouped launches
@@ -514,7 +576,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         for (int q = 0; q < L.num_tasks; ++q) {
           L.task[q] = dt[t0 + q];
           L.cta_base[q] = ctas;
-          ctas += (int)kt::ceil_div(dt[t0 + q].E, kTile);
+          ctas += (int)kt::ceil_div(dt[t0 + q].E, 32 * cpl);
         }
         L.cta_base[L.num_tasks] = ctas;
         if (ctas > 0) kern<<<(unsigned)ctas, kThreads, smem, ctx->stream>>>(L);

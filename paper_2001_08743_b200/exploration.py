@@ -119,12 +119,15 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
             import torch
             init = t.init_idx.to(torch.uint16).contiguous() if t.init_idx.dtype != torch.uint16 else t.init_idx.contiguous()
             E = init.shape[0]
-            mk = lambda shape, dt: torch.empty(shape, dtype=dt, device=init.device)
-            o = dict(idx=mk((E, T + 1, D), torch.uint16),
-                     score=mk((E, T + 1), torch.float64) if t.cost_model is not None else None,
-                     actions=mk((E, T, D), torch.int8) if t.want_trajectory else None,
-                     logp=mk((E, T), torch.float64) if t.want_trajectory else None,
-                     value=mk((E, T), torch.float64) if t.want_trajectory else None)
+            if host_out is not None:  # caller-provided persistent device buffers
+                o = host_out[i]
+            else:
+                mk = lambda shape, dt: torch.empty(shape, dtype=dt, device=init.device)
+                o = dict(idx=mk((E, T + 1, D), torch.uint16),
+                         score=mk((E, T + 1), torch.float64) if t.cost_model is not None else None,
+                         actions=mk((E, T, D), torch.int8) if t.want_trajectory else None,
+                         logp=mk((E, T), torch.float64) if t.want_trajectory else None,
+                         value=mk((E, T), torch.float64) if t.want_trajectory else None)
             pp = lambda a: None if a is None else C.c_void_p(a.data_ptr())
             init_p = C.c_void_p(init.data_ptr())
             keep.append(init)
