@@ -262,7 +262,8 @@ def main():
     from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
     from paper_2001_08743_b200.workloads import encode
 
-    ctx = Context(local)
+    from paper_2001_08743_b200.distributed import create_context
+    ctx = create_context(local, rank, world)  # NCCL communicator for the k-means all-gathers when world > 1
     stream = torch.cuda.Stream()  # a real stream handle shared by torch and libktune_cuda
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
@@ -359,7 +360,7 @@ def main():
         ctx.set_stream(stream.cuda_stream)
 
     kmeans = None
-    if not args.no_kmeans and rank == 0:
+    if not args.no_kmeans:  # every rank participates (sharded assignment + NCCL all-gather)
         try:
             kmeans = kmeans_secondary(ctx, args, cpu=(world == 1 and not args.no_cpu))
         except Exception as ex:  # reported, not hidden

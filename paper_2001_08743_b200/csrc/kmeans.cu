@@ -355,7 +355,8 @@ __global__ void __launch_bounds__(kBT) assign_kernel(KtSpaceParams sp, int lut_t
                                                      int32_t* __restrict__ asg,
                                                      double* __restrict__ d2,
                                                      double* __restrict__ chunk_sum,
-                                                     unsigned long long* __restrict__ changed) {
+                                                     unsigned long long* __restrict__ changed,
+                                                     int64_t chunk0) {
   extern __shared__ double sdyn[];
   __shared__ double red[32];
   const int D = sp.D;
@@ -364,7 +365,8 @@ __global__ void __launch_bounds__(kBT) assign_kernel(KtSpaceParams sp, int lut_t
   for (int i = threadIdx.x; i < k * D; i += blockDim.x) s_cent[i] = cent[i];
   const double* lut = stage_lut(sp, s_lut, lut_total);
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  const int64_t cidx = chunk0 + blockIdx.x;  // this rank's shard starts at chunk chunk0
+  const int64_t base = cidx * kChunk;
   double part = 0.0;
   int nchg = 0;
   for (int j = 0; j < kChunk / kBT; ++j) {
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(kBT) assign_kernel(KtSpaceParams sp, int lut_t
     }
   }
   const double s = block_sum(part, red);
-  if (threadIdx.x == 0) chunk_sum[blockIdx.x] = s;
+  if (threadIdx.x == 0) chunk_sum[cidx] = s;
   if (prev) {
     for (int o = 16; o > 0; o >>= 1) nchg += __shfl_down_sync(0xffffffff, nchg, o);
     if ((threadIdx.x & 31) == 0 && nchg) atomicAdd(changed, (unsigned long long)nchg);
@@ -981,6 +983,8 @@ struct KMeans {
   int max_segs;
   int32_t* csb;       // per-cluster segment bases [k+1]
   int32_t* seqcnt;    // segments summed sequentially (stat)
+  int world = 1, rank = 0;
+  int64_t shard_chunks = 0, cap = 0;
 
   void setup(ktune_ctx* c, const ktune_space* s, const IdxT* p, int64_t n) {
     ctx = c;
@@ -990,15 +994,21 @@ struct KMeans {
     D = s->D;
     lut_total = s->lut_total;
     nchunks = kt::ceil_div(N, kChunk);
+    // multi-GPU: rank r assigns chunks [r*shard_chunks, (r+1)*shard_chunks); the
+    // per-point results are all-gathered so every rank holds the full state.
+    world = ctx->world;
+    rank = ctx->rank;
+    shard_chunks = kt::ceil_div(nchunks, world);
+    cap = (int64_t)world * shard_chunks * kChunk;
     lut_smem = sizeof(double) * lut_total;
     d2 = (double*)ctx->dev(kt::WS_D2, sizeof(double) * N);
-    chunk = (double*)ctx->dev(kt::WS_BLOCK, sizeof(double) * nchunks);
+    chunk = (double*)ctx->dev(kt::WS_BLOCK, sizeof(double) * world * shard_chunks);
     scratch = (double*)ctx->dev(kt::WS_BLOCK2, sizeof(double) * nchunks);
     kst = (KppState*)ctx->dev(kt::WS_KPP, sizeof(KppState));
-    asg_a = (int32_t*)ctx->dev(kt::WS_ASSIGN, sizeof(int32_t) * N);
-    asg_b = (int32_t*)ctx->dev(kt::WS_ASSIGN2, sizeof(int32_t) * N);
-    d2_a = (double*)ctx->dev(kt::WS_D2B, sizeof(double) * N * 2);
-    d2_b = d2_a + N;
+    asg_a = (int32_t*)ctx->dev(kt::WS_ASSIGN, sizeof(int32_t) * cap);
+    asg_b = (int32_t*)ctx->dev(kt::WS_ASSIGN2, sizeof(int32_t) * cap);
+    d2_a = (double*)ctx->dev(kt::WS_D2B, sizeof(double) * cap * 2);
+    d2_b = d2_a + cap;
     members = (int32_t*)ctx->dev(kt::WS_MEMBERS, sizeof(int32_t) * N);
     blockcounts = (int32_t*)ctx->dev(kt::WS_SCRATCH, sizeof(int32_t) * nchunks * kt::kMaxK);
     counts = (int32_t*)ctx->dev(kt::WS_SCRATCH2, sizeof(int32_t) * (4 * kt::kMaxK + 16));
@@ -1046,10 +1056,28 @@ struct KMeans {
                 unsigned long long* changed_out) {
     KT_CUDA(cudaMemsetAsync(ull, 0, 16, s()));
     const size_t smem = sizeof(double) * (k * D) + lut_smem;
-    kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
-    assign_kernel<IdxT><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent, k, prev, asg,
-                                                        dd, chunk, ull);
-    kt::check_launch(ctx, "assign");
+    if (world == 1) {
+      kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
+      assign_kernel<IdxT><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent, k, prev, asg,
+                                                          dd, chunk, ull, 0);
+      kt::check_launch(ctx, "assign");
+    } else {
+      const int64_t c0 = (int64_t)rank * shard_chunks;
+      const int64_t nloc = std::max<int64_t>(0, std::min<int64_t>(nchunks, c0 + shard_chunks) - c0);
+      if (nloc > 0) {
+        kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
+        assign_kernel<IdxT><<<(unsigned)nloc, kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent, k, prev,
+                                                                asg, dd, chunk, ull, c0);
+        kt::check_launch(ctx, "assign");
+      }
+      if (nloc < shard_chunks)  // zero the padding chunks of the last shard
+        KT_CUDA(cudaMemsetAsync(chunk + c0 + nloc, 0, sizeof(double) * (shard_chunks - nloc), s()));
+      const int64_t S = shard_chunks * kChunk;
+      kt::allgather(ctx, asg + rank * S, asg, sizeof(int32_t) * S);
+      kt::allgather(ctx, dd + rank * S, dd, sizeof(double) * S);
+      kt::allgather(ctx, chunk + c0, chunk, sizeof(double) * shard_chunks);
+      kt::allreduce_sum(ctx, ull, 1, false);
+    }
     sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk, nchunks, dscal);
     kt::check_launch(ctx, "sum_chunks");
     struct {
