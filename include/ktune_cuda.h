@@ -218,6 +218,14 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
  * row numbers in rank order; *out_n = count. Host pointers. */
 int ktune_make_candidate_set(ktune_ctx* ctx, const uint64_t* ids, const double* pred, int64_t n,
                              int64_t* out_rows, int64_t* out_n);
+/* Device version over knob-index rows (e.g. a rollout trajectory, uint16 n x D):
+ * ids computed on the device (design_space.cpp:158-167), dedup keeping the
+ * first occurrence, rank by (pred desc, id asc) via stable radix sorts.
+ * out_rows / out_ids (may be NULL) need capacity n; *out_n = kept count.
+ * Honours KTUNE_F_DEVICE. */
+int ktune_candidates_from_rows(ktune_ctx* ctx, const ktune_space* space, const uint16_t* idx,
+                               const double* pred, int64_t n, int64_t* out_rows, uint64_t* out_ids,
+                               int64_t* out_n, int flags);
 
 /* ------------------------------------------------------------------ k-means
  * kmeans_run (sampling.hpp:37-38, sampling.cpp:157-175) over lattice points

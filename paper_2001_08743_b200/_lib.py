@@ -102,6 +102,7 @@ SIGNATURES = {
     "ktune_ac_forward": (C.c_int, [P, P, P, i64, P, P, P, C.c_int]),
     "ktune_rollout": (C.c_int, [P, C.c_int, C.POINTER(RolloutTaskC), C.c_int32, C.c_int]),
     "ktune_make_candidate_set": (C.c_int, [P, P, P, i64, P, C.POINTER(i64)]),
+    "ktune_candidates_from_rows": (C.c_int, [P, P, P, P, i64, P, P, C.POINTER(i64), C.c_int]),
     "ktune_kmeans_run": (C.c_int, [P, P, P, C.c_int, i64, C.c_int, u64, C.c_int, C.c_int,
                                    C.POINTER(KmeansOutC), C.c_int]),
     "ktune_adaptive_sweep": (C.c_int, [P, P, P, C.c_int, P, i64, C.POINTER(SamplingParamsC), u64,

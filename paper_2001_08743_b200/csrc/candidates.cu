@@ -1,0 +1,118 @@
+// make_candidate_set on the device (sampling.cpp:16-31):
+//   ids = id_of(row) (design_space.cpp:158-167, mixed radix, last knob fastest)
+//   dedup by id, FIRST occurrence wins  -> stable radix sort of (id, row) by id,
+//                                          keep the head of every equal-id run
+//   rank by (predicted desc, id asc)    -> the kept rows are already in id order;
+//                                          a stable radix sort on the descending
+//                                          fitness key keeps id order within ties
+// Radix sorts: CUB (CUDA toolkit CCCL) DeviceRadixSort — library primitive.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "internal.cuh"
+
+namespace {
+
+__global__ void ids_kernel(KtSpaceParams sp, const uint16_t* __restrict__ idx, int64_t n,
+                           uint64_t* __restrict__ ids, int64_t* __restrict__ rows) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t id = 0;
+    for (int d = 0; d < sp.D; ++d) id = id * (uint64_t)sp.card[d] + (uint64_t)idx[i * sp.D + d];
+    ids[i] = id;
+    rows[i] = i;
+  }
+}
+
+__global__ void head_flags_kernel(const uint64_t* __restrict__ ids, int64_t n, uint8_t* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || ids[i] != ids[i - 1]) ? 1 : 0;
+}
+
+// Descending order on doubles as an ascending unsigned key.
+__device__ __forceinline__ uint64_t desc_key(double x) {
+  if (x == 0.0) x = 0.0;  // -0.0 ties with +0.0 as in the reference comparator
+  uint64_t b = (uint64_t)__double_as_longlong(x);
+  b = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // ascending total order
+  return ~b;                                          // descending
+}
+
+__global__ void rank_keys_kernel(const int64_t* __restrict__ rows, const double* __restrict__ pred, int64_t m,
+                                 uint64_t* __restrict__ keys) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = desc_key(pred[rows[i]]);
+}
+
+__global__ void gather_ids_kernel(const int64_t* __restrict__ rows, const uint64_t* __restrict__ ids_by_row,
+                                  int64_t m, uint64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ids_by_row[rows[i]];
+}
+
+}  // namespace
+
+extern "C" int ktune_candidates_from_rows(ktune_ctx* ctx, const ktune_space* space, const uint16_t* idx,
+                                          const double* pred, int64_t n, int64_t* out_rows, uint64_t* out_ids,
+                                          int64_t* out_n, int flags) {
+  return kt_guard(ctx, [&] {
+    if (n < 0) kt::fail(KTUNE_ERR_CONFIG, "make_candidate_set: negative count");
+    const bool dev = flags & KTUNE_F_DEVICE;
+    if (n == 0) {
+      *out_n = 0;
+      return;
+    }
+    if (n > (int64_t)INT32_MAX) kt::fail(KTUNE_ERR_CONFIG, "make_candidate_set: at most 2^31-1 rows per call");
+    const int D = space->D;
+    cudaStream_t s = ctx->stream;
+    const uint16_t* d_idx = (const uint16_t*)kt::stage_in(ctx, kt::WS_IN0, idx, sizeof(uint16_t) * n * D, dev);
+    const double* d_pred = (const double*)kt::stage_in(ctx, kt::WS_IN1, pred, sizeof(double) * n, dev);
+    // scratch: ids_row[n] (id per original row), keys/vals ping-pong, flags
+    char* base = (char*)ctx->dev(kt::WS_SCRATCH, (size_t)n * (8 * 5 + 8 + 1) + 256);
+    uint64_t* ids_row = (uint64_t*)base;
+    uint64_t* k0 = ids_row + n;
+    uint64_t* k1 = k0 + n;
+    int64_t* v0 = (int64_t*)(k1 + n);
+    int64_t* v1 = v0 + n;
+    int64_t* kept = v1 + n;
+    uint8_t* flag = (uint8_t*)(kept + n);
+    int64_t* d_count = (int64_t*)ctx->dev(kt::WS_VALID, 64);
+    const int th = 256;
+    const int grid = (int)std::min<int64_t>(kt::ceil_div(n, th), (int64_t)kt::sm_count(ctx) * 16);
+    ids_kernel<<<grid, th, 0, s>>>(space->params, d_idx, n, ids_row, v0);
+    KT_CUDA(cudaMemcpyAsync(k0, ids_row, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, s));
+    // 1) stable sort (id, row) by id
+    cub::DoubleBuffer<uint64_t> keys(k0, k1);
+    cub::DoubleBuffer<int64_t> vals(v0, v1);
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, (int)n, 0, 64, s);
+    void* d_tmp = ctx->dev(kt::WS_SCRATCH2, tmp + 256);
+    KT_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp, keys, vals, (int)n, 0, 64, s));
+    // 2) first occurrence of every id
+    head_flags_kernel<<<grid, th, 0, s>>>(keys.Current(), n, flag);
+    size_t tmp2 = 0;
+    cub::DeviceSelect::Flagged(nullptr, tmp2, vals.Current(), flag, kept, d_count, (int)n, s);
+    d_tmp = ctx->dev(kt::WS_SCRATCH2, std::max(tmp, tmp2) + 256);
+    KT_CUDA(cub::DeviceSelect::Flagged(d_tmp, tmp2, vals.Current(), flag, kept, d_count, (int)n, s));
+    int64_t m = 0;
+    KT_CUDA(cudaMemcpyAsync(&m, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    KT_CUDA(cudaStreamSynchronize(s));
+    // 3) stable sort of the id-ordered kept rows by descending predicted fitness
+    rank_keys_kernel<<<grid, th, 0, s>>>(kept, d_pred, m, k0);
+    cub::DoubleBuffer<uint64_t> keys2(k0, k1);
+    cub::DoubleBuffer<int64_t> vals2(kept, v0);
+    size_t tmp3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp3, keys2, vals2, (int)m, 0, 64, s);
+    d_tmp = ctx->dev(kt::WS_SCRATCH2, std::max(std::max(tmp, tmp2), tmp3) + 256);
+    KT_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp3, keys2, vals2, (int)m, 0, 64, s));
+    int64_t* d_rows = (int64_t*)kt::out_buf(ctx, kt::WS_OUT0, out_rows, sizeof(int64_t) * m, dev);
+    KT_CUDA(cudaMemcpyAsync(d_rows, vals2.Current(), sizeof(int64_t) * m, cudaMemcpyDeviceToDevice, s));
+    if (out_ids) {
+      uint64_t* d_ids = (uint64_t*)kt::out_buf(ctx, kt::WS_OUT1, out_ids, sizeof(uint64_t) * m, dev);
+      gather_ids_kernel<<<grid, th, 0, s>>>(d_rows, ids_row, m, d_ids);
+      kt::stage_out(ctx, out_ids, d_ids, sizeof(uint64_t) * m, dev);
+    }
+    kt::check_launch(ctx, "make_candidate_set", 6);
+    kt::stage_out(ctx, out_rows, d_rows, sizeof(int64_t) * m, dev);
+    KT_CUDA(cudaStreamSynchronize(s));
+    *out_n = m;
+  });
+}

@@ -66,6 +66,33 @@ def make_candidate_set(space: Space, idx, predicted, ids=None) -> CandidateSet:
     return CandidateSet(idx[rows], ids[rows], pred[rows])
 
 
+def candidates_from_rows(space: Space, idx, predicted):
+    """make_candidate_set on the GPU over knob-index rows (e.g. a rollout trajectory).
+
+    Host arrays -> host CandidateSet; CUDA tensors -> (rows, ids) CUDA tensors."""
+    if hasattr(idx, "is_cuda") and idx.is_cuda:
+        import torch
+        n = idx.numel() // space.D
+        rows = torch.empty(n, dtype=torch.int64, device=idx.device)
+        ids = torch.empty(n, dtype=torch.uint64, device=idx.device)
+        m = C.c_int64()
+        space.ctx.check(L.lib().ktune_candidates_from_rows(
+            space.ctx.h, space.h, C.c_void_p(idx.data_ptr()), C.c_void_p(predicted.data_ptr()), n,
+            C.c_void_p(rows.data_ptr()), C.c_void_p(ids.data_ptr()), C.byref(m), L.F_DEVICE))
+        return rows[:m.value], ids[:m.value]
+    rows_idx = np.ascontiguousarray(idx, np.uint16).reshape(-1, space.D)
+    pred = np.ascontiguousarray(predicted, np.float64).reshape(-1)
+    n = len(rows_idx)
+    rows = np.zeros(n, np.int64)
+    ids = np.zeros(n, np.uint64)
+    m = C.c_int64()
+    space.ctx.check(L.lib().ktune_candidates_from_rows(
+        space.ctx.h, space.h, rows_idx.ctypes.data_as(C.c_void_p), pred.ctypes.data_as(C.c_void_p), n,
+        rows.ctypes.data_as(C.c_void_p), ids.ctypes.data_as(C.c_void_p), C.byref(m), 0))
+    rows = rows[:m.value]
+    return CandidateSet(rows_idx[rows].astype(np.int32), ids[:m.value], pred[rows])
+
+
 def _packed(space: Space, idx):
     if hasattr(idx, "is_cuda") and idx.is_cuda:
         return idx, True
