@@ -41,7 +41,7 @@ def test_rollout_to_candidates_on_device(O, ctx):
     osp, og, pm = fitted(O, sp, seed=4)
     ds = Space(sp, ctx)
     agent = ActorCritic(8, 128, 64, seed=3, ctx=ctx)
-    init = torch.from_numpy(np.zeros((256, 8), np.uint16) + 3).cuda()
+    init = torch.from_numpy(np.ones((256, 8), np.uint16)).cuda()  # every card >= 2
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     out = run_episodes_batch([RolloutTask(ds, agent, DeviceGbt(pm, ds), init, 0, 1)], 40, ctx)[0]
     rows, ids = candidates_from_rows(ds, out["idx"].reshape(-1, 8), out["score"].reshape(-1))
