@@ -198,6 +198,52 @@ __global__ void __launch_bounds__(256) gbt_predict_idx_kernel(
   }
 }
 
+// K1 fast path. Complete trees of compile-time depth; node word = (feature
+// column byte offset << 16) | t1, so a level is: LDS node, LDS idx at
+// column+offset, compare, 2n+1+right. Two configurations per thread (ILP), a
+// persistent grid over 512-config chunks, trees + knob-index columns in smem.
+constexpr int kScoreThreads = 256;
+template <class IdxT, int DEPTH>
+__global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
+    const IdxT* __restrict__ idx, int64_t B, int D, int T, const uint32_t* __restrict__ g_node,
+    const double* __restrict__ g_leaf, double base, double lr, double* __restrict__ out) {
+  constexpr int NI = (1 << DEPTH) - 1, NL = 1 << DEPTH;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* s_leaf = reinterpret_cast<double*>(smem);
+  uint32_t* s_node = reinterpret_cast<uint32_t*>(s_leaf + (size_t)T * NL);
+  int32_t* s_idx = reinterpret_cast<int32_t*>(s_node + (((size_t)T * NI + 3) & ~(size_t)3));
+  for (int i = threadIdx.x; i < T * NL; i += kScoreThreads) s_leaf[i] = g_leaf[i];
+  for (int i = threadIdx.x; i < T * NI; i += kScoreThreads) s_node[i] = g_node[i];
+  __syncthreads();
+  const unsigned char* col0 = reinterpret_cast<const unsigned char*>(s_idx + threadIdx.x);
+  const unsigned char* col1 = reinterpret_cast<const unsigned char*>(s_idx + D * kScoreThreads + threadIdx.x);
+  for (int64_t c0 = (int64_t)blockIdx.x * 2 * kScoreThreads; c0 < B; c0 += (int64_t)gridDim.x * 2 * kScoreThreads) {
+    const int64_t i0 = c0 + threadIdx.x, i1 = i0 + kScoreThreads;
+    for (int d = 0; d < D; ++d) {  // transposed columns: thread-private, conflict-free
+      s_idx[d * kScoreThreads + threadIdx.x] = i0 < B ? (int32_t)idx[i0 * D + d] : 0;
+      s_idx[(D + d) * kScoreThreads + threadIdx.x] = i1 < B ? (int32_t)idx[i1 * D + d] : 0;
+    }
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll 2
+    for (int t = 0; t < T; ++t) {
+      const uint32_t* tn = s_node + t * NI;
+      int n0 = 0, n1 = 0;
+#pragma unroll
+      for (int l = 0; l < DEPTH; ++l) {
+        const uint32_t w0 = tn[n0], w1 = tn[n1];
+        const int v0 = *reinterpret_cast<const int32_t*>(col0 + (w0 >> 16));
+        const int v1 = *reinterpret_cast<const int32_t*>(col1 + (w1 >> 16));
+        n0 = 2 * n0 + 1 + (v0 >= (int)(w0 & 0xFFFFu) ? 1 : 0);
+        n1 = 2 * n1 + 1 + (v1 >= (int)(w1 & 0xFFFFu) ? 1 : 0);
+      }
+      s0 = kt::dadd(s0, s_leaf[t * NL + (n0 - NI)]);
+      s1 = kt::dadd(s1, s_leaf[t * NL + (n1 - NI)]);
+    }
+    if (i0 < B) out[i0] = kt::dadd(base, kt::dmul(lr, s0));
+    if (i1 < B) out[i1] = kt::dadd(base, kt::dmul(lr, s1));
+  }
+}
+
 // fp64 feature rows (generic CostModel::predict(MatrixXd) seam).
 __global__ void __launch_bounds__(256) gbt_predict_feat_kernel(
     const double* __restrict__ x, int64_t B, int F, int T, int depth,
@@ -262,6 +308,38 @@ void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_id
   }
   const int ni = (1 << g->depth) - 1, nl = 1 << g->depth;
   const size_t tree_bytes = (size_t)g->num_trees * (ni * 4 + nl * 8);
+  if (g->d_inode_pk) {  // K1 fast path
+    const size_t smem = tree_bytes + 16 + (size_t)2 * g->D * kScoreThreads * 4;
+    if (smem <= 200 * 1024) {
+      const int per_sm = std::max(1, std::min(8, (int)((220 * 1024) / smem)));
+      const int grid = (int)std::min<int64_t>(ceil_div(B, 2 * kScoreThreads), (int64_t)sm_count(ctx) * per_sm);
+      kt::ProfScope prof(ctx, KTUNE_STAT_GBT_NS);
+#define KT_SCORE(T_, DEP)                                                                                    \
+  {                                                                                                          \
+    auto kern = gbt_score_kernel<T_, DEP>;                                                                   \
+    KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
+    kern<<<grid, kScoreThreads, smem, ctx->stream>>>((const T_*)d_idx, B, g->D, g->num_trees, g->d_inode_pk, \
+                                                     g->d_leaf, g->base, g->lr, d_out);                      \
+  }
+#define KT_SCORE_D(T_)                         \
+  switch (g->depth) {                          \
+    case 0: KT_SCORE(T_, 0) break;             \
+    case 1: KT_SCORE(T_, 1) break;             \
+    case 2: KT_SCORE(T_, 2) break;             \
+    case 3: KT_SCORE(T_, 3) break;             \
+    case 4: KT_SCORE(T_, 4) break;             \
+    case 5: KT_SCORE(T_, 5) break;             \
+    case 6: KT_SCORE(T_, 6) break;             \
+    case 7: KT_SCORE(T_, 7) break;             \
+    default: KT_SCORE(T_, 8) break;            \
+  }
+      if (idx_bytes == 1) KT_SCORE_D(uint8_t) else KT_SCORE_D(uint16_t)
+#undef KT_SCORE_D
+#undef KT_SCORE
+      check_launch(ctx, "gbt_score");
+      return;
+    }
+  }
   const size_t idx_bytes_smem = (size_t)threads * g->D * 4;
   const bool use_smem = tree_bytes + idx_bytes_smem <= 200 * 1024;
   const size_t smem = (use_smem ? tree_bytes : 0) + idx_bytes_smem;
@@ -378,6 +456,7 @@ int ktune_gbt_create(ktune_ctx* ctx, const ktune_space* space, int num_features,
     if (g->complete) {
       const int ni = (1 << depth) - 1, nl = 1 << depth;
       std::vector<uint32_t> inode_idx((size_t)num_trees * ni + 1, kAlwaysLeft);
+      std::vector<uint32_t> inode_pk((size_t)num_trees * ni + 1, 0xFFFFu);  // always left (idx < 65535)
       std::vector<int32_t> inode_feat((size_t)num_trees * ni + 1, 0);
       std::vector<double> inode_thr((size_t)num_trees * ni + 1, INFINITY);
       std::vector<double> leaf((size_t)num_trees * nl);
@@ -398,6 +477,7 @@ int ktune_gbt_create(ktune_ctx* ctx, const ktune_space* space, int num_features,
           const size_t k = (size_t)t * ni + pos;
           if (tn[nd].feature < 0) {  // pad a shallow leaf: both children keep its value
             inode_idx[k] = kAlwaysLeft;
+            inode_pk[k] = 0xFFFFu;
             inode_feat[k] = 0;
             inode_thr[k] = INFINITY;
             stack.push_back({2 * pos + 1, nd});
@@ -414,6 +494,7 @@ int ktune_gbt_create(ktune_ctx* ctx, const ktune_space* space, int num_features,
               for (int i = 0; i < card; ++i)
                 if (space->lut[space->val_off[f] + i] <= thr) t1 = i + 1;
               inode_idx[k] = ((uint32_t)f << 24) | (uint32_t)t1;
+              inode_pk[k] = ((uint32_t)(f * kScoreThreads * 4) << 16) | (uint32_t)std::min(t1, 65535);
             }
             stack.push_back({2 * pos + 1, tn[nd].left});
             stack.push_back({2 * pos + 2, tn[nd].right});
@@ -421,6 +502,13 @@ int ktune_gbt_create(ktune_ctx* ctx, const ktune_space* space, int num_features,
         }
       }
       KT_CUDA(cudaMalloc(&g->d_inode_idx, sizeof(uint32_t) * inode_idx.size()));
+      bool pk_ok = space != nullptr;
+      if (space)
+        for (int d = 0; d < space->D; ++d) pk_ok = pk_ok && space->card[d] < 65535;
+      if (pk_ok) {
+        KT_CUDA(cudaMalloc(&g->d_inode_pk, sizeof(uint32_t) * inode_pk.size()));
+        KT_CUDA(cudaMemcpy(g->d_inode_pk, inode_pk.data(), sizeof(uint32_t) * inode_pk.size(), cudaMemcpyHostToDevice));
+      }
       KT_CUDA(cudaMalloc(&g->d_inode_feat, sizeof(int32_t) * inode_feat.size()));
       KT_CUDA(cudaMalloc(&g->d_inode_thr, sizeof(double) * inode_thr.size()));
       KT_CUDA(cudaMalloc(&g->d_leaf, sizeof(double) * std::max<size_t>(1, leaf.size())));
@@ -443,6 +531,7 @@ int ktune_gbt_create(ktune_ctx* ctx, const ktune_space* space, int num_features,
 int ktune_gbt_destroy(ktune_gbt* g) {
   if (!g) return KTUNE_OK;
   cudaFree(g->d_inode_idx);
+  cudaFree(g->d_inode_pk);
   cudaFree(g->d_inode_feat);
   cudaFree(g->d_inode_thr);
   cudaFree(g->d_leaf);

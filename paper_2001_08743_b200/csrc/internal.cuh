@@ -148,7 +148,8 @@ struct ktune_gbt {
   int D = 0;
   int idx_card_max = 0;
   // device arrays
-  uint32_t* d_inode_idx = nullptr;  // [T][2^depth - 1] (feature << 16) | idx threshold
+  uint32_t* d_inode_idx = nullptr;  // [T][2^depth - 1] (feature << 24) | idx threshold t1
+  uint32_t* d_inode_pk = nullptr;   // [T][2^depth - 1] (column byte offset << 16) | t1 (fast path)
   double* d_inode_thr = nullptr;    // [T][2^depth - 1] fp64 thresholds (feature path)
   int32_t* d_inode_feat = nullptr;  // [T][2^depth - 1]
   double* d_leaf = nullptr;         // [T][2^depth]
