@@ -18,6 +18,8 @@
 
 #include "device.cuh"
 #include "exactsum.cuh"
+#include "tcgen05.cuh"
+#include <cuda_fp16.h>
 #include "internal.cuh"
 
 namespace {
@@ -401,6 +403,186 @@ __global__ void __launch_bounds__(kBT) assign_kernel(KtSpaceParams sp, int lut_t
     for (int o = 16; o > 0; o >>= 1) nchg += __shfl_down_sync(0xffffffff, nchg, o);
     if ((threadIdx.x & 31) == 0 && nchg) atomicAdd(changed, (unsigned long long)nchg);
   }
+}
+
+// ------------------------------------------------------------------ assign on tcgen05 (K3 fast path)
+// Screening GEMM on the 5th-gen tensor cores: for a tile of 128 points,
+//   dot[p][c] = sum_d idx[p][d] * (2^10 * c[c][d] / (card_d - 1))
+// with A = [idx | idx] (fp16, exact for idx < 2048) and B = [hi | lo] (the
+// fp16 split of the scaled centroid coordinate), K = 32, fp32 accumulation in
+// TMEM, so dot = sum_d x_d c_d to ~2^-21. score_c = |c|^2 - 2 dot ranks the
+// clusters like the exact d2 (|x|^2 is common). A rigorous per-cluster bound
+// E_c certifies the winner; the winner's d2 is then recomputed EXACTLY in the
+// reference order (sequential over knobs, fp64, no FMA), and any uncertain
+// point falls back to the full exact scan — assignments and d2 stay bit-exact.
+constexpr int kTcPts = 128;
+constexpr int kTcK = 32;   // 2 x 16 knobs
+constexpr int kTcMaxN = 64;
+
+template <class IdxT>
+__global__ void __launch_bounds__(kTcPts) assign_tc_kernel(
+    KtSpaceParams sp, int lut_total, const IdxT* __restrict__ pts, int64_t N, const double* __restrict__ cent,
+    int k, const int32_t* __restrict__ prev, int32_t* __restrict__ asg, double* __restrict__ d2,
+    double* __restrict__ tile_sum, unsigned long long* __restrict__ counters, int64_t tile_begin,
+    int64_t tile_end) {
+  extern __shared__ __align__(128) unsigned char tsm[];
+  unsigned char* sA = tsm;                              // 128 x 32 fp16 = 8 KB
+  unsigned char* sB = sA + kTcPts * kTcK * 2;           // 64 x 32 fp16 = 4 KB
+  double* s_cent = reinterpret_cast<double*>(sB + kTcMaxN * kTcK * 2);  // k x D
+  double* s_cn2 = s_cent + kt::kMaxK * kt::kMaxKnobs;   // k
+  double* s_lut = s_cn2 + kt::kMaxK;                    // feature LUT
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tbase;
+  __shared__ double red[32];
+  const int D = sp.D, t = threadIdx.x, w = t >> 5, lane = t & 31;
+  const int NN = (k + 15) & ~15;  // MMA N (multiple of 16 for M = 128)
+  for (int i = t; i < k * D; i += kTcPts) s_cent[i] = cent[i];
+  const double* lut = stage_lut(sp, s_lut, lut_total);
+  __syncthreads();
+  // B = [hi | lo] of v = 2^10 * c / (card - 1)
+  for (int i = t; i < NN * 16; i += kTcPts) {
+    const int c = i / 16, d = i % 16;
+    __half hi = __float2half(0.f), lo = __float2half(0.f);
+    if (c < k && d < D && sp.card[d] > 1) {
+      const double v = kt::dmul(kt::ddiv(s_cent[c * D + d], (double)(sp.card[d] - 1)), 1024.0);
+      hi = __double2half(v);
+      lo = __double2half(kt::dsub(v, (double)__half2float(hi)));
+    }
+    *reinterpret_cast<__half*>(sB + kt::tc::kmajor_offset(c, d, kTcK)) = hi;
+    *reinterpret_cast<__half*>(sB + kt::tc::kmajor_offset(c, 16 + d, kTcK)) = lo;
+  }
+  if (t < k) {  // |c|^2, sequential
+    double s = 0.0;
+    for (int d = 0; d < D; ++d) s = kt::dadd(s, kt::dmul(s_cent[t * D + d], s_cent[t * D + d]));
+    s_cn2[t] = s;
+  }
+  if (w == 0) kt::tc::tmem_alloc(&tbase, 64);
+  if (t == 0) {
+    kt::tc::mbar_init(&mbar, 1);
+    kt::tc::fence_mbar_init();
+  }
+  kt::tc::fence_before();
+  __syncthreads();
+  kt::tc::fence_after();
+  const uint32_t tmem = tbase;
+  const uint32_t idesc = kt::tc::idesc_f16_f32(kTcPts, NN);
+  const double eps_rel = (double)(2 * D + 4) * 0x1.0p-23;
+  uint32_t phase = 0;
+  double part = 0.0;
+  unsigned nchg = 0, nunc = 0;
+  for (int64_t tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x) {
+    const int64_t p = tile * kTcPts + t;
+    const bool live = p < N;
+    int ix[16];
+    int sidx = 0;
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      ix[d] = (live && d < D) ? (int)pts[p * D + d] : 0;
+      sidx += ix[d];
+      const __half h = __int2half_rn(ix[d]);
+      *reinterpret_cast<__half*>(sA + kt::tc::kmajor_offset(t, d, kTcK)) = h;
+      *reinterpret_cast<__half*>(sA + kt::tc::kmajor_offset(t, 16 + d, kTcK)) = h;
+    }
+    kt::tc::fence_proxy_async();
+    kt::tc::fence_before();
+    __syncthreads();
+    kt::tc::fence_after();
+    if (t == 0) {
+#pragma unroll
+      for (int kb = 0; kb < kTcK / 16; ++kb) {
+        const uint64_t ad = kt::tc::smem_desc(kt::tc::smem_u32(sA + kb * 256), 128, (kTcK / 8) * 128);
+        const uint64_t bd = kt::tc::smem_desc(kt::tc::smem_u32(sB + kb * 256), 128, (kTcK / 8) * 128);
+        kt::tc::mma_f16(tmem, ad, bd, idesc, kb > 0);
+      }
+      kt::tc::commit(&mbar);
+    }
+    kt::tc::mbar_wait(&mbar, phase);
+    phase ^= 1;
+    kt::tc::fence_after();
+    float dotf[kTcMaxN];
+#pragma unroll
+    for (int c0 = 0; c0 < kTcMaxN; c0 += 16) {
+      if (c0 < NN) {
+        uint32_t r[16];
+        kt::tc::ld_32x32b_x16(tmem + ((uint32_t)(32 * w) << 16) + (uint32_t)c0, r);
+        kt::tc::ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dotf[c0 + j] = __uint_as_float(r[j]);
+      }
+    }
+    if (live) {
+      // screening: best score and the tightest competitor, with per-cluster bounds
+      const double abs_term = (double)sidx * 0x1.0p-35 + 1e-15;
+      double best = INFINITY, best_e = 0.0, lb_others = INFINITY;
+      int bc = 0;
+#pragma unroll
+      for (int c = 0; c < kTcMaxN; ++c) {
+        if (c < k) {
+          const double dot = (double)dotf[c] * 0x1.0p-10;
+          const double sc = s_cn2[c] - 2.0 * dot;
+          const double e = 2.0 * (eps_rel * (fabs(dot) * 1.001 + 1e-12) + abs_term) + 1e-12 +
+                           1e-15 * (s_cn2[c] + 2.0 * fabs(dot));
+          if (sc < best) {
+            if (best < INFINITY) lb_others = fmin(lb_others, best - best_e);
+            best = sc;
+            best_e = e;
+            bc = c;
+          } else {
+            lb_others = fmin(lb_others, sc - e);
+          }
+        }
+      }
+      double x[16];
+#pragma unroll
+      for (int d = 0; d < 16; ++d) x[d] = d < D ? lut[sp.lut_off[d] + ix[d]] : 0.0;
+      double bestd;
+      if (lb_others > best + best_e) {  // certified: exact d2 of the winner only
+        double tt = kt::dsub(x[0], s_cent[bc * D]);
+        bestd = kt::dmul(tt, tt);
+        for (int d = 1; d < D; ++d) {
+          tt = kt::dsub(x[d], s_cent[bc * D + d]);
+          bestd = kt::dadd(bestd, kt::dmul(tt, tt));
+        }
+      } else {  // uncertain: the full exact scan (sampling.cpp:39-54)
+        ++nunc;
+        bestd = INFINITY;
+        bc = 0;
+        for (int c = 0; c < k; ++c) {
+          double tt = kt::dsub(x[0], s_cent[c * D]);
+          double s = kt::dmul(tt, tt);
+          for (int d = 1; d < D; ++d) {
+            tt = kt::dsub(x[d], s_cent[c * D + d]);
+            s = kt::dadd(s, kt::dmul(tt, tt));
+          }
+          if (s < bestd) {
+            bestd = s;
+            bc = c;
+          }
+        }
+      }
+      asg[p] = bc;
+      d2[p] = bestd;
+      part = kt::dadd(part, bestd);
+      if (prev && prev[p] != bc) ++nchg;
+    }
+    const double ts = block_sum(live ? part : 0.0, red);
+    if (t == 0) tile_sum[tile] = ts;
+    part = 0.0;
+    kt::tc::fence_before();
+    __syncthreads();
+    kt::tc::fence_after();
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    nchg += __shfl_down_sync(0xffffffff, nchg, o);
+    nunc += __shfl_down_sync(0xffffffff, nunc, o);
+  }
+  if (lane == 0) {
+    if (nchg) atomicAdd(counters, (unsigned long long)nchg);
+    if (nunc) atomicAdd(counters + 2, (unsigned long long)nunc);
+  }
+  kt::tc::fence_before();
+  __syncthreads();
+  if (w == 0) kt::tc::tmem_dealloc(tmem, 64);
 }
 
 // ------------------------------------------------------------------ centroid update (K4)
@@ -985,6 +1167,8 @@ struct KMeans {
   int32_t* seqcnt;    // segments summed sequentially (stat)
   int world = 1, rank = 0;
   int64_t shard_chunks = 0, cap = 0;
+  double* tile_sum = nullptr;  // tcgen05 assign: per-128-point-tile loss partials
+  bool use_tc = false;
 
   void setup(ktune_ctx* c, const ktune_space* s, const IdxT* p, int64_t n) {
     ctx = c;
@@ -1015,6 +1199,10 @@ struct KMeans {
     csb = counts + 2 * kt::kMaxK + 8;
     seqcnt = csb + kt::kMaxK + 4;
     max_segs = (int)(kt::ceil_div(N, kt::xsum::kSeg) + kt::kMaxK);
+    tile_sum = (double*)ctx->dev(kt::WS_TILESUM, sizeof(double) * (size_t)world * shard_chunks * (kChunk / kTcPts));
+    use_tc = ctx->opt_kmeans_mode != 1 && D <= 16 &&
+             (size_t)lut_total * 8 + kTcPts * kTcK * 2 + kTcMaxN * kTcK * 2 + (kt::kMaxK * kt::kMaxKnobs + kt::kMaxK) * 8 <= 200 * 1024;
+    for (int d = 0; d < D; ++d) use_tc = use_tc && s->card[d] <= 2048;  // idx exact in fp16
     sorted = (IdxT*)ctx->dev(kt::WS_SORTED, sizeof(IdxT) * N * D);
     xs_approx = (double*)ctx->dev(kt::WS_XS_APPROX, sizeof(double) * (size_t)max_segs * D);
     xs_maps = (kt::xsum::SegMap*)ctx->dev(kt::WS_XS_MAPS, sizeof(kt::xsum::SegMap) * (size_t)max_segs * D);
@@ -1054,9 +1242,33 @@ struct KMeans {
   // assignment against cent; returns loss estimate; changed count if prev != null
   double assign(const double* cent, int k, const int32_t* prev, int32_t* asg, double* dd,
                 unsigned long long* changed_out) {
-    KT_CUDA(cudaMemsetAsync(ull, 0, 16, s()));
+    KT_CUDA(cudaMemsetAsync(ull, 0, 24, s()));
     const size_t smem = sizeof(double) * (k * D) + lut_smem;
-    if (world == 1) {
+    if (use_tc && k <= kTcMaxN) {
+      // tcgen05 screening + certified exact winner (this rank's chunk range)
+      const int64_t c0 = (int64_t)rank * shard_chunks;
+      const int64_t cend = std::min<int64_t>(nchunks, c0 + shard_chunks);
+      const int64_t t0 = c0 * (kChunk / kTcPts), t1 = std::min<int64_t>(kt::ceil_div(N, kTcPts), cend * (kChunk / kTcPts));
+      const size_t tsmem = kTcPts * kTcK * 2 + kTcMaxN * kTcK * 2 + (kt::kMaxK * kt::kMaxKnobs + kt::kMaxK) * 8 + lut_smem;
+      if (t1 > t0) {
+        kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
+        KT_CUDA(cudaFuncSetAttribute(assign_tc_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
+        const int grid = (int)std::min<int64_t>(t1 - t0, (int64_t)kt::sm_count(ctx) * 4);
+        assign_tc_kernel<IdxT><<<grid, kTcPts, tsmem, s()>>>(sp->params, lut_total, pts, N, cent, k, prev, asg, dd,
+                                                             tile_sum, ull, t0, t1);
+        kt::check_launch(ctx, "assign_tc");
+        sum_chunks_kernel<<<1, 1024, 0, s()>>>(tile_sum + t0, t1 - t0, dscal);
+      } else {
+        KT_CUDA(cudaMemsetAsync(dscal, 0, 8, s()));
+      }
+      if (world > 1) {
+        const int64_t S = shard_chunks * kChunk;
+        kt::allgather(ctx, asg + rank * S, asg, sizeof(int32_t) * S);
+        kt::allgather(ctx, dd + rank * S, dd, sizeof(double) * S);
+        kt::allreduce_sum(ctx, ull, 1, false);
+        kt::allreduce_sum(ctx, dscal, 1, true);
+      }
+    } else if (world == 1) {
       kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
       assign_kernel<IdxT><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent, k, prev, asg,
                                                           dd, chunk, ull, 0);
@@ -1078,23 +1290,26 @@ struct KMeans {
       kt::allgather(ctx, chunk + c0, chunk, sizeof(double) * shard_chunks);
       kt::allreduce_sum(ctx, ull, 1, false);
     }
-    sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk, nchunks, dscal);
+    if (!(use_tc && k <= kTcMaxN)) sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk, nchunks, dscal);
     kt::check_launch(ctx, "sum_chunks");
     struct {
       double loss;
       unsigned long long changed;
       int32_t seq, segs;
+      unsigned long long unc;
     } h;
     KT_CUDA(cudaMemcpyAsync(&h.loss, dscal, 8, cudaMemcpyDeviceToHost, s()));
     KT_CUDA(cudaMemcpyAsync(&h.changed, ull, 8, cudaMemcpyDeviceToHost, s()));
     KT_CUDA(cudaMemcpyAsync(&h.seq, seqcnt, 4, cudaMemcpyDeviceToHost, s()));
     KT_CUDA(cudaMemcpyAsync(&h.segs, csb + k, 4, cudaMemcpyDeviceToHost, s()));
+    KT_CUDA(cudaMemcpyAsync(&h.unc, ull + 2, 8, cudaMemcpyDeviceToHost, s()));
     KT_CUDA(cudaMemsetAsync(seqcnt, 0, 4, s()));
     KT_CUDA(cudaStreamSynchronize(s()));
     if (prev) {
       ctx->stats[KTUNE_STAT_XS_SEQUENTIAL] += h.seq;
       ctx->stats[KTUNE_STAT_XS_SEGMENTS] += (int64_t)h.segs * D;
     }
+    ctx->stats[KTUNE_STAT_ASSIGN_FALLBACKS] += (int64_t)h.unc;
     if (changed_out) *changed_out = h.changed;
     return h.loss;
   }

@@ -140,3 +140,26 @@ def test_kmeans_large_vs_oracle(O, ctx):
     assert np.array_equal(got.assignments, want["assignments"])
     assert np.array_equal(got.centroids, want["centroids"])
     assert ctx.stat(L.STAT_KPP_PICKS) == 8
+
+
+@pytest.mark.parametrize("mode", [0, 1])  # 0: tcgen05 screening (default), 1: exact SIMT scan
+@pytest.mark.parametrize("name,n,k,seed", [("synthetic16", 20000, 24, 7), ("alexnet_c3_u16", 8000, 63, 8),
+                                           ("resnet_c2", 6000, 9, 9)])
+def test_assign_paths_bit_exact(O, ctx, ref_ok, mode, name, n, k, seed):
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.sampling import kmeans_run
+    sp = SPACES[name]()
+    osp = O.OSpace(sp)
+    cidx, cids, _ = candidate_set(O, osp, n, seed)
+    ds = _space(ctx, sp)
+    ctx.set_option(L.OPT_KMEANS_MODE, mode)
+    ctx.reset_stats()
+    try:
+        got = kmeans_run(ds, cidx, k, seed, restarts=2)
+    finally:
+        ctx.set_option(L.OPT_KMEANS_MODE, 0)
+    want = O.kmeans_run(osp.encode(cidx), k, seed, restarts=2, impl="ref")
+    assert np.array_equal(got.assignments, want["assignments"])
+    assert np.array_equal(got.centroids, want["centroids"])
+    assert got.l2_loss == want["loss"]
+    print("uncertain (exact-fallback) points:", ctx.stat(L.STAT_ASSIGN_FALLBACKS))
