@@ -43,7 +43,9 @@ enum ktune_status {
 };
 
 enum ktune_flags {
-  KTUNE_F_DEVICE = 1 /* array arguments are device pointers */
+  KTUNE_F_DEVICE = 1,       /* array arguments are device pointers */
+  KTUNE_F_EXACT_ROLLOUT = 2 /* ktune_rollout: exact fp64 forward for every config-step (logp/value
+                               bit-exact too); default is the tcgen05 path with certified sampling */
 };
 
 typedef struct ktune_ctx ktune_ctx;
@@ -71,7 +73,11 @@ int ktune_ctx_synchronize(ktune_ctx* ctx);
 enum ktune_option {
   KTUNE_OPT_FORCE_EXACT = 1, /* 1: k-means decisions always via the exact-order fallback chains */
   KTUNE_OPT_KMEANS_MODE = 2, /* 0 auto, 1 exact-order centroids (mode A), 2 certified integer centroids (mode B) */
-  KTUNE_OPT_PROFILE = 3      /* 1: bracket the hot kernels with CUDA events on their stream (KTUNE_STAT_*_NS) */
+  KTUNE_OPT_PROFILE = 3,     /* 1: bracket the hot kernels with CUDA events on their stream (KTUNE_STAT_*_NS) */
+  KTUNE_OPT_ROLLOUT_DELTA = 4, /* certification margin of the tcgen05 rollout, in units of 1e-12
+                                  (0 = default) */
+  KTUNE_OPT_ROLLOUT_CHECK = 5  /* 1: re-decide EVERY sampling decision exactly and count disagreements
+                                  (calibration/verification mode, slow) */
 };
 int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value);
 
@@ -90,7 +96,12 @@ enum ktune_stat {
   KTUNE_STAT_ASSIGN_NS = 12,        /* summed device time of k-means assign launches */
   KTUNE_STAT_ASSIGN_CALLS = 13,
   KTUNE_STAT_XS_SEQUENTIAL = 14,    /* exact-sum segments summed sequentially (binade crossings) */
-  KTUNE_STAT_XS_SEGMENTS = 15       /* exact-sum segments in total */
+  KTUNE_STAT_XS_SEGMENTS = 15,      /* exact-sum segments in total */
+  KTUNE_STAT_ROLLOUT_FALLBACKS = 16, /* tcgen05 rollout: knob decisions re-decided by the exact fp64 forward */
+  KTUNE_STAT_ROLLOUT_CHECKED = 17,   /* KTUNE_OPT_ROLLOUT_CHECK: knob decisions checked */
+  KTUNE_STAT_ROLLOUT_MISMATCH = 18,  /* certified fast decisions that disagreed with the exact one (must be 0) */
+  KTUNE_STAT_ROLLOUT_MAXERR = 19,    /* max |p_fast - p_exact| over checked decisions, in units of 1e-12 */
+  KTUNE_STAT_ROLLOUT_TC = 20         /* config-steps run on the tcgen05 path */
 };
 int ktune_ctx_stat(ktune_ctx* ctx, int stat, int64_t* value);
 int ktune_ctx_reset_stats(ktune_ctx* ctx);

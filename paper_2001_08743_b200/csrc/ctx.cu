@@ -253,6 +253,7 @@ int ktune_ctx_destroy(ktune_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto& b : ctx->ws) b.release();
   for (auto& b : ctx->pinned) b.release();
+  if (ctx->d_counters) cudaFree(ctx->d_counters);
   kt_nccl_destroy(ctx);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -274,14 +275,17 @@ int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value) {
     if (option == KTUNE_OPT_FORCE_EXACT) ctx->opt_force_exact = value;
     else if (option == KTUNE_OPT_KMEANS_MODE) ctx->opt_kmeans_mode = value;
     else if (option == KTUNE_OPT_PROFILE) ctx->opt_profile = value;
+    else if (option == KTUNE_OPT_ROLLOUT_DELTA) ctx->opt_rollout_delta = value;
+    else if (option == KTUNE_OPT_ROLLOUT_CHECK) ctx->opt_rollout_check = value;
     else kt::fail(KTUNE_ERR_CONFIG, "unknown option");
   });
 }
 
 int ktune_ctx_stat(ktune_ctx* ctx, int stat, int64_t* value) {
   return kt_guard(ctx, [&] {
-    if (stat < 0 || stat >= 16) kt::fail(KTUNE_ERR_CONFIG, "unknown stat");
+    if (stat < 0 || stat >= ktune_ctx::kNumStats) kt::fail(KTUNE_ERR_CONFIG, "unknown stat");
     kt::resolve_timings(ctx);
+    kt::resolve_counters(ctx);
     *value = ctx->stats[stat];
   });
 }
@@ -289,6 +293,7 @@ int ktune_ctx_stat(ktune_ctx* ctx, int stat, int64_t* value) {
 int ktune_ctx_reset_stats(ktune_ctx* ctx) {
   return kt_guard(ctx, [&] {
     kt::resolve_timings(ctx);
+    kt::resolve_counters(ctx);
     std::fill(std::begin(ctx->stats), std::end(ctx->stats), 0);
   });
 }

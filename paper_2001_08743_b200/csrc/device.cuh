@@ -216,6 +216,28 @@ __device__ __forceinline__ double kt_tanh_bf(double x) {
   return x == 0.0 ? x : res;
 }
 
+// Per-knob log-softmax over {dec, stay, inc} (actor_critic.hpp:13-14).
+struct Knob3 {
+  double lp[3], p[3];
+};
+__device__ __forceinline__ Knob3 softmax3(double l0, double l1, double l2) {
+  double m = l0;
+  if (l1 > m) m = l1;
+  if (l2 > m) m = l2;
+  const double e0 = kt_exp(dsub(l0, m)), e1 = kt_exp(dsub(l1, m)),
+               e2 = kt_exp(dsub(l2, m));
+  const double s = dadd(dadd(e0, e1), e2);
+  const double lse = dadd(m, kt_log(s));
+  Knob3 r;
+  r.lp[0] = dsub(l0, lse);
+  r.lp[1] = dsub(l1, lse);
+  r.lp[2] = dsub(l2, lse);
+  r.p[0] = ddiv(e0, s);
+  r.p[1] = ddiv(e1, s);
+  r.p[2] = ddiv(e2, s);
+  return r;
+}
+
 // ---------------------------------------------------------------- validity.cpp:162-204
 template <class IdxAt>
 __device__ inline bool rule_eval(const KtSpaceParams& sp, IdxAt idx_at) {

@@ -94,7 +94,11 @@ struct ktune_ctx {
   int64_t opt_force_exact = 0;
   int64_t opt_kmeans_mode = 0;
   int64_t opt_profile = 0;
-  int64_t stats[16] = {0};
+  int64_t opt_rollout_delta = 0;  // 1e-12 units, 0 = default
+  int64_t opt_rollout_check = 0;
+  static constexpr int kNumStats = 32;
+  int64_t stats[kNumStats] = {0};
+  unsigned long long* d_counters = nullptr;  // device counters of the tcgen05 rollout (4 x u64)
   struct PendingTiming {
     cudaEvent_t a, b;
     int stat_ns;
@@ -186,6 +190,29 @@ void allgather(ktune_ctx* ctx, const void* send, void* recv, size_t bytes_per_ra
 }  // namespace kt
 
 void kt_nccl_destroy(ktune_ctx* ctx);
+
+namespace kt {
+// One rollout workload with device pointers (shared by the exact and the
+// tcgen05 rollout kernels).
+struct RolloutWork {
+  const ktune_space* space;
+  const ktune_ac* ac;
+  int64_t E;
+  int64_t episode_offset;
+  uint64_t seed;
+  const uint16_t* init_idx;
+  uint16_t* idx;
+  int8_t* actions;
+  double* logp;
+  double* value;
+};
+// tcgen05 rollout (rollout_tc.cu): eligibility (h = 128, g = 64, n <= 21,
+// cardinalities <= 2049, representable weight scales) and the launch.
+bool rollout_tc_eligible(const ktune_ac* ac, const ktune_space* sp);
+void rollout_tc(ktune_ctx* ctx, const std::vector<RolloutWork>& work, int T);
+// Folds the device counters of the tcgen05 rollout into ctx->stats.
+void resolve_counters(ktune_ctx* ctx);
+}  // namespace kt
 
 namespace kt {
 // Brackets one launch with CUDA events on ctx->stream when KTUNE_OPT_PROFILE is set.

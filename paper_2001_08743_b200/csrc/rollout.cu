@@ -229,27 +229,8 @@ __device__ void forward_tile(const double* __restrict__ P, const AcOff& o, int n
   __syncthreads();
 }
 
-// Per-knob log-softmax over {dec, stay, inc} (actor_critic.hpp:13-14).
-struct Knob3 {
-  double lp[3], p[3];
-};
-__device__ __forceinline__ Knob3 softmax3(double l0, double l1, double l2) {
-  double m = l0;
-  if (l1 > m) m = l1;
-  if (l2 > m) m = l2;
-  const double e0 = kt::kt_exp(kt::dsub(l0, m)), e1 = kt::kt_exp(kt::dsub(l1, m)),
-               e2 = kt::kt_exp(kt::dsub(l2, m));
-  const double s = kt::dadd(kt::dadd(e0, e1), e2);
-  const double lse = kt::dadd(m, kt::kt_log(s));
-  Knob3 r;
-  r.lp[0] = kt::dsub(l0, lse);
-  r.lp[1] = kt::dsub(l1, lse);
-  r.lp[2] = kt::dsub(l2, lse);
-  r.p[0] = kt::ddiv(e0, s);
-  r.p[1] = kt::ddiv(e1, s);
-  r.p[2] = kt::ddiv(e2, s);
-  return r;
-}
+using kt::Knob3;
+using kt::softmax3;
 
 template <bool SP, int CPL>
 __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_constant__ RolloutLaunch L) {
@@ -554,8 +535,20 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       r.logp = h.d_logp;
       r.value = h.d_val;
     }
-    // one launch config for all tasks: smem sized for the largest task; 64-episode
-    // tiles (2 per lane) when they fit, else 32
+    // tcgen05 path with certified sampling unless the exact fp64 forward is
+    // requested (or a task is outside the tensor-core path's shapes)
+    bool use_tc = !(flags & KTUNE_F_EXACT_ROLLOUT);
+    for (int k = 0; k < num_tasks && use_tc; ++k) use_tc = kt::rollout_tc_eligible(tasks[k].ac, tasks[k].space);
+    if (use_tc) {
+      std::vector<kt::RolloutWork> work(num_tasks);
+      for (int k = 0; k < num_tasks; ++k)
+        work[k] = {tasks[k].space, tasks[k].ac,  dt[k].E,     dt[k].episode_offset, dt[k].seed,
+                   dt[k].init_idx, dt[k].idx,    dt[k].actions, dt[k].logp,         dt[k].value};
+      kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
+      kt::rollout_tc(ctx, work, T);
+    }
+    // exact path: one launch config for all tasks: smem sized for the largest task;
+    // 64-episode tiles (2 per lane) when they fit, else 32
     int cpl = 2;
     for (int k = 0; k < num_tasks; ++k)
       if (!smem_params || rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, true, 2) > 227 * 1024 || 2 * dt[k].g > 128)
@@ -563,8 +556,8 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     size_t smem = 0;
     for (int k = 0; k < num_tasks; ++k)
       smem = std::max(smem, rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, smem_params, cpl));
-    if (smem > 227 * 1024) kt::fail(KTUNE_ERR_CONFIG, "rollout: agent too large for shared memory");
-    {
+    if (!use_tc && smem > 227 * 1024) kt::fail(KTUNE_ERR_CONFIG, "rollout: agent too large for shared memory");
+    if (!use_tc) {
       auto kern = smem_params ? (cpl == 2 ? rollout_kernel<true, 2> : rollout_kernel<true, 1>)
                               : rollout_kernel<false, 1>;
       KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

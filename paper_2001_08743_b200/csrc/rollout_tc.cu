@@ -1,0 +1,717 @@
+// K2 on the 5th-generation tensor cores: the batched Adaptive-Exploration
+// rollout (run_episodes; ActorCritic::forward,
+// actor_critic.hpp:18-64) with CERTIFIED sampling.
+//
+// Per config-step the actor-critic MLP runs as three tcgen05.mma GEMMs with
+// fp32 accumulators in TMEM:
+//   L1  h0  = tanh(W0 x + b0)        A = [idx | idx] (fp16, exact integers)
+//                                    B = [hi | lo] of W0/(card-1) * 2^e1
+//   L2  [hp|hv] = tanh(W h0 + b)     A = h0 * 2^14 split hi/lo (fp16),
+//                                    B = [Wp1;Wv1] * 2^e2 split hi/lo,
+//                                    3 products hi*hi + hi*lo + lo*hi
+//   L3  logits = Wp2 hp + bp2        same split, N = roundup16(3n)
+// (fp16 pairs carry 22 significant bits; products are exact in fp32), so the
+// logits agree with the exact fp64 forward to ~1e-6. The value head
+// (wv2 . hv + bv2) is an fp32 dot product in the L2 epilogue.
+//
+// Sampling is CERTIFIED: the fast probabilities p0 = P(dec), c1 = P(dec) +
+// P(stay) decide the action only when the draw u is farther than delta from
+// both (|u - p0| > delta and |u - c1| > delta); otherwise the warp recomputes
+// that row's forward EXACTLY in fp64 (the same operations as the exact kernel
+// and the oracle: DFMA chains in ascending input order, the portable tanh/
+// exp/log of DESIGN.md §5.3) and decides with the exact probabilities.
+// Knob indices, actions and therefore every visited configuration are
+// bit-identical to the exact path; log-probabilities and values are fp32-
+// accurate (north star: 1e-5 relative).
+//
+// Layout: one persistent CTA per SM (512 threads = 4 slots x 4 warps). A slot
+// is a tile of up to 128 episodes (one TMEM lane and one thread per episode,
+// 128 TMEM columns per slot); its configurations live in the owning threads'
+// registers for the whole episode. Weights are staged once per CTA into shared
+// memory as fp16 hi/lo (UMMA K-major, no swizzle); each slot has a 32 KB
+// operand buffer reused by every layer (L2 runs in two K halves). Slots run
+// independently (named barrier + mbarrier per slot), so one slot's MMAs
+// overlap the other slots' SIMT epilogues.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "device.cuh"
+#include "internal.cuh"
+#include "tcgen05.cuh"
+
+namespace {
+
+constexpr int kH = 128, kG = 64;  // hidden sizes of the tensor-core path
+constexpr int kSlots = 4;
+constexpr int kThr = kSlots * 128;
+constexpr int kTcMaxN = 21;       // 3n <= 64: the L3 accumulator stays clear of hv's TMEM columns
+constexpr int kMaxTcTasks = 12;
+constexpr float kActScale = 16384.f;  // 2^14 activation scale inside the fp16 operands
+
+struct TcTask {
+  int32_t card[kt::kMaxKnobs];
+  const double* params;  // fp64 flat layout (actor_critic.hpp:52-53)
+  int32_t n, T;
+  int64_t E, episode_offset;
+  uint64_t seed;
+  const uint16_t* init_idx;
+  uint16_t* idx;
+  int8_t* actions;
+  double* logp;
+  double* value;
+  int32_t cta_base, ctas, warps;  // CTAs [cta_base, cta_base + ctas) share warps = ceil(E/32)
+  int32_t e1, e2, e3;             // power-of-two weight scales of L1, L2, L3
+};
+
+struct TcLaunch {
+  int32_t num_tasks;
+  int32_t check;
+  float delta;
+  unsigned long long* counters;  // [fallbacks, checked, mismatches, max err (float bits)]
+  TcTask task[kMaxTcTasks];
+};
+
+// Shared-memory carve-up (bytes).
+constexpr uint32_t kOffB2 = 0;             // [128 x 256] fp16: [Wp1;Wv1] hi (K 0..127) | lo
+constexpr uint32_t kOffA = 65536;          // kSlots x [128 x 128] fp16 operand buffers
+constexpr uint32_t kABytes = 32768;
+constexpr uint32_t kOffB1 = kOffA + kSlots * kABytes;
+__host__ __device__ inline int nk_of(int n) { return (n + 7) & ~7; }
+__host__ __device__ inline int n3_of(int n) { return (3 * n + 15) & ~15; }
+__host__ __device__ inline uint32_t off_b3(int n) { return kOffB1 + 128u * 2 * nk_of(n) * 2; }
+__host__ __device__ inline uint32_t off_f32(int n) { return off_b3(n) + (uint32_t)n3_of(n) * 256; }
+constexpr int kNF32 = 128 + 64 + 64 + 64 + 64 + 4;  // b0 bp1 bv1 wv2 bp2 bv2
+__host__ __device__ inline uint32_t tc_smem_bytes(int n) { return off_f32(n) + kNF32 * 4 + 1024; }
+
+// ---------------------------------------------------------------- fast math
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcpf(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2f(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// scale * tanh(x) = sign(x) * scale * (1 - e) / (1 + e), e = exp(-2|x|); abs error ~1e-7 * scale
+__device__ __forceinline__ float tanh_scaled(float x, float scale) {
+  const float e = ex2f(fabsf(x) * -2.8853900817779268f);
+  const float r = rcpf(1.0f + e);
+  const float t = __fmul_rn(fmaf(-e, scale, scale), r);
+  return copysignf(t, x);
+}
+
+__device__ __forceinline__ uint32_t h2bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// Eight consecutive K values of row r (already scaled): hi at column k0, lo
+// at column 64 + k0 of a [128 x 128] K-major operand buffer.
+__device__ __forceinline__ void store8_split(unsigned char* Ab, int r, int k0, const float* v) {
+  uint32_t hi[4], lo[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const __half2 h = __floats2half2_rn(v[2 * p], v[2 * p + 1]);
+    const float2 f = __half22float2(h);
+    hi[p] = h2bits(h);
+    lo[p] = h2bits(__floats2half2_rn(__fsub_rn(v[2 * p], f.x), __fsub_rn(v[2 * p + 1], f.y)));
+  }
+  *reinterpret_cast<uint4*>(Ab + kt::tc::kmajor_offset(r, k0, 128)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  *reinterpret_cast<uint4*>(Ab + kt::tc::kmajor_offset(r, 64 + k0, 128)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+}
+
+__device__ __forceinline__ void sync_slot(int slot) {
+  kt::tc::fence_proxy_async();
+  kt::tc::fence_before();
+  kt::tc::named_bar(1 + slot, 128);
+}
+
+// Three-product split GEMM: K = 16 * nkb per operand half.
+// A hi chunk kb at Ab + kb*256, lo at Ab + 1024 + kb*256 (SBO 2048);
+// B hi chunk c at B + c*256, lo at B + blo + c*256 (SBO bsbo).
+__device__ __forceinline__ void mma_split(uint32_t d, uint32_t a, uint32_t b, uint32_t blo, uint32_t bsbo,
+                                          int c0, int nkb, uint32_t idesc, bool accumulate) {
+#pragma unroll 1
+  for (int kb = 0; kb < nkb; ++kb) {
+    const uint64_t ahi = kt::tc::smem_desc(a + kb * 256, 128, 2048);
+    const uint64_t alo = kt::tc::smem_desc(a + 1024 + kb * 256, 128, 2048);
+    const uint64_t bhi = kt::tc::smem_desc(b + (c0 + kb) * 256, 128, bsbo);
+    const uint64_t bl = kt::tc::smem_desc(b + blo + (c0 + kb) * 256, 128, bsbo);
+    kt::tc::mma_f16(d, ahi, bhi, idesc, (accumulate || kb > 0) ? 1u : 0u);
+    kt::tc::mma_f16(d, ahi, bl, idesc, 1u);
+    kt::tc::mma_f16(d, alo, bhi, idesc, 1u);
+  }
+}
+
+// Packed configuration (two uint16 knob indices per register).
+template <int NMAX>
+struct Cfg {
+  uint32_t w[NMAX / 2];
+  __device__ __forceinline__ int get(int d) const { return (int)((w[d >> 1] >> ((d & 1) * 16)) & 0xFFFFu); }
+  __device__ __forceinline__ void set(int d, int v) {
+    const int sh = (d & 1) * 16;
+    w[d >> 1] = (w[d >> 1] & ~(0xFFFFu << sh)) | ((uint32_t)v << sh);
+  }
+};
+
+template <int NMAX>
+__device__ __forceinline__ void store_row_idx(uint16_t* dst, const Cfg<NMAX>& c, int n) {
+  if ((n & 7) == 0) {
+#pragma unroll
+    for (int q = 0; q < NMAX / 8; ++q)
+      if (8 * q < n)
+        reinterpret_cast<uint4*>(dst)[q] = make_uint4(c.w[4 * q], c.w[4 * q + 1], c.w[4 * q + 2], c.w[4 * q + 3]);
+  } else if ((n & 1) == 0) {
+#pragma unroll
+    for (int q = 0; q < NMAX / 2; ++q)
+      if (2 * q < n) reinterpret_cast<uint32_t*>(dst)[q] = c.w[q];
+  } else {
+#pragma unroll
+    for (int d = 0; d < NMAX; ++d)
+      if (d < n) dst[d] = (uint16_t)c.get(d);
+  }
+}
+
+// Exact fp64 re-decision of row `L`'s flagged knobs by the whole warp (same
+// operations and order as the exact kernel's forward_tile and the oracle).
+// Returns, in lane L, the exact actions (2 bits per knob) and the sum of the
+// exact log-probabilities of the flagged knobs; check-mode statistics too.
+struct Redecided {
+  uint64_t acts;
+  float lp;
+};
+
+template <int NMAX>
+__device__ __noinline__ Redecided exact_redecide(const TcTask& tk, int t, int L, uint32_t fm, Cfg<NMAX> cfg,
+                                                 const int* scard, double* sh0, double* shp, double* slg,
+                                                 int64_t ge_L, uint64_t acts, const float* fast_p0,
+                                                 const float* fast_c1, uint32_t fast_cert,
+                                                 unsigned long long* stats) {
+  float lp_exact = 0.f;
+  const int lane = threadIdx.x & 31;
+  const int n = tk.n;
+  const double* P = tk.params;
+  const int ob0 = kH * n, owp1 = ob0 + kH, obp1 = owp1 + kG * kH, owp2 = obp1 + kG, obp2 = owp2 + 3 * n * kG;
+  double x[NMAX];
+#pragma unroll
+  for (int d = 0; d < NMAX; ++d) {
+    const int c = (int)((__shfl_sync(0xffffffffu, cfg.w[d >> 1], L) >> ((d & 1) * 16)) & 0xFFFFu);
+    x[d] = (d < n && scard[d] > 1) ? kt::ddiv((double)c, (double)(scard[d] - 1)) : 0.0;
+  }
+  // h0 = tanh(W0 x + b0): W0 column-major (h x n)
+#pragma unroll
+  for (int m = 0; m < kH / 32; ++m) {
+    const int u = lane + 32 * m;
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i)
+      if (i < n) acc = __fma_rn(P[i * kH + u], x[i], acc);
+    sh0[u] = kt::kt_tanh_bf(kt::dadd(acc, P[ob0 + u]));
+  }
+  __syncwarp();
+  // hp = tanh(Wp1 h0 + bp1): Wp1 column-major (g x h)
+#pragma unroll
+  for (int m = 0; m < kG / 32; ++m) {
+    const int u = lane + 32 * m;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int i = 0; i < kH; ++i) acc = __fma_rn(P[owp1 + i * kG + u], sh0[i], acc);
+    shp[u] = kt::kt_tanh_bf(kt::dadd(acc, P[obp1 + u]));
+  }
+  __syncwarp();
+  // logits of the flagged knobs: item it -> (k-th flagged knob, a)
+  const int nf = __popc(fm);
+  for (int it = lane; it < 3 * nf; it += 32) {
+    uint32_t mm = fm;
+    for (int q = 0; q < it / 3; ++q) mm &= mm - 1;
+    const int a = 3 * (__ffs(mm) - 1) + it % 3;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int j = 0; j < kG; ++j) acc = __fma_rn(P[owp2 + j * 3 * n + a], shp[j], acc);
+    slg[it] = kt::dadd(acc, P[obp2 + a]);
+  }
+  __syncwarp();
+  if (lane == L) {
+    int it = 0;
+    const uint64_t ge = (uint64_t)ge_L;
+#pragma unroll
+    for (int d = 0; d < NMAX; ++d) {
+      if (!((fm >> d) & 1u)) continue;
+      const kt::Knob3 k3 = kt::softmax3(slg[3 * it], slg[3 * it + 1], slg[3 * it + 2]);
+      const double u = kt::hash01(tk.seed, (ge * (uint64_t)tk.T + (uint64_t)t) * (uint64_t)n + (uint64_t)d);
+      const double c1 = kt::dadd(k3.p[0], k3.p[1]);
+      const int ae = u < k3.p[0] ? 0 : (u < c1 ? 1 : 2);
+      if (stats) {  // check mode: compare against the fast decision
+        const float err = fmaxf(fabsf((float)(fast_p0[d] - k3.p[0])), fabsf((float)(fast_c1[d] - c1)));
+        atomicMax(reinterpret_cast<unsigned int*>(stats + 3), __float_as_uint(err));
+        if ((fast_cert >> d) & 1u) {
+          const int af = (int)((acts >> (2 * d)) & 3u);
+          if (af != ae) atomicAdd(stats + 2, 1ull);
+        }
+      }
+      acts = (acts & ~(3ull << (2 * d))) | ((uint64_t)ae << (2 * d));
+      lp_exact += (float)k3.lp[ae];
+      ++it;
+    }
+  }
+  __syncwarp();
+  return {acts, lp_exact};
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_constant__ TcLaunch L) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ uint64_t mbar[kSlots];
+  __shared__ uint32_t tbase_sh;
+  __shared__ int scard[kt::kMaxKnobs];
+  int ti = 0;
+  while (ti + 1 < L.num_tasks && L.task[ti + 1].cta_base <= (int)blockIdx.x) ++ti;
+  const TcTask& tk = L.task[ti];
+  const int jc = (int)blockIdx.x - tk.cta_base;
+  const int wbase = tk.warps / tk.ctas, wextra = tk.warps % tk.ctas;
+  const int nw = wbase + (jc < wextra ? 1 : 0);  // live warps of this CTA
+  const int64_t row0 = (int64_t)(jc * wbase + min(jc, wextra)) * 32;
+  const int n = tk.n, T = tk.T, nk = nk_of(n), K1 = 2 * nk, N3 = n3_of(n);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const double* __restrict__ P = tk.params;
+  const int ob0 = kH * n, owp1 = ob0 + kH, obp1 = owp1 + kG * kH, owp2 = obp1 + kG, obp2 = owp2 + 3 * n * kG,
+            owv1 = obp2 + 3 * n, obv1 = owv1 + kG * kH, owv2 = obv1 + kG, obv2 = owv2 + kG;
+
+  unsigned char* B2 = sm + kOffB2;
+  unsigned char* B1 = sm + kOffB1;
+  unsigned char* B3 = sm + off_b3(n);
+  float* f32 = reinterpret_cast<float*>(sm + off_f32(n));
+  float* sb0 = f32;
+  float* sbp1 = sb0 + 128;
+  float* sbv1 = sbp1 + 64;
+  float* swv2 = sbv1 + 64;
+  float* sbp2 = swv2 + 64;
+  float* sbv2 = sbp2 + 64;
+
+  // ---- prologue: weights -> fp16 hi/lo operands, biases -> fp32
+  if (tid < kt::kMaxKnobs) scard[tid] = tk.card[tid];
+  __syncthreads();
+  {
+    const double s1 = ldexp(1.0, tk.e1), s2 = ldexp(1.0, tk.e2), s3 = ldexp(1.0, tk.e3);
+    for (int i = tid; i < 128 * K1; i += kThr) {
+      const int j = i / K1, k = i % K1, part = k >= nk, kk = part ? k - nk : k;
+      double v = 0.0;
+      if (kk < n && scard[kk] > 1) v = kt::dmul(kt::ddiv(P[kk * kH + j], (double)(scard[kk] - 1)), s1);
+      const __half hi = __double2half(v);
+      const __half o = part ? __double2half(kt::dsub(v, (double)__half2float(hi))) : hi;
+      *reinterpret_cast<__half*>(B1 + kt::tc::kmajor_offset(j, k, K1)) = o;
+    }
+    for (int i = tid; i < 128 * 256; i += kThr) {
+      const int u = i >> 8, k = i & 255, part = k >> 7, kk = k & 127;
+      const double wv = u < kG ? P[owp1 + kk * kG + u] : P[owv1 + kk * kG + (u - kG)];
+      const double v = kt::dmul(wv, s2);
+      const __half hi = __double2half(v);
+      const __half o = part ? __double2half(kt::dsub(v, (double)__half2float(hi))) : hi;
+      *reinterpret_cast<__half*>(B2 + kt::tc::kmajor_offset(u, k, 256)) = o;
+    }
+    for (int i = tid; i < N3 * 128; i += kThr) {
+      const int a = i >> 7, k = i & 127, part = k >> 6, kk = k & 63;
+      const double v = a < 3 * n ? kt::dmul(P[owp2 + kk * 3 * n + a], s3) : 0.0;
+      const __half hi = __double2half(v);
+      const __half o = part ? __double2half(kt::dsub(v, (double)__half2float(hi))) : hi;
+      *reinterpret_cast<__half*>(B3 + kt::tc::kmajor_offset(a, k, 128)) = o;
+    }
+    for (int i = tid; i < kNF32; i += kThr) {
+      float v = 0.f;
+      if (i < 128) v = (float)P[ob0 + i];
+      else if (i < 192) v = (float)P[obp1 + i - 128];
+      else if (i < 256) v = (float)P[obv1 + i - 192];
+      else if (i < 320) v = (float)P[owv2 + i - 256];
+      else if (i < 384) v = i - 320 < 3 * n ? (float)P[obp2 + i - 320] : 0.f;
+      else if (i == 384) v = (float)P[obv2];
+      f32[i] = v;
+    }
+  }
+  if (w == 0) kt::tc::tmem_alloc(&tbase_sh, 512);
+  if (tid == 0) {
+    for (int s = 0; s < kSlots; ++s) kt::tc::mbar_init(&mbar[s], 1);
+    kt::tc::fence_mbar_init();
+  }
+  kt::tc::fence_proxy_async();
+  kt::tc::fence_before();
+  __syncthreads();
+  kt::tc::fence_after();
+
+  const int slot = w >> 2, q = w & 3;
+  const bool slot_used = 4 * slot < nw;
+  unsigned long long n_fallback = 0, n_checked = 0;
+  if (slot_used) {
+    const bool lw = w < nw;
+    const int64_t e = row0 + 32 * w + lane;
+    const bool lr = lw && e < tk.E;
+    const int r = 32 * q + lane;  // TMEM lane / operand row
+    unsigned char* Ab = sm + kOffA + slot * kABytes;
+    const uint32_t a_addr = kt::tc::smem_u32(Ab);
+    const uint32_t tcol = tbase_sh + ((uint32_t)(32 * q) << 16) + (uint32_t)(128 * slot);
+    const uint32_t tslot = tbase_sh + (uint32_t)(128 * slot);
+    const bool leader = q == 0 && lane == 0;
+    uint64_t* mb = &mbar[slot];
+    const float sc1 = ldexpf(1.f, -tk.e1), sc2 = ldexpf(1.f, -(14 + tk.e2)), sc3 = ldexpf(1.f, -(14 + tk.e3));
+    const uint32_t id128 = kt::tc::idesc_f16_f32(128, 128), idn3 = kt::tc::idesc_f16_f32(128, N3);
+    const uint32_t b1 = kt::tc::smem_u32(B1), b2 = kt::tc::smem_u32(B2), b3 = kt::tc::smem_u32(B3);
+    const uint64_t ge = (uint64_t)(tk.episode_offset + e);
+    double* sh0 = reinterpret_cast<double*>(Ab + (4 * q) * 2048 + 1024);
+    double* shp = reinterpret_cast<double*>(Ab + (4 * q + 1) * 2048 + 1024);
+    double* slg = reinterpret_cast<double*>(Ab + (4 * q + 2) * 2048 + 1024);
+
+    Cfg<NMAX> cfg;
+#pragma unroll
+    for (int i = 0; i < NMAX / 2; ++i) cfg.w[i] = 0;
+    if (lr) {
+#pragma unroll
+      for (int d = 0; d < NMAX; ++d)
+        if (d < n) cfg.set(d, tk.init_idx[e * n + d]);
+      store_row_idx(tk.idx + e * (int64_t)(T + 1) * n, cfg, n);
+    }
+    uint32_t ph = 0;
+    for (int t = 0; t < T; ++t) {
+      // ---- L1 operand: [idx | idx] as fp16 (exact integers)
+      if (lw) {
+#pragma unroll
+        for (int c = 0; c < NMAX / 8; ++c) {
+          if (8 * c < nk) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              const int d = 8 * c + 2 * p;
+              pk[p] = h2bits(__floats2half2_rn((float)cfg.get(d), (float)cfg.get(d + 1)));
+            }
+            const uint4 v = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4*>(Ab + kt::tc::kmajor_offset(r, 8 * c, 128)) = v;
+            *reinterpret_cast<uint4*>(Ab + kt::tc::kmajor_offset(r, nk + 8 * c, 128)) = v;
+          }
+        }
+      }
+      sync_slot(slot);
+      if (leader) {
+        kt::tc::fence_after();
+        for (int kb = 0; kb < K1 / 16; ++kb)
+          kt::tc::mma_f16(tslot, kt::tc::smem_desc(a_addr + kb * 256, 128, 2048),
+                          kt::tc::smem_desc(b1 + kb * 256, 128, (K1 / 8) * 128), id128, kb > 0);
+        kt::tc::commit(mb);
+      }
+      float hb[64];
+      if (lw) {
+        kt::tc::mbar_wait(mb, ph);
+        kt::tc::fence_after();
+        // ---- L1 epilogue: h0 = tanh(acc * 2^-e1 + b0); units 0..63 -> operand, 64..127 held
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t v[32];
+          kt::tc::ld_32x32b_x32(tcol + c0, v);
+          kt::tc::ld_wait();
+          float hv[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) hv[j] = tanh_scaled(fmaf(__uint_as_float(v[j]), sc1, sb0[c0 + j]), kActScale);
+          if (c0 < 64) {
+#pragma unroll
+            for (int m = 0; m < 4; ++m) store8_split(Ab, r, c0 + 8 * m, hv + 8 * m);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) hb[c0 - 64 + j] = hv[j];
+          }
+        }
+      }
+      ph ^= 1;
+      sync_slot(slot);
+      if (leader) {  // L2, K half 0
+        kt::tc::fence_after();
+        mma_split(tslot, a_addr, b2, 2048, 4096, 0, 4, id128, false);
+        kt::tc::commit(mb);
+      }
+      if (lw) {
+        kt::tc::mbar_wait(mb, ph);
+        kt::tc::fence_after();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) store8_split(Ab, r, 8 * m, hb + 8 * m);
+      }
+      ph ^= 1;
+      sync_slot(slot);
+      if (leader) {  // L2, K half 1
+        kt::tc::fence_after();
+        mma_split(tslot, a_addr, b2, 2048, 4096, 4, 4, id128, true);
+        kt::tc::commit(mb);
+      }
+      if (lw) {
+        kt::tc::mbar_wait(mb, ph);
+        kt::tc::fence_after();
+        // ---- L2 epilogue (policy half): hp -> L3 operand
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t v[32];
+          kt::tc::ld_32x32b_x32(tcol + c0, v);
+          kt::tc::ld_wait();
+          float hv[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) hv[j] = tanh_scaled(fmaf(__uint_as_float(v[j]), sc2, sbp1[c0 + j]), kActScale);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) store8_split(Ab, r, c0 + 8 * m, hv + 8 * m);
+        }
+      }
+      ph ^= 1;
+      sync_slot(slot);
+      if (leader) {  // L3 logits (accumulator columns 0..N3-1; hv stays in 64..127)
+        kt::tc::fence_after();
+        mma_split(tslot, a_addr, b3, 1024, 2048, 0, 4, idn3, false);
+        kt::tc::commit(mb);
+      }
+      if (lw) {
+        // ---- L2 epilogue (value half), overlapping the L3 MMAs: v = wv2 . tanh(.) + bv2
+        float vs = 0.f;
+#pragma unroll
+        for (int c0 = 64; c0 < 128; c0 += 32) {
+          uint32_t v[32];
+          kt::tc::ld_32x32b_x32(tcol + c0, v);
+          kt::tc::ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            vs = fmaf(swv2[c0 - 64 + j], tanh_scaled(fmaf(__uint_as_float(v[j]), sc2, sbv1[c0 - 64 + j]), 1.f), vs);
+        }
+        if (lr && tk.value) tk.value[e * T + t] = (double)(vs + sbv2[0]);
+        kt::tc::mbar_wait(mb, ph);
+        kt::tc::fence_after();
+        // ---- L3 epilogue: per-knob softmax, certified inverse-CDF draw, saturating move
+        constexpr int kLg = ((3 * NMAX + 15) / 16) * 16;
+        float lg[kLg];
+#pragma unroll
+        for (int c0 = 0; c0 < kLg; c0 += 16) {
+          if (c0 < N3) {
+            uint32_t v[16];
+            kt::tc::ld_32x32b_x16(tcol + c0, v);
+            kt::tc::ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) lg[c0 + j] = fmaf(__uint_as_float(v[j]), sc3, sbp2[c0 + j]);
+          }
+        }
+        uint64_t acts = 0;
+        uint32_t fb = 0, cert = 0;
+        float lpj = 0.f;
+        float p0s[NMAX], c1s[NMAX];
+        const float delta = L.delta;
+#pragma unroll
+        for (int d = 0; d < NMAX; ++d) {
+          if (d < n) {
+            const float l0 = lg[3 * d], l1 = lg[3 * d + 1], l2 = lg[3 * d + 2];
+            const float m = fmaxf(l0, fmaxf(l1, l2));
+            const float e0 = ex2f((l0 - m) * 1.4426950408889634f), e1 = ex2f((l1 - m) * 1.4426950408889634f),
+                        e2 = ex2f((l2 - m) * 1.4426950408889634f);
+            const float s = e0 + e1 + e2;
+            const float rs = rcpf(s);
+            const float p0 = e0 * rs, c1 = (e0 + e1) * rs;
+            const uint64_t hsh =
+                kt::mix64(tk.seed ^ kt::mix64((ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n + (uint64_t)d +
+                                              0x9E3779B97F4A7C15ULL));
+            const float uf = (float)(uint32_t)(hsh >> 40) * 0x1.0p-24f;  // |uf - u| < 2^-24
+            const int a = uf < p0 ? 0 : (uf < c1 ? 1 : 2);
+            const bool ok = fabsf(uf - p0) > delta && fabsf(uf - c1) > delta;
+            acts |= (uint64_t)a << (2 * d);
+            if (L.check) {
+              p0s[d] = p0;
+              c1s[d] = c1;
+            }
+            if (ok) {
+              cert |= 1u << d;
+              lpj += (a == 0 ? l0 : (a == 1 ? l1 : l2)) - m - lg2f(s) * 0.69314718055994531f;
+            }
+          }
+        }
+        const uint32_t allk = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
+        fb = L.check ? allk : (allk & ~cert);
+        if (!lr) fb = 0;
+        n_fallback += L.check ? 0 : __popc(fb);
+        n_checked += L.check ? __popc(fb) : 0;
+        unsigned pend = __ballot_sync(0xffffffffu, fb != 0);
+        float lpx = 0.f;
+        while (pend) {
+          const int Lr = __ffs(pend) - 1;
+          pend &= pend - 1;
+          const uint32_t fm = __shfl_sync(0xffffffffu, fb, Lr);
+          const int64_t geL = __shfl_sync(0xffffffffu, (long long)ge, Lr);
+          const Redecided rd = exact_redecide<NMAX>(tk, t, Lr, fm, cfg, scard, sh0, shp, slg, geL, acts, p0s, c1s,
+                                                    cert, L.check ? L.counters : nullptr);
+          if (lane == Lr) {
+            acts = rd.acts;
+            lpx = rd.lp;
+          }
+        }
+        if (L.check) lpj = lpx;  // every knob re-decided: exact log-probabilities
+        else lpj += lpx;
+        // saturating move (design_space.cpp:175-187) and the trajectory writes
+        uint32_t apk[(NMAX + 3) / 4];
+#pragma unroll
+        for (int i = 0; i < (NMAX + 3) / 4; ++i) apk[i] = 0;
+#pragma unroll
+        for (int d = 0; d < NMAX; ++d) {
+          if (d < n) {
+            const int a = (int)((acts >> (2 * d)) & 3u);
+            int v = cfg.get(d) + a - 1;
+            v = v < 0 ? 0 : (v > scard[d] - 1 ? scard[d] - 1 : v);
+            cfg.set(d, v);
+            apk[d >> 2] |= (uint32_t)(uint8_t)(int8_t)(a - 1) << (8 * (d & 3));
+          }
+        }
+        if (lr) {
+          store_row_idx(tk.idx + (e * (int64_t)(T + 1) + t + 1) * n, cfg, n);
+          if (tk.actions) {
+            int8_t* ad = tk.actions + (e * (int64_t)T + t) * n;
+            if ((n & 3) == 0) {
+#pragma unroll
+              for (int i = 0; i < (NMAX + 3) / 4; ++i)
+                if (4 * i < n) reinterpret_cast<uint32_t*>(ad)[i] = apk[i];
+            } else {
+#pragma unroll
+              for (int d = 0; d < NMAX; ++d)
+                if (d < n) ad[d] = (int8_t)((apk[d >> 2] >> (8 * (d & 3))) & 0xFF);
+            }
+          }
+          if (tk.logp) tk.logp[e * T + t] = (double)lpj;
+        }
+      }
+      ph ^= 1;
+    }
+  }
+  // counters
+  for (int o = 16; o > 0; o >>= 1) {
+    n_fallback += __shfl_down_sync(0xffffffffu, n_fallback, o);
+    n_checked += __shfl_down_sync(0xffffffffu, n_checked, o);
+  }
+  if (lane == 0 && L.counters) {
+    if (n_fallback) atomicAdd(L.counters + 0, n_fallback);
+    if (n_checked) atomicAdd(L.counters + 1, n_checked);
+  }
+  kt::tc::fence_before();
+  __syncthreads();
+  if (w == 0) kt::tc::tmem_dealloc(tbase_sh, 512);
+}
+
+// Power-of-two scale e with max|W| * 2^e < 2^14 (0 for an all-zero matrix).
+int pow2_scale(double maxabs) {
+  if (!(maxabs > 0.0)) return 0;
+  int ex = 0;
+  std::frexp(maxabs, &ex);  // maxabs < 2^ex
+  return 14 - ex;
+}
+
+}  // namespace
+
+namespace kt {
+
+bool rollout_tc_eligible(const ktune_ac* ac, const ktune_space* sp) {
+  if (!ac || !sp || ac->h != kH || ac->g != kG || ac->n < 1 || ac->n > kTcMaxN || sp->D != ac->n) return false;
+  for (int c : sp->card)
+    if (c > 2049) return false;  // fp16 holds the knob indices exactly up to 2048
+  return true;
+}
+
+void resolve_counters(ktune_ctx* ctx) {
+  if (!ctx->d_counters) return;
+  unsigned long long c[4];
+  KT_CUDA(cudaStreamSynchronize(ctx->stream));
+  KT_CUDA(cudaMemcpy(c, ctx->d_counters, sizeof(c), cudaMemcpyDeviceToHost));
+  KT_CUDA(cudaMemset(ctx->d_counters, 0, sizeof(c)));
+  ctx->stats[KTUNE_STAT_ROLLOUT_FALLBACKS] += (int64_t)c[0];
+  ctx->stats[KTUNE_STAT_ROLLOUT_CHECKED] += (int64_t)c[1];
+  ctx->stats[KTUNE_STAT_ROLLOUT_MISMATCH] += (int64_t)c[2];
+  float mx;
+  const unsigned int bits = (unsigned int)c[3];
+  std::memcpy(&mx, &bits, 4);
+  ctx->stats[KTUNE_STAT_ROLLOUT_MAXERR] =
+      std::max<int64_t>(ctx->stats[KTUNE_STAT_ROLLOUT_MAXERR], (int64_t)std::llround((double)mx * 1e12));
+}
+
+void rollout_tc(ktune_ctx* ctx, const std::vector<RolloutWork>& work, int T) {
+  if (!ctx->d_counters) {
+    KT_CUDA(cudaMalloc(&ctx->d_counters, 4 * sizeof(unsigned long long)));
+    KT_CUDA(cudaMemsetAsync(ctx->d_counters, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  }
+  // Certification margin: fast-vs-exact probability error (calibrated with
+  // KTUNE_OPT_ROLLOUT_CHECK) plus the 2^-24 draw truncation.
+  const float delta = ctx->opt_rollout_delta > 0 ? (float)((double)ctx->opt_rollout_delta * 1e-12)
+                                                  : (float)(0x1.0p-16 + 0x1.0p-24);
+  const int S = sm_count(ctx);
+  for (size_t t0 = 0; t0 < work.size(); t0 += kMaxTcTasks) {
+    const size_t nt = std::min<size_t>(kMaxTcTasks, work.size() - t0);
+    TcLaunch L{};
+    L.check = ctx->opt_rollout_check ? 1 : 0;
+    L.delta = delta;
+    L.counters = ctx->d_counters;
+    // warps per task, then the smallest per-CTA warp count m whose CTA total fits one wave
+    std::vector<int64_t> W(nt);
+    int64_t wsum = 0;
+    int nmax = 1;
+    for (size_t k = 0; k < nt; ++k) {
+      W[k] = ceil_div(work[t0 + k].E, 32);
+      wsum += W[k];
+      nmax = std::max(nmax, work[t0 + k].ac->n);
+    }
+    int m = 16;
+    if (wsum <= (int64_t)16 * S) {
+      for (m = 1; m < 16; ++m) {
+        int64_t c = 0;
+        for (size_t k = 0; k < nt; ++k) c += ceil_div(W[k], m);
+        if (c <= S) break;
+      }
+    }
+    int ctas = 0;
+    int nl = 0;
+    for (size_t k = 0; k < nt; ++k) {
+      if (W[k] == 0) continue;
+      const RolloutWork& rw = work[t0 + k];
+      TcTask& tk = L.task[nl++];
+      for (int d = 0; d < kMaxKnobs; ++d) tk.card[d] = d < rw.space->D ? rw.space->card[d] : 1;
+      tk.params = rw.ac->d_params;
+      tk.n = rw.ac->n;
+      tk.T = T;
+      tk.E = rw.E;
+      tk.episode_offset = rw.episode_offset;
+      tk.seed = rw.seed;
+      tk.init_idx = rw.init_idx;
+      tk.idx = rw.idx;
+      tk.actions = rw.actions;
+      tk.logp = rw.logp;
+      tk.value = rw.value;
+      tk.warps = (int32_t)W[k];
+      tk.ctas = (int32_t)ceil_div(W[k], m);
+      tk.cta_base = ctas;
+      ctas += tk.ctas;
+      // weight scales from the host copy of the parameters
+      const int n = tk.n;
+      const std::vector<double>& p = rw.ac->host_params;
+      const int ob0 = kH * n, owp1 = ob0 + kH, obp1 = owp1 + kG * kH, owp2 = obp1 + kG, obp2 = owp2 + 3 * n * kG,
+                owv1 = obp2 + 3 * n, obv1 = owv1 + kG * kH;
+      double m1 = 0, m2 = 0, m3 = 0;
+      for (int i = 0; i < n; ++i)
+        if (tk.card[i] > 1)
+          for (int j = 0; j < kH; ++j) m1 = std::max(m1, std::fabs(p[i * kH + j]) / (double)(tk.card[i] - 1));
+      for (int i = owp1; i < obp1; ++i) m2 = std::max(m2, std::fabs(p[i]));
+      for (int i = owv1; i < obv1; ++i) m2 = std::max(m2, std::fabs(p[i]));
+      for (int i = owp2; i < obp2; ++i) m3 = std::max(m3, std::fabs(p[i]));
+      tk.e1 = pow2_scale(m1);
+      tk.e2 = pow2_scale(m2);
+      tk.e3 = pow2_scale(m3);
+      if (tk.e1 > 100 || tk.e2 > 100 || tk.e3 > 100 || tk.e1 < -100 || tk.e2 < -100 || tk.e3 < -100)
+        fail(KTUNE_ERR_CONFIG, "rollout: actor-critic weights out of the tensor-core path's range");
+      ctx->stats[KTUNE_STAT_ROLLOUT_TC] += rw.E * (int64_t)T;
+    }
+    L.num_tasks = nl;
+    if (ctas == 0 || T == 0) continue;
+    const size_t smem = tc_smem_bytes(nmax);
+    auto kern = nmax <= 8 ? rollout_tc_kernel<8> : (nmax <= 16 ? rollout_tc_kernel<16> : rollout_tc_kernel<24>);
+    KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)ctas, kThr, smem, ctx->stream>>>(L);
+    check_launch(ctx, "rollout_tc");
+  }
+}
+
+}  // namespace kt

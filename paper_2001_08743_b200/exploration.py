@@ -97,13 +97,17 @@ class RolloutTask:
 
 
 def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Context] = None,
-                       device_out: bool = False, host_out: Optional[list] = None):
+                       device_out: bool = False, host_out: Optional[list] = None, exact: bool = False):
     """Grouped run_episodes over several workloads in ONE persistent-kernel launch.
 
     Host arrays in/out by default; with CUDA-tensor init_idx and device_out=True
     everything stays on the device (torch tensors) and the call is stream-ordered.
     Returns per task dict(idx E x (T+1) x D uint16, score E x (T+1), actions
     E x T x D int8, logp E x T, value E x T).
+
+    Default: the tcgen05 rollout with certified sampling (configurations,
+    actions and scores bit-exact; logp/value fp32-accurate). exact=True runs
+    the fp64 forward on every config-step (logp/value bit-exact as well).
     """
     ctx = ctx or tasks[0].space.ctx
     arr = (L.RolloutTaskC * len(tasks))()
@@ -159,12 +163,13 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
         a.logp = pp(o["logp"])
         a.value = pp(o["value"])
         outs.append(o)
-    ctx.check(L.lib().ktune_rollout(ctx.h, len(tasks), arr, T, L.F_DEVICE if dev else 0))
+    ctx.check(L.lib().ktune_rollout(ctx.h, len(tasks), arr, T,
+                                    (L.F_DEVICE if dev else 0) | (L.F_EXACT_ROLLOUT if exact else 0)))
     return outs
 
 
 def run_episodes(space: Space, cost_model: Optional[DeviceGbt], agent: ActorCritic, init_idx, T: int,
-                 root_seed: int = 0, episode_offset: int = 0):
+                 root_seed: int = 0, episode_offset: int = 0, exact: bool = False):
     """run_episodes(space, cost_model, net, params, initial_configs, rng) (SPEC.md:258).
 
     Returns (candidates, trajectory): candidates is a CandidateSet over every
@@ -173,7 +178,8 @@ def run_episodes(space: Space, cost_model: Optional[DeviceGbt], agent: ActorCrit
     per-step rewards r_t = pred(Θ_{t+1}) - pred(Θ_t).
     """
     from .sampling import make_candidate_set
-    o = run_episodes_batch([RolloutTask(space, agent, cost_model, init_idx, episode_offset, root_seed)], T)[0]
+    o = run_episodes_batch([RolloutTask(space, agent, cost_model, init_idx, episode_offset, root_seed)], T,
+                           exact=exact)[0]
     E = o["idx"].shape[0]
     flat = o["idx"].reshape(-1, space.D).astype(np.int32)
     score = o["score"].reshape(-1) if o["score"] is not None else np.zeros(len(flat))

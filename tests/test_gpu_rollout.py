@@ -50,7 +50,8 @@ def test_rollout_bit_exact(O, ctx, name, E, T):
     from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
     sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=E)
     init = osp.random_valid(E, E) if O.ref_available() else np.zeros((E, sp.num_knobs), np.int32)
-    out = run_episodes_batch([RolloutTask(dspace, agent, dg, init, episode_offset=5, root_seed=17)], T)[0]
+    out = run_episodes_batch([RolloutTask(dspace, agent, dg, init, episode_offset=5, root_seed=17)], T,
+                             exact=True)[0]
     from paper_2001_08743_b200.spaces import stream_seed
     want = O.run_episodes(osp, og, 128, 64, agent.params, init, T, 5, stream_seed(17, "explore"))
     assert np.array_equal(out["idx"].astype(np.int32), want["idx"])
@@ -69,7 +70,7 @@ def test_grouped_launch_matches_per_task(O, ctx):
         init = osp.random_valid(i, 40) if O.ref_available() else np.zeros((40, sp.num_knobs), np.int32)
         tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=100 * i, root_seed=i))
         wants.append(O.run_episodes(osp, og, 128, 64, agent.params, init, 15, 100 * i, stream_seed(i, "explore")))
-    outs = run_episodes_batch(tasks, 15)
+    outs = run_episodes_batch(tasks, 15, exact=True)
     for o, w in zip(outs, wants):
         assert np.array_equal(o["idx"].astype(np.int32), w["idx"])
         assert np.array_equal(o["score"], w["score"])
@@ -94,3 +95,81 @@ def test_rollout_large_spot_replay(O, ctx):
     assert np.all(idx.max(axis=(0, 1)) < np.array(sp.cards))
     assert np.all(np.abs(np.diff(idx, axis=1)) <= 1)
     assert np.array_equal(np.diff(idx, axis=1) != 0, out["actions"] != 0) or True
+
+
+# ---------------------------------------------------------------- tcgen05 path
+# Tolerances of the fast path (north star): configurations, actions and scores
+# bit-exact; log-probabilities and values within 1e-5 relative (fp32-accurate;
+# an absolute floor of 1e-5 covers values near zero).
+def _close(a, b, tol=1e-5):
+    return np.all(np.abs(a - b) <= tol * np.maximum(1.0, np.abs(b)))
+
+
+@pytest.mark.parametrize("name,E,T", [("resnet_c2", 37, 25), ("synthetic16", 200, 30),
+                                      ("resnet_dense_u16", 5, 40), ("vgg_c4", 300, 12),
+                                      ("synthetic8", 129, 17)])
+def test_rollout_tc_matches_oracle(O, ctx, name, E, T):
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    from paper_2001_08743_b200.spaces import stream_seed
+    sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=E)
+    init = osp.random_valid(E, E) if O.ref_available() else np.zeros((E, sp.num_knobs), np.int32)
+    out = run_episodes_batch([RolloutTask(dspace, agent, dg, init, episode_offset=5, root_seed=17)], T)[0]
+    want = O.run_episodes(osp, og, 128, 64, agent.params, init, T, 5, stream_seed(17, "explore"))
+    assert np.array_equal(out["idx"].astype(np.int32), want["idx"])
+    assert np.array_equal(out["actions"], want["actions"])
+    assert np.array_equal(out["score"], want["score"])
+    assert _close(out["logp"], want["logp"]), np.abs(out["logp"] - want["logp"]).max()
+    assert _close(out["value"], want["value"]), np.abs(out["value"] - want["value"]).max()
+
+
+def test_rollout_tc_equals_exact_kernel_at_scale(O, ctx):
+    """Grouped 12-task launch (the bench's shape, shorter episodes): the tcgen05
+    path and the exact fp64 kernel visit identical configurations."""
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    names = ["resnet_c2", "vgg_c4", "synthetic8", "synthetic16"]
+    tasks = []
+    for i in range(12):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, names[i % 4], seed=i)
+        init = osp.random_valid(i, 1024) if O.ref_available() else np.zeros((1024, sp.num_knobs), np.int32)
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=1024 * i, root_seed=i))
+    ctx.set_option(L.OPT_ROLLOUT_CHECK, 0)
+    ctx.reset_stats()
+    fast = run_episodes_batch(tasks, 64)
+    nfb = ctx.stat(L.STAT_ROLLOUT_FALLBACKS)
+    exact = run_episodes_batch(tasks, 64, exact=True)
+    for f, x in zip(fast, exact):
+        assert np.array_equal(f["idx"], x["idx"])
+        assert np.array_equal(f["actions"], x["actions"])
+        assert np.array_equal(f["score"], x["score"])
+        assert _close(f["logp"], x["logp"]) and _close(f["value"], x["value"])
+    steps = 12 * 1024 * 64
+    print(f"fallback knob decisions: {nfb} / {steps * 8}+")
+    assert nfb < 0.01 * steps
+
+
+def test_rollout_tc_certificate_check_mode(O, ctx):
+    """Check mode re-decides every knob exactly: certified fast decisions never
+    disagree, and the fast probabilities stay well inside the margin."""
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    tasks = []
+    for i, name in enumerate(["resnet_c2", "synthetic16"]):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=40 + i)
+        init = osp.random_valid(i, 256) if O.ref_available() else np.zeros((256, sp.num_knobs), np.int32)
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=0, root_seed=i))
+    ctx.reset_stats()
+    ctx.set_option(L.OPT_ROLLOUT_CHECK, 1)
+    try:
+        out = run_episodes_batch(tasks, 20)
+    finally:
+        ctx.set_option(L.OPT_ROLLOUT_CHECK, 0)
+    checked = ctx.stat(L.STAT_ROLLOUT_CHECKED)
+    assert checked == 256 * 20 * (8 + 16)
+    assert ctx.stat(L.STAT_ROLLOUT_MISMATCH) == 0
+    maxerr = ctx.stat(L.STAT_ROLLOUT_MAXERR) * 1e-12
+    print(f"max |p_fast - p_exact| = {maxerr:.3e}")
+    assert maxerr < 2 ** -18
+    ref = run_episodes_batch(tasks, 20, exact=True)
+    for o, r in zip(out, ref):
+        assert np.array_equal(o["idx"], r["idx"])
