@@ -42,31 +42,39 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
+
+    nvidia-smi is started (and its first sample awaited) BEFORE the warm-up:
+    its start-up stalls GPU work for a few hundred ms, which must not land in
+    the timed region. summary() keeps the samples taken inside [t0, t1]."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, period_ms: int = 50):
         self.gpu = gpu
+        self.period_ms = period_ms
         self.proc = None
-        self.lines = []
+        self.lines = []  # (perf_counter, line)
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 10:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc:
@@ -76,10 +84,12 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t0=None, t1=None):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
+            if t0 is not None and not (t0 <= ts <= t1):
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -229,7 +239,7 @@ def kmeans_secondary(ctx, args, cpu=True):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tasks", type=int, default=12)
@@ -244,6 +254,7 @@ def main():
     ap.add_argument("--no-kmeans", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--exact", action="store_true", help="exact fp64 rollout kernel instead of the tcgen05 path")
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -283,8 +294,9 @@ def main():
     dev_out = [dict(idx=mkd((E, T + 1, D0), torch.uint16), score=mkd((E, T + 1), torch.float64),
                     actions=mkd((E, T, D0), torch.int8), logp=mkd((E, T), torch.float64),
                     value=mkd((E, T), torch.float64)) for _ in specs]  # persistent trajectory buffers
+    clk = ClockSampler(local).__enter__()  # before the warm-up: nvidia-smi start-up stalls the GPU
     for _ in range(args.warmup):
-        run_episodes_batch(tasks, T, ctx, host_out=dev_out)
+        run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact)
     torch.cuda.synchronize()
 
     def barrier():
@@ -295,18 +307,22 @@ def main():
     ctx.set_option(L.OPT_PROFILE, 1)
     ctx.reset_stats()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        start.record(stream)
-        for _ in range(args.steps):
-            flush.zero_()
-            run_episodes_batch(tasks, T, ctx, host_out=dev_out)
-        end.record(stream)
-        barrier()
+    barrier()
+    tc0 = time.perf_counter()
+    start.record(stream)
+    for _ in range(args.steps):
+        flush.zero_()  # 256 MB > L2 between timed steps
+        run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact)
+    end.record(stream)
+    barrier()
+    tc1 = time.perf_counter()
+    clk.__exit__()
+    clocks = clk.summary(tc0, tc1)
     ms = start.elapsed_time(end)
     launches = ctx.stat(L.STAT_LAUNCHES)
     roll_ns, roll_calls = ctx.stat(L.STAT_ROLLOUT_NS), ctx.stat(L.STAT_ROLLOUT_CALLS)
     gbt_ns, gbt_calls = ctx.stat(L.STAT_GBT_NS), ctx.stat(L.STAT_GBT_CALLS)
+    fallbacks, tc_steps = ctx.stat(L.STAT_ROLLOUT_FALLBACKS), ctx.stat(L.STAT_ROLLOUT_TC)
     ctx.set_option(L.OPT_PROFILE, 0)
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -342,11 +358,11 @@ def main():
         htasks = [RolloutTask(d, a, g, hi, episode_offset=rank * E, root_seed=s.seed)
                   for s, d, a, g, hi in zip(specs, spaces, agents, gbts, host_init)]
         ctx.set_stream(None)
-        run_episodes_batch(htasks, T, ctx, host_out=host_out)  # warm
+        run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact)  # warm
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            run_episodes_batch(htasks, T, ctx, host_out=host_out)
+            run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact)
         barrier()
         dt = time.perf_counter() - t0
         if world > 1:
@@ -379,21 +395,31 @@ def main():
             "metric": "candidate configs scored/sec (rollout+cost model)",
             "value": value, "unit": "config-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if args.exact else "f32 (fp16 hi/lo tcgen05 MLP, fp32 accum) + f64 (scores, certified fallback)",
             "data": "synthetic (seeded AutoTVM-style ResNet-18 conv spaces, SyntheticBackend-fitted GBT, seeded agent)",
             "config": {"workload": "resnet18-12tasks-rollout (BASELINE configs[1])", "tasks": len(specs),
                        "episodes_per_task_per_gpu": E, "T": T, "knobs": n_knobs, "hidden": [128, 64],
-                       "gbt": "50 trees depth<=4", "path": "exact fp64 (bit-exact with the oracle)",
+                       "gbt": "50 trees depth<=4",
+                       "path": ("exact fp64 kernel (bit-exact with the oracle)" if args.exact else
+                                "tcgen05 rollout, certified sampling: configs/actions/scores bit-exact with the "
+                                "oracle, logp/value fp32-accurate"),
                        "l2": "256 MB buffer written between timed steps; outputs 1.2 GB/step > L2",
                        "parallelism": f"dp{world} (episodes sharded, no collective)"},
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "rollout_kernel",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "rollout_kernel" if args.exact else "rollout_tc_kernel",
                          "kernel_ms": roll_s * 1e3, "flop_per_config_step": flop,
                          "peak_source": f"{peak_src} bf16_tflops_sustained",
-                         "note": "exact path runs on the FP64 pipe (SIMT, no FMA); tensor-pipe fraction reported against bf16 as BASELINE.md asks"},
+                         "note": ("exact path runs on the FP64 pipe (SIMT); tensor-pipe fraction reported against bf16"
+                                  if args.exact else
+                                  "algorithmic MLP FLOPs counted once; the kernel issues 3x (fp16 hi/lo split) "
+                                  "tcgen05 work plus 256 tanh/config-step on the SFU (epilogue-bound, DESIGN.md §5.6)")},
+            "rollout_fallbacks": {"knob_decisions_redecided_exactly": fallbacks, "config_steps": tc_steps,
+                                  "per_config_step": fallbacks / max(1, tc_steps)},
             "gbt_kernel_ms_per_step": gbt_ns / max(1, gbt_calls) * 1e-6 * len(specs),
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "secondary": kmeans,

@@ -300,6 +300,9 @@ int ktune_synthesize_sample(const ktune_space* space, const int32_t* cand_idx, i
  * (op 0 exp, 1 log, 2 tanh) on n host doubles — lets tests pin
  * the device implementation bit-for-bit against the oracle's. */
 int ktune_debug_math(ktune_ctx* ctx, int op, const double* x, int64_t n, double* out);
+/* Copies the tcgen05 rollout's device counters and, after a run with
+ * KTUNE_OPT_ROLLOUT_CHECK = 2, its per-phase clock trace (4 + 128 u64). */
+int ktune_debug_trace(ktune_ctx* ctx, unsigned long long* out);
 
 #ifdef __cplusplus
 }

@@ -44,8 +44,9 @@
 namespace {
 
 constexpr int kH = 128, kG = 64;  // hidden sizes of the tensor-core path
-constexpr int kSlots = 4;
+constexpr int kSlots = 3;  // 3 x 128 episodes per SM: 384 threads, up to 168 registers each
 constexpr int kThr = kSlots * 128;
+constexpr int kMaxWarps = kSlots * 4;
 constexpr int kTcMaxN = 21;       // 3n <= 64: the L3 accumulator stays clear of hv's TMEM columns
 constexpr int kMaxTcTasks = 12;
 constexpr float kActScale = 16384.f;  // 2^14 activation scale inside the fp16 operands
@@ -101,12 +102,13 @@ __device__ __forceinline__ float lg2f(float x) {
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// scale * tanh(x) = sign(x) * scale * (1 - e) / (1 + e), e = exp(-2|x|); abs error ~1e-7 * scale
-__device__ __forceinline__ float tanh_scaled(float x, float scale) {
-  const float e = ex2f(fabsf(x) * -2.8853900817779268f);
-  const float r = rcpf(1.0f + e);
-  const float t = __fmul_rn(fmaf(-e, scale, scale), r);
-  return copysignf(t, x);
+// S * tanh(x) from y = -2 log2(e) x (the scale is folded into the
+// pre-activation FMA): e = exp(-2x), S tanh(x) = 2S/(1 + e) - S. Two SFU ops;
+// absolute error ~4e-7 * S (x -> -inf: e = inf, 1/(1+e) = 0 -> -S).
+constexpr float kK2L = -2.8853900817779268f;  // -2 log2(e)
+__device__ __forceinline__ float act_scaled(float y, float S) {
+  const float r = rcpf(1.0f + ex2f(y));
+  return fmaf(r, 2.f * S, -S);
 }
 
 __device__ __forceinline__ uint32_t h2bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
@@ -126,23 +128,28 @@ __device__ __forceinline__ void store8_split(unsigned char* Ab, int r, int k0, c
   *reinterpret_cast<uint4*>(Ab + kt::tc::kmajor_offset(r, 64 + k0, 128)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
 }
 
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 f = __half22float2(h);
+  hi = h2bits(h);
+  lo = h2bits(__floats2half2_rn(__fsub_rn(a, f.x), __fsub_rn(b, f.y)));
+}
+
 __device__ __forceinline__ void sync_slot(int slot) {
   kt::tc::fence_proxy_async();
   kt::tc::fence_before();
   kt::tc::named_bar(1 + slot, 128);
 }
 
-// Three-product split GEMM: K = 16 * nkb per operand half.
-// A hi chunk kb at Ab + kb*256, lo at Ab + 1024 + kb*256 (SBO 2048);
-// B hi chunk c at B + c*256, lo at B + blo + c*256 (SBO bsbo).
-__device__ __forceinline__ void mma_split(uint32_t d, uint32_t a, uint32_t b, uint32_t blo, uint32_t bsbo,
-                                          int c0, int nkb, uint32_t idesc, bool accumulate) {
-#pragma unroll 1
-  for (int kb = 0; kb < nkb; ++kb) {
-    const uint64_t ahi = kt::tc::smem_desc(a + kb * 256, 128, 2048);
-    const uint64_t alo = kt::tc::smem_desc(a + 1024 + kb * 256, 128, 2048);
-    const uint64_t bhi = kt::tc::smem_desc(b + (c0 + kb) * 256, 128, bsbo);
-    const uint64_t bl = kt::tc::smem_desc(b + blo + (c0 + kb) * 256, 128, bsbo);
+// Three-product split GEMM over 4 K chunks of 16: hi*hi + hi*lo + lo*hi.
+// Descriptors are precomputed: +16 in the address field = +256 bytes.
+// A: hi chunk kb at +kb*16, lo at +64 (1024 B); B: chunk c at +c*16, lo at +blo16.
+__device__ __forceinline__ void mma_split4(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t blo16, int c0,
+                                           uint32_t idesc, bool accumulate) {
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) {
+    const uint64_t ahi = adesc + 16 * kb, alo = adesc + 64 + 16 * kb;
+    const uint64_t bhi = bdesc + 16 * (c0 + kb), bl = bdesc + blo16 + 16 * (c0 + kb);
     kt::tc::mma_f16(d, ahi, bhi, idesc, (accumulate || kb > 0) ? 1u : 0u);
     kt::tc::mma_f16(d, ahi, bl, idesc, 1u);
     kt::tc::mma_f16(d, alo, bhi, idesc, 1u);
@@ -190,8 +197,7 @@ struct Redecided {
 template <int NMAX>
 __device__ __noinline__ Redecided exact_redecide(const TcTask& tk, int t, int L, uint32_t fm, Cfg<NMAX> cfg,
                                                  const int* scard, double* sh0, double* shp, double* slg,
-                                                 int64_t ge_L, uint64_t acts, const float* fast_p0,
-                                                 const float* fast_c1, uint32_t fast_cert,
+                                                 int64_t ge_L, uint64_t acts, const float* fastp, uint32_t fast_cert,
                                                  unsigned long long* stats) {
   float lp_exact = 0.f;
   const int lane = threadIdx.x & 31;
@@ -248,7 +254,7 @@ __device__ __noinline__ Redecided exact_redecide(const TcTask& tk, int t, int L,
       const double c1 = kt::dadd(k3.p[0], k3.p[1]);
       const int ae = u < k3.p[0] ? 0 : (u < c1 ? 1 : 2);
       if (stats) {  // check mode: compare against the fast decision
-        const float err = fmaxf(fabsf((float)(fast_p0[d] - k3.p[0])), fabsf((float)(fast_c1[d] - c1)));
+        const float err = fmaxf(fabsf((float)(fastp[2 * d] - k3.p[0])), fabsf((float)(fastp[2 * d + 1] - c1)));
         atomicMax(reinterpret_cast<unsigned int*>(stats + 3), __float_as_uint(err));
         if ((fast_cert >> d) & 1u) {
           const int af = (int)((acts >> (2 * d)) & 3u);
@@ -324,9 +330,9 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
     }
     for (int i = tid; i < kNF32; i += kThr) {
       float v = 0.f;
-      if (i < 128) v = (float)P[ob0 + i];
-      else if (i < 192) v = (float)P[obp1 + i - 128];
-      else if (i < 256) v = (float)P[obv1 + i - 192];
+      if (i < 128) v = (float)(P[ob0 + i] * (double)kK2L);  // tanh layers: bias * -2log2(e)
+      else if (i < 192) v = (float)(P[obp1 + i - 128] * (double)kK2L);
+      else if (i < 256) v = (float)(P[obv1 + i - 192] * (double)kK2L);
       else if (i < 320) v = (float)P[owv2 + i - 256];
       else if (i < 384) v = i - 320 < 3 * n ? (float)P[obp2 + i - 320] : 0.f;
       else if (i == 384) v = (float)P[obv2];
@@ -357,13 +363,19 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
     const uint32_t tslot = tbase_sh + (uint32_t)(128 * slot);
     const bool leader = q == 0 && lane == 0;
     uint64_t* mb = &mbar[slot];
-    const float sc1 = ldexpf(1.f, -tk.e1), sc2 = ldexpf(1.f, -(14 + tk.e2)), sc3 = ldexpf(1.f, -(14 + tk.e3));
+    // pre-activation scales (with -2log2(e) folded in for the tanh layers)
+    const float sc1 = ldexpf(kK2L, -tk.e1), sc2 = ldexpf(kK2L, -(14 + tk.e2)), sc3 = ldexpf(1.f, -(14 + tk.e3));
     const uint32_t id128 = kt::tc::idesc_f16_f32(128, 128), idn3 = kt::tc::idesc_f16_f32(128, N3);
-    const uint32_t b1 = kt::tc::smem_u32(B1), b2 = kt::tc::smem_u32(B2), b3 = kt::tc::smem_u32(B3);
+    const uint64_t ad0 = kt::tc::smem_desc(a_addr, 128, 2048);
+    const uint64_t b1d = kt::tc::smem_desc(kt::tc::smem_u32(B1), 128, (K1 / 8) * 128);
+    const uint64_t b2d = kt::tc::smem_desc(kt::tc::smem_u32(B2), 128, 4096);
+    const uint64_t b3d = kt::tc::smem_desc(kt::tc::smem_u32(B3), 128, 2048);
     const uint64_t ge = (uint64_t)(tk.episode_offset + e);
-    double* sh0 = reinterpret_cast<double*>(Ab + (4 * q) * 2048 + 1024);
-    double* shp = reinterpret_cast<double*>(Ab + (4 * q + 1) * 2048 + 1024);
-    double* slg = reinterpret_cast<double*>(Ab + (4 * q + 2) * 2048 + 1024);
+    // exact re-decision scratch: the warp's own 8 KB of the operand buffer (its
+    // rows' row groups), free between the L3 MMA and the next step's L1 operand
+    double* sh0 = reinterpret_cast<double*>(Ab + 8192 * q);
+    double* shp = reinterpret_cast<double*>(Ab + 8192 * q + 1024);
+    double* slg = reinterpret_cast<double*>(Ab + 8192 * q + 1536);
 
     Cfg<NMAX> cfg;
 #pragma unroll
@@ -375,7 +387,12 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       store_row_idx(tk.idx + e * (int64_t)(T + 1) * n, cfg, n);
     }
     uint32_t ph = 0;
+    const bool trace_cta = L.check == 2 && blockIdx.x == 0 && q == 0 && lane == 0;
+#define TR(k)                                                                                  \
+  if (trace_cta && (t == 200 || t == 201))                                                      \
+    L.counters[4 + (slot * 2 + (t - 200)) * 16 + (k)] = (unsigned long long)clock64();
     for (int t = 0; t < T; ++t) {
+      TR(0)
       // ---- L1 operand: [idx | idx] as fp16 (exact integers)
       if (lw) {
 #pragma unroll
@@ -394,143 +411,169 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         }
       }
       sync_slot(slot);
+      TR(1)
       if (leader) {
         kt::tc::fence_after();
-        for (int kb = 0; kb < K1 / 16; ++kb)
-          kt::tc::mma_f16(tslot, kt::tc::smem_desc(a_addr + kb * 256, 128, 2048),
-                          kt::tc::smem_desc(b1 + kb * 256, 128, (K1 / 8) * 128), id128, kb > 0);
+        for (int kb = 0; kb < K1 / 16; ++kb) kt::tc::mma_f16(tslot, ad0 + 16 * kb, b1d + 16 * kb, id128, kb > 0);
         kt::tc::commit(mb);
       }
-      float hb[64];
+      uint32_t raw[64];
+      float ufs[NMAX];  // this step's counter-RNG draws, computed while the L1 MMA runs
       if (lw) {
+#pragma unroll
+        for (int d = 0; d < NMAX; ++d) {
+          const uint64_t hsh = kt::mix64(tk.seed ^ kt::mix64((ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n +
+                                                             (uint64_t)d + 0x9E3779B97F4A7C15ULL));
+          ufs[d] = (float)(uint32_t)(hsh >> 40) * 0x1.0p-24f;  // |uf - u| < 2^-24
+        }
         kt::tc::mbar_wait(mb, ph);
         kt::tc::fence_after();
-        // ---- L1 epilogue: h0 = tanh(acc * 2^-e1 + b0); units 0..63 -> operand, 64..127 held
+        TR(2)
+        // ---- L1 epilogue, units 0..63: h0 = tanh(W0 x + b0) -> L2 operand (K half 0)
 #pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          uint32_t v[32];
-          kt::tc::ld_32x32b_x32(tcol + c0, v);
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint32_t v[16];
+          kt::tc::ld_32x32b_x16(tcol + c0, v);
           kt::tc::ld_wait();
-          float hv[32];
+          float hv[16];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) hv[j] = tanh_scaled(fmaf(__uint_as_float(v[j]), sc1, sb0[c0 + j]), kActScale);
-          if (c0 < 64) {
-#pragma unroll
-            for (int m = 0; m < 4; ++m) store8_split(Ab, r, c0 + 8 * m, hv + 8 * m);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) hb[c0 - 64 + j] = hv[j];
-          }
+          for (int j = 0; j < 16; ++j) hv[j] = act_scaled(fmaf(__uint_as_float(v[j]), sc1, sb0[c0 + j]), kActScale);
+          store8_split(Ab, r, c0, hv);
+          store8_split(Ab, r, c0 + 8, hv + 8);
         }
+        // units 64..127: raw accumulators to registers before L2 overwrites the columns
+        uint32_t* r0 = raw;
+        kt::tc::ld_32x32b_x32(tcol + 64, *reinterpret_cast<uint32_t(*)[32]>(r0));
+        kt::tc::ld_32x32b_x32(tcol + 96, *reinterpret_cast<uint32_t(*)[32]>(r0 + 32));
+        kt::tc::ld_wait();
       }
       ph ^= 1;
+      TR(3)
       sync_slot(slot);
+      TR(4)
       if (leader) {  // L2, K half 0
         kt::tc::fence_after();
-        mma_split(tslot, a_addr, b2, 2048, 4096, 0, 4, id128, false);
+        mma_split4(tslot, ad0, b2d, 128, 0, id128, false);
         kt::tc::commit(mb);
       }
       if (lw) {
+        // units 64..127 while the L2 MMAs run: tanh + hi/lo split in registers
+#pragma unroll
+        for (int j = 0; j < 64; j += 2) {
+          const float a = act_scaled(fmaf(__uint_as_float(raw[j]), sc1, sb0[64 + j]), kActScale);
+          const float b = act_scaled(fmaf(__uint_as_float(raw[j + 1]), sc1, sb0[65 + j]), kActScale);
+          split2(a, b, raw[j], raw[j + 1]);  // raw[j] = hi pair, raw[j+1] = lo pair
+        }
+        TR(5)
         kt::tc::mbar_wait(mb, ph);
         kt::tc::fence_after();
+        TR(6)
 #pragma unroll
-        for (int m = 0; m < 8; ++m) store8_split(Ab, r, 8 * m, hb + 8 * m);
-      }
-      ph ^= 1;
-      sync_slot(slot);
-      if (leader) {  // L2, K half 1
-        kt::tc::fence_after();
-        mma_split(tslot, a_addr, b2, 2048, 4096, 4, 4, id128, true);
-        kt::tc::commit(mb);
-      }
-      if (lw) {
-        kt::tc::mbar_wait(mb, ph);
-        kt::tc::fence_after();
-        // ---- L2 epilogue (policy half): hp -> L3 operand
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          uint32_t v[32];
-          kt::tc::ld_32x32b_x32(tcol + c0, v);
-          kt::tc::ld_wait();
-          float hv[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) hv[j] = tanh_scaled(fmaf(__uint_as_float(v[j]), sc2, sbp1[c0 + j]), kActScale);
-#pragma unroll
-          for (int m = 0; m < 4; ++m) store8_split(Ab, r, c0 + 8 * m, hv + 8 * m);
+        for (int m = 0; m < 8; ++m) {
+          *reinterpret_cast<uint4*>(Ab + kt::tc::kmajor_offset(r, 8 * m, 128)) =
+              make_uint4(raw[8 * m], raw[8 * m + 2], raw[8 * m + 4], raw[8 * m + 6]);
+          *reinterpret_cast<uint4*>(Ab + kt::tc::kmajor_offset(r, 64 + 8 * m, 128)) =
+              make_uint4(raw[8 * m + 1], raw[8 * m + 3], raw[8 * m + 5], raw[8 * m + 7]);
         }
       }
       ph ^= 1;
       sync_slot(slot);
+      TR(8)
+      if (leader) {  // L2, K half 1
+        kt::tc::fence_after();
+        mma_split4(tslot, ad0, b2d, 128, 4, id128, true);
+        kt::tc::commit(mb);
+      }
+      if (lw) {
+        kt::tc::mbar_wait(mb, ph);
+        kt::tc::fence_after();
+        TR(9)
+        // ---- L2 epilogue (policy half): hp -> L3 operand
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint32_t v[16];
+          kt::tc::ld_32x32b_x16(tcol + c0, v);
+          kt::tc::ld_wait();
+          float hv[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) hv[j] = act_scaled(fmaf(__uint_as_float(v[j]), sc2, sbp1[c0 + j]), kActScale);
+          store8_split(Ab, r, c0, hv);
+          store8_split(Ab, r, c0 + 8, hv + 8);
+        }
+      }
+      ph ^= 1;
+      sync_slot(slot);
+      TR(11)
       if (leader) {  // L3 logits (accumulator columns 0..N3-1; hv stays in 64..127)
         kt::tc::fence_after();
-        mma_split(tslot, a_addr, b3, 1024, 2048, 0, 4, idn3, false);
+        mma_split4(tslot, ad0, b3d, 64, 0, idn3, false);
         kt::tc::commit(mb);
       }
       if (lw) {
         // ---- L2 epilogue (value half), overlapping the L3 MMAs: v = wv2 . tanh(.) + bv2
         float vs = 0.f;
 #pragma unroll
-        for (int c0 = 64; c0 < 128; c0 += 32) {
-          uint32_t v[32];
-          kt::tc::ld_32x32b_x32(tcol + c0, v);
+        for (int c0 = 64; c0 < 128; c0 += 16) {
+          uint32_t v[16];
+          kt::tc::ld_32x32b_x16(tcol + c0, v);
           kt::tc::ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            vs = fmaf(swv2[c0 - 64 + j], tanh_scaled(fmaf(__uint_as_float(v[j]), sc2, sbv1[c0 - 64 + j]), 1.f), vs);
+          for (int j = 0; j < 16; ++j)
+            vs = fmaf(swv2[c0 - 64 + j], act_scaled(fmaf(__uint_as_float(v[j]), sc2, sbv1[c0 - 64 + j]), 1.f), vs);
         }
         if (lr && tk.value) tk.value[e * T + t] = (double)(vs + sbv2[0]);
+        TR(12)
         kt::tc::mbar_wait(mb, ph);
         kt::tc::fence_after();
+        TR(13)
         // ---- L3 epilogue: per-knob softmax, certified inverse-CDF draw, saturating move
-        constexpr int kLg = ((3 * NMAX + 15) / 16) * 16;
-        float lg[kLg];
+        uint64_t acts = 0;
+        uint32_t cert = 0;
+        float lpj = 0.f;
+        const float delta = L.delta;
+        float* fastp = reinterpret_cast<float*>(Ab + 8192 * q + 2048);  // check mode: fast p0/c1 per (row, knob)
 #pragma unroll
-        for (int c0 = 0; c0 < kLg; c0 += 16) {
-          if (c0 < N3) {
-            uint32_t v[16];
-            kt::tc::ld_32x32b_x16(tcol + c0, v);
+        for (int g = 0; g < NMAX / 8; ++g) {  // knob groups of 8: 24 logit columns
+          if (8 * g < n) {
+            uint32_t v[24];
+            kt::tc::ld_32x32b_x16(tcol + 24 * g, *reinterpret_cast<uint32_t(*)[16]>(v));
+            kt::tc::ld_32x32b_x8(tcol + 24 * g + 16, *reinterpret_cast<uint32_t(*)[8]>(v + 16));
             kt::tc::ld_wait();
 #pragma unroll
-            for (int j = 0; j < 16; ++j) lg[c0 + j] = fmaf(__uint_as_float(v[j]), sc3, sbp2[c0 + j]);
-          }
-        }
-        uint64_t acts = 0;
-        uint32_t fb = 0, cert = 0;
-        float lpj = 0.f;
-        float p0s[NMAX], c1s[NMAX];
-        const float delta = L.delta;
-#pragma unroll
-        for (int d = 0; d < NMAX; ++d) {
-          if (d < n) {
-            const float l0 = lg[3 * d], l1 = lg[3 * d + 1], l2 = lg[3 * d + 2];
-            const float m = fmaxf(l0, fmaxf(l1, l2));
-            const float e0 = ex2f((l0 - m) * 1.4426950408889634f), e1 = ex2f((l1 - m) * 1.4426950408889634f),
-                        e2 = ex2f((l2 - m) * 1.4426950408889634f);
-            const float s = e0 + e1 + e2;
-            const float rs = rcpf(s);
-            const float p0 = e0 * rs, c1 = (e0 + e1) * rs;
-            const uint64_t hsh =
-                kt::mix64(tk.seed ^ kt::mix64((ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n + (uint64_t)d +
-                                              0x9E3779B97F4A7C15ULL));
-            const float uf = (float)(uint32_t)(hsh >> 40) * 0x1.0p-24f;  // |uf - u| < 2^-24
-            const int a = uf < p0 ? 0 : (uf < c1 ? 1 : 2);
-            const bool ok = fabsf(uf - p0) > delta && fabsf(uf - c1) > delta;
-            acts |= (uint64_t)a << (2 * d);
-            if (L.check) {
-              p0s[d] = p0;
-              c1s[d] = c1;
-            }
-            if (ok) {
-              cert |= 1u << d;
-              lpj += (a == 0 ? l0 : (a == 1 ? l1 : l2)) - m - lg2f(s) * 0.69314718055994531f;
+            for (int dd = 0; dd < 8; ++dd) {
+              const int d = 8 * g + dd;
+              if (d < n) {
+                const float l0 = fmaf(__uint_as_float(v[3 * dd]), sc3, sbp2[3 * d]);
+                const float l1 = fmaf(__uint_as_float(v[3 * dd + 1]), sc3, sbp2[3 * d + 1]);
+                const float l2 = fmaf(__uint_as_float(v[3 * dd + 2]), sc3, sbp2[3 * d + 2]);
+                const float m = fmaxf(l0, fmaxf(l1, l2));
+                const float e0 = ex2f((l0 - m) * 1.4426950408889634f), e1 = ex2f((l1 - m) * 1.4426950408889634f),
+                            e2 = ex2f((l2 - m) * 1.4426950408889634f);
+                const float s = e0 + e1 + e2;
+                const float rs = rcpf(s);
+                const float p0 = e0 * rs, c1 = (e0 + e1) * rs;
+                const float uf = ufs[d];
+                const int a = uf < p0 ? 0 : (uf < c1 ? 1 : 2);
+                const bool ok = fabsf(uf - p0) > delta && fabsf(uf - c1) > delta;
+                acts |= (uint64_t)a << (2 * d);
+                if (L.check == 1) {
+                  fastp[(lane * NMAX + d) * 2] = p0;
+                  fastp[(lane * NMAX + d) * 2 + 1] = c1;
+                }
+                const float lpa = (a == 0 ? l0 : (a == 1 ? l1 : l2)) - m - lg2f(s) * 0.69314718055994531f;
+                cert |= ok ? 1u << d : 0u;
+                lpj += ok ? lpa : 0.f;  // branch-free; uncertain knobs add their exact log-probability later
+              }
             }
           }
         }
+        uint32_t fb;
+        TR(14)
         const uint32_t allk = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
-        fb = L.check ? allk : (allk & ~cert);
+        fb = L.check == 1 ? allk : (allk & ~cert);
         if (!lr) fb = 0;
-        n_fallback += L.check ? 0 : __popc(fb);
-        n_checked += L.check ? __popc(fb) : 0;
+        n_fallback += L.check == 1 ? 0 : __popc(fb);
+        n_checked += L.check == 1 ? __popc(fb) : 0;
         unsigned pend = __ballot_sync(0xffffffffu, fb != 0);
         float lpx = 0.f;
         while (pend) {
@@ -538,14 +581,14 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
           pend &= pend - 1;
           const uint32_t fm = __shfl_sync(0xffffffffu, fb, Lr);
           const int64_t geL = __shfl_sync(0xffffffffu, (long long)ge, Lr);
-          const Redecided rd = exact_redecide<NMAX>(tk, t, Lr, fm, cfg, scard, sh0, shp, slg, geL, acts, p0s, c1s,
-                                                    cert, L.check ? L.counters : nullptr);
+          const Redecided rd = exact_redecide<NMAX>(tk, t, Lr, fm, cfg, scard, sh0, shp, slg, geL, acts,
+                                                    fastp + Lr * NMAX * 2, cert, L.check == 1 ? L.counters : nullptr);
           if (lane == Lr) {
             acts = rd.acts;
             lpx = rd.lp;
           }
         }
-        if (L.check) lpj = lpx;  // every knob re-decided: exact log-probabilities
+        if (L.check == 1) lpj = lpx;  // every knob re-decided: exact log-probabilities
         else lpj += lpx;
         // saturating move (design_space.cpp:175-187) and the trajectory writes
         uint32_t apk[(NMAX + 3) / 4];
@@ -579,7 +622,9 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         }
       }
       ph ^= 1;
+      TR(15)
     }
+#undef TR
   }
   // counters
   for (int o = 16; o > 0; o >>= 1) {
@@ -632,8 +677,8 @@ void resolve_counters(ktune_ctx* ctx) {
 
 void rollout_tc(ktune_ctx* ctx, const std::vector<RolloutWork>& work, int T) {
   if (!ctx->d_counters) {
-    KT_CUDA(cudaMalloc(&ctx->d_counters, 4 * sizeof(unsigned long long)));
-    KT_CUDA(cudaMemsetAsync(ctx->d_counters, 0, 4 * sizeof(unsigned long long), ctx->stream));
+    KT_CUDA(cudaMalloc(&ctx->d_counters, (4 + 8 * 16) * sizeof(unsigned long long)));
+    KT_CUDA(cudaMemsetAsync(ctx->d_counters, 0, (4 + 8 * 16) * sizeof(unsigned long long), ctx->stream));
   }
   // Certification margin: fast-vs-exact probability error (calibrated with
   // KTUNE_OPT_ROLLOUT_CHECK) plus the 2^-24 draw truncation.
@@ -643,7 +688,7 @@ void rollout_tc(ktune_ctx* ctx, const std::vector<RolloutWork>& work, int T) {
   for (size_t t0 = 0; t0 < work.size(); t0 += kMaxTcTasks) {
     const size_t nt = std::min<size_t>(kMaxTcTasks, work.size() - t0);
     TcLaunch L{};
-    L.check = ctx->opt_rollout_check ? 1 : 0;
+    L.check = (int)ctx->opt_rollout_check;  // 2: phase trace (debug)
     L.delta = delta;
     L.counters = ctx->d_counters;
     // warps per task, then the smallest per-CTA warp count m whose CTA total fits one wave
@@ -655,9 +700,9 @@ void rollout_tc(ktune_ctx* ctx, const std::vector<RolloutWork>& work, int T) {
       wsum += W[k];
       nmax = std::max(nmax, work[t0 + k].ac->n);
     }
-    int m = 16;
-    if (wsum <= (int64_t)16 * S) {
-      for (m = 1; m < 16; ++m) {
+    int m = kMaxWarps;
+    if (wsum <= (int64_t)kMaxWarps * S) {
+      for (m = 1; m < kMaxWarps; ++m) {
         int64_t c = 0;
         for (size_t k = 0; k < nt; ++k) c += ceil_div(W[k], m);
         if (c <= S) break;
@@ -715,3 +760,11 @@ void rollout_tc(ktune_ctx* ctx, const std::vector<RolloutWork>& work, int T) {
 }
 
 }  // namespace kt
+
+extern "C" int ktune_debug_trace(ktune_ctx* ctx, unsigned long long* out) {
+  return kt_guard(ctx, [&] {
+    if (!ctx->d_counters) kt::fail(KTUNE_ERR_CONFIG, "no tcgen05 rollout has run on this context");
+    KT_CUDA(cudaStreamSynchronize(ctx->stream));
+    KT_CUDA(cudaMemcpy(out, ctx->d_counters, (4 + 8 * 16) * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  });
+}
