@@ -76,8 +76,10 @@ enum ktune_option {
   KTUNE_OPT_PROFILE = 3,     /* 1: bracket the hot kernels with CUDA events on their stream (KTUNE_STAT_*_NS) */
   KTUNE_OPT_ROLLOUT_DELTA = 4, /* certification margin of the tcgen05 rollout, in units of 1e-12
                                   (0 = default) */
-  KTUNE_OPT_ROLLOUT_CHECK = 5  /* 1: re-decide EVERY sampling decision exactly and count disagreements
+  KTUNE_OPT_ROLLOUT_CHECK = 5, /* 1: re-decide EVERY sampling decision exactly and count disagreements
                                   (calibration/verification mode, slow) */
+  KTUNE_OPT_ROLLOUT_FUSE_GBT = 6 /* 1: walk the GBT inside the tcgen05 rollout (during its MMA waits)
+                                    instead of a separate K1 launch; measured slower on B200, DESIGN.md §5.6 */
 };
 int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value);
 

@@ -277,6 +277,7 @@ int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value) {
     else if (option == KTUNE_OPT_PROFILE) ctx->opt_profile = value;
     else if (option == KTUNE_OPT_ROLLOUT_DELTA) ctx->opt_rollout_delta = value;
     else if (option == KTUNE_OPT_ROLLOUT_CHECK) ctx->opt_rollout_check = value;
+    else if (option == KTUNE_OPT_ROLLOUT_FUSE_GBT) ctx->opt_rollout_fuse_gbt = value;
     else kt::fail(KTUNE_ERR_CONFIG, "unknown option");
   });
 }

@@ -96,6 +96,7 @@ struct ktune_ctx {
   int64_t opt_profile = 0;
   int64_t opt_rollout_delta = 0;  // 1e-12 units, 0 = default
   int64_t opt_rollout_check = 0;
+  int64_t opt_rollout_fuse_gbt = 0;  // 1: GBT walk inside the rollout kernel instead of a separate K1
   static constexpr int kNumStats = 32;
   int64_t stats[kNumStats] = {0};
   unsigned long long* d_counters = nullptr;  // device counters of the tcgen05 rollout (4 x u64)
@@ -205,11 +206,14 @@ struct RolloutWork {
   int8_t* actions;
   double* logp;
   double* value;
+  const ktune_gbt* gbt;  // may be NULL
+  double* score;         // E x (T+1), may be NULL
+  bool scored = false;   // set by rollout_tc when the scores were fused into the rollout
 };
 // tcgen05 rollout (rollout_tc.cu): eligibility (h = 128, g = 64, n <= 21,
 // cardinalities <= 2049, representable weight scales) and the launch.
 bool rollout_tc_eligible(const ktune_ac* ac, const ktune_space* sp);
-void rollout_tc(ktune_ctx* ctx, const std::vector<RolloutWork>& work, int T);
+void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T);
 // Folds the device counters of the tcgen05 rollout into ctx->stats.
 void resolve_counters(ktune_ctx* ctx);
 }  // namespace kt

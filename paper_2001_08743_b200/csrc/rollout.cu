@@ -538,14 +538,16 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     // tcgen05 path with certified sampling unless the exact fp64 forward is
     // requested (or a task is outside the tensor-core path's shapes)
     bool use_tc = !(flags & KTUNE_F_EXACT_ROLLOUT);
+    std::vector<char> scored(num_tasks, 0);
     for (int k = 0; k < num_tasks && use_tc; ++k) use_tc = kt::rollout_tc_eligible(tasks[k].ac, tasks[k].space);
     if (use_tc) {
       std::vector<kt::RolloutWork> work(num_tasks);
       for (int k = 0; k < num_tasks; ++k)
-        work[k] = {tasks[k].space, tasks[k].ac,  dt[k].E,     dt[k].episode_offset, dt[k].seed,
-                   dt[k].init_idx, dt[k].idx,    dt[k].actions, dt[k].logp,         dt[k].value};
+        work[k] = {tasks[k].space, tasks[k].ac, dt[k].E,     dt[k].episode_offset, dt[k].seed, dt[k].init_idx,
+                   dt[k].idx,      dt[k].actions, dt[k].logp, dt[k].value,         tasks[k].gbt, io[k].d_score};
       kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
       kt::rollout_tc(ctx, work, T);
+      for (int k = 0; k < num_tasks; ++k) scored[k] = work[k].scored;
     }
     // exact path: one launch config for all tasks: smem sized for the largest task;
     // 64-episode tiles (2 per lane) when they fit, else 32
@@ -580,7 +582,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     // cost-model scores of every visited configuration (K1 over the trajectory)
     for (int k = 0; k < num_tasks; ++k) {
       const ktune_rollout_task& t = tasks[k];
-      if (t.gbt && io[k].d_score && t.num_episodes > 0)
+      if (t.gbt && io[k].d_score && t.num_episodes > 0 && !scored[k])
         kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx, 2, t.num_episodes * (int64_t)(T + 1), io[k].d_score);
     }
     if (!dev) {

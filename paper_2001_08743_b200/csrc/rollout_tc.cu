@@ -64,6 +64,12 @@ struct TcTask {
   double* value;
   int32_t cta_base, ctas, warps;  // CTAs [cta_base, cta_base + ctas) share warps = ceil(E/32)
   int32_t e1, e2, e3;             // power-of-two weight scales of L1, L2, L3
+  // fused cost-model scoring (K1 in the epilogue; gnode == nullptr: scored by a separate K1 launch)
+  const uint32_t* gnode;  // complete trees: (feature << 24) | t1 (ktune_gbt::d_inode_idx)
+  const double* gleaf;
+  int32_t ntrees, depth;
+  double gbase, glr;
+  double* score;  // E x (T+1)
 };
 
 struct TcLaunch {
@@ -84,7 +90,38 @@ __host__ __device__ inline int n3_of(int n) { return (3 * n + 15) & ~15; }
 __host__ __device__ inline uint32_t off_b3(int n) { return kOffB1 + 128u * 2 * nk_of(n) * 2; }
 __host__ __device__ inline uint32_t off_f32(int n) { return off_b3(n) + (uint32_t)n3_of(n) * 256; }
 constexpr int kNF32 = 128 + 64 + 64 + 64 + 64 + 4;  // b0 bp1 bv1 wv2 bp2 bv2
-__host__ __device__ inline uint32_t tc_smem_bytes(int n) { return off_f32(n) + kNF32 * 4 + 1024; }
+__host__ __device__ inline uint32_t off_gbt(int n) { return (off_f32(n) + kNF32 * 4 + 15) & ~15u; }
+// + fused GBT: leaves f64 [ntrees][2^depth], node words u32 [ntrees][2^depth - 1], then the
+// thread-private knob columns int32 [n][kThr] the tree walks index (conflict-free).
+__host__ __device__ inline uint32_t gbt_leaf_bytes(int ntrees, int depth) { return (uint32_t)ntrees * (8u << depth); }
+__host__ __device__ inline uint32_t gbt_node_bytes(int ntrees, int depth) {
+  return ((uint32_t)ntrees * 4u * ((1u << depth) - 1) + 15) & ~15u;
+}
+__host__ __device__ inline uint32_t tc_smem_bytes(int n, int ntrees, int depth) {
+  const uint32_t g = ntrees > 0 ? gbt_leaf_bytes(ntrees, depth) + gbt_node_bytes(ntrees, depth) + (uint32_t)n * kThr * 4 : 0;
+  return off_gbt(n) + g + 1024;
+}
+
+// Partial GBT walk over trees [t0, t1): s += leaf_t(x) in tree order. The full
+// score base + lr * s is bit-exact with cost_model.cpp:179-187 and K1.
+// col: this thread's knob column (col[d * kThr]); node word = (byte offset of column d) << 16 | t1.
+__device__ __forceinline__ double gbt_walk(double s, const uint32_t* __restrict__ s_node,
+                                           const double* __restrict__ s_leaf, const unsigned char* col, int t0,
+                                           int t1, int depth) {
+  const int NI = (1 << depth) - 1, NL = 1 << depth;
+#pragma unroll 2
+  for (int tr = t0; tr < t1; ++tr) {
+    const uint32_t* tn = s_node + tr * NI;
+    int nd = 0;
+    for (int l = 0; l < depth; ++l) {
+      const uint32_t w = tn[nd];
+      const int v = *reinterpret_cast<const int*>(col + (w >> 16));
+      nd = 2 * nd + 1 + (v >= (int)(w & 0xFFFFu) ? 1 : 0);
+    }
+    s = kt::dadd(s, s_leaf[tr * NL + (nd - NI)]);
+  }
+  return s;
+}
 
 // ---------------------------------------------------------------- fast math
 __device__ __forceinline__ float ex2f(float x) {
@@ -339,6 +376,18 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       f32[i] = v;
     }
   }
+  double* s_leaf = reinterpret_cast<double*>(sm + off_gbt(n));
+  uint32_t* s_node = reinterpret_cast<uint32_t*>(sm + off_gbt(n) + (tk.gnode ? gbt_leaf_bytes(tk.ntrees, tk.depth) : 0));
+  int32_t* s_col = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(s_node) +
+                                              (tk.gnode ? gbt_node_bytes(tk.ntrees, tk.depth) : 0));
+  if (tk.gnode) {
+    const int NI = (1 << tk.depth) - 1, NL = 1 << tk.depth;
+    for (int i = tid; i < tk.ntrees * NL; i += kThr) s_leaf[i] = tk.gleaf[i];
+    for (int i = tid; i < tk.ntrees * NI; i += kThr) {
+      const uint32_t wd = tk.gnode[i];
+      s_node[i] = ((uint32_t)((wd >> 24) * kThr * 4) << 16) | min(wd & 0xFFFFFFu, 0xFFFFu);
+    }
+  }
   if (w == 0) kt::tc::tmem_alloc(&tbase_sh, 512);
   if (tid == 0) {
     for (int s = 0; s < kSlots; ++s) kt::tc::mbar_init(&mbar[s], 1);
@@ -386,6 +435,13 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         if (d < n) cfg.set(d, tk.init_idx[e * n + d]);
       store_row_idx(tk.idx + e * (int64_t)(T + 1) * n, cfg, n);
     }
+    const unsigned char* mycol = reinterpret_cast<const unsigned char*>(s_col + tid);
+    if (tk.gnode) {
+#pragma unroll
+      for (int d = 0; d < NMAX; ++d)
+        if (d < n) s_col[d * kThr + tid] = cfg.get(d);
+    }
+    const int gh = tk.ntrees / 2;  // the walk of row t runs in two halves inside step t's MMA waits
     uint32_t ph = 0;
     const bool trace_cta = L.check == 2 && blockIdx.x == 0 && q == 0 && lane == 0;
 #define TR(k)                                                                                  \
@@ -418,6 +474,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         kt::tc::commit(mb);
       }
       uint32_t raw[64];
+      double gs = 0.0;
       float ufs[NMAX];  // this step's counter-RNG draws, computed while the L1 MMA runs
       if (lw) {
 #pragma unroll
@@ -426,6 +483,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
                                                              (uint64_t)d + 0x9E3779B97F4A7C15ULL));
           ufs[d] = (float)(uint32_t)(hsh >> 40) * 0x1.0p-24f;  // |uf - u| < 2^-24
         }
+        if (tk.gnode) gs = gbt_walk(0.0, s_node, s_leaf, mycol, 0, gh, tk.depth);  // fused K1, row t
         kt::tc::mbar_wait(mb, ph);
         kt::tc::fence_after();
         TR(2)
@@ -485,6 +543,10 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         kt::tc::commit(mb);
       }
       if (lw) {
+        if (tk.gnode) {  // fused K1, row t: second half of the walk while the L2 MMAs run
+          gs = gbt_walk(gs, s_node, s_leaf, mycol, gh, tk.ntrees, tk.depth);
+          if (lr) tk.score[e * (int64_t)(T + 1) + t] = kt::dadd(tk.gbase, kt::dmul(tk.glr, gs));
+        }
         kt::tc::mbar_wait(mb, ph);
         kt::tc::fence_after();
         TR(9)
@@ -604,6 +666,11 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
             apk[d >> 2] |= (uint32_t)(uint8_t)(int8_t)(a - 1) << (8 * (d & 3));
           }
         }
+        if (tk.gnode) {  // the new configuration (row t+1) for the next step's fused walk
+#pragma unroll
+          for (int d = 0; d < NMAX; ++d)
+            if (d < n) s_col[d * kThr + tid] = cfg.get(d);
+        }
         if (lr) {
           store_row_idx(tk.idx + (e * (int64_t)(T + 1) + t + 1) * n, cfg, n);
           if (tk.actions) {
@@ -625,6 +692,9 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       TR(15)
     }
 #undef TR
+    if (tk.gnode && lr)  // row T
+      tk.score[e * (int64_t)(T + 1) + T] =
+          kt::dadd(tk.gbase, kt::dmul(tk.glr, gbt_walk(0.0, s_node, s_leaf, mycol, 0, tk.ntrees, tk.depth)));
   }
   // counters
   for (int o = 16; o > 0; o >>= 1) {
@@ -675,7 +745,7 @@ void resolve_counters(ktune_ctx* ctx) {
       std::max<int64_t>(ctx->stats[KTUNE_STAT_ROLLOUT_MAXERR], (int64_t)std::llround((double)mx * 1e12));
 }
 
-void rollout_tc(ktune_ctx* ctx, const std::vector<RolloutWork>& work, int T) {
+void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T) {
   if (!ctx->d_counters) {
     KT_CUDA(cudaMalloc(&ctx->d_counters, (4 + 8 * 16) * sizeof(unsigned long long)));
     KT_CUDA(cudaMemsetAsync(ctx->d_counters, 0, (4 + 8 * 16) * sizeof(unsigned long long), ctx->stream));
@@ -742,6 +812,20 @@ void rollout_tc(ktune_ctx* ctx, const std::vector<RolloutWork>& work, int T) {
       for (int i = owp1; i < obp1; ++i) m2 = std::max(m2, std::fabs(p[i]));
       for (int i = owv1; i < obv1; ++i) m2 = std::max(m2, std::fabs(p[i]));
       for (int i = owp2; i < obp2; ++i) m3 = std::max(m3, std::fabs(p[i]));
+      // optional fused scoring (complete-tree index layout that fits in shared memory)
+      const ktune_gbt* g = rw.gbt;
+      tk.gnode = nullptr;
+      if (g && rw.score && g->has_space && g->complete && g->d_inode_idx && g->depth <= 8 &&
+          tc_smem_bytes(n, g->num_trees, g->depth) <= 227 * 1024 && ctx->opt_rollout_fuse_gbt) {
+        tk.gnode = g->d_inode_idx;
+        tk.gleaf = g->d_leaf;
+        tk.ntrees = g->num_trees;
+        tk.depth = g->depth;
+        tk.gbase = g->base;
+        tk.glr = g->lr;
+        tk.score = rw.score;
+        work[t0 + k].scored = true;
+      }
       tk.e1 = pow2_scale(m1);
       tk.e2 = pow2_scale(m2);
       tk.e3 = pow2_scale(m3);
@@ -751,7 +835,10 @@ void rollout_tc(ktune_ctx* ctx, const std::vector<RolloutWork>& work, int T) {
     }
     L.num_tasks = nl;
     if (ctas == 0 || T == 0) continue;
-    const size_t smem = tc_smem_bytes(nmax);
+    size_t smem = 0;
+    for (int k = 0; k < nl; ++k)
+      smem = std::max<size_t>(smem, tc_smem_bytes(L.task[k].n, L.task[k].gnode ? L.task[k].ntrees : 0,
+                                                   L.task[k].depth));
     auto kern = nmax <= 8 ? rollout_tc_kernel<8> : (nmax <= 16 ? rollout_tc_kernel<16> : rollout_tc_kernel<24>);
     KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)ctas, kThr, smem, ctx->stream>>>(L);

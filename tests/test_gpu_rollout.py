@@ -173,3 +173,23 @@ def test_rollout_tc_certificate_check_mode(O, ctx):
     ref = run_episodes_batch(tasks, 20, exact=True)
     for o, r in zip(out, ref):
         assert np.array_equal(o["idx"], r["idx"])
+
+
+def test_rollout_tc_fused_scores_equal_unfused(O, ctx):
+    """GBT walk fused into the rollout epilogue vs the separate K1 launch: identical scores."""
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    tasks = []
+    for i, name in enumerate(["resnet_c2", "synthetic16", "resnet_dense_u16"]):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=60 + i)
+        init = osp.random_valid(i, 300) if O.ref_available() else np.zeros((300, sp.num_knobs), np.int32)
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=7, root_seed=i))
+    sep = run_episodes_batch(tasks, 33)
+    ctx.set_option(L.OPT_ROLLOUT_FUSE_GBT, 1)
+    try:
+        fused = run_episodes_batch(tasks, 33)
+    finally:
+        ctx.set_option(L.OPT_ROLLOUT_FUSE_GBT, 0)
+    for f, s_ in zip(fused, sep):
+        assert np.array_equal(f["idx"], s_["idx"])
+        assert np.array_equal(f["score"], s_["score"])
