@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         kt::tc::fence_after();
         TR(2)
         // ---- L1 epilogue, units 0..63: h0 = tanh(W0 x + b0) -> L2 operand (K half 0)
-#pragma unroll
+#pragma unroll 1
         for (int c0 = 0; c0 < 64; c0 += 16) {
           uint32_t v[16];
           kt::tc::ld_32x32b_x16(tcol + c0, v);
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         kt::tc::fence_after();
         TR(9)
         // ---- L2 epilogue (policy half): hp -> L3 operand
-#pragma unroll
+#pragma unroll 1
         for (int c0 = 0; c0 < 64; c0 += 16) {
           uint32_t v[16];
           kt::tc::ld_32x32b_x16(tcol + c0, v);
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       if (lw) {
         // ---- L2 epilogue (value half), overlapping the L3 MMAs: v = wv2 . tanh(.) + bv2
         float vs = 0.f;
-#pragma unroll
+#pragma unroll 1
         for (int c0 = 64; c0 < 128; c0 += 16) {
           uint32_t v[16];
           kt::tc::ld_32x32b_x16(tcol + c0, v);
@@ -650,6 +650,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
             lpx = rd.lp;
           }
         }
+        TR(7)
         if (L.check == 1) lpj = lpx;  // every knob re-decided: exact log-probabilities
         else lpj += lpx;
         // saturating move (design_space.cpp:175-187) and the trajectory writes
@@ -671,6 +672,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
           for (int d = 0; d < NMAX; ++d)
             if (d < n) s_col[d * kThr + tid] = cfg.get(d);
         }
+        TR(10)
         if (lr) {
           store_row_idx(tk.idx + (e * (int64_t)(T + 1) + t + 1) * n, cfg, n);
           if (tk.actions) {

@@ -31,10 +31,10 @@ buf = np.zeros(4 + 128, np.uint64)
 lib.ktune_debug_trace.restype = C.c_int
 ctx.check(lib.ktune_debug_trace(ctx.h, buf.ctypes.data_as(C.c_void_p)))
 tr = buf[4:].reshape(8, 16).astype(np.int64)
-names = ["start", "bar1", "L1 wait", "L1 epi a", "bar2", "epi b", "L2a wait", "-", "bar3", "L2b wait", "-", "bar4",
+names = ["start", "bar1", "L1 wait", "L1 epi a", "bar2", "epi b", "L2a wait", "fallbk", "bar3", "L2b wait", "apply", "bar4",
          "value", "L3 wait", "knobs", "end"]
 for row in range(8):
     s = tr[row]
     if s[0] == 0: continue
     print(f"slot {row//2} step {200 + row % 2}: total {s[15]-s[0]}")
-    print("   " + " ".join(f"{names[k]}:{s[k]-s[0]}" for k in range(16) if s[k]))
+    print("   " + " ".join(f"{names[k]}:{s[k]-s[0]}" for k in sorted(range(16), key=lambda k: s[k]) if s[k]))
