@@ -78,8 +78,10 @@ enum ktune_option {
                                   (0 = default) */
   KTUNE_OPT_ROLLOUT_CHECK = 5, /* 1: re-decide EVERY sampling decision exactly and count disagreements
                                   (calibration/verification mode, slow) */
-  KTUNE_OPT_ROLLOUT_FUSE_GBT = 6 /* 1: walk the GBT inside the tcgen05 rollout (during its MMA waits)
+  KTUNE_OPT_ROLLOUT_FUSE_GBT = 6, /* 1: walk the GBT inside the tcgen05 rollout (during its MMA waits)
                                     instead of a separate K1 launch; measured slower on B200, DESIGN.md §5.6 */
+  KTUNE_OPT_ROLLOUT_SEGMENTS = 7  /* host-buffer rollouts: step segments overlapped with the D2H copies
+                                     (0 = auto, 1 = no segmentation) */
 };
 int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value);
 

@@ -255,6 +255,7 @@ int ktune_ctx_destroy(ktune_ctx* ctx) {
   for (auto& b : ctx->pinned) b.release();
   if (ctx->d_counters) cudaFree(ctx->d_counters);
   kt_nccl_destroy(ctx);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return KTUNE_OK;
@@ -278,6 +279,7 @@ int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value) {
     else if (option == KTUNE_OPT_ROLLOUT_DELTA) ctx->opt_rollout_delta = value;
     else if (option == KTUNE_OPT_ROLLOUT_CHECK) ctx->opt_rollout_check = value;
     else if (option == KTUNE_OPT_ROLLOUT_FUSE_GBT) ctx->opt_rollout_fuse_gbt = value;
+    else if (option == KTUNE_OPT_ROLLOUT_SEGMENTS) ctx->opt_rollout_segments = value;
     else kt::fail(KTUNE_ERR_CONFIG, "unknown option");
   });
 }

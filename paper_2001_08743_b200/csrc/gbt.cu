@@ -206,7 +206,7 @@ constexpr int kScoreThreads = 256;
 template <class IdxT, int DEPTH>
 __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
     const IdxT* __restrict__ idx, int64_t B, int D, int T, const uint32_t* __restrict__ g_node,
-    const double* __restrict__ g_leaf, double base, double lr, double* __restrict__ out) {
+    const double* __restrict__ g_leaf, double base, double lr, double* __restrict__ out, kt::RowMap map) {
   constexpr int NI = (1 << DEPTH) - 1, NL = 1 << DEPTH;
   extern __shared__ __align__(16) unsigned char smem[];
   double* s_leaf = reinterpret_cast<double*>(smem);
@@ -218,10 +218,11 @@ __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
   const unsigned char* col0 = reinterpret_cast<const unsigned char*>(s_idx + threadIdx.x);
   const unsigned char* col1 = reinterpret_cast<const unsigned char*>(s_idx + D * kScoreThreads + threadIdx.x);
   for (int64_t c0 = (int64_t)blockIdx.x * 2 * kScoreThreads; c0 < B; c0 += (int64_t)gridDim.x * 2 * kScoreThreads) {
-    const int64_t i0 = c0 + threadIdx.x, i1 = i0 + kScoreThreads;
+    const int64_t j0 = c0 + threadIdx.x, j1 = j0 + kScoreThreads;
+    const int64_t i0 = map(j0), i1 = map(j1);  // row of the j-th scored configuration
     for (int d = 0; d < D; ++d) {  // transposed columns: thread-private, conflict-free
-      s_idx[d * kScoreThreads + threadIdx.x] = i0 < B ? (int32_t)idx[i0 * D + d] : 0;
-      s_idx[(D + d) * kScoreThreads + threadIdx.x] = i1 < B ? (int32_t)idx[i1 * D + d] : 0;
+      s_idx[d * kScoreThreads + threadIdx.x] = j0 < B ? (int32_t)idx[i0 * D + d] : 0;
+      s_idx[(D + d) * kScoreThreads + threadIdx.x] = j1 < B ? (int32_t)idx[i1 * D + d] : 0;
     }
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll 2
@@ -239,8 +240,8 @@ __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
       s0 = kt::dadd(s0, s_leaf[t * NL + (n0 - NI)]);
       s1 = kt::dadd(s1, s_leaf[t * NL + (n1 - NI)]);
     }
-    if (i0 < B) out[i0] = kt::dadd(base, kt::dmul(lr, s0));
-    if (i1 < B) out[i1] = kt::dadd(base, kt::dmul(lr, s1));
+    if (j0 < B) out[i0] = kt::dadd(base, kt::dmul(lr, s0));
+    if (j1 < B) out[i1] = kt::dadd(base, kt::dmul(lr, s1));
   }
 }
 
@@ -297,8 +298,9 @@ namespace kt {
 
 // Launch K1 over device arrays on ctx->stream (also used by the rollout).
 void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_idx, int idx_bytes,
-                            int64_t B, double* d_out) {
+                            int64_t B, double* d_out, RowMap map) {
   if (B <= 0) return;
+  if (!map.identity() && !g->d_inode_pk) fail(KTUNE_ERR_CONFIG, "cost model: strided scoring needs the K1 layout");
   if (!g->has_space) fail(KTUNE_ERR_CONFIG, "cost model: uploaded without a design space; use predict_features");
   const int threads = 256;
   if (!g->complete) {
@@ -319,7 +321,7 @@ void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_id
     auto kern = gbt_score_kernel<T_, DEP>;                                                                   \
     KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
     kern<<<grid, kScoreThreads, smem, ctx->stream>>>((const T_*)d_idx, B, g->D, g->num_trees, g->d_inode_pk, \
-                                                     g->d_leaf, g->base, g->lr, d_out);                      \
+                                                     g->d_leaf, g->base, g->lr, d_out, map);                 \
   }
 #define KT_SCORE_D(T_)                         \
   switch (g->depth) {                          \

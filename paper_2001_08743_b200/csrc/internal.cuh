@@ -78,7 +78,7 @@ enum WsSlot {
   WS_IN0, WS_IN1, WS_IN2, WS_OUT0, WS_OUT1, WS_OUT2, WS_OUT3, WS_OUT4,
   WS_D2, WS_D2B, WS_ASSIGN, WS_ASSIGN2, WS_MEMBERS, WS_BLOCK, WS_BLOCK2, WS_CENT, WS_CENT2,
   WS_SCRATCH, WS_SCRATCH2, WS_KPP, WS_SNAP, WS_VALID, WS_TASKS, WS_BEST_ASSIGN, WS_BEST_D2,
-  WS_PREV_ASSIGN, WS_PREV_D2, WS_SORTED, WS_XS_APPROX, WS_XS_MAPS, WS_TILESUM, WS_NUM_SLOTS
+  WS_PREV_ASSIGN, WS_PREV_D2, WS_SORTED, WS_XS_APPROX, WS_XS_MAPS, WS_TILESUM, WS_ROLLOUT, WS_NUM_SLOTS
 };
 
 }  // namespace kt
@@ -90,13 +90,15 @@ struct ktune_ctx {
   void* nccl = nullptr;  // ncclComm_t
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // D2H of segmented rollouts, overlapping the compute
   std::string last_error;
   int64_t opt_force_exact = 0;
   int64_t opt_kmeans_mode = 0;
   int64_t opt_profile = 0;
   int64_t opt_rollout_delta = 0;  // 1e-12 units, 0 = default
   int64_t opt_rollout_check = 0;
-  int64_t opt_rollout_fuse_gbt = 0;  // 1: GBT walk inside the rollout kernel instead of a separate K1
+  int64_t opt_rollout_fuse_gbt = 0;
+  int64_t opt_rollout_segments = 0;  // 0 auto  // 1: GBT walk inside the rollout kernel instead of a separate K1
   static constexpr int kNumStats = 32;
   int64_t stats[kNumStats] = {0};
   unsigned long long* d_counters = nullptr;  // device counters of the tcgen05 rollout (4 x u64)
@@ -193,6 +195,19 @@ void allgather(ktune_ctx* ctx, const void* send, void* recv, size_t bytes_per_ra
 void kt_nccl_destroy(ktune_ctx* ctx);
 
 namespace kt {
+// Row map of a strided scoring pass: the j-th scored row is
+// (j / len) * stride + off + j % len (identity when len == 0).
+struct RowMap {
+  int64_t len = 0, stride = 0, off = 0;
+  __host__ __device__ bool identity() const { return len == 0; }
+  __host__ __device__ int64_t operator()(int64_t j) const {
+    if (len == 0) return j;
+    const uint32_t q = (uint32_t)((uint64_t)j / (uint64_t)len), r = (uint32_t)((uint64_t)j % (uint64_t)len);
+    return (int64_t)q * stride + off + r;
+  }
+};
+void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_idx, int idx_bytes, int64_t B,
+                            double* d_out, RowMap map = RowMap());
 // One rollout workload with device pointers (shared by the exact and the
 // tcgen05 rollout kernels).
 struct RolloutWork {
@@ -213,7 +228,7 @@ struct RolloutWork {
 // tcgen05 rollout (rollout_tc.cu): eligibility (h = 128, g = 64, n <= 21,
 // cardinalities <= 2049, representable weight scales) and the launch.
 bool rollout_tc_eligible(const ktune_ac* ac, const ktune_space* sp);
-void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T);
+void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end);
 // Folds the device counters of the tcgen05 rollout into ctx->stats.
 void resolve_counters(ktune_ctx* ctx);
 }  // namespace kt

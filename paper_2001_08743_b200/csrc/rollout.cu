@@ -16,6 +16,7 @@
 //   D: per (config, knob) log-softmax, counter-RNG draw, saturating move
 //   E: joint log-probability, trajectory writes
 #include <algorithm>
+#include <array>
 
 #include "device.cuh"
 #include "internal.cuh"
@@ -380,10 +381,6 @@ void check_dims(int n, int h, int g) {
 
 }  // namespace
 
-namespace kt {
-void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_idx, int idx_bytes,
-                            int64_t B, double* d_out);
-}
 
 extern "C" {
 
@@ -480,7 +477,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     if (num_tasks == 0) return;
     const bool dev = flags & KTUNE_F_DEVICE;
     std::vector<RolloutTask> dt(num_tasks);
-    // device buffers for host-pointer calls
+    // device buffers (host-pointer calls: one grow-only context arena, 256-byte aligned slices)
     struct HostIo {
       const uint16_t* d_init;
       uint16_t* d_idx;
@@ -490,14 +487,14 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       double* d_score;
     };
     std::vector<HostIo> io(num_tasks);
-    std::vector<void*> temp;
-    auto alloc = [&](size_t bytes) {
-      void* p = nullptr;
-      KT_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
-      temp.push_back(p);
-      return p;
-    };
     bool smem_params = true;
+    size_t arena = 0;
+    auto slice = [&](size_t bytes) {
+      const size_t o = arena;
+      arena += (std::max<size_t>(bytes, 8) + 255) & ~(size_t)255;
+      return o;
+    };
+    std::vector<std::array<size_t, 6>> offs(num_tasks);
     for (int k = 0; k < num_tasks; ++k) {
       const ktune_rollout_task& t = tasks[k];
       if (!t.space || !t.ac) kt::fail(KTUNE_ERR_CONFIG, "rollout: task needs a space and an agent");
@@ -505,19 +502,27 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       if (t.gbt && t.gbt->num_features != t.space->D) kt::fail(KTUNE_ERR_CONFIG, "rollout: cost model/space mismatch");
       if (t.num_episodes < 0 || !t.idx) kt::fail(KTUNE_ERR_CONFIG, "rollout: bad episode count or missing idx output");
       smem_params = smem_params && fits_smem(t.ac->n, t.ac->h, t.ac->g);
+      if (!dev) {
+        const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
+        offs[k] = {slice(E * n * 2), slice(E * (T + 1) * n * 2), t.actions ? slice(E * T * n) : SIZE_MAX,
+                   t.logp ? slice(E * T * 8) : SIZE_MAX, t.value ? slice(E * T * 8) : SIZE_MAX,
+                   t.score ? slice(E * (T + 1) * 8) : SIZE_MAX};
+      }
+    }
+    unsigned char* base = dev ? nullptr : (unsigned char*)ctx->dev(kt::WS_ROLLOUT, std::max<size_t>(arena, 256));
+    auto at = [&](size_t o) { return o == SIZE_MAX ? nullptr : (void*)(base + o); };
+    for (int k = 0; k < num_tasks; ++k) {
+      const ktune_rollout_task& t = tasks[k];
       const int n = t.ac->n;
       const int64_t E = t.num_episodes;
       HostIo& h = io[k];
       if (dev) {
         h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score};
       } else {
-        h.d_init = (const uint16_t*)alloc(std::max<size_t>(2, (size_t)E * n * 2));
-        KT_CUDA(cudaMemcpyAsync((void*)h.d_init, t.init_idx, (size_t)E * n * 2, cudaMemcpyHostToDevice, ctx->stream));
-        h.d_idx = (uint16_t*)alloc(std::max<size_t>(2, (size_t)E * (T + 1) * n * 2));
-        h.d_act = t.actions ? (int8_t*)alloc(std::max<size_t>(1, (size_t)E * T * n)) : nullptr;
-        h.d_logp = t.logp ? (double*)alloc(std::max<size_t>(8, (size_t)E * T * 8)) : nullptr;
-        h.d_val = t.value ? (double*)alloc(std::max<size_t>(8, (size_t)E * T * 8)) : nullptr;
-        h.d_score = t.score ? (double*)alloc(std::max<size_t>(8, (size_t)E * (T + 1) * 8)) : nullptr;
+        h = {(const uint16_t*)at(offs[k][0]), (uint16_t*)at(offs[k][1]), (int8_t*)at(offs[k][2]),
+             (double*)at(offs[k][3]),         (double*)at(offs[k][4]),   (double*)at(offs[k][5])};
+        if (E > 0)
+          KT_CUDA(cudaMemcpyAsync((void*)h.d_init, t.init_idx, (size_t)E * n * 2, cudaMemcpyHostToDevice, ctx->stream));
       }
       RolloutTask& r = dt[k];
       for (int d = 0; d < kt::kMaxKnobs; ++d) r.card[d] = d < n ? t.space->card[d] : 1;
@@ -538,28 +543,88 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     // tcgen05 path with certified sampling unless the exact fp64 forward is
     // requested (or a task is outside the tensor-core path's shapes)
     bool use_tc = !(flags & KTUNE_F_EXACT_ROLLOUT);
-    std::vector<char> scored(num_tasks, 0);
     for (int k = 0; k < num_tasks && use_tc; ++k) use_tc = kt::rollout_tc_eligible(tasks[k].ac, tasks[k].space);
+    // Host outputs on the tcgen05 path: the episode runs in S segments of
+    // steps; each segment's scoring and device->host copies (copy stream)
+    // overlap the next segment's compute, so the end-to-end call approaches
+    // max(compute, PCIe) instead of their sum.
+    bool segmented = use_tc && !dev && T >= 128;
+    for (int k = 0; k < num_tasks && segmented; ++k)
+      if (tasks[k].gbt && tasks[k].score && !tasks[k].gbt->d_inode_pk) segmented = false;
+    if (ctx->opt_rollout_segments == 1) segmented = false;
+    const int S = !segmented ? 1
+                  : ctx->opt_rollout_segments > 1 ? (int)std::min<int64_t>(ctx->opt_rollout_segments, T)
+                                                  : (int)std::min<int64_t>(8, std::max<int64_t>(2, T / 100));
+    if (segmented && !ctx->copy_stream) KT_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> events;
+    auto score_rows = [&](int k, int r0, int r1) {  // trajectory rows [r0, r1] of every episode
+      const ktune_rollout_task& t = tasks[k];
+      if (!t.gbt || !io[k].d_score || t.num_episodes == 0) return;
+      const int64_t len = r1 - r0 + 1;
+      kt::RowMap m;
+      if (len != T + 1) m = kt::RowMap{len, (int64_t)T + 1, r0};
+      kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx, 2, t.num_episodes * len, io[k].d_score, m);
+    };
+    auto copy_out = [&](int k, int t0, int t1, cudaStream_t st) {  // steps [t0, t1): rows (t0, t1] (+ row 0)
+      const ktune_rollout_task& t = tasks[k];
+      const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
+      if (E == 0) return;
+      const HostIo& h = io[k];
+      const int r0 = t0 == 0 ? 0 : t0 + 1;
+      const size_t rows = (size_t)(t1 - r0 + 1), steps = (size_t)(t1 - t0);
+      KT_CUDA(cudaMemcpy2DAsync(t.idx + r0 * n, (T + 1) * n * 2, h.d_idx + r0 * n, (T + 1) * n * 2, rows * n * 2, E,
+                                cudaMemcpyDeviceToHost, st));
+      if (t.actions && steps)
+        KT_CUDA(cudaMemcpy2DAsync(t.actions + t0 * n, T * n, h.d_act + t0 * n, T * n, steps * n, E,
+                                  cudaMemcpyDeviceToHost, st));
+      if (t.logp && steps)
+        KT_CUDA(cudaMemcpy2DAsync(t.logp + t0, T * 8, h.d_logp + t0, T * 8, steps * 8, E, cudaMemcpyDeviceToHost, st));
+      if (t.value && steps)
+        KT_CUDA(cudaMemcpy2DAsync(t.value + t0, T * 8, h.d_val + t0, T * 8, steps * 8, E, cudaMemcpyDeviceToHost, st));
+      if (t.score && t.gbt)
+        KT_CUDA(cudaMemcpy2DAsync(t.score + r0, (T + 1) * 8, h.d_score + r0, (T + 1) * 8, rows * 8, E,
+                                  cudaMemcpyDeviceToHost, st));
+    };
+    std::vector<char> scored(num_tasks, 0);
     if (use_tc) {
       std::vector<kt::RolloutWork> work(num_tasks);
       for (int k = 0; k < num_tasks; ++k)
         work[k] = {tasks[k].space, tasks[k].ac, dt[k].E,     dt[k].episode_offset, dt[k].seed, dt[k].init_idx,
                    dt[k].idx,      dt[k].actions, dt[k].logp, dt[k].value,         tasks[k].gbt, io[k].d_score};
+      if (segmented) {
+        for (int sg = 0; sg < S; ++sg) {
+          const int t0 = (int)((int64_t)sg * T / S), t1 = (int)((int64_t)(sg + 1) * T / S);
+          {
+            kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
+            kt::rollout_tc(ctx, work, T, t0, t1);
+          }
+          for (int k = 0; k < num_tasks; ++k) score_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
+          cudaEvent_t ev;
+          KT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          events.push_back(ev);
+          KT_CUDA(cudaEventRecord(ev, ctx->stream));
+          KT_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev, 0));
+          for (int k = 0; k < num_tasks; ++k) copy_out(k, t0, t1, ctx->copy_stream);
+        }
+        KT_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+        for (cudaEvent_t ev : events) cudaEventDestroy(ev);
+        KT_CUDA(cudaStreamSynchronize(ctx->stream));
+        return;
+      }
       kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
-      kt::rollout_tc(ctx, work, T);
+      kt::rollout_tc(ctx, work, T, 0, T);
       for (int k = 0; k < num_tasks; ++k) scored[k] = work[k].scored;
-    }
-    // exact path: one launch config for all tasks: smem sized for the largest task;
-    // 64-episode tiles (2 per lane) when they fit, else 32
-    int cpl = 2;
-    for (int k = 0; k < num_tasks; ++k)
-      if (!smem_params || rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, true, 2) > 227 * 1024 || 2 * dt[k].g > 128)
-        cpl = 1;
-    size_t smem = 0;
-    for (int k = 0; k < num_tasks; ++k)
-      smem = std::max(smem, rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, smem_params, cpl));
-    if (!use_tc && smem > 227 * 1024) kt::fail(KTUNE_ERR_CONFIG, "rollout: agent too large for shared memory");
-    if (!use_tc) {
+    } else {
+      // exact path: one launch config for all tasks: smem sized for the largest task;
+      // 64-episode tiles (2 per lane) when they fit, else 32
+      int cpl = 2;
+      for (int k = 0; k < num_tasks; ++k)
+        if (!smem_params || rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, true, 2) > 227 * 1024 || 2 * dt[k].g > 128)
+          cpl = 1;
+      size_t smem = 0;
+      for (int k = 0; k < num_tasks; ++k)
+        smem = std::max(smem, rollout_smem_bytes(dt[k].n, dt[k].h, dt[k].g, smem_params, cpl));
+      if (smem > 227 * 1024) kt::fail(KTUNE_ERR_CONFIG, "rollout: agent too large for shared memory");
       auto kern = smem_params ? (cpl == 2 ? rollout_kernel<true, 2> : rollout_kernel<true, 1>)
                               : rollout_kernel<false, 1>;
       KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -576,30 +641,15 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         L.cta_base[L.num_tasks] = ctas;
         if (ctas > 0) kern<<<(unsigned)ctas, kThreads, smem, ctx->stream>>>(L);
       }
-
       kt::check_launch(ctx, "rollout");
     }
     // cost-model scores of every visited configuration (K1 over the trajectory)
-    for (int k = 0; k < num_tasks; ++k) {
-      const ktune_rollout_task& t = tasks[k];
-      if (t.gbt && io[k].d_score && t.num_episodes > 0 && !scored[k])
-        kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx, 2, t.num_episodes * (int64_t)(T + 1), io[k].d_score);
-    }
+    for (int k = 0; k < num_tasks; ++k)
+      if (!scored[k]) score_rows(k, 0, T);
     if (!dev) {
-      for (int k = 0; k < num_tasks; ++k) {
-        const ktune_rollout_task& t = tasks[k];
-        const int64_t E = t.num_episodes;
-        const int n = t.ac->n;
-        const HostIo& h = io[k];
-        KT_CUDA(cudaMemcpyAsync(t.idx, h.d_idx, (size_t)E * (T + 1) * n * 2, cudaMemcpyDeviceToHost, ctx->stream));
-        if (t.actions) KT_CUDA(cudaMemcpyAsync(t.actions, h.d_act, (size_t)E * T * n, cudaMemcpyDeviceToHost, ctx->stream));
-        if (t.logp) KT_CUDA(cudaMemcpyAsync(t.logp, h.d_logp, (size_t)E * T * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        if (t.value) KT_CUDA(cudaMemcpyAsync(t.value, h.d_val, (size_t)E * T * 8, cudaMemcpyDeviceToHost, ctx->stream));
-        if (t.score && t.gbt) KT_CUDA(cudaMemcpyAsync(t.score, h.d_score, (size_t)E * (T + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
-      }
+      for (int k = 0; k < num_tasks; ++k) copy_out(k, 0, T, ctx->stream);
+      KT_CUDA(cudaStreamSynchronize(ctx->stream));
     }
-    for (void* p : temp) KT_CUDA(cudaFreeAsync(p, ctx->stream));
-    if (!dev) KT_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -74,6 +74,7 @@ struct TcTask {
 
 struct TcLaunch {
   int32_t num_tasks;
+  int32_t t_begin, t_end;  // steps [t_begin, t_end) of a T-step episode (segmented launches)
   int32_t check;
   float delta;
   unsigned long long* counters;  // [fallbacks, checked, mismatches, max err (float bits)]
@@ -430,10 +431,17 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
 #pragma unroll
     for (int i = 0; i < NMAX / 2; ++i) cfg.w[i] = 0;
     if (lr) {
+      if (L.t_begin == 0) {
 #pragma unroll
-      for (int d = 0; d < NMAX; ++d)
-        if (d < n) cfg.set(d, tk.init_idx[e * n + d]);
-      store_row_idx(tk.idx + e * (int64_t)(T + 1) * n, cfg, n);
+        for (int d = 0; d < NMAX; ++d)
+          if (d < n) cfg.set(d, tk.init_idx[e * n + d]);
+        store_row_idx(tk.idx + e * (int64_t)(T + 1) * n, cfg, n);
+      } else {  // resume a segmented rollout from trajectory row t_begin
+        const uint16_t* src = tk.idx + (e * (int64_t)(T + 1) + L.t_begin) * n;
+#pragma unroll
+        for (int d = 0; d < NMAX; ++d)
+          if (d < n) cfg.set(d, src[d]);
+      }
     }
     const unsigned char* mycol = reinterpret_cast<const unsigned char*>(s_col + tid);
     if (tk.gnode) {
@@ -447,7 +455,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
 #define TR(k)                                                                                  \
   if (trace_cta && (t == 200 || t == 201))                                                      \
     L.counters[4 + (slot * 2 + (t - 200)) * 16 + (k)] = (unsigned long long)clock64();
-    for (int t = 0; t < T; ++t) {
+    for (int t = L.t_begin; t < L.t_end; ++t) {
       TR(0)
       // ---- L1 operand: [idx | idx] as fp16 (exact integers)
       if (lw) {
@@ -694,7 +702,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       TR(15)
     }
 #undef TR
-    if (tk.gnode && lr)  // row T
+    if (tk.gnode && lr && L.t_end == T)  // row T
       tk.score[e * (int64_t)(T + 1) + T] =
           kt::dadd(tk.gbase, kt::dmul(tk.glr, gbt_walk(0.0, s_node, s_leaf, mycol, 0, tk.ntrees, tk.depth)));
   }
@@ -747,7 +755,7 @@ void resolve_counters(ktune_ctx* ctx) {
       std::max<int64_t>(ctx->stats[KTUNE_STAT_ROLLOUT_MAXERR], (int64_t)std::llround((double)mx * 1e12));
 }
 
-void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T) {
+void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end) {
   if (!ctx->d_counters) {
     KT_CUDA(cudaMalloc(&ctx->d_counters, (4 + 8 * 16) * sizeof(unsigned long long)));
     KT_CUDA(cudaMemsetAsync(ctx->d_counters, 0, (4 + 8 * 16) * sizeof(unsigned long long), ctx->stream));
@@ -761,6 +769,8 @@ void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T) {
     const size_t nt = std::min<size_t>(kMaxTcTasks, work.size() - t0);
     TcLaunch L{};
     L.check = (int)ctx->opt_rollout_check;  // 2: phase trace (debug)
+    L.t_begin = t_begin;
+    L.t_end = t_end;
     L.delta = delta;
     L.counters = ctx->d_counters;
     // warps per task, then the smallest per-CTA warp count m whose CTA total fits one wave
@@ -817,7 +827,7 @@ void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T) {
       // optional fused scoring (complete-tree index layout that fits in shared memory)
       const ktune_gbt* g = rw.gbt;
       tk.gnode = nullptr;
-      if (g && rw.score && g->has_space && g->complete && g->d_inode_idx && g->depth <= 8 &&
+      if (g && rw.score && g->has_space && g->complete && g->d_inode_idx && g->depth <= 8 && t_begin == 0 && t_end == T &&
           tc_smem_bytes(n, g->num_trees, g->depth) <= 227 * 1024 && ctx->opt_rollout_fuse_gbt) {
         tk.gnode = g->d_inode_idx;
         tk.gleaf = g->d_leaf;
@@ -833,10 +843,10 @@ void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T) {
       tk.e3 = pow2_scale(m3);
       if (tk.e1 > 100 || tk.e2 > 100 || tk.e3 > 100 || tk.e1 < -100 || tk.e2 < -100 || tk.e3 < -100)
         fail(KTUNE_ERR_CONFIG, "rollout: actor-critic weights out of the tensor-core path's range");
-      ctx->stats[KTUNE_STAT_ROLLOUT_TC] += rw.E * (int64_t)T;
+      ctx->stats[KTUNE_STAT_ROLLOUT_TC] += rw.E * (int64_t)(t_end - t_begin);
     }
     L.num_tasks = nl;
-    if (ctas == 0 || T == 0) continue;
+    if (ctas == 0 || t_end <= t_begin) continue;
     size_t smem = 0;
     for (int k = 0; k < nl; ++k)
       smem = std::max<size_t>(smem, tc_smem_bytes(L.task[k].n, L.task[k].gnode ? L.task[k].ntrees : 0,

@@ -193,3 +193,31 @@ def test_rollout_tc_fused_scores_equal_unfused(O, ctx):
     for f, s_ in zip(fused, sep):
         assert np.array_equal(f["idx"], s_["idx"])
         assert np.array_equal(f["score"], s_["score"])
+
+
+def test_rollout_tc_segmented_host_path(O, ctx):
+    """Host buffers with T >= 128: the rollout runs in step segments whose
+    scoring and D2H copies overlap the next segment; results equal the
+    device-buffer (single launch) path and the oracle."""
+    import torch
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    from paper_2001_08743_b200.spaces import stream_seed
+    tasks, dtasks, inits = [], [], []
+    for i, name in enumerate(["resnet_c2", "synthetic16"]):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=80 + i)
+        init = osp.random_valid(i, 70) if O.ref_available() else np.zeros((70, sp.num_knobs), np.int32)
+        inits.append((osp, og, agent, init))
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=3, root_seed=i))
+        dtasks.append(RolloutTask(dspace, agent, dg, torch.from_numpy(init.astype(np.int32)).cuda(),
+                                  episode_offset=3, root_seed=i))
+    T = 333
+    host = run_episodes_batch(tasks, T)
+    devo = run_episodes_batch(dtasks, T)
+    torch.cuda.synchronize()
+    for h, d in zip(host, devo):
+        for k in ["idx", "actions", "score", "logp", "value"]:
+            assert np.array_equal(h[k], d[k].cpu().numpy()), k
+    osp, og, agent, init = inits[0]
+    want = O.run_episodes(osp, og, 128, 64, agent.params, init[:6], T, 3, stream_seed(0, "explore"))
+    assert np.array_equal(host[0]["idx"][:6].astype(np.int32), want["idx"])
+    assert np.array_equal(host[0]["score"][:6], want["score"])
