@@ -33,12 +33,23 @@ FLOP_PER_CONFIG_STEP = lambda n, h=128, g=64: 2 * (h * n + 2 * h * g + 3 * n * g
 
 
 def load_peaks():
+    """Roofline denominators: the driver-written MEASURED_PEAKS.json; if absent, the
+    values it held when SURVEY.md §8d was written (same pool), else the profiling
+    guide's fallback."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
         return p, "measured"
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+        return {"hbm_gbs": 6547.2, "bf16_tflops": 1657.0, "bf16_tflops_sustained": 1383.3}, \
+            "measured (MEASURED_PEAKS.json as recorded in SURVEY.md §8d; file absent here)"
+
+
+SFU_OPS_PER_SM_CLK = 16  # MUFU lanes per SM per clock (ex2/rcp/lg2)
+
+
+def sfu_ops_per_config_step(n):
+    return 2 * (128 + 64 + 64) + 5 * n  # 2 per tanh (ex2 + rcp), 5 per knob softmax (3 ex2, rcp, lg2)
 
 
 class ClockSampler:
@@ -216,8 +227,8 @@ def kmeans_secondary(ctx, args, cpu=True):
            "assign_kernel_ms": a_ms,
            "assign_roofline": {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                "frac": ach / peaks["hbm_gbs"], "bytes_per_point": bytes_pt,
-                               "note": "exact fp64 SIMT argmin, FP64-pipe bound (3*k*D flop/point); "
-                                       "per-iteration time is dominated by the exact-order centroid sums"}}
+                               "note": "tcgen05 screening + certified exact fp64 winner; the iteration is "
+                                       "dominated by the exact-order centroid sums, not the assignment"}}
     if cpu:
         try:
             from oracle import pyoracle as O
@@ -334,10 +345,11 @@ def main():
     flop = FLOP_PER_CONFIG_STEP(n_knobs)
     roll_s = roll_ns / max(1, roll_calls) * 1e-9
     peaks, peak_src = load_peaks()
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     achieved = len(specs) * E * T * flop / roll_s / 1e12
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "rollout_ncu_summary.json")
+    prof = os.path.join(ROOT, "profiles", "r01_rollout_exact_kernel.json" if args.exact else "r01_rollout_tc_kernel.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
@@ -411,11 +423,19 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "rollout_kernel" if args.exact else "rollout_tc_kernel",
                          "kernel_ms": roll_s * 1e3, "flop_per_config_step": flop,
-                         "peak_source": f"{peak_src} bf16_tflops_sustained",
+                         "peak_source": f"bf16_tflops_sustained, {peak_src}",
                          "note": ("exact path runs on the FP64 pipe (SIMT); tensor-pipe fraction reported against bf16"
                                   if args.exact else
                                   "algorithmic MLP FLOPs counted once; the kernel issues 3x (fp16 hi/lo split) "
                                   "tcgen05 work plus 256 tanh/config-step on the SFU (epilogue-bound, DESIGN.md §5.6)")},
+            "sfu_roofline": None if args.exact else {
+                "bound": "sfu", "unit": "Gop/s",
+                "achieved": len(specs) * E * T * sfu_ops_per_config_step(n_knobs) / roll_s / 1e9,
+                "peak": SFU_OPS_PER_SM_CLK * sm_count * (clocks.get("sm_mhz") or 1965.0) * 1e6 / 1e9,
+                "frac": (len(specs) * E * T * sfu_ops_per_config_step(n_knobs) / roll_s) /
+                        (SFU_OPS_PER_SM_CLK * sm_count * (clocks.get("sm_mhz") or 1965.0) * 1e6),
+                "ops_per_config_step": sfu_ops_per_config_step(n_knobs),
+                "note": "MUFU ex2/rcp/lg2 at 16/SM/clk at the sampled SM clock: the unit that bounds K2-TC"},
             "rollout_fallbacks": {"knob_decisions_redecided_exactly": fallbacks, "config_steps": tc_steps,
                                   "per_config_step": fallbacks / max(1, tc_steps)},
             "gbt_kernel_ms_per_step": gbt_ns / max(1, gbt_calls) * 1e-6 * len(specs),
