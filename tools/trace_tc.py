@@ -27,10 +27,10 @@ lib = L.lib()
 # read the trace buffer through the ctx's device counters pointer (debug only)
 class Ctx(C.Structure):
     pass
-buf = np.zeros(4 + 128, np.uint64)
+buf = np.zeros(4 + 128 + 1024, np.uint64)
 lib.ktune_debug_trace.restype = C.c_int
 ctx.check(lib.ktune_debug_trace(ctx.h, buf.ctypes.data_as(C.c_void_p)))
-tr = buf[4:].reshape(8, 16).astype(np.int64)
+tr = buf[4:132].reshape(8, 16).astype(np.int64)
 names = ["start", "bar1", "L1 wait", "L1 epi a", "bar2", "epi b", "L2a wait", "fallbk", "bar3", "L2b wait", "apply", "bar4",
          "value", "L3 wait", "knobs", "end"]
 for row in range(8):
@@ -38,3 +38,12 @@ for row in range(8):
     if s[0] == 0: continue
     print(f"slot {row//2} step {200 + row % 2}: total {s[15]-s[0]}")
     print("   " + " ".join(f"{names[k]}:{s[k]-s[0]}" for k in sorted(range(16), key=lambda k: s[k]) if s[k]))
+
+gt = buf[132:132 + 512].reshape(256, 2).astype(np.int64)
+ck = buf[132 + 512:132 + 1024].reshape(2, 256).astype(np.int64)
+live = gt[:, 0] > 0
+t0 = gt[live, 0].min()
+dur = (gt[live, 1] - gt[live, 0]) / 1e6
+cyc = ck[1, live] - ck[0, live]
+print(f"CTAs {live.sum()}: duration ms min {dur.min():.3f} median {np.median(dur):.3f} max {dur.max():.3f}; "
+      f"start spread {(gt[live,0].max()-t0)/1e6:.3f} ms; effective clock GHz median {np.median(cyc/((gt[live,1]-gt[live,0]))):.3f}")
