@@ -42,6 +42,8 @@ for row in range(8):
 gt = buf[132:132 + 512].reshape(256, 2).astype(np.int64)
 ck = buf[132 + 512:132 + 1024].reshape(2, 256).astype(np.int64)
 live = gt[:, 0] > 0
+if not live.any():
+    sys.exit(0)
 t0 = gt[live, 0].min()
 dur = (gt[live, 1] - gt[live, 0]) / 1e6
 cyc = ck[1, live] - ck[0, live]
