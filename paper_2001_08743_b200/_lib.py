@@ -12,7 +12,7 @@ import os
 from .errors import BackendError, ConfigError, CudaError, LogicError, SpaceExhaustedError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libktune_cuda.so")
+LIB_PATH = os.environ.get("KTUNE_LIB_PATH") or os.path.join(HERE, "libktune_cuda.so")  # override: A/B builds
 
 KTUNE_OK, ERR_CONFIG, ERR_BACKEND, ERR_EXHAUSTED, ERR_LOGIC, ERR_CUDA, ERR_NOMEM = range(7)
 F_DEVICE = 1
