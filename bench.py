@@ -70,6 +70,8 @@ class ClockSampler:
         self.lines = []  # (perf_counter, line)
 
     def __enter__(self):
+        if os.environ.get("BENCH_NO_SMI"):  # diagnostics only
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
@@ -247,6 +249,57 @@ def kmeans_secondary(ctx, args, cpu=True):
     return out
 
 
+def c5_secondary(ctx, args):
+    """synthetic 16-knob space (cards 2..32), 1M configurations x 1000 steps
+    (1.05e9 config-steps) in one grouped launch + K1 scoring, device buffers (~40 GB)."""
+    import torch
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
+    from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
+    from paper_2001_08743_b200.workloads import encode, make_tasks
+    sp = S.synthetic_space(0, 16)
+    spec = make_tasks([sp], 1, seed=args.seed + 77)[0]
+    E, T = args.c5_episodes, args.c5_T
+    ds = Space(sp, ctx)
+    g = DeviceGbt(fit_gbt(encode(sp, spec.train_idx), spec.train_y, seed=spec.seed), ds)
+    agent = ActorCritic(16, 128, 64, seed=spec.seed, ctx=ctx)
+    gen = torch.Generator(device="cuda").manual_seed(args.seed)
+    cards = torch.tensor(sp.cards, device="cuda")
+    init = (torch.rand((E, 16), device="cuda", generator=gen) * cards).to(torch.int32).to(torch.uint16)
+    mk = lambda shape, dt: torch.empty(shape, dtype=dt, device="cuda")
+    out = [dict(idx=mk((E, T + 1, 16), torch.uint16), score=mk((E, T + 1), torch.float64), actions=None,
+                logp=None, value=None)]
+    task = RolloutTask(ds, agent, g, init, 0, spec.seed, want_trajectory=False)
+    run_episodes_batch([task], 8, ctx, host_out=[dict(idx=mk((E, 9, 16), torch.uint16),
+                                                      score=mk((E, 9), torch.float64), actions=None, logp=None,
+                                                      value=None)])  # warm-up
+    torch.cuda.synchronize()
+    ctx.set_option(L.OPT_PROFILE, 1)
+    ctx.reset_stats()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    run_episodes_batch([task], T, ctx, host_out=out)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    roll = ctx.stat(L.STAT_ROLLOUT_NS) / 1e6
+    fb, steps = ctx.stat(L.STAT_ROLLOUT_FALLBACKS), ctx.stat(L.STAT_ROLLOUT_TC)
+    ctx.set_option(L.OPT_PROFILE, 0)
+    idx = out[0]["idx"]
+    smp = idx[:: max(1, E // 4096)].to(torch.int32)  # properties on a 4096-episode sample
+    ok_range = bool((smp.amax(dim=(0, 1)) < cards).all())
+    moves = (smp[:, 1:] - smp[:, :-1]).abs().amax().item()
+    res = {"workload": "synthetic16 (SURVEY C5), 1M configs x 1000 steps, 1 GPU, device buffers",
+           "config_steps": E * T, "ms": ms, "value": E * T / (ms * 1e-3), "unit": "config-steps/s",
+           "rollout_kernel_ms": roll, "fallbacks_per_config_step": fb / max(1, steps),
+           "properties": {"idx_in_range": ok_range, "max_move_per_knob": int(moves)}}
+    del out, idx
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -266,6 +319,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exact", action="store_true", help="exact fp64 rollout kernel instead of the tcgen05 path")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-size tcgen05 vs exact comparison")
+    ap.add_argument("--c5", type=int, default=1, help="run the SURVEY C5 scale workload (1M x 1000, 1 step)")
+    ap.add_argument("--c5-episodes", type=int, default=1 << 20)
+    ap.add_argument("--c5-T", type=int, default=1000)
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -387,6 +444,29 @@ def main():
                "d2h_bytes_per_step": bo}
         ctx.set_stream(stream.cuda_stream)
 
+    # ---- parity at the full bench size (outside the timed region): the tcgen05 path vs the
+    # exact fp64 kernel (configurations/actions/scores bit-identical, logp/value within 1e-5)
+    parity = None
+    if not args.exact and not args.no_parity:
+        exact_out = [{k: torch.empty_like(v) for k, v in o.items()} for o in dev_out]
+        run_episodes_batch(tasks, T, ctx, host_out=exact_out, exact=True)
+        run_episodes_batch(tasks, T, ctx, host_out=dev_out)
+        torch.cuda.synchronize()
+        eq = lambda k: all(bool(torch.equal(a[k], b[k])) for a, b in zip(dev_out, exact_out))
+        rel = lambda k: max(float(((a[k] - b[k]).abs() / b[k].abs().clamp_min(1.0)).max()) for a, b in zip(dev_out, exact_out))
+        parity = {"vs": "exact fp64 kernel (bit-exact with the oracle by the test suite)",
+                  "config_steps": len(specs) * E * T, "idx_equal": eq("idx"), "actions_equal": eq("actions"),
+                  "score_equal": eq("score"), "logp_max_rel": rel("logp"), "value_max_rel": rel("value")}
+        del exact_out
+
+    # ---- synthetic 16-knob space, 1M configurations x 1000 steps, one step
+    scale = None
+    if args.c5 and world == 1:
+        try:
+            scale = c5_secondary(ctx, args)
+        except Exception as ex:  # reported, not hidden
+            scale = {"error": repr(ex)}
+
     kmeans = None
     if not args.no_kmeans:  # every rank participates (sharded assignment + NCCL all-gather)
         try:
@@ -442,7 +522,9 @@ def main():
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity_full_size": parity,
             "secondary": kmeans,
+            "scale_c5": scale,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
