@@ -115,6 +115,7 @@ SIGNATURES = {
                                         P, C.POINTER(C.c_int32)]),
     "ktune_synthesize_sample": (C.c_int, [P, P, i64, P, i64, C.POINTER(u64), P]),
     "ktune_debug_math": (C.c_int, [P, C.c_int, P, i64, P]),
+    "ktune_debug_trace": (C.c_int, [P, P]),
 }
 
 _lib = None
