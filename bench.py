@@ -320,6 +320,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exact", action="store_true", help="exact fp64 rollout kernel instead of the tcgen05 path")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size tcgen05 vs exact comparison")
+    ap.add_argument("--no-sa", action="store_true", help="skip the simulated-annealing baseline measurement")
     ap.add_argument("--c5", type=int, default=1, help="run the SURVEY C5 scale workload (1M x 1000, 1 step)")
     ap.add_argument("--c5-episodes", type=int, default=1 << 20)
     ap.add_argument("--c5-T", type=int, default=1000)
@@ -459,6 +460,25 @@ def main():
                   "score_equal": eq("score"), "logp_max_rel": rel("logp"), "value_max_rel": rel("value")}
         del exact_out
 
+    # ---- the AutoTVM SA baseline (K7) on the same 12 tasks x 4096 chains x T steps (host buffers)
+    sa = None
+    if not args.no_sa and world == 1:
+        try:
+            from paper_2001_08743_b200.exploration import SaParams, sa_search
+            ctx.set_stream(None)
+            p = SaParams(num_chains=E, max_steps=T)
+            sa_search(spaces[0], gbts[0], specs[0].init_idx, SaParams(num_chains=256, max_steps=8), rng_seed=1)
+            t0 = time.perf_counter()
+            for s_, d_, g_ in zip(specs, spaces, gbts):
+                sa_search(d_, g_, s_.init_idx, p, rng_seed=s_.seed)
+            dt = time.perf_counter() - t0
+            sa = {"metric": "SA chain-steps/s (sa_search, SPEC.md:229-237; host buffers incl. D2H)",
+                  "value": len(specs) * E * T / dt, "unit": "chain-steps/s", "tasks": len(specs), "chains": E,
+                  "T": T, "ms": dt * 1e3}
+            ctx.set_stream(stream.cuda_stream)
+        except Exception as ex:  # reported, not hidden
+            sa = {"error": repr(ex)}
+
     # ---- synthetic 16-knob space, 1M configurations x 1000 steps, one step
     scale = None
     if args.c5 and world == 1:
@@ -525,6 +545,7 @@ def main():
             "parity_full_size": parity,
             "secondary": kmeans,
             "scale_c5": scale,
+            "sa_baseline": sa,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

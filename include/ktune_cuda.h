@@ -227,6 +227,27 @@ typedef struct {
 int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks, int32_t T,
                   int flags);
 
+/* ------------------------------------------------------------------ simulated annealing
+ * sa_search: the AutoTVM parallel-SA baseline, builder-pinned
+ * (oracle/ktune_oracle.c ko_sa_search). One task = num_chains
+ * chains on one space; T steps each. */
+typedef struct {
+  double initial_temperature; /* 1.0 (SPEC.md SaParams) */
+  double cooling_rate;        /* 0.99 per step */
+} ktune_sa_params;
+typedef struct {
+  const ktune_space* space;
+  const ktune_gbt* gbt;       /* uploaded with `space` */
+  int64_t num_chains;         /* E */
+  int64_t chain_offset;       /* global id of the first chain (RNG key; sharding) */
+  uint64_t sa_seed;           /* stream_seed(root, "sa") */
+  const uint16_t* init_idx;   /* E x D seeds */
+  uint16_t* idx;              /* E x (T+1) x D chain states */
+  double* score;              /* E x (T+1) predicted fitness of the states */
+  uint8_t* accepted;          /* E x T (may be NULL) */
+} ktune_sa_task;
+int ktune_sa_search(ktune_ctx* ctx, int num_tasks, const ktune_sa_task* tasks, int32_t T,
+                    const ktune_sa_params* params, int flags);
 /* ------------------------------------------------------------------ candidates
  * make_candidate_set (sampling.cpp:16-31): dedup by id (first occurrence
  * wins) then rank by (predicted fitness desc, id asc). Returns the kept raw

@@ -513,6 +513,108 @@ int ko_run_episodes(const ko_space* s, const ko_gbt* m, int h, int g, const doub
 }
 
 /* ======================================================================
+ * sa_search (the AutoTVM simulated-annealing baseline; no
+ * reference code — builder-pinned):
+ *  chain c (global id gc = chain_offset + c): Θ_0 = seeds[c], f_0 = pred(Θ_0),
+ *  temp = T0. Step t draws u_j = hash01(sa_seed, (gc*T + t)*3 + j), j = 0,1,2:
+ *  knob = (int)(u_0 * D); dir = u_1 < 0.5 ? -1 : +1; the proposal moves that
+ *  knob saturating (design_space.cpp:175-187); Δ = pred(proposal) - f_t;
+ *  accept iff Δ >= 0 || u_2 < exp(Δ / temp) (portable exp);
+ *  Θ_{t+1} = accept ? proposal : Θ_t; temp = temp * cooling_rate.
+ *  Outputs: states [E][T+1][D], their predicted fitness [E][T+1], accepted [E][T].
+ * ==================================================================== */
+typedef struct {
+  const ko_space* s;
+  const ko_gbt* m;
+  int64_t c_begin, c_end;
+  int32_t T;
+  int64_t chain_offset;
+  uint64_t seed;
+  double t0, rate;
+  const int32_t* init_idx;
+  int32_t* idx_out;
+  double* score_out;
+  uint8_t* acc_out;
+} sa_job;
+
+static void* sa_chain_range(void* arg) {
+  const sa_job* J = (const sa_job*)arg;
+  const int D = J->s->D;
+  double* x = (double*)malloc(sizeof(double) * (size_t)D);
+  int32_t* prop = (int32_t*)malloc(sizeof(int32_t) * (size_t)D);
+  for (int64_t c = J->c_begin; c < J->c_end; ++c) {
+    const uint64_t gc = (uint64_t)(J->chain_offset + c);
+    int32_t* traj = J->idx_out + c * (int64_t)(J->T + 1) * D;
+    double* sc = J->score_out + c * (int64_t)(J->T + 1);
+    memcpy(traj, J->init_idx + c * D, sizeof(int32_t) * (size_t)D);
+    ko_encode(J->s, traj, x);
+    double f = ko_gbt_predict_one(J->m, x);
+    sc[0] = f;
+    double temp = J->t0;
+    for (int32_t t = 0; t < J->T; ++t) {
+      const int32_t* cur = traj + (int64_t)t * D;
+      int32_t* nxt = traj + (int64_t)(t + 1) * D;
+      const uint64_t base = (gc * (uint64_t)J->T + (uint64_t)t) * 3u;
+      const double u0 = ko_hash01(J->seed, base), u1 = ko_hash01(J->seed, base + 1),
+                   u2 = ko_hash01(J->seed, base + 2);
+      const int knob = (int)(u0 * (double)D);
+      const int dir = u1 < 0.5 ? -1 : 1;
+      memcpy(prop, cur, sizeof(int32_t) * (size_t)D);
+      int v = prop[knob] + dir;
+      if (v < 0) v = 0;
+      if (v > J->s->card[knob] - 1) v = J->s->card[knob] - 1;
+      prop[knob] = v;
+      ko_encode(J->s, prop, x);
+      const double fp = ko_gbt_predict_one(J->m, x);
+      const double delta = fp - f;
+      const int accept = delta >= 0.0 || u2 < ko_exp(delta / temp);
+      memcpy(nxt, accept ? prop : cur, sizeof(int32_t) * (size_t)D);
+      if (accept) f = fp;
+      sc[t + 1] = f;
+      if (J->acc_out) J->acc_out[c * (int64_t)J->T + t] = (uint8_t)accept;
+      temp = temp * J->rate;
+    }
+  }
+  free(x);
+  free(prop);
+  return NULL;
+}
+
+int ko_sa_search(const ko_space* s, const ko_gbt* m, int64_t E, int32_t T, int64_t chain_offset,
+                 uint64_t sa_seed, double t0, double rate, const int32_t* init_idx, int32_t* idx_out,
+                 double* score_out, uint8_t* acc_out, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > E) threads = (int)(E > 0 ? E : 1);
+  sa_job* jobs = (sa_job*)calloc((size_t)threads, sizeof(sa_job));
+  pthread_t* th = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+  for (int w = 0; w < threads; ++w) {
+    sa_job* J = &jobs[w];
+    J->s = s;
+    J->m = m;
+    J->c_begin = E * w / threads;
+    J->c_end = E * (w + 1) / threads;
+    J->T = T;
+    J->chain_offset = chain_offset;
+    J->seed = sa_seed;
+    J->t0 = t0;
+    J->rate = rate;
+    J->init_idx = init_idx;
+    J->idx_out = idx_out;
+    J->score_out = score_out;
+    J->acc_out = acc_out;
+  }
+  if (threads == 1) {
+    sa_chain_range(&jobs[0]);
+  } else {
+    for (int w = 0; w < threads; ++w) pthread_create(&th[w], NULL, sa_chain_range, &jobs[w]);
+    for (int w = 0; w < threads; ++w) pthread_join(th[w], NULL);
+  }
+  free(jobs);
+  free(th);
+  return 0;
+}
+
+/* ======================================================================
  * make_candidate_set (sampling.cpp:16-31)
  * ==================================================================== */
 typedef struct {

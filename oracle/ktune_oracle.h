@@ -91,6 +91,9 @@ void ko_ac_forward(int n, int h, int g, const double* params, const double* stat
  * idx_out: E x (T+1) x D visited configs (row t = Θ_t), score_out E x (T+1),
  * actions_out E x T x D in {-1,0,+1}, logp_out/value_out E x T.
  * Any output except idx_out may be NULL. threads>1 splits episodes. */
+int ko_sa_search(const ko_space* s, const ko_gbt* m, int64_t E, int32_t T, int64_t chain_offset,
+                 uint64_t sa_seed, double t0, double rate, const int32_t* init_idx, int32_t* idx_out,
+                 double* score_out, uint8_t* acc_out, int threads);
 int ko_run_episodes(const ko_space* s, const ko_gbt* m, int h, int g, const double* params,
                     int64_t E, int32_t T, int64_t episode_offset, uint64_t explore_seed,
                     const int32_t* init_idx, int32_t* idx_out, double* score_out,

@@ -107,6 +107,8 @@ def _setup_port(L):
     L.ko_run_episodes.argtypes = [C.POINTER(KoSpace), C.POINTER(KoGbt), C.c_int, C.c_int, f64p,
                                   C.c_int64, C.c_int32, C.c_int64, C.c_uint64, i32p, i32p, P, P,
                                   P, P, C.c_int]
+    L.ko_sa_search.argtypes = [C.POINTER(KoSpace), C.POINTER(KoGbt), C.c_int64, C.c_int32, C.c_int64,
+                               C.c_uint64, C.c_double, C.c_double, i32p, i32p, f64p, P, C.c_int]
     L.ko_make_candidate_set.restype = C.c_int64
     L.ko_make_candidate_set.argtypes = [C.c_int, i32p, u64p, f64p, C.c_int64, i64p]
     L.ko_kmeans_run.argtypes = [f64p, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int,
@@ -462,6 +464,19 @@ def run_episodes(sp: OSpace, g: Optional[Gbt], h, gh, params, init_idx, T, episo
                            E, T, episode_offset, explore_seed, init_idx, idx, ptr(score),
                            ptr(acts), ptr(logp), ptr(val), threads)
     return dict(idx=idx, score=score, actions=acts, logp=logp, value=val)
+
+
+def sa_search(sp: OSpace, g: Gbt, init_idx, T, chain_offset, sa_seed, t0=1.0, rate=0.99, threads=1):
+    """sa_search, builder-pinned: chain states, their
+    predicted fitness and the acceptance flags."""
+    init_idx = np.ascontiguousarray(init_idx, np.int32).reshape(-1, sp.D)
+    E = len(init_idx)
+    idx = np.zeros((E, T + 1, sp.D), np.int32)
+    score = np.zeros((E, T + 1), np.float64)
+    acc = np.zeros((E, T), np.uint8)
+    port().ko_sa_search(C.byref(sp.ko), C.byref(g.ko()), E, T, chain_offset, sa_seed, t0, rate, init_idx, idx,
+                        score, acc.ctypes.data_as(C.c_void_p), threads)
+    return dict(idx=idx, score=score, accepted=acc)
 
 
 def make_candidate_set(D, idx, ids, pred, impl="port"):

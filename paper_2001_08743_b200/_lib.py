@@ -54,6 +54,15 @@ class RolloutTaskC(C.Structure):
                 ("score", P), ("actions", P), ("logp", P), ("value", P)]
 
 
+class SaParamsC(C.Structure):
+    _fields_ = [("initial_temperature", C.c_double), ("cooling_rate", C.c_double)]
+
+
+class SaTaskC(C.Structure):
+    _fields_ = [("space", P), ("gbt", P), ("num_chains", i64), ("chain_offset", i64), ("sa_seed", u64),
+                ("init_idx", P), ("idx", P), ("score", P), ("accepted", P)]
+
+
 class KmeansOutC(C.Structure):
     _fields_ = [("centroids", P), ("assignments", P), ("l2_loss", P), ("iteration_losses", P),
                 ("num_losses", P)]
@@ -104,6 +113,7 @@ SIGNATURES = {
     "ktune_ac_destroy": (C.c_int, [P]),
     "ktune_ac_forward": (C.c_int, [P, P, P, i64, P, P, P, C.c_int]),
     "ktune_rollout": (C.c_int, [P, C.c_int, C.POINTER(RolloutTaskC), C.c_int32, C.c_int]),
+    "ktune_sa_search": (C.c_int, [P, C.c_int, C.POINTER(SaTaskC), C.c_int32, C.POINTER(SaParamsC), C.c_int]),
     "ktune_make_candidate_set": (C.c_int, [P, P, P, i64, P, C.POINTER(i64)]),
     "ktune_candidates_from_rows": (C.c_int, [P, P, P, P, i64, P, P, C.POINTER(i64), C.c_int]),
     "ktune_kmeans_run": (C.c_int, [P, P, P, C.c_int, i64, C.c_int, u64, C.c_int, C.c_int,

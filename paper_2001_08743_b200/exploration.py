@@ -20,7 +20,7 @@ from . import _lib as L
 from .context import Context, Space, default_context, ptr_of
 from .cost_model import DeviceGbt
 from .errors import ConfigError
-from .spaces import stream_seed
+from .spaces import mix64, stream_seed
 
 
 def num_parameters(n: int, h: int = 128, g: int = 64) -> int:
@@ -188,3 +188,48 @@ def run_episodes(space: Space, cost_model: Optional[DeviceGbt], agent: ActorCrit
     if o["score"] is not None:
         traj["reward"] = o["score"][:, 1:] - o["score"][:, :-1]
     return cands, traj
+
+
+@dataclass
+class SaParams:  # SPEC.md SaParams (the temperature schedule is SPEC-invented)
+    num_chains: int = 128
+    max_steps: int = 500
+    initial_temperature: float = 1.0
+    cooling_rate: float = 0.99
+
+
+def sa_search(space: Space, cost_model: DeviceGbt, seeds, params: SaParams = SaParams(), rng_seed: int = 0,
+              chain_offset: int = 0, ctx: Optional[Context] = None):
+    """sa_search(space, cost_model, seeds, params, rng_seed) -> CandidateSet (SPEC.md:229-237).
+
+    The AutoTVM parallel simulated-annealing baseline on the GPU (K7, sa.cu):
+    `num_chains` chains of `max_steps` Metropolis steps on the cost model,
+    builder-pinned semantics. Seeds are padded with uniformly
+    random configurations (stream_seed(rng_seed, "sa-pad")) when fewer than
+    num_chains are given. Returns (CandidateSet over every chain state ranked by
+    predicted fitness and deduplicated, trajectory dict(idx, score, accepted)).
+    """
+    from .sampling import make_candidate_set
+    ctx = ctx or space.ctx
+    D = space.D
+    seeds = np.asarray(seeds, np.int64).reshape(-1, D) if len(seeds) else np.zeros((0, D), np.int64)
+    E = params.num_chains
+    if len(seeds) < E:
+        st = stream_seed(rng_seed, "sa-pad")
+        pad = np.zeros((E - len(seeds), D), np.int64)
+        for i in range(len(pad)):
+            for d, c in enumerate(space.card):
+                pad[i, d] = mix64((st + i * D + d + 1) & 0xFFFFFFFFFFFFFFFF) % int(c)
+        seeds = np.concatenate([seeds, pad])
+    init = np.ascontiguousarray(seeds[:E], np.uint16)
+    T = params.max_steps
+    idx = np.zeros((E, T + 1, D), np.uint16)
+    score = np.zeros((E, T + 1))
+    acc = np.zeros((E, T), np.uint8)
+    t = L.SaTaskC(space.h, cost_model.h, E, chain_offset, stream_seed(rng_seed, "sa"),
+                  init.ctypes.data_as(C.c_void_p), idx.ctypes.data_as(C.c_void_p), score.ctypes.data_as(C.c_void_p),
+                  acc.ctypes.data_as(C.c_void_p))
+    p = L.SaParamsC(params.initial_temperature, params.cooling_rate)
+    ctx.check(L.lib().ktune_sa_search(ctx.h, 1, C.byref(t), T, C.byref(p), 0))
+    cands = make_candidate_set(space, idx.reshape(-1, D).astype(np.int32), score.reshape(-1))
+    return cands, dict(idx=idx, score=score, accepted=acc)

@@ -1,0 +1,62 @@
+"""K7 sa_search on the GPU vs the oracle restatement
+(builder-pinned semantics): chain states, predicted fitness and
+acceptance flags bit-exact; SPEC examples as properties."""
+import numpy as np
+import pytest
+
+from helpers import SPACES, fitted
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(O, ctx, name, seed):
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt
+    sp = SPACES[name]()
+    osp, og, pm = fitted(O, sp, seed=seed)
+    ds = Space(sp, ctx)
+    return sp, osp, og, ds, DeviceGbt(pm, ds)
+
+
+@pytest.mark.parametrize("name,E,T", [("resnet_c2", 128, 60), ("synthetic16", 300, 40), ("resnet_dense_u16", 7, 90)])
+def test_sa_matches_oracle(O, ctx, name, E, T):
+    from paper_2001_08743_b200.exploration import SaParams, sa_search
+    from paper_2001_08743_b200.spaces import stream_seed
+    sp, osp, og, ds, dg = _setup(O, ctx, name, E)
+    seeds = osp.random_valid(E, E) if O.ref_available() else np.zeros((E, sp.num_knobs), np.int32)
+    p = SaParams(num_chains=E, max_steps=T, initial_temperature=0.02, cooling_rate=0.97)
+    cands, tr = sa_search(ds, dg, seeds, p, rng_seed=9)
+    want = O.sa_search(osp, og, seeds, T, 0, stream_seed(9, "sa"), 0.02, 0.97)
+    assert np.array_equal(tr["idx"].astype(np.int32), want["idx"])
+    assert np.array_equal(tr["score"], want["score"])
+    assert np.array_equal(tr["accepted"], want["accepted"])
+    assert 0 < tr["accepted"].mean() < 1  # a non-degenerate schedule
+    # CandidateSet: deduplicated, ranked by predicted fitness (desc)
+    assert len(np.unique(cands.ids)) == len(cands.ids)
+    assert np.all(np.diff(cands.predicted) <= 0)
+
+
+def test_sa_spec_examples(O, ctx):
+    """T -> 0: only improvements are accepted, so every chain's fitness is
+    non-decreasing (SPEC.md:235 hill-climb limit); a Δ = 0 proposal is always
+    accepted (exp(0) = 1)."""
+    from paper_2001_08743_b200.exploration import SaParams, sa_search
+    sp, osp, og, ds, dg = _setup(O, ctx, "resnet_c2", 3)
+    _, tr = sa_search(ds, dg, np.zeros((0, sp.num_knobs)), SaParams(64, 80, 1e-300, 0.5), rng_seed=1)
+    assert np.all(np.diff(tr["score"], axis=1) >= 0)
+    assert tr["score"][:, -1].min() >= tr["score"][:, 0].min()
+    same = np.diff(tr["score"], axis=1) == 0
+    moved = np.any(tr["idx"][:, 1:] != tr["idx"][:, :-1], axis=2)
+    assert np.all(tr["accepted"][same & moved] == 1)  # equal fitness moves were taken
+
+
+def test_sa_chain_sharding_invariance(O, ctx):
+    """Chains keyed by global id: a shard with chain_offset reproduces the full run."""
+    from paper_2001_08743_b200.exploration import SaParams, sa_search
+    sp, osp, og, ds, dg = _setup(O, ctx, "synthetic8", 5)
+    seeds = np.random.default_rng(0).integers(0, 2, (100, sp.num_knobs))
+    p = SaParams(100, 30, 0.05, 0.95)
+    _, full = sa_search(ds, dg, seeds, p, rng_seed=4)
+    _, part = sa_search(ds, dg, seeds[60:], SaParams(40, 30, 0.05, 0.95), rng_seed=4, chain_offset=60)
+    assert np.array_equal(full["idx"][60:], part["idx"])
+    assert np.array_equal(full["score"][60:], part["score"])

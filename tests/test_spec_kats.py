@@ -179,3 +179,22 @@ def test_portable_math_faithful(O):
         assert abs(L.ko_exp(x) - math.exp(x)) <= 4e-16 * math.exp(x)
         if x > 0:
             assert abs(L.ko_log(x) - math.log(x)) <= 4e-16 * max(1.0, abs(math.log(x)))
+
+
+def test_sa_search_oracle_spec_examples(O):
+    """sa_search on the oracle: T -> 0 is a hill climb
+    (fitness non-decreasing); Δ = 0 proposals are accepted
+    (exp(0) = 1); deterministic from the seed."""
+    from helpers import SPACES, fitted
+    sp = SPACES["synthetic8"]()
+    osp, og, _ = fitted(O, sp, seed=2)
+    init = np.zeros((16, sp.num_knobs), np.int32)
+    r = O.sa_search(osp, og, init, 60, 0, 77, 1e-300, 0.5)
+    assert np.all(np.diff(r["score"], axis=1) >= 0)
+    same = np.diff(r["score"], axis=1) == 0
+    moved = np.any(r["idx"][:, 1:] != r["idx"][:, :-1], axis=2)
+    assert np.all(r["accepted"][same & moved] == 1)
+    r2 = O.sa_search(osp, og, init, 60, 0, 77, 1e-300, 0.5)
+    assert np.array_equal(r["idx"], r2["idx"])
+    hot = O.sa_search(osp, og, init, 60, 0, 77, 1.0, 0.99)  # T = 1: nearly every move accepted
+    assert hot["accepted"].mean() > 0.9
