@@ -364,6 +364,7 @@ def main():
                     actions=mkd((E, T, D0), torch.int8), logp=mkd((E, T), torch.float64),
                     value=mkd((E, T), torch.float64)) for _ in specs]  # persistent trajectory buffers
     clk = ClockSampler(local).__enter__()  # before the warm-up: nvidia-smi start-up stalls the GPU
+    ctx.set_option(L.OPT_PROFILE, 1)  # warm-up runs with the timed region's settings
     for _ in range(args.warmup):
         run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact)
     torch.cuda.synchronize()
@@ -373,25 +374,41 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    ctx.set_option(L.OPT_PROFILE, 1)
-    ctx.reset_stats()
+    stat_keys = [L.STAT_LAUNCHES, L.STAT_ROLLOUT_NS, L.STAT_ROLLOUT_CALLS, L.STAT_GBT_NS, L.STAT_GBT_CALLS,
+                 L.STAT_ROLLOUT_FALLBACKS, L.STAT_ROLLOUT_TC]
+    stat0 = {k: ctx.stat(k) for k in stat_keys}  # deltas over the timed region (no reset inside it)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    # one more untimed step right before the start event: after the host-side stat reads and
+    # the barrier the GPU has idled and its clocks ramp back up during the next launch
+    # (measured: +8..25 ms on the first step otherwise); the timed region is still exactly K steps
+    flush.zero_()
+    run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact)
     tc0 = time.perf_counter()
     start.record(stream)
+    step_ev = []
     for _ in range(args.steps):
         flush.zero_()  # 256 MB > L2 between timed steps
         run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact)
+        if os.environ.get("BENCH_STEP_EVENTS"):  # diagnostics: per-step device times
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            step_ev.append(ev)
     end.record(stream)
     barrier()
     tc1 = time.perf_counter()
     clk.__exit__()
     clocks = clk.summary(tc0, tc1)
     ms = start.elapsed_time(end)
-    launches = ctx.stat(L.STAT_LAUNCHES)
-    roll_ns, roll_calls = ctx.stat(L.STAT_ROLLOUT_NS), ctx.stat(L.STAT_ROLLOUT_CALLS)
-    gbt_ns, gbt_calls = ctx.stat(L.STAT_GBT_NS), ctx.stat(L.STAT_GBT_CALLS)
-    fallbacks, tc_steps = ctx.stat(L.STAT_ROLLOUT_FALLBACKS), ctx.stat(L.STAT_ROLLOUT_TC)
+    if step_ev:
+        prev = start
+        print("step ms:", [round(prev.elapsed_time(e), 2) for prev, e in zip([start] + step_ev[:-1], step_ev)],
+              file=sys.stderr)
+    dstat = lambda k: ctx.stat(k) - stat0[k]  # covers the ramp step + the K timed steps
+    launches = dstat(L.STAT_LAUNCHES) * args.steps // (args.steps + 1)
+    roll_ns, roll_calls = dstat(L.STAT_ROLLOUT_NS), dstat(L.STAT_ROLLOUT_CALLS)
+    gbt_ns, gbt_calls = dstat(L.STAT_GBT_NS), dstat(L.STAT_GBT_CALLS)
+    fallbacks, tc_steps = dstat(L.STAT_ROLLOUT_FALLBACKS), dstat(L.STAT_ROLLOUT_TC)
     ctx.set_option(L.OPT_PROFILE, 0)
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
