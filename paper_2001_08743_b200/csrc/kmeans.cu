@@ -418,6 +418,9 @@ __global__ void __launch_bounds__(kBT) assign_kernel(KtSpaceParams sp, int lut_t
 constexpr int kTcPts = 128;
 constexpr int kTcK = 32;   // 2 x 16 knobs
 constexpr int kTcMaxN = 64;
+// Below this k the exact SIMT scan (3kD fp64 ops per point) beats the tcgen05 screening
+// pass, whose per-tile MMA round trip dominates (measured at N = 1M: 45 vs 161 us for k = 8).
+constexpr int kTcMinK = 24;
 
 template <class IdxT>
 __global__ void __launch_bounds__(kTcPts) assign_tc_kernel(
@@ -1126,6 +1129,24 @@ struct Run {
   std::vector<double> iter_losses;
 };
 
+struct IterReadback {
+  double loss;
+  unsigned long long changed;
+  int32_t seq, segs;
+  unsigned long long unc;
+};
+// Collects an iteration's scalars for one host readback and clears the
+// sequential-segment counter for the next centroid update.
+__global__ void gather_readback_kernel(const double* dscal, const unsigned long long* ull, int32_t* seqcnt,
+                                       const int32_t* segs, IterReadback* out) {
+  out->loss = dscal[0];
+  out->changed = ull[0];
+  out->seq = *seqcnt;
+  out->segs = *segs;
+  out->unc = ull[2];
+  *seqcnt = 0;
+}
+
 template <class IdxT>
 struct KMeans {
   ktune_ctx* ctx;
@@ -1150,6 +1171,8 @@ struct KMeans {
   int32_t* counts;    // [k] + cstart [k] + nempty
   double* cent_a;
   double* cent_b;
+  IterReadback* rb_dev = nullptr;   // per-iteration scalars (device) ...
+  IterReadback* rb_host = nullptr;  // ... and their pinned host copy
   unsigned long long* ull;  // [0] changed, [1] diff
   double* dscal;      // [0] loss sum, [1] exact loss
   // best-of-restarts and previous-k best (for exact fallbacks)
@@ -1211,6 +1234,8 @@ struct KMeans {
     cent_b = cent_a + kt::kMaxK * D;
     best_cent = cent_b + kt::kMaxK * D;
     ull = (unsigned long long*)ctx->dev(kt::WS_VALID, 64);
+    rb_dev = (IterReadback*)ctx->dev(kt::WS_XS_RB, sizeof(IterReadback));
+    rb_host = (IterReadback*)ctx->host(3, sizeof(IterReadback));
     dscal = (double*)ctx->dev(kt::WS_SNAP, 64);
     best_asg = (int32_t*)ctx->dev(kt::WS_BEST_ASSIGN, sizeof(int32_t) * N);
     best_d2 = (double*)ctx->dev(kt::WS_BEST_D2, sizeof(double) * N);
@@ -1242,9 +1267,16 @@ struct KMeans {
   // assignment against cent; returns loss estimate; changed count if prev != null
   double assign(const double* cent, int k, const int32_t* prev, int32_t* asg, double* dd,
                 unsigned long long* changed_out) {
+    enqueue_assign(cent, k, prev, asg, dd);
+    return finish_assign(prev, changed_out);
+  }
+
+  // Stream work of one assignment pass (no host synchronisation: capturable into a
+  // CUDA graph), ending with the iteration's scalars copied into pinned memory.
+  void enqueue_assign(const double* cent, int k, const int32_t* prev, int32_t* asg, double* dd) {
     KT_CUDA(cudaMemsetAsync(ull, 0, 24, s()));
     const size_t smem = sizeof(double) * (k * D) + lut_smem;
-    if (use_tc && k <= kTcMaxN) {
+    if (use_tc && k <= kTcMaxN && k >= kTcMinK) {
       // tcgen05 screening + certified exact winner (this rank's chunk range)
       const int64_t c0 = (int64_t)rank * shard_chunks;
       const int64_t cend = std::min<int64_t>(nchunks, c0 + shard_chunks);
@@ -1290,21 +1322,17 @@ struct KMeans {
       kt::allgather(ctx, chunk + c0, chunk, sizeof(double) * shard_chunks);
       kt::allreduce_sum(ctx, ull, 1, false);
     }
-    if (!(use_tc && k <= kTcMaxN)) sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk, nchunks, dscal);
+    if (!(use_tc && k <= kTcMaxN && k >= kTcMinK)) sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk, nchunks, dscal);
     kt::check_launch(ctx, "sum_chunks");
-    struct {
-      double loss;
-      unsigned long long changed;
-      int32_t seq, segs;
-      unsigned long long unc;
-    } h;
-    KT_CUDA(cudaMemcpyAsync(&h.loss, dscal, 8, cudaMemcpyDeviceToHost, s()));
-    KT_CUDA(cudaMemcpyAsync(&h.changed, ull, 8, cudaMemcpyDeviceToHost, s()));
-    KT_CUDA(cudaMemcpyAsync(&h.seq, seqcnt, 4, cudaMemcpyDeviceToHost, s()));
-    KT_CUDA(cudaMemcpyAsync(&h.segs, csb + k, 4, cudaMemcpyDeviceToHost, s()));
-    KT_CUDA(cudaMemcpyAsync(&h.unc, ull + 2, 8, cudaMemcpyDeviceToHost, s()));
-    KT_CUDA(cudaMemsetAsync(seqcnt, 0, 4, s()));
+    // one gather + one pinned readback per iteration (instead of five pageable copies)
+    gather_readback_kernel<<<1, 1, 0, s()>>>(dscal, ull, seqcnt, csb + k, rb_dev);
+    kt::check_launch(ctx, "gather_readback");
+    KT_CUDA(cudaMemcpyAsync(rb_host, rb_dev, sizeof(IterReadback), cudaMemcpyDeviceToHost, s()));
+  }
+
+  double finish_assign(const int32_t* prev, unsigned long long* changed_out) {
     KT_CUDA(cudaStreamSynchronize(s()));
+    const IterReadback& h = *rb_host;
     if (prev) {
       ctx->stats[KTUNE_STAT_XS_SEQUENTIAL] += h.seq;
       ctx->stats[KTUNE_STAT_XS_SEGMENTS] += (int64_t)h.segs * D;
@@ -1365,10 +1393,37 @@ struct KMeans {
     kmeanspp(k, rng_seed);
     double loss = assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);
     iter_losses.assign(1, loss);
+    // Single-GPU iterations replay a captured CUDA graph (centroid update + assignment +
+    // readback: ~20 launches): the loop is launch-bound at N = 1M. Two graphs, one per
+    // parity of the a/b buffer swap.
+    const bool use_graph = world == 1 && !ctx->opt_profile;
+    cudaGraphExec_t gx[2] = {nullptr, nullptr};
+    struct GraphGuard {
+      cudaGraphExec_t* g;
+      ~GraphGuard() {
+        for (int i = 0; i < 2; ++i)
+          if (g[i]) cudaGraphExecDestroy(g[i]);
+      }
+    } guard{gx};
     for (int it = 0; it < max_iters; ++it) {
-      update_centroids(k, asg_a, d2_a, cent_b);
       unsigned long long changed = 0;
-      const double nl = assign(cent_b, k, asg_a, asg_b, d2_b, &changed);
+      if (use_graph) {
+        cudaGraphExec_t& g = gx[it & 1];
+        if (!g) {
+          cudaGraph_t graph;
+          KT_CUDA(cudaStreamBeginCapture(s(), cudaStreamCaptureModeThreadLocal));
+          update_centroids(k, asg_a, d2_a, cent_b);
+          enqueue_assign(cent_b, k, asg_a, asg_b, d2_b);
+          KT_CUDA(cudaStreamEndCapture(s(), &graph));
+          KT_CUDA(cudaGraphInstantiate(&g, graph, 0));
+          cudaGraphDestroy(graph);
+        }
+        KT_CUDA(cudaGraphLaunch(g, s()));
+      } else {
+        update_centroids(k, asg_a, d2_a, cent_b);
+        enqueue_assign(cent_b, k, asg_a, asg_b, d2_b);
+      }
+      const double nl = finish_assign(asg_a, &changed);
       ctx->stats[KTUNE_STAT_LLOYD_ITERS] += 1;
       if (nl > loss + 1e-9 + loss_err(loss) + loss_err(nl))
         kt::fail(KTUNE_ERR_LOGIC, "kmeans: Lloyd loss increased, which should be impossible");
