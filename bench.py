@@ -208,7 +208,15 @@ def kmeans_secondary(ctx, args, cpu=True):
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     iters = len(r.iteration_losses) - 1
+    # marginal cost of a Lloyd iteration: the same run stopped after one iteration (same staging,
+    # kmeans++ init and exact finalisation) subtracted
+    t1 = time.perf_counter()
+    kmeans_run(ds, idx, 8, 11, max_iters=1, restarts=1)
+    torch.cuda.synchronize()
+    dt1 = time.perf_counter() - t1
+    per_iter = (dt - dt1) / max(1, iters - 1)
     seq, segs = ctx.stat(L.STAT_XS_SEQUENTIAL), ctx.stat(L.STAT_XS_SEGMENTS)
+    aborts = ctx.stat(L.STAT_KMEANS_ABORTS)
     ctx.set_option(L.OPT_PROFILE, 1)  # separate short run: CUDA-event time of the assign kernel
     ctx.reset_stats()
     kmeans_run(ds, idx, 8, 11, max_iters=4, restarts=1)
@@ -223,11 +231,16 @@ def kmeans_secondary(ctx, args, cpu=True):
     a_ms = max(assign_ns / assign_calls / 1e6, 1e-6)
     peaks, src = load_peaks()
     ach = N * bytes_pt / (a_ms * 1e-3) / 1e9
-    out = {"metric": "k-means sampling ms/iter", "value": 1e3 * dt / max(1, iters), "unit": "ms/iter",
+    out = {"metric": "k-means sampling ms/iter", "value": 1e3 * per_iter, "unit": "ms/iter",
+           "value_note": "marginal Lloyd iteration: (kmeans_run to convergence - kmeans_run stopped after 1 "
+                         "iteration) / (iterations - 1); kmeans_run_ms is the whole call (H2D of the points, "
+                         "kmeans++, iterations, exact final centroids and loss)",
+           "ms_per_iter_whole_call": 1e3 * dt / max(1, iters),
            "higher_is_better": False,
            "workload": f"alexnet.c2 space (u16 idx), N={N} candidates, k=8, 1 restart, to convergence",
            "lloyd_iters": iters, "kmeans_run_ms": 1e3 * dt, "adaptive_sample_ms": 1e3 * dsw, "sweep_k": sw.k,
            "exact_sum_sequential_segments": f"{seq}/{segs}",
+           "certified_runs_aborted_to_exact": aborts,
            "assign_kernel_ms": a_ms,
            "assign_roofline": {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                "frac": ach / peaks["hbm_gbs"], "bytes_per_point": bytes_pt,

@@ -72,7 +72,8 @@ int ktune_ctx_synchronize(ktune_ctx* ctx);
 
 enum ktune_option {
   KTUNE_OPT_FORCE_EXACT = 1, /* 1: k-means decisions always via the exact-order fallback chains */
-  KTUNE_OPT_KMEANS_MODE = 2, /* 0 auto, 1 exact-order centroids (mode A), 2 certified integer centroids (mode B) */
+  KTUNE_OPT_KMEANS_MODE = 2, /* 0 auto (= 2 on one GPU), 1 exact-order centroids every iteration (mode A),
+                                2 certified integer-sum centroids with exact fallback (mode B) */
   KTUNE_OPT_PROFILE = 3,     /* 1: bracket the hot kernels with CUDA events on their stream (KTUNE_STAT_*_NS) */
   KTUNE_OPT_ROLLOUT_DELTA = 4, /* certification margin of the tcgen05 rollout, in units of 1e-12
                                   (0 = default) */
@@ -105,7 +106,8 @@ enum ktune_stat {
   KTUNE_STAT_ROLLOUT_CHECKED = 17,   /* KTUNE_OPT_ROLLOUT_CHECK: knob decisions checked */
   KTUNE_STAT_ROLLOUT_MISMATCH = 18,  /* certified fast decisions that disagreed with the exact one (must be 0) */
   KTUNE_STAT_ROLLOUT_MAXERR = 19,    /* max |p_fast - p_exact| over checked decisions, in units of 1e-12 */
-  KTUNE_STAT_ROLLOUT_TC = 20         /* config-steps run on the tcgen05 path */
+  KTUNE_STAT_ROLLOUT_TC = 20,        /* config-steps run on the tcgen05 path */
+  KTUNE_STAT_KMEANS_ABORTS = 21      /* certified Lloyd runs that fell back to the exact-order mode */
 };
 int ktune_ctx_stat(ktune_ctx* ctx, int stat, int64_t* value);
 int ktune_ctx_reset_stats(ktune_ctx* ctx);

@@ -23,7 +23,7 @@ STAT_LAUNCHES, STAT_KPP_FALLBACKS, STAT_DECISION_FALLBACKS, STAT_ASSIGN_FALLBACK
     STAT_SNAP_CHAINS, STAT_LLOYD_ITERS, STAT_KPP_PICKS, STAT_ROLLOUT_NS, STAT_ROLLOUT_CALLS, \
     STAT_GBT_NS, STAT_GBT_CALLS, STAT_ASSIGN_NS, STAT_ASSIGN_CALLS, STAT_XS_SEQUENTIAL, \
     STAT_XS_SEGMENTS, STAT_ROLLOUT_FALLBACKS, STAT_ROLLOUT_CHECKED, STAT_ROLLOUT_MISMATCH, \
-    STAT_ROLLOUT_MAXERR, STAT_ROLLOUT_TC = range(1, 21)
+    STAT_ROLLOUT_MAXERR, STAT_ROLLOUT_TC, STAT_KMEANS_ABORTS = range(1, 22)
 
 P = C.c_void_p
 i32 = C.c_int32

@@ -405,6 +405,183 @@ __global__ void __launch_bounds__(kBT) assign_kernel(KtSpaceParams sp, int lut_t
   }
 }
 
+// ------------------------------------------------------------------ certified Lloyd (mode B)
+// Speculative iterations on centroids computed from EXACT INTEGER sums of knob
+// indices: c_B = RN(S / (count * (card - 1))) is within 2^-53 relative of the
+// exact mean, and the reference's sequential fp64 centroid (sampling.cpp:112-121)
+// is within (count + 4) 2^-53 relative of it, so |c_B - c_ref| <= delta. Every
+// assignment is certified against that bound (the winner's d2 interval must not
+// overlap any other cluster's); an uncertain point or an empty cluster aborts the
+// speculation and the run restarts in the exact-order mode A, so the assignment
+// sequence is the reference's either way. The run's final centroids and d2 are
+// recomputed exactly (mode A) after convergence.
+
+// Segmented warp sums: lanes with the same cluster reduce their knob indices
+// and count; the group leader adds them into the block's shared sums.
+template <class IdxT>
+__device__ __forceinline__ void warp_cluster_sums(bool live, int c, const IdxT* row, int D, int32_t* s_sum,
+                                                  int32_t* s_cnt) {
+  const int lane = threadIdx.x & 31;
+  unsigned todo = __ballot_sync(0xffffffffu, live);
+  while (todo) {
+    const int leader = __ffs(todo) - 1;
+    const int cl = __shfl_sync(0xffffffffu, c, leader);
+    const unsigned m = __ballot_sync(0xffffffffu, live && c == cl) & todo;
+    if ((m >> lane) & 1u) {
+      for (int d = 0; d < D; ++d) {
+        const unsigned v = __reduce_add_sync(m, (unsigned)row[d]);
+        if (lane == leader) atomicAdd(&s_sum[cl * D + d], (int32_t)v);
+      }
+      if (lane == leader) atomicAdd(&s_cnt[cl], __popc(m));
+    }
+    todo &= ~m;
+  }
+}
+
+// Adds the block's (possibly negative) integer sums into the global ones (two's complement).
+__device__ __forceinline__ void flush_cluster_sums(int k, int D, const int32_t* s_sum, const int32_t* s_cnt,
+                                                   unsigned long long* g_sum, unsigned long long* g_cnt) {
+  for (int i = threadIdx.x; i < k * D; i += blockDim.x)
+    if (s_sum[i]) atomicAdd(&g_sum[i], (unsigned long long)(long long)s_sum[i]);
+  for (int i = threadIdx.x; i < k; i += blockDim.x)
+    if (s_cnt[i]) atomicAdd(&g_cnt[i], (unsigned long long)(long long)s_cnt[i]);
+}
+
+// Integer sums of an (exact) assignment.
+template <class IdxT>
+__global__ void __launch_bounds__(kBT) cluster_sums_kernel(const IdxT* __restrict__ pts, int64_t N, int D, int k,
+                                                           const int32_t* __restrict__ asg,
+                                                           unsigned long long* __restrict__ g_sum,
+                                                           unsigned long long* __restrict__ g_cnt) {
+  __shared__ int32_t s_sum[kt::kMaxK * kt::kMaxKnobs];
+  __shared__ int32_t s_cnt[kt::kMaxK];
+  for (int i = threadIdx.x; i < k * D; i += blockDim.x) s_sum[i] = 0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  for (int j = 0; j < kChunk / kBT; ++j) {
+    const int64_t i = base + j * kBT + threadIdx.x;
+    const bool live = i < N;
+    warp_cluster_sums(live, live ? asg[i] : 0, pts + (live ? i : 0) * D, D, s_sum, s_cnt);
+  }
+  __syncthreads();
+  flush_cluster_sums(k, D, s_sum, s_cnt, g_sum, g_cnt);
+}
+
+// c_B and its bound delta from the integer sums; counts empty clusters.
+__global__ void centroids_from_sums_kernel(KtSpaceParams sp, int k, const unsigned long long* __restrict__ g_sum,
+                                           const unsigned long long* __restrict__ g_cnt, double* __restrict__ cB,
+                                           double* __restrict__ dB, unsigned long long* __restrict__ empty) {
+  const int D = sp.D;
+  for (int i = threadIdx.x; i < k * D; i += blockDim.x) {
+    const int c = i / D, d = i % D;
+    const unsigned long long cnt = g_cnt[c];
+    double v = 0.0, del = 0.0;
+    if (cnt > 0 && sp.card[d] > 1) {
+      v = kt::ddiv((double)g_sum[i], kt::dmul((double)cnt, (double)(sp.card[d] - 1)));
+      del = ((double)cnt + 4.0) * 0x1.0p-53 * v * (1.0 + 0x1.0p-20);
+    }
+    cB[i] = v;
+    dB[i] = del;
+  }
+  if (threadIdx.x < k && g_cnt[threadIdx.x] == 0) atomicAdd(empty, 1ull);
+}
+
+// Certified assignment against c_B: d2 in the reference's operation order with
+// c_B, a rigorous interval per cluster, the winner only if its interval is
+// strictly below every other cluster's. Fused: the integer sums are updated in
+// place by the points that changed cluster (block-aggregated deltas), plus the
+// changed / uncertain counts and the loss estimate.
+template <class IdxT>
+__global__ void __launch_bounds__(kBT) assign_cert_kernel(
+    KtSpaceParams sp, int lut_total, const IdxT* __restrict__ pts, int64_t N, const double* __restrict__ cB,
+    const double* __restrict__ dB, int k, const int32_t* __restrict__ prev, int32_t* __restrict__ asg,
+    double* __restrict__ d2, double* __restrict__ chunk_sum, unsigned long long* __restrict__ counters,
+    unsigned long long* __restrict__ g_sum, unsigned long long* __restrict__ g_cnt) {
+  extern __shared__ double sdyn[];
+  __shared__ double red[32];
+  __shared__ int32_t s_sum[kt::kMaxK * kt::kMaxKnobs];
+  __shared__ int32_t s_cnt[kt::kMaxK];
+  const int D = sp.D;
+  double* s_c = sdyn;
+  double* s_d = sdyn + k * D;
+  double* s_lut = sdyn + 2 * k * D;
+  for (int i = threadIdx.x; i < k * D; i += blockDim.x) {
+    s_c[i] = cB[i];
+    s_d[i] = dB[i];
+    s_sum[i] = 0;
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s_cnt[i] = 0;
+  const double* lut = stage_lut(sp, s_lut, lut_total);
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  double part = 0.0;
+  int nchg = 0, nunc = 0;
+  const double grow = (double)(2 * D + 4) * 0x1.0p-53;
+  for (int j = 0; j < kChunk / kBT; ++j) {
+    const int64_t i = base + j * kBT + threadIdx.x;
+    const bool live = i < N;
+    int bc = 0;
+    if (live) {
+      double x[kt::kMaxKnobs];
+      for (int d = 0; d < D; ++d) x[d] = feat(sp, lut, pts + i * D, d);
+      double best = INFINITY, best_e = 0.0, lo_others = INFINITY;
+      for (int c = 0; c < k; ++c) {
+        const double* cc = s_c + c * D;
+        const double* dd = s_d + c * D;
+        double t = kt::dsub(x[0], cc[0]);
+        double s = kt::dmul(t, t);
+        double e = dd[0] * (2.0 * fabs(t) + dd[0]);
+        for (int d = 1; d < D; ++d) {
+          t = kt::dsub(x[d], cc[d]);
+          s = kt::dadd(s, kt::dmul(t, t));
+          e += dd[d] * (2.0 * fabs(t) + dd[d]);
+        }
+        // |d2_ref - s| <= e (centroid difference) + the rounding of both evaluations
+        e = (e + grow * (s + e)) * (1.0 + 0x1.0p-20) + 1e-300;
+        if (s < best) {  // strict <: lowest index on ties, as the reference
+          if (best < INFINITY) lo_others = fmin(lo_others, best - best_e);
+          best = s;
+          best_e = e;
+          bc = c;
+        } else {
+          lo_others = fmin(lo_others, s - e);
+        }
+      }
+      // certified only if no other cluster's interval reaches the winner's
+      if (!(lo_others > best + best_e)) ++nunc;
+      asg[i] = bc;
+      d2[i] = best;
+      part = kt::dadd(part, best);
+      const int pc = prev[i];
+      if (pc != bc) {  // move this point's indices between the clusters' integer sums
+        ++nchg;
+        for (int d = 0; d < D; ++d) {
+          const int v = (int)pts[i * D + d];
+          if (v) {
+            atomicAdd(&s_sum[bc * D + d], v);
+            atomicAdd(&s_sum[pc * D + d], -v);
+          }
+        }
+        atomicAdd(&s_cnt[bc], 1);
+        atomicAdd(&s_cnt[pc], -1);
+      }
+    }
+  }
+  const double s = block_sum(part, red);
+  if (threadIdx.x == 0) chunk_sum[blockIdx.x] = s;
+  for (int o = 16; o > 0; o >>= 1) {
+    nchg += __shfl_down_sync(0xffffffff, nchg, o);
+    nunc += __shfl_down_sync(0xffffffff, nunc, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (nchg) atomicAdd(counters, (unsigned long long)nchg);
+    if (nunc) atomicAdd(counters + 2, (unsigned long long)nunc);
+  }
+  __syncthreads();
+  flush_cluster_sums(k, D, s_sum, s_cnt, g_sum, g_cnt);
+}
+
 // ------------------------------------------------------------------ assign on tcgen05 (K3 fast path)
 // Screening GEMM on the 5th-gen tensor cores: for a tile of 128 points,
 //   dot[p][c] = sum_d idx[p][d] * (2^10 * c[c][d] / (card_d - 1))
@@ -1134,16 +1311,19 @@ struct IterReadback {
   unsigned long long changed;
   int32_t seq, segs;
   unsigned long long unc;
+  unsigned long long empty;  // certified mode: empty clusters seen by centroids_from_sums
 };
 // Collects an iteration's scalars for one host readback and clears the
 // sequential-segment counter for the next centroid update.
 __global__ void gather_readback_kernel(const double* dscal, const unsigned long long* ull, int32_t* seqcnt,
-                                       const int32_t* segs, IterReadback* out) {
+                                       const int32_t* segs, IterReadback* outs, int* slot = nullptr) {
+  IterReadback* out = slot ? outs + (*slot)++ : outs;
   out->loss = dscal[0];
   out->changed = ull[0];
   out->seq = *seqcnt;
   out->segs = *segs;
   out->unc = ull[2];
+  out->empty = ull[3];
   *seqcnt = 0;
 }
 
@@ -1171,6 +1351,10 @@ struct KMeans {
   int32_t* counts;    // [k] + cstart [k] + nempty
   double* cent_a;
   double* cent_b;
+  unsigned long long* isum[2] = {nullptr, nullptr};  // certified mode: integer sums [k*D] + counts [k]
+  double* cB = nullptr;  // certified mode: centroids from the integer sums and their bounds
+  double* dB = nullptr;
+  int* rb_slot = nullptr;           // next readback slot of a batched certified run
   IterReadback* rb_dev = nullptr;   // per-iteration scalars (device) ...
   IterReadback* rb_host = nullptr;  // ... and their pinned host copy
   unsigned long long* ull;  // [0] changed, [1] diff
@@ -1234,8 +1418,18 @@ struct KMeans {
     cent_b = cent_a + kt::kMaxK * D;
     best_cent = cent_b + kt::kMaxK * D;
     ull = (unsigned long long*)ctx->dev(kt::WS_VALID, 64);
-    rb_dev = (IterReadback*)ctx->dev(kt::WS_XS_RB, sizeof(IterReadback));
-    rb_host = (IterReadback*)ctx->host(3, sizeof(IterReadback));
+    rb_dev = (IterReadback*)ctx->dev(kt::WS_XS_RB, sizeof(IterReadback) * 8 + 64);
+    rb_slot = reinterpret_cast<int*>(rb_dev + 8);
+    {
+      const size_t words = (size_t)kt::kMaxK * (kt::kMaxKnobs + 1);
+      unsigned long long* w = (unsigned long long*)ctx->dev(kt::WS_KM_CERT, sizeof(unsigned long long) * words * 2 +
+                                                                                sizeof(double) * kt::kMaxK * D * 2);
+      isum[0] = w;
+      isum[1] = w + words;
+      cB = reinterpret_cast<double*>(w + 2 * words);
+      dB = cB + kt::kMaxK * D;
+    }
+    rb_host = (IterReadback*)ctx->host(3, sizeof(IterReadback) * 8);
     dscal = (double*)ctx->dev(kt::WS_SNAP, 64);
     best_asg = (int32_t*)ctx->dev(kt::WS_BEST_ASSIGN, sizeof(int32_t) * N);
     best_d2 = (double*)ctx->dev(kt::WS_BEST_D2, sizeof(double) * N);
@@ -1437,6 +1631,105 @@ struct KMeans {
     return loss;
   }
 
+  // Certified speculative Lloyd (mode B, see assign_cert_kernel): returns false
+  // (the caller reruns the exact mode A) on an uncertain point or an empty
+  // cluster. On success the final centroids and d2 are recomputed exactly from
+  // the last two assignments, as the reference's loop leaves them.
+  bool lloyd_cert(int k, uint64_t rng_seed, int max_iters, std::vector<double>& iter_losses) {
+    kmeanspp(k, rng_seed);
+    double loss = assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);  // exact
+    iter_losses.assign(1, loss);
+    const size_t words = (size_t)kt::kMaxK * (kt::kMaxKnobs + 1);
+    const size_t tsmem = sizeof(double) * 2 * k * D + lut_smem;
+    KT_CUDA(cudaFuncSetAttribute(assign_cert_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
+    int cur = 0;
+    KT_CUDA(cudaMemsetAsync(isum[cur], 0, sizeof(unsigned long long) * words, s()));
+    cluster_sums_kernel<IdxT><<<(unsigned)nchunks, kBT, 0, s()>>>(pts, N, D, k, asg_a, isum[cur],
+                                                                  isum[cur] + (size_t)kt::kMaxK * kt::kMaxKnobs);
+    kt::check_launch(ctx, "cluster_sums");
+    // Iterations run in batches of kCertBatch replayed CUDA graphs (one per parity of the
+    // a/b swap) with ONE readback per batch. Iterations past convergence are idempotent
+    // (same assignment, same sums), so overshooting inside a batch changes no state.
+    constexpr int kCertBatch = 4;
+    unsigned long long* cs = isum[cur];  // sums of asg_a; updated in place to those of asg_b
+    cudaGraphExec_t gx[2] = {nullptr, nullptr};
+    struct GraphGuard {
+      cudaGraphExec_t* g;
+      ~GraphGuard() {
+        for (int i = 0; i < 2; ++i)
+          if (g[i]) cudaGraphExecDestroy(g[i]);
+      }
+    } guard{gx};
+    auto enqueue_iter = [&]() {
+      KT_CUDA(cudaMemsetAsync(ull, 0, 32, s()));
+      centroids_from_sums_kernel<<<1, 1024, 0, s()>>>(sp->params, k, cs, cs + (size_t)kt::kMaxK * kt::kMaxKnobs, cB,
+                                                      dB, ull + 3);
+      assign_cert_kernel<IdxT><<<(unsigned)nchunks, kBT, tsmem, s()>>>(
+          sp->params, lut_total, pts, N, cB, dB, k, asg_a, asg_b, d2_b, chunk, ull, cs,
+          cs + (size_t)kt::kMaxK * kt::kMaxKnobs);
+      kt::check_launch(ctx, "assign_cert", 2);
+      sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk, nchunks, dscal);
+      gather_readback_kernel<<<1, 1, 0, s()>>>(dscal, ull, seqcnt, csb + k, rb_dev, rb_slot);
+    };
+    int iters = 0;
+    bool done = false;
+    for (int it0 = 0; it0 < max_iters && !done; it0 += kCertBatch) {
+      const int nb = std::min(kCertBatch, max_iters - it0);
+      KT_CUDA(cudaMemsetAsync(rb_slot, 0, sizeof(int), s()));
+      int32_t* sa = asg_a;  // the device-side view of the swaps inside this batch
+      int32_t* sb = asg_b;
+      double* da = d2_a;
+      double* db = d2_b;
+      for (int j = 0; j < nb; ++j) {
+        cudaGraphExec_t& g = gx[(it0 + j) & 1];
+        if (!g) {
+          cudaGraph_t graph;
+          KT_CUDA(cudaStreamBeginCapture(s(), cudaStreamCaptureModeThreadLocal));
+          enqueue_iter();
+          KT_CUDA(cudaStreamEndCapture(s(), &graph));
+          KT_CUDA(cudaGraphInstantiate(&g, graph, 0));
+          cudaGraphDestroy(graph);
+        }
+        KT_CUDA(cudaGraphLaunch(g, s()));
+        std::swap(asg_a, asg_b);
+        std::swap(d2_a, d2_b);
+      }
+      asg_a = sa;
+      asg_b = sb;
+      d2_a = da;
+      d2_b = db;
+      KT_CUDA(cudaMemcpyAsync(rb_host, rb_dev, sizeof(IterReadback) * nb, cudaMemcpyDeviceToHost, s()));
+      KT_CUDA(cudaStreamSynchronize(s()));
+      for (int j = 0; j < nb; ++j) {
+        const IterReadback h = rb_host[j];
+        if (h.empty || h.unc) return false;  // speculation off: rerun exactly
+        ctx->stats[KTUNE_STAT_LLOYD_ITERS] += 1;
+        if (h.loss > loss * (1.0 + 1e-9) + 1e-9 + loss_err(loss) + loss_err(h.loss))
+          kt::fail(KTUNE_ERR_LOGIC, "kmeans: Lloyd loss increased, which should be impossible");
+        std::swap(asg_a, asg_b);
+        std::swap(d2_a, d2_b);
+        loss = h.loss;
+        iter_losses.push_back(h.loss);
+        ++iters;
+        if (h.changed == 0) {
+          done = true;
+          break;
+        }
+      }
+    }
+    if (iters > 0) {
+      // exact final state: centroids from the previous assignment (asg_b), then the exact
+      // d2 against them; the certified assignment must be reproduced exactly
+      update_centroids(k, asg_b, d2_b, cent_b);
+      assign(cent_b, k, nullptr, asg_b, d2_b, nullptr);
+      if (!same_assign(asg_a, asg_b)) return false;
+      std::swap(cent_a, cent_b);
+      std::swap(asg_a, asg_b);
+      std::swap(d2_a, d2_b);
+    }
+    return true;
+  }
+
   struct Result {
     double loss, loss_exact;
     std::vector<double> iter_losses;
@@ -1450,7 +1743,12 @@ struct KMeans {
     bool have = false;
     for (int r = 0; r < std::max(1, restarts); ++r) {
       std::vector<double> il;
-      lloyd(k, kt::seed_combine(seed, (uint64_t)r), max_iters, il);
+      const uint64_t rs = kt::seed_combine(seed, (uint64_t)r);
+      const bool spec = world == 1 && !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1;
+      if (!spec || !lloyd_cert(k, rs, max_iters, il)) {
+        if (spec) ctx->stats[KTUNE_STAT_KMEANS_ABORTS] += 1;
+        lloyd(k, rs, max_iters, il);
+      }
       const double Lx = exact_loss(d2_a);
       il.back() = Lx;
       if (!have || Lx < best.loss_exact) {

@@ -163,3 +163,29 @@ def test_assign_paths_bit_exact(O, ctx, ref_ok, mode, name, n, k, seed):
     assert np.array_equal(got.centroids, want["centroids"])
     assert got.l2_loss == want["loss"]
     print("uncertain (exact-fallback) points:", ctx.stat(L.STAT_ASSIGN_FALLBACKS))
+
+
+@pytest.mark.parametrize("name,n,k,seed", [("alexnet_c3_u16", 30000, 8, 3), ("synthetic16", 20000, 12, 4)])
+def test_certified_lloyd_equals_exact_mode(O, ctx, name, n, k, seed):
+    """Mode B (integer-sum centroids, certified assignments, exact finalisation) and
+    mode A (exact-order sums every iteration) give identical runs; mode B ran
+    without falling back."""
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.sampling import kmeans_run
+    sp = SPACES[name]()
+    osp = O.OSpace(sp)
+    cidx, cids, _ = candidate_set(O, osp, n, seed)
+    ds = _space(ctx, sp)
+    ctx.reset_stats()
+    b = kmeans_run(ds, cidx, k, seed, restarts=2)
+    aborts = ctx.stat(L.STAT_KMEANS_ABORTS)
+    ctx.set_option(L.OPT_KMEANS_MODE, 1)
+    try:
+        a = kmeans_run(ds, cidx, k, seed, restarts=2)
+    finally:
+        ctx.set_option(L.OPT_KMEANS_MODE, 0)
+    assert aborts == 0
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centroids, b.centroids)
+    assert a.l2_loss == b.l2_loss
+    assert len(a.iteration_losses) == len(b.iteration_losses)
