@@ -478,7 +478,8 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       TR(1)
       if (leader) {
         kt::tc::fence_after();
-        for (int kb = 0; kb < K1 / 16; ++kb) kt::tc::mma_f16(tslot, ad0 + 16 * kb, b1d + 16 * kb, id128, kb > 0);
+        if (L.check != 3)
+          for (int kb = 0; kb < K1 / 16; ++kb) kt::tc::mma_f16(tslot, ad0 + 16 * kb, b1d + 16 * kb, id128, kb > 0);
         kt::tc::commit(mb);
       }
       uint32_t raw[64];
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       TR(4)
       if (leader) {  // L2, K half 0
         kt::tc::fence_after();
-        mma_split4(tslot, ad0, b2d, 128, 0, id128, false);
+        if (L.check != 3) mma_split4(tslot, ad0, b2d, 128, 0, id128, false);
         kt::tc::commit(mb);
       }
       if (lw) {
@@ -547,7 +548,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       TR(8)
       if (leader) {  // L2, K half 1
         kt::tc::fence_after();
-        mma_split4(tslot, ad0, b2d, 128, 4, id128, true);
+        if (L.check != 3) mma_split4(tslot, ad0, b2d, 128, 4, id128, true);
         kt::tc::commit(mb);
       }
       if (lw) {
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       TR(11)
       if (leader) {  // L3 logits (accumulator columns 0..N3-1; hv stays in 64..127)
         kt::tc::fence_after();
-        mma_split4(tslot, ad0, b3d, 64, 0, idn3, false);
+        if (L.check != 3) mma_split4(tslot, ad0, b3d, 64, 0, idn3, false);
         kt::tc::commit(mb);
       }
       if (lw) {
@@ -640,7 +641,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         uint32_t fb;
         TR(14)
         const uint32_t allk = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
-        fb = L.check == 1 ? allk : (allk & ~cert);
+        fb = L.check == 1 ? allk : (L.check == 3 ? 0u : (allk & ~cert));  // 3: timing experiment (no MMAs)
         if (!lr) fb = 0;
         n_fallback += L.check == 1 ? 0 : __popc(fb);
         n_checked += L.check == 1 ? __popc(fb) : 0;

@@ -30,7 +30,7 @@ for _ in range(2):
     run_episodes_batch(tasks, T, ctx, host_out=out, exact=exact)
 torch.cuda.synchronize()
 mode = os.environ.get("MODE", "")
-if os.environ.get("STAGGER"): ctx.set_option(L.OPT_ROLLOUT_STAGGER, int(os.environ["STAGGER"]))
+if os.environ.get("CHECKMODE"): ctx.set_option(L.OPT_ROLLOUT_CHECK, int(os.environ["CHECKMODE"]))
 if "prof" in mode: ctx.set_option(L.OPT_PROFILE, 1)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 clk = None
