@@ -265,6 +265,11 @@ int ktune_candidates_from_rows(ktune_ctx* ctx, const ktune_space* space, const u
                                const double* pred, int64_t n, int64_t* out_rows, uint64_t* out_ids,
                                int64_t* out_n, int flags);
 
+/* knob_options' counting pass (sampling.cpp:249-256) on the device: counts has
+ * sum(card) entries, counts[sum(card[0..d-1]) + v] = #{i : idx[i][d] == v}.
+ * Honours KTUNE_F_DEVICE. */
+int ktune_knob_histogram(ktune_ctx* ctx, const ktune_space* space, const void* idx, int idx_bytes,
+                         int64_t N, uint64_t* counts, int flags);
 /* ------------------------------------------------------------------ k-means
  * kmeans_run (sampling.hpp:37-38, sampling.cpp:157-175) over lattice points
  * given as knob indices (N x D, idx_bytes 1 or 2) of `space` (features are

@@ -116,3 +116,68 @@ extern "C" int ktune_candidates_from_rows(ktune_ctx* ctx, const ktune_space* spa
     *out_n = m;
   });
 }
+
+// ------------------------------------------------------------------ knob histograms
+// knob_options' counting pass (sampling.cpp:249-256) over a candidate set on the
+// device: counts[lut_off[d] + v] = #{i : idx[i][d] == v}. Block-private shared
+// histograms when the space's total cardinality fits, global atomics otherwise.
+namespace {
+constexpr int kHistThreads = 256;
+constexpr int kHistSmemBins = 12288;
+
+template <class IdxT>
+__global__ void __launch_bounds__(kHistThreads) knob_hist_kernel(KtSpaceParams sp, int total, const IdxT* __restrict__ idx,
+                                                                 int64_t N, unsigned long long* __restrict__ counts,
+                                                                 int use_smem) {
+  __shared__ int32_t h[kHistSmemBins];
+  const int D = sp.D;
+  if (use_smem) {
+    for (int i = threadIdx.x; i < total; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+  }
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N * D; e += (int64_t)gridDim.x * blockDim.x) {
+    const int d = (int)(e % D);
+    const int bin = sp.lut_off[d] + (int)idx[e];
+    if (use_smem) atomicAdd(&h[bin], 1);
+    else atomicAdd(&counts[bin], 1ull);
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < total; i += blockDim.x)
+      if (h[i]) atomicAdd(&counts[i], (unsigned long long)h[i]);
+  }
+}
+}  // namespace
+
+namespace kt {
+void knob_histogram_device(ktune_ctx* ctx, const ktune_space* space, const void* d_idx, int idx_bytes, int64_t N,
+                           unsigned long long* d_counts) {
+  const int total = space->lut_total;
+  KT_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(unsigned long long) * std::max(1, total), ctx->stream));
+  if (N <= 0) return;
+  const int use_smem = total <= kHistSmemBins ? 1 : 0;
+  const int grid = (int)std::min<int64_t>(ceil_div(N * space->D, kHistThreads), (int64_t)sm_count(ctx) * 8);
+  if (idx_bytes == 1)
+    knob_hist_kernel<uint8_t><<<grid, kHistThreads, 0, ctx->stream>>>(space->params, total, (const uint8_t*)d_idx,
+                                                                      N, d_counts, use_smem);
+  else
+    knob_hist_kernel<uint16_t><<<grid, kHistThreads, 0, ctx->stream>>>(space->params, total, (const uint16_t*)d_idx,
+                                                                       N, d_counts, use_smem);
+  check_launch(ctx, "knob_hist");
+}
+}  // namespace kt
+
+extern "C" int ktune_knob_histogram(ktune_ctx* ctx, const ktune_space* space, const void* idx, int idx_bytes,
+                                    int64_t N, uint64_t* counts, int flags) {
+  return kt_guard(ctx, [&] {
+    if (!space || N < 0 || (idx_bytes != 1 && idx_bytes != 2))
+      kt::fail(KTUNE_ERR_CONFIG, "knob_histogram: bad space, count or index width");
+    const bool dev = flags & KTUNE_F_DEVICE;
+    const void* d_idx = kt::stage_in(ctx, kt::WS_IN0, idx, (size_t)N * space->D * idx_bytes, dev);
+    unsigned long long* d_c = (unsigned long long*)kt::out_buf(ctx, kt::WS_OUT0, counts,
+                                                               sizeof(uint64_t) * std::max(1, space->lut_total), dev);
+    kt::knob_histogram_device(ctx, space, d_idx, idx_bytes, N, d_c);
+    kt::stage_out(ctx, counts, d_c, sizeof(uint64_t) * space->lut_total, dev);
+    if (!dev) KT_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}

@@ -76,6 +76,22 @@ struct KnobOption {
 
 // knob_options (sampling.cpp:249-269): per knob, observed indices ordered by
 // (count desc, index asc).
+// Ordering of per-knob counts (counts[lut_off[d] + v], e.g. from the device histogram).
+std::vector<std::vector<KnobOption>> options_from_counts(const ktune_space* s, const uint64_t* counts) {
+  std::vector<std::vector<KnobOption>> out(s->D);
+  int off = 0;
+  for (int d = 0; d < s->D; ++d) {
+    for (int v = 0; v < s->card[d]; ++v)
+      if (counts[off + v] > 0) out[d].push_back({v, (int)counts[off + v]});
+    off += s->card[d];
+    std::sort(out[d].begin(), out[d].end(), [](const KnobOption& a, const KnobOption& b) {
+      if (a.count != b.count) return a.count > b.count;
+      return a.index < b.index;
+    });
+  }
+  return out;
+}
+
 std::vector<std::vector<KnobOption>> knob_options(const ktune_space* s, const int32_t* cand, int64_t n) {
   std::vector<std::vector<KnobOption>> out(s->D);
   for (int d = 0; d < s->D; ++d) {
@@ -188,10 +204,8 @@ void random_valid_unvisited(const ktune_space* s, const Visited& vis, Rng& rng, 
 }
 
 // synthesize_sample (sampling.cpp:379-403).
-void synthesize(const ktune_space* s, const int32_t* cand, int64_t n, const Visited& vis, Rng& rng,
-                int32_t* out) {
-  if (n == 0) kt::fail(KTUNE_ERR_CONFIG, "synthesize_sample: empty candidate set");
-  const auto opts = knob_options(s, cand, n);
+void synthesize_with(const ktune_space* s, const std::vector<std::vector<KnobOption>>& opts, const Visited& vis,
+                     Rng& rng, int32_t* out) {
   std::vector<int32_t> asm_cfg;
   const bool have = best_valid_assembly(s, opts, asm_cfg);
   if (have && !vis.count(id_of(s, asm_cfg.data()))) {
@@ -215,6 +229,12 @@ void synthesize(const ktune_space* s, const int32_t* cand, int64_t n, const Visi
     }
   }
   random_valid_unvisited(s, vis, rng, out);
+}
+
+void synthesize(const ktune_space* s, const int32_t* cand, int64_t n, const Visited& vis, Rng& rng,
+                int32_t* out) {
+  if (n == 0) kt::fail(KTUNE_ERR_CONFIG, "synthesize_sample: empty candidate set");
+  synthesize_with(s, knob_options(s, cand, n), vis, rng, out);
 }
 
 }  // namespace
@@ -276,9 +296,19 @@ int ktune_adaptive_sample(ktune_ctx* ctx, const ktune_space* space, const int32_
     if (rc != KTUNE_OK) throw kt::Error(rc, ctx->last_error);
     Visited vis(visited, visited + n_visited);
     Rng rng{stream_seed(rng_seed, "synthesis")};  // sampling.cpp:454
+    // knob_options is a function of the candidate set alone (sampling.cpp:384): its
+    // counting pass runs once, on the device, the first time a snapped config is visited
+    std::vector<std::vector<KnobOption>> opts;
     for (int c = 0; c < k; ++c) {
       int32_t* cfg = snapped.data() + (size_t)c * D;
-      if (vis.count(id_of(space, cfg))) synthesize(space, cand_idx, N, vis, rng, cfg);
+      if (!vis.count(id_of(space, cfg))) continue;
+      if (opts.empty()) {
+        std::vector<uint64_t> counts(std::max(1, space->lut_total));
+        const int rh = ktune_knob_histogram(ctx, space, packed.data(), ib, N, counts.data(), 0);
+        if (rh != KTUNE_OK) throw kt::Error(rh, ctx->last_error);
+        opts = options_from_counts(space, counts.data());
+      }
+      synthesize_with(space, opts, vis, rng, cfg);
     }
     std::memcpy(out_idx, snapped.data(), sizeof(int32_t) * k * D);
     *out_count = k;

@@ -50,3 +50,22 @@ def test_rollout_to_candidates_on_device(O, ctx):
     host = make_candidate_set(ds, out["idx"].cpu().numpy().reshape(-1, 8).astype(np.int32),
                               out["score"].cpu().numpy().reshape(-1))
     assert np.array_equal(ids.cpu().numpy(), host.ids)
+
+
+@pytest.mark.parametrize("name,n", [("alexnet_c3_u16", 50000), ("synthetic16", 30000), ("resnet_c2", 1)])
+def test_knob_histogram_matches_counts(ctx, name, n):
+    """knob_options' counting pass (sampling.cpp:249-256) on the device."""
+    import ctypes as C
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.context import Space
+    sp = SPACES[name]()
+    ds = Space(sp, ctx)
+    g = np.random.default_rng(n)
+    idx = np.stack([g.integers(0, c, n) for c in sp.cards], 1).astype(ds.idx_dtype)
+    counts = np.zeros(sum(sp.cards), np.uint64)
+    ctx.check(L.lib().ktune_knob_histogram(ctx.h, ds.h, idx.ctypes.data_as(C.c_void_p), ds.index_bytes, n,
+                                           counts.ctypes.data_as(C.c_void_p), 0))
+    off = 0
+    for d, c in enumerate(sp.cards):
+        assert np.array_equal(counts[off:off + c], np.bincount(idx[:, d].astype(np.int64), minlength=c)), d
+        off += c
