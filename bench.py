@@ -119,6 +119,16 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def allreduce_max(v: float) -> float:
+    """Max over ranks (device tensor for NCCL, host tensor for gloo)."""
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -348,10 +358,17 @@ def main():
 
     import torch
     world, rank, local = dist_env()
+    # BENCH_DIST_BACKEND=gloo + fewer GPUs than ranks: a functional test of the N > 1 path
+    # on one GPU (ranks share devices); the driver's runs use NCCL with one GPU per rank
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2001_08743_b200 import _lib as L
     from paper_2001_08743_b200.context import Context, Space
     from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
@@ -359,7 +376,8 @@ def main():
     from paper_2001_08743_b200.workloads import encode
 
     from paper_2001_08743_b200.distributed import create_context
-    ctx = create_context(local, rank, world)  # NCCL communicator for the k-means all-gathers when world > 1
+    # the library's NCCL communicator is only needed by the sharded k-means (--kmeans-dist)
+    ctx = create_context(local, rank, world) if (world > 1 and args.kmeans_dist) else create_context(local, 0, 1)
     stream = torch.cuda.Stream()  # a real stream handle shared by torch and libktune_cuda
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
@@ -427,9 +445,7 @@ def main():
     fallbacks, tc_steps = dstat(L.STAT_ROLLOUT_FALLBACKS), dstat(L.STAT_ROLLOUT_TC)
     ctx.set_option(L.OPT_PROFILE, 0)
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = allreduce_max(ms)
     units_per_step = world * len(specs) * E * T
     value = units_per_step * args.steps / (ms * 1e-3)
     n_knobs = specs[0].space.num_knobs
@@ -469,9 +485,7 @@ def main():
         barrier()
         dt = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            dt = float(t.item())
+            dt = allreduce_max(dt)
         bi = sum(h.nbytes for h in host_init)
         bo = sum(sum(v.nbytes for v in o.values()) for o in host_out)
         e2e = {"value": units_per_step * args.steps / dt, "unit": "config-steps/s", "h2d_bytes_per_step": bi,
