@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
           for (int j = 0; j < 16; ++j)
             vs = fmaf(swv2[c0 - 64 + j], act_scaled(fmaf(__uint_as_float(v[j]), sc2, sbv1[c0 - 64 + j]), 1.f), vs);
         }
-        if (lr && tk.value) tk.value[e * T + t] = (double)(vs + sbv2[0]);
+        if (lr && tk.value && L.check != 4) tk.value[e * T + t] = (double)(vs + sbv2[0]);
         TR(12)
         kt::tc::mbar_wait(mb, ph);
         kt::tc::fence_after();
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
             if (d < n) s_col[d * kThr + tid] = cfg.get(d);
         }
         TR(10)
-        if (lr) {
+        if (lr && L.check != 4) {  // 4: timing experiment (no trajectory writes)
           store_row_idx(tk.idx + (e * (int64_t)(T + 1) + t + 1) * n, cfg, n);
           if (tk.actions) {
             int8_t* ad = tk.actions + (e * (int64_t)T + t) * n;
