@@ -847,7 +847,7 @@ void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_beg
       ctx->stats[KTUNE_STAT_ROLLOUT_TC] += rw.E * (int64_t)(t_end - t_begin);
     }
     L.num_tasks = nl;
-    if (ctas == 0 || t_end <= t_begin) continue;
+    if (ctas == 0 || (t_end <= t_begin && t_begin != 0)) continue;  // T = 0 still writes row 0
     size_t smem = 0;
     for (int k = 0; k < nl; ++k)
       smem = std::max<size_t>(smem, tc_smem_bytes(L.task[k].n, L.task[k].gnode ? L.task[k].ntrees : 0,

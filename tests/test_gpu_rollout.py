@@ -221,3 +221,28 @@ def test_rollout_tc_segmented_host_path(O, ctx):
     want = O.run_episodes(osp, og, 128, 64, agent.params, init[:6], T, 3, stream_seed(0, "explore"))
     assert np.array_equal(host[0]["idx"][:6].astype(np.int32), want["idx"])
     assert np.array_equal(host[0]["score"][:6], want["score"])
+
+
+@pytest.mark.parametrize("cards,E,T", [((5,), 1, 7), ((1, 3, 1, 9), 33, 12), ((2,) * 21, 40, 6), ((7, 4, 2), 65, 0),
+                                       ((3, 17, 2, 5, 11), 97, 1)])
+def test_rollout_tc_edge_shapes(O, ctx, cards, E, T):
+    """Edge shapes on the tcgen05 path: one knob, cardinality-1 knobs, 21 knobs (the
+    largest N3 <= 64), T = 0 / 1, episode counts that leave partial warps and tiles."""
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt
+    from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
+    from paper_2001_08743_b200.spaces import stream_seed
+    sp = S.small_space(list(cards))
+    osp, og, pm = fitted(O, sp, seed=E + T)
+    ds = Space(sp, ctx)
+    agent = ActorCritic(sp.num_knobs, 128, 64, seed=E, ctx=ctx)
+    g = np.random.default_rng(E)
+    init = np.stack([g.integers(0, c, E) for c in cards], 1).astype(np.int32)
+    out = run_episodes_batch([RolloutTask(ds, agent, DeviceGbt(pm, ds), init, 11, 5)], T)[0]
+    want = O.run_episodes(osp, og, 128, 64, agent.params, init, T, 11, stream_seed(5, "explore"))
+    assert np.array_equal(out["idx"].astype(np.int32), want["idx"])
+    assert np.array_equal(out["score"], want["score"])
+    if T:
+        assert np.array_equal(out["actions"], want["actions"])
+        assert _close(out["logp"], want["logp"]) and _close(out["value"], want["value"])
