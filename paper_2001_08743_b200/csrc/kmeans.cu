@@ -484,7 +484,19 @@ __global__ void centroids_from_sums_kernel(KtSpaceParams sp, int k, const unsign
     cB[i] = v;
     dB[i] = del;
   }
-  if (threadIdx.x < k && g_cnt[threadIdx.x] == 0) atomicAdd(empty, 1ull);
+  __syncthreads();
+  // per-cluster bound of |d2(x, c_B) - d2(x, c_ref)| without the rounding term: features and
+  // centroids lie in [0, 1], so |x_d - c_d| <= 1 and sum_d delta_d (2|x_d - c_d| + delta_d)
+  // <= sum_d delta_d (2 + delta_d)
+  if (threadIdx.x < k) {
+    double e = 0.0;
+    for (int d = 0; d < D; ++d) {
+      const double del = dB[threadIdx.x * D + d];
+      e += del * (2.0 + del);
+    }
+    dB[kt::kMaxK * kt::kMaxKnobs + threadIdx.x] = e * (1.0 + 0x1.0p-20);
+    if (g_cnt[threadIdx.x] == 0) atomicAdd(empty, 1ull);
+  }
 }
 
 // Certified assignment against c_B: d2 in the reference's operation order with
@@ -504,13 +516,13 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
   __shared__ int32_t s_cnt[kt::kMaxK];
   const int D = sp.D;
   double* s_c = sdyn;
-  double* s_d = sdyn + k * D;
-  double* s_lut = sdyn + 2 * k * D;
+  double* s_e = sdyn + k * D;  // per-cluster centroid-difference bound E_c
+  double* s_lut = sdyn + k * D + kt::kMaxK;
   for (int i = threadIdx.x; i < k * D; i += blockDim.x) {
     s_c[i] = cB[i];
-    s_d[i] = dB[i];
     s_sum[i] = 0;
   }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s_e[i] = dB[kt::kMaxK * kt::kMaxKnobs + i];
   for (int i = threadIdx.x; i < k; i += blockDim.x) s_cnt[i] = 0;
   const double* lut = stage_lut(sp, s_lut, lut_total);
   __syncthreads();
@@ -528,17 +540,14 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
       double best = INFINITY, best_e = 0.0, lo_others = INFINITY;
       for (int c = 0; c < k; ++c) {
         const double* cc = s_c + c * D;
-        const double* dd = s_d + c * D;
         double t = kt::dsub(x[0], cc[0]);
         double s = kt::dmul(t, t);
-        double e = dd[0] * (2.0 * fabs(t) + dd[0]);
         for (int d = 1; d < D; ++d) {
           t = kt::dsub(x[d], cc[d]);
           s = kt::dadd(s, kt::dmul(t, t));
-          e += dd[d] * (2.0 * fabs(t) + dd[d]);
         }
-        // |d2_ref - s| <= e (centroid difference) + the rounding of both evaluations
-        e = (e + grow * (s + e)) * (1.0 + 0x1.0p-20) + 1e-300;
+        // |d2_ref - s| <= E_c (centroid difference) + the rounding of both evaluations
+        const double e = (s_e[c] + grow * (s + s_e[c])) * (1.0 + 0x1.0p-20) + 1e-300;
         if (s < best) {  // strict <: lowest index on ties, as the reference
           if (best < INFINITY) lo_others = fmin(lo_others, best - best_e);
           best = s;
@@ -1422,12 +1431,13 @@ struct KMeans {
     rb_slot = reinterpret_cast<int*>(rb_dev + 8);
     {
       const size_t words = (size_t)kt::kMaxK * (kt::kMaxKnobs + 1);
-      unsigned long long* w = (unsigned long long*)ctx->dev(kt::WS_KM_CERT, sizeof(unsigned long long) * words * 2 +
-                                                                                sizeof(double) * kt::kMaxK * D * 2);
+      unsigned long long* w = (unsigned long long*)ctx->dev(
+          kt::WS_KM_CERT, sizeof(unsigned long long) * words * 2 +
+                              sizeof(double) * (kt::kMaxK * kt::kMaxKnobs * 2 + kt::kMaxK));
       isum[0] = w;
       isum[1] = w + words;
       cB = reinterpret_cast<double*>(w + 2 * words);
-      dB = cB + kt::kMaxK * D;
+      dB = cB + kt::kMaxK * kt::kMaxKnobs;  // [k x D] deltas, then [kMaxK] per-cluster bounds
     }
     rb_host = (IterReadback*)ctx->host(3, sizeof(IterReadback) * 8);
     dscal = (double*)ctx->dev(kt::WS_SNAP, 64);
@@ -1640,7 +1650,7 @@ struct KMeans {
     double loss = assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);  // exact
     iter_losses.assign(1, loss);
     const size_t words = (size_t)kt::kMaxK * (kt::kMaxKnobs + 1);
-    const size_t tsmem = sizeof(double) * 2 * k * D + lut_smem;
+    const size_t tsmem = sizeof(double) * (k * D + kt::kMaxK) + lut_smem;
     KT_CUDA(cudaFuncSetAttribute(assign_cert_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
     int cur = 0;
     KT_CUDA(cudaMemsetAsync(isum[cur], 0, sizeof(unsigned long long) * words, s()));
