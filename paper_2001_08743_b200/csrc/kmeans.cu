@@ -26,6 +26,20 @@ namespace {
 
 constexpr int kChunk = 1024;  // points per block-sum chunk (kmeans++ / loss)
 constexpr int kBT = 256;      // threads per block for point kernels
+// Runs STMT with DM_ = the compile-time knob bound (8 / 16 / 32) covering D.
+#define KT_DISPATCH_DM(D, ...)             \
+  do {                                     \
+    if ((D) <= 8) {                        \
+      constexpr int DM_ = 8;               \
+      __VA_ARGS__;                         \
+    } else if ((D) <= 16) {                \
+      constexpr int DM_ = 16;              \
+      __VA_ARGS__;                         \
+    } else {                               \
+      constexpr int DM_ = kt::kMaxKnobs;   \
+      __VA_ARGS__;                         \
+    }                                      \
+  } while (0)
 constexpr double kU = 1.1102230246251565e-16;  // 2^-53
 
 template <class IdxT>
@@ -349,7 +363,7 @@ __global__ void __launch_bounds__(1024) kpp_select_kernel(const double* __restri
 // Exact argmin over centroids (strict <, lowest index wins ties,
 // sampling.cpp:39-54); writes d2 of the chosen centroid, the number of
 // changed assignments and per-chunk loss partial sums.
-template <class IdxT>
+template <class IdxT, int DM>
 __global__ void __launch_bounds__(kBT) assign_kernel(KtSpaceParams sp, int lut_total,
                                                      const IdxT* __restrict__ pts, int64_t N,
                                                      const double* __restrict__ cent, int k,
@@ -374,17 +388,21 @@ __global__ void __launch_bounds__(kBT) assign_kernel(KtSpaceParams sp, int lut_t
   for (int j = 0; j < kChunk / kBT; ++j) {
     const int64_t i = base + j * kBT + threadIdx.x;
     if (i < N) {
-      double x[kt::kMaxKnobs];
-      for (int d = 0; d < D; ++d) x[d] = feat(sp, lut, pts + i * D, d);
+      double x[DM];  // DM >= D, compile-time: the features stay in registers
+#pragma unroll
+      for (int d = 0; d < DM; ++d) x[d] = d < D ? feat(sp, lut, pts + i * D, d) : 0.0;
       double best = INFINITY;
       int bc = 0;
       for (int c = 0; c < k; ++c) {
         const double* cc = s_cent + c * D;
         double t = kt::dsub(x[0], cc[0]);
         double s = kt::dmul(t, t);
-        for (int d = 1; d < D; ++d) {
-          t = kt::dsub(x[d], cc[d]);
-          s = kt::dadd(s, kt::dmul(t, t));
+#pragma unroll
+        for (int d = 1; d < DM; ++d) {
+          if (d < D) {
+            t = kt::dsub(x[d], cc[d]);
+            s = kt::dadd(s, kt::dmul(t, t));
+          }
         }
         if (s < best) {
           best = s;
@@ -504,7 +522,7 @@ __global__ void centroids_from_sums_kernel(KtSpaceParams sp, int k, const unsign
 // strictly below every other cluster's. Fused: the integer sums are updated in
 // place by the points that changed cluster (block-aggregated deltas), plus the
 // changed / uncertain counts and the loss estimate.
-template <class IdxT>
+template <class IdxT, int DM>
 __global__ void __launch_bounds__(kBT) assign_cert_kernel(
     KtSpaceParams sp, int lut_total, const IdxT* __restrict__ pts, int64_t N, const double* __restrict__ cB,
     const double* __restrict__ dB, int k, const int32_t* __restrict__ prev, int32_t* __restrict__ asg,
@@ -535,16 +553,20 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
     const bool live = i < N;
     int bc = 0;
     if (live) {
-      double x[kt::kMaxKnobs];
-      for (int d = 0; d < D; ++d) x[d] = feat(sp, lut, pts + i * D, d);
+      double x[DM];  // DM >= D, compile-time: the features stay in registers
+#pragma unroll
+      for (int d = 0; d < DM; ++d) x[d] = d < D ? feat(sp, lut, pts + i * D, d) : 0.0;
       double best = INFINITY, best_e = 0.0, lo_others = INFINITY;
       for (int c = 0; c < k; ++c) {
         const double* cc = s_c + c * D;
         double t = kt::dsub(x[0], cc[0]);
         double s = kt::dmul(t, t);
-        for (int d = 1; d < D; ++d) {
-          t = kt::dsub(x[d], cc[d]);
-          s = kt::dadd(s, kt::dmul(t, t));
+#pragma unroll
+        for (int d = 1; d < DM; ++d) {
+          if (d < D) {
+            t = kt::dsub(x[d], cc[d]);
+            s = kt::dadd(s, kt::dmul(t, t));
+          }
         }
         // |d2_ref - s| <= E_c (centroid difference) + the rounding of both evaluations
         const double e = (s_e[c] + grow * (s + s_e[c])) * (1.0 + 0x1.0p-20) + 1e-300;
@@ -1506,16 +1528,16 @@ struct KMeans {
       }
     } else if (world == 1) {
       kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
-      assign_kernel<IdxT><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent, k, prev, asg,
-                                                          dd, chunk, ull, 0);
+      KT_DISPATCH_DM(D, assign_kernel<IdxT, DM_><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent,
+                                                                                 k, prev, asg, dd, chunk, ull, 0));
       kt::check_launch(ctx, "assign");
     } else {
       const int64_t c0 = (int64_t)rank * shard_chunks;
       const int64_t nloc = std::max<int64_t>(0, std::min<int64_t>(nchunks, c0 + shard_chunks) - c0);
       if (nloc > 0) {
         kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
-        assign_kernel<IdxT><<<(unsigned)nloc, kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent, k, prev,
-                                                                asg, dd, chunk, ull, c0);
+        KT_DISPATCH_DM(D, assign_kernel<IdxT, DM_><<<(unsigned)nloc, kBT, smem, s()>>>(
+                              sp->params, lut_total, pts, N, cent, k, prev, asg, dd, chunk, ull, c0));
         kt::check_launch(ctx, "assign");
       }
       if (nloc < shard_chunks)  // zero the padding chunks of the last shard
@@ -1651,7 +1673,8 @@ struct KMeans {
     iter_losses.assign(1, loss);
     const size_t words = (size_t)kt::kMaxK * (kt::kMaxKnobs + 1);
     const size_t tsmem = sizeof(double) * (k * D + kt::kMaxK) + lut_smem;
-    KT_CUDA(cudaFuncSetAttribute(assign_cert_kernel<IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
+    KT_DISPATCH_DM(D, KT_CUDA(cudaFuncSetAttribute(assign_cert_kernel<IdxT, DM_>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem)));
     int cur = 0;
     KT_CUDA(cudaMemsetAsync(isum[cur], 0, sizeof(unsigned long long) * words, s()));
     cluster_sums_kernel<IdxT><<<(unsigned)nchunks, kBT, 0, s()>>>(pts, N, D, k, asg_a, isum[cur],
@@ -1674,9 +1697,9 @@ struct KMeans {
       KT_CUDA(cudaMemsetAsync(ull, 0, 32, s()));
       centroids_from_sums_kernel<<<1, 1024, 0, s()>>>(sp->params, k, cs, cs + (size_t)kt::kMaxK * kt::kMaxKnobs, cB,
                                                       dB, ull + 3);
-      assign_cert_kernel<IdxT><<<(unsigned)nchunks, kBT, tsmem, s()>>>(
-          sp->params, lut_total, pts, N, cB, dB, k, asg_a, asg_b, d2_b, chunk, ull, cs,
-          cs + (size_t)kt::kMaxK * kt::kMaxKnobs);
+      KT_DISPATCH_DM(D, assign_cert_kernel<IdxT, DM_><<<(unsigned)nchunks, kBT, tsmem, s()>>>(
+                            sp->params, lut_total, pts, N, cB, dB, k, asg_a, asg_b, d2_b, chunk, ull, cs,
+                            cs + (size_t)kt::kMaxK * kt::kMaxKnobs));
       kt::check_launch(ctx, "assign_cert", 2);
       sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk, nchunks, dscal);
       gather_readback_kernel<<<1, 1, 0, s()>>>(dscal, ull, seqcnt, csb + k, rb_dev, rb_slot);
