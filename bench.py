@@ -33,16 +33,15 @@ FLOP_PER_CONFIG_STEP = lambda n, h=128, g=64: 2 * (h * n + 2 * h * g + 3 * n * g
 
 
 def load_peaks():
-    """Roofline denominators: the driver-written MEASURED_PEAKS.json; if absent, the
-    values it held when SURVEY.md §8d was written (same pool), else the profiling
-    guide's fallback."""
+    """Roofline denominators: the driver-written MEASURED_PEAKS.json, else the fallback the
+    profiling guide states (6.65 TB/s, 1.59 PFLOP/s burst, ~1.4 sustained)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
         return p, "measured"
     except Exception:
-        return {"hbm_gbs": 6547.2, "bf16_tflops": 1657.0, "bf16_tflops_sustained": 1383.3}, \
-            "measured (MEASURED_PEAKS.json as recorded in SURVEY.md §8d; file absent here)"
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
 
 
 SFU_OPS_PER_SM_CLK = 16  # MUFU lanes per SM per clock (ex2/rcp/lg2)
