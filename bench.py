@@ -470,9 +470,12 @@ def main():
         for h, s in zip(host_init, specs):
             h[:] = s.init_idx
         D = n_knobs
+        # logp / value as fp32: the tcgen05 path computes both in fp32, so shipping
+        # them as doubles would only add PCIe bytes
         host_out = [dict(idx=pinned((E, T + 1, D), torch.int16).view(np.uint16),
                          score=pinned((E, T + 1), torch.float64), actions=pinned((E, T, D), torch.int8),
-                         logp=pinned((E, T), torch.float64), value=pinned((E, T), torch.float64)) for _ in specs]
+                         logp=None, value=None, logp32=pinned((E, T), torch.float32),
+                         value32=pinned((E, T), torch.float32)) for _ in specs]
         htasks = [RolloutTask(d, a, g, hi, episode_offset=rank * E, root_seed=s.seed)
                   for s, d, a, g, hi in zip(specs, spaces, agents, gbts, host_init)]
         ctx.set_stream(None)
@@ -486,7 +489,7 @@ def main():
         if world > 1:
             dt = allreduce_max(dt)
         bi = sum(h.nbytes for h in host_init)
-        bo = sum(sum(v.nbytes for v in o.values()) for o in host_out)
+        bo = sum(sum(v.nbytes for v in o.values() if v is not None) for o in host_out)
         e2e = {"value": units_per_step * args.steps / dt, "unit": "config-steps/s", "h2d_bytes_per_step": bi,
                "d2h_bytes_per_step": bo}
         ctx.set_stream(stream.cuda_stream)

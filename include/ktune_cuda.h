@@ -225,6 +225,8 @@ typedef struct {
   int8_t* actions;          /* E x T x D directions in {-1,0,+1} */
   double* logp;             /* E x T joint log-probability */
   double* value;            /* E x T value estimate */
+  float* logp_f32;          /* E x T, fp32 copies (may be NULL): the tcgen05 path computes both in fp32, */
+  float* value_f32;         /* so these halve their device->host bytes without losing anything */
 } ktune_rollout_task;
 int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks, int32_t T,
                   int flags);

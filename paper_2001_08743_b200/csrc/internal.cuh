@@ -223,6 +223,8 @@ struct RolloutWork {
   double* value;
   const ktune_gbt* gbt;  // may be NULL
   double* score;         // E x (T+1), may be NULL
+  float* logp32 = nullptr;   // fp32 copies (may be NULL)
+  float* value32 = nullptr;
   bool scored = false;   // set by rollout_tc when the scores were fused into the rollout
 };
 // tcgen05 rollout (rollout_tc.cu): eligibility (h = 128, g = 64, n <= 21,

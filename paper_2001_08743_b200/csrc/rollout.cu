@@ -60,6 +60,8 @@ struct RolloutTask {
   int8_t* actions;
   double* logp;
   double* value;
+  float* logp32;
+  float* value32;
 };
 
 // Whole launch description passed BY VALUE (kernel parameter space), so a
@@ -318,6 +320,8 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
         for (int d = 0; d < n; ++d) lp = kt::dadd(lp, act[(3 * d) * tile + el]);
         if (out_logp) out_logp[e * T + t] = lp;
         if (out_val) out_val[e * T + t] = val[el];
+        if (tkp->logp32) tkp->logp32[e * T + t] = (float)lp;
+        if (tkp->value32) tkp->value32[e * T + t] = (float)val[el];
       }
     }
     __syncthreads();
@@ -485,6 +489,8 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       double* d_logp;
       double* d_val;
       double* d_score;
+      float* d_logp32;
+      float* d_val32;
     };
     std::vector<HostIo> io(num_tasks);
     bool smem_params = true;
@@ -494,7 +500,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       arena += (std::max<size_t>(bytes, 8) + 255) & ~(size_t)255;
       return o;
     };
-    std::vector<std::array<size_t, 6>> offs(num_tasks);
+    std::vector<std::array<size_t, 8>> offs(num_tasks);
     for (int k = 0; k < num_tasks; ++k) {
       const ktune_rollout_task& t = tasks[k];
       if (!t.space || !t.ac) kt::fail(KTUNE_ERR_CONFIG, "rollout: task needs a space and an agent");
@@ -506,7 +512,8 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
         offs[k] = {slice(E * n * 2), slice(E * (T + 1) * n * 2), t.actions ? slice(E * T * n) : SIZE_MAX,
                    t.logp ? slice(E * T * 8) : SIZE_MAX, t.value ? slice(E * T * 8) : SIZE_MAX,
-                   t.score ? slice(E * (T + 1) * 8) : SIZE_MAX};
+                   t.score ? slice(E * (T + 1) * 8) : SIZE_MAX, t.logp_f32 ? slice(E * T * 4) : SIZE_MAX,
+                   t.value_f32 ? slice(E * T * 4) : SIZE_MAX};
       }
     }
     unsigned char* base = dev ? nullptr : (unsigned char*)ctx->dev(kt::WS_ROLLOUT, std::max<size_t>(arena, 256));
@@ -517,10 +524,11 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       const int64_t E = t.num_episodes;
       HostIo& h = io[k];
       if (dev) {
-        h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score};
+        h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score, t.logp_f32, t.value_f32};
       } else {
         h = {(const uint16_t*)at(offs[k][0]), (uint16_t*)at(offs[k][1]), (int8_t*)at(offs[k][2]),
-             (double*)at(offs[k][3]),         (double*)at(offs[k][4]),   (double*)at(offs[k][5])};
+             (double*)at(offs[k][3]),         (double*)at(offs[k][4]),   (double*)at(offs[k][5]),
+             (float*)at(offs[k][6]),          (float*)at(offs[k][7])};
         if (E > 0)
           KT_CUDA(cudaMemcpyAsync((void*)h.d_init, t.init_idx, (size_t)E * n * 2, cudaMemcpyHostToDevice, ctx->stream));
       }
@@ -539,6 +547,8 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       r.actions = h.d_act;
       r.logp = h.d_logp;
       r.value = h.d_val;
+      r.logp32 = h.d_logp32;
+      r.value32 = h.d_val32;
     }
     // tcgen05 path with certified sampling unless the exact fp64 forward is
     // requested (or a task is outside the tensor-core path's shapes)
@@ -581,6 +591,12 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         KT_CUDA(cudaMemcpy2DAsync(t.logp + t0, T * 8, h.d_logp + t0, T * 8, steps * 8, E, cudaMemcpyDeviceToHost, st));
       if (t.value && steps)
         KT_CUDA(cudaMemcpy2DAsync(t.value + t0, T * 8, h.d_val + t0, T * 8, steps * 8, E, cudaMemcpyDeviceToHost, st));
+      if (t.logp_f32 && steps)
+        KT_CUDA(cudaMemcpy2DAsync(t.logp_f32 + t0, T * 4, h.d_logp32 + t0, T * 4, steps * 4, E,
+                                  cudaMemcpyDeviceToHost, st));
+      if (t.value_f32 && steps)
+        KT_CUDA(cudaMemcpy2DAsync(t.value_f32 + t0, T * 4, h.d_val32 + t0, T * 4, steps * 4, E,
+                                  cudaMemcpyDeviceToHost, st));
       if (t.score && t.gbt)
         KT_CUDA(cudaMemcpy2DAsync(t.score + r0, (T + 1) * 8, h.d_score + r0, (T + 1) * 8, rows * 8, E,
                                   cudaMemcpyDeviceToHost, st));
@@ -590,7 +606,8 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       std::vector<kt::RolloutWork> work(num_tasks);
       for (int k = 0; k < num_tasks; ++k)
         work[k] = {tasks[k].space, tasks[k].ac, dt[k].E,     dt[k].episode_offset, dt[k].seed, dt[k].init_idx,
-                   dt[k].idx,      dt[k].actions, dt[k].logp, dt[k].value,         tasks[k].gbt, io[k].d_score};
+                   dt[k].idx,      dt[k].actions, dt[k].logp, dt[k].value,         tasks[k].gbt, io[k].d_score,
+                   io[k].d_logp32, io[k].d_val32};
       if (segmented) {
         for (int sg = 0; sg < S; ++sg) {
           const int t0 = (int)((int64_t)sg * T / S), t1 = (int)((int64_t)(sg + 1) * T / S);

@@ -62,6 +62,8 @@ struct TcTask {
   int8_t* actions;
   double* logp;
   double* value;
+  float* logp32;
+  float* value32;
   int32_t cta_base, ctas, warps;  // CTAs [cta_base, cta_base + ctas) share warps = ceil(E/32)
   int32_t e1, e2, e3;             // power-of-two weight scales of L1, L2, L3
   // fused cost-model scoring (K1 in the epilogue; gnode == nullptr: scored by a separate K1 launch)
@@ -592,7 +594,11 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
           for (int j = 0; j < 16; ++j)
             vs = fmaf(swv2[c0 - 64 + j], act_scaled(fmaf(__uint_as_float(v[j]), sc2, sbv1[c0 - 64 + j]), 1.f), vs);
         }
-        if (lr && tk.value && L.check != 4) tk.value[e * T + t] = (double)(vs + sbv2[0]);
+        if (lr && L.check != 4) {
+          const float v = vs + sbv2[0];
+          if (tk.value) tk.value[e * T + t] = (double)v;
+          if (tk.value32) tk.value32[e * T + t] = v;
+        }
         TR(12)
         kt::tc::mbar_wait(mb, ph);
         kt::tc::fence_after();
@@ -697,6 +703,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
             }
           }
           if (tk.logp) tk.logp[e * T + t] = (double)lpj;
+          if (tk.logp32) tk.logp32[e * T + t] = lpj;
         }
       }
       ph ^= 1;
@@ -809,6 +816,8 @@ void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_beg
       tk.actions = rw.actions;
       tk.logp = rw.logp;
       tk.value = rw.value;
+      tk.logp32 = rw.logp32;
+      tk.value32 = rw.value32;
       tk.warps = (int32_t)W[k];
       tk.ctas = (int32_t)ceil_div(W[k], m);
       tk.cta_base = ctas;

@@ -246,3 +246,20 @@ def test_rollout_tc_edge_shapes(O, ctx, cards, E, T):
     if T:
         assert np.array_equal(out["actions"], want["actions"])
         assert _close(out["logp"], want["logp"]) and _close(out["value"], want["value"])
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_rollout_fp32_outputs(O, ctx, exact):
+    """logp_f32 / value_f32 are the fp32 roundings of the fp64 outputs (host path, segmented)."""
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    sp, osp, og, dspace, dg, agent = _setup(O, ctx, "resnet_c2", seed=91)
+    E, T = 50, 140
+    init = osp.random_valid(91, E) if O.ref_available() else np.zeros((E, sp.num_knobs), np.int32)
+    mk = lambda: dict(idx=np.zeros((E, T + 1, sp.num_knobs), np.uint16), score=np.zeros((E, T + 1)),
+                      actions=np.zeros((E, T, sp.num_knobs), np.int8), logp=np.zeros((E, T)),
+                      value=np.zeros((E, T)), logp32=np.zeros((E, T), np.float32),
+                      value32=np.zeros((E, T), np.float32))
+    o = mk()
+    run_episodes_batch([RolloutTask(dspace, agent, dg, init, 0, 3)], T, host_out=[o], exact=exact)
+    assert np.array_equal(o["logp32"], o["logp"].astype(np.float32))
+    assert np.array_equal(o["value32"], o["value"].astype(np.float32))
