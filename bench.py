@@ -472,10 +472,13 @@ def main():
         D = n_knobs
         # logp / value as fp32: the tcgen05 path computes both in fp32, so shipping
         # them as doubles would only add PCIe bytes
-        host_out = [dict(idx=pinned((E, T + 1, D), torch.int16).view(np.uint16),
+        # and the visited configurations as uint8 wherever every cardinality fits (the API's idx_u8)
+        small = [max(s.space.cards) <= 256 for s in specs]
+        host_out = [dict(idx=None if sm else pinned((E, T + 1, D), torch.int16).view(np.uint16),
+                         idx8=pinned((E, T + 1, D), torch.uint8) if sm else None,
                          score=pinned((E, T + 1), torch.float64), actions=pinned((E, T, D), torch.int8),
                          logp=None, value=None, logp32=pinned((E, T), torch.float32),
-                         value32=pinned((E, T), torch.float32)) for _ in specs]
+                         value32=pinned((E, T), torch.float32)) for sm in small]
         htasks = [RolloutTask(d, a, g, hi, episode_offset=rank * E, root_seed=s.seed)
                   for s, d, a, g, hi in zip(specs, spaces, agents, gbts, host_init)]
         ctx.set_stream(None)

@@ -219,14 +219,17 @@ typedef struct {
   int64_t episode_offset;   /* global id of this shard's first episode (RNG key) */
   uint64_t explore_seed;    /* stream_seed(root, "explore") */
   const uint16_t* init_idx; /* E x D */
-  /* outputs (any may be NULL except idx): */
-  uint16_t* idx;            /* E x (T+1) x D visited configs, row t = Θ_t */
+  /* outputs (any may be NULL except idx, see idx_u8): */
+  uint16_t* idx;            /* E x (T+1) x D visited configs, row t = Θ_t (NULL allowed with idx_u8, host pointers) */
   double* score;            /* E x (T+1) predicted fitness of Θ_t */
   int8_t* actions;          /* E x T x D directions in {-1,0,+1} */
   double* logp;             /* E x T joint log-probability */
   double* value;            /* E x T value estimate */
   float* logp_f32;          /* E x T, fp32 copies (may be NULL): the tcgen05 path computes both in fp32, */
   float* value_f32;         /* so these halve their device->host bytes without losing anything */
+  uint8_t* idx_u8;          /* E x (T+1) x D visited configs as uint8 (may be NULL; every cardinality
+                               <= 256). Host-pointer calls may then pass idx = NULL: only these bytes
+                               cross PCIe */
 } ktune_rollout_task;
 int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks, int32_t T,
                   int flags);

@@ -373,6 +373,16 @@ __global__ void debug_math_kernel(int op, const double* __restrict__ x, int64_t 
     out[i] = op == 0 ? kt::kt_exp(x[i]) : (op == 1 ? kt::kt_log(x[i]) : kt::kt_tanh(x[i]));
 }
 
+// uint16 -> uint8 copy of trajectory rows [r0, r0 + rows) of every episode (idx_u8 outputs).
+__global__ void narrow_idx_kernel(const uint16_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t E,
+                                  int rows_per_ep, int n, int r0, int rows) {
+  const int64_t per = (int64_t)rows * n, total = E * per;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / per, j = (e * rows_per_ep + r0) * n + (i % per);
+    dst[j] = (uint8_t)src[j];
+  }
+}
+
 bool fits_smem(int n, int h, int g, int cpl = 1) { return rollout_smem_bytes(n, h, g, true, cpl) <= 227 * 1024; }
 
 
@@ -491,6 +501,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       double* d_score;
       float* d_logp32;
       float* d_val32;
+      uint8_t* d_u8;
     };
     std::vector<HostIo> io(num_tasks);
     bool smem_params = true;
@@ -500,20 +511,24 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       arena += (std::max<size_t>(bytes, 8) + 255) & ~(size_t)255;
       return o;
     };
-    std::vector<std::array<size_t, 8>> offs(num_tasks);
+    std::vector<std::array<size_t, 9>> offs(num_tasks);
     for (int k = 0; k < num_tasks; ++k) {
       const ktune_rollout_task& t = tasks[k];
       if (!t.space || !t.ac) kt::fail(KTUNE_ERR_CONFIG, "rollout: task needs a space and an agent");
       if (t.ac->n != t.space->D) kt::fail(KTUNE_ERR_CONFIG, "rollout: agent/space knob count mismatch");
       if (t.gbt && t.gbt->num_features != t.space->D) kt::fail(KTUNE_ERR_CONFIG, "rollout: cost model/space mismatch");
-      if (t.num_episodes < 0 || !t.idx) kt::fail(KTUNE_ERR_CONFIG, "rollout: bad episode count or missing idx output");
+      if (t.num_episodes < 0 || (!t.idx && (dev || !t.idx_u8)))
+        kt::fail(KTUNE_ERR_CONFIG, "rollout: bad episode count or missing idx output");
+      if (t.idx_u8)
+        for (int c : t.space->card)
+          if (c > 256) kt::fail(KTUNE_ERR_CONFIG, "rollout: idx_u8 needs every knob cardinality <= 256");
       smem_params = smem_params && fits_smem(t.ac->n, t.ac->h, t.ac->g);
       if (!dev) {
         const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
         offs[k] = {slice(E * n * 2), slice(E * (T + 1) * n * 2), t.actions ? slice(E * T * n) : SIZE_MAX,
                    t.logp ? slice(E * T * 8) : SIZE_MAX, t.value ? slice(E * T * 8) : SIZE_MAX,
                    t.score ? slice(E * (T + 1) * 8) : SIZE_MAX, t.logp_f32 ? slice(E * T * 4) : SIZE_MAX,
-                   t.value_f32 ? slice(E * T * 4) : SIZE_MAX};
+                   t.value_f32 ? slice(E * T * 4) : SIZE_MAX, t.idx_u8 ? slice(E * (T + 1) * n) : SIZE_MAX};
       }
     }
     unsigned char* base = dev ? nullptr : (unsigned char*)ctx->dev(kt::WS_ROLLOUT, std::max<size_t>(arena, 256));
@@ -524,11 +539,11 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       const int64_t E = t.num_episodes;
       HostIo& h = io[k];
       if (dev) {
-        h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score, t.logp_f32, t.value_f32};
+        h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score, t.logp_f32, t.value_f32, t.idx_u8};
       } else {
         h = {(const uint16_t*)at(offs[k][0]), (uint16_t*)at(offs[k][1]), (int8_t*)at(offs[k][2]),
              (double*)at(offs[k][3]),         (double*)at(offs[k][4]),   (double*)at(offs[k][5]),
-             (float*)at(offs[k][6]),          (float*)at(offs[k][7])};
+             (float*)at(offs[k][6]),          (float*)at(offs[k][7]),    (uint8_t*)at(offs[k][8])};
         if (E > 0)
           KT_CUDA(cudaMemcpyAsync((void*)h.d_init, t.init_idx, (size_t)E * n * 2, cudaMemcpyHostToDevice, ctx->stream));
       }
@@ -575,6 +590,15 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       if (len != T + 1) m = kt::RowMap{len, (int64_t)T + 1, r0};
       kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx, 2, t.num_episodes * len, io[k].d_score, m);
     };
+    auto narrow_rows = [&](int k, int r0, int r1) {  // uint16 -> uint8 trajectory rows [r0, r1]
+      const ktune_rollout_task& t = tasks[k];
+      if (!t.idx_u8 || t.num_episodes == 0) return;
+      narrow_idx_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(t.num_episodes * (int64_t)(r1 - r0 + 1) * t.ac->n, 256),
+                                                     (int64_t)kt::sm_count(ctx) * 16),
+                          256, 0, ctx->stream>>>(io[k].d_idx, io[k].d_u8, t.num_episodes, T + 1, t.ac->n, r0,
+                                                 r1 - r0 + 1);
+      kt::check_launch(ctx, "narrow_idx");
+    };
     auto copy_out = [&](int k, int t0, int t1, cudaStream_t st) {  // steps [t0, t1): rows (t0, t1] (+ row 0)
       const ktune_rollout_task& t = tasks[k];
       const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
@@ -582,8 +606,12 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       const HostIo& h = io[k];
       const int r0 = t0 == 0 ? 0 : t0 + 1;
       const size_t rows = (size_t)(t1 - r0 + 1), steps = (size_t)(t1 - t0);
-      KT_CUDA(cudaMemcpy2DAsync(t.idx + r0 * n, (T + 1) * n * 2, h.d_idx + r0 * n, (T + 1) * n * 2, rows * n * 2, E,
-                                cudaMemcpyDeviceToHost, st));
+      if (t.idx)
+        KT_CUDA(cudaMemcpy2DAsync(t.idx + r0 * n, (T + 1) * n * 2, h.d_idx + r0 * n, (T + 1) * n * 2, rows * n * 2,
+                                  E, cudaMemcpyDeviceToHost, st));
+      if (t.idx_u8)
+        KT_CUDA(cudaMemcpy2DAsync(t.idx_u8 + r0 * n, (T + 1) * n, h.d_u8 + r0 * n, (T + 1) * n, rows * n, E,
+                                  cudaMemcpyDeviceToHost, st));
       if (t.actions && steps)
         KT_CUDA(cudaMemcpy2DAsync(t.actions + t0 * n, T * n, h.d_act + t0 * n, T * n, steps * n, E,
                                   cudaMemcpyDeviceToHost, st));
@@ -615,7 +643,10 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
             kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
             kt::rollout_tc(ctx, work, T, t0, t1);
           }
-          for (int k = 0; k < num_tasks; ++k) score_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
+          for (int k = 0; k < num_tasks; ++k) {
+            score_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
+            narrow_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
+          }
           cudaEvent_t ev;
           KT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
           events.push_back(ev);
@@ -661,8 +692,10 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       kt::check_launch(ctx, "rollout");
     }
     // cost-model scores of every visited configuration (K1 over the trajectory)
-    for (int k = 0; k < num_tasks; ++k)
+    for (int k = 0; k < num_tasks; ++k) {
       if (!scored[k]) score_rows(k, 0, T);
+      narrow_rows(k, 0, T);
+    }
     if (!dev) {
       for (int k = 0; k < num_tasks; ++k) copy_out(k, 0, T, ctx->stream);
       KT_CUDA(cudaStreamSynchronize(ctx->stream));

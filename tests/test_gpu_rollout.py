@@ -260,6 +260,13 @@ def test_rollout_fp32_outputs(O, ctx, exact):
                       value=np.zeros((E, T)), logp32=np.zeros((E, T), np.float32),
                       value32=np.zeros((E, T), np.float32))
     o = mk()
+    o["idx8"] = np.zeros((E, T + 1, sp.num_knobs), np.uint8)
     run_episodes_batch([RolloutTask(dspace, agent, dg, init, 0, 3)], T, host_out=[o], exact=exact)
     assert np.array_equal(o["logp32"], o["logp"].astype(np.float32))
     assert np.array_equal(o["value32"], o["value"].astype(np.float32))
+    assert np.array_equal(o["idx8"], o["idx"].astype(np.uint8)) and o["idx"].max() < 256
+    o2 = mk()
+    o2["idx"] = None
+    o2["idx8"] = np.zeros((E, T + 1, sp.num_knobs), np.uint8)
+    run_episodes_batch([RolloutTask(dspace, agent, dg, init, 0, 3)], T, host_out=[o2], exact=exact)
+    assert np.array_equal(o2["idx8"], o["idx8"]) and np.array_equal(o2["score"], o["score"])
