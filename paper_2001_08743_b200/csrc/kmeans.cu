@@ -1250,16 +1250,17 @@ __global__ void __launch_bounds__(kBT) snap_fallback_kernel(KtSpaceParams sp, in
   extern __shared__ double sdyn[];
   const int c = blockIdx.y;
   const int D = sp.D;
-  unsigned long long* outp = part + ((int64_t)c * gridDim.x + blockIdx.x) * 3;
+  unsigned long long* outp = part + ((int64_t)c * gridDim.x + blockIdx.x) * 4;
   if (!need[c]) {
-    if (threadIdx.x == 0) outp[0] = outp[1] = outp[2] = ~0ull;
+    if (threadIdx.x == 0) outp[0] = outp[1] = outp[2] = outp[3] = ~0ull;
     return;
   }
   const double* lut = stage_lut(sp, sdyn, lut_total);
   __shared__ double cc[kt::kMaxKnobs];
   if (threadIdx.x < D) cc[threadIdx.x] = cent[c * D + threadIdx.x];
   __syncthreads();
-  unsigned long long b0 = ~0ull, b1 = ~0ull, b2 = ~0ull;  // (invalid, d2 bits, id)
+  // key (invalid, d2 bits, id) and the row it came from (ids are unique: the key decides)
+  unsigned long long b0 = ~0ull, b1 = ~0ull, b2 = ~0ull, b3 = ~0ull;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
        i += (int64_t)gridDim.x * blockDim.x) {
     const IdxT* row = cand + i * D;
@@ -1274,12 +1275,14 @@ __global__ void __launch_bounds__(kBT) snap_fallback_kernel(KtSpaceParams sp, in
       b0 = k0;
       b1 = k1;
       b2 = k2;
+      b3 = (unsigned long long)i;
     }
   }
-  __shared__ unsigned long long s0[kBT], s1[kBT], s2[kBT];
+  __shared__ unsigned long long s0[kBT], s1[kBT], s2[kBT], s3[kBT];
   s0[threadIdx.x] = b0;
   s1[threadIdx.x] = b1;
   s2[threadIdx.x] = b2;
+  s3[threadIdx.x] = b3;
   __syncthreads();
   for (int o = kBT / 2; o > 0; o >>= 1) {
     if (threadIdx.x < o) {
@@ -1289,6 +1292,7 @@ __global__ void __launch_bounds__(kBT) snap_fallback_kernel(KtSpaceParams sp, in
         s0[threadIdx.x] = s0[q];
         s1[threadIdx.x] = s1[q];
         s2[threadIdx.x] = s2[q];
+        s3[threadIdx.x] = s3[q];
       }
     }
     __syncthreads();
@@ -1297,6 +1301,7 @@ __global__ void __launch_bounds__(kBT) snap_fallback_kernel(KtSpaceParams sp, in
     outp[0] = s0[0];
     outp[1] = s1[0];
     outp[2] = s2[0];
+    outp[3] = s3[0];
   }
 }
 
@@ -1307,23 +1312,19 @@ __global__ void snap_reduce_kernel(KtSpaceParams sp, const int32_t* __restrict__
                                    int64_t N, int32_t* __restrict__ out) {
   const int c = blockIdx.x;
   if (!need[c] || threadIdx.x != 0) return;
-  const unsigned long long* p = part + (int64_t)c * nblk * 3;
-  unsigned long long b0 = ~0ull, b1 = ~0ull, b2 = ~0ull;
+  const unsigned long long* p = part + (int64_t)c * nblk * 4;
+  unsigned long long b0 = ~0ull, b1 = ~0ull, b2 = ~0ull, b3 = ~0ull;
   for (int q = 0; q < nblk; ++q) {
-    const unsigned long long k0 = p[3 * q], k1 = p[3 * q + 1], k2 = p[3 * q + 2];
+    const unsigned long long k0 = p[4 * q], k1 = p[4 * q + 1], k2 = p[4 * q + 2];
     if (k0 < b0 || (k0 == b0 && (k1 < b1 || (k1 == b1 && k2 < b2)))) {
       b0 = k0;
       b1 = k1;
       b2 = k2;
+      b3 = p[4 * q + 3];
     }
   }
   if (b0 == ~0ull) return;  // no candidates: keep the rounding (sampling.cpp:233)
-  // ids are unique (CandidateSet is deduplicated): find the row with id b2
-  for (int64_t i = 0; i < N; ++i)
-    if (ids[i] == b2) {
-      for (int d = 0; d < sp.D; ++d) out[c * sp.D + d] = (int32_t)cand[i * sp.D + d];
-      return;
-    }
+  for (int d = 0; d < sp.D; ++d) out[c * sp.D + d] = (int32_t)cand[(int64_t)b3 * sp.D + d];
 }
 
 // ------------------------------------------------------------------ host orchestration
@@ -1806,7 +1807,7 @@ void snap_device(ktune_ctx* ctx, const ktune_space* sp, const double* d_cent, in
   kt::check_launch(ctx, "snap_round");
   if (N <= 0) return;
   const int nblk = (int)std::min<int64_t>(kt::ceil_div(N, kBT), 256);
-  unsigned long long* part = (unsigned long long*)ctx->dev(kt::WS_OUT3, sizeof(unsigned long long) * 3 * nblk * k);
+  unsigned long long* part = (unsigned long long*)ctx->dev(kt::WS_OUT3, sizeof(unsigned long long) * 4 * nblk * k);
   dim3 grid(nblk, k);
   snap_fallback_kernel<IdxT><<<grid, kBT, sizeof(double) * sp->lut_total, ctx->stream>>>(
       sp->params, sp->lut_total, d_cent, need, d_cand, d_ids, N, part);
