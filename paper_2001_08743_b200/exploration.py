@@ -180,13 +180,12 @@ def run_episodes(space: Space, cost_model: Optional[DeviceGbt], agent: ActorCrit
     fitness; trajectory holds actions, log-probabilities, values and the
     per-step rewards r_t = pred(Θ_{t+1}) - pred(Θ_t).
     """
-    from .sampling import make_candidate_set
+    from .sampling import candidates_from_rows
     o = run_episodes_batch([RolloutTask(space, agent, cost_model, init_idx, episode_offset, root_seed)], T,
                            exact=exact)[0]
-    E = o["idx"].shape[0]
-    flat = o["idx"].reshape(-1, space.D).astype(np.int32)
+    flat = o["idx"].reshape(-1, space.D)
     score = o["score"].reshape(-1) if o["score"] is not None else np.zeros(len(flat))
-    cands = make_candidate_set(space, flat, score)
+    cands = candidates_from_rows(space, flat, score)  # make_candidate_set on the device
     traj = dict(o)
     if o["score"] is not None:
         traj["reward"] = o["score"][:, 1:] - o["score"][:, :-1]
@@ -212,7 +211,7 @@ def sa_search(space: Space, cost_model: DeviceGbt, seeds, params: SaParams = SaP
     num_chains are given. Returns (CandidateSet over every chain state ranked by
     predicted fitness and deduplicated, trajectory dict(idx, score, accepted)).
     """
-    from .sampling import make_candidate_set
+    from .sampling import candidates_from_rows
     ctx = ctx or space.ctx
     D = space.D
     seeds = np.asarray(seeds, np.int64).reshape(-1, D) if len(seeds) else np.zeros((0, D), np.int64)
@@ -234,5 +233,5 @@ def sa_search(space: Space, cost_model: DeviceGbt, seeds, params: SaParams = SaP
                   acc.ctypes.data_as(C.c_void_p))
     p = L.SaParamsC(params.initial_temperature, params.cooling_rate)
     ctx.check(L.lib().ktune_sa_search(ctx.h, 1, C.byref(t), T, C.byref(p), 0))
-    cands = make_candidate_set(space, idx.reshape(-1, D).astype(np.int32), score.reshape(-1))
+    cands = candidates_from_rows(space, idx.reshape(-1, D), score.reshape(-1))  # on the device
     return cands, dict(idx=idx, score=score, accepted=acc)
