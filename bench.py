@@ -345,6 +345,7 @@ def main():
     ap.add_argument("--exact", action="store_true", help="exact fp64 rollout kernel instead of the tcgen05 path")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size tcgen05 vs exact comparison")
     ap.add_argument("--no-sa", action="store_true", help="skip the simulated-annealing baseline measurement")
+    ap.add_argument("--no-cand", action="store_true", help="skip the device make_candidate_set measurement")
     ap.add_argument("--kmeans-dist", action="store_true", help="N > 1: also run the NCCL-sharded k-means secondary")
     ap.add_argument("--c5", type=int, default=1, help="run the SURVEY C5 scale workload (1M x 1000, 1 step)")
     ap.add_argument("--c5-episodes", type=int, default=1 << 20)
@@ -512,6 +513,29 @@ def main():
                   "score_equal": eq("score"), "logp_max_rel": rel("logp"), "value_max_rel": rel("value")}
         del exact_out
 
+    # ---- f1: make_candidate_set on the device over the whole trajectory of every task
+    cand = None
+    if not args.no_cand:
+        try:
+            from paper_2001_08743_b200.sampling import candidates_from_rows
+            for o, d_ in zip(dev_out, spaces):
+                candidates_from_rows(d_, o["idx"], o["score"])  # warm-up
+            torch.cuda.synchronize()
+            ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ca.record(stream)
+            kept = 0
+            for o, d_ in zip(dev_out, spaces):
+                rows_, ids_ = candidates_from_rows(d_, o["idx"], o["score"])
+                kept += int(rows_.numel())
+            cb.record(stream)
+            torch.cuda.synchronize()
+            cms = ca.elapsed_time(cb)
+            nrows = len(specs) * E * (T + 1)
+            cand = {"metric": "make_candidate_set rows/s (device: id_of + dedup + rank, sampling.cpp:16-31)",
+                    "value": nrows / (cms * 1e-3), "unit": "rows/s", "rows": nrows, "kept": kept, "ms": cms}
+        except Exception as ex:  # reported, not hidden
+            cand = {"error": repr(ex)}
+
     # ---- the AutoTVM SA baseline (K7) on the same 12 tasks x 4096 chains x T steps (host buffers)
     sa = None
     if not args.no_sa and world == 1:
@@ -601,6 +625,7 @@ def main():
             "secondary": kmeans,
             "scale_c5": scale,
             "sa_baseline": sa,
+            "candidates": cand,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
