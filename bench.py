@@ -477,7 +477,8 @@ def main():
         small = [max(s.space.cards) <= 256 for s in specs]
         host_out = [dict(idx=None if sm else pinned((E, T + 1, D), torch.int16).view(np.uint16),
                          idx8=pinned((E, T + 1, D), torch.uint8) if sm else None,
-                         score=pinned((E, T + 1), torch.float64), actions=pinned((E, T, D), torch.int8),
+                         score=pinned((E, T + 1), torch.float64), actions=None,
+                         actions2=pinned((E, T, (D + 3) // 4), torch.uint8),  # 2 bits per direction
                          logp=None, value=None, logp32=pinned((E, T), torch.float32),
                          value32=pinned((E, T), torch.float32)) for sm in small]
         htasks = [RolloutTask(d, a, g, hi, episode_offset=rank * E, root_seed=s.seed)

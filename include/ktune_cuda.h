@@ -230,6 +230,9 @@ typedef struct {
   uint8_t* idx_u8;          /* E x (T+1) x D visited configs as uint8 (may be NULL; every cardinality
                                <= 256). Host-pointer calls may then pass idx = NULL: only these bytes
                                cross PCIe */
+  uint8_t* actions_u2;      /* E x T x ceil(D/4) bytes, 2 bits per knob: byte j holds knobs 4j..4j+3 as
+                               (direction + 1) << 2*(d - 4j) (may be NULL; host-pointer calls may then
+                               pass actions = NULL) */
 } ktune_rollout_task;
 int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks, int32_t T,
                   int flags);

@@ -383,6 +383,25 @@ __global__ void narrow_idx_kernel(const uint16_t* __restrict__ src, uint8_t* __r
   }
 }
 
+// int8 directions -> 2-bit codes (direction + 1), 4 knobs per byte, for steps [t0, t0 + steps).
+__global__ void pack_actions_kernel(const int8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t E, int T,
+                                    int n, int t0, int steps) {
+  const int nb = (n + 3) / 4;
+  const int64_t per = (int64_t)steps * nb, total = E * per;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / per, rem = i % per;
+    const int64_t step = t0 + rem / nb;
+    const int b = (int)(rem % nb);
+    const int8_t* a = src + (e * T + step) * n;
+    uint32_t v = 0;
+    for (int j = 0; j < 4; ++j) {
+      const int d = 4 * b + j;
+      if (d < n) v |= (uint32_t)(a[d] + 1) << (2 * j);
+    }
+    dst[(e * T + step) * nb + b] = (uint8_t)v;
+  }
+}
+
 bool fits_smem(int n, int h, int g, int cpl = 1) { return rollout_smem_bytes(n, h, g, true, cpl) <= 227 * 1024; }
 
 
@@ -502,6 +521,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       float* d_logp32;
       float* d_val32;
       uint8_t* d_u8;
+      uint8_t* d_a2;
     };
     std::vector<HostIo> io(num_tasks);
     bool smem_params = true;
@@ -511,7 +531,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       arena += (std::max<size_t>(bytes, 8) + 255) & ~(size_t)255;
       return o;
     };
-    std::vector<std::array<size_t, 9>> offs(num_tasks);
+    std::vector<std::array<size_t, 10>> offs(num_tasks);
     for (int k = 0; k < num_tasks; ++k) {
       const ktune_rollout_task& t = tasks[k];
       if (!t.space || !t.ac) kt::fail(KTUNE_ERR_CONFIG, "rollout: task needs a space and an agent");
@@ -519,16 +539,19 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       if (t.gbt && t.gbt->num_features != t.space->D) kt::fail(KTUNE_ERR_CONFIG, "rollout: cost model/space mismatch");
       if (t.num_episodes < 0 || (!t.idx && (dev || !t.idx_u8)))
         kt::fail(KTUNE_ERR_CONFIG, "rollout: bad episode count or missing idx output");
+      if (t.actions_u2 && dev && !t.actions)
+        kt::fail(KTUNE_ERR_CONFIG, "rollout: device-pointer calls need actions alongside actions_u2");
       if (t.idx_u8)
         for (int c : t.space->card)
           if (c > 256) kt::fail(KTUNE_ERR_CONFIG, "rollout: idx_u8 needs every knob cardinality <= 256");
       smem_params = smem_params && fits_smem(t.ac->n, t.ac->h, t.ac->g);
       if (!dev) {
         const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
-        offs[k] = {slice(E * n * 2), slice(E * (T + 1) * n * 2), t.actions ? slice(E * T * n) : SIZE_MAX,
+        offs[k] = {slice(E * n * 2), slice(E * (T + 1) * n * 2), (t.actions || t.actions_u2) ? slice(E * T * n) : SIZE_MAX,
                    t.logp ? slice(E * T * 8) : SIZE_MAX, t.value ? slice(E * T * 8) : SIZE_MAX,
                    t.score ? slice(E * (T + 1) * 8) : SIZE_MAX, t.logp_f32 ? slice(E * T * 4) : SIZE_MAX,
-                   t.value_f32 ? slice(E * T * 4) : SIZE_MAX, t.idx_u8 ? slice(E * (T + 1) * n) : SIZE_MAX};
+                   t.value_f32 ? slice(E * T * 4) : SIZE_MAX, t.idx_u8 ? slice(E * (T + 1) * n) : SIZE_MAX,
+                   t.actions_u2 ? slice(E * T * ((n + 3) / 4)) : SIZE_MAX};
       }
     }
     unsigned char* base = dev ? nullptr : (unsigned char*)ctx->dev(kt::WS_ROLLOUT, std::max<size_t>(arena, 256));
@@ -539,11 +562,12 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       const int64_t E = t.num_episodes;
       HostIo& h = io[k];
       if (dev) {
-        h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score, t.logp_f32, t.value_f32, t.idx_u8};
+        h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score, t.logp_f32, t.value_f32, t.idx_u8, t.actions_u2};
       } else {
         h = {(const uint16_t*)at(offs[k][0]), (uint16_t*)at(offs[k][1]), (int8_t*)at(offs[k][2]),
              (double*)at(offs[k][3]),         (double*)at(offs[k][4]),   (double*)at(offs[k][5]),
-             (float*)at(offs[k][6]),          (float*)at(offs[k][7]),    (uint8_t*)at(offs[k][8])};
+             (float*)at(offs[k][6]),          (float*)at(offs[k][7]),    (uint8_t*)at(offs[k][8]),
+             (uint8_t*)at(offs[k][9])};
         if (E > 0)
           KT_CUDA(cudaMemcpyAsync((void*)h.d_init, t.init_idx, (size_t)E * n * 2, cudaMemcpyHostToDevice, ctx->stream));
       }
@@ -599,6 +623,14 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
                                                  r1 - r0 + 1);
       kt::check_launch(ctx, "narrow_idx");
     };
+    auto pack_steps = [&](int k, int t0, int t1) {  // int8 -> 2-bit actions of steps [t0, t1)
+      const ktune_rollout_task& t = tasks[k];
+      if (!t.actions_u2 || t.num_episodes == 0 || t1 <= t0) return;
+      const int64_t work = t.num_episodes * (int64_t)(t1 - t0) * ((t.ac->n + 3) / 4);
+      pack_actions_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(work, 256), (int64_t)kt::sm_count(ctx) * 16), 256,
+                            0, ctx->stream>>>(io[k].d_act, io[k].d_a2, t.num_episodes, T, t.ac->n, t0, t1 - t0);
+      kt::check_launch(ctx, "pack_actions");
+    };
     auto copy_out = [&](int k, int t0, int t1, cudaStream_t st) {  // steps [t0, t1): rows (t0, t1] (+ row 0)
       const ktune_rollout_task& t = tasks[k];
       const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
@@ -615,6 +647,11 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       if (t.actions && steps)
         KT_CUDA(cudaMemcpy2DAsync(t.actions + t0 * n, T * n, h.d_act + t0 * n, T * n, steps * n, E,
                                   cudaMemcpyDeviceToHost, st));
+      if (t.actions_u2 && steps) {
+        const size_t nb = (n + 3) / 4;
+        KT_CUDA(cudaMemcpy2DAsync(t.actions_u2 + t0 * nb, T * nb, h.d_a2 + t0 * nb, T * nb, steps * nb, E,
+                                  cudaMemcpyDeviceToHost, st));
+      }
       if (t.logp && steps)
         KT_CUDA(cudaMemcpy2DAsync(t.logp + t0, T * 8, h.d_logp + t0, T * 8, steps * 8, E, cudaMemcpyDeviceToHost, st));
       if (t.value && steps)
@@ -646,6 +683,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
           for (int k = 0; k < num_tasks; ++k) {
             score_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
             narrow_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
+            pack_steps(k, t0, t1);
           }
           cudaEvent_t ev;
           KT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -695,6 +733,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     for (int k = 0; k < num_tasks; ++k) {
       if (!scored[k]) score_rows(k, 0, T);
       narrow_rows(k, 0, T);
+      pack_steps(k, 0, T);
     }
     if (!dev) {
       for (int k = 0; k < num_tasks; ++k) copy_out(k, 0, T, ctx->stream);

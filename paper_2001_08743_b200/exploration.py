@@ -165,10 +165,18 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
         a.logp_f32 = pp(o.get("logp32"))
         a.value_f32 = pp(o.get("value32"))
         a.idx_u8 = pp(o.get("idx8"))
+        a.actions_u2 = pp(o.get("actions2"))
         outs.append(o)
     ctx.check(L.lib().ktune_rollout(ctx.h, len(tasks), arr, T,
                                     (L.F_DEVICE if dev else 0) | (L.F_EXACT_ROLLOUT if exact else 0)))
     return outs
+
+
+def unpack_actions(packed, D: int) -> np.ndarray:
+    """Directions from the 2-bit `actions_u2` output: ... x ceil(D/4) bytes -> ... x D int8."""
+    p = np.asarray(packed, np.uint8)
+    codes = (p[..., :, None] >> (2 * np.arange(4, dtype=np.uint8))) & 3
+    return (codes.reshape(*p.shape[:-1], -1)[..., :D].astype(np.int8) - 1)
 
 
 def run_episodes(space: Space, cost_model: Optional[DeviceGbt], agent: ActorCritic, init_idx, T: int,

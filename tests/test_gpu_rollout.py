@@ -268,5 +268,9 @@ def test_rollout_fp32_outputs(O, ctx, exact):
     o2 = mk()
     o2["idx"] = None
     o2["idx8"] = np.zeros((E, T + 1, sp.num_knobs), np.uint8)
+    o2["actions"] = None
+    o2["actions2"] = np.zeros((E, T, (sp.num_knobs + 3) // 4), np.uint8)
     run_episodes_batch([RolloutTask(dspace, agent, dg, init, 0, 3)], T, host_out=[o2], exact=exact)
     assert np.array_equal(o2["idx8"], o["idx8"]) and np.array_equal(o2["score"], o["score"])
+    from paper_2001_08743_b200.exploration import unpack_actions
+    assert np.array_equal(unpack_actions(o2["actions2"], sp.num_knobs), o["actions"])
