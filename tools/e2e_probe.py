@@ -20,17 +20,19 @@ E, T, D = 4096, 500, 8
 pinned = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()
 host_init = [pinned(s.init_idx.shape, torch.int16).view(np.uint16) for s in specs]
 for h, s in zip(host_init, specs): h[:] = s.init_idx
-host_out = [dict(idx=pinned((E, T + 1, D), torch.int16).view(np.uint16), score=pinned((E, T + 1), torch.float64),
-                 actions=pinned((E, T, D), torch.int8), logp=pinned((E, T), torch.float64),
-                 value=pinned((E, T), torch.float64)) for _ in specs]
+small = [max(s.space.cards) <= 256 for s in specs]
+host_out = [dict(idx=None if sm else pinned((E, T + 1, D), torch.int16).view(np.uint16),
+                 idx8=pinned((E, T + 1, D), torch.uint8) if sm else None, score=pinned((E, T + 1), torch.float64),
+                 actions=None, actions2=pinned((E, T, 2), torch.uint8), logp=None, value=None,
+                 logp32=pinned((E, T), torch.float32), value32=pinned((E, T), torch.float32)) for sm in small]
 tasks = [RolloutTask(d, a, g, hi, 0, s.seed) for s, d, a, g, hi in zip(specs, spaces, agents, gbts, host_init)]
-tot = sum(sum(v.nbytes for v in o.values()) for o in host_out)
+tot = sum(sum(v.nbytes for v in o.values() if v is not None) for o in host_out)
 # raw D2H bandwidth of one big pinned copy
 dbuf = torch.empty(tot, dtype=torch.uint8, device="cuda"); hbuf = torch.empty(tot, dtype=torch.uint8, pin_memory=True)
 for _ in range(2): hbuf.copy_(dbuf); torch.cuda.synchronize()
 t0 = time.perf_counter(); hbuf.copy_(dbuf); torch.cuda.synchronize(); dt = time.perf_counter() - t0
 print(f"raw D2H {tot/1e9:.2f} GB in {dt*1e3:.1f} ms = {tot/dt/1e9:.1f} GB/s")
-for S in [1, 2, 3, 5, 8, 16]:
+for S in [1, 2, 3, 4, 5, 6, 8]:
     ctx.set_option(L.OPT_ROLLOUT_SEGMENTS, S)
     run_episodes_batch(tasks, T, ctx, host_out=host_out)
     t0 = time.perf_counter()
