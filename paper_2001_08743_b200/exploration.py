@@ -208,6 +208,86 @@ class SaParams:  # SPEC.md SaParams (the temperature schedule is SPEC-invented)
     cooling_rate: float = 0.99
 
 
+@dataclass
+class SaTask:
+    """One workload of a grouped sa_search launch (chains = rows of init_idx)."""
+    space: Space
+    cost_model: DeviceGbt
+    init_idx: object          # E x D knob indices (numpy / CUDA uint16 tensor); see sa_seeds
+    chain_offset: int = 0     # global id of the first chain (RNG key; sharding)
+    rng_seed: int = 0         # SA stream = stream_seed(rng_seed, "sa")
+
+
+def sa_seeds(space: Space, seeds, num_chains: int, rng_seed: int = 0) -> np.ndarray:
+    """The chains' start states: the given seeds, padded with uniformly random
+    configurations from stream_seed(rng_seed, "sa-pad")."""
+    D = space.D
+    seeds = np.asarray(seeds, np.int64).reshape(-1, D) if len(seeds) else np.zeros((0, D), np.int64)
+    if len(seeds) < num_chains:
+        st = stream_seed(rng_seed, "sa-pad")
+        pad = np.zeros((num_chains - len(seeds), D), np.int64)
+        for i in range(len(pad)):
+            for d, c in enumerate(space.card):
+                pad[i, d] = mix64((st + i * D + d + 1) & 0xFFFFFFFFFFFFFFFF) % int(c)
+        seeds = np.concatenate([seeds, pad])
+    return np.ascontiguousarray(seeds[:num_chains], np.uint16)
+
+
+def sa_search_batch(tasks: Sequence[SaTask], params: SaParams, ctx: Optional[Context] = None,
+                    device_out: bool = False, host_out: Optional[list] = None, want_accepted: bool = True):
+    """Grouped sa_search over several workloads in ONE kernel launch (K7).
+
+    Host arrays by default (pass pinned `host_out` buffers for full PCIe speed);
+    with CUDA-tensor init_idx and device_out=True the trajectory stays on the
+    device and the call is stream-ordered. Returns per task dict(idx E x (T+1)
+    x D uint16, score E x (T+1), accepted E x T uint8)."""
+    ctx = ctx or tasks[0].space.ctx
+    T = params.max_steps
+    arr = (L.SaTaskC * len(tasks))()
+    outs, keep = [], []
+    dev = False
+    for i, t in enumerate(tasks):
+        D = t.space.D
+        dev = hasattr(t.init_idx, "is_cuda") and t.init_idx.is_cuda
+        if dev:
+            import torch
+            init = t.init_idx.to(torch.uint16).contiguous()
+            E = init.shape[0]
+            mk = lambda shape, dt: torch.empty(shape, dtype=dt, device=init.device)
+            pp = lambda a: None if a is None else C.c_void_p(a.data_ptr())
+            if not device_out:
+                raise ConfigError("sa_search_batch: device inputs need device_out=True")
+        else:
+            init = np.ascontiguousarray(t.init_idx, np.uint16).reshape(-1, D)
+            E = len(init)
+            mk = lambda shape, dt: np.zeros(shape, {"u16": np.uint16, "f64": np.float64, "u8": np.uint8}[dt])
+            pp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
+        if host_out is not None:
+            o = host_out[i]
+        elif dev:
+            import torch
+            o = dict(idx=mk((E, T + 1, D), torch.uint16), score=mk((E, T + 1), torch.float64),
+                     accepted=mk((E, T), torch.uint8) if want_accepted else None)
+        else:
+            o = dict(idx=mk((E, T + 1, D), "u16"), score=mk((E, T + 1), "f64"),
+                     accepted=mk((E, T), "u8") if want_accepted else None)
+        keep.append(init)
+        a = arr[i]
+        a.space = t.space.h
+        a.gbt = t.cost_model.h
+        a.num_chains = E
+        a.chain_offset = t.chain_offset
+        a.sa_seed = stream_seed(t.rng_seed, "sa")
+        a.init_idx = pp(init)
+        a.idx = pp(o["idx"])
+        a.score = pp(o["score"])
+        a.accepted = pp(o.get("accepted"))
+        outs.append(o)
+    p = L.SaParamsC(params.initial_temperature, params.cooling_rate)
+    ctx.check(L.lib().ktune_sa_search(ctx.h, len(tasks), arr, T, C.byref(p), L.F_DEVICE if dev else 0))
+    return outs
+
+
 def sa_search(space: Space, cost_model: DeviceGbt, seeds, params: SaParams = SaParams(), rng_seed: int = 0,
               chain_offset: int = 0, ctx: Optional[Context] = None):
     """sa_search(space, cost_model, seeds, params, rng_seed) -> CandidateSet (SPEC.md:229-237).
@@ -220,26 +300,7 @@ def sa_search(space: Space, cost_model: DeviceGbt, seeds, params: SaParams = SaP
     predicted fitness and deduplicated, trajectory dict(idx, score, accepted)).
     """
     from .sampling import candidates_from_rows
-    ctx = ctx or space.ctx
-    D = space.D
-    seeds = np.asarray(seeds, np.int64).reshape(-1, D) if len(seeds) else np.zeros((0, D), np.int64)
-    E = params.num_chains
-    if len(seeds) < E:
-        st = stream_seed(rng_seed, "sa-pad")
-        pad = np.zeros((E - len(seeds), D), np.int64)
-        for i in range(len(pad)):
-            for d, c in enumerate(space.card):
-                pad[i, d] = mix64((st + i * D + d + 1) & 0xFFFFFFFFFFFFFFFF) % int(c)
-        seeds = np.concatenate([seeds, pad])
-    init = np.ascontiguousarray(seeds[:E], np.uint16)
-    T = params.max_steps
-    idx = np.zeros((E, T + 1, D), np.uint16)
-    score = np.zeros((E, T + 1))
-    acc = np.zeros((E, T), np.uint8)
-    t = L.SaTaskC(space.h, cost_model.h, E, chain_offset, stream_seed(rng_seed, "sa"),
-                  init.ctypes.data_as(C.c_void_p), idx.ctypes.data_as(C.c_void_p), score.ctypes.data_as(C.c_void_p),
-                  acc.ctypes.data_as(C.c_void_p))
-    p = L.SaParamsC(params.initial_temperature, params.cooling_rate)
-    ctx.check(L.lib().ktune_sa_search(ctx.h, 1, C.byref(t), T, C.byref(p), 0))
-    cands = candidates_from_rows(space, idx.reshape(-1, D), score.reshape(-1))  # on the device
-    return cands, dict(idx=idx, score=score, accepted=acc)
+    init = sa_seeds(space, seeds, params.num_chains, rng_seed)
+    o = sa_search_batch([SaTask(space, cost_model, init, chain_offset, rng_seed)], params, ctx)[0]
+    cands = candidates_from_rows(space, o["idx"].reshape(-1, space.D), o["score"].reshape(-1))  # on the device
+    return cands, o

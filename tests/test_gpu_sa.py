@@ -60,3 +60,27 @@ def test_sa_chain_sharding_invariance(O, ctx):
     _, part = sa_search(ds, dg, seeds[60:], SaParams(40, 30, 0.05, 0.95), rng_seed=4, chain_offset=60)
     assert np.array_equal(full["idx"][60:], part["idx"])
     assert np.array_equal(full["score"][60:], part["score"])
+
+
+def test_sa_grouped_launch_equals_single_calls(O, ctx):
+    """sa_search_batch: several spaces in one launch = one call per task; the
+    device-resident variant returns the same trajectory."""
+    import torch
+    from paper_2001_08743_b200.exploration import SaParams, SaTask, sa_search, sa_search_batch, sa_seeds
+    p = SaParams(96, 25, 0.05, 0.95)
+    tasks, singles = [], []
+    for k, name in enumerate(["resnet_c2", "synthetic16", "resnet_dense_u16"]):
+        sp, osp, og, ds, dg = _setup(O, ctx, name, 11 + k)
+        init = sa_seeds(ds, np.zeros((0, sp.num_knobs)), p.num_chains, rng_seed=k)
+        tasks.append(SaTask(ds, dg, init, 0, k))
+        singles.append(sa_search(ds, dg, init, p, rng_seed=k)[1])
+    grouped = sa_search_batch(tasks, p)
+    dev_tasks = [SaTask(t.space, t.cost_model, torch.from_numpy(t.init_idx.view(np.int16)).cuda(), 0, t.rng_seed)
+                 for t in tasks]
+    on_dev = sa_search_batch(dev_tasks, p, device_out=True)
+    for g, s1, d in zip(grouped, singles, on_dev):
+        for key in ("idx", "score", "accepted"):
+            assert np.array_equal(g[key], s1[key])
+        assert np.array_equal(d["idx"].view(torch.int16).cpu().numpy().view(np.uint16), g["idx"])
+        assert np.array_equal(d["score"].cpu().numpy(), g["score"])
+        assert np.array_equal(d["accepted"].cpu().numpy(), g["accepted"])
