@@ -215,30 +215,40 @@ __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
   for (int i = threadIdx.x; i < T * NL; i += kScoreThreads) s_leaf[i] = g_leaf[i];
   for (int i = threadIdx.x; i < T * NI; i += kScoreThreads) s_node[i] = g_node[i];
   __syncthreads();
-  const unsigned char* col0 = reinterpret_cast<const unsigned char*>(s_idx + threadIdx.x);
-  const unsigned char* col1 = reinterpret_cast<const unsigned char*>(s_idx + D * kScoreThreads + threadIdx.x);
+  // Byte offsets inside the dynamic smem window. A column entry carries its own
+  // byte offset in the high half, (coff << 16) | idx, so the node test
+  // idx >= t1 is ONE unsigned compare against the node word (coff << 16) | t1
+  // (the high halves are equal by construction). Node addresses are walked as
+  // byte offsets inside the tree (r = 4n).
+  const unsigned char* sb = smem;
+  const uint32_t nodes = (uint32_t)(reinterpret_cast<const unsigned char*>(s_node) - sb);
+  const uint32_t col0 = (uint32_t)(reinterpret_cast<const unsigned char*>(s_idx + threadIdx.x) - sb);
+  const uint32_t col1 = col0 + (uint32_t)D * kScoreThreads * 4;
+  auto ld32 = [&](uint32_t a) { return *reinterpret_cast<const uint32_t*>(sb + a); };
   for (int64_t c0 = (int64_t)blockIdx.x * 2 * kScoreThreads; c0 < B; c0 += (int64_t)gridDim.x * 2 * kScoreThreads) {
     const int64_t j0 = c0 + threadIdx.x, j1 = j0 + kScoreThreads;
     const int64_t i0 = map(j0), i1 = map(j1);  // row of the j-th scored configuration
     for (int d = 0; d < D; ++d) {  // transposed columns: thread-private, conflict-free
-      s_idx[d * kScoreThreads + threadIdx.x] = j0 < B ? (int32_t)idx[i0 * D + d] : 0;
-      s_idx[(D + d) * kScoreThreads + threadIdx.x] = j1 < B ? (int32_t)idx[i1 * D + d] : 0;
+      const uint32_t tag = (uint32_t)(d * kScoreThreads * 4) << 16;
+      s_idx[d * kScoreThreads + threadIdx.x] = (int32_t)(tag | (j0 < B ? (uint32_t)idx[i0 * D + d] : 0u));
+      s_idx[(D + d) * kScoreThreads + threadIdx.x] = (int32_t)(tag | (j1 < B ? (uint32_t)idx[i1 * D + d] : 0u));
     }
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll 2
     for (int t = 0; t < T; ++t) {
-      const uint32_t* tn = s_node + t * NI;
-      int n0 = 0, n1 = 0;
+      const uint32_t tb = nodes + (uint32_t)(t * NI * 4);
+      uint32_t r0 = 0, r1 = 0;  // byte offset of the current node inside the tree: 4n
 #pragma unroll
       for (int l = 0; l < DEPTH; ++l) {
-        const uint32_t w0 = tn[n0], w1 = tn[n1];
-        const int v0 = *reinterpret_cast<const int32_t*>(col0 + (w0 >> 16));
-        const int v1 = *reinterpret_cast<const int32_t*>(col1 + (w1 >> 16));
-        n0 = 2 * n0 + 1 + (v0 >= (int)(w0 & 0xFFFFu) ? 1 : 0);
-        n1 = 2 * n1 + 1 + (v1 >= (int)(w1 & 0xFFFFu) ? 1 : 0);
+        const uint32_t w0 = ld32(tb + r0), w1 = ld32(tb + r1);
+        const uint32_t v0 = ld32(col0 + (w0 >> 16)), v1 = ld32(col1 + (w1 >> 16));
+        r0 = 2 * r0 + (v0 >= w0 ? 8u : 4u);  // children of n: 2n+1, 2n+2
+        r1 = 2 * r1 + (v1 >= w1 ? 8u : 4u);
       }
-      s0 = kt::dadd(s0, s_leaf[t * NL + (n0 - NI)]);
-      s1 = kt::dadd(s1, s_leaf[t * NL + (n1 - NI)]);
+      // leaf of node n = r/4 is n - NI; s_leaf sits at smem offset 0
+      const uint32_t lb = (uint32_t)(t * NL * 8) - (uint32_t)(NI * 8);
+      s0 = kt::dadd(s0, *reinterpret_cast<const double*>(sb + lb + 2 * r0));
+      s1 = kt::dadd(s1, *reinterpret_cast<const double*>(sb + lb + 2 * r1));
     }
     if (j0 < B) out[i0] = kt::dadd(base, kt::dmul(lr, s0));
     if (j1 < B) out[i1] = kt::dadd(base, kt::dmul(lr, s1));

@@ -36,6 +36,7 @@ struct SaTask {
   double* score;
   uint8_t* accepted;
   int32_t cta_base;
+  int32_t row_vec;  // 8: uint4 row stores, 2: uint32, 1: uint16 (from D and the idx alignment)
 };
 
 struct SaLaunch {
@@ -48,16 +49,37 @@ __host__ __device__ inline size_t sa_smem_bytes(int D, int ntrees, int depth) {
          (size_t)D * kSaThreads * 4;
 }
 
+// One ensemble evaluation of the chain's column: the trees are walked G at a
+// time level by level (G independent smem chains in flight per thread), then
+// their leaves are added in tree order — the reference's sequential sum
+// (cost_model.cpp:179-187) — and scaled: base + lr * sum.
+template <int DEPTH>
 __device__ __forceinline__ double walk(const uint32_t* __restrict__ s_node, const double* __restrict__ s_leaf,
-                                       const unsigned char* col, int ntrees, int depth, double base, double lr) {
-  const int NI = (1 << depth) - 1, NL = 1 << depth;
+                                       const unsigned char* col, int ntrees, double base, double lr) {
+  constexpr int NI = (1 << DEPTH) - 1, NL = 1 << DEPTH, G = 8;
   double s = 0.0;
-#pragma unroll 2
-  for (int tr = 0; tr < ntrees; ++tr) {
-    const uint32_t* tn = s_node + tr * NI;
+  int tr = 0;
+  for (; tr + G <= ntrees; tr += G) {
+    int nd[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) nd[g] = 0;
+#pragma unroll
+    for (int l = 0; l < DEPTH; ++l) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const uint32_t w = s_node[(tr + g) * NI + nd[g]];
+        const int v = *reinterpret_cast<const int*>(col + (w >> 16));
+        nd[g] = 2 * nd[g] + 1 + (v >= (int)(w & 0xFFFFu) ? 1 : 0);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) s = kt::dadd(s, s_leaf[(tr + g) * NL + (nd[g] - NI)]);
+  }
+  for (; tr < ntrees; ++tr) {
     int nd = 0;
-    for (int l = 0; l < depth; ++l) {
-      const uint32_t w = tn[nd];
+#pragma unroll
+    for (int l = 0; l < DEPTH; ++l) {
+      const uint32_t w = s_node[tr * NI + nd];
       const int v = *reinterpret_cast<const int*>(col + (w >> 16));
       nd = 2 * nd + 1 + (v >= (int)(w & 0xFFFFu) ? 1 : 0);
     }
@@ -66,12 +88,34 @@ __device__ __forceinline__ double walk(const uint32_t* __restrict__ s_node, cons
   return kt::dadd(base, kt::dmul(lr, s));
 }
 
+// The chain's configuration (thread-private smem column) -> trajectory row t.
+__device__ __forceinline__ void store_row(uint16_t* row, const int32_t* col, int D, int vec) {
+  if (vec == 8) {
+    for (int d = 0; d < D; d += 8) {
+      uint4 q;
+      q.x = (uint32_t)col[(d + 0) * kSaThreads] | ((uint32_t)col[(d + 1) * kSaThreads] << 16);
+      q.y = (uint32_t)col[(d + 2) * kSaThreads] | ((uint32_t)col[(d + 3) * kSaThreads] << 16);
+      q.z = (uint32_t)col[(d + 4) * kSaThreads] | ((uint32_t)col[(d + 5) * kSaThreads] << 16);
+      q.w = (uint32_t)col[(d + 6) * kSaThreads] | ((uint32_t)col[(d + 7) * kSaThreads] << 16);
+      *reinterpret_cast<uint4*>(row + d) = q;
+    }
+  } else if (vec == 2) {
+    for (int d = 0; d < D; d += 2)
+      *reinterpret_cast<uint32_t*>(row + d) =
+          (uint32_t)col[d * kSaThreads] | ((uint32_t)col[(d + 1) * kSaThreads] << 16);
+  } else {
+    for (int d = 0; d < D; ++d) row[d] = (uint16_t)col[d * kSaThreads];
+  }
+}
+
+template <int DEPTH>
 __global__ void __launch_bounds__(kSaThreads) sa_kernel(const __grid_constant__ SaLaunch L) {
   extern __shared__ __align__(16) unsigned char sm[];
   int ti = 0;
   while (ti + 1 < L.num_tasks && L.task[ti + 1].cta_base <= (int)blockIdx.x) ++ti;
   const SaTask& tk = L.task[ti];
-  const int D = tk.D, T = tk.T, NI = (1 << tk.depth) - 1, NL = 1 << tk.depth;
+  const int D = tk.D, T = tk.T;
+  constexpr int NI = (1 << DEPTH) - 1, NL = 1 << DEPTH;
   double* s_leaf = reinterpret_cast<double*>(sm);
   uint32_t* s_node = reinterpret_cast<uint32_t*>(sm + (size_t)tk.ntrees * NL * 8);
   int32_t* s_col = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(s_node) +
@@ -87,12 +131,9 @@ __global__ void __launch_bounds__(kSaThreads) sa_kernel(const __grid_constant__ 
   int32_t* col = s_col + threadIdx.x;  // col[d * kSaThreads]
   const unsigned char* colb = reinterpret_cast<const unsigned char*>(col);
   uint16_t* out = tk.idx + c * (int64_t)(T + 1) * D;
-  for (int d = 0; d < D; ++d) {
-    const uint16_t v = tk.init_idx[c * D + d];
-    col[d * kSaThreads] = v;
-    out[d] = v;
-  }
-  double f = walk(s_node, s_leaf, colb, tk.ntrees, tk.depth, tk.base, tk.lr);
+  for (int d = 0; d < D; ++d) col[d * kSaThreads] = tk.init_idx[c * D + d];
+  store_row(out, col, D, tk.row_vec);
+  double f = walk<DEPTH>(s_node, s_leaf, colb, tk.ntrees, tk.base, tk.lr);
   double* sc = tk.score + c * (int64_t)(T + 1);
   sc[0] = f;
   double temp = tk.t0;
@@ -107,18 +148,21 @@ __global__ void __launch_bounds__(kSaThreads) sa_kernel(const __grid_constant__ 
     int v = old + dir;
     v = v < 0 ? 0 : (v > tk.card[knob] - 1 ? tk.card[knob] - 1 : v);
     col[knob * kSaThreads] = v;
-    const double fp = walk(s_node, s_leaf, colb, tk.ntrees, tk.depth, tk.base, tk.lr);
+    const double fp = walk<DEPTH>(s_node, s_leaf, colb, tk.ntrees, tk.base, tk.lr);
     const double delta = kt::dsub(fp, f);
     const bool accept = delta >= 0.0 || u2 < kt::kt_exp(kt::ddiv(delta, temp));
     if (accept) f = fp;
     else col[knob * kSaThreads] = old;
-    uint16_t* row = out + (int64_t)(t + 1) * D;
-    for (int d = 0; d < D; ++d) row[d] = (uint16_t)col[d * kSaThreads];
+    store_row(out + (int64_t)(t + 1) * D, col, D, tk.row_vec);
     sc[t + 1] = f;
     if (tk.accepted) tk.accepted[c * (int64_t)T + t] = accept ? 1 : 0;
     temp = kt::dmul(temp, tk.rate);
   }
 }
+
+using SaKernel = void (*)(SaLaunch);
+constexpr SaKernel kSaKernels[9] = {sa_kernel<0>, sa_kernel<1>, sa_kernel<2>, sa_kernel<3>, sa_kernel<4>,
+                                    sa_kernel<5>, sa_kernel<6>, sa_kernel<7>, sa_kernel<8>};
 
 }  // namespace
 
@@ -178,20 +222,29 @@ extern "C" int ktune_sa_search(ktune_ctx* ctx, int num_tasks, const ktune_sa_tas
         s.score = (double*)alloc(E * (T + 1) * 8);
         s.accepted = t.accepted ? (uint8_t*)alloc(E * T) : nullptr;
       }
+      const uintptr_t a = reinterpret_cast<uintptr_t>(s.idx);
+      s.row_vec = (D % 8 == 0 && a % 16 == 0) ? 8 : (D % 2 == 0 && a % 4 == 0) ? 2 : 1;
       smem = std::max(smem, sa_smem_bytes(D, g->num_trees, g->depth));
     }
     if (smem > 227 * 1024) kt::fail(KTUNE_ERR_CONFIG, "sa_search: cost model too large for shared memory");
-    KT_CUDA(cudaFuncSetAttribute(sa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    for (int t0 = 0; t0 < num_tasks; t0 += kMaxSaTasks) {
-      SaLaunch L{};
-      L.num_tasks = std::min(kMaxSaTasks, num_tasks - t0);
-      int ctas = 0;
-      for (int q = 0; q < L.num_tasks; ++q) {
-        L.task[q] = st[t0 + q];
-        L.task[q].cta_base = ctas;
-        ctas += (int)kt::ceil_div(st[t0 + q].E, kSaThreads);
+    // one launch per tree depth present (complete trees: the walk is compiled per depth)
+    for (int dep = 0; dep <= 8; ++dep) {
+      std::vector<SaTask> sel;
+      for (const SaTask& s : st)
+        if (s.depth == dep) sel.push_back(s);
+      if (sel.empty()) continue;
+      KT_CUDA(cudaFuncSetAttribute(kSaKernels[dep], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      for (size_t t0 = 0; t0 < sel.size(); t0 += kMaxSaTasks) {
+        SaLaunch L{};
+        L.num_tasks = (int)std::min<size_t>(kMaxSaTasks, sel.size() - t0);
+        int ctas = 0;
+        for (int q = 0; q < L.num_tasks; ++q) {
+          L.task[q] = sel[t0 + q];
+          L.task[q].cta_base = ctas;
+          ctas += (int)kt::ceil_div(sel[t0 + q].E, kSaThreads);
+        }
+        if (ctas > 0) kSaKernels[dep]<<<(unsigned)ctas, kSaThreads, smem, ctx->stream>>>(L);
       }
-      if (ctas > 0) sa_kernel<<<(unsigned)ctas, kSaThreads, smem, ctx->stream>>>(L);
     }
     kt::check_launch(ctx, "sa_search");
     if (!dev) {
