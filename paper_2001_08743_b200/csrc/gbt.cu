@@ -200,9 +200,10 @@ __global__ void __launch_bounds__(256) gbt_predict_idx_kernel(
 
 // K1 fast path. Complete trees of compile-time depth; node word = (feature
 // column byte offset << 16) | t1, so a level is: LDS node, LDS idx at
-// column+offset, compare, 2n+1+right. Two configurations per thread (ILP), a
-// persistent grid over 512-config chunks, trees + knob-index columns in smem.
+// column+offset, compare, 2n+1+right. kScoreCfg configurations per thread (ILP), a
+// persistent grid over kScoreCfg*256-config chunks, trees + knob-index columns in smem.
 constexpr int kScoreThreads = 256;
+constexpr int kScoreCfg = 2;  // configurations per thread (independent walks in flight)
 template <class IdxT, int DEPTH>
 __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
     const IdxT* __restrict__ idx, int64_t B, int D, int T, const uint32_t* __restrict__ g_node,
@@ -223,35 +224,48 @@ __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
   const unsigned char* sb = smem;
   const uint32_t nodes = (uint32_t)(reinterpret_cast<const unsigned char*>(s_node) - sb);
   const uint32_t col0 = (uint32_t)(reinterpret_cast<const unsigned char*>(s_idx + threadIdx.x) - sb);
-  const uint32_t col1 = col0 + (uint32_t)D * kScoreThreads * 4;
   auto ld32 = [&](uint32_t a) { return *reinterpret_cast<const uint32_t*>(sb + a); };
-  for (int64_t c0 = (int64_t)blockIdx.x * 2 * kScoreThreads; c0 < B; c0 += (int64_t)gridDim.x * 2 * kScoreThreads) {
-    const int64_t j0 = c0 + threadIdx.x, j1 = j0 + kScoreThreads;
-    const int64_t i0 = map(j0), i1 = map(j1);  // row of the j-th scored configuration
+  constexpr int NC = kScoreCfg;
+  for (int64_t c0 = (int64_t)blockIdx.x * NC * kScoreThreads; c0 < B; c0 += (int64_t)gridDim.x * NC * kScoreThreads) {
+    int64_t row[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const int64_t j = c0 + q * kScoreThreads + threadIdx.x;
+      row[q] = j < B ? map(j) : -1;  // row of the j-th scored configuration
+    }
     for (int d = 0; d < D; ++d) {  // transposed columns: thread-private, conflict-free
       const uint32_t tag = (uint32_t)(d * kScoreThreads * 4) << 16;
-      s_idx[d * kScoreThreads + threadIdx.x] = (int32_t)(tag | (j0 < B ? (uint32_t)idx[i0 * D + d] : 0u));
-      s_idx[(D + d) * kScoreThreads + threadIdx.x] = (int32_t)(tag | (j1 < B ? (uint32_t)idx[i1 * D + d] : 0u));
+#pragma unroll
+      for (int q = 0; q < NC; ++q)
+        s_idx[(q * D + d) * kScoreThreads + threadIdx.x] =
+            (int32_t)(tag | (row[q] >= 0 ? (uint32_t)idx[row[q] * D + d] : 0u));
     }
-    double s0 = 0.0, s1 = 0.0;
+    double s[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) s[q] = 0.0;
 #pragma unroll 2
     for (int t = 0; t < T; ++t) {
       const uint32_t tb = nodes + (uint32_t)(t * NI * 4);
-      uint32_t r0 = 0, r1 = 0;  // byte offset of the current node inside the tree: 4n
+      uint32_t r[NC];  // byte offset of the current node inside the tree: 4n
+#pragma unroll
+      for (int q = 0; q < NC; ++q) r[q] = 0;
 #pragma unroll
       for (int l = 0; l < DEPTH; ++l) {
-        const uint32_t w0 = ld32(tb + r0), w1 = ld32(tb + r1);
-        const uint32_t v0 = ld32(col0 + (w0 >> 16)), v1 = ld32(col1 + (w1 >> 16));
-        r0 = 2 * r0 + (v0 >= w0 ? 8u : 4u);  // children of n: 2n+1, 2n+2
-        r1 = 2 * r1 + (v1 >= w1 ? 8u : 4u);
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+          const uint32_t w = ld32(tb + r[q]);
+          const uint32_t v = ld32(col0 + (uint32_t)(q * D * kScoreThreads * 4) + (w >> 16));
+          r[q] = 2 * r[q] + (v >= w ? 8u : 4u);  // children of n: 2n+1, 2n+2
+        }
       }
       // leaf of node n = r/4 is n - NI; s_leaf sits at smem offset 0
       const uint32_t lb = (uint32_t)(t * NL * 8) - (uint32_t)(NI * 8);
-      s0 = kt::dadd(s0, *reinterpret_cast<const double*>(sb + lb + 2 * r0));
-      s1 = kt::dadd(s1, *reinterpret_cast<const double*>(sb + lb + 2 * r1));
+#pragma unroll
+      for (int q = 0; q < NC; ++q) s[q] = kt::dadd(s[q], *reinterpret_cast<const double*>(sb + lb + 2 * r[q]));
     }
-    if (j0 < B) out[i0] = kt::dadd(base, kt::dmul(lr, s0));
-    if (j1 < B) out[i1] = kt::dadd(base, kt::dmul(lr, s1));
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+      if (row[q] >= 0) out[row[q]] = kt::dadd(base, kt::dmul(lr, s[q]));
   }
 }
 
@@ -321,10 +335,10 @@ void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_id
   const int ni = (1 << g->depth) - 1, nl = 1 << g->depth;
   const size_t tree_bytes = (size_t)g->num_trees * (ni * 4 + nl * 8);
   if (g->d_inode_pk) {  // K1 fast path
-    const size_t smem = tree_bytes + 16 + (size_t)2 * g->D * kScoreThreads * 4;
+    const size_t smem = tree_bytes + 16 + (size_t)kScoreCfg * g->D * kScoreThreads * 4;
     if (smem <= 200 * 1024) {
       const int per_sm = std::max(1, std::min(8, (int)((220 * 1024) / smem)));
-      const int grid = (int)std::min<int64_t>(ceil_div(B, 2 * kScoreThreads), (int64_t)sm_count(ctx) * per_sm);
+      const int grid = (int)std::min<int64_t>(ceil_div(B, kScoreCfg * kScoreThreads), (int64_t)sm_count(ctx) * per_sm);
       kt::ProfScope prof(ctx, KTUNE_STAT_GBT_NS);
 #define KT_SCORE(T_, DEP)                                                                                    \
   {                                                                                                          \

@@ -532,15 +532,32 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
   __shared__ double red[32];
   __shared__ int32_t s_sum[kt::kMaxK * kt::kMaxKnobs];
   __shared__ int32_t s_cnt[kt::kMaxK];
+  __shared__ __align__(16) float s_c32[kt::kMaxK * kt::kMaxKnobs];  // [k][DM], zero-padded
+  __shared__ float s_amax;
   const int D = sp.D;
   double* s_c = sdyn;
   double* s_e = sdyn + k * D;  // per-cluster centroid-difference bound E_c
   double* s_lut = sdyn + k * D + kt::kMaxK;
+  // fp32 screening bound |s32 - d2_ref| <= A + R s32 for every cluster (features and
+  // centroids in [0, 1]): conversions and the difference cost <= 1.5 ulp(1) per knob,
+  // squaring <= 2x that, the FMA chain D 2^-24 relative; A also carries max_c E_c and
+  // both are doubled for the fp32 arithmetic of the test itself.
+  const float R32 = (float)(2 * D + 8) * 0x1.0p-24f;
+  const double A32 = (double)(12 * D + 4) * 0x1.0p-24;
   for (int i = threadIdx.x; i < k * D; i += blockDim.x) {
     s_c[i] = cB[i];
     s_sum[i] = 0;
   }
+  for (int i = threadIdx.x; i < k * DM; i += blockDim.x) {
+    const int c = i / DM, d = i % DM;
+    s_c32[i] = d < D ? (float)cB[c * D + d] : 0.f;
+  }
   for (int i = threadIdx.x; i < k; i += blockDim.x) s_e[i] = dB[kt::kMaxK * kt::kMaxKnobs + i];
+  if (threadIdx.x == 0) {
+    double emax = 0.0;
+    for (int c = 0; c < k; ++c) emax = fmax(emax, dB[kt::kMaxK * kt::kMaxKnobs + c]);
+    s_amax = __double2float_ru(A32 + 2.0 * emax);
+  }
   for (int i = threadIdx.x; i < k; i += blockDim.x) s_cnt[i] = 0;
   const double* lut = stage_lut(sp, s_lut, lut_total);
   __syncthreads();
@@ -553,34 +570,80 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
     const bool live = i < N;
     int bc = 0;
     if (live) {
+      // (1) fp32 screening: the winner is certified if the runner-up's interval lies
+      // strictly above the winner's: s2 (1 - R) - A > s1 (1 + R) + A
       double x[DM];  // DM >= D, compile-time: the features stay in registers
 #pragma unroll
       for (int d = 0; d < DM; ++d) x[d] = d < D ? feat(sp, lut, pts + i * D, d) : 0.0;
-      double best = INFINITY, best_e = 0.0, lo_others = INFINITY;
+      float xf[DM];
+#pragma unroll
+      for (int d = 0; d < DM; ++d) xf[d] = (float)x[d];  // padded knobs add 0 exactly
+      float s1 = INFINITY, s2 = INFINITY;
+      int w32 = 0;
       for (int c = 0; c < k; ++c) {
-        const double* cc = s_c + c * D;
+        const float4* cc = reinterpret_cast<const float4*>(s_c32 + c * DM);
+        float s32 = 0.f;
+#pragma unroll
+        for (int q = 0; q < DM / 4; ++q) {
+          const float4 v = cc[q];
+          float t = xf[4 * q] - v.x;
+          s32 = fmaf(t, t, s32);
+          t = xf[4 * q + 1] - v.y;
+          s32 = fmaf(t, t, s32);
+          t = xf[4 * q + 2] - v.z;
+          s32 = fmaf(t, t, s32);
+          t = xf[4 * q + 3] - v.w;
+          s32 = fmaf(t, t, s32);
+        }
+        if (s32 < s1) {
+          s2 = s1;
+          s1 = s32;
+          w32 = c;
+        } else {
+          s2 = fminf(s2, s32);
+        }
+      }
+      const float amax = s_amax;
+      double best = INFINITY;
+      if (fmaf(-R32, s2, s2) - amax > fmaf(R32, s1, s1) + amax) {  // (2a) the winner's d2 against c_B in the reference order
+        const double* cc = s_c + w32 * D;
         double t = kt::dsub(x[0], cc[0]);
-        double s = kt::dmul(t, t);
+        best = kt::dmul(t, t);
 #pragma unroll
         for (int d = 1; d < DM; ++d) {
           if (d < D) {
             t = kt::dsub(x[d], cc[d]);
-            s = kt::dadd(s, kt::dmul(t, t));
+            best = kt::dadd(best, kt::dmul(t, t));
           }
         }
-        // |d2_ref - s| <= E_c (centroid difference) + the rounding of both evaluations
-        const double e = (s_e[c] + grow * (s + s_e[c])) * (1.0 + 0x1.0p-20) + 1e-300;
-        if (s < best) {  // strict <: lowest index on ties, as the reference
-          if (best < INFINITY) lo_others = fmin(lo_others, best - best_e);
-          best = s;
-          best_e = e;
-          bc = c;
-        } else {
-          lo_others = fmin(lo_others, s - e);
+        bc = w32;
+      } else {  // (2b) near tie: the full fp64 scan with its own certificate
+        double best_e = 0.0, lo_others = INFINITY;
+        for (int c = 0; c < k; ++c) {
+          const double* cc = s_c + c * D;
+          double t = kt::dsub(x[0], cc[0]);
+          double s = kt::dmul(t, t);
+#pragma unroll
+          for (int d = 1; d < DM; ++d) {
+            if (d < D) {
+              t = kt::dsub(x[d], cc[d]);
+              s = kt::dadd(s, kt::dmul(t, t));
+            }
+          }
+          // |d2_ref - s| <= E_c (centroid difference) + the rounding of both evaluations
+          const double e = (s_e[c] + grow * (s + s_e[c])) * (1.0 + 0x1.0p-20) + 1e-300;
+          if (s < best) {  // strict <: lowest index on ties, as the reference
+            if (best < INFINITY) lo_others = fmin(lo_others, best - best_e);
+            best = s;
+            best_e = e;
+            bc = c;
+          } else {
+            lo_others = fmin(lo_others, s - e);
+          }
         }
+        // certified only if no other cluster's interval reaches the winner's
+        if (!(lo_others > best + best_e)) ++nunc;
       }
-      // certified only if no other cluster's interval reaches the winner's
-      if (!(lo_others > best + best_e)) ++nunc;
       asg[i] = bc;
       d2[i] = best;
       part = kt::dadd(part, best);

@@ -165,7 +165,9 @@ def test_assign_paths_bit_exact(O, ctx, ref_ok, mode, name, n, k, seed):
     print("uncertain (exact-fallback) points:", ctx.stat(L.STAT_ASSIGN_FALLBACKS))
 
 
-@pytest.mark.parametrize("name,n,k,seed", [("alexnet_c3_u16", 30000, 8, 3), ("synthetic16", 20000, 12, 4)])
+@pytest.mark.parametrize("name,n,k,seed", [("alexnet_c3_u16", 30000, 8, 3), ("synthetic16", 20000, 12, 4),
+                                           ("alexnet_c3_u16", 30000, 63, 5), ("resnet_c2", 8000, 40, 6),
+                                           ("synthetic16", 20000, 33, 7)])
 def test_certified_lloyd_equals_exact_mode(O, ctx, name, n, k, seed):
     """Mode B (integer-sum centroids, certified assignments, exact finalisation) and
     mode A (exact-order sums every iteration) give identical runs; mode B ran
