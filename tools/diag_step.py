@@ -31,6 +31,7 @@ for _ in range(2):
 torch.cuda.synchronize()
 mode = os.environ.get("MODE", "")
 if os.environ.get("CHECKMODE"): ctx.set_option(L.OPT_ROLLOUT_CHECK, int(os.environ["CHECKMODE"]))
+if os.environ.get("DELTA"): ctx.set_option(L.OPT_ROLLOUT_DELTA, int(float(os.environ["DELTA"]) * 1e12))  # probability units
 if "prof" in mode: ctx.set_option(L.OPT_PROFILE, 1)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 clk = None
