@@ -53,6 +53,8 @@ constexpr float kActScale = 16384.f;  // 2^14 activation scale inside the fp16 o
 
 struct TcTask {
   int32_t card[kt::kMaxKnobs];
+  int32_t foff[kt::kMaxKnobs];  // feature LUT offsets: x_d = flut[foff[d] + idx_d] (design_space.cpp:195-197)
+  const double* flut;
   const double* params;  // fp64 flat layout (actor_critic.hpp:52-53)
   int32_t n, T;
   int64_t E, episode_offset;
@@ -248,7 +250,7 @@ __device__ __noinline__ Redecided exact_redecide(const TcTask& tk, int t, int L,
 #pragma unroll
   for (int d = 0; d < NMAX; ++d) {
     const int c = (int)((__shfl_sync(0xffffffffu, cfg.w[d >> 1], L) >> ((d & 1) * 16)) & 0xFFFFu);
-    x[d] = (d < n && scard[d] > 1) ? kt::ddiv((double)c, (double)(scard[d] - 1)) : 0.0;
+    x[d] = d < n ? tk.flut[tk.foff[d] + c] : 0.0;  // = c / (card - 1) (0 if card = 1), host-divided
   }
   // h0 = tanh(W0 x + b0): W0 column-major (h x n)
 #pragma unroll
@@ -804,7 +806,11 @@ void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_beg
       if (W[k] == 0) continue;
       const RolloutWork& rw = work[t0 + k];
       TcTask& tk = L.task[nl++];
-      for (int d = 0; d < kMaxKnobs; ++d) tk.card[d] = d < rw.space->D ? rw.space->card[d] : 1;
+      for (int d = 0; d < kMaxKnobs; ++d) {
+        tk.card[d] = d < rw.space->D ? rw.space->card[d] : 1;
+        tk.foff[d] = d < rw.space->D ? (int32_t)rw.space->val_off[d] : 0;
+      }
+      tk.flut = rw.space->d_lut;
       tk.params = rw.ac->d_params;
       tk.n = rw.ac->n;
       tk.T = T;
