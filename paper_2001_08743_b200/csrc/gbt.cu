@@ -209,12 +209,16 @@ __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
     const IdxT* __restrict__ idx, int64_t B, int D, int T, const uint32_t* __restrict__ g_node,
     const double* __restrict__ g_leaf, double base, double lr, double* __restrict__ out, kt::RowMap map) {
   constexpr int NI = (1 << DEPTH) - 1, NL = 1 << DEPTH;
+  constexpr int NIP = (NI + 3) & ~3;  // node words per tree, padded: every tree starts 16-byte aligned
   extern __shared__ __align__(16) unsigned char smem[];
   double* s_leaf = reinterpret_cast<double*>(smem);
   uint32_t* s_node = reinterpret_cast<uint32_t*>(s_leaf + (size_t)T * NL);
-  int32_t* s_idx = reinterpret_cast<int32_t*>(s_node + (((size_t)T * NI + 3) & ~(size_t)3));
+  int32_t* s_idx = reinterpret_cast<int32_t*>(s_node + (size_t)T * NIP);
   for (int i = threadIdx.x; i < T * NL; i += kScoreThreads) s_leaf[i] = g_leaf[i];
-  for (int i = threadIdx.x; i < T * NI; i += kScoreThreads) s_node[i] = g_node[i];
+  for (int i = threadIdx.x; i < T * NIP; i += kScoreThreads) {
+    const int tr = i / NIP, k = i % NIP;
+    s_node[i] = k < NI ? g_node[tr * NI + k] : 0u;
+  }
   __syncthreads();
   // Byte offsets inside the dynamic smem window. A column entry carries its own
   // byte offset in the high half, (coff << 16) | idx, so the node test
@@ -245,12 +249,25 @@ __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
     for (int q = 0; q < NC; ++q) s[q] = 0.0;
 #pragma unroll 2
     for (int t = 0; t < T; ++t) {
-      const uint32_t tb = nodes + (uint32_t)(t * NI * 4);
+      const uint32_t tb = nodes + (uint32_t)(t * NIP * 4);
       uint32_t r[NC];  // byte offset of the current node inside the tree: 4n
+      if constexpr (DEPTH >= 2) {
+        // levels 0 and 1 from ONE broadcast 16-byte load of nodes 0..3 (shared by all configs)
+        const uint4 q01 = *reinterpret_cast<const uint4*>(sb + tb);
 #pragma unroll
-      for (int q = 0; q < NC; ++q) r[q] = 0;
+        for (int q = 0; q < NC; ++q) {
+          const uint32_t v = ld32(col0 + (uint32_t)(q * D * kScoreThreads * 4) + (q01.x >> 16));
+          const bool right = v >= q01.x;
+          const uint32_t w = right ? q01.z : q01.y;
+          const uint32_t v1 = ld32(col0 + (uint32_t)(q * D * kScoreThreads * 4) + (w >> 16));
+          r[q] = (right ? 16u : 8u) + (v1 >= w ? 8u : 4u);  // 2 * (4n1) + 4|8 with n1 = 1|2
+        }
+      } else {
 #pragma unroll
-      for (int l = 0; l < DEPTH; ++l) {
+        for (int q = 0; q < NC; ++q) r[q] = 0;
+      }
+#pragma unroll
+      for (int l = DEPTH >= 2 ? 2 : 0; l < DEPTH; ++l) {
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
           const uint32_t w = ld32(tb + r[q]);
@@ -334,8 +351,9 @@ void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_id
   }
   const int ni = (1 << g->depth) - 1, nl = 1 << g->depth;
   const size_t tree_bytes = (size_t)g->num_trees * (ni * 4 + nl * 8);
-  if (g->d_inode_pk) {  // K1 fast path
-    const size_t smem = tree_bytes + 16 + (size_t)kScoreCfg * g->D * kScoreThreads * 4;
+  if (g->d_inode_pk) {  // K1 fast path (node words padded to a multiple of 4 per tree)
+    const size_t smem = (size_t)g->num_trees * (((ni + 3) & ~3) * 4 + nl * 8) + 16 +
+                        (size_t)kScoreCfg * g->D * kScoreThreads * 4;
     if (smem <= 200 * 1024) {
       const int per_sm = std::max(1, std::min(8, (int)((220 * 1024) / smem)));
       const int grid = (int)std::min<int64_t>(ceil_div(B, kScoreCfg * kScoreThreads), (int64_t)sm_count(ctx) * per_sm);
