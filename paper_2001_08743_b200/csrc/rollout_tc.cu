@@ -488,14 +488,8 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       }
       uint32_t raw[64];
       double gs = 0.0;
-      float ufs[NMAX];  // this step's counter-RNG draws, computed while the L1 MMA runs
+      float ufs[NMAX];  // this step's counter-RNG draws, computed while the L2 (K half 1) MMAs run
       if (lw) {
-#pragma unroll
-        for (int d = 0; d < NMAX; ++d) {
-          const uint64_t hsh = kt::mix64(tk.seed ^ kt::mix64((ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n +
-                                                             (uint64_t)d + 0x9E3779B97F4A7C15ULL));
-          ufs[d] = (float)(uint32_t)(hsh >> 40) * 0x1.0p-24f;  // |uf - u| < 2^-24
-        }
         if (tk.gnode) gs = gbt_walk(0.0, s_node, s_leaf, mycol, 0, gh, tk.depth);  // fused K1, row t
         kt::tc::mbar_wait(mb, ph);
         kt::tc::fence_after();
@@ -556,6 +550,12 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         kt::tc::commit(mb);
       }
       if (lw) {
+#pragma unroll
+        for (int d = 0; d < NMAX; ++d) {
+          const uint64_t hsh = kt::mix64(tk.seed ^ kt::mix64((ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n +
+                                                             (uint64_t)d + 0x9E3779B97F4A7C15ULL));
+          ufs[d] = (float)(uint32_t)(hsh >> 40) * 0x1.0p-24f;  // |uf - u| < 2^-24
+        }
         if (tk.gnode) {  // fused K1, row t: second half of the walk while the L2 MMAs run
           gs = gbt_walk(gs, s_node, s_leaf, mycol, gh, tk.ntrees, tk.depth);
           if (lr) tk.score[e * (int64_t)(T + 1) + t] = kt::dadd(tk.gbase, kt::dmul(tk.glr, gs));
