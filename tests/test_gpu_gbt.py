@@ -75,3 +75,34 @@ def test_predict_1m_device_resident(O, ctx):
     ctx.set_stream(None)
     sel = np.random.default_rng(0).choice(len(idx), 20_000, replace=False)
     assert np.array_equal(out.cpu().numpy()[sel], O.port_predict_idx(g, osp, idx[sel]))
+
+
+def _host_predict(pm, X):
+    """Plain restatement of predict_one (cost_model.cpp:117-124,179-187): sequential fp64."""
+    out = np.empty(len(X))
+    for r, x in enumerate(X):
+        s = 0.0
+        for t in range(pm.num_trees):
+            nd = int(pm.offsets[t])
+            while pm.feature[nd] >= 0:
+                nd = int(pm.offsets[t] + (pm.left[nd] if x[pm.feature[nd]] <= pm.threshold[nd] else pm.right[nd]))
+            s = s + float(pm.value[nd])
+        out[r] = pm.base_prediction + pm.learning_rate * s
+    return out
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3, 5, 8])
+def test_predict_idx_every_tree_depth(O, ctx, depth):
+    """K1 is compiled per complete-tree depth (levels 0-1 from one broadcast load
+    when depth >= 2): every depth agrees bit-for-bit with a host restatement."""
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt, GbtParams, fit_gbt
+    sp = SPACES["synthetic16"]()
+    osp = O.OSpace(sp)
+    tr = osp.random_valid(7, 1500)
+    y = np.nan_to_num(O.synthetic_fitness(osp, tr, seed=7))
+    pm = fit_gbt(osp.encode(tr), y, GbtParams(num_trees=12, max_depth=depth, min_samples_leaf=1), seed=7)
+    dg = DeviceGbt(pm, Space(sp, ctx))
+    q = random_idx(sp, 3000, 8)
+    want = _host_predict(pm, osp.encode(q))
+    assert np.array_equal(dg.predict_idx(q.astype(np.uint8)), want)
