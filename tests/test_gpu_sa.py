@@ -84,3 +84,27 @@ def test_sa_grouped_launch_equals_single_calls(O, ctx):
         assert np.array_equal(d["idx"].view(torch.int16).cpu().numpy().view(np.uint16), g["idx"])
         assert np.array_equal(d["score"].cpu().numpy(), g["score"])
         assert np.array_equal(d["accepted"].cpu().numpy(), g["accepted"])
+
+
+@pytest.mark.parametrize("depth,ntrees", [(2, 13), (6, 9), (1, 20)])
+def test_sa_every_tree_depth(O, ctx, depth, ntrees):
+    """K7's walk is compiled per tree depth and interleaves trees 8 at a time
+    (remainder trees walked singly): bit-exact with the oracle at other depths
+    and tree counts."""
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt, GbtModel
+    from paper_2001_08743_b200.exploration import SaParams, sa_search
+    from paper_2001_08743_b200.spaces import stream_seed
+    sp = SPACES["synthetic16"]()
+    osp = O.OSpace(sp)
+    g = O.fitted_model(osp, seed=depth, n_train=800, num_trees=ntrees, max_depth=depth)
+    pm = GbtModel(g.base, g.lr, g.num_features, g.offsets, g.feature, g.left, g.right, g.threshold, g.value)
+    ds = Space(sp, ctx)
+    E, T = 70, 30
+    seeds = osp.random_valid(3, E)
+    p = SaParams(num_chains=E, max_steps=T, initial_temperature=0.05, cooling_rate=0.95)
+    _, tr = sa_search(ds, DeviceGbt(pm, ds), seeds, p, rng_seed=depth)
+    want = O.sa_search(osp, g, seeds, T, 0, stream_seed(depth, "sa"), 0.05, 0.95)
+    assert np.array_equal(tr["idx"].astype(np.int32), want["idx"])
+    assert np.array_equal(tr["score"], want["score"])
+    assert np.array_equal(tr["accepted"], want["accepted"])
