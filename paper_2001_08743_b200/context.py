@@ -32,7 +32,7 @@ class Context:
 
     def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
         h = C.c_void_p()
-        if world > 1:
+        if world > 1 or nccl_id is not None:  # one-rank communicator: tests of the sharded paths
             buf = C.create_string_buffer(bytes(nccl_id), 128)
             L.check(L.lib().ktune_ctx_create_dist(device, rank, world, buf, C.byref(h)))
         else:

@@ -93,6 +93,7 @@ struct ktune_ctx {
   cudaStream_t copy_stream = nullptr;  // D2H of segmented rollouts, overlapping the compute
   std::string last_error;
   int64_t opt_force_exact = 0;
+  int64_t opt_force_sharded = 0;  // k-means: the NCCL-sharded path on one rank (tests)
   int64_t opt_kmeans_mode = 0;
   int64_t opt_profile = 0;
   int64_t opt_rollout_delta = 0;  // 1e-12 units, 0 = default

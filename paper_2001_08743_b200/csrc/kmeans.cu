@@ -1468,6 +1468,7 @@ struct KMeans {
   int32_t* csb;       // per-cluster segment bases [k+1]
   int32_t* seqcnt;    // segments summed sequentially (stat)
   int world = 1, rank = 0;
+  bool sharded = false;  // per-point state all-gathered over NCCL (world > 1, or forced for tests)
   int64_t shard_chunks = 0, cap = 0;
   double* tile_sum = nullptr;  // tcgen05 assign: per-128-point-tile loss partials
   bool use_tc = false;
@@ -1484,6 +1485,7 @@ struct KMeans {
     // per-point results are all-gathered so every rank holds the full state.
     world = ctx->world;
     rank = ctx->rank;
+    sharded = world > 1 || (ctx->opt_force_sharded && ctx->nccl);
     shard_chunks = kt::ceil_div(nchunks, world);
     cap = (int64_t)world * shard_chunks * kChunk;
     lut_smem = sizeof(double) * lut_total;
@@ -1583,14 +1585,14 @@ struct KMeans {
       } else {
         KT_CUDA(cudaMemsetAsync(dscal, 0, 8, s()));
       }
-      if (world > 1) {
+      if (sharded) {
         const int64_t S = shard_chunks * kChunk;
         kt::allgather(ctx, asg + rank * S, asg, sizeof(int32_t) * S);
         kt::allgather(ctx, dd + rank * S, dd, sizeof(double) * S);
         kt::allreduce_sum(ctx, ull, 1, false);
         kt::allreduce_sum(ctx, dscal, 1, true);
       }
-    } else if (world == 1) {
+    } else if (!sharded) {
       kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
       KT_DISPATCH_DM(D, assign_kernel<IdxT, DM_><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent,
                                                                                  k, prev, asg, dd, chunk, ull, 0));
@@ -1686,7 +1688,7 @@ struct KMeans {
     // Single-GPU iterations replay a captured CUDA graph (centroid update + assignment +
     // readback: ~20 launches): the loop is launch-bound at N = 1M. Two graphs, one per
     // parity of the a/b buffer swap.
-    const bool use_graph = world == 1 && !ctx->opt_profile;
+    const bool use_graph = !sharded && !ctx->opt_profile;
     cudaGraphExec_t gx[2] = {nullptr, nullptr};
     struct GraphGuard {
       cudaGraphExec_t* g;
@@ -1841,7 +1843,7 @@ struct KMeans {
     for (int r = 0; r < std::max(1, restarts); ++r) {
       std::vector<double> il;
       const uint64_t rs = kt::seed_combine(seed, (uint64_t)r);
-      const bool spec = world == 1 && !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1;
+      const bool spec = !sharded && !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1;
       if (!spec || !lloyd_cert(k, rs, max_iters, il)) {
         if (spec) ctx->stats[KTUNE_STAT_KMEANS_ABORTS] += 1;
         lloyd(k, rs, max_iters, il);

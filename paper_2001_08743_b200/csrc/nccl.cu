@@ -58,15 +58,15 @@ void kt_nccl_destroy(ktune_ctx* ctx) {
 }
 
 namespace kt {
-// In-place sum all-reduce on the context stream (no-op for world == 1).
+// In-place sum all-reduce on the context stream (no-op without a communicator).
 void allreduce_sum(ktune_ctx* ctx, void* buf, size_t count, bool is_double) {
-  if (ctx->world <= 1 || !ctx->nccl) return;
+  if (!ctx->nccl) return;
   nccl_check(api().AllReduce(buf, buf, count, is_double ? ncclFloat64 : ncclInt64, ncclSum,
                              (ncclComm_t)ctx->nccl, ctx->stream),
              "ncclAllReduce");
 }
 void allgather(ktune_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank) {
-  if (ctx->world <= 1 || !ctx->nccl) {
+  if (!ctx->nccl) {
     if (send != recv) KT_CUDA(cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, ctx->stream));
     return;
   }
@@ -106,7 +106,7 @@ int ktune_ctx_create_dist(int device, int rank, int world, const void* nccl_id, 
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    if (world > 1) {
+    if (world > 1 || nccl_id) {  // a one-rank communicator (nccl_id given) exercises the sharded paths
       if (!nccl_id) kt::fail(KTUNE_ERR_CONFIG, "world > 1 needs an ncclUniqueId");
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));

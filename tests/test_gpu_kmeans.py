@@ -191,3 +191,34 @@ def test_certified_lloyd_equals_exact_mode(O, ctx, name, n, k, seed):
     assert np.array_equal(a.centroids, b.centroids)
     assert a.l2_loss == b.l2_loss
     assert len(a.iteration_losses) == len(b.iteration_losses)
+
+
+@pytest.mark.parametrize("name,n,k,seed", [("alexnet_c3_u16", 20000, 8, 21), ("synthetic16", 12000, 30, 22)])
+def test_nccl_sharded_path_on_one_rank(O, ctx, ref_ok, name, n, k, seed):
+    """The multi-GPU k-means path (rank-local chunk assignment, NCCL all-gathers of
+    the per-point state, all-reduced counters) run through a one-rank NCCL
+    communicator on the real GPU: same clustering as the single-GPU path and as
+    the reference, the adaptive sweep too."""
+    import torch  # noqa: F401  (loads the bundled libnccl the library binds with dlopen)
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.context import Context
+    from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep, kmeans_run
+    sp = SPACES[name]()
+    osp = O.OSpace(sp)
+    cidx, cids, _ = candidate_set(O, osp, n, seed)
+    want = kmeans_run(_space(ctx, sp), cidx, k, seed, restarts=2)
+    dctx = Context(0, 0, 1, Context.nccl_unique_id())
+    dctx.set_option(L.OPT_FORCE_SHARDED, 1)
+    ds = _space(dctx, sp)
+    dctx.reset_stats()
+    got = kmeans_run(ds, cidx, k, seed, restarts=2)
+    assert dctx.stat(L.STAT_XS_SEGMENTS) > 0  # the sharded path (exact-order sums every iteration) ran
+    assert np.array_equal(got.assignments, want.assignments)
+    assert np.array_equal(got.centroids, want.centroids)
+    assert got.l2_loss == want.l2_loss
+    ref = O.kmeans_run(osp.encode(cidx), k, seed, restarts=2, impl="ref")
+    assert np.array_equal(got.assignments, ref["assignments"])
+    cs = CandidateSet(cidx, cids, np.zeros(len(cids)))
+    a = adaptive_sweep(ds, cs, SamplingParams(k_max_exclusive=12), 3)
+    b = adaptive_sweep(_space(ctx, sp), cs, SamplingParams(k_max_exclusive=12), 3)
+    assert a.k == b.k and a.k_losses == b.k_losses and np.array_equal(a.snapped, b.snapped)

@@ -32,7 +32,7 @@ dbuf = torch.empty(tot, dtype=torch.uint8, device="cuda"); hbuf = torch.empty(to
 for _ in range(2): hbuf.copy_(dbuf); torch.cuda.synchronize()
 t0 = time.perf_counter(); hbuf.copy_(dbuf); torch.cuda.synchronize(); dt = time.perf_counter() - t0
 print(f"raw D2H {tot/1e9:.2f} GB in {dt*1e3:.1f} ms = {tot/dt/1e9:.1f} GB/s")
-for S in [1, 2, 3, 4, 5, 6, 8]:
+for S in [int(x) for x in os.environ.get("SEGS", "1,2,3,4,5,6,8").split(",")]:
     ctx.set_option(L.OPT_ROLLOUT_SEGMENTS, S)
     run_episodes_batch(tasks, T, ctx, host_out=host_out)
     t0 = time.perf_counter()
