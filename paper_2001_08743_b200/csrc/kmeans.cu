@@ -1422,6 +1422,28 @@ __global__ void gather_readback_kernel(const double* dscal, const unsigned long 
   *seqcnt = 0;
 }
 
+// CUDA graph capture is illegal on the legacy default stream (a context bound to
+// torch's default stream); those runs take the uncaptured paths.
+inline bool capturable(cudaStream_t st) { return st != nullptr && st != cudaStreamLegacy; }
+
+// Ends an open stream capture if an error unwinds through it, so that a failed
+// capture does not leave the stream (and, in thread-local mode, the thread) capturing.
+struct CaptureGuard {
+  cudaStream_t s;
+  bool open = true;
+  void end(cudaGraph_t* g) {
+    open = false;
+    KT_CUDA(cudaStreamEndCapture(s, g));
+  }
+  ~CaptureGuard() {
+    if (!open) return;
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+  }
+};
+
 template <class IdxT>
 struct KMeans {
   ktune_ctx* ctx;
@@ -1688,7 +1710,8 @@ struct KMeans {
     // Single-GPU iterations replay a captured CUDA graph (centroid update + assignment +
     // readback: ~20 launches): the loop is launch-bound at N = 1M. Two graphs, one per
     // parity of the a/b buffer swap.
-    const bool use_graph = !sharded && !ctx->opt_profile;
+    // no graphs on the legacy default stream (capture is illegal there) or while profiling
+    const bool use_graph = !sharded && !ctx->opt_profile && capturable(s());
     cudaGraphExec_t gx[2] = {nullptr, nullptr};
     struct GraphGuard {
       cudaGraphExec_t* g;
@@ -1704,9 +1727,10 @@ struct KMeans {
         if (!g) {
           cudaGraph_t graph;
           KT_CUDA(cudaStreamBeginCapture(s(), cudaStreamCaptureModeThreadLocal));
+          CaptureGuard cg{s()};
           update_centroids(k, asg_a, d2_a, cent_b);
           enqueue_assign(cent_b, k, asg_a, asg_b, d2_b);
-          KT_CUDA(cudaStreamEndCapture(s(), &graph));
+          cg.end(&graph);
           KT_CUDA(cudaGraphInstantiate(&g, graph, 0));
           cudaGraphDestroy(graph);
         }
@@ -1784,8 +1808,9 @@ struct KMeans {
         if (!g) {
           cudaGraph_t graph;
           KT_CUDA(cudaStreamBeginCapture(s(), cudaStreamCaptureModeThreadLocal));
+          CaptureGuard cg{s()};
           enqueue_iter();
-          KT_CUDA(cudaStreamEndCapture(s(), &graph));
+          cg.end(&graph);
           KT_CUDA(cudaGraphInstantiate(&g, graph, 0));
           cudaGraphDestroy(graph);
         }
@@ -1843,7 +1868,7 @@ struct KMeans {
     for (int r = 0; r < std::max(1, restarts); ++r) {
       std::vector<double> il;
       const uint64_t rs = kt::seed_combine(seed, (uint64_t)r);
-      const bool spec = !sharded && !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1;
+      const bool spec = !sharded && !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1 && capturable(ctx->stream);
       if (!spec || !lloyd_cert(k, rs, max_iters, il)) {
         if (spec) ctx->stats[KTUNE_STAT_KMEANS_ABORTS] += 1;
         lloyd(k, rs, max_iters, il);

@@ -138,26 +138,37 @@ class SweepResult:
 
 def adaptive_sweep(space: Space, cands: CandidateSet, params: SamplingParams = SamplingParams(),
                    rng_seed: int = 0) -> SweepResult:
-    """The k-sweep of adaptive_sample (sampling.cpp:436-446) + snap (:448-452), on the GPU."""
-    arr, _ = _packed(space, cands.idx)
-    ids = np.ascontiguousarray(cands.ids, np.uint64)
-    N = len(ids)
+    """The k-sweep of adaptive_sample (sampling.cpp:436-446) + snap (:448-452), on the GPU.
+
+    Host arrays, or a device-resident candidate set (CUDA tensors: idx N x D in the
+    space's index width, ids uint64): then centroids, assignments and the snapped
+    configurations come back as CUDA tensors and nothing crosses PCIe but the
+    per-k scalars."""
+    arr, dev = _packed(space, cands.idx)
     kmax = max(1, params.k_max_exclusive)
     k = C.c_int32()
-    cen = np.zeros((kmax, space.D))
-    asg = np.zeros(N, np.int32)
     loss = C.c_double()
     kl = np.zeros(kmax)
     nk = C.c_int32()
-    snap = np.zeros((kmax, space.D), np.int32)
-    out = L.SweepOutC(C.cast(C.pointer(k), C.c_void_p), cen.ctypes.data_as(C.c_void_p),
-                      asg.ctypes.data_as(C.c_void_p), C.cast(C.pointer(loss), C.c_void_p),
-                      kl.ctypes.data_as(C.c_void_p), C.cast(C.pointer(nk), C.c_void_p),
-                      snap.ctypes.data_as(C.c_void_p))
+    if dev:
+        import torch
+        ids = cands.ids
+        N = ids.numel()
+        mk = lambda shape, dt: torch.empty(shape, dtype=dt, device=arr.device)
+        cen, asg, snap = mk((kmax, space.D), torch.float64), mk((N,), torch.int32), mk((kmax, space.D), torch.int32)
+        ptr = lambda t: C.c_void_p(t.data_ptr())
+        idx_p, ids_p = ptr(arr), ptr(ids)
+    else:
+        ids = np.ascontiguousarray(cands.ids, np.uint64)
+        N = len(ids)
+        cen, asg, snap = np.zeros((kmax, space.D)), np.zeros(N, np.int32), np.zeros((kmax, space.D), np.int32)
+        ptr = lambda a: a.ctypes.data_as(C.c_void_p)
+        idx_p, ids_p = ptr(arr), ptr(ids)
+    out = L.SweepOutC(C.cast(C.pointer(k), C.c_void_p), ptr(cen), ptr(asg), C.cast(C.pointer(loss), C.c_void_p),
+                      kl.ctypes.data_as(C.c_void_p), C.cast(C.pointer(nk), C.c_void_p), ptr(snap))
     pc = params.c()
-    space.ctx.check(L.lib().ktune_adaptive_sweep(space.ctx.h, space.h, arr.ctypes.data_as(C.c_void_p),
-                                                 space.index_bytes, ids.ctypes.data_as(C.c_void_p), N,
-                                                 C.byref(pc), rng_seed, C.byref(out), 0))
+    space.ctx.check(L.lib().ktune_adaptive_sweep(space.ctx.h, space.h, idx_p, space.index_bytes, ids_p, N,
+                                                 C.byref(pc), rng_seed, C.byref(out), L.F_DEVICE if dev else 0))
     kk = k.value
     return SweepResult(kk, cen[:kk], asg, loss.value, list(kl[:nk.value]), snap[:kk])
 

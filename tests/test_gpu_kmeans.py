@@ -222,3 +222,30 @@ def test_nccl_sharded_path_on_one_rank(O, ctx, ref_ok, name, n, k, seed):
     a = adaptive_sweep(ds, cs, SamplingParams(k_max_exclusive=12), 3)
     b = adaptive_sweep(_space(ctx, sp), cs, SamplingParams(k_max_exclusive=12), 3)
     assert a.k == b.k and a.k_losses == b.k_losses and np.array_equal(a.snapped, b.snapped)
+
+
+@pytest.mark.parametrize("name,n", [("resnet_c2", 6000), ("alexnet_c3_u16", 5000)])
+def test_adaptive_sweep_device_resident(O, ctx, name, n):
+    """A candidate set already on the GPU (CUDA tensors) sweeps to the same k,
+    losses, assignments and snapped configurations as the host call."""
+    import torch
+    from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep
+    sp = SPACES[name]()
+    osp = O.OSpace(sp)
+    cidx, cids, _ = candidate_set(O, osp, n, 31)
+    ds = _space(ctx, sp)
+    p = SamplingParams(k_max_exclusive=14)
+    host = adaptive_sweep(ds, CandidateSet(cidx, cids, np.zeros(len(cids))), p, 9)
+    narrow = np.ascontiguousarray(cidx, ds.idx_dtype)
+    didx = torch.from_numpy(narrow.view(np.int16) if narrow.dtype == np.uint16 else narrow).cuda()
+    dids = torch.from_numpy(cids.view(np.int64)).cuda()
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    try:
+        dev = adaptive_sweep(ds, CandidateSet(didx, dids, None), p, 9)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_stream(None)
+    assert dev.k == host.k and dev.k_losses == host.k_losses and dev.l2_loss == host.l2_loss
+    assert np.array_equal(dev.assignments.cpu().numpy(), host.assignments)
+    assert np.array_equal(dev.centroids.cpu().numpy(), host.centroids)
+    assert np.array_equal(dev.snapped.cpu().numpy(), host.snapped)
