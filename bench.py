@@ -191,6 +191,53 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def c3_pipeline(ctx, args):
+    """SURVEY C3 as one Chameleon iteration on the device: VGG-16 conv layer, 65,536
+    explorer episodes x T = 500 (tcgen05 rollout + K1 scoring), the CandidateSet of
+    every visited configuration (device make_candidate_set), then Adaptive Sampling's
+    k-sweep + snap over that candidate set, all device-resident; stage times."""
+    import torch
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
+    from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
+    from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep, candidates_from_rows
+    from paper_2001_08743_b200.workloads import encode, make_tasks
+    sp = S.vgg16_tasks()[3]
+    spec = make_tasks([sp], args.c3_episodes, seed=args.seed + 33)[0]
+    ds = Space(sp, ctx)
+    g = DeviceGbt(fit_gbt(encode(sp, spec.train_idx), spec.train_y, seed=spec.seed), ds)
+    agent = ActorCritic(sp.num_knobs, 128, 64, seed=spec.seed, ctx=ctx)
+    init = torch.from_numpy(spec.init_idx.astype(np.uint16).view(np.int16)).cuda()
+    T, D = args.c3_T, sp.num_knobs
+    task = RolloutTask(ds, agent, g, init.view(torch.uint16), 0, spec.seed)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    run_episodes_batch([task], 8, ctx, device_out=True)  # warm-up
+    times = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    o = run_episodes_batch([task], T, ctx, device_out=True)[0]
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    rows, ids = candidates_from_rows(ds, o["idx"].view(-1, D), o["score"].view(-1))
+    cidx = o["idx"].view(torch.int16).view(-1, D)[rows]
+    cidx = cidx.to(torch.uint8) if ds.index_bytes == 1 else cidx
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    sw = adaptive_sweep(ds, CandidateSet(cidx, ids.view(torch.int64), None), SamplingParams(), spec.seed)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    ctx.set_stream(None)
+    steps = args.c3_episodes * T
+    return {"workload": f"SURVEY C3: VGG-16 layer {sp.workload} (D={D}), {args.c3_episodes} episodes x {T} steps, "
+                        f"then Adaptive Sampling over every visited configuration; 1 GPU, device-resident",
+            "rollout_ms": 1e3 * (t1 - t0), "config_steps_per_s": steps / (t1 - t0),
+            "candidates": int(rows.numel()), "candidate_set_ms": 1e3 * (t2 - t1),
+            "adaptive_sweep_ms": 1e3 * (t3 - t2), "sweep_k": sw.k, "sweep_k_losses": len(sw.k_losses),
+            "total_ms": 1e3 * (t3 - t0)}
+
+
 def kmeans_secondary(ctx, args, cpu=True):
     """k-means sampling ms/iter (BASELINE metric 2): AlexNet conv2 space (uint16
     knob indices), 1M deduplicated candidates, k=8, exact Lloyd iterations; plus
@@ -365,6 +412,8 @@ def main():
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size tcgen05 vs exact comparison")
     ap.add_argument("--no-sa", action="store_true", help="skip the simulated-annealing baseline measurement")
     ap.add_argument("--no-cand", action="store_true", help="skip the device make_candidate_set measurement")
+    ap.add_argument("--c3-episodes", type=int, default=65536, help="SURVEY C3 pipeline episodes (0 = skip)")
+    ap.add_argument("--c3-T", type=int, default=500)
     ap.add_argument("--no-full-sweep", action="store_true", help="skip the forced k = 8..63 k-means sweep (SURVEY C4)")
     ap.add_argument("--kmeans-dist", action="store_true", help="N > 1: also run the NCCL-sharded k-means secondary")
     ap.add_argument("--c5", type=int, default=1, help="run the SURVEY C5 scale workload (1M x 1000, 1 step)")
@@ -591,6 +640,13 @@ def main():
         except Exception as ex:  # reported, not hidden
             scale = {"error": repr(ex)}
 
+    c3 = None
+    if args.c3_episodes and world == 1:
+        try:
+            c3 = c3_pipeline(ctx, args)
+        except Exception as ex:  # reported, not hidden
+            c3 = {"error": repr(ex)}
+
     kmeans = None
     if not args.no_kmeans and (world == 1 or args.kmeans_dist):
         # N > 1: every rank would join the sharded assignment's NCCL all-gathers; that path is
@@ -652,6 +708,7 @@ def main():
             "parity_full_size": parity,
             "secondary": kmeans,
             "scale_c5": scale,
+            "pipeline_c3": c3,
             "sa_baseline": sa,
             "candidates": cand,
         }

@@ -765,7 +765,8 @@ void resolve_counters(ktune_ctx* ctx) {
       std::max<int64_t>(ctx->stats[KTUNE_STAT_ROLLOUT_MAXERR], (int64_t)std::llround((double)mx * 1e12));
 }
 
-void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end) {
+static void rollout_tc_launch(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end,
+                              bool allow_fuse) {
   if (!ctx->d_counters) {
     KT_CUDA(cudaMalloc(&ctx->d_counters, (4 + 8 * 16) * sizeof(unsigned long long)));
     KT_CUDA(cudaMemsetAsync(ctx->d_counters, 0, (4 + 8 * 16) * sizeof(unsigned long long), ctx->stream));
@@ -844,7 +845,7 @@ void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_beg
       const ktune_gbt* g = rw.gbt;
       tk.gnode = nullptr;
       if (g && rw.score && g->has_space && g->complete && g->d_inode_idx && g->depth <= 8 && t_begin == 0 && t_end == T &&
-          tc_smem_bytes(n, g->num_trees, g->depth) <= 227 * 1024 && ctx->opt_rollout_fuse_gbt) {
+          tc_smem_bytes(n, g->num_trees, g->depth) <= 227 * 1024 && ctx->opt_rollout_fuse_gbt && allow_fuse) {
         tk.gnode = g->d_inode_idx;
         tk.gleaf = g->d_leaf;
         tk.ntrees = g->num_trees;
@@ -872,6 +873,46 @@ void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_beg
     kern<<<(unsigned)ctas, kThr, smem, ctx->stream>>>(L);
     check_launch(ctx, "rollout_tc");
   }
+}
+
+// Episodes [e, E) of a workload as a workload of its own (global ids, pointers advanced).
+static RolloutWork episode_tail(const RolloutWork& w, int64_t e, int T) {
+  RolloutWork t = w;
+  const int64_t n = w.ac->n;
+  t.E = w.E - e;
+  t.episode_offset = w.episode_offset + e;
+  t.init_idx = w.init_idx + e * n;
+  t.idx = w.idx + e * (T + 1) * n;
+  if (w.actions) t.actions = w.actions + e * T * n;
+  if (w.logp) t.logp = w.logp + e * T;
+  if (w.value) t.value = w.value + e * T;
+  if (w.logp32) t.logp32 = w.logp32 + e * T;
+  if (w.value32) t.value32 = w.value32 + e * T;
+  if (w.score) t.score = w.score + e * (T + 1);
+  t.scored = false;
+  return t;
+}
+
+void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end) {
+  // A tile of episodes is bound to its slot for all T steps, so a workload larger than one
+  // resident wave (kMaxWarps warps on every SM) would end with a part-filled wave running
+  // at the full per-step latency. One workload: full waves, then the remainder spread thin
+  // over every SM (e.g. 65,536 episodes = 1.15 waves).
+  const int64_t cap = (int64_t)kMaxWarps * sm_count(ctx);
+  if (work.size() != 1 || ceil_div(work[0].E, 32) <= cap) {
+    rollout_tc_launch(ctx, work, T, t_begin, t_end, true);
+    return;
+  }
+  RolloutWork rest = work[0];
+  while (ceil_div(rest.E, 32) > cap) {
+    std::vector<RolloutWork> wave(1, rest);
+    wave[0].E = cap * 32;
+    rollout_tc_launch(ctx, wave, T, t_begin, t_end, false);
+    rest = episode_tail(rest, cap * 32, T);
+  }
+  std::vector<RolloutWork> last(1, rest);
+  rollout_tc_launch(ctx, last, T, t_begin, t_end, false);
+  work[0].scored = false;
 }
 
 }  // namespace kt

@@ -148,6 +148,23 @@ def test_rollout_tc_equals_exact_kernel_at_scale(O, ctx):
     assert nfb < 0.01 * steps
 
 
+@pytest.mark.parametrize("E", [60_001, 2 * 56_832 + 97])
+def test_rollout_more_episodes_than_one_wave(O, ctx, E):
+    """A workload larger than one resident wave (12 warps on every SM) runs as full
+    waves plus a thin remainder over every SM: the same trajectories as the exact
+    kernel, episodes keyed by their global id across the wave boundary."""
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    sp, osp, og, dspace, dg, agent = _setup(O, ctx, "synthetic8", seed=4)
+    init = np.random.default_rng(E).integers(0, 2, (E, sp.num_knobs))
+    task = RolloutTask(dspace, agent, dg, init, episode_offset=5, root_seed=4)
+    fast = run_episodes_batch([task], 6)[0]
+    exact = run_episodes_batch([task], 6, exact=True)[0]
+    assert np.array_equal(fast["idx"], exact["idx"])
+    assert np.array_equal(fast["actions"], exact["actions"])
+    assert np.array_equal(fast["score"], exact["score"])
+    assert _close(fast["logp"], exact["logp"]) and _close(fast["value"], exact["value"])
+
+
 def test_rollout_tc_certificate_check_mode(O, ctx):
     """Check mode re-decides every knob exactly: certified fast decisions never
     disagree, and the fast probabilities stay well inside the margin."""
