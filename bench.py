@@ -211,7 +211,8 @@ def c3_pipeline(ctx, args):
     init = torch.from_numpy(spec.init_idx.astype(np.uint16).view(np.int16)).cuda()
     T, D = args.c3_T, sp.num_knobs
     task = RolloutTask(ds, agent, g, init.view(torch.uint16), 0, spec.seed)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     run_episodes_batch([task], 8, ctx, device_out=True)  # warm-up
     times = {}
@@ -229,6 +230,7 @@ def c3_pipeline(ctx, args):
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     ctx.set_stream(None)
+    torch.cuda.set_stream(torch.cuda.default_stream())
     steps = args.c3_episodes * T
     return {"workload": f"SURVEY C3: VGG-16 layer {sp.workload} (D={D}), {args.c3_episodes} episodes x {T} steps, "
                         f"then Adaptive Sampling over every visited configuration; 1 GPU, device-resident",

@@ -122,8 +122,9 @@ __device__ const double* stage_lut(const KtSpaceParams& sp, double* s_lut, int l
 struct KppState {
   uint64_t rng;
   int64_t pick;
-  int32_t fallbacks;
-  int32_t pad;
+  int32_t fallbacks;   // picks decided by the exact parallel replay (kpp_x_* kernels)
+  int32_t need_exact;  // set by kpp_select when the certified decision is undecided
+  uint64_t rng_fb;     // generator state the exact replay starts from
 };
 
 // d2[i] = (first ? v : min(d2[i], v)), v = |p_i - centroid c|^2, plus chunk sums.
@@ -167,55 +168,6 @@ __global__ void __launch_bounds__(kBT) kpp_d2_kernel(KtSpaceParams sp, int lut_t
 
 __device__ __forceinline__ double gamma_bound(double terms) { return terms * kU * 1.0625; }
 
-// Exact reference order for the kmeans++ total (Eigen contiguous sum, A.3) and
-// cumulative scan (sampling.cpp:74-88). Run by thread 0..3 of one block.
-__device__ void kpp_exact(const double* __restrict__ d2, int64_t N, uint64_t& rng, double* lanes,
-                          int64_t* pick_out) {
-  const int t = threadIdx.x;
-  const int64_t aligned2 = (N / 4) * 4, aligned = (N / 2) * 2;
-  if (t < 4 && aligned > 2) {
-    double s = d2[t];
-    for (int64_t i = 4 + t; i < aligned2; i += 4) s = kt::dadd(s, d2[i]);
-    lanes[t] = s;
-  }
-  __syncthreads();
-  if (t == 0) {
-    double total;
-    if (aligned == 0) {
-      total = d2[0];
-      for (int64_t i = 1; i < N; ++i) total = kt::dadd(total, d2[i]);
-    } else {
-      double a0 = d2[0], a1 = d2[1];
-      if (aligned > 2) {
-        a0 = kt::dadd(lanes[0], lanes[2]);
-        a1 = kt::dadd(lanes[1], lanes[3]);
-        if (aligned > aligned2) {
-          a0 = kt::dadd(a0, d2[aligned2]);
-          a1 = kt::dadd(a1, d2[aligned2 + 1]);
-        }
-      }
-      total = kt::dadd(a0, a1);
-      for (int64_t i = aligned; i < N; ++i) total = kt::dadd(total, d2[i]);
-    }
-    int64_t pick;
-    if (total <= 0.0) {
-      pick = (int64_t)kt::rng_below(rng, (uint64_t)N);
-    } else {
-      const double r = kt::dmul(kt::rng_uniform01(rng), total);
-      double cum = 0.0;
-      pick = N - 1;
-      for (int64_t i = 0; i < N; ++i) {
-        cum = kt::dadd(cum, d2[i]);
-        if (cum > r) {
-          pick = i;
-          break;
-        }
-      }
-    }
-    *pick_out = pick;
-  }
-  __syncthreads();
-}
 
 // One CTA of 1024 threads: decide the next kmeans++ pick.
 // mode 0: first pick (below(N)); mode 1: D^2 sampling; force_exact: always chain.
@@ -225,12 +177,10 @@ __global__ void __launch_bounds__(1024) kpp_select_kernel(const double* __restri
                                                           int force_exact,
                                                           double* __restrict__ scratch) {
   __shared__ double red[32];
-  __shared__ double lanes[4];
   __shared__ double sh_u, sh_tot;
   __shared__ int sh_branch;  // 0 below, 1 sample
   __shared__ unsigned long long sh_ib, sh_ia;
   __shared__ int sh_bfirst, sh_bsecond;
-  __shared__ int64_t sh_pick;
   const int tid = threadIdx.x;
   uint64_t rng = st->rng;
   if (mode == 0) {
@@ -260,12 +210,10 @@ __global__ void __launch_bounds__(1024) kpp_select_kernel(const double* __restri
     }
   }
   __syncthreads();
-  if (force_exact) {
-    kpp_exact(d2, N, rng, lanes, &sh_pick);
+  if (force_exact) {  // the exact replay decides (kpp_x_* kernels, launched next)
     if (tid == 0) {
-      st->pick = sh_pick;
-      st->rng = rng;
-      st->fallbacks += 1;
+      st->need_exact = 1;
+      st->rng_fb = rng;
     }
     return;
   }
@@ -347,15 +295,11 @@ __global__ void __launch_bounds__(1024) kpp_select_kernel(const double* __restri
     if (tid == 0) st->pick = pick;
     return;
   }
-  // exact fallback: re-run the reference order (rng state rewound to before
-  // the uniform01 draw: the branch is identical, the draw is repeated).
-  uint64_t r0 = st[0].rng;  // already advanced by one draw
-  r0 -= 0x9E3779B97F4A7C15ULL;
-  kpp_exact(d2, N, r0, lanes, &sh_pick);
+  // undecided: the exact parallel replay of the reference order decides (kpp_x_*
+  // kernels, launched next), from the rng state rewound to before the uniform01 draw
   if (tid == 0) {
-    st->pick = sh_pick;
-    st->rng = r0;
-    st->fallbacks += 1;
+    st->need_exact = 1;
+    st->rng_fb = st->rng - 0x9E3779B97F4A7C15ULL;  // the branch is identical, the draw is repeated
   }
 }
 
@@ -1097,6 +1041,183 @@ __device__ __forceinline__ double warp_compose(At at, MapAt map_at, int nseg, in
   return s;
 }
 
+// ---- kmeans++ exact replay (sampling.cpp:65-96), in parallel. Taken when the
+// certified pick is undecided (more likely at tens of millions of points, where the
+// rigorous bound of the parallel prefix grows like N u) or when forced. The reference
+// draws r = uniform01 * total with total = d2.sum() in Eigen's 4-lane order
+// (eigen_shim: lane v sums d2[v + 4j] sequentially, then (l0 + l2) + (l1 + l3), tail),
+// and picks the first i whose SEQUENTIAL cum exceeds r. Views 0..3 are the four
+// strided lanes, view 4 the natural order; each is summed exactly with the segment
+// maps of exactsum.cuh (approximate prefix -> binade -> maps -> warp composition).
+constexpr int kKppViews = 5;
+struct KppView {
+  const double* x;
+  int64_t off, stride, n;
+  __device__ double operator()(int64_t i) const { return x[off + stride * i]; }
+};
+__device__ __forceinline__ KppView kpp_view(const double* d2, int64_t N, int v) {
+  return v < 4 ? KppView{d2, v, 4, N >= 4 ? N / 4 : 0} : KppView{d2, 0, 1, N};
+}
+
+__global__ void kpp_x_partial_kernel(const double* __restrict__ d2, int64_t N, int64_t S, const KppState* st,
+                                     double* __restrict__ approx) {
+  if (!st->need_exact) return;
+  const KppView x = kpp_view(d2, N, blockIdx.y);
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t lo = g * kt::xsum::kSeg;
+  if (lo >= x.n) return;
+  const int64_t hi = min(x.n, lo + kt::xsum::kSeg);
+  double s = 0.0;
+  for (int64_t i = lo; i < hi; ++i) s = kt::dadd(s, x(i));
+  approx[blockIdx.y * S + g] = s;
+}
+
+__global__ void kpp_x_prefix_kernel(int64_t N, int64_t S, const KppState* st, double* __restrict__ approx) {
+  if (!st->need_exact) return;
+  const int v = threadIdx.x >> 5;
+  if (v >= kKppViews) return;
+  const int64_t n = v < 4 ? (N >= 4 ? N / 4 : 0) : N;
+  warp_exclusive_scan(approx + v * S, (n + kt::xsum::kSeg - 1) / kt::xsum::kSeg, 1);
+}
+
+__global__ void kpp_x_map_kernel(const double* __restrict__ d2, int64_t N, int64_t S, const KppState* st,
+                                 const double* __restrict__ prefix, kt::xsum::SegMap* __restrict__ maps) {
+  if (!st->need_exact) return;
+  const KppView x = kpp_view(d2, N, blockIdx.y);
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t lo = g * kt::xsum::kSeg;
+  if (lo >= x.n) return;
+  const int len = (int)(min(x.n, lo + kt::xsum::kSeg) - lo);
+  auto at = [&](int i) { return x(lo + i); };
+  const double p = prefix[blockIdx.y * S + g];
+  maps[blockIdx.y * S + g] = p > 0.0 ? kt::xsum::segment_map(at, len, kt::xsum::binade_of(p))
+                                     : kt::xsum::zero_segment_map(at, len);
+}
+
+// 4 warps: the exact lane sums -> total -> r; then warp 0 walks the natural-order
+// composition batch by batch and, in the batch where the exact running sum first
+// exceeds r, segment by segment, then element by element.
+__global__ void __launch_bounds__(128) kpp_x_pick_kernel(const double* __restrict__ d2, int64_t N, int64_t S,
+                                                         KppState* st, const kt::xsum::SegMap* __restrict__ maps) {
+  __shared__ double lanes[4];
+  __shared__ double sh_r;
+  __shared__ int sh_case;  // 0: below(N) already picked, 1: search cum > r
+  if (!st->need_exact) return;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    const KppView x = kpp_view(d2, N, w);
+    const int64_t nseg = (x.n + kt::xsum::kSeg - 1) / kt::xsum::kSeg;
+    int nseq = 0;
+    const double s = x.n > 0 ? warp_compose([&](int i) { return x(i); }, [&](int g) { return maps[w * S + g]; },
+                                            (int)nseg, (int)x.n, &nseq)
+                             : 0.0;
+    if (lane == 0) lanes[w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // Eigen's vectorised sum (the shim's pinned order, see oracle/eigen_shim/Eigen/Core)
+    const int64_t aligned2 = (N / 4) * 4, aligned = (N / 2) * 2;
+    double total;
+    if (aligned == 0) {
+      total = d2[0];
+      for (int64_t i = 1; i < N; ++i) total = kt::dadd(total, d2[i]);
+    } else {
+      double a0 = d2[0], a1 = d2[1];
+      if (aligned > 2) {
+        a0 = kt::dadd(lanes[0], lanes[2]);
+        a1 = kt::dadd(lanes[1], lanes[3]);
+        if (aligned > aligned2) {
+          a0 = kt::dadd(a0, d2[aligned2]);
+          a1 = kt::dadd(a1, d2[aligned2 + 1]);
+        }
+      }
+      total = kt::dadd(a0, a1);
+      for (int64_t i = aligned; i < N; ++i) total = kt::dadd(total, d2[i]);
+    }
+    uint64_t rng = st->rng_fb;
+    if (total <= 0.0) {
+      st->pick = (int64_t)kt::rng_below(rng, (uint64_t)N);
+      sh_case = 0;
+    } else {
+      sh_r = kt::dmul(kt::rng_uniform01(rng), total);
+      sh_case = 1;
+    }
+    st->rng = rng;
+    st->fallbacks += 1;
+  }
+  __syncthreads();
+  if (w != 0 || sh_case == 0) {
+    if (threadIdx.x == 0) st->need_exact = 0;
+    return;
+  }
+  const double r = sh_r;
+  const KppView x = kpp_view(d2, N, 4);
+  const kt::xsum::SegMap* m4 = maps + 4 * S;
+  const int nseg = (int)((N + kt::xsum::kSeg - 1) / kt::xsum::kSeg);
+  double s = 0.0;  // cum = 0.0, then += in order
+  int64_t pick = N - 1;
+  bool found = false;
+  for (int g0 = 0; g0 < nseg && !found; g0 += 32) {
+    const int mcount = min(32, nseg - g0);
+    kt::xsum::SegMap mine{0, 0, 0, 2};
+    if (lane < mcount) mine = m4[g0 + lane];
+    // whole batch at once when every map is valid in one binade and the batch ends <= r
+    const unsigned real = __ballot_sync(0xffffffff, lane < mcount && mine.ok != 2);
+    if (real == 0) continue;  // all-zero segments: cum unchanged
+    const int e0 = __shfl_sync(0xffffffff, mine.e, __ffs(real) - 1);
+    const bool uniform = __all_sync(0xffffffff, lane >= mcount || mine.ok == 2 || (mine.ok == 1 && mine.e == e0));
+    if (uniform && s > 0.0) {
+      uint64_t c0 = mine.ok == 2 ? 0 : mine.F0, c1 = mine.ok == 2 ? 0 : mine.F1;
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t p0 = __shfl_up_sync(0xffffffff, c0, off);
+        const uint64_t p1 = __shfl_up_sync(0xffffffff, c1, off);
+        if (lane >= off) {
+          const uint64_t n0 = p0 + ((p0 & 1u) ? c1 : c0);
+          const uint64_t n1 = p1 + (((1u + p1) & 1u) ? c1 : c0);
+          c0 = n0;
+          c1 = n1;
+        }
+      }
+      kt::xsum::SegMap all;
+      all.F0 = __shfl_sync(0xffffffff, c0, mcount - 1);
+      all.F1 = __shfl_sync(0xffffffff, c1, mcount - 1);
+      all.e = e0;
+      all.ok = all.F0 < (1ull << 53) && all.F1 < (1ull << 53);
+      double s_end = s;
+      if (kt::xsum::apply_map(s_end, all) && !(s_end > r)) {
+        s = s_end;
+        continue;
+      }
+    }
+    for (int q = 0; q < mcount && !found; ++q) {
+      kt::xsum::SegMap m;
+      m.F0 = __shfl_sync(0xffffffff, mine.F0, q);
+      m.F1 = __shfl_sync(0xffffffff, mine.F1, q);
+      m.e = __shfl_sync(0xffffffff, mine.e, q);
+      m.ok = __shfl_sync(0xffffffff, mine.ok, q);
+      const int lo = (g0 + q) * kt::xsum::kSeg, hi = (int)(N < (int64_t)lo + kt::xsum::kSeg ? N : (int64_t)lo + kt::xsum::kSeg);
+      double s_next = s;
+      if (!kt::xsum::apply_map(s_next, m)) s_next = warp_seq_segment(s, [&](int i) { return x(i); }, lo, hi);
+      if (s_next > r) {  // the first i with cum > r lies in this segment
+        double c = s;
+        for (int i = lo; i < hi; ++i) {
+          c = kt::dadd(c, x(i));
+          if (c > r) {
+            pick = i;
+            break;
+          }
+        }
+        found = true;
+      }
+      s = s_next;
+    }
+  }
+  if (lane == 0) {
+    st->pick = pick;
+    st->need_exact = 0;
+  }
+}
+
 // warp per (cluster c, knob d): compose the segment maps from s = 0 exactly;
 // centroid = s / count (sampling.cpp:110-121).
 template <class IdxT>
@@ -1561,7 +1682,7 @@ struct KMeans {
   int grid_pts() const { return (int)nchunks; }
 
   void kmeanspp(int k, uint64_t rng_seed) {
-    KppState h{rng_seed, 0, 0, 0};
+    KppState h{rng_seed, 0, 0, 0, 0};
     KT_CUDA(cudaMemcpyAsync(kst, &h, sizeof(h), cudaMemcpyHostToDevice, s()));
     kpp_select_kernel<<<1, 1024, 0, s()>>>(d2, chunk, N, kst, 0, 0, scratch);
     kt::check_launch(ctx, "kpp_select");
@@ -1572,7 +1693,16 @@ struct KMeans {
       kt::check_launch(ctx, "kpp_d2");
       if (c + 1 < k) {
         kpp_select_kernel<<<1, 1024, 0, s()>>>(d2, chunk, N, kst, 1, (int)ctx->opt_force_exact, scratch);
-        kt::check_launch(ctx, "kpp_select");
+        // exact replay, a no-op unless kpp_select left the pick undecided
+        const int64_t S = kt::ceil_div(N, kt::xsum::kSeg);
+        double* xa = (double*)ctx->dev(kt::WS_KPP_X, (sizeof(double) + sizeof(kt::xsum::SegMap)) * kKppViews * S);
+        kt::xsum::SegMap* xm = reinterpret_cast<kt::xsum::SegMap*>(xa + kKppViews * S);
+        const dim3 gv((unsigned)kt::ceil_div(S, 128), kKppViews);
+        kpp_x_partial_kernel<<<gv, 128, 0, s()>>>(d2, N, S, kst, xa);
+        kpp_x_prefix_kernel<<<1, 32 * kKppViews, 0, s()>>>(N, S, kst, xa);
+        kpp_x_map_kernel<<<gv, 128, 0, s()>>>(d2, N, S, kst, xa, xm);
+        kpp_x_pick_kernel<<<1, 128, 0, s()>>>(d2, N, S, kst, xm);
+        kt::check_launch(ctx, "kpp_select", 5);
         ctx->stats[KTUNE_STAT_KPP_PICKS] += 1;
       }
     }
@@ -1796,6 +1926,7 @@ struct KMeans {
     };
     int iters = 0;
     bool done = false;
+    const bool graphs = capturable(s());  // legacy default stream: the same work, uncaptured
     for (int it0 = 0; it0 < max_iters && !done; it0 += kCertBatch) {
       const int nb = std::min(kCertBatch, max_iters - it0);
       KT_CUDA(cudaMemsetAsync(rb_slot, 0, sizeof(int), s()));
@@ -1804,17 +1935,21 @@ struct KMeans {
       double* da = d2_a;
       double* db = d2_b;
       for (int j = 0; j < nb; ++j) {
-        cudaGraphExec_t& g = gx[(it0 + j) & 1];
-        if (!g) {
-          cudaGraph_t graph;
-          KT_CUDA(cudaStreamBeginCapture(s(), cudaStreamCaptureModeThreadLocal));
-          CaptureGuard cg{s()};
+        if (!graphs) {
           enqueue_iter();
-          cg.end(&graph);
-          KT_CUDA(cudaGraphInstantiate(&g, graph, 0));
-          cudaGraphDestroy(graph);
+        } else {
+          cudaGraphExec_t& g = gx[(it0 + j) & 1];
+          if (!g) {
+            cudaGraph_t graph;
+            KT_CUDA(cudaStreamBeginCapture(s(), cudaStreamCaptureModeThreadLocal));
+            CaptureGuard cg{s()};
+            enqueue_iter();
+            cg.end(&graph);
+            KT_CUDA(cudaGraphInstantiate(&g, graph, 0));
+            cudaGraphDestroy(graph);
+          }
+          KT_CUDA(cudaGraphLaunch(g, s()));
         }
-        KT_CUDA(cudaGraphLaunch(g, s()));
         std::swap(asg_a, asg_b);
         std::swap(d2_a, d2_b);
       }
@@ -1868,11 +2003,15 @@ struct KMeans {
     for (int r = 0; r < std::max(1, restarts); ++r) {
       std::vector<double> il;
       const uint64_t rs = kt::seed_combine(seed, (uint64_t)r);
-      const bool spec = !sharded && !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1 && capturable(ctx->stream);
+      const bool spec = !sharded && !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1;
       if (!spec || !lloyd_cert(k, rs, max_iters, il)) {
         if (spec) ctx->stats[KTUNE_STAT_KMEANS_ABORTS] += 1;
         lloyd(k, rs, max_iters, il);
       }
+      int32_t nfb = 0;  // kmeans++ picks decided by the exact replay (this restart)
+      KT_CUDA(cudaMemcpyAsync(&nfb, &kst->fallbacks, sizeof(nfb), cudaMemcpyDeviceToHost, s()));
+      KT_CUDA(cudaStreamSynchronize(s()));
+      ctx->stats[KTUNE_STAT_KPP_FALLBACKS] += nfb;
       const double Lx = exact_loss(d2_a);
       il.back() = Lx;
       if (!have || Lx < best.loss_exact) {
