@@ -461,6 +461,13 @@ __global__ void centroids_from_sums_kernel(KtSpaceParams sp, int k, const unsign
   }
 }
 
+// Sharded certified Lloyd: every rank adds the all-reduced deltas of the points that
+// moved (integer sums: exact and order-free) to its replica of the sums.
+__global__ void add_sums_kernel(unsigned long long* __restrict__ cs, const unsigned long long* __restrict__ delta,
+                                int n) {
+  for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < n; i += blockDim.x * gridDim.x) cs[i] += delta[i];
+}
+
 // Certified assignment against c_B: d2 in the reference's operation order with
 // c_B, a rigorous interval per cluster, the winner only if its interval is
 // strictly below every other cluster's. Fused: the integer sums are updated in
@@ -471,7 +478,7 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
     KtSpaceParams sp, int lut_total, const IdxT* __restrict__ pts, int64_t N, const double* __restrict__ cB,
     const double* __restrict__ dB, int k, const int32_t* __restrict__ prev, int32_t* __restrict__ asg,
     double* __restrict__ d2, double* __restrict__ chunk_sum, unsigned long long* __restrict__ counters,
-    unsigned long long* __restrict__ g_sum, unsigned long long* __restrict__ g_cnt) {
+    unsigned long long* __restrict__ g_sum, unsigned long long* __restrict__ g_cnt, int64_t chunk0) {
   extern __shared__ double sdyn[];
   __shared__ double red[32];
   __shared__ int32_t s_sum[kt::kMaxK * kt::kMaxKnobs];
@@ -505,7 +512,7 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
   for (int i = threadIdx.x; i < k; i += blockDim.x) s_cnt[i] = 0;
   const double* lut = stage_lut(sp, s_lut, lut_total);
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  const int64_t base = (chunk0 + blockIdx.x) * kChunk;  // this launch's chunk range (a rank's shard)
   double part = 0.0;
   int nchg = 0, nunc = 0;
   const double grow = (double)(2 * D + 4) * 0x1.0p-53;
@@ -607,7 +614,7 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
     }
   }
   const double s = block_sum(part, red);
-  if (threadIdx.x == 0) chunk_sum[blockIdx.x] = s;
+  if (threadIdx.x == 0) chunk_sum[chunk0 + blockIdx.x] = s;
   for (int o = 16; o > 0; o >>= 1) {
     nchg += __shfl_down_sync(0xffffffff, nchg, o);
     nunc += __shfl_down_sync(0xffffffff, nunc, o);
@@ -1913,20 +1920,36 @@ struct KMeans {
           if (g[i]) cudaGraphExecDestroy(g[i]);
       }
     } guard{gx};
+    // sharded: this rank's chunks only; the moved-point deltas of the integer sums, the
+    // changed/uncertain counters and the loss estimate are all-reduced (O(k D) words per
+    // iteration), assignments stay rank-local until the exact finalisation
+    const int64_t c0 = sharded ? (int64_t)rank * shard_chunks : 0;
+    const int64_t nloc = sharded ? std::max<int64_t>(0, std::min<int64_t>(nchunks, c0 + shard_chunks) - c0) : nchunks;
+    unsigned long long* dsum = isum[1];
     auto enqueue_iter = [&]() {
       KT_CUDA(cudaMemsetAsync(ull, 0, 32, s()));
       centroids_from_sums_kernel<<<1, 1024, 0, s()>>>(sp->params, k, cs, cs + (size_t)kt::kMaxK * kt::kMaxKnobs, cB,
                                                       dB, ull + 3);
-      KT_DISPATCH_DM(D, assign_cert_kernel<IdxT, DM_><<<(unsigned)nchunks, kBT, tsmem, s()>>>(
-                            sp->params, lut_total, pts, N, cB, dB, k, asg_a, asg_b, d2_b, chunk, ull, cs,
-                            cs + (size_t)kt::kMaxK * kt::kMaxKnobs));
+      unsigned long long* tgt = sharded ? dsum : cs;
+      if (sharded) KT_CUDA(cudaMemsetAsync(dsum, 0, sizeof(unsigned long long) * words, s()));
+      if (nloc > 0)
+        KT_DISPATCH_DM(D, assign_cert_kernel<IdxT, DM_><<<(unsigned)nloc, kBT, tsmem, s()>>>(
+                              sp->params, lut_total, pts, N, cB, dB, k, asg_a, asg_b, d2_b, chunk, ull, tgt,
+                              tgt + (size_t)kt::kMaxK * kt::kMaxKnobs, c0));
       kt::check_launch(ctx, "assign_cert", 2);
-      sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk, nchunks, dscal);
+      if (nloc > 0) sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk + c0, nloc, dscal);
+      else KT_CUDA(cudaMemsetAsync(dscal, 0, 8, s()));
+      if (sharded) {
+        kt::allreduce_sum(ctx, dsum, words, false);
+        add_sums_kernel<<<(int)kt::ceil_div((int64_t)words, 256), 256, 0, s()>>>(cs, dsum, (int)words);
+        kt::allreduce_sum(ctx, ull, 3, false);
+        kt::allreduce_sum(ctx, dscal, 1, true);
+      }
       gather_readback_kernel<<<1, 1, 0, s()>>>(dscal, ull, seqcnt, csb + k, rb_dev, rb_slot);
     };
     int iters = 0;
     bool done = false;
-    const bool graphs = capturable(s());  // legacy default stream: the same work, uncaptured
+    const bool graphs = capturable(s()) && !sharded;  // legacy stream / NCCL calls: the same work, uncaptured
     for (int it0 = 0; it0 < max_iters && !done; it0 += kCertBatch) {
       const int nb = std::min(kCertBatch, max_iters - it0);
       KT_CUDA(cudaMemsetAsync(rb_slot, 0, sizeof(int), s()));
@@ -1977,6 +2000,11 @@ struct KMeans {
       }
     }
     if (iters > 0) {
+      if (sharded) {  // every rank needs both full assignments for the exact finalisation
+        const int64_t S = shard_chunks * kChunk;
+        kt::allgather(ctx, asg_a + rank * S, asg_a, sizeof(int32_t) * S);
+        kt::allgather(ctx, asg_b + rank * S, asg_b, sizeof(int32_t) * S);
+      }
       // exact final state: centroids from the previous assignment (asg_b), then the exact
       // d2 against them; the certified assignment must be reproduced exactly
       update_centroids(k, asg_b, d2_b, cent_b);
@@ -2003,7 +2031,7 @@ struct KMeans {
     for (int r = 0; r < std::max(1, restarts); ++r) {
       std::vector<double> il;
       const uint64_t rs = kt::seed_combine(seed, (uint64_t)r);
-      const bool spec = !sharded && !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1;
+      const bool spec = !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1;
       if (!spec || !lloyd_cert(k, rs, max_iters, il)) {
         if (spec) ctx->stats[KTUNE_STAT_KMEANS_ABORTS] += 1;
         lloyd(k, rs, max_iters, il);

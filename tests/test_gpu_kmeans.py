@@ -210,12 +210,17 @@ def test_nccl_sharded_path_on_one_rank(O, ctx, ref_ok, name, n, k, seed):
     dctx = Context(0, 0, 1, Context.nccl_unique_id())
     dctx.set_option(L.OPT_FORCE_SHARDED, 1)
     ds = _space(dctx, sp)
-    dctx.reset_stats()
-    got = kmeans_run(ds, cidx, k, seed, restarts=2)
-    assert dctx.stat(L.STAT_XS_SEGMENTS) > 0  # the sharded path (exact-order sums every iteration) ran
-    assert np.array_equal(got.assignments, want.assignments)
-    assert np.array_equal(got.centroids, want.centroids)
-    assert got.l2_loss == want.l2_loss
+    for mode in (1, 0):  # exact-order sums every iteration (mode A), then the sharded certified mode B
+        dctx.set_option(L.OPT_KMEANS_MODE, mode)
+        dctx.reset_stats()
+        got = kmeans_run(ds, cidx, k, seed, restarts=2)
+        if mode == 1:
+            assert dctx.stat(L.STAT_XS_SEGMENTS) > 0  # the sharded mode-A path ran
+        else:
+            assert dctx.stat(L.STAT_KMEANS_ABORTS) == 0
+        assert np.array_equal(got.assignments, want.assignments)
+        assert np.array_equal(got.centroids, want.centroids)
+        assert got.l2_loss == want.l2_loss
     ref = O.kmeans_run(osp.encode(cidx), k, seed, restarts=2, impl="ref")
     assert np.array_equal(got.assignments, ref["assignments"])
     cs = CandidateSet(cidx, cids, np.zeros(len(cids)))
