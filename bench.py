@@ -328,8 +328,10 @@ def kmeans_secondary(ctx, args, cpu=True):
            "assign_kernel_ms": a_ms,
            "assign_roofline": {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                "frac": ach / peaks["hbm_gbs"], "bytes_per_point": bytes_pt,
-                               "note": "exact-path assign kernel (profiled run); the default certified iteration "
-                                       "screens in fp32 with a rigorous bound and recomputes only the winner in fp64"},
+                               "note": "exact assignment kernel of a profiled run (fp32 screen against the exact "
+                                       "centroids with a rigorous bound, the winner's d2 and near ties in the "
+                                       "reference's fp64 order); the certified iterations run the same kernel "
+                                       "against integer-sum centroids"},
            "forced_full_sweep": full}
     if cpu:
         try:

@@ -72,8 +72,10 @@ int ktune_ctx_synchronize(ktune_ctx* ctx);
 
 enum ktune_option {
   KTUNE_OPT_FORCE_EXACT = 1, /* 1: k-means decisions always via the exact-order fallback chains */
-  KTUNE_OPT_KMEANS_MODE = 2, /* 0 auto (= 2 on one GPU), 1 exact-order centroids every iteration (mode A),
-                                2 certified integer-sum centroids with exact fallback (mode B) */
+  KTUNE_OPT_KMEANS_MODE = 2, /* 0 auto (= 2), 1 exact-order centroids every iteration with the plain exact
+                                fp64 assignment scan (mode A), 2 certified integer-sum centroids with exact
+                                fallback (mode B), 3 mode A with the tcgen05 screening assignment (kept for
+                                comparison: slower than the default fp32-screened exact assignment) */
   KTUNE_OPT_PROFILE = 3,     /* 1: bracket the hot kernels with CUDA events on their stream (KTUNE_STAT_*_NS) */
   KTUNE_OPT_ROLLOUT_DELTA = 4, /* certification margin of the tcgen05 rollout, in units of 1e-12
                                   (0 = default) */

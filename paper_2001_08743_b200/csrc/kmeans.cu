@@ -598,18 +598,20 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
       asg[i] = bc;
       d2[i] = best;
       part = kt::dadd(part, best);
-      const int pc = prev[i];
+      const int pc = prev ? prev[i] : bc;
       if (pc != bc) {  // move this point's indices between the clusters' integer sums
         ++nchg;
-        for (int d = 0; d < D; ++d) {
-          const int v = (int)pts[i * D + d];
-          if (v) {
-            atomicAdd(&s_sum[bc * D + d], v);
-            atomicAdd(&s_sum[pc * D + d], -v);
+        if (g_sum) {
+          for (int d = 0; d < D; ++d) {
+            const int v = (int)pts[i * D + d];
+            if (v) {
+              atomicAdd(&s_sum[bc * D + d], v);
+              atomicAdd(&s_sum[pc * D + d], -v);
+            }
           }
+          atomicAdd(&s_cnt[bc], 1);
+          atomicAdd(&s_cnt[pc], -1);
         }
-        atomicAdd(&s_cnt[bc], 1);
-        atomicAdd(&s_cnt[pc], -1);
       }
     }
   }
@@ -624,7 +626,7 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
     if (nunc) atomicAdd(counters + 2, (unsigned long long)nunc);
   }
   __syncthreads();
-  flush_cluster_sums(k, D, s_sum, s_cnt, g_sum, g_cnt);
+  if (g_sum) flush_cluster_sums(k, D, s_sum, s_cnt, g_sum, g_cnt);
 }
 
 // ------------------------------------------------------------------ assign on tcgen05 (K3 fast path)
@@ -1621,7 +1623,9 @@ struct KMeans {
   bool sharded = false;  // per-point state all-gathered over NCCL (world > 1, or forced for tests)
   int64_t shard_chunks = 0, cap = 0;
   double* tile_sum = nullptr;  // tcgen05 assign: per-128-point-tile loss partials
-  bool use_tc = false;
+  bool use_tc = false;         // tcgen05 screening assignment (KTUNE_OPT_KMEANS_MODE = 3; measured slower)
+  double* dzero = nullptr;      // all-zero bound block: assign_cert_kernel against exact centroids
+  size_t screen_smem = 0;
 
   void setup(ktune_ctx* c, const ktune_space* s, const IdxT* p, int64_t n) {
     ctx = c;
@@ -1654,7 +1658,7 @@ struct KMeans {
     seqcnt = csb + kt::kMaxK + 4;
     max_segs = (int)(kt::ceil_div(N, kt::xsum::kSeg) + kt::kMaxK);
     tile_sum = (double*)ctx->dev(kt::WS_TILESUM, sizeof(double) * (size_t)world * shard_chunks * (kChunk / kTcPts));
-    use_tc = ctx->opt_kmeans_mode != 1 && D <= 16 &&
+    use_tc = ctx->opt_kmeans_mode == 3 && D <= 16 &&
              (size_t)lut_total * 8 + kTcPts * kTcK * 2 + kTcMaxN * kTcK * 2 + (kt::kMaxK * kt::kMaxKnobs + kt::kMaxK) * 8 <= 200 * 1024;
     for (int d = 0; d < D; ++d) use_tc = use_tc && s->card[d] <= 2048;  // idx exact in fp16
     sorted = (IdxT*)ctx->dev(kt::WS_SORTED, sizeof(IdxT) * N * D);
@@ -1669,14 +1673,19 @@ struct KMeans {
     rb_slot = reinterpret_cast<int*>(rb_dev + 8);
     {
       const size_t words = (size_t)kt::kMaxK * (kt::kMaxKnobs + 1);
+      const size_t nb = kt::kMaxK * kt::kMaxKnobs + kt::kMaxK;  // bound block: [k x D] deltas, [kMaxK] E_c
       unsigned long long* w = (unsigned long long*)ctx->dev(
-          kt::WS_KM_CERT, sizeof(unsigned long long) * words * 2 +
-                              sizeof(double) * (kt::kMaxK * kt::kMaxKnobs * 2 + kt::kMaxK));
+          kt::WS_KM_CERT, sizeof(unsigned long long) * words * 2 + sizeof(double) * (kt::kMaxK * kt::kMaxKnobs + 2 * nb));
       isum[0] = w;
       isum[1] = w + words;
       cB = reinterpret_cast<double*>(w + 2 * words);
       dB = cB + kt::kMaxK * kt::kMaxKnobs;  // [k x D] deltas, then [kMaxK] per-cluster bounds
+      dzero = dB + nb;                      // exact centroids: every bound 0
+      KT_CUDA(cudaMemsetAsync(dzero, 0, sizeof(double) * nb, ctx->stream));
     }
+    screen_smem = sizeof(double) * (kt::kMaxK * D + kt::kMaxK) + lut_smem;
+    KT_DISPATCH_DM(D, KT_CUDA(cudaFuncSetAttribute(assign_cert_kernel<IdxT, DM_>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_smem)));
     rb_host = (IterReadback*)ctx->host(3, sizeof(IterReadback) * 8);
     dscal = (double*)ctx->dev(kt::WS_SNAP, 64);
     best_asg = (int32_t*)ctx->dev(kt::WS_BEST_ASSIGN, sizeof(int32_t) * N);
@@ -1751,6 +1760,28 @@ struct KMeans {
         kt::allreduce_sum(ctx, ull, 1, false);
         kt::allreduce_sum(ctx, dscal, 1, true);
       }
+    } else if (ctx->opt_kmeans_mode != 1) {
+      // fp32 screening against the exact centroids (zero centroid bounds), the winner's d2
+      // and near ties in the reference's fp64 order: exact assignment, d2 and chunk sums
+      const int64_t c0 = sharded ? (int64_t)rank * shard_chunks : 0;
+      const int64_t nloc = sharded ? std::max<int64_t>(0, std::min<int64_t>(nchunks, c0 + shard_chunks) - c0) : nchunks;
+      if (nloc > 0) {
+        kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
+        KT_DISPATCH_DM(D, assign_cert_kernel<IdxT, DM_><<<(unsigned)nloc, kBT, screen_smem, s()>>>(
+                              sp->params, lut_total, pts, N, cent, dzero, k, prev, asg, dd, chunk, ull, nullptr,
+                              nullptr, c0));
+        kt::check_launch(ctx, "assign_screen");
+      }
+      if (sharded) {
+        if (nloc < shard_chunks)  // zero the padding chunks of the last shard
+          KT_CUDA(cudaMemsetAsync(chunk + c0 + nloc, 0, sizeof(double) * (shard_chunks - nloc), s()));
+        const int64_t S = shard_chunks * kChunk;
+        kt::allgather(ctx, asg + rank * S, asg, sizeof(int32_t) * S);
+        kt::allgather(ctx, dd + rank * S, dd, sizeof(double) * S);
+        kt::allgather(ctx, chunk + c0, chunk, sizeof(double) * shard_chunks);
+        kt::allreduce_sum(ctx, ull, 1, false);
+      }
+      KT_CUDA(cudaMemsetAsync(ull + 2, 0, 8, s()));  // near ties were resolved by the exact scan
     } else if (!sharded) {
       kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
       KT_DISPATCH_DM(D, assign_kernel<IdxT, DM_><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, cent,
@@ -1899,9 +1930,7 @@ struct KMeans {
     double loss = assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);  // exact
     iter_losses.assign(1, loss);
     const size_t words = (size_t)kt::kMaxK * (kt::kMaxKnobs + 1);
-    const size_t tsmem = sizeof(double) * (k * D + kt::kMaxK) + lut_smem;
-    KT_DISPATCH_DM(D, KT_CUDA(cudaFuncSetAttribute(assign_cert_kernel<IdxT, DM_>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem)));
+    const size_t tsmem = sizeof(double) * (k * D + kt::kMaxK) + lut_smem;  // <= screen_smem (setup's attribute)
     int cur = 0;
     KT_CUDA(cudaMemsetAsync(isum[cur], 0, sizeof(unsigned long long) * words, s()));
     cluster_sums_kernel<IdxT><<<(unsigned)nchunks, kBT, 0, s()>>>(pts, N, D, k, asg_a, isum[cur],
@@ -2031,7 +2060,7 @@ struct KMeans {
     for (int r = 0; r < std::max(1, restarts); ++r) {
       std::vector<double> il;
       const uint64_t rs = kt::seed_combine(seed, (uint64_t)r);
-      const bool spec = !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1;
+      const bool spec = !ctx->opt_force_exact && ctx->opt_kmeans_mode != 1 && ctx->opt_kmeans_mode != 3;
       if (!spec || !lloyd_cert(k, rs, max_iters, il)) {
         if (spec) ctx->stats[KTUNE_STAT_KMEANS_ABORTS] += 1;
         lloyd(k, rs, max_iters, il);

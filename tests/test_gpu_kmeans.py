@@ -142,7 +142,7 @@ def test_kmeans_large_vs_oracle(O, ctx):
     assert ctx.stat(L.STAT_KPP_PICKS) == 8
 
 
-@pytest.mark.parametrize("mode", [0, 1])  # 0: tcgen05 screening (default), 1: exact SIMT scan
+@pytest.mark.parametrize("mode", [0, 1, 3])  # 0: default (fp32-screened), 1: exact SIMT scan, 3: tcgen05 screening
 @pytest.mark.parametrize("name,n,k,seed", [("synthetic16", 20000, 24, 7), ("alexnet_c3_u16", 8000, 63, 8),
                                            ("resnet_c2", 6000, 9, 9)])
 def test_assign_paths_bit_exact(O, ctx, ref_ok, mode, name, n, k, seed):
