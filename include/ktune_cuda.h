@@ -85,9 +85,11 @@ enum ktune_option {
                                     instead of a separate K1 launch; measured slower on B200, DESIGN.md §5.6 */
   KTUNE_OPT_ROLLOUT_SEGMENTS = 7, /* host-buffer rollouts: step segments overlapped with the D2H copies
                                      (0 = auto, 1 = no segmentation) */
-  KTUNE_OPT_FORCE_SHARDED = 8     /* 1: run the multi-GPU k-means path (per-point state all-gathered over
+  KTUNE_OPT_FORCE_SHARDED = 8,    /* 1: run the multi-GPU k-means path (per-point state all-gathered over
                                      NCCL) even on one rank; needs a context created by
                                      ktune_ctx_create_dist with an ncclUniqueId (tests on one GPU) */
+  KTUNE_OPT_KMEANS_BOUND_LOG2 = 9  /* tests: inflate the certified k-means centroid bounds by 2^value so that
+                                     speculative iterations fail and the exact rescue path runs */
 };
 int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value);
 

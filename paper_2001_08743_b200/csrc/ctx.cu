@@ -281,6 +281,7 @@ int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value) {
     else if (option == KTUNE_OPT_ROLLOUT_FUSE_GBT) ctx->opt_rollout_fuse_gbt = value;
     else if (option == KTUNE_OPT_ROLLOUT_SEGMENTS) ctx->opt_rollout_segments = value;
     else if (option == KTUNE_OPT_FORCE_SHARDED) ctx->opt_force_sharded = value;
+    else if (option == KTUNE_OPT_KMEANS_BOUND_LOG2) ctx->opt_kmeans_bound_log2 = value;
     else kt::fail(KTUNE_ERR_CONFIG, "unknown option");
   });
 }

@@ -78,7 +78,7 @@ enum WsSlot {
   WS_IN0, WS_IN1, WS_IN2, WS_OUT0, WS_OUT1, WS_OUT2, WS_OUT3, WS_OUT4,
   WS_D2, WS_D2B, WS_ASSIGN, WS_ASSIGN2, WS_MEMBERS, WS_BLOCK, WS_BLOCK2, WS_CENT, WS_CENT2,
   WS_SCRATCH, WS_SCRATCH2, WS_KPP, WS_SNAP, WS_VALID, WS_TASKS, WS_BEST_ASSIGN, WS_BEST_D2,
-  WS_PREV_ASSIGN, WS_PREV_D2, WS_SORTED, WS_XS_APPROX, WS_XS_MAPS, WS_TILESUM, WS_ROLLOUT, WS_XS_RB, WS_KM_CERT, WS_KPP_X, WS_NUM_SLOTS
+  WS_PREV_ASSIGN, WS_PREV_D2, WS_SORTED, WS_XS_APPROX, WS_XS_MAPS, WS_TILESUM, WS_ROLLOUT, WS_XS_RB, WS_KM_CERT, WS_KPP_X, WS_CERT_SNAP, WS_NUM_SLOTS
 };
 
 }  // namespace kt
@@ -93,7 +93,8 @@ struct ktune_ctx {
   cudaStream_t copy_stream = nullptr;  // D2H of segmented rollouts, overlapping the compute
   std::string last_error;
   int64_t opt_force_exact = 0;
-  int64_t opt_force_sharded = 0;  // k-means: the NCCL-sharded path on one rank (tests)
+  int64_t opt_force_sharded = 0;
+  int64_t opt_kmeans_bound_log2 = 0;  // tests: inflate the certified k-means bounds by 2^v (forces rescues)  // k-means: the NCCL-sharded path on one rank (tests)
   int64_t opt_kmeans_mode = 0;
   int64_t opt_profile = 0;
   int64_t opt_rollout_delta = 0;  // 1e-12 units, 0 = default

@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kBT) kpp_d2_kernel(KtSpaceParams sp, int lut_t
   __shared__ double red[32];
   __shared__ double cs[kt::kMaxKnobs];
   const double* lut = stage_lut(sp, sdyn, lut_total);
+  __syncthreads();  // the staged table is read below by other threads than those that wrote it
   const int D = sp.D;
   const int64_t pick = st->pick;
   if (threadIdx.x < D) {
@@ -433,7 +434,8 @@ __global__ void __launch_bounds__(kBT) cluster_sums_kernel(const IdxT* __restric
 // c_B and its bound delta from the integer sums; counts empty clusters.
 __global__ void centroids_from_sums_kernel(KtSpaceParams sp, int k, const unsigned long long* __restrict__ g_sum,
                                            const unsigned long long* __restrict__ g_cnt, double* __restrict__ cB,
-                                           double* __restrict__ dB, unsigned long long* __restrict__ empty) {
+                                           double* __restrict__ dB, unsigned long long* __restrict__ empty,
+                                           double bound_scale = 1.0) {
   const int D = sp.D;
   for (int i = threadIdx.x; i < k * D; i += blockDim.x) {
     const int c = i / D, d = i % D;
@@ -456,7 +458,7 @@ __global__ void centroids_from_sums_kernel(KtSpaceParams sp, int k, const unsign
       const double del = dB[threadIdx.x * D + d];
       e += del * (2.0 + del);
     }
-    dB[kt::kMaxK * kt::kMaxKnobs + threadIdx.x] = e * (1.0 + 0x1.0p-20);
+    dB[kt::kMaxK * kt::kMaxKnobs + threadIdx.x] = e * (1.0 + 0x1.0p-20) * bound_scale;  // scale: tests only
     if (g_cnt[threadIdx.x] == 0) atomicAdd(empty, 1ull);
   }
 }
@@ -1875,6 +1877,11 @@ struct KMeans {
     kmeanspp(k, rng_seed);
     double loss = assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);
     iter_losses.assign(1, loss);
+    return lloyd_loop(k, 0, max_iters, loss, iter_losses);
+  }
+
+  // Exact Lloyd iterations it0 .. max_iters-1 from the exact state (asg_a, d2_a).
+  double lloyd_loop(int k, int it0, int max_iters, double loss, std::vector<double>& iter_losses) {
     // Single-GPU iterations replay a captured CUDA graph (centroid update + assignment +
     // readback: ~20 launches): the loop is launch-bound at N = 1M. Two graphs, one per
     // parity of the a/b buffer swap.
@@ -1888,7 +1895,7 @@ struct KMeans {
           if (g[i]) cudaGraphExecDestroy(g[i]);
       }
     } guard{gx};
-    for (int it = 0; it < max_iters; ++it) {
+    for (int it = it0; it < max_iters; ++it) {
       unsigned long long changed = 0;
       if (use_graph) {
         cudaGraphExec_t& g = gx[it & 1];
@@ -1958,7 +1965,7 @@ struct KMeans {
     auto enqueue_iter = [&]() {
       KT_CUDA(cudaMemsetAsync(ull, 0, 32, s()));
       centroids_from_sums_kernel<<<1, 1024, 0, s()>>>(sp->params, k, cs, cs + (size_t)kt::kMaxK * kt::kMaxKnobs, cB,
-                                                      dB, ull + 3);
+                                                      dB, ull + 3, std::ldexp(1.0, (int)ctx->opt_kmeans_bound_log2));
       unsigned long long* tgt = sharded ? dsum : cs;
       if (sharded) KT_CUDA(cudaMemsetAsync(dsum, 0, sizeof(unsigned long long) * words, s()));
       if (nloc > 0)
@@ -1979,8 +1986,35 @@ struct KMeans {
     int iters = 0;
     bool done = false;
     const bool graphs = capturable(s()) && !sharded;  // legacy stream / NCCL calls: the same work, uncaptured
+    // Rescue instead of restart: the state at each batch start is certified, so an
+    // uncertain point or an empty cluster inside a batch continues EXACTLY (mode A) from
+    // there. Snapshot: the exact initial (assignment, d2) before the first batch, the
+    // previous assignment before later ones (its exact centroids reproduce the current one).
+    int32_t* snap_asg = (int32_t*)ctx->dev(kt::WS_CERT_SNAP, (sizeof(int32_t) + sizeof(double)) * N);
+    double* snap_d2 = reinterpret_cast<double*>(snap_asg + N);
+    auto rescue = [&](int t, double at_loss) {
+      ctx->stats[KTUNE_STAT_KMEANS_ABORTS] += 1;
+      if (t == 0) {  // back to the exact initial assignment
+        KT_CUDA(cudaMemcpyAsync(asg_a, snap_asg, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s()));
+        KT_CUDA(cudaMemcpyAsync(d2_a, snap_d2, sizeof(double) * N, cudaMemcpyDeviceToDevice, s()));
+      } else {  // exact centroids of the previous assignment (certified: no empty cluster), exact assign
+        KT_CUDA(cudaMemcpyAsync(asg_b, snap_asg, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s()));
+        update_centroids(k, asg_b, d2_b, cent_a);
+        assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);
+      }
+      lloyd_loop(k, t, max_iters, at_loss, iter_losses);
+    };
     for (int it0 = 0; it0 < max_iters && !done; it0 += kCertBatch) {
       const int nb = std::min(kCertBatch, max_iters - it0);
+      if (iters == 0) {
+        KT_CUDA(cudaMemcpyAsync(snap_asg, asg_a, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s()));
+        KT_CUDA(cudaMemcpyAsync(snap_d2, d2_a, sizeof(double) * N, cudaMemcpyDeviceToDevice, s()));
+      } else {
+        KT_CUDA(cudaMemcpyAsync(snap_asg, asg_b, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s()));
+      }
+      const int t_batch = iters;
+      const double loss_batch = loss;
+      const size_t nl_batch = iter_losses.size();
       KT_CUDA(cudaMemsetAsync(rb_slot, 0, sizeof(int), s()));
       int32_t* sa = asg_a;  // the device-side view of the swaps inside this batch
       int32_t* sb = asg_b;
@@ -2013,7 +2047,15 @@ struct KMeans {
       KT_CUDA(cudaStreamSynchronize(s()));
       for (int j = 0; j < nb; ++j) {
         const IterReadback h = rb_host[j];
-        if (h.empty || h.unc) return false;  // speculation off: rerun exactly
+        if (h.empty || h.unc) {  // speculation off: continue exactly from the batch start
+          asg_a = sa;
+          asg_b = sb;
+          d2_a = da;
+          d2_b = db;
+          iter_losses.resize(nl_batch);
+          rescue(t_batch, loss_batch);
+          return true;
+        }
         ctx->stats[KTUNE_STAT_LLOYD_ITERS] += 1;
         if (h.loss > loss * (1.0 + 1e-9) + 1e-9 + loss_err(loss) + loss_err(h.loss))
           kt::fail(KTUNE_ERR_LOGIC, "kmeans: Lloyd loss increased, which should be impossible");

@@ -254,3 +254,57 @@ def test_adaptive_sweep_device_resident(O, ctx, name, n):
     assert np.array_equal(dev.assignments.cpu().numpy(), host.assignments)
     assert np.array_equal(dev.centroids.cpu().numpy(), host.centroids)
     assert np.array_equal(dev.snapped.cpu().numpy(), host.snapped)
+
+
+@pytest.mark.parametrize("log2", [30, 45])
+@pytest.mark.parametrize("name,n,k,seed", [("alexnet_c3_u16", 20000, 8, 41), ("synthetic16", 15000, 20, 42)])
+def test_certified_lloyd_rescue(O, ctx, name, n, k, seed, log2):
+    """Inflated centroid bounds make speculative iterations fail (uncertain points):
+    the run continues exactly from the last certified batch and still matches the
+    exact mode and the reference."""
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.sampling import kmeans_run
+    sp = SPACES[name]()
+    osp = O.OSpace(sp)
+    cidx, cids, _ = candidate_set(O, osp, n, seed)
+    ds = _space(ctx, sp)
+    ctx.set_option(L.OPT_KMEANS_MODE, 1)
+    try:
+        a = kmeans_run(ds, cidx, k, seed, restarts=2)
+    finally:
+        ctx.set_option(L.OPT_KMEANS_MODE, 0)
+    ctx.reset_stats()
+    ctx.set_option(L.OPT_KMEANS_BOUND_LOG2, log2)
+    try:
+        b = kmeans_run(ds, cidx, k, seed, restarts=2)
+        rescues = ctx.stat(L.STAT_KMEANS_ABORTS)
+    finally:
+        ctx.set_option(L.OPT_KMEANS_BOUND_LOG2, 0)
+    assert rescues > 0
+    assert np.array_equal(a.assignments, b.assignments)
+    assert np.array_equal(a.centroids, b.centroids)
+    assert a.l2_loss == b.l2_loss
+    assert len(a.iteration_losses) == len(b.iteration_losses)
+    ref = O.kmeans_run(osp.encode(cidx), k, seed, restarts=2, impl="ref")
+    assert np.array_equal(b.assignments, ref["assignments"])
+
+
+def test_kmeans_two_million_points_deterministic_and_exact(O, ctx, ref_ok):
+    """2M points (2000 chunk blocks per pass): repeated calls give identical results
+    (a shared-memory staging race in the kmeans++ distance kernel once made the picks
+    nondeterministic at this size) and the result equals the reference's."""
+    from paper_2001_08743_b200.sampling import kmeans_run
+    sp = SPACES["alexnet_c3_u16"]()
+    osp = O.OSpace(sp)
+    g = np.random.default_rng(77)
+    idx = np.stack([g.integers(0, c, 2_000_000) for c in sp.cards], 1).astype(np.int32)
+    ds = _space(ctx, sp)
+    runs = [kmeans_run(ds, idx, 9, 5, restarts=1) for _ in range(3)]
+    for r in runs[1:]:
+        assert np.array_equal(r.assignments, runs[0].assignments)
+        assert np.array_equal(r.centroids, runs[0].centroids)
+        assert r.l2_loss == runs[0].l2_loss
+    want = O.kmeans_run(osp.encode(idx), 9, 5, restarts=1, impl="ref")
+    assert np.array_equal(runs[0].assignments, want["assignments"])
+    assert np.array_equal(runs[0].centroids, want["centroids"])
+    assert runs[0].l2_loss == want["loss"]
