@@ -15,6 +15,31 @@ def _is_torch_cuda(a) -> bool:
     return hasattr(a, "is_cuda") and bool(getattr(a, "is_cuda"))
 
 
+_NP_TO_TORCH = None
+
+
+def host_empty(shape, dtype) -> np.ndarray:
+    """Output buffer for host-pointer calls: page-locked memory from torch's caching host
+    allocator when torch is present (device->host copies at PCIe speed and no page faults;
+    blocks return to the cache when the array dies and are reused by the next call), else a
+    plain numpy array. Contents are uninitialised: every element is written by the call."""
+    global _NP_TO_TORCH
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            raise ImportError
+    except ImportError:
+        return np.empty(shape, dtype)
+    if _NP_TO_TORCH is None:
+        _NP_TO_TORCH = {np.dtype(np.uint8): torch.uint8, np.dtype(np.int8): torch.int8,
+                        np.dtype(np.uint16): torch.int16, np.dtype(np.int16): torch.int16,
+                        np.dtype(np.int32): torch.int32, np.dtype(np.float32): torch.float32,
+                        np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64}
+    dt = np.dtype(dtype)
+    t = torch.empty(shape, dtype=_NP_TO_TORCH[dt], pin_memory=True)
+    return t.numpy().view(dt)
+
+
 def ptr_of(a, dtype=None):
     """(pointer, is_device, keepalive) for a numpy array or a CUDA torch tensor."""
     if a is None:

@@ -17,7 +17,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _lib as L
-from .context import Context, Space, default_context, ptr_of
+from .context import Context, Space, default_context, host_empty, ptr_of
 from .cost_model import DeviceGbt
 from .errors import ConfigError
 from .spaces import mix64, stream_seed
@@ -141,11 +141,11 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
             if host_out is not None:  # caller-provided (e.g. pinned) host buffers
                 o = host_out[i]
             else:
-                o = dict(idx=np.zeros((E, T + 1, D), np.uint16),
-                         score=np.zeros((E, T + 1)) if t.cost_model is not None else None,
-                         actions=np.zeros((E, T, D), np.int8) if t.want_trajectory else None,
-                         logp=np.zeros((E, T)) if t.want_trajectory else None,
-                         value=np.zeros((E, T)) if t.want_trajectory else None)
+                o = dict(idx=host_empty((E, T + 1, D), np.uint16),
+                         score=host_empty((E, T + 1), np.float64) if t.cost_model is not None else None,
+                         actions=host_empty((E, T, D), np.int8) if t.want_trajectory else None,
+                         logp=host_empty((E, T), np.float64) if t.want_trajectory else None,
+                         value=host_empty((E, T), np.float64) if t.want_trajectory else None)
             pp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
             init_p = init.ctypes.data_as(C.c_void_p)
             keep.append(init)
@@ -260,7 +260,7 @@ def sa_search_batch(tasks: Sequence[SaTask], params: SaParams, ctx: Optional[Con
         else:
             init = np.ascontiguousarray(t.init_idx, np.uint16).reshape(-1, D)
             E = len(init)
-            mk = lambda shape, dt: np.zeros(shape, {"u16": np.uint16, "f64": np.float64, "u8": np.uint8}[dt])
+            mk = lambda shape, dt: host_empty(shape, {"u16": np.uint16, "f64": np.float64, "u8": np.uint8}[dt])
             pp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
         if host_out is not None:
             o = host_out[i]
