@@ -245,6 +245,42 @@ def c3_pipeline(ctx, args):
             "total_ms": 1e3 * (t_roll + t3 - t1)}
 
 
+def gbt_standalone(ctx, args, specs, spaces, gbts):
+    """standalone K1 scoring of a device-resident candidate array (ResNet-18 task 0,
+    16M random configurations, u8 indices), rows/s with its HBM roofline (D + 8 bytes per config:
+    the row read, the fp64 score written) — the kernel is shared-memory (LSU) bound by design."""
+    import torch
+    from paper_2001_08743_b200.workloads import random_configs
+    sp, ds, g = specs[0].space, spaces[0], gbts[0]
+    n = args.gbt_rows
+    idx = torch.from_numpy(random_configs(sp, n, 17).astype(ds.idx_dtype).view(np.int8 if ds.index_bytes == 1 else np.int16)).cuda()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)
+    ctx.set_stream(st.cuda_stream)
+    for _ in range(3):
+        g.predict_idx(idx, out)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    reps = 10
+    ev[0].record(st)
+    for _ in range(reps):
+        g.predict_idx(idx, out)
+    ev[1].record(st)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / reps
+    ctx.set_stream(None)
+    torch.cuda.set_stream(torch.cuda.default_stream())
+    peaks, _ = load_peaks()
+    bpr = sp.num_knobs * ds.index_bytes + 8
+    gbs = n * bpr / (ms * 1e-3) / 1e9
+    return {"metric": "GBT scoring rows/s (K1 over a device-resident candidate array)", "rows": n,
+            "ms": ms, "value": n / (ms * 1e-3), "unit": "rows/s",
+            "hbm_roofline": {"bound": "hbm", "bytes_per_row": bpr, "achieved": gbs, "peak": peaks["hbm_gbs"],
+                             "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"]},
+            "note": "50 trees x depth 4: ~8 shared-memory wavefronts per tree walk; LSU-bound (ncu: shared "
+                    "pipe ~85%, issue ~80%, profiles/r01_gbt_score_kernel.json), far below the HBM bound"}
+
+
 def kmeans_secondary(ctx, args, cpu=True):
     """k-means sampling ms/iter (BASELINE metric 2): AlexNet conv2 space (uint16
     knob indices), 1M deduplicated candidates, k=8, exact Lloyd iterations; plus
@@ -424,6 +460,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size tcgen05 vs exact comparison")
     ap.add_argument("--no-sa", action="store_true", help="skip the simulated-annealing baseline measurement")
     ap.add_argument("--no-cand", action="store_true", help="skip the device make_candidate_set measurement")
+    ap.add_argument("--gbt-rows", type=int, default=1 << 24, help="standalone K1 scoring rows (0 = skip)")
     ap.add_argument("--c3-episodes", type=int, default=65536, help="SURVEY C3 pipeline episodes (0 = skip)")
     ap.add_argument("--c3-T", type=int, default=500)
     ap.add_argument("--no-full-sweep", action="store_true", help="skip the forced k = 8..63 k-means sweep (SURVEY C4)")
@@ -652,6 +689,13 @@ def main():
         except Exception as ex:  # reported, not hidden
             scale = {"error": repr(ex)}
 
+    gbt_s = None
+    if args.gbt_rows and world == 1:
+        try:
+            gbt_s = gbt_standalone(ctx, args, specs, spaces, gbts)
+        except Exception as ex:  # reported, not hidden
+            gbt_s = {"error": repr(ex)}
+
     c3 = None
     if args.c3_episodes and world == 1:
         try:
@@ -721,6 +765,7 @@ def main():
             "secondary": kmeans,
             "scale_c5": scale,
             "pipeline_c3": c3,
+            "gbt_standalone": gbt_s,
             "sa_baseline": sa,
             "candidates": cand,
         }
