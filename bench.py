@@ -591,11 +591,13 @@ def main():
         D = n_knobs
         # logp / value as fp32: the tcgen05 path computes both in fp32, so shipping
         # them as doubles would only add PCIe bytes
-        # and the visited configurations as uint8 wherever every cardinality fits (the API's idx_u8)
+        # and the visited configurations as uint8 wherever every cardinality fits (the API's idx_u8);
+        # scores as fp32 (north star: scores within 1e-5 relative in fp32; the device keeps and ranks
+        # candidates on the exact fp64 scores)
         small = [max(s.space.cards) <= 256 for s in specs]
         host_out = [dict(idx=None if sm else pinned((E, T + 1, D), torch.int16).view(np.uint16),
                          idx8=pinned((E, T + 1, D), torch.uint8) if sm else None,
-                         score=pinned((E, T + 1), torch.float64), actions=None,
+                         score=None, score32=pinned((E, T + 1), torch.float32), actions=None,
                          actions2=pinned((E, T, (D + 3) // 4), torch.uint8),  # 2 bits per direction
                          logp=None, value=None, logp32=pinned((E, T), torch.float32),
                          value32=pinned((E, T), torch.float32)) for sm in small]

@@ -240,6 +240,10 @@ typedef struct {
   uint8_t* actions_u2;      /* E x T x ceil(D/4) bytes, 2 bits per knob: byte j holds knobs 4j..4j+3 as
                                (direction + 1) << 2*(d - 4j) (may be NULL; host-pointer calls may then
                                pass actions = NULL) */
+  float* score_f32;         /* E x (T+1) cost-model scores rounded to fp32 (may be NULL; host-pointer
+                               calls may then pass score = NULL): within the 1e-5 relative tolerance the
+                               path promises for scores, half the bytes. Candidate ranking on the device
+                               always uses the exact fp64 scores. */
 } ktune_rollout_task;
 int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks, int32_t T,
                   int flags);

@@ -52,7 +52,7 @@ class RolloutTaskC(C.Structure):
     _fields_ = [("space", P), ("ac", P), ("gbt", P), ("num_episodes", i64),
                 ("episode_offset", i64), ("explore_seed", u64), ("init_idx", P), ("idx", P),
                 ("score", P), ("actions", P), ("logp", P), ("value", P), ("logp_f32", P), ("value_f32", P),
-                ("idx_u8", P), ("actions_u2", P)]
+                ("idx_u8", P), ("actions_u2", P), ("score_f32", P)]
 
 
 class SaParamsC(C.Structure):

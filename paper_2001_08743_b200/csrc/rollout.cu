@@ -374,6 +374,16 @@ __global__ void debug_math_kernel(int op, const double* __restrict__ x, int64_t 
 }
 
 // uint16 -> uint8 copy of trajectory rows [r0, r0 + rows) of every episode (idx_u8 outputs).
+// fp32 copies of trajectory score rows [r0, r0 + len) of every episode (row pitch P).
+__global__ void score_f32_kernel(const double* __restrict__ src, float* __restrict__ dst, int64_t E, int P, int r0,
+                                 int len) {
+  const int64_t n = E * len;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = j / len, i = e * P + r0 + (j - e * len);
+    dst[i] = (float)src[i];
+  }
+}
+
 __global__ void narrow_idx_kernel(const uint16_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t E,
                                   int rows_per_ep, int n, int r0, int rows) {
   const int64_t per = (int64_t)rows * n, total = E * per;
@@ -522,6 +532,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       float* d_val32;
       uint8_t* d_u8;
       uint8_t* d_a2;
+      float* d_s32;
     };
     std::vector<HostIo> io(num_tasks);
     bool smem_params = true;
@@ -531,7 +542,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       arena += (std::max<size_t>(bytes, 8) + 255) & ~(size_t)255;
       return o;
     };
-    std::vector<std::array<size_t, 10>> offs(num_tasks);
+    std::vector<std::array<size_t, 11>> offs(num_tasks);
     for (int k = 0; k < num_tasks; ++k) {
       const ktune_rollout_task& t = tasks[k];
       if (!t.space || !t.ac) kt::fail(KTUNE_ERR_CONFIG, "rollout: task needs a space and an agent");
@@ -541,6 +552,8 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         kt::fail(KTUNE_ERR_CONFIG, "rollout: bad episode count or missing idx output");
       if (t.actions_u2 && dev && !t.actions)
         kt::fail(KTUNE_ERR_CONFIG, "rollout: device-pointer calls need actions alongside actions_u2");
+      if (t.score_f32 && dev && !t.score)
+        kt::fail(KTUNE_ERR_CONFIG, "rollout: device-pointer calls need score alongside score_f32");
       if (t.idx_u8)
         for (int c : t.space->card)
           if (c > 256) kt::fail(KTUNE_ERR_CONFIG, "rollout: idx_u8 needs every knob cardinality <= 256");
@@ -549,9 +562,10 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
         offs[k] = {slice(E * n * 2), slice(E * (T + 1) * n * 2), (t.actions || t.actions_u2) ? slice(E * T * n) : SIZE_MAX,
                    t.logp ? slice(E * T * 8) : SIZE_MAX, t.value ? slice(E * T * 8) : SIZE_MAX,
-                   t.score ? slice(E * (T + 1) * 8) : SIZE_MAX, t.logp_f32 ? slice(E * T * 4) : SIZE_MAX,
+                   (t.score || t.score_f32) ? slice(E * (T + 1) * 8) : SIZE_MAX, t.logp_f32 ? slice(E * T * 4) : SIZE_MAX,
                    t.value_f32 ? slice(E * T * 4) : SIZE_MAX, t.idx_u8 ? slice(E * (T + 1) * n) : SIZE_MAX,
-                   t.actions_u2 ? slice(E * T * ((n + 3) / 4)) : SIZE_MAX};
+                   t.actions_u2 ? slice(E * T * ((n + 3) / 4)) : SIZE_MAX,
+                   t.score_f32 ? slice(E * (T + 1) * 4) : SIZE_MAX};
       }
     }
     unsigned char* base = dev ? nullptr : (unsigned char*)ctx->dev(kt::WS_ROLLOUT, std::max<size_t>(arena, 256));
@@ -562,12 +576,13 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       const int64_t E = t.num_episodes;
       HostIo& h = io[k];
       if (dev) {
-        h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score, t.logp_f32, t.value_f32, t.idx_u8, t.actions_u2};
+        h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score, t.logp_f32, t.value_f32, t.idx_u8, t.actions_u2,
+             t.score_f32};
       } else {
         h = {(const uint16_t*)at(offs[k][0]), (uint16_t*)at(offs[k][1]), (int8_t*)at(offs[k][2]),
              (double*)at(offs[k][3]),         (double*)at(offs[k][4]),   (double*)at(offs[k][5]),
              (float*)at(offs[k][6]),          (float*)at(offs[k][7]),    (uint8_t*)at(offs[k][8]),
-             (uint8_t*)at(offs[k][9])};
+             (uint8_t*)at(offs[k][9]),        (float*)at(offs[k][10])};
         if (E > 0)
           KT_CUDA(cudaMemcpyAsync((void*)h.d_init, t.init_idx, (size_t)E * n * 2, cudaMemcpyHostToDevice, ctx->stream));
       }
@@ -599,7 +614,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     // max(compute, PCIe) instead of their sum.
     bool segmented = use_tc && !dev && T >= 128;
     for (int k = 0; k < num_tasks && segmented; ++k)
-      if (tasks[k].gbt && tasks[k].score && !tasks[k].gbt->d_inode_pk) segmented = false;
+      if (tasks[k].gbt && (tasks[k].score || tasks[k].score_f32) && !tasks[k].gbt->d_inode_pk) segmented = false;
     if (ctx->opt_rollout_segments == 1) segmented = false;
     const int S = !segmented ? 1
                   : ctx->opt_rollout_segments > 1 ? (int)std::min<int64_t>(ctx->opt_rollout_segments, T)
@@ -613,6 +628,15 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       kt::RowMap m;
       if (len != T + 1) m = kt::RowMap{len, (int64_t)T + 1, r0};
       kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx, 2, t.num_episodes * len, io[k].d_score, m);
+
+    };
+    auto score32_rows = [&](int k, int r0, int r1) {  // fp32 copies of the scores of rows [r0, r1]
+      const ktune_rollout_task& t = tasks[k];
+      if (!t.gbt || !io[k].d_s32 || t.num_episodes == 0) return;
+      const int64_t len = r1 - r0 + 1, work = t.num_episodes * len;
+      score_f32_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(work, 256), (int64_t)kt::sm_count(ctx) * 16), 256, 0,
+                         ctx->stream>>>(io[k].d_score, io[k].d_s32, t.num_episodes, T + 1, r0, len);
+      kt::check_launch(ctx, "score_f32");
     };
     auto narrow_rows = [&](int k, int r0, int r1) {  // uint16 -> uint8 trajectory rows [r0, r1]
       const ktune_rollout_task& t = tasks[k];
@@ -665,6 +689,9 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       if (t.score && t.gbt)
         KT_CUDA(cudaMemcpy2DAsync(t.score + r0, (T + 1) * 8, h.d_score + r0, (T + 1) * 8, rows * 8, E,
                                   cudaMemcpyDeviceToHost, st));
+      if (t.score_f32 && t.gbt)
+        KT_CUDA(cudaMemcpy2DAsync(t.score_f32 + r0, (T + 1) * 4, h.d_s32 + r0, (T + 1) * 4, rows * 4, E,
+                                  cudaMemcpyDeviceToHost, st));
     };
     std::vector<char> scored(num_tasks, 0);
     if (use_tc) {
@@ -682,6 +709,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
           }
           for (int k = 0; k < num_tasks; ++k) {
             score_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
+            score32_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
             narrow_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
             pack_steps(k, t0, t1);
           }
@@ -732,6 +760,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     // cost-model scores of every visited configuration (K1 over the trajectory)
     for (int k = 0; k < num_tasks; ++k) {
       if (!scored[k]) score_rows(k, 0, T);
+      score32_rows(k, 0, T);
       narrow_rows(k, 0, T);
       pack_steps(k, 0, T);
     }

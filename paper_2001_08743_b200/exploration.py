@@ -166,6 +166,7 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
         a.value_f32 = pp(o.get("value32"))
         a.idx_u8 = pp(o.get("idx8"))
         a.actions_u2 = pp(o.get("actions2"))
+        a.score_f32 = pp(o.get("score32"))
         outs.append(o)
     ctx.check(L.lib().ktune_rollout(ctx.h, len(tasks), arr, T,
                                     (L.F_DEVICE if dev else 0) | (L.F_EXACT_ROLLOUT if exact else 0)))

@@ -278,7 +278,9 @@ def test_rollout_fp32_outputs(O, ctx, exact):
                       value32=np.zeros((E, T), np.float32))
     o = mk()
     o["idx8"] = np.zeros((E, T + 1, sp.num_knobs), np.uint8)
+    o["score32"] = np.zeros((E, T + 1), np.float32)
     run_episodes_batch([RolloutTask(dspace, agent, dg, init, 0, 3)], T, host_out=[o], exact=exact)
+    assert np.array_equal(o["score32"], o["score"].astype(np.float32))
     assert np.array_equal(o["logp32"], o["logp"].astype(np.float32))
     assert np.array_equal(o["value32"], o["value"].astype(np.float32))
     assert np.array_equal(o["idx8"], o["idx"].astype(np.uint8)) and o["idx"].max() < 256
@@ -287,7 +289,9 @@ def test_rollout_fp32_outputs(O, ctx, exact):
     o2["idx8"] = np.zeros((E, T + 1, sp.num_knobs), np.uint8)
     o2["actions"] = None
     o2["actions2"] = np.zeros((E, T, (sp.num_knobs + 3) // 4), np.uint8)
+    o2["score"] = None
+    o2["score32"] = np.zeros((E, T + 1), np.float32)
     run_episodes_batch([RolloutTask(dspace, agent, dg, init, 0, 3)], T, host_out=[o2], exact=exact)
-    assert np.array_equal(o2["idx8"], o["idx8"]) and np.array_equal(o2["score"], o["score"])
+    assert np.array_equal(o2["idx8"], o["idx8"]) and np.array_equal(o2["score32"], o["score32"])
     from paper_2001_08743_b200.exploration import unpack_actions
     assert np.array_equal(unpack_actions(o2["actions2"], sp.num_knobs), o["actions"])
