@@ -216,7 +216,9 @@ def c3_pipeline(ctx, args):
     ctx.set_stream(stream.cuda_stream)
     run_episodes_batch([task], 8, ctx, device_out=True)  # warm-up
     roll = []
+    o = None
     for _ in range(3):  # median of 3 rollouts; the last one's trajectory feeds the sampling stages
+        o = None  # release the previous trajectory first: the caching allocator reuses its blocks
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         o = run_episodes_batch([task], T, ctx, device_out=True)[0]
