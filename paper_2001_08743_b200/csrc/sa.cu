@@ -68,8 +68,8 @@ __device__ __forceinline__ double walk(const uint32_t* __restrict__ s_node, cons
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const uint32_t w = s_node[(tr + g) * NI + nd[g]];
-        const int v = *reinterpret_cast<const int*>(col + (w >> 16));
-        nd[g] = 2 * nd[g] + 1 + (v >= (int)(w & 0xFFFFu) ? 1 : 0);
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(col + (w >> 16));
+        nd[g] = 2 * nd[g] + 1 + (v >= w ? 1 : 0);  // tagged column entry vs node word: one compare
       }
     }
 #pragma unroll
@@ -80,8 +80,8 @@ __device__ __forceinline__ double walk(const uint32_t* __restrict__ s_node, cons
 #pragma unroll
     for (int l = 0; l < DEPTH; ++l) {
       const uint32_t w = s_node[tr * NI + nd];
-      const int v = *reinterpret_cast<const int*>(col + (w >> 16));
-      nd = 2 * nd + 1 + (v >= (int)(w & 0xFFFFu) ? 1 : 0);
+      const uint32_t v = *reinterpret_cast<const uint32_t*>(col + (w >> 16));
+      nd = 2 * nd + 1 + (v >= w ? 1 : 0);
     }
     s = kt::dadd(s, s_leaf[tr * NL + (nd - NI)]);
   }
@@ -93,16 +93,16 @@ __device__ __forceinline__ void store_row(uint16_t* row, const int32_t* col, int
   if (vec == 8) {
     for (int d = 0; d < D; d += 8) {
       uint4 q;
-      q.x = (uint32_t)col[(d + 0) * kSaThreads] | ((uint32_t)col[(d + 1) * kSaThreads] << 16);
-      q.y = (uint32_t)col[(d + 2) * kSaThreads] | ((uint32_t)col[(d + 3) * kSaThreads] << 16);
-      q.z = (uint32_t)col[(d + 4) * kSaThreads] | ((uint32_t)col[(d + 5) * kSaThreads] << 16);
-      q.w = (uint32_t)col[(d + 6) * kSaThreads] | ((uint32_t)col[(d + 7) * kSaThreads] << 16);
+      q.x = __byte_perm((uint32_t)col[(d + 0) * kSaThreads], (uint32_t)col[(d + 1) * kSaThreads], 0x5410);
+      q.y = __byte_perm((uint32_t)col[(d + 2) * kSaThreads], (uint32_t)col[(d + 3) * kSaThreads], 0x5410);
+      q.z = __byte_perm((uint32_t)col[(d + 4) * kSaThreads], (uint32_t)col[(d + 5) * kSaThreads], 0x5410);
+      q.w = __byte_perm((uint32_t)col[(d + 6) * kSaThreads], (uint32_t)col[(d + 7) * kSaThreads], 0x5410);
       *reinterpret_cast<uint4*>(row + d) = q;
     }
   } else if (vec == 2) {
     for (int d = 0; d < D; d += 2)
       *reinterpret_cast<uint32_t*>(row + d) =
-          (uint32_t)col[d * kSaThreads] | ((uint32_t)col[(d + 1) * kSaThreads] << 16);
+          __byte_perm((uint32_t)col[d * kSaThreads], (uint32_t)col[(d + 1) * kSaThreads], 0x5410);
   } else {
     for (int d = 0; d < D; ++d) row[d] = (uint16_t)col[d * kSaThreads];
   }
@@ -131,7 +131,9 @@ __global__ void __launch_bounds__(kSaThreads) sa_kernel(const __grid_constant__ 
   int32_t* col = s_col + threadIdx.x;  // col[d * kSaThreads]
   const unsigned char* colb = reinterpret_cast<const unsigned char*>(col);
   uint16_t* out = tk.idx + c * (int64_t)(T + 1) * D;
-  for (int d = 0; d < D; ++d) col[d * kSaThreads] = tk.init_idx[c * D + d];
+  // column entries carry their own byte offset in the high half, (coff << 16) | idx, like the
+  // node words (coff << 16) | t1: a node test is one unsigned compare (the K1 encoding)
+  for (int d = 0; d < D; ++d) col[d * kSaThreads] = (int32_t)(((uint32_t)(d * kSaThreads * 4) << 16) | tk.init_idx[c * D + d]);
   store_row(out, col, D, tk.row_vec);
   double f = walk<DEPTH>(s_node, s_leaf, colb, tk.ntrees, tk.base, tk.lr);
   double* sc = tk.score + c * (int64_t)(T + 1);
@@ -145,9 +147,10 @@ __global__ void __launch_bounds__(kSaThreads) sa_kernel(const __grid_constant__ 
     const int knob = (int)kt::dmul(u0, (double)D);
     const int dir = u1 < 0.5 ? -1 : 1;
     const int old = col[knob * kSaThreads];
-    int v = old + dir;
+    const int tag = old & ~0xFFFF;
+    int v = (old & 0xFFFF) + dir;
     v = v < 0 ? 0 : (v > tk.card[knob] - 1 ? tk.card[knob] - 1 : v);
-    col[knob * kSaThreads] = v;
+    col[knob * kSaThreads] = tag | v;
     const double fp = walk<DEPTH>(s_node, s_leaf, colb, tk.ntrees, tk.base, tk.lr);
     const double delta = kt::dsub(fp, f);
     const bool accept = delta >= 0.0 || u2 < kt::kt_exp(kt::ddiv(delta, temp));
