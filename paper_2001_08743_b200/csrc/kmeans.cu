@@ -47,6 +47,30 @@ __device__ __forceinline__ double feat(const KtSpaceParams& sp, const double* lu
   return lut_s[sp.lut_off[d] + (int)p[d]];
 }
 
+// The D knob indices of row p as fp64 features, one 16-byte (or 8-byte) load when the row
+// is that wide and aligned (D = 8 uint16 / uint8 rows), else per element.
+template <class IdxT, int DM>
+__device__ __forceinline__ void load_feats(const KtSpaceParams& sp, const double* lut_s, const IdxT* p, int D,
+                                           double (&x)[DM]) {
+  if (DM == 8 && D == 8 && (reinterpret_cast<uintptr_t>(p) & (sizeof(IdxT) * 8 - 1)) == 0) {
+    uint32_t w[4];
+    if (sizeof(IdxT) == 2) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+      w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) x[d] = lut_s[sp.lut_off[d] + (int)((w[d >> 1] >> (16 * (d & 1))) & 0xFFFFu)];
+    } else {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+      w[0] = v.x; w[1] = v.y;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) x[d] = lut_s[sp.lut_off[d] + (int)((w[d >> 2] >> (8 * (d & 3))) & 0xFFu)];
+    }
+    return;
+  }
+#pragma unroll
+  for (int d = 0; d < DM; ++d) x[d] = d < D ? feat(sp, lut_s, p, d) : 0.0;
+}
+
 // Sequential squared distance.
 template <class IdxT>
 __device__ __forceinline__ double row_d2(const KtSpaceParams& sp, const double* lut, const IdxT* p,
@@ -334,8 +358,7 @@ __global__ void __launch_bounds__(kBT) assign_kernel(KtSpaceParams sp, int lut_t
     const int64_t i = base + j * kBT + threadIdx.x;
     if (i < N) {
       double x[DM];  // DM >= D, compile-time: the features stay in registers
-#pragma unroll
-      for (int d = 0; d < DM; ++d) x[d] = d < D ? feat(sp, lut, pts + i * D, d) : 0.0;
+      load_feats<IdxT, DM>(sp, lut, pts + i * D, D, x);
       double best = INFINITY;
       int bc = 0;
       for (int c = 0; c < k; ++c) {
@@ -475,22 +498,33 @@ __global__ void add_sums_kernel(unsigned long long* __restrict__ cs, const unsig
 // strictly below every other cluster's. Fused: the integer sums are updated in
 // place by the points that changed cluster (block-aggregated deltas), plus the
 // changed / uncertain counts and the loss estimate.
+// 128-thread blocks (8 points per thread per 1024-point chunk): twice the resident blocks
+// of the 256-thread layout, so 1M points (1024 chunks) run in one wave instead of 1.7
+constexpr int kCertBT = 128;
+// dynamic shared memory of assign_cert_kernel<IdxT, DM> for k clusters (layout in the kernel)
+inline size_t cert_smem_bytes(int k, int D, int DM, size_t lut_bytes) {
+  const size_t dbl = (size_t)((k * D + kt::kMaxK + 1) & ~1) * 8;
+  const size_t ints = (size_t)k * DM * 4 + (size_t)k * D * 4 + (size_t)(((k + 1) & ~1) + ((k * D) & 1)) * 4;
+  return dbl + ints + lut_bytes + 16;
+}
 template <class IdxT, int DM>
-__global__ void __launch_bounds__(kBT) assign_cert_kernel(
+__global__ void __launch_bounds__(kCertBT) assign_cert_kernel(
     KtSpaceParams sp, int lut_total, const IdxT* __restrict__ pts, int64_t N, const double* __restrict__ cB,
     const double* __restrict__ dB, int k, const int32_t* __restrict__ prev, int32_t* __restrict__ asg,
     double* __restrict__ d2, double* __restrict__ chunk_sum, unsigned long long* __restrict__ counters,
     unsigned long long* __restrict__ g_sum, unsigned long long* __restrict__ g_cnt, int64_t chunk0) {
-  extern __shared__ double sdyn[];
+  extern __shared__ __align__(16) double sdyn[];
   __shared__ double red[32];
-  __shared__ int32_t s_sum[kt::kMaxK * kt::kMaxKnobs];
-  __shared__ int32_t s_cnt[kt::kMaxK];
-  __shared__ __align__(16) float s_c32[kt::kMaxK * kt::kMaxKnobs];  // [k][DM], zero-padded
   __shared__ float s_amax;
   const int D = sp.D;
+  // dynamic layout sized by k (cert_smem_bytes): c_B (fp64), E_c, c_B rows in fp32 zero-padded to
+  // DM (16-byte aligned for float4), the block's integer-sum deltas and counts, the feature table
   double* s_c = sdyn;
   double* s_e = sdyn + k * D;  // per-cluster centroid-difference bound E_c
-  double* s_lut = sdyn + k * D + kt::kMaxK;
+  float* s_c32 = reinterpret_cast<float*>(sdyn + ((k * D + kt::kMaxK + 1) & ~1));  // [k][DM]
+  int32_t* s_sum = reinterpret_cast<int32_t*>(s_c32 + k * DM);
+  int32_t* s_cnt = s_sum + k * D;
+  double* s_lut = reinterpret_cast<double*>(s_cnt + ((k + 1) & ~1) + ((k * D) & 1));
   // fp32 screening bound |s32 - d2_ref| <= A + R s32 for every cluster (features and
   // centroids in [0, 1]): conversions and the difference cost <= 1.5 ulp(1) per knob,
   // squaring <= 2x that, the FMA chain D 2^-24 relative; A also carries max_c E_c and
@@ -518,16 +552,15 @@ __global__ void __launch_bounds__(kBT) assign_cert_kernel(
   double part = 0.0;
   int nchg = 0, nunc = 0;
   const double grow = (double)(2 * D + 4) * 0x1.0p-53;
-  for (int j = 0; j < kChunk / kBT; ++j) {
-    const int64_t i = base + j * kBT + threadIdx.x;
+  for (int j = 0; j < kChunk / kCertBT; ++j) {
+    const int64_t i = base + j * kCertBT + threadIdx.x;
     const bool live = i < N;
     int bc = 0;
     if (live) {
       // (1) fp32 screening: the winner is certified if the runner-up's interval lies
       // strictly above the winner's: s2 (1 - R) - A > s1 (1 + R) + A
       double x[DM];  // DM >= D, compile-time: the features stay in registers
-#pragma unroll
-      for (int d = 0; d < DM; ++d) x[d] = d < D ? feat(sp, lut, pts + i * D, d) : 0.0;
+      load_feats<IdxT, DM>(sp, lut, pts + i * D, D, x);
       float xf[DM];
 #pragma unroll
       for (int d = 0; d < DM; ++d) xf[d] = (float)x[d];  // padded knobs add 0 exactly
@@ -1685,7 +1718,7 @@ struct KMeans {
       dzero = dB + nb;                      // exact centroids: every bound 0
       KT_CUDA(cudaMemsetAsync(dzero, 0, sizeof(double) * nb, ctx->stream));
     }
-    screen_smem = sizeof(double) * (kt::kMaxK * D + kt::kMaxK) + lut_smem;
+    screen_smem = cert_smem_bytes(kt::kMaxK, D, D <= 8 ? 8 : (D <= 16 ? 16 : kt::kMaxKnobs), lut_smem);
     KT_DISPATCH_DM(D, KT_CUDA(cudaFuncSetAttribute(assign_cert_kernel<IdxT, DM_>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_smem)));
     rb_host = (IterReadback*)ctx->host(3, sizeof(IterReadback) * 8);
@@ -1769,7 +1802,7 @@ struct KMeans {
       const int64_t nloc = sharded ? std::max<int64_t>(0, std::min<int64_t>(nchunks, c0 + shard_chunks) - c0) : nchunks;
       if (nloc > 0) {
         kt::ProfScope prof(ctx, KTUNE_STAT_ASSIGN_NS);
-        KT_DISPATCH_DM(D, assign_cert_kernel<IdxT, DM_><<<(unsigned)nloc, kBT, screen_smem, s()>>>(
+        KT_DISPATCH_DM(D, assign_cert_kernel<IdxT, DM_><<<(unsigned)nloc, kCertBT, cert_smem_bytes(k, D, DM_, lut_smem), s()>>>(
                               sp->params, lut_total, pts, N, cent, dzero, k, prev, asg, dd, chunk, ull, nullptr,
                               nullptr, c0));
         kt::check_launch(ctx, "assign_screen");
@@ -1937,7 +1970,7 @@ struct KMeans {
     double loss = assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);  // exact
     iter_losses.assign(1, loss);
     const size_t words = (size_t)kt::kMaxK * (kt::kMaxKnobs + 1);
-    const size_t tsmem = sizeof(double) * (k * D + kt::kMaxK) + lut_smem;  // <= screen_smem (setup's attribute)
+    const size_t tsmem = cert_smem_bytes(k, D, D <= 8 ? 8 : (D <= 16 ? 16 : kt::kMaxKnobs), lut_smem);  // <= screen_smem
     int cur = 0;
     KT_CUDA(cudaMemsetAsync(isum[cur], 0, sizeof(unsigned long long) * words, s()));
     cluster_sums_kernel<IdxT><<<(unsigned)nchunks, kBT, 0, s()>>>(pts, N, D, k, asg_a, isum[cur],
@@ -1969,7 +2002,7 @@ struct KMeans {
       unsigned long long* tgt = sharded ? dsum : cs;
       if (sharded) KT_CUDA(cudaMemsetAsync(dsum, 0, sizeof(unsigned long long) * words, s()));
       if (nloc > 0)
-        KT_DISPATCH_DM(D, assign_cert_kernel<IdxT, DM_><<<(unsigned)nloc, kBT, tsmem, s()>>>(
+        KT_DISPATCH_DM(D, assign_cert_kernel<IdxT, DM_><<<(unsigned)nloc, kCertBT, tsmem, s()>>>(
                               sp->params, lut_total, pts, N, cB, dB, k, asg_a, asg_b, d2_b, chunk, ull, tgt,
                               tgt + (size_t)kt::kMaxK * kt::kMaxKnobs, c0));
       kt::check_launch(ctx, "assign_cert", 2);
