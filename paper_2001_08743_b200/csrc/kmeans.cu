@@ -1587,6 +1587,29 @@ __global__ void gather_readback_kernel(const double* dscal, const unsigned long 
   *seqcnt = 0;
 }
 
+// Certified iteration tail in one launch: the loss estimate over the chunk sums, the
+// iteration's readback, then the counters cleared for the next iteration.
+__global__ void __launch_bounds__(1024) sum_gather_kernel(const double* __restrict__ cs, int64_t n, double* dscal,
+                                                          unsigned long long* ull, int32_t* seqcnt,
+                                                          const int32_t* segs, IterReadback* outs, int* slot) {
+  __shared__ double red[32];
+  double p = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) p = kt::dadd(p, cs[i]);
+  const double s = block_sum(p, red);
+  if (threadIdx.x == 0) {
+    dscal[0] = s;
+    IterReadback* out = outs + (*slot)++;
+    out->loss = s;
+    out->changed = ull[0];
+    out->seq = *seqcnt;
+    out->segs = *segs;
+    out->unc = ull[2];
+    out->empty = ull[3];
+    *seqcnt = 0;
+    ull[0] = ull[1] = ull[2] = ull[3] = 0;
+  }
+}
+
 // CUDA graph capture is illegal on the legacy default stream (a context bound to
 // torch's default stream); those runs take the uncaptured paths.
 inline bool capturable(cudaStream_t st) { return st != nullptr && st != cudaStreamLegacy; }
@@ -1995,8 +2018,9 @@ struct KMeans {
     const int64_t c0 = sharded ? (int64_t)rank * shard_chunks : 0;
     const int64_t nloc = sharded ? std::max<int64_t>(0, std::min<int64_t>(nchunks, c0 + shard_chunks) - c0) : nchunks;
     unsigned long long* dsum = isum[1];
+    if (!sharded) KT_CUDA(cudaMemsetAsync(ull, 0, 32, s()));  // then cleared by each iteration's tail
     auto enqueue_iter = [&]() {
-      KT_CUDA(cudaMemsetAsync(ull, 0, 32, s()));
+      if (sharded) KT_CUDA(cudaMemsetAsync(ull, 0, 32, s()));
       centroids_from_sums_kernel<<<1, 1024, 0, s()>>>(sp->params, k, cs, cs + (size_t)kt::kMaxK * kt::kMaxKnobs, cB,
                                                       dB, ull + 3, std::ldexp(1.0, (int)ctx->opt_kmeans_bound_log2));
       unsigned long long* tgt = sharded ? dsum : cs;
@@ -2006,6 +2030,11 @@ struct KMeans {
                               sp->params, lut_total, pts, N, cB, dB, k, asg_a, asg_b, d2_b, chunk, ull, tgt,
                               tgt + (size_t)kt::kMaxK * kt::kMaxKnobs, c0));
       kt::check_launch(ctx, "assign_cert", 2);
+      if (!sharded) {
+        sum_gather_kernel<<<1, 1024, 0, s()>>>(chunk, nloc, dscal, ull, seqcnt, csb + k, rb_dev, rb_slot);
+        kt::check_launch(ctx, "sum_gather");
+        return;
+      }
       if (nloc > 0) sum_chunks_kernel<<<1, 1024, 0, s()>>>(chunk + c0, nloc, dscal);
       else KT_CUDA(cudaMemsetAsync(dscal, 0, 8, s()));
       if (sharded) {
