@@ -116,3 +116,25 @@ def test_make_candidate_set_matches_reference(O, ref_ok, seed):
     assert rc == 0
     want = O.make_candidate_set(1, np.zeros((n, 1), np.int32), ids, pred, "ref")
     assert np.array_equal(rows[:m.value], want)
+
+
+def test_unpack_actions_roundtrip():
+    """2-bit action codes (the rollout's actions_u2 output): byte j holds knobs 4j..4j+3 as
+    (direction + 1) << 2 (d - 4j); unpacking restores the int8 directions for any D."""
+    from paper_2001_08743_b200.exploration import unpack_actions
+    g = np.random.default_rng(3)
+    for D in (1, 3, 4, 7, 8, 16, 21):
+        a = g.integers(-1, 2, (5, 9, D)).astype(np.int8)
+        packed = np.zeros((5, 9, (D + 3) // 4), np.uint8)
+        for d in range(D):
+            packed[..., d // 4] |= ((a[..., d] + 1).astype(np.uint8) << (2 * (d % 4))).astype(np.uint8)
+        assert np.array_equal(unpack_actions(packed, D), a)
+
+
+def test_host_empty_without_cuda_is_numpy():
+    """Default host outputs: pinned (torch caching allocator) on a GPU box, plain numpy here."""
+    from paper_2001_08743_b200.context import host_empty
+    x = host_empty((3, 4), np.float32)
+    assert isinstance(x, np.ndarray) and x.shape == (3, 4) and x.dtype == np.float32
+    y = host_empty((2, 5), np.uint16)
+    assert y.dtype == np.uint16 and y.shape == (2, 5)
