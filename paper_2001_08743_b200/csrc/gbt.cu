@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) gbt_predict_idx_kernel(
 // column+offset, compare, 2n+1+right. kScoreCfg configurations per thread (ILP), a
 // persistent grid over kScoreCfg*256-config chunks, trees + knob-index columns in smem.
 constexpr int kScoreThreads = 256;
-constexpr int kScoreCfg = 2;  // configurations per thread (independent walks in flight)
+constexpr int kScoreCfg = 3;  // configurations per thread (independent walks in flight)
 template <class IdxT, int DEPTH>
 __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
     const IdxT* __restrict__ idx, int64_t B, int D, int T, const uint32_t* __restrict__ g_node,
