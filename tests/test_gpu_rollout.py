@@ -148,8 +148,8 @@ def test_rollout_tc_equals_exact_kernel_at_scale(O, ctx):
     assert nfb < 0.01 * steps
 
 
-@pytest.mark.parametrize("E", [60_001, 2 * 56_832 + 97])
-def test_rollout_more_episodes_than_one_wave(O, ctx, E):
+@pytest.mark.parametrize("E,T", [(60_001, 6), (2 * 56_832 + 97, 6), (60_001, 130)])
+def test_rollout_more_episodes_than_one_wave(O, ctx, E, T):
     """A workload larger than one resident wave (12 warps on every SM) runs as full
     waves plus a thin remainder over every SM: the same trajectories as the exact
     kernel, episodes keyed by their global id across the wave boundary."""
@@ -157,8 +157,8 @@ def test_rollout_more_episodes_than_one_wave(O, ctx, E):
     sp, osp, og, dspace, dg, agent = _setup(O, ctx, "synthetic8", seed=4)
     init = np.random.default_rng(E).integers(0, 2, (E, sp.num_knobs))
     task = RolloutTask(dspace, agent, dg, init, episode_offset=5, root_seed=4)
-    fast = run_episodes_batch([task], 6)[0]
-    exact = run_episodes_batch([task], 6, exact=True)[0]
+    fast = run_episodes_batch([task], T)[0]  # T >= 128: the segmented host path, every segment in waves
+    exact = run_episodes_batch([task], T, exact=True)[0]
     assert np.array_equal(fast["idx"], exact["idx"])
     assert np.array_equal(fast["actions"], exact["actions"])
     assert np.array_equal(fast["score"], exact["score"])
