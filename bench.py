@@ -135,60 +135,170 @@ def dist_env():
     return world, rank, local
 
 
-def build_tasks(args, rank):
-    from paper_2001_08743_b200 import spaces as S
-    from paper_2001_08743_b200.workloads import make_tasks
+def build_tasks(args, rank, product=True):
+    """The headline workload: ResNet-18's 12 tasks x E episodes (workloads/, builder-defined,
+    SURVEY.md §8d). product=False builds the same specs without importing the product
+    package (the reference arm)."""
+    if product:
+        from paper_2001_08743_b200 import spaces as S
+    else:
+        from workloads import spaces as S
+    from workloads.tasks import make_tasks
     spaces = S.resnet18_tasks()[: args.tasks]
     return make_tasks(spaces, args.episodes, seed=args.seed + 7919 * rank)
 
 
-def cpu_sample(specs, models, agents_params, args, threads):
-    """Oracle (CPU restatement; the rollout has no reference code) on a bounded sample."""
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_sample(specs, models, agents_params, E, T, threads):
+    """The CPU rollout (oracle/ktune_oracle.c: the rollout has no reference code, its scoring
+    is bit-identical to the reference's predict_batch) over episodes [0, E) x steps [0, T) of
+    the bench's own tasks: a prefix of exactly the timed workload."""
     from oracle import pyoracle as O
-    from paper_2001_08743_b200.spaces import stream_seed
-    E, T = args.cpu_episodes, args.cpu_T
+    from workloads.spaces import stream_seed
     t0 = time.perf_counter()
     n = 0
     for spec, m, p in zip(specs, models, agents_params):
         osp = O.OSpace(spec.space)
         og = O.Gbt(m.base_prediction, m.learning_rate, m.num_features, m.offsets, m.feature, m.left, m.right,
-                   m.threshold, m.value, m.training_sse)
-        O.run_episodes(osp, og, 128, 64, p, spec.init_idx[:E], T, 0, stream_seed(spec.seed, "explore"),
+                   m.threshold, m.value, m.training_sse) if hasattr(m, "base_prediction") else m
+        init = spec.init_idx[:E]
+        O.run_episodes(osp, og, 128, 64, p, init, T, 0, stream_seed(spec.seed, "explore"),
                        threads=threads, want_traj=True)
-        n += E * T
+        n += len(init) * T
     dt = time.perf_counter() - t0
-    return n / dt, f"{len(specs)} tasks x {E} episodes x {T} steps ({n} config-steps) in {dt:.2f}s"
+    return n / dt, f"{len(specs)} tasks x {n // (T * len(specs))} episodes x {T} steps ({n} config-steps) in {dt:.2f}s"
+
+
+def cpu_baselines(specs, models, params, args):
+    """All host threads over the first args.cpu_T steps of every episode of every task, plus the
+    single-thread figure (the reference's hot path is single-threaded) on a smaller prefix."""
+    threads = os.cpu_count() or 1
+    v, sample = cpu_sample(specs, models, params, args.episodes, args.cpu_T, threads)
+    v1, sample1 = cpu_sample(specs, models, params, args.cpu1_episodes, args.cpu_T, 1)
+    return {"value": v, "unit": "config-steps/s", "cores": threads, "kind": "port", "sample": sample,
+            "cpu_model": cpu_model(), "same_config": True,
+            "prefix": f"steps [0, {args.cpu_T}) of the timed workload's episodes (same tasks, seeds, models)",
+            "single_thread": {"value": v1, "cores": 1, "sample": sample1}}
 
 
 def run_reference(args):
+    """--impl reference: the CPU path on the box's host cores, without importing the product:
+    spaces from workloads/ (pure Python), the GBT fitted by the REFERENCE's own fit_gbt
+    (oracle/_ref, cost_model.cpp:126-177), the agent initialised by the oracle (ko_ac_init),
+    the rollout + scoring by the oracle restatement."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from paper_2001_08743_b200.cost_model import fit_gbt
-    from paper_2001_08743_b200.exploration import init_parameters
-    from paper_2001_08743_b200.workloads import encode
-    specs = build_tasks(args, 0)
-    models = [fit_gbt(encode(s.space, s.train_idx), s.train_y, seed=s.seed) for s in specs]
-    params = [init_parameters(s.space.num_knobs, 128, 64, s.seed) for s in specs]
+    from oracle import pyoracle as O
+    from workloads.tasks import encode
+    specs = build_tasks(args, 0, product=False)
+    models = [O.ref_fit_gbt(encode(s.space, s.train_idx), s.train_y, seed=s.seed) for s in specs]
+    params = [O.ac_init(s.space.num_knobs, 128, 64, s.seed) for s in specs]
     threads = os.cpu_count() or 1
     vals = []
+    sample = ""
     for i in range(args.warmup + args.steps):
-        v, sample = cpu_sample(specs, models, params, args, threads)
+        v, sample = cpu_sample(specs, models, params, args.episodes, args.cpu_T, threads)
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
+    v1, sample1 = cpu_sample(specs, models, params, args.cpu1_episodes, args.cpu_T, 1)
+    units = len(specs) * args.episodes * args.cpu_T
     line = {"metric": "candidate configs scored/sec (rollout+cost model)", "value": value,
             "unit": "config-steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * (args.cpu_episodes * args.cpu_T * len(specs)) / value,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded AutoTVM-style ResNet-18 conv spaces, SyntheticBackend-fitted GBT)",
-            "config": {"workload": "resnet18-12tasks-rollout (CPU sample)", "tasks": len(specs),
-                       "episodes_per_task": args.cpu_episodes, "T": args.cpu_T},
+            "ms_per_step": 1e3 * units / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": DATA_NOTE, "config": headline_config(args, args.gpus),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "config-steps/s", "cores": threads, "kind": "port",
-                             "sample": sample},
+                             "sample": f"per step: {sample}", "cpu_model": cpu_model(), "same_config": True,
+                             "prefix": f"each step runs steps [0, {args.cpu_T}) of every episode of the "
+                                       f"timed workload (same tasks, seeds, models, agents)",
+                             "single_thread": {"value": v1, "cores": 1, "sample": sample1}},
             "e2e": {"value": value, "unit": "config-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+DATA_NOTE = ("synthetic (seeded AutoTVM-style ResNet-18 conv spaces, GBT fitted on SyntheticBackend samples, "
+             "seeded agent, initial configs by random_valid_configuration)")
+
+
+def headline_config(args, world):
+    return {"workload": "resnet18-12tasks-rollout (BASELINE configs[1])", "tasks": args.tasks,
+            "episodes_per_task_per_gpu": args.episodes, "T": args.T, "knobs": 8, "hidden": [128, 64],
+            "gbt": "50 trees depth<=4",
+            "path": ("exact fp64 kernel (bit-exact with the oracle)" if args.exact else
+                     "tcgen05 rollout, certified sampling: configs/actions/scores bit-exact with the "
+                     "oracle, logp/value fp32-accurate"),
+            "l2": "256 MB buffer written between timed steps; outputs 1.2 GB/step > L2",
+            "parallelism": f"dp{world} (episodes sharded, no collective)"}
+
+
+def c1_secondary(ctx, args):
+    """SURVEY C1 = BASELINE configs[0] timed IN FULL on the GPU and on one CPU core: one
+    Chameleon iteration on a ResNet-18 conv layer (resnet18.c2): 64 configs x 500 steps of
+    run_episodes (rollout + GBT scoring + the CandidateSet of every visited configuration),
+    then adaptive_sample over that CandidateSet (k sweep, snap, synthesis against the visited
+    set = the 64 initial configs). GPU: the product's public API with host arrays in and out;
+    CPU: the oracle rollout (1 thread) + the REFERENCE's make_candidate_set and
+    adaptive_sample (oracle/_ref). The selected configurations are compared."""
+    from oracle import pyoracle as O
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
+    from paper_2001_08743_b200.exploration import ActorCritic, run_episodes
+    from paper_2001_08743_b200.sampling import SamplingParams, adaptive_sample
+    from workloads.tasks import encode, make_tasks
+    sp = S.resnet18_tasks()[1]
+    spec = make_tasks([sp], 64, seed=args.seed + 11)[0]
+    ds = Space(sp, ctx)
+    model = fit_gbt(encode(sp, spec.train_idx), spec.train_y, seed=spec.seed)
+    g = DeviceGbt(model, ds)
+    agent = ActorCritic(sp.num_knobs, 128, 64, seed=spec.seed, ctx=ctx)
+    visited = ds.id_of(spec.init_idx)
+    T = 500
+
+    def gpu_iter():
+        cands, _ = run_episodes(ds, g, agent, spec.init_idx, T, root_seed=spec.seed)
+        return cands, adaptive_sample(ds, cands, visited, SamplingParams(), rng_seed=spec.seed)
+
+    gpu_iter()  # warm-up
+    ts = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        cands, sel = gpu_iter()
+        ts.append(time.perf_counter() - t0)
+    gpu_ms = 1e3 * float(np.median(ts))
+    osp = O.OSpace(sp)
+    og = O.Gbt(model.base_prediction, model.learning_rate, model.num_features, model.offsets, model.feature,
+               model.left, model.right, model.threshold, model.value, model.training_sse)
+    t0 = time.perf_counter()
+    ro = O.run_episodes(osp, og, 128, 64, agent.params, spec.init_idx, T, 0, S.stream_seed(spec.seed, "explore"))
+    t1 = time.perf_counter()
+    flat = ro["idx"].reshape(-1, sp.num_knobs)
+    pred = ro["score"].reshape(-1)
+    rows = O.make_candidate_set(sp.num_knobs, flat, osp.ids(flat), pred, impl="ref")
+    t2 = time.perf_counter()
+    ref = O.ref_adaptive_sample(osp, flat[rows], osp.ids(flat[rows]), pred[rows], visited,
+                                rng_seed=spec.seed)
+    t3 = time.perf_counter()
+    cpu_ms = 1e3 * (t3 - t0)
+    return {"workload": "SURVEY C1 = BASELINE configs[0]: resnet18.c2 space, 64 configs x 500 steps + "
+                        "CandidateSet + adaptive_sample, timed in full",
+            "gpu_ms": gpu_ms, "cpu_ms": cpu_ms, "speedup": cpu_ms / gpu_ms,
+            "cpu": {"cores": 1, "rollout_ms": 1e3 * (t1 - t0), "candidate_set_ms": 1e3 * (t2 - t1),
+                    "adaptive_sample_ms": 1e3 * (t3 - t2), "kind": "port rollout + reference sampling"},
+            "candidates": len(cands), "selected": int(len(sel)),
+            "selected_equal_reference": bool(np.array_equal(np.asarray(sel, np.int32), ref["configs"])),
+            "candidate_set_equal_reference": bool(np.array_equal(np.asarray(cands.idx, np.int32), flat[rows]))}
 
 
 def c3_pipeline(ctx, args):
@@ -202,7 +312,7 @@ def c3_pipeline(ctx, args):
     from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
     from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
     from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep, candidates_from_rows
-    from paper_2001_08743_b200.workloads import encode, make_tasks
+    from workloads.tasks import encode, make_tasks
     sp = S.vgg16_tasks()[3]
     spec = make_tasks([sp], args.c3_episodes, seed=args.seed + 33)[0]
     ds = Space(sp, ctx)
@@ -252,7 +362,7 @@ def gbt_standalone(ctx, args, specs, spaces, gbts):
     16M random configurations, u8 indices), rows/s with its HBM roofline (D + 8 bytes per config:
     the row read, the fp64 score written) — the kernel is shared-memory (LSU) bound by design."""
     import torch
-    from paper_2001_08743_b200.workloads import random_configs
+    from workloads.tasks import random_configs
     sp, ds, g = specs[0].space, spaces[0], gbts[0]
     n = args.gbt_rows
     idx = torch.from_numpy(random_configs(sp, n, 17).astype(ds.idx_dtype).view(np.int8 if ds.index_bytes == 1 else np.int16)).cuda()
@@ -293,7 +403,7 @@ def kmeans_secondary(ctx, args, cpu=True):
     from paper_2001_08743_b200 import spaces as S
     from paper_2001_08743_b200.context import Space
     from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep, kmeans_run
-    from paper_2001_08743_b200.workloads import encode, random_configs
+    from workloads.tasks import encode, random_configs
     sp = S.alexnet_tasks()[1]
     ds = Space(sp, ctx)
     idx = random_configs(sp, args.kmeans_n, 123)
@@ -398,7 +508,7 @@ def c5_secondary(ctx, args):
     from paper_2001_08743_b200.context import Space
     from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
     from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
-    from paper_2001_08743_b200.workloads import encode, make_tasks
+    from workloads.tasks import encode, make_tasks
     sp = S.synthetic_space(0, 16)
     spec = make_tasks([sp], 1, seed=args.seed + 77)[0]
     E, T = args.c5_episodes, args.c5_T
@@ -450,8 +560,9 @@ def main():
     ap.add_argument("--episodes", type=int, default=4096)
     ap.add_argument("--T", type=int, default=500)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--cpu-episodes", type=int, default=128)
-    ap.add_argument("--cpu-T", type=int, default=500)
+    ap.add_argument("--cpu-T", type=int, default=8, help="CPU legs: steps [0, cpu_T) of every timed episode")
+    ap.add_argument("--cpu1-episodes", type=int, default=256, help="single-thread CPU figure: episodes per task")
+    ap.add_argument("--no-c1", action="store_true", help="skip SURVEY C1 (BASELINE configs[0]) timed in full")
     ap.add_argument("--kmeans-n", type=int, default=1 << 20)
     ap.add_argument("--kmeans-cpu-n", type=int, default=200_000)
     ap.add_argument("--kmeans-cpu-iters", type=int, default=5)
@@ -493,7 +604,7 @@ def main():
     from paper_2001_08743_b200.context import Context, Space
     from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
     from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
-    from paper_2001_08743_b200.workloads import encode
+    from workloads.tasks import encode
 
     from paper_2001_08743_b200.distributed import create_context
     # the library's NCCL communicator is only needed by the sharded k-means (--kmeans-dist)
@@ -717,13 +828,16 @@ def main():
         except Exception as ex:  # reported, not hidden
             kmeans = {"error": repr(ex)}
 
+    c1 = None
+    if rank == 0 and world == 1 and not args.no_c1:
+        try:
+            c1 = c1_secondary(ctx, args)
+        except Exception as ex:  # reported, not hidden
+            c1 = {"error": repr(ex)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        from paper_2001_08743_b200.exploration import init_parameters
-        params = [a.params for a in agents]
-        threads = os.cpu_count() or 1
-        v, sample = cpu_sample(specs, models, params, args, threads)
-        cpu = {"value": v, "unit": "config-steps/s", "cores": threads, "kind": "port", "sample": sample}
+        cpu = cpu_baselines(specs, models, [a.params for a in agents], args)
 
     if rank == 0:
         line = {
@@ -732,15 +846,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f64" if args.exact else "f32 (fp16 hi/lo tcgen05 MLP, fp32 accum) + f64 (scores, certified fallback)",
-            "data": "synthetic (seeded AutoTVM-style ResNet-18 conv spaces, SyntheticBackend-fitted GBT, seeded agent)",
-            "config": {"workload": "resnet18-12tasks-rollout (BASELINE configs[1])", "tasks": len(specs),
-                       "episodes_per_task_per_gpu": E, "T": T, "knobs": n_knobs, "hidden": [128, 64],
-                       "gbt": "50 trees depth<=4",
-                       "path": ("exact fp64 kernel (bit-exact with the oracle)" if args.exact else
-                                "tcgen05 rollout, certified sampling: configs/actions/scores bit-exact with the "
-                                "oracle, logp/value fp32-accurate"),
-                       "l2": "256 MB buffer written between timed steps; outputs 1.2 GB/step > L2",
-                       "parallelism": f"dp{world} (episodes sharded, no collective)"},
+            "data": DATA_NOTE, "config": headline_config(args, world),
             "gpu_launches": launches,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -772,6 +878,7 @@ def main():
             "gbt_standalone": gbt_s,
             "sa_baseline": sa,
             "candidates": cand,
+            "c1": c1,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

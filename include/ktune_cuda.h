@@ -64,6 +64,16 @@ int ktune_ctx_create(int device, ktune_ctx** out);
  * the 128-byte ncclUniqueId from rank 0 (NULL when world == 1). */
 int ktune_ctx_create_dist(int device, int rank, int world, const void* nccl_id, ktune_ctx** out);
 int ktune_nccl_get_unique_id(void* out128);
+/* Host-transport variant for multi-process runs without one GPU per rank (tests): the
+ * library's collectives (the sharded k-means exchanges, the distributed CandidateSet
+ * merge) call these instead of NCCL, on pinned HOST buffers, after synchronising the
+ * context stream. allreduce: in-place sum of `count` elements (dtype 0 = int64/uint64,
+ * 1 = float64); allgather: rank-ordered concatenation of every rank's `bytes`. Return 0
+ * on success. */
+typedef int (*ktune_host_allreduce_fn)(void* buf, int64_t count, int dtype, void* user);
+typedef int (*ktune_host_allgather_fn)(const void* send, void* recv, int64_t bytes, void* user);
+int ktune_ctx_create_hostcomm(int device, int rank, int world, ktune_host_allreduce_fn allreduce,
+                              ktune_host_allgather_fn allgather, void* user, ktune_ctx** out);
 int ktune_ctx_destroy(ktune_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch.cuda.current_stream()) — NULL restores the own stream. */
 int ktune_ctx_set_stream(ktune_ctx* ctx, void* cuda_stream);
@@ -80,7 +90,9 @@ enum ktune_option {
   KTUNE_OPT_ROLLOUT_DELTA = 4, /* certification margin of the tcgen05 rollout, in units of 1e-12
                                   (0 = default) */
   KTUNE_OPT_ROLLOUT_CHECK = 5, /* 1: re-decide EVERY sampling decision exactly and count disagreements
-                                  (calibration/verification mode, slow) */
+                                  (calibration/verification mode, slow); 5: the same with PLANTED draws,
+                                  each placed 2 delta below/above a fast CDF value (tests the margin
+                                  where it is tightest; changes the trajectory, tests only) */
   KTUNE_OPT_ROLLOUT_FUSE_GBT = 6, /* 1: walk the GBT inside the tcgen05 rollout (during its MMA waits)
                                     instead of a separate K1 launch; measured slower on B200, DESIGN.md §5.6 */
   KTUNE_OPT_ROLLOUT_SEGMENTS = 7, /* host-buffer rollouts: step segments overlapped with the D2H copies
@@ -112,7 +124,9 @@ enum ktune_stat {
   KTUNE_STAT_ROLLOUT_FALLBACKS = 16, /* tcgen05 rollout: knob decisions re-decided by the exact fp64 forward */
   KTUNE_STAT_ROLLOUT_CHECKED = 17,   /* KTUNE_OPT_ROLLOUT_CHECK: knob decisions checked */
   KTUNE_STAT_ROLLOUT_MISMATCH = 18,  /* certified fast decisions that disagreed with the exact one (must be 0) */
-  KTUNE_STAT_ROLLOUT_MAXERR = 19,    /* max |p_fast - p_exact| over checked decisions, in units of 1e-12 */
+  KTUNE_STAT_ROLLOUT_MAXERR = 19,    /* max |p_fast - p_exact| over every exactly re-decided knob (the
+                                        certificate's fallbacks in normal runs, every knob in check
+                                        mode), in units of 1e-12: the live margin monitor */
   KTUNE_STAT_ROLLOUT_TC = 20,        /* config-steps run on the tcgen05 path */
   KTUNE_STAT_KMEANS_ABORTS = 21      /* certified Lloyd runs that fell back to the exact-order mode */
 };

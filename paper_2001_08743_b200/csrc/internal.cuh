@@ -88,6 +88,12 @@ struct ktune_ctx {
   int rank = 0;
   int world = 1;
   void* nccl = nullptr;  // ncclComm_t
+  // Host-memory collectives supplied by the caller (ktune_ctx_create_hostcomm): the same
+  // sharded code paths as NCCL, with every exchange staged through pinned host memory
+  // (multi-process tests on one GPU; gloo or any host transport underneath).
+  ktune_host_allreduce_fn hc_allreduce = nullptr;
+  ktune_host_allgather_fn hc_allgather = nullptr;
+  void* hc_user = nullptr;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // D2H of segmented rollouts, overlapping the compute

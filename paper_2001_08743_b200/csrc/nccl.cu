@@ -60,12 +60,35 @@ void kt_nccl_destroy(ktune_ctx* ctx) {
 namespace kt {
 // In-place sum all-reduce on the context stream (no-op without a communicator).
 void allreduce_sum(ktune_ctx* ctx, void* buf, size_t count, bool is_double) {
+  if (ctx->hc_allreduce) {  // host transport: stage through pinned memory
+    void* h = ctx->host(3, count * 8);
+    KT_CUDA(cudaMemcpyAsync(h, buf, count * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    KT_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->hc_allreduce(h, (int64_t)count, is_double ? 1 : 0, ctx->hc_user) != 0)
+      fail(KTUNE_ERR_BACKEND, "host all-reduce failed");
+    KT_CUDA(cudaMemcpyAsync(buf, h, count * 8, cudaMemcpyHostToDevice, ctx->stream));
+    KT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
   if (!ctx->nccl) return;
   nccl_check(api().AllReduce(buf, buf, count, is_double ? ncclFloat64 : ncclInt64, ncclSum,
                              (ncclComm_t)ctx->nccl, ctx->stream),
              "ncclAllReduce");
 }
+// Rank-ordered all-gather; `send` may alias recv + rank * bytes_per_rank (in place).
 void allgather(ktune_ctx* ctx, const void* send, void* recv, size_t bytes_per_rank) {
+  if (ctx->hc_allgather) {
+    const size_t total = bytes_per_rank * (size_t)ctx->world;
+    char* h = (char*)ctx->host(3, total + bytes_per_rank);
+    char* hs = h + total;
+    KT_CUDA(cudaMemcpyAsync(hs, send, bytes_per_rank, cudaMemcpyDeviceToHost, ctx->stream));
+    KT_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->hc_allgather(hs, h, (int64_t)bytes_per_rank, ctx->hc_user) != 0)
+      fail(KTUNE_ERR_BACKEND, "host all-gather failed");
+    KT_CUDA(cudaMemcpyAsync(recv, h, total, cudaMemcpyHostToDevice, ctx->stream));
+    KT_CUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
   if (!ctx->nccl) {
     if (send != recv) KT_CUDA(cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, ctx->stream));
     return;
@@ -73,6 +96,7 @@ void allgather(ktune_ctx* ctx, const void* send, void* recv, size_t bytes_per_ra
   nccl_check(api().AllGather(send, recv, bytes_per_rank, ncclUint8, (ncclComm_t)ctx->nccl, ctx->stream),
              "ncclAllGather");
 }
+bool has_comm(const ktune_ctx* ctx) { return ctx->nccl || ctx->hc_allgather; }
 }  // namespace kt
 
 extern "C" {
@@ -122,6 +146,21 @@ int ktune_ctx_create_dist(int device, int rank, int world, const void* nccl_id, 
     }
     return rc;
   }
+  *out = ctx;
+  return KTUNE_OK;
+}
+
+int ktune_ctx_create_hostcomm(int device, int rank, int world, ktune_host_allreduce_fn allreduce,
+                              ktune_host_allgather_fn allgather, void* user, ktune_ctx** out) {
+  if (!allreduce || !allgather || world < 1 || rank < 0 || rank >= world) return KTUNE_ERR_CONFIG;
+  ktune_ctx* ctx = nullptr;
+  const int rc = ktune_ctx_create_dist(device, 0, 1, nullptr, &ctx);
+  if (rc != KTUNE_OK) return rc;
+  ctx->rank = rank;
+  ctx->world = world;
+  ctx->hc_allreduce = allreduce;
+  ctx->hc_allgather = allgather;
+  ctx->hc_user = user;
   *out = ctx;
   return KTUNE_OK;
 }

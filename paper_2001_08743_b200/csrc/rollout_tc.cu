@@ -24,7 +24,7 @@
 // bit-identical to the exact path; log-probabilities and values are fp32-
 // accurate (north star: 1e-5 relative).
 //
-// Layout: one persistent CTA per SM (512 threads = 4 slots x 4 warps). A slot
+// Layout: one persistent CTA per SM (384 threads = 3 slots x 4 warps). A slot
 // is a tile of up to 128 episodes (one TMEM lane and one thread per episode,
 // 128 TMEM columns per slot); its configurations live in the owning threads'
 // registers for the whole episode. Weights are staged once per CTA into shared
@@ -240,7 +240,7 @@ template <int NMAX>
 __device__ __noinline__ Redecided exact_redecide(const TcTask& tk, int t, int L, uint32_t fm, Cfg<NMAX> cfg,
                                                  const int* scard, double* sh0, double* shp, double* slg,
                                                  int64_t ge_L, uint64_t acts, const float* fastp, uint32_t fast_cert,
-                                                 unsigned long long* stats) {
+                                                 unsigned long long* stats, int check) {
   float lp_exact = 0.f;
   const int lane = threadIdx.x & 31;
   const int n = tk.n;
@@ -292,12 +292,17 @@ __device__ __noinline__ Redecided exact_redecide(const TcTask& tk, int t, int L,
     for (int d = 0; d < NMAX; ++d) {
       if (!((fm >> d) & 1u)) continue;
       const kt::Knob3 k3 = kt::softmax3(slg[3 * it], slg[3 * it + 1], slg[3 * it + 2]);
-      const double u = kt::hash01(tk.seed, (ge * (uint64_t)tk.T + (uint64_t)t) * (uint64_t)n + (uint64_t)d);
+      // check mode 5 (planted draws): u was placed 2 delta from a FAST CDF value (fastp[2d+1])
+      const double u = check == 5 ? (double)fastp[2 * d + 1]
+                                  : kt::hash01(tk.seed, (ge * (uint64_t)tk.T + (uint64_t)t) * (uint64_t)n + (uint64_t)d);
       const double c1 = kt::dadd(k3.p[0], k3.p[1]);
       const int ae = u < k3.p[0] ? 0 : (u < c1 ? 1 : 2);
-      if (stats) {  // check mode: compare against the fast decision
-        const float err = fmaxf(fabsf((float)(fastp[2 * d] - k3.p[0])), fabsf((float)(fastp[2 * d + 1] - c1)));
-        atomicMax(reinterpret_cast<unsigned int*>(stats + 3), __float_as_uint(err));
+      // margin monitor (every re-decided knob, every mode): max |p_fast - p_exact| of the
+      // decision's CDF values, so production runs keep measuring the certificate's margin
+      const float e0 = fabsf((float)(fastp[2 * d] - k3.p[0]));
+      const float err = check == 5 ? e0 : fmaxf(e0, fabsf((float)(fastp[2 * d + 1] - c1)));
+      atomicMax(reinterpret_cast<unsigned int*>(stats + 3), __float_as_uint(err));
+      if (check == 1 || check == 5) {  // compare against the fast decision
         if ((fast_cert >> d) & 1u) {
           const int af = (int)((acts >> (2 * d)) & 3u);
           if (af != ae) atomicAdd(stats + 2, 1ull);
@@ -631,13 +636,18 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
                 const float s = e0 + e1 + e2;
                 const float rs = rcpf(s);
                 const float p0 = e0 * rs, c1 = (e0 + e1) * rs;
-                const float uf = ufs[d];
+                float uf = ufs[d];
+                if (L.check == 5) {  // planted draw 2 delta below/above p0 or c1 (bits of the real draw)
+                  const float base = uf < 0.5f ? p0 : c1;
+                  uf = fminf(fmaxf(base + ((uf * 4.f - floorf(uf * 4.f)) < 0.5f ? -2.f : 2.f) * delta, 0.f),
+                             0x1.fffffep-1f);
+                }
                 const int a = uf < p0 ? 0 : (uf < c1 ? 1 : 2);
                 const bool ok = fabsf(uf - p0) > delta && fabsf(uf - c1) > delta;
                 acts |= (uint64_t)a << (2 * d);
-                if (L.check == 1) {
+                if (L.check == 1 || L.check == 5 || !ok) {  // the re-decision compares against these
                   fastp[(lane * NMAX + d) * 2] = p0;
-                  fastp[(lane * NMAX + d) * 2 + 1] = c1;
+                  fastp[(lane * NMAX + d) * 2 + 1] = L.check == 5 ? uf : c1;
                 }
                 const float lpa = (a == 0 ? l0 : (a == 1 ? l1 : l2)) - m - lg2f(s) * 0.69314718055994531f;
                 cert |= ok ? 1u << d : 0u;
@@ -649,10 +659,11 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         uint32_t fb;
         TR(14)
         const uint32_t allk = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
-        fb = L.check == 1 ? allk : (L.check == 3 ? 0u : (allk & ~cert));  // 3: timing experiment (no MMAs)
+        const bool chk = L.check == 1 || L.check == 5;  // every knob re-decided exactly
+        fb = chk ? allk : (L.check == 3 ? 0u : (allk & ~cert));  // 3: timing experiment (no MMAs)
         if (!lr) fb = 0;
-        n_fallback += L.check == 1 ? 0 : __popc(fb);
-        n_checked += L.check == 1 ? __popc(fb) : 0;
+        n_fallback += chk ? 0 : __popc(fb);
+        n_checked += chk ? __popc(fb) : 0;
         unsigned pend = __ballot_sync(0xffffffffu, fb != 0);
         float lpx = 0.f;
         while (pend) {
@@ -661,14 +672,14 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
           const uint32_t fm = __shfl_sync(0xffffffffu, fb, Lr);
           const int64_t geL = __shfl_sync(0xffffffffu, (long long)ge, Lr);
           const Redecided rd = exact_redecide<NMAX>(tk, t, Lr, fm, cfg, scard, sh0, shp, slg, geL, acts,
-                                                    fastp + Lr * NMAX * 2, cert, L.check == 1 ? L.counters : nullptr);
+                                                    fastp + Lr * NMAX * 2, cert, L.counters, L.check);
           if (lane == Lr) {
             acts = rd.acts;
             lpx = rd.lp;
           }
         }
         TR(7)
-        if (L.check == 1) lpj = lpx;  // every knob re-decided: exact log-probabilities
+        if (chk) lpj = lpx;  // every knob re-decided: exact log-probabilities
         else lpj += lpx;
         // saturating move (design_space.cpp:175-187) and the trajectory writes
         uint32_t apk[(NMAX + 3) / 4];

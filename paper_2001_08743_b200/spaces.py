@@ -1,4 +1,4 @@
-"""Design spaces (design_space.hpp:18-60) and the synthetic workloads the bench uses.
+"""Design spaces (design_space.hpp:18-60).
 
 `DesignSpace` mirrors the reference's value type: ordered knobs with strictly
 increasing integer values, an optional validity rule in the validity.hpp:10-19
@@ -6,23 +6,14 @@ grammar, mixed-radix size (design_space.cpp:13-58). It validates exactly the
 way the reference constructor does and raises `ConfigError` on the same
 conditions.
 
-Workloads (builder-defined, SURVEY.md §8d — the reference ships no examples/):
-
-* `conv_space`: one conv2d task with the 8 Table-1 knobs.
-  Split knobs use AutoTVM's ordered factorisations (4-way for f/y/x, 2-way for
-  rc/ry/rx); a split knob's integer value is the lexicographic code of its
-  factor tuple (strictly increasing in enumeration order). The validity rule
-  "auto_unroll_max_step * unroll_explicit <= 512" marks explicit unrolling at
-  step 1500 invalid (1/6 of every space).
-* `resnet18_tasks` (12), `vgg16_tasks` (9), `alexnet_tasks` (5): PAPER.md:610-612.
-* `synthetic_space`: D knobs of cardinality 2 + mix64(seed + d) % 31 (2..32),
-  values 1..card, optional rule.
+The synthetic workload catalogue (AutoTVM-style conv spaces, the synthetic
+16-knob space) lives in the top-level `workloads` package (bench/test
+fixtures); the wrappers below build product `DesignSpace`s from it.
 """
 from __future__ import annotations
 
 import json
 from dataclasses import dataclass, field
-from functools import lru_cache
 from typing import List, Optional, Sequence
 
 from .errors import ConfigError
@@ -158,90 +149,39 @@ class DesignSpace:
 
 
 # ---------------------------------------------------------------------------
-# AutoTVM-style conv2d spaces
+# The builder-defined catalogue (workloads/spaces.py) as product DesignSpaces
 # ---------------------------------------------------------------------------
 
-@lru_cache(maxsize=None)
-def ordered_factorizations(n: int, parts: int) -> tuple:
-    """All ordered tuples of `parts` positive integers whose product is n, lexicographic."""
-    if parts == 1:
-        return ((n,),)
-    out = []
-    for f in range(1, n + 1):
-        if n % f == 0:
-            for rest in ordered_factorizations(n // f, parts - 1):
-                out.append((f,) + rest)
-    return tuple(out)
+def _make(workload, knobs, rule):
+    return DesignSpace(workload, [Knob(n, list(v)) for n, v in knobs], rule)
 
 
-def _split_knob(name: str, n: int, parts: int) -> Knob:
-    base = n + 1
-    vals = []
-    for tup in ordered_factorizations(n, parts):
-        code = 0
-        for f in tup:
-            code = code * base + f
-        vals.append(code)
-    return Knob(name, vals)
-
-
-CONV_RULE = "auto_unroll_max_step * unroll_explicit <= 512"
-
-
-def conv_space(workload: str, c_in: int, c_out: int, h_out: int, w_out: int, kh: int, kw: int,
-               rule: Optional[str] = CONV_RULE) -> DesignSpace:
-    knobs = [
-        _split_knob("tile_f", c_out, 4),
-        _split_knob("tile_y", h_out, 4),
-        _split_knob("tile_x", w_out, 4),
-        _split_knob("tile_rc", c_in, 2),
-        _split_knob("tile_ry", kh, 2),
-        _split_knob("tile_rx", kw, 2),
-        Knob("auto_unroll_max_step", [0, 512, 1500]),
-        Knob("unroll_explicit", [0, 1]),
-    ]
-    return DesignSpace(workload, knobs, rule)
+def conv_space(*a, **k) -> DesignSpace:
+    from workloads import spaces as W
+    return W.conv_space(*a, make=_make, **k)
 
 
 def resnet18_tasks() -> List[DesignSpace]:
-    """The 12 tuning tasks of ResNet-18: its 11 distinct conv2d
-    workloads plus the final 512->1000 dense layer expressed as a 1x1 conv on a
-    1x1 map (single-valued tile_y/tile_x knobs, tile_f cardinality 400)."""
-    L = [("resnet18.c1", 3, 64, 112, 112, 7, 7), ("resnet18.c2", 64, 64, 56, 56, 3, 3),
-         ("resnet18.c3", 64, 128, 28, 28, 3, 3), ("resnet18.c4", 64, 128, 28, 28, 1, 1),
-         ("resnet18.c5", 128, 128, 28, 28, 3, 3), ("resnet18.c6", 128, 256, 14, 14, 3, 3),
-         ("resnet18.c7", 128, 256, 14, 14, 1, 1), ("resnet18.c8", 256, 256, 14, 14, 3, 3),
-         ("resnet18.c9", 256, 512, 7, 7, 3, 3), ("resnet18.c10", 256, 512, 7, 7, 1, 1),
-         ("resnet18.c11", 512, 512, 7, 7, 3, 3), ("resnet18.dense", 512, 1000, 1, 1, 1, 1)]
-    return [conv_space(*a) for a in L]
+    from workloads import spaces as W
+    return W.resnet18_tasks(make=_make)
 
 
 def vgg16_tasks() -> List[DesignSpace]:
-    """The 9 distinct conv2d workloads of VGG-16."""
-    L = [("vgg16.c1", 3, 64, 224, 224, 3, 3), ("vgg16.c2", 64, 64, 224, 224, 3, 3),
-         ("vgg16.c3", 64, 128, 112, 112, 3, 3), ("vgg16.c4", 128, 128, 112, 112, 3, 3),
-         ("vgg16.c5", 128, 256, 56, 56, 3, 3), ("vgg16.c6", 256, 256, 56, 56, 3, 3),
-         ("vgg16.c7", 256, 512, 28, 28, 3, 3), ("vgg16.c8", 512, 512, 28, 28, 3, 3),
-         ("vgg16.c9", 512, 512, 14, 14, 3, 3)]
-    return [conv_space(*a) for a in L]
+    from workloads import spaces as W
+    return W.vgg16_tasks(make=_make)
 
 
 def alexnet_tasks() -> List[DesignSpace]:
-    """The 5 conv2d workloads of AlexNet."""
-    L = [("alexnet.c1", 3, 64, 55, 55, 11, 11), ("alexnet.c2", 64, 192, 27, 27, 5, 5),
-         ("alexnet.c3", 192, 384, 13, 13, 3, 3), ("alexnet.c4", 384, 256, 13, 13, 3, 3),
-         ("alexnet.c5", 256, 256, 13, 13, 3, 3)]
-    return [conv_space(*a) for a in L]
+    from workloads import spaces as W
+    return W.alexnet_tasks(make=_make)
 
 
 def synthetic_space(seed: int = 0, num_knobs: int = 16, rule: Optional[str] = None,
                     workload: str = "synthetic") -> DesignSpace:
-    knobs = []
-    for d in range(num_knobs):
-        card = 2 + mix64((seed + d) & MASK64) % 31
-        knobs.append(Knob(f"k{d}", list(range(1, card + 1))))
-    return DesignSpace(f"{workload}{num_knobs}", knobs, rule)
+    from workloads import spaces as W
+    return W.synthetic_space(seed, num_knobs, rule, workload, make=_make)
 
 
 def small_space(cards: Sequence[int], rule: Optional[str] = None, workload: str = "small") -> DesignSpace:
-    return DesignSpace(workload, [Knob(f"k{i}", list(range(1, c + 1))) for i, c in enumerate(cards)], rule)
+    from workloads import spaces as W
+    return W.small_space(cards, rule, workload, make=_make)

@@ -94,7 +94,9 @@ def test_rollout_large_spot_replay(O, ctx):
     idx = out["idx"].astype(np.int64)
     assert np.all(idx.max(axis=(0, 1)) < np.array(sp.cards))
     assert np.all(np.abs(np.diff(idx, axis=1)) <= 1)
-    assert np.array_equal(np.diff(idx, axis=1) != 0, out["actions"] != 0) or True
+    # every move is the saturating application of the recorded action (design_space.cpp:175-187)
+    cards = np.array(sp.cards)
+    assert np.array_equal(np.diff(idx, axis=1), np.clip(idx[:, :-1] + out["actions"], 0, cards - 1) - idx[:, :-1])
 
 
 # ---------------------------------------------------------------- tcgen05 path
@@ -295,3 +297,75 @@ def test_rollout_fp32_outputs(O, ctx, exact):
     assert np.array_equal(o2["idx8"], o["idx8"]) and np.array_equal(o2["score32"], o["score32"])
     from paper_2001_08743_b200.exploration import unpack_actions
     assert np.array_equal(unpack_actions(o2["actions2"], sp.num_knobs), o["actions"])
+
+
+def test_rollout_tc_planted_draws(O, ctx):
+    """Check mode 5: every draw is PLANTED 2 delta below or above a fast CDF value (where
+    the certificate's margin is tightest) and every knob is then re-decided exactly with
+    the same draw: the fast decisions never disagree."""
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    tasks = []
+    for i, name in enumerate(["resnet_c2", "synthetic16", "vgg_c4"]):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=140 + i)
+        init = osp.random_valid(i, 512) if O.ref_available() else np.zeros((512, sp.num_knobs), np.int32)
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=0, root_seed=i))
+    ctx.reset_stats()
+    ctx.set_option(L.OPT_ROLLOUT_CHECK, 5)
+    try:
+        run_episodes_batch(tasks, 24)
+    finally:
+        ctx.set_option(L.OPT_ROLLOUT_CHECK, 0)
+    assert ctx.stat(L.STAT_ROLLOUT_CHECKED) == 512 * 24 * (8 + 16 + 8)
+    assert ctx.stat(L.STAT_ROLLOUT_MISMATCH) == 0
+    print(f"planted: max |p0_fast - p0_exact| = {ctx.stat(L.STAT_ROLLOUT_MAXERR) * 1e-12:.3e}")
+
+
+def test_rollout_tc_check_mode_c2_shape(O, ctx):
+    """The bench's shape (BASELINE configs[1]: 12 ResNet-18 tasks x 4096 episodes, one grouped
+    launch) at T = 64 in check mode: all 25.2M knob decisions re-decided exactly, 0
+    disagreements, the fast probabilities well inside the margin; the trajectories equal
+    the exact fp64 kernel's, and spot episodes replay on the oracle."""
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt
+    from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
+    from paper_2001_08743_b200.spaces import stream_seed
+    E, T = 4096, 64
+    tasks, orc = [], []
+    for i, sp in enumerate(S.resnet18_tasks()):
+        osp, og, pm = fitted(O, sp, seed=200 + i)
+        ds = Space(sp, ctx)
+        agent = ActorCritic(sp.num_knobs, 128, 64, seed=200 + i, ctx=ctx)
+        init = osp.random_valid(i, E) if O.ref_available() else np.zeros((E, sp.num_knobs), np.int32)
+        tasks.append(RolloutTask(ds, agent, DeviceGbt(pm, ds), init, episode_offset=0, root_seed=i))
+        orc.append((osp, og, agent, init))
+    ctx.reset_stats()
+    ctx.set_option(L.OPT_ROLLOUT_CHECK, 1)
+    try:
+        chk = run_episodes_batch(tasks, T)
+    finally:
+        ctx.set_option(L.OPT_ROLLOUT_CHECK, 0)
+    assert ctx.stat(L.STAT_ROLLOUT_CHECKED) == 12 * E * T * 8
+    assert ctx.stat(L.STAT_ROLLOUT_MISMATCH) == 0
+    maxerr = ctx.stat(L.STAT_ROLLOUT_MAXERR) * 1e-12
+    print(f"C2 shape: max |p_fast - p_exact| = {maxerr:.3e} over {12 * E * T * 8} decisions")
+    assert maxerr < 2 ** -18
+    ctx.reset_stats()
+    fast = run_episodes_batch(tasks, T)
+    exact = run_episodes_batch(tasks, T, exact=True)
+    for f, c, x in zip(fast, chk, exact):
+        for k in ("idx", "actions", "score"):
+            assert np.array_equal(f[k], x[k]) and np.array_equal(c[k], x[k]), k
+        assert _close(f["logp"], x["logp"]) and _close(f["value"], x["value"])
+    # the live margin monitor of the normal run: every fallback re-decision inside the margin
+    assert ctx.stat(L.STAT_ROLLOUT_FALLBACKS) > 0 and ctx.stat(L.STAT_ROLLOUT_MAXERR) * 1e-12 < 2 ** -18
+    g = np.random.default_rng(5)
+    for i in g.choice(12, 3, replace=False):
+        osp, og, agent, init = orc[i]
+        for e in g.choice(E, 2, replace=False):
+            w = O.run_episodes(osp, og, 128, 64, agent.params, init[e:e + 1], T, int(e), stream_seed(int(i), "explore"))
+            assert np.array_equal(fast[i]["idx"][e].astype(np.int32), w["idx"][0])
+            assert np.array_equal(fast[i]["actions"][e], w["actions"][0])
+            assert np.array_equal(fast[i]["score"][e], w["score"][0])

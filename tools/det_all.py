@@ -7,7 +7,7 @@ from paper_2001_08743_b200.context import Space
 from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
 from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, SaParams, SaTask, run_episodes_batch, sa_search_batch
 from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep, candidates_from_rows
-from paper_2001_08743_b200.workloads import encode
+from workloads.tasks import encode
 from paper_2001_08743_b200.distributed import create_context
 H = lambda t: hashlib.sha1((t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)).tobytes()).hexdigest()[:10]
 class A: tasks = 12; episodes = 4096; seed = 0

@@ -7,7 +7,7 @@ from paper_2001_08743_b200 import _lib as L
 from paper_2001_08743_b200.context import Space
 from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
 from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
-from paper_2001_08743_b200.workloads import encode
+from workloads.tasks import encode
 from paper_2001_08743_b200.distributed import create_context
 
 class A: tasks = 12; episodes = 4096; seed = 0

@@ -6,7 +6,7 @@ from paper_2001_08743_b200 import _lib as L
 from paper_2001_08743_b200 import spaces as S
 from paper_2001_08743_b200.context import Context, Space
 from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep
-from paper_2001_08743_b200.workloads import random_configs
+from workloads.tasks import random_configs
 ctx = Context(0)
 for name, sp in (("alexnet.c2", S.alexnet_tasks()[1]), ("resnet18.t1", S.resnet18_tasks()[1])):
     ds = Space(sp, ctx)

@@ -5,7 +5,7 @@ from paper_2001_08743_b200 import _lib as L
 from paper_2001_08743_b200 import spaces as S
 from paper_2001_08743_b200.context import Context, Space
 from paper_2001_08743_b200.sampling import kmeans_run
-from paper_2001_08743_b200.workloads import random_configs
+from workloads.tasks import random_configs
 ctx = Context(0)
 sp = S.alexnet_tasks()[1]
 ds = Space(sp, ctx)

@@ -7,7 +7,7 @@ from oracle import pyoracle as O
 from paper_2001_08743_b200 import spaces as S
 from paper_2001_08743_b200.context import Context, Space
 from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep, kmeans_run
-from paper_2001_08743_b200.workloads import random_configs
+from workloads.tasks import random_configs
 ctx = Context(0)
 sp = S.alexnet_tasks()[1]
 ds = Space(sp, ctx)

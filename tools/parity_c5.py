@@ -8,7 +8,7 @@ from paper_2001_08743_b200 import spaces as S
 from paper_2001_08743_b200.context import Space
 from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
 from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
-from paper_2001_08743_b200.workloads import encode, make_tasks
+from workloads.tasks import encode, make_tasks
 from paper_2001_08743_b200.distributed import create_context
 ctx = create_context(0, 0, 1)
 st = torch.cuda.Stream(); torch.cuda.set_stream(st); ctx.set_stream(st.cuda_stream)

@@ -9,7 +9,7 @@ from paper_2001_08743_b200.context import Space
 from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
 from paper_2001_08743_b200.exploration import SaParams, SaTask, sa_search_batch
 from paper_2001_08743_b200.spaces import stream_seed
-from paper_2001_08743_b200.workloads import encode
+from workloads.tasks import encode
 from paper_2001_08743_b200.distributed import create_context
 class A: tasks = 4; episodes = 4096; seed = 0
 ctx = create_context(0, 0, 1)
