@@ -301,60 +301,95 @@ def c1_secondary(ctx, args):
             "candidate_set_equal_reference": bool(np.array_equal(np.asarray(cands.idx, np.int32), flat[rows]))}
 
 
-def c3_pipeline(ctx, args):
+def c3_pipeline(ctx, args, rank=0, world=1):
     """SURVEY C3 as one Chameleon iteration on the device: VGG-16 conv layer, 65,536
     explorer episodes x T = 500 (tcgen05 rollout + K1 scoring), the CandidateSet of
     every visited configuration (device make_candidate_set), then Adaptive Sampling's
-    k-sweep + snap over that candidate set, all device-resident; stage times."""
+    k-sweep + snap over that candidate set, all device-resident; stage times.
+
+    world > 1 (BASELINE configs[2]: "65536 configs sharded across 2/4/8 B200 with NCCL
+    k-means"): rank r rolls out its contiguous share of the 65,536 episodes (global
+    episode ids), the global CandidateSet is all-gathered over NCCL
+    (ktune_candidates_gather) and the k-sweep runs the sharded certified Lloyd (NCCL
+    all-reduces of the integer centroid-sum deltas); stage times are maxima over ranks
+    and the result digest must agree on every rank."""
+    import hashlib
     import torch
     from paper_2001_08743_b200 import spaces as S
     from paper_2001_08743_b200.context import Space
     from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
+    from paper_2001_08743_b200.distributed import shard_range
     from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
-    from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep, candidates_from_rows
+    from paper_2001_08743_b200.sampling import (CandidateSet, SamplingParams, adaptive_sweep, candidates_from_rows,
+                                                candidates_gather)
     from workloads.tasks import encode, make_tasks
     sp = S.vgg16_tasks()[3]
     spec = make_tasks([sp], args.c3_episodes, seed=args.seed + 33)[0]
     ds = Space(sp, ctx)
     g = DeviceGbt(fit_gbt(encode(sp, spec.train_idx), spec.train_y, seed=spec.seed), ds)
     agent = ActorCritic(sp.num_knobs, 128, 64, seed=spec.seed, ctx=ctx)
-    init = torch.from_numpy(spec.init_idx.astype(np.uint16).view(np.int16)).cuda()
+    lo, hi = shard_range(args.c3_episodes, rank, world)
+    init = torch.from_numpy(spec.init_idx[lo:hi].astype(np.uint16).view(np.int16)).cuda()
     T, D = args.c3_T, sp.num_knobs
-    task = RolloutTask(ds, agent, g, init.view(torch.uint16), 0, spec.seed)
+    task = RolloutTask(ds, agent, g, init.view(torch.uint16), lo, spec.seed)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def mx(v):
+        return allreduce_max(v) if world > 1 else v
+
     run_episodes_batch([task], 8, ctx, device_out=True)  # warm-up
     roll = []
     o = None
     for _ in range(3):  # median of 3 rollouts; the last one's trajectory feeds the sampling stages
         o = None  # release the previous trajectory first: the caching allocator reuses its blocks
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         o = run_episodes_batch([task], T, ctx, device_out=True)[0]
         torch.cuda.synchronize()
-        roll.append(time.perf_counter() - t0)
+        roll.append(mx(time.perf_counter() - t0))
     t_roll = float(np.median(roll))
     for _ in range(2):  # the second pass is timed (the first sizes the workspaces)
-        torch.cuda.synchronize()
+        barrier()
         t1 = time.perf_counter()
-        rows, ids = candidates_from_rows(ds, o["idx"].view(-1, D), o["score"].view(-1))
-        cidx = o["idx"].view(torch.int16).view(-1, D)[rows]
+        if world > 1:
+            c = candidates_gather(ds, o["idx"].view(-1, D), o["score"].view(-1))
+            cidx, cids, npts = c.idx, c.ids, len(c)
+        else:
+            rows, ids = candidates_from_rows(ds, o["idx"].view(-1, D), o["score"].view(-1))
+            cidx, cids, npts = o["idx"].view(torch.int16).view(-1, D)[rows], ids.view(torch.int64), int(rows.numel())
         cidx = cidx.to(torch.uint8) if ds.index_bytes == 1 else cidx
         torch.cuda.synchronize()
         t2 = time.perf_counter()
-        sw = adaptive_sweep(ds, CandidateSet(cidx, ids.view(torch.int64), None), SamplingParams(), spec.seed)
+        sw = adaptive_sweep(ds, CandidateSet(cidx, cids, None), SamplingParams(), spec.seed)
         torch.cuda.synchronize()
         t3 = time.perf_counter()
+        d_cand, d_sweep = mx(t2 - t1), mx(t3 - t2)
     ctx.set_stream(None)
     torch.cuda.set_stream(torch.cuda.default_stream())
-    steps = args.c3_episodes * T
-    return {"workload": f"SURVEY C3: VGG-16 layer {sp.workload} (D={D}), {args.c3_episodes} episodes x {T} steps, "
-                        f"then Adaptive Sampling over every visited configuration; 1 GPU, device-resident",
-            "rollout_ms": 1e3 * t_roll, "config_steps_per_s": steps / t_roll,
-            "candidates": int(rows.numel()), "candidate_set_ms": 1e3 * (t2 - t1),
-            "adaptive_sweep_ms": 1e3 * (t3 - t2), "sweep_k": sw.k, "sweep_k_losses": len(sw.k_losses),
-            "total_ms": 1e3 * (t_roll + t3 - t1)}
+    h = hashlib.sha256(np.ascontiguousarray(sw.snapped.cpu().numpy()).tobytes())
+    h.update(np.array(sw.k_losses).tobytes())
+    h.update(np.ascontiguousarray(cids.cpu().numpy()).tobytes())
+    digest = h.hexdigest()[:16]
+    same = True
+    if world > 1:
+        allg = [None] * world
+        torch.distributed.all_gather_object(allg, digest)
+        same = len(set(allg)) == 1
+    return {"workload": f"SURVEY C3 (BASELINE configs[2]): VGG-16 layer {sp.workload} (D={D}), {args.c3_episodes} "
+                        f"episodes x {T} steps sharded over {world} GPU(s), then Adaptive Sampling over every "
+                        f"visited configuration (global CandidateSet all-gathered, NCCL k-means); device-resident",
+            "n_gpus": world, "rollout_ms": 1e3 * t_roll, "config_steps_per_s": args.c3_episodes * T / t_roll,
+            "candidates": npts, "candidate_set_ms": 1e3 * d_cand,
+            "adaptive_sweep_ms": 1e3 * d_sweep, "sweep_k": sw.k, "sweep_k_losses": len(sw.k_losses),
+            "total_ms": 1e3 * (t_roll + d_cand + d_sweep), "result_digest": digest, "digest_equal_on_all_ranks": same,
+            "timing": "wall clock per stage, synchronised, max over ranks"}
 
 
 def gbt_standalone(ctx, args, specs, spaces, gbts):
@@ -595,6 +630,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init lines (nranks) on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -607,8 +644,12 @@ def main():
     from workloads.tasks import encode
 
     from paper_2001_08743_b200.distributed import create_context
-    # the library's NCCL communicator is only needed by the sharded k-means (--kmeans-dist)
-    ctx = create_context(local, rank, world) if (world > 1 and args.kmeans_dist) else create_context(local, 0, 1)
+    # the library's NCCL communicator (the C3 pipeline's CandidateSet all-gather and sharded
+    # k-means); NCCL_DEBUG=INFO (set before the first communicator) logs its init per rank
+    # BENCH_DIST_BACKEND=gloo: several ranks share a GPU, so the library's collectives use the
+    # host transport over the gloo group instead of NCCL (same sharded code paths)
+    transport = "nccl" if os.environ.get("BENCH_DIST_BACKEND", "nccl") == "nccl" else "host"
+    ctx = create_context(local, rank, world, transport=transport) if world > 1 else create_context(local, 0, 1)
     stream = torch.cuda.Stream()  # a real stream handle shared by torch and libktune_cuda
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
@@ -812,17 +853,16 @@ def main():
             gbt_s = {"error": repr(ex)}
 
     c3 = None
-    if args.c3_episodes and world == 1:
+    if args.c3_episodes:
         try:
-            c3 = c3_pipeline(ctx, args)
+            c3 = c3_pipeline(ctx, args, rank, world)
         except Exception as ex:  # reported, not hidden
             c3 = {"error": repr(ex)}
 
     kmeans = None
     if not args.no_kmeans and (world == 1 or args.kmeans_dist):
-        # N > 1: every rank would join the sharded assignment's NCCL all-gathers; that path is
-        # built but has never run on a multi-GPU box (one GPU available to this build), so the
-        # scaling runs measure the rollout only unless --kmeans-dist is given
+        # N > 1: the sharded k-means runs inside the C3 pipeline above; this 1M-point
+        # secondary (replicated points) stays single-GPU unless --kmeans-dist is given
         try:
             kmeans = kmeans_secondary(ctx, args, cpu=(world == 1 and not args.no_cpu))
         except Exception as ex:  # reported, not hidden

@@ -298,6 +298,19 @@ int ktune_candidates_from_rows(ktune_ctx* ctx, const ktune_space* space, const u
                                const double* pred, int64_t n, int64_t* out_rows, uint64_t* out_ids,
                                int64_t* out_n, int flags);
 
+/* Distributed make_candidate_set (the end-of-rollout exchange). Every rank
+ * passes the rows of ITS episode shard (uint16 n x D + scores); the result is the global
+ * CandidateSet over all ranks' rows, identical on every rank and identical to the
+ * single-GPU make_candidate_set over the concatenated trajectories: per-rank dedup +
+ * rank, an all-gather of the per-rank sets (NCCL, or the host transport of
+ * ktune_ctx_create_hostcomm), and make_candidate_set of their union. The result stays in
+ * the context: *out_n = its size; ktune_candidates_gather_copy copies it out (idx uint16
+ * out_n x D, pred, ids; any may be NULL). Honours KTUNE_F_DEVICE (inputs and outputs). */
+int ktune_candidates_gather(ktune_ctx* ctx, const ktune_space* space, const uint16_t* idx, const double* pred,
+                            int64_t n, int64_t* out_n, int flags);
+int ktune_candidates_gather_copy(ktune_ctx* ctx, const ktune_space* space, uint16_t* out_idx, double* out_pred,
+                                 uint64_t* out_ids, int flags);
+
 /* knob_options' counting pass (sampling.cpp:249-256) on the device: counts has
  * sum(card) entries, counts[sum(card[0..d-1]) + v] = #{i : idx[i][d] == v}.
  * Honours KTUNE_F_DEVICE. */

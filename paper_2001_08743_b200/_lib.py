@@ -117,6 +117,9 @@ SIGNATURES = {
     "ktune_sa_search": (C.c_int, [P, C.c_int, C.POINTER(SaTaskC), C.c_int32, C.POINTER(SaParamsC), C.c_int]),
     "ktune_make_candidate_set": (C.c_int, [P, P, P, i64, P, C.POINTER(i64)]),
     "ktune_candidates_from_rows": (C.c_int, [P, P, P, P, i64, P, P, C.POINTER(i64), C.c_int]),
+    "ktune_candidates_gather": (C.c_int, [P, P, P, P, i64, C.POINTER(i64), C.c_int]),
+    "ktune_candidates_gather_copy": (C.c_int, [P, P, P, P, P, C.c_int]),
+    "ktune_ctx_create_hostcomm": (C.c_int, [C.c_int, C.c_int, C.c_int, P, P, P, C.POINTER(P)]),
     "ktune_knob_histogram": (C.c_int, [P, P, P, C.c_int, i64, P, C.c_int]),
     "ktune_kmeans_run": (C.c_int, [P, P, P, C.c_int, i64, C.c_int, u64, C.c_int, C.c_int,
                                    C.POINTER(KmeansOutC), C.c_int]),

@@ -67,6 +67,41 @@ class Context:
         self.rank = rank
         self.world = world
 
+    @classmethod
+    def with_host_transport(cls, device: int, rank: int, world: int, allreduce, allgather) -> "Context":
+        """A context whose collectives run through caller-supplied HOST functions
+        (ktune_ctx_create_hostcomm): allreduce(np_array) sums in place, allgather(send_u8,
+        recv_u8) fills recv with every rank's send in rank order. The product's sharded
+        code paths run unchanged; several processes can share one GPU (tests)."""
+        import numpy as np
+        ar_t = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p)
+        ag_t = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+        def _ar(buf, count, dtype, user):
+            try:
+                ct = C.c_double if dtype == 1 else C.c_int64
+                allreduce(np.ctypeslib.as_array((ct * count).from_address(buf)))
+                return 0
+            except Exception:  # reported through the library's error path
+                return 1
+
+        def _ag(send, recv, nbytes, user):
+            try:
+                snd = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(send))
+                rcv = np.ctypeslib.as_array((C.c_uint8 * (nbytes * world)).from_address(recv))
+                allgather(snd, rcv)
+                return 0
+            except Exception:
+                return 1
+
+        self = cls.__new__(cls)
+        self._callbacks = (ar_t(_ar), ag_t(_ag))  # kept alive with the context
+        h = C.c_void_p()
+        L.check(L.lib().ktune_ctx_create_hostcomm(device, rank, world, C.cast(self._callbacks[0], C.c_void_p),
+                                                  C.cast(self._callbacks[1], C.c_void_p), None, C.byref(h)))
+        self.h, self.device, self.rank, self.world = h, device, rank, world
+        return self
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)

@@ -78,7 +78,7 @@ enum WsSlot {
   WS_IN0, WS_IN1, WS_IN2, WS_OUT0, WS_OUT1, WS_OUT2, WS_OUT3, WS_OUT4,
   WS_D2, WS_D2B, WS_ASSIGN, WS_ASSIGN2, WS_MEMBERS, WS_BLOCK, WS_BLOCK2, WS_CENT, WS_CENT2,
   WS_SCRATCH, WS_SCRATCH2, WS_KPP, WS_SNAP, WS_VALID, WS_TASKS, WS_BEST_ASSIGN, WS_BEST_D2,
-  WS_PREV_ASSIGN, WS_PREV_D2, WS_SORTED, WS_XS_APPROX, WS_XS_MAPS, WS_TILESUM, WS_ROLLOUT, WS_XS_RB, WS_KM_CERT, WS_KPP_X, WS_CERT_SNAP, WS_NUM_SLOTS
+  WS_PREV_ASSIGN, WS_PREV_D2, WS_SORTED, WS_XS_APPROX, WS_XS_MAPS, WS_TILESUM, WS_ROLLOUT, WS_XS_RB, WS_KM_CERT, WS_KPP_X, WS_CERT_SNAP, WS_CAND_LOCAL, WS_CAND_SEND, WS_CAND_RECV, WS_CAND_OUT, WS_NUM_SLOTS
 };
 
 }  // namespace kt
@@ -115,6 +115,7 @@ struct ktune_ctx {
     int stat_ns;
   };
   std::vector<PendingTiming> pending;  // resolved lazily by ktune_ctx_stat
+  int64_t cand_count = -1;  // rows of the last ktune_candidates_gather result (WS_CAND_OUT)
   kt::DevBuf ws[kt::WS_NUM_SLOTS];
   kt::HostBuf pinned[4];
   void* dev(int slot, size_t bytes) { return ws[slot].get(bytes); }

@@ -2061,6 +2061,10 @@ struct KMeans {
         KT_CUDA(cudaMemcpyAsync(d2_a, snap_d2, sizeof(double) * N, cudaMemcpyDeviceToDevice, s()));
       } else {  // exact centroids of the previous assignment (certified: no empty cluster), exact assign
         KT_CUDA(cudaMemcpyAsync(asg_b, snap_asg, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s()));
+        if (sharded) {  // certified iterations keep assignments rank-local: every rank needs all of them
+          const int64_t S = shard_chunks * kChunk;
+          kt::allgather(ctx, asg_b + rank * S, asg_b, sizeof(int32_t) * S);
+        }
         update_centroids(k, asg_b, d2_b, cent_a);
         assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);
       }

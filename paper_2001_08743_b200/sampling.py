@@ -93,6 +93,26 @@ def candidates_from_rows(space: Space, idx, predicted):
     return CandidateSet(rows_idx[rows].astype(np.int32), ids[:m.value], pred[rows])
 
 
+def candidates_gather(space: Space, idx, predicted) -> CandidateSet:
+    """The GLOBAL CandidateSet of a sharded rollout (ktune_candidates_gather): every rank
+    passes its own trajectory rows (CUDA tensors: uint16 n x D, float64 n) and gets the
+    same CandidateSet, equal to make_candidate_set over all ranks' rows.
+    Returns CUDA tensors (idx int16-viewed uint16 rows, ids uint64, predicted float64)."""
+    import torch
+    n = idx.numel() // space.D
+    m = C.c_int64()
+    space.ctx.check(L.lib().ktune_candidates_gather(space.ctx.h, space.h, C.c_void_p(idx.data_ptr()),
+                                                    C.c_void_p(predicted.data_ptr()), n, C.byref(m), L.F_DEVICE))
+    g = m.value
+    oidx = torch.empty((g, space.D), dtype=torch.int16, device=idx.device)
+    opred = torch.empty(g, dtype=torch.float64, device=idx.device)
+    oids = torch.empty(g, dtype=torch.int64, device=idx.device)
+    space.ctx.check(L.lib().ktune_candidates_gather_copy(space.ctx.h, space.h, C.c_void_p(oidx.data_ptr()),
+                                                         C.c_void_p(opred.data_ptr()), C.c_void_p(oids.data_ptr()),
+                                                         L.F_DEVICE))
+    return CandidateSet(oidx, oids, opred)
+
+
 def _packed(space: Space, idx):
     if hasattr(idx, "is_cuda") and idx.is_cuda:
         return idx, True

@@ -97,3 +97,67 @@ def test_shard_plans_cover_exactly(n, world):
         assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
     lo, hi = kmeans_chunk_range(n, 1, world)
     assert lo % 1024 == 0 or lo == n
+
+
+def _merge_worker(rank, world, port, q):
+    """The distributed CandidateSet protocol of ktune_candidates_gather (counts all-gather,
+    padded row all-gather, rank-ordered union, make_candidate_set of the union) over the
+    product's host transport (distributed.host_collectives), with the oracle's
+    make_candidate_set standing in for the device sort: equals the single-GPU set."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import pyoracle as O
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.distributed import host_collectives, shard_range
+    allreduce, allgather = host_collectives(world)
+    sp = O.OSpace(S.synthetic_space(3, 5))
+    E, T = 37, 9
+    g = np.random.default_rng(2)
+    init = np.stack([g.integers(0, c, E) for c in sp.card], 1).astype(np.int32)
+    p = O.ac_init(5, 16, 8, 4)
+    gb = O.fitted_model(sp, seed=1, n_train=200) if O.ref_available() else None
+    lo, hi = shard_range(E, rank, world)
+    part = O.run_episodes(sp, gb, 16, 8, p, init[lo:hi], T, lo, 7)
+    rows_idx = part["idx"].reshape(-1, 5)
+    pred = part["score"].reshape(-1)
+    keep = O.make_candidate_set(5, rows_idx, sp.ids(rows_idx), pred)
+    m = np.array([len(keep)], np.int64)
+    cnt = np.zeros(world, np.int64)
+    allgather(m.view(np.uint8), cnt.view(np.uint8))
+    M = int(cnt.max())
+    send = np.zeros((M, 5 * 2 + 8), np.uint8)  # padded rows: idx uint16 x D, then pred
+    send[:len(keep), :10] = rows_idx[keep].astype(np.uint16).view(np.uint8).reshape(len(keep), 10)
+    send[:len(keep), 10:] = pred[keep].view(np.uint8).reshape(len(keep), 8)
+    recv = np.zeros((world * M, 18), np.uint8)
+    allgather(send.reshape(-1), recv.reshape(-1))
+    parts = [recv[r * M:r * M + cnt[r]] for r in range(world)]
+    u = np.concatenate(parts)
+    uidx = u[:, :10].copy().view(np.uint16).astype(np.int32).reshape(-1, 5)
+    upred = u[:, 10:].copy().view(np.float64).reshape(-1)
+    sel = O.make_candidate_set(5, uidx, sp.ids(uidx), upred)
+    tot = np.array([float(len(sel))])
+    allreduce(tot)  # the float64 all-reduce path
+    if rank == 0:
+        full = O.run_episodes(sp, gb, 16, 8, p, init, T, 0, 7)
+        fidx = full["idx"].reshape(-1, 5)
+        fp = full["score"].reshape(-1)
+        want = O.make_candidate_set(5, fidx, sp.ids(fidx), fp)
+        q.put(bool(np.array_equal(uidx[sel], fidx[want]) and np.array_equal(upred[sel], fp[want])
+                   and tot[0] == world * len(sel)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_candidate_merge_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_merge_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=10) is True
