@@ -228,6 +228,58 @@ int ktune_ac_forward(ktune_ctx* ctx, const ktune_ac* ac, const double* states, i
                      double* log_probs /* B x 3n */, double* probs /* B x 3n */,
                      double* values /* B */, int flags);
 
+/* ActorCritic::forward with the full Forward cache (actor_critic.hpp:31-43): h0 B x h,
+ * hp/hv B x g, logits/log_probs/probs B x 3n, values B (any may be NULL). Same exact fp64
+ * arithmetic as ktune_ac_forward. Honours KTUNE_F_DEVICE. */
+int ktune_ac_forward_cache(ktune_ctx* ctx, const ktune_ac* ac, const double* states, int64_t B, double* h0,
+                           double* hp, double* hv, double* logits, double* log_probs, double* probs, double* values,
+                           int flags);
+/* ActorCritic::backward (actor_critic.hpp:45-49): the cache of a forward on the same
+ * parameters (states B x n, h0, hp, hv) and upstream gradients w.r.t. the logits (B x 3n)
+ * and values (B) -> flat parameter gradient (num_params). Batch reductions are sequential
+ * in ascending sample order. Honours KTUNE_F_DEVICE. */
+int ktune_ac_backward(ktune_ctx* ctx, const ktune_ac* ac, const double* states, const double* h0,
+                      const double* hp, const double* hv, int64_t B, const double* d_logits,
+                      const double* d_values, double* grad, int flags);
+/* Current parameters of an agent (after ktune_ppo_update), flat layout, host memory. */
+int ktune_ac_get_params(ktune_ctx* ctx, const ktune_ac* ac, double* out);
+
+/* AdamOptimizer (actor_critic.hpp:66-79): moments on the device, step counter t. */
+typedef struct ktune_adam ktune_adam;
+int ktune_adam_create(ktune_ctx* ctx, int64_t dim, double step_size, double beta1, double beta2, double epsilon,
+                      ktune_adam** out);
+int ktune_adam_destroy(ktune_adam* adam);
+/* AdamOptimizer::step(params, grad): in-place update of params (dim). Honours KTUNE_F_DEVICE. */
+int ktune_adam_step(ktune_ctx* ctx, ktune_adam* adam, double* params, const double* grad, int flags);
+/* Moments (host copies, may be NULL) and step count. */
+int ktune_adam_state(ktune_ctx* ctx, const ktune_adam* adam, double* m, double* v, int64_t* t);
+
+/* compute_gae for E episodes of T steps (row-major E x T):
+ * delta_t = r_t + gamma v_{t+1} - v_t (v_T = terminal_values[e]), A_t = delta_t +
+ * gamma lambda A_{t+1}, returns_t = A_t + v_t. Honours KTUNE_F_DEVICE. */
+int ktune_compute_gae(ktune_ctx* ctx, int64_t E, int32_t T, const double* rewards, const double* values,
+                      const double* terminal_values, double gamma, double lambda, double* advantages,
+                      double* returns, int flags);
+
+/* ppo_update (PpoParams SPEC.md:209-216): advantages normalised over the
+ * N samples, num_epochs epochs of minibatches drawn from a Fisher-Yates permutation of
+ * Rng(seed_combine(seed, epoch)), per minibatch the clipped surrogate + value_coef *
+ * (V - R)^2 - entropy_coef * H loss, backward and one Adam step; agent parameters are
+ * updated in place on the device. states N x n (encoded features), actions N x n in
+ * {-1,0,+1}, old_logp/advantages/returns N. stats (may be NULL): mean over minibatch
+ * steps of (policy loss, value loss, entropy). Honours KTUNE_F_DEVICE (inputs). */
+typedef struct {
+  double clip_epsilon;   /* 0.3 */
+  double value_coef;     /* 1.0 */
+  double entropy_coef;   /* 0.1 */
+  int32_t num_epochs;    /* 3 */
+  int32_t pad;
+  int64_t minibatch_size; /* 256 */
+} ktune_ppo_params;
+int ktune_ppo_update(ktune_ctx* ctx, ktune_ac* ac, ktune_adam* adam, const ktune_ppo_params* params, int64_t N,
+                     const double* states, const int8_t* actions, const double* old_logp, const double* advantages,
+                     const double* returns, uint64_t seed, double* stats, int flags);
+
 /* ------------------------------------------------------------------ rollout
  * run_episodes (pinned details DESIGN.md §5.2). One task =
  * one workload (space + agent + cost model); tasks are batched into one

@@ -86,6 +86,25 @@ void ko_ac_forward(int n, int h, int g, const double* params, const double* stat
                    double* h0, double* hp, double* hv, double* logits, double* log_probs,
                    double* probs, double* values);
 
+/* PPO training step (actor_critic.hpp:45-49,66-79), builder-pinned
+ * arithmetic. */
+void ko_ac_backward(int n, int h, int g, const double* params, const double* states, const double* h0,
+                    const double* hp, const double* hv, int64_t B, const double* d_logits,
+                    const double* d_values, double* grad);
+void ko_adam_bias(double beta1, double beta2, int64_t t, double* bc1, double* bc2);
+void ko_adam_step(int64_t dim, double* params, const double* grad, double* m, double* v, double lr,
+                  double beta1, double beta2, double eps, double bc1, double bc2);
+void ko_compute_gae(int64_t E, int32_t T, const double* rewards, const double* values,
+                    const double* terminal_values, double gamma, double lambda, double* adv, double* ret);
+void ko_normalize_advantages(int64_t N, const double* adv, double* out);
+void ko_ppo_loss_grad(int n, int64_t B, const double* logp, const double* probs, const double* values,
+                      const int8_t* actions, const double* old_logp, const double* adv, const double* ret,
+                      double clip_eps, double c_v, double c_e, double* dl, double* dv, double* sums);
+int ko_ppo_update(int n, int h, int g, double* params, double* adam_m, double* adam_v, int64_t* adam_t,
+                  int64_t N, const double* states, const int8_t* actions, const double* old_logp,
+                  const double* adv, const double* ret, int num_epochs, int64_t mb, double lr,
+                  double clip_eps, double c_v, double c_e, uint64_t seed, double* stats);
+
 /* run_episodes, builder-pinned details in DESIGN.md §5.
  * E episodes with global ids episode_offset..episode_offset+E-1, T steps each.
  * idx_out: E x (T+1) x D visited configs (row t = Θ_t), score_out E x (T+1),

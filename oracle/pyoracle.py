@@ -556,3 +556,69 @@ def ref_adaptive_sample(sp: OSpace, cand_idx, cand_ids, cand_pred, visited, thre
     if rc != 0:
         raise RuntimeError(f"adaptive_sample rc={rc}: {ref_error()}")
     return dict(configs=out[:cnt.value], k_losses=kl[:kc.value])
+
+
+# ---------------------------------------------------------------- PPO
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def ac_backward(n, h, g, params, cache, d_logits, d_values):
+    P = port()
+    B = len(cache["states"])
+    grad = np.zeros(P.ko_ac_num_params(n, h, g))
+    c = {k: np.ascontiguousarray(cache[k], np.float64) for k in ("states", "h0", "hp", "hv")}
+    dl = np.ascontiguousarray(d_logits, np.float64)
+    dv = np.ascontiguousarray(d_values, np.float64)
+    P.ko_ac_backward(n, h, g, _p(np.ascontiguousarray(params, np.float64)), _p(c["states"]), _p(c["h0"]),
+                     _p(c["hp"]), _p(c["hv"]), C.c_int64(B), _p(dl), _p(dv), _p(grad))
+    return grad
+
+
+def adam_step(params, grad, m, v, t, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
+    """One AdamOptimizer::step at step number t (1-based); arrays updated in place."""
+    P = port()
+    bc1, bc2 = C.c_double(), C.c_double()
+    P.ko_adam_bias(C.c_double(b1), C.c_double(b2), C.c_int64(t), C.byref(bc1), C.byref(bc2))
+    P.ko_adam_step(C.c_int64(len(params)), _p(params), _p(np.ascontiguousarray(grad, np.float64)), _p(m), _p(v),
+                   C.c_double(lr), C.c_double(b1), C.c_double(b2), C.c_double(eps), bc1, bc2)
+
+
+def compute_gae(rewards, values, terminal_values, gamma=0.9, lam=0.99):
+    r = np.ascontiguousarray(rewards, np.float64)
+    r2 = r.reshape(-1, r.shape[-1]) if r.ndim > 1 else r.reshape(1, -1)
+    E, T = r2.shape
+    v = np.ascontiguousarray(values, np.float64).reshape(E, T)
+    tv = np.ascontiguousarray(terminal_values, np.float64).reshape(E)
+    adv, ret = np.zeros((E, T)), np.zeros((E, T))
+    port().ko_compute_gae(C.c_int64(E), C.c_int32(T), _p(r2), _p(v), _p(tv), C.c_double(gamma), C.c_double(lam),
+                          _p(adv), _p(ret))
+    return adv.reshape(r.shape), ret.reshape(r.shape)
+
+
+def ppo_loss_grad(n, fwd, actions, old_logp, adv, ret, clip_eps=0.3, c_v=1.0, c_e=0.1):
+    B = len(fwd["values"])
+    dl, dv, sums = np.zeros((B, 3 * n)), np.zeros(B), np.zeros(3)
+    a = np.ascontiguousarray(actions, np.int8)
+    f = {k: np.ascontiguousarray(fwd[k], np.float64) for k in ("log_probs", "probs", "values")}
+    port().ko_ppo_loss_grad(n, C.c_int64(B), _p(f["log_probs"]), _p(f["probs"]), _p(f["values"]), _p(a),
+                            _p(np.ascontiguousarray(old_logp, np.float64)), _p(np.ascontiguousarray(adv, np.float64)),
+                            _p(np.ascontiguousarray(ret, np.float64)), C.c_double(clip_eps), C.c_double(c_v),
+                            C.c_double(c_e), _p(dl), _p(dv), _p(sums))
+    return dl, dv, sums
+
+
+def ppo_update(n, h, g, params, adam_m, adam_v, adam_t, states, actions, old_logp, adv, ret, num_epochs=3, mb=256,
+               lr=1e-3, clip_eps=0.3, c_v=1.0, c_e=0.1, seed=0):
+    """ko_ppo_update: params / adam_m / adam_v updated in place; returns (adam_t, stats)."""
+    t = C.c_int64(adam_t)
+    st = np.zeros(3)
+    S = np.ascontiguousarray(states, np.float64)
+    N = len(S)
+    rc = port().ko_ppo_update(n, h, g, _p(params), _p(adam_m), _p(adam_v), C.byref(t), C.c_int64(N), _p(S),
+                              _p(np.ascontiguousarray(actions, np.int8)), _p(np.ascontiguousarray(old_logp, np.float64)),
+                              _p(np.ascontiguousarray(adv, np.float64)), _p(np.ascontiguousarray(ret, np.float64)),
+                              num_epochs, C.c_int64(mb), C.c_double(lr), C.c_double(clip_eps), C.c_double(c_v),
+                              C.c_double(c_e), C.c_uint64(seed), _p(st))
+    assert rc == 0
+    return t.value, st

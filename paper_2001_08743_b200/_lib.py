@@ -74,6 +74,11 @@ class SamplingParamsC(C.Structure):
                 ("max_iters", C.c_int32), ("restarts", C.c_int32)]
 
 
+class PpoParamsC(C.Structure):
+    _fields_ = [("clip_epsilon", C.c_double), ("value_coef", C.c_double), ("entropy_coef", C.c_double),
+                ("num_epochs", C.c_int32), ("pad", C.c_int32), ("minibatch_size", C.c_int64)]
+
+
 class SweepOutC(C.Structure):
     _fields_ = [("k", P), ("centroids", P), ("assignments", P), ("l2_loss", P), ("k_losses", P),
                 ("num_k", P), ("snapped", P)]
@@ -113,6 +118,15 @@ SIGNATURES = {
     "ktune_ac_create": (C.c_int, [P, C.c_int, C.c_int, C.c_int, P, C.POINTER(P)]),
     "ktune_ac_destroy": (C.c_int, [P]),
     "ktune_ac_forward": (C.c_int, [P, P, P, i64, P, P, P, C.c_int]),
+    "ktune_ac_forward_cache": (C.c_int, [P, P, P, i64, P, P, P, P, P, P, P, C.c_int]),
+    "ktune_ac_backward": (C.c_int, [P, P, P, P, P, P, i64, P, P, P, C.c_int]),
+    "ktune_ac_get_params": (C.c_int, [P, P, P]),
+    "ktune_adam_create": (C.c_int, [P, i64, dbl, dbl, dbl, dbl, C.POINTER(P)]),
+    "ktune_adam_destroy": (C.c_int, [P]),
+    "ktune_adam_step": (C.c_int, [P, P, P, P, C.c_int]),
+    "ktune_adam_state": (C.c_int, [P, P, P, P, C.POINTER(i64)]),
+    "ktune_compute_gae": (C.c_int, [P, i64, C.c_int32, P, P, P, dbl, dbl, P, P, C.c_int]),
+    "ktune_ppo_update": (C.c_int, [P, P, P, C.POINTER(PpoParamsC), i64, P, P, P, P, P, u64, P, C.c_int]),
     "ktune_rollout": (C.c_int, [P, C.c_int, C.POINTER(RolloutTaskC), C.c_int32, C.c_int]),
     "ktune_sa_search": (C.c_int, [P, C.c_int, C.POINTER(SaTaskC), C.c_int32, C.POINTER(SaParamsC), C.c_int]),
     "ktune_make_candidate_set": (C.c_int, [P, P, P, i64, P, C.POINTER(i64)]),

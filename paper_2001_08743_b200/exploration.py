@@ -76,12 +76,122 @@ class ActorCritic:
                                                     v.ctypes.data_as(C.c_void_p), 0))
         return dict(log_probs=lp, probs=pr, values=v)
 
+    def forward_cache(self, states):
+        """ActorCritic::forward with the full Forward cache (actor_critic.hpp:31-43): dict(states,
+        h0, hp, hv, logits, log_probs, probs, values), exact fp64 (bit-exact with the oracle)."""
+        S = np.ascontiguousarray(states, np.float64).reshape(-1, self.n)
+        B = len(S)
+        out = dict(states=S, h0=np.zeros((B, self.h)), hp=np.zeros((B, self.g)), hv=np.zeros((B, self.g)),
+                   logits=np.zeros((B, 3 * self.n)), log_probs=np.zeros((B, 3 * self.n)),
+                   probs=np.zeros((B, 3 * self.n)), values=np.zeros(B))
+        if B:
+            p = lambda k: out[k].ctypes.data_as(C.c_void_p)
+            self.ctx.check(L.lib().ktune_ac_forward_cache(self.ctx.h, self.h_dev, p("states"), B, p("h0"), p("hp"),
+                                                          p("hv"), p("logits"), p("log_probs"), p("probs"),
+                                                          p("values"), 0))
+        return out
+
+    def backward(self, cache, d_logits, d_values) -> np.ndarray:
+        """ActorCritic::backward (actor_critic.hpp:45-49) -> flat parameter gradient."""
+        B = len(cache["states"])
+        dl = np.ascontiguousarray(d_logits, np.float64).reshape(B, 3 * self.n)
+        dv = np.ascontiguousarray(d_values, np.float64).reshape(B)
+        grad = np.zeros(self.num_parameters)
+        c = {k: np.ascontiguousarray(cache[k], np.float64) for k in ("states", "h0", "hp", "hv")}
+        p = lambda a: a.ctypes.data_as(C.c_void_p)
+        self.ctx.check(L.lib().ktune_ac_backward(self.ctx.h, self.h_dev, p(c["states"]), p(c["h0"]), p(c["hp"]),
+                                                 p(c["hv"]), B, p(dl), p(dv), p(grad), 0))
+        return grad
+
+    def sync_parameters(self) -> np.ndarray:
+        """Refresh the host copy after device-side training (ppo_update)."""
+        self.ctx.check(L.lib().ktune_ac_get_params(self.ctx.h, self.h_dev, self.params.ctypes.data_as(C.c_void_p)))
+        return self.params
+
     def __del__(self):
         try:
             if self.h_dev is not None:
                 L.lib().ktune_ac_destroy(self.h_dev)
         except Exception:
             pass
+
+
+class Adam:
+    """ktune::AdamOptimizer (actor_critic.hpp:66-79); moments live on the device."""
+
+    def __init__(self, dim: int, step_size: float = 1e-3, beta1: float = 0.9, beta2: float = 0.999,
+                 epsilon: float = 1e-8, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.dim = dim
+        h = C.c_void_p()
+        self.ctx.check(L.lib().ktune_adam_create(self.ctx.h, dim, step_size, beta1, beta2, epsilon, C.byref(h)))
+        self.h = h
+
+    def step(self, params: np.ndarray, grad) -> None:
+        """AdamOptimizer::step: params updated in place (host array)."""
+        g = np.ascontiguousarray(grad, np.float64)
+        self.ctx.check(L.lib().ktune_adam_step(self.ctx.h, self.h, params.ctypes.data_as(C.c_void_p),
+                                               g.ctypes.data_as(C.c_void_p), 0))
+
+    def state(self):
+        m, v, t = np.zeros(self.dim), np.zeros(self.dim), C.c_int64()
+        self.ctx.check(L.lib().ktune_adam_state(self.ctx.h, self.h, m.ctypes.data_as(C.c_void_p),
+                                                v.ctypes.data_as(C.c_void_p), C.byref(t)))
+        return m, v, t.value
+
+    def __del__(self):
+        try:
+            L.lib().ktune_adam_destroy(self.h)
+        except Exception:
+            pass
+
+
+@dataclass
+class PpoParams:  # SPEC.md PpoParams (:209-216)
+    adam_step_size: float = 1e-3
+    discount_gamma: float = 0.9
+    gae_lambda: float = 0.99
+    num_epochs: int = 3
+    clip_epsilon: float = 0.3
+    value_coef: float = 1.0
+    entropy_coef: float = 0.1
+    minibatch_size: int = 256
+
+
+def compute_gae(rewards, values, terminal_values, gamma: float = 0.9, lam: float = 0.99,
+                ctx: Optional[Context] = None):
+    """compute_gae over E episodes x T steps on the GPU -> (advantages, returns)."""
+    ctx = ctx or default_context()
+    r = np.ascontiguousarray(rewards, np.float64)
+    r2 = r.reshape(-1, r.shape[-1]) if r.ndim > 1 else r.reshape(1, -1)
+    E, T = r2.shape
+    v = np.ascontiguousarray(values, np.float64).reshape(E, T)
+    if v.shape != r2.shape:
+        raise ConfigError("compute_gae: length mismatch")
+    tv = np.ascontiguousarray(terminal_values, np.float64).reshape(E)
+    adv, ret = np.zeros((E, T)), np.zeros((E, T))
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    ctx.check(L.lib().ktune_compute_gae(ctx.h, E, T, p(r2), p(v), p(tv), gamma, lam, p(adv), p(ret), 0))
+    return adv.reshape(r.shape), ret.reshape(r.shape)
+
+
+def ppo_update(agent: ActorCritic, adam: Adam, states, actions, old_logp, advantages, returns,
+               params: PpoParams = PpoParams(), seed: int = 0) -> dict:
+    """ppo_update on the GPU; the agent's parameters are updated in place
+    (device and host copies). Returns the training statistics."""
+    n = agent.n
+    S = np.ascontiguousarray(states, np.float64).reshape(-1, n)
+    N = len(S)
+    A = np.ascontiguousarray(actions, np.int8).reshape(N, n)
+    arr = [np.ascontiguousarray(x, np.float64).reshape(N) for x in (old_logp, advantages, returns)]
+    st = np.zeros(3)
+    pc = L.PpoParamsC(params.clip_epsilon, params.value_coef, params.entropy_coef, params.num_epochs, 0,
+                      params.minibatch_size)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    agent.ctx.check(L.lib().ktune_ppo_update(agent.ctx.h, agent.h_dev, adam.h, C.byref(pc), N, p(S), p(A),
+                                             p(arr[0]), p(arr[1]), p(arr[2]), seed, p(st), 0))
+    agent.sync_parameters()
+    return dict(policy_loss=st[0], value_loss=st[1], entropy=st[2])
 
 
 @dataclass
