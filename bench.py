@@ -392,6 +392,55 @@ def c3_pipeline(ctx, args, rank=0, world=1):
             "timing": "wall clock per stage, synchronised, max over ranks"}
 
 
+def ppo_secondary(ctx, args):
+    """one PPO training step at the paper's scale (PAPER.md:684-691,727-733:
+    128 episodes x 500 steps = 64,000 samples, 3 epochs of 256-sample minibatches = 750 Adam
+    steps) on ResNet-18 layer c2, after an exact rollout + GAE; the GPU ppo_update vs the
+    oracle restatement on one core (bit-identical parameters required)."""
+    from oracle import pyoracle as O
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
+    from paper_2001_08743_b200.exploration import (ActorCritic, Adam, PpoParams, RolloutTask, compute_gae,
+                                                   ppo_update, run_episodes_batch)
+    from workloads.tasks import encode, make_tasks
+    sp = S.resnet18_tasks()[1]
+    E, T = 128, 500
+    spec = make_tasks([sp], E, seed=args.seed + 13)[0]
+    ds = Space(sp, ctx)
+    model = fit_gbt(encode(sp, spec.train_idx), spec.train_y, seed=spec.seed)
+    agent = ActorCritic(sp.num_knobs, 128, 64, seed=spec.seed, ctx=ctx)
+    n = sp.num_knobs
+    tr = run_episodes_batch([RolloutTask(ds, agent, DeviceGbt(model, ds), spec.init_idx, 0, spec.seed)], T,
+                            exact=True)[0]
+    X = encode(sp, tr["idx"].reshape(-1, n)).reshape(E, T + 1, n)
+    pp = PpoParams()
+    term = agent.forward_cache(X[:, T])["values"]
+    adv, ret = compute_gae(tr["score"][:, 1:] - tr["score"][:, :-1], tr["value"], term, pp.discount_gamma,
+                           pp.gae_lambda, ctx=ctx)
+    Sx, A, lp = X[:, :T].reshape(-1, n), tr["actions"].reshape(-1, n), tr["logp"].reshape(-1)
+    p0 = agent.params.copy()
+    ts = []
+    for i in range(3):
+        agent.set_parameters(p0)
+        opt = Adam(agent.num_parameters, pp.adam_step_size, ctx=ctx)
+        t0 = time.perf_counter()
+        st = ppo_update(agent, opt, Sx, A, lp, adv.reshape(-1), ret.reshape(-1), pp, seed=1)
+        ts.append(time.perf_counter() - t0)
+    q = p0.copy()
+    m, v = np.zeros_like(q), np.zeros_like(q)
+    t0 = time.perf_counter()
+    O.ppo_update(n, 128, 64, q, m, v, 0, Sx, A, lp, adv.reshape(-1), ret.reshape(-1), pp.num_epochs,
+                 pp.minibatch_size, pp.adam_step_size, pp.clip_epsilon, pp.value_coef, pp.entropy_coef, 1)
+    cpu_s = time.perf_counter() - t0
+    gpu_ms = 1e3 * float(np.median(ts))
+    return {"workload": "ppo_update (SPEC.md:276-284): 128 episodes x 500 steps = 64,000 samples, 3 epochs x 256-sample "
+                        "minibatches (750 Adam steps), resnet18.c2 agent 128/64; host arrays in, parameters out",
+            "gpu_ms": gpu_ms, "samples_per_s": 3 * E * T / (gpu_ms * 1e-3),
+            "cpu_ms": 1e3 * cpu_s, "cpu_cores": 1, "cpu_kind": "port (oracle ko_ppo_update)",
+            "params_equal_oracle": bool(np.array_equal(agent.params, q)), "stats": st}
+
+
 def gbt_standalone(ctx, args, specs, spaces, gbts):
     """standalone K1 scoring of a device-resident candidate array (ResNet-18 task 0,
     16M random configurations, u8 indices), rows/s with its HBM roofline (D + 8 bytes per config:
@@ -598,6 +647,7 @@ def main():
     ap.add_argument("--cpu-T", type=int, default=8, help="CPU legs: steps [0, cpu_T) of every timed episode")
     ap.add_argument("--cpu1-episodes", type=int, default=256, help="single-thread CPU figure: episodes per task")
     ap.add_argument("--no-c1", action="store_true", help="skip SURVEY C1 (BASELINE configs[0]) timed in full")
+    ap.add_argument("--no-ppo", action="store_true", help="skip the PPO training-step secondary (SURVEY §8f row 4)")
     ap.add_argument("--kmeans-n", type=int, default=1 << 20)
     ap.add_argument("--kmeans-cpu-n", type=int, default=200_000)
     ap.add_argument("--kmeans-cpu-iters", type=int, default=5)
@@ -868,6 +918,13 @@ def main():
         except Exception as ex:  # reported, not hidden
             kmeans = {"error": repr(ex)}
 
+    ppo = None
+    if rank == 0 and world == 1 and not args.no_ppo:
+        try:
+            ppo = ppo_secondary(ctx, args)
+        except Exception as ex:  # reported, not hidden
+            ppo = {"error": repr(ex)}
+
     c1 = None
     if rank == 0 and world == 1 and not args.no_c1:
         try:
@@ -919,6 +976,7 @@ def main():
             "sa_baseline": sa,
             "candidates": cand,
             "c1": c1,
+            "ppo_update": ppo,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -14,9 +14,11 @@
 #define KTUNE_GPU_HPP
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -57,7 +59,7 @@ class Context {
 // its source text (validity.hpp:35) with the library's parser.
 class Space {
  public:
-  Space(Context& ctx, const DesignSpace& s) : ctx_(ctx), space_(s) {
+  Space(Context& ctx, const DesignSpace& s) : ctx_(ctx), space_(s), serial_(next_serial()) {
     std::vector<int32_t> card;
     std::vector<int64_t> values;
     std::vector<std::string> names;
@@ -88,6 +90,7 @@ class Space {
   Context& ctx() const { return ctx_; }
   const DesignSpace& space() const { return space_; }
   int index_bytes() const { return max_card_ <= 256 ? 1 : 2; }
+  uint64_t serial() const { return serial_; }  // unique per uploaded space (cache keys)
 
   // Lattice features back to knob indices: idx = round(x * (card - 1)) is exact
   // for x = idx / (card - 1) (design_space.cpp:195-197).
@@ -106,8 +109,13 @@ class Space {
   }
 
  private:
+  static uint64_t next_serial() {
+    static std::atomic<uint64_t> n{0};
+    return ++n;
+  }
   Context& ctx_;
   const DesignSpace& space_;
+  uint64_t serial_;
   ktune_space* h_ = nullptr;
   int max_card_ = 1;
 };
@@ -152,42 +160,105 @@ inline Clusterer make_clusterer(const Space& s, const SamplingParams& p) {
   };
 }
 
-// predict_batch / CostModel::predict (cost_model.hpp:62,82) on the GPU.
-inline Eigen::VectorXd predict(const Space& s, const GbtModel& m, const Eigen::MatrixXd& features) {
-  std::vector<int32_t> off;
-  std::vector<ktune_tree_node> nodes;
-  for (const RegressionTree& t : m.trees) {
+// A fitted ensemble uploaded to the device ONCE per fit (the K1 layout with integer
+// thresholds for this space); reuse it for every predict until the next fit.
+class Ensemble {
+ public:
+  Ensemble(const Space& s, const GbtModel& m) : ctx_(s.ctx().get()), num_features_(m.num_features) {
+    std::vector<int32_t> off;
+    std::vector<ktune_tree_node> nodes;
+    for (const RegressionTree& t : m.trees) {
+      off.push_back((int32_t)nodes.size());
+      for (const TreeNode& n : t.nodes) {
+        ktune_tree_node x{};
+        x.feature = n.feature;
+        x.left = n.left;
+        x.right = n.right;
+        x.threshold = n.threshold;
+        x.value = n.value;
+        nodes.push_back(x);
+      }
+    }
     off.push_back((int32_t)nodes.size());
+    check(ktune_gbt_create(ctx_, s.get(), m.num_features, m.base_prediction, m.learning_rate, (int)m.trees.size(),
+                           off.data(), nodes.data(), &h_),
+          ctx_);
+  }
+  ~Ensemble() { ktune_gbt_destroy(h_); }
+  Ensemble(const Ensemble&) = delete;
+  Ensemble& operator=(const Ensemble&) = delete;
+  ktune_gbt* get() const { return h_; }
+
+  // CostModel::predict (cost_model.cpp:231-236): fp64 feature rows.
+  Eigen::VectorXd predict(const Eigen::MatrixXd& features) const {
+    if (features.rows() && features.cols() != num_features_)
+      throw ConfigError("cost model: feature dimension " + std::to_string(features.cols()) +
+                        " does not match training dimension " + std::to_string(num_features_));
+    std::vector<double> x((size_t)features.rows() * (size_t)features.cols());
+    for (Eigen::Index i = 0; i < features.rows(); ++i)
+      for (Eigen::Index j = 0; j < features.cols(); ++j) x[(size_t)(i * features.cols() + j)] = features(i, j);
+    std::vector<double> y((size_t)features.rows());
+    check(ktune_gbt_predict_features(ctx_, h_, x.data(), features.rows(), y.data(), 0), ctx_);
+    Eigen::VectorXd out(features.rows());
+    for (Eigen::Index i = 0; i < features.rows(); ++i) out[i] = y[(size_t)i];
+    return out;
+  }
+
+ private:
+  ktune_ctx* ctx_;
+  int num_features_;
+  ktune_gbt* h_ = nullptr;
+};
+
+// Fingerprint of a model's complete content (FNV-1a over every field): the ensemble
+// cache below is keyed by it, so a refit (new trees) is never served a stale upload.
+inline uint64_t model_fingerprint(const GbtModel& m) {
+  uint64_t h = 0xCBF29CE484222325ULL;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = (const unsigned char*)p;
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001B3ULL;
+  };
+  mix(&m.base_prediction, 8);
+  mix(&m.learning_rate, 8);
+  mix(&m.num_features, sizeof(int));
+  for (const RegressionTree& t : m.trees) {
+    const size_t k = t.nodes.size();
+    mix(&k, sizeof(k));
     for (const TreeNode& n : t.nodes) {
-      ktune_tree_node x{};
-      x.feature = n.feature;
-      x.left = n.left;
-      x.right = n.right;
-      x.threshold = n.threshold;
-      x.value = n.value;
-      nodes.push_back(x);
+      mix(&n.feature, sizeof(int));
+      mix(&n.threshold, 8);
+      mix(&n.left, sizeof(int));
+      mix(&n.right, sizeof(int));
+      mix(&n.value, 8);
     }
   }
-  off.push_back((int32_t)nodes.size());
-  ktune_gbt* g = nullptr;
-  check(ktune_gbt_create(s.ctx().get(), s.get(), m.num_features, m.base_prediction, m.learning_rate,
-                         (int)m.trees.size(), off.data(), nodes.data(), &g),
-        s.ctx().get());
-  std::vector<double> x((size_t)features.rows() * (size_t)features.cols());
-  for (Eigen::Index i = 0; i < features.rows(); ++i)
-    for (Eigen::Index j = 0; j < features.cols(); ++j) x[(size_t)(i * features.cols() + j)] = features(i, j);
-  std::vector<double> y((size_t)features.rows());
-  const int rc = features.rows() && features.cols() != m.num_features
-                     ? KTUNE_ERR_CONFIG
-                     : ktune_gbt_predict_features(s.ctx().get(), g, x.data(), features.rows(), y.data(), 0);
-  ktune_gbt_destroy(g);
-  if (rc == KTUNE_ERR_CONFIG && features.cols() != m.num_features)
-    throw ConfigError("cost model: feature dimension " + std::to_string(features.cols()) +
-                      " does not match training dimension " + std::to_string(m.num_features));
-  check(rc, s.ctx().get());
-  Eigen::VectorXd out(features.rows());
-  for (Eigen::Index i = 0; i < features.rows(); ++i) out[i] = y[(size_t)i];
-  return out;
+  return h;
+}
+
+// predict_batch / CostModel::predict (cost_model.hpp:62,82) on the GPU. The uploaded
+// ensemble is cached per (space, model content) — a handful of live entries per thread —
+// so repeated predicts between fits upload nothing.
+inline Eigen::VectorXd predict(const Space& s, const GbtModel& m, const Eigen::MatrixXd& features) {
+  struct Entry {
+    uint64_t space;
+    uint64_t fp;
+    std::shared_ptr<Ensemble> e;
+  };
+  static thread_local std::vector<Entry> cache;
+  const uint64_t fp = model_fingerprint(m);
+  std::shared_ptr<Ensemble> e;
+  for (size_t i = 0; i < cache.size(); ++i)
+    if (cache[i].space == s.serial() && cache[i].fp == fp) {
+      e = cache[i].e;
+      std::rotate(cache.begin(), cache.begin() + i, cache.begin() + i + 1);  // most recent first
+      break;
+    }
+  if (!e) {
+    e = std::make_shared<Ensemble>(s, m);
+    cache.insert(cache.begin(), Entry{s.serial(), fp, e});
+    if (cache.size() > 4) cache.pop_back();
+  }
+  return e->predict(features);
 }
 
 }  // namespace gpu
