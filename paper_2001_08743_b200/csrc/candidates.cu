@@ -1,31 +1,28 @@
 // make_candidate_set on the device (sampling.cpp:16-31):
 //   ids = id_of(row) (design_space.cpp:158-167, mixed radix, last knob fastest)
-//   dedup by id, FIRST occurrence wins  -> stable radix sort of (id, row) by id,
-//                                          keep the head of every equal-id run
-//   rank by (predicted desc, id asc)    -> the kept rows are already in id order;
-//                                          a stable radix sort on the descending
-//                                          fitness key keeps id order within ties
-// Radix sorts: CUB (CUDA toolkit CCCL) DeviceRadixSort — library primitive.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_select.cuh>
-
+//   dedup by id, FIRST occurrence wins  -> stable radix sort of (id, row) by id over
+//                                          ceil(log2 |space|) key bits, keep the head of
+//                                          every equal-id run (an order-keeping compaction)
+//   rank by (predicted desc, id asc)    -> the kept rows are already in id order; a stable
+//                                          radix sort on a descending 64-bit image of the
+//                                          fitness keeps id order within ties
+// Sorts: the hand-written LSD radix sort of radix.cuh. No host round trip inside the
+// pipeline: the kept count stays in device memory and sizes the ranking sort's tiles.
 #include "internal.cuh"
+#include "radix.cuh"
 
 namespace {
 
-__global__ void ids_kernel(KtSpaceParams sp, const uint16_t* __restrict__ idx, int64_t n,
-                           uint64_t* __restrict__ ids, int64_t* __restrict__ rows) {
+template <class K>
+__global__ void ids_kernel(KtSpaceParams sp, const uint16_t* __restrict__ idx, int64_t n, uint64_t* __restrict__ ids,
+                           K* __restrict__ keys, uint32_t* __restrict__ rows) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t id = 0;
     for (int d = 0; d < sp.D; ++d) id = id * (uint64_t)sp.card[d] + (uint64_t)idx[i * sp.D + d];
     ids[i] = id;
-    rows[i] = i;
+    keys[i] = (K)id;
+    rows[i] = (uint32_t)i;
   }
-}
-
-__global__ void head_flags_kernel(const uint64_t* __restrict__ ids, int64_t n, uint8_t* __restrict__ flag) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    flag[i] = (i == 0 || ids[i] != ids[i - 1]) ? 1 : 0;
 }
 
 // Descending order on doubles as an ascending unsigned key.
@@ -36,16 +33,137 @@ __device__ __forceinline__ uint64_t desc_key(double x) {
   return ~b;                                          // descending
 }
 
-__global__ void rank_keys_kernel(const int64_t* __restrict__ rows, const double* __restrict__ pred, int64_t m,
-                                 uint64_t* __restrict__ keys) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    keys[i] = desc_key(pred[rows[i]]);
+constexpr int kCT = kt::rsort::kThreads, kCPer = kt::rsort::kPer, kCTile = kt::rsort::kTile;
+
+// Heads of equal-key runs of the id-sorted keys: per-tile head counts.
+template <class K>
+__global__ void __launch_bounds__(kCT) head_count_kernel(const K* __restrict__ k, int64_t n, uint32_t* __restrict__ cnt) {
+  __shared__ uint32_t c;
+  if (threadIdx.x == 0) c = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kCTile;
+  uint32_t mine = 0;
+  for (int q = 0; q < kCPer; ++q) {
+    const int64_t i = base + q * kCT + threadIdx.x;
+    if (i < n && (i == 0 || k[i] != k[i - 1])) ++mine;
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&c, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) cnt[blockIdx.x] = c;
+}
+
+// Exclusive scan of the per-tile counts (one block), total -> *d_m.
+__global__ void __launch_bounds__(1024) tile_scan_kernel(uint32_t* __restrict__ cnt, int tiles, int64_t* __restrict__ d_m) {
+  __shared__ uint32_t part[1024];
+  const int per = (tiles + 1023) / 1024, b0 = threadIdx.x * per, b1 = min(tiles, b0 + per);
+  uint32_t s = 0;
+  for (int b = b0; b < b1; ++b) s += cnt[b];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const uint32_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t run = part[threadIdx.x] - s;
+  for (int b = b0; b < b1; ++b) {
+    const uint32_t c = cnt[b];
+    cnt[b] = run;
+    run += c;
+  }
+  if (threadIdx.x == 1023) *d_m = part[1023];
+}
+
+// Order-keeping compaction of the run heads (blocked: thread t owns items t*kCPer..):
+// kept[j] = row, key2[j] = desc_key(pred[row]).
+template <class K>
+__global__ void __launch_bounds__(kCT) head_write_kernel(const K* __restrict__ k, const uint32_t* __restrict__ rows,
+                                                         int64_t n, const uint32_t* __restrict__ off,
+                                                         const double* __restrict__ pred, uint32_t* __restrict__ kept,
+                                                         uint64_t* __restrict__ key2) {
+  __shared__ uint32_t part[kCT];
+  const int64_t base = (int64_t)blockIdx.x * kCTile + (int64_t)threadIdx.x * kCPer;
+  uint32_t mask = 0;
+  for (int q = 0; q < kCPer; ++q) {
+    const int64_t i = base + q;
+    if (i < n && (i == 0 || k[i] != k[i - 1])) mask |= 1u << q;
+  }
+  const uint32_t c = __popc(mask);
+  part[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = 1; o < kCT; o <<= 1) {
+    const uint32_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t pos = off[blockIdx.x] + part[threadIdx.x] - c;
+  for (int q = 0; q < kCPer; ++q)
+    if ((mask >> q) & 1u) {
+      const uint32_t r = rows[base + q];
+      kept[pos] = r;
+      key2[pos] = desc_key(pred[r]);
+      ++pos;
+    }
+}
+
+__global__ void rows_out_kernel(const uint32_t* __restrict__ kept, const int64_t* __restrict__ d_m, int64_t cap,
+                                int64_t* __restrict__ out) {
+  const int64_t m = *d_m;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m && i < cap; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)kept[i];
 }
 
 __global__ void gather_ids_kernel(const int64_t* __restrict__ rows, const uint64_t* __restrict__ ids_by_row,
                                   int64_t m, uint64_t* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = ids_by_row[rows[i]];
+}
+
+template <class K>
+int64_t candidate_rows_impl(ktune_ctx* ctx, const ktune_space* space, const uint16_t* d_idx, const double* d_pred,
+                            int64_t n, int bits, int64_t** d_rows_out, uint64_t** d_ids_by_row) {
+  cudaStream_t s = ctx->stream;
+  const int tiles = (int)kt::ceil_div(n, kCTile);
+  // workspace: ids_row u64[n] | keys K[2n] | key2 u64[2n] | rows out i64[n] | vals u32[2n] | kept u32[2n] | counts
+  const size_t words = kt::rsort::scratch_words(n);
+  char* base = (char*)ctx->dev(kt::WS_SCRATCH, (size_t)n * (8 + 2 * sizeof(K) + 16 + 8 + 8 + 8) + 4 * (words + tiles) + 1024);
+  uint64_t* ids_row = (uint64_t*)base;
+  uint64_t* key2a = ids_row + n;
+  uint64_t* key2b = key2a + n;
+  int64_t* rows64 = (int64_t*)(key2b + n);
+  K* ka = (K*)(rows64 + n);
+  K* kb = ka + n;
+  uint32_t* va = (uint32_t*)(kb + n);
+  uint32_t* vb = va + n;
+  uint32_t* kept_a = vb + n;
+  uint32_t* kept_b = kept_a + n;
+  uint32_t* scratch = kept_b + n;
+  uint32_t* tcnt = scratch + words;
+  int64_t* d_m = (int64_t*)ctx->dev(kt::WS_VALID, 64);
+  const int th = 256;
+  const int grid = (int)std::min<int64_t>(kt::ceil_div(n, th), (int64_t)kt::sm_count(ctx) * 16);
+  ids_kernel<K><<<grid, th, 0, s>>>(space->params, d_idx, n, ids_row, ka, va);
+  // 1) stable sort (id, row) by the id's significant bits
+  const bool f1 = kt::rsort::sort_pairs<K>(s, ka, va, kb, vb, nullptr, n, bits, scratch);
+  const K* ks = f1 ? kb : ka;
+  const uint32_t* vs = f1 ? vb : va;
+  // 2) first occurrence of every id, in id order, with its descending fitness key
+  head_count_kernel<K><<<tiles, kCT, 0, s>>>(ks, n, tcnt);
+  tile_scan_kernel<<<1, 1024, 0, s>>>(tcnt, tiles, d_m);
+  head_write_kernel<K><<<tiles, kCT, 0, s>>>(ks, vs, n, tcnt, d_pred, kept_a, key2a);
+  // 3) stable sort of the kept rows by descending fitness (count from device memory)
+  const bool f2 = kt::rsort::sort_pairs<uint64_t>(s, key2a, kept_a, key2b, kept_b, d_m, n, 64, scratch);
+  rows_out_kernel<<<grid, th, 0, s>>>(f2 ? kept_b : kept_a, d_m, n, rows64);
+  kt::check_launch(ctx, "make_candidate_set", 5 + 3 * ((bits + 7) / 8) + 3 * 8);
+  int64_t m = 0;
+  KT_CUDA(cudaMemcpyAsync(&m, d_m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  KT_CUDA(cudaStreamSynchronize(s));
+  *d_rows_out = rows64;
+  *d_ids_by_row = ids_row;
+  return m;
 }
 
 }  // namespace
@@ -57,49 +175,13 @@ namespace kt {
 int64_t candidate_rows_dev(ktune_ctx* ctx, const ktune_space* space, const uint16_t* d_idx, const double* d_pred,
                            int64_t n, int64_t** d_rows_out, uint64_t** d_ids_by_row) {
   if (n > (int64_t)INT32_MAX) fail(KTUNE_ERR_CONFIG, "make_candidate_set: at most 2^31-1 rows per call");
-  cudaStream_t s = ctx->stream;
-  // scratch: ids_row[n] (id per original row), keys/vals ping-pong, flags
-  char* base = (char*)ctx->dev(kt::WS_SCRATCH, (size_t)n * (8 * 5 + 8 + 1) + 256);
-  uint64_t* ids_row = (uint64_t*)base;
-  uint64_t* k0 = ids_row + n;
-  uint64_t* k1 = k0 + n;
-  int64_t* v0 = (int64_t*)(k1 + n);
-  int64_t* v1 = v0 + n;
-  int64_t* kept = v1 + n;
-  uint8_t* flag = (uint8_t*)(kept + n);
-  int64_t* d_count = (int64_t*)ctx->dev(kt::WS_VALID, 64);
-  const int th = 256;
-  const int grid = (int)std::min<int64_t>(kt::ceil_div(n, th), (int64_t)kt::sm_count(ctx) * 16);
-  ids_kernel<<<grid, th, 0, s>>>(space->params, d_idx, n, ids_row, v0);
-  KT_CUDA(cudaMemcpyAsync(k0, ids_row, sizeof(uint64_t) * n, cudaMemcpyDeviceToDevice, s));
-  // 1) stable sort (id, row) by id
-  cub::DoubleBuffer<uint64_t> keys(k0, k1);
-  cub::DoubleBuffer<int64_t> vals(v0, v1);
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, vals, (int)n, 0, 64, s);
-  void* d_tmp = ctx->dev(kt::WS_SCRATCH2, tmp + 256);
-  KT_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp, keys, vals, (int)n, 0, 64, s));
-  // 2) first occurrence of every id
-  head_flags_kernel<<<grid, th, 0, s>>>(keys.Current(), n, flag);
-  size_t tmp2 = 0;
-  cub::DeviceSelect::Flagged(nullptr, tmp2, vals.Current(), flag, kept, d_count, (int)n, s);
-  d_tmp = ctx->dev(kt::WS_SCRATCH2, std::max(tmp, tmp2) + 256);
-  KT_CUDA(cub::DeviceSelect::Flagged(d_tmp, tmp2, vals.Current(), flag, kept, d_count, (int)n, s));
-  int64_t m = 0;
-  KT_CUDA(cudaMemcpyAsync(&m, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  KT_CUDA(cudaStreamSynchronize(s));
-  // 3) stable sort of the id-ordered kept rows by descending predicted fitness
-  rank_keys_kernel<<<grid, th, 0, s>>>(kept, d_pred, m, k0);
-  cub::DoubleBuffer<uint64_t> keys2(k0, k1);
-  cub::DoubleBuffer<int64_t> vals2(kept, v0);
-  size_t tmp3 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp3, keys2, vals2, (int)m, 0, 64, s);
-  d_tmp = ctx->dev(kt::WS_SCRATCH2, std::max(std::max(tmp, tmp2), tmp3) + 256);
-  KT_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp3, keys2, vals2, (int)m, 0, 64, s));
-  check_launch(ctx, "make_candidate_set", 5);
-  *d_rows_out = vals2.Current();
-  *d_ids_by_row = ids_row;
-  return m;
+  // significant id bits: ids < |space| (design_space.cpp:13-58 checks it fits 64 bits)
+  unsigned __int128 size = 1;
+  for (int d = 0; d < space->D; ++d) size *= (unsigned __int128)space->card[d];
+  int bits = 0;
+  while (bits < 64 && (((unsigned __int128)1) << bits) < size) ++bits;
+  if (bits <= 32) return candidate_rows_impl<uint32_t>(ctx, space, d_idx, d_pred, n, bits, d_rows_out, d_ids_by_row);
+  return candidate_rows_impl<uint64_t>(ctx, space, d_idx, d_pred, n, bits, d_rows_out, d_ids_by_row);
 }
 }  // namespace kt
 

@@ -215,9 +215,11 @@ __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
   uint32_t* s_node = reinterpret_cast<uint32_t*>(s_leaf + (size_t)T * NL);
   int32_t* s_idx = reinterpret_cast<int32_t*>(s_node + (size_t)T * NIP);
   for (int i = threadIdx.x; i < T * NL; i += kScoreThreads) s_leaf[i] = g_leaf[i];
-  for (int i = threadIdx.x; i < T * NIP; i += kScoreThreads) {
-    const int tr = i / NIP, k = i % NIP;
-    s_node[i] = k < NI ? g_node[tr * NI + k] : 0u;
+  if constexpr (NIP > 0) {  // depth 0 (single-leaf trees) has no internal nodes
+    for (int i = threadIdx.x; i < T * NIP; i += kScoreThreads) {
+      const int tr = i / NIP, k = i % NIP;
+      s_node[i] = k < NI ? g_node[tr * NI + k] : 0u;
+    }
   }
   __syncthreads();
   // Byte offsets inside the dynamic smem window. A column entry carries its own

@@ -10,14 +10,18 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("name,n,seed", [("resnet_c2", 20000, 0), ("synthetic8", 50000, 1),
-                                         ("resnet_dense_u16", 3000, 2)])
+                                         ("resnet_dense_u16", 3000, 2),
+                                         # radix-sort edges: one row, one tile exactly, tile + 1,
+                                         # several tiles, 64-bit ids (synthetic16 > 2^32 configs)
+                                         ("resnet_c2", 1, 3), ("resnet_c2", 2048, 4), ("synthetic8", 2049, 5),
+                                         ("synthetic16", 300_001, 6), ("vgg_c4", 1_000_003, 7)])
 def test_candidates_from_rows_matches_reference(O, ctx, ref_ok, name, n, seed):
     from paper_2001_08743_b200.context import Space
     from paper_2001_08743_b200.sampling import candidates_from_rows
     sp = SPACES[name]()
     osp = O.OSpace(sp)
     g = np.random.default_rng(seed)
-    base = np.stack([g.integers(0, c, n // 3) for c in sp.cards], 1).astype(np.int32)
+    base = np.stack([g.integers(0, c, max(1, n // 3)) for c in sp.cards], 1).astype(np.int32)
     idx = base[g.integers(0, len(base), n)]          # many duplicates
     ids = osp.ids(idx)
     pred_of = {i: v for i, v in zip(np.unique(ids), np.round(g.random(len(np.unique(ids))), 2))}
