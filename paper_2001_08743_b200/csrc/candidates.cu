@@ -189,6 +189,7 @@ extern "C" int ktune_candidates_from_rows(ktune_ctx* ctx, const ktune_space* spa
                                           const double* pred, int64_t n, int64_t* out_rows, uint64_t* out_ids,
                                           int64_t* out_n, int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_candidates_from_rows");
     if (n < 0) kt::fail(KTUNE_ERR_CONFIG, "make_candidate_set: negative count");
     const bool dev = flags & KTUNE_F_DEVICE;
     if (n == 0) {
@@ -239,6 +240,7 @@ __global__ void gather_rows_kernel(const int64_t* __restrict__ rows, int64_t m, 
 extern "C" int ktune_candidates_gather(ktune_ctx* ctx, const ktune_space* space, const uint16_t* idx,
                                        const double* pred, int64_t n, int64_t* out_n, int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_candidates_gather");
     if (n < 0 || !space) kt::fail(KTUNE_ERR_CONFIG, "candidates_gather: bad space or count");
     const bool dev = flags & KTUNE_F_DEVICE;
     const int D = space->D, W = ctx->world;

@@ -590,6 +590,7 @@ int ktune_gbt_destroy(ktune_gbt* g) {
 int ktune_gbt_predict_idx(ktune_ctx* ctx, const ktune_gbt* g, const void* idx, int idx_bytes,
                           int64_t B, double* out, int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_gbt_predict_idx");
     if (idx_bytes != 1 && idx_bytes != 2) kt::fail(KTUNE_ERR_CONFIG, "idx_bytes must be 1 or 2");
     if (B < 0) kt::fail(KTUNE_ERR_CONFIG, "negative batch");
     if (B == 0) return;
@@ -605,6 +606,7 @@ int ktune_gbt_predict_idx(ktune_ctx* ctx, const ktune_gbt* g, const void* idx, i
 int ktune_gbt_predict_features(ktune_ctx* ctx, const ktune_gbt* g, const double* x, int64_t B,
                                double* out, int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_gbt_predict_features");
     if (B < 0) kt::fail(KTUNE_ERR_CONFIG, "negative batch");
     if (B == 0) return;
     const bool dev = flags & KTUNE_F_DEVICE;

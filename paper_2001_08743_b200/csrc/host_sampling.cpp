@@ -277,6 +277,7 @@ int ktune_adaptive_sample(ktune_ctx* ctx, const ktune_space* space, const int32_
                           int64_t n_visited, const ktune_sampling_params* params, uint64_t rng_seed,
                           int32_t* out_idx, int32_t* out_count) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_adaptive_sample");
     if (N == 0) kt::fail(KTUNE_ERR_CONFIG, "adaptive_sample: empty candidate set");
     const int D = space->D;
     const int ib = *std::max_element(space->card.begin(), space->card.end()) <= 256 ? 1 : 2;

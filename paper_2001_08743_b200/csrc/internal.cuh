@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstring>
@@ -270,6 +271,14 @@ namespace kt {
 }  // namespace kt
 
 // Run `body` converting exceptions to status codes.
+// NVTX range over a C-ABI call (header-only NVTX v3: a no-op unless a tool such as
+// Nsight Systems / ncu --nvtx injects itself).
+struct KtRange {
+  explicit KtRange(const char* name) { nvtxRangePushA(name); }
+  ~KtRange() { nvtxRangePop(); }
+};
+#define KT_RANGE(name) KtRange kt_range_(name)
+
 template <class F>
 int kt_guard(ktune_ctx* ctx, F&& body) {
   try {

@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(kCertBT) assign_cert_kernel(
   const int D = sp.D;
   // dynamic layout sized by k (cert_smem_bytes): c_B (fp64), E_c, c_B rows in fp32 zero-padded to
   // DM (16-byte aligned for float4), the block's integer-sum deltas and counts, the feature table
-  double* s_c = sdyn;
+  double* s_c = sdyn;  // knob-major [d][c]: lanes reading different clusters' coordinate d hit distinct banks
   double* s_e = sdyn + k * D;  // per-cluster centroid-difference bound E_c
   float* s_c32 = reinterpret_cast<float*>(sdyn + ((k * D + kt::kMaxK + 1) & ~1));  // [k][DM]
   int32_t* s_sum = reinterpret_cast<int32_t*>(s_c32 + k * DM);
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(kCertBT) assign_cert_kernel(
   const float R32 = (float)(2 * D + 8) * 0x1.0p-24f;
   const double A32 = (double)(12 * D + 4) * 0x1.0p-24;
   for (int i = threadIdx.x; i < k * D; i += blockDim.x) {
-    s_c[i] = cB[i];
+    s_c[(i % D) * k + i / D] = cB[i];
     s_sum[i] = 0;
   }
   for (int i = threadIdx.x; i < k * DM; i += blockDim.x) {
@@ -592,13 +592,13 @@ __global__ void __launch_bounds__(kCertBT) assign_cert_kernel(
       const float amax = s_amax;
       double best = INFINITY;
       if (fmaf(-R32, s2, s2) - amax > fmaf(R32, s1, s1) + amax) {  // (2a) the winner's d2 against c_B in the reference order
-        const double* cc = s_c + w32 * D;
+        const double* cc = s_c + w32;  // coordinate d at cc[d * k]
         double t = kt::dsub(x[0], cc[0]);
         best = kt::dmul(t, t);
 #pragma unroll
         for (int d = 1; d < DM; ++d) {
           if (d < D) {
-            t = kt::dsub(x[d], cc[d]);
+            t = kt::dsub(x[d], cc[d * k]);
             best = kt::dadd(best, kt::dmul(t, t));
           }
         }
@@ -606,13 +606,13 @@ __global__ void __launch_bounds__(kCertBT) assign_cert_kernel(
       } else {  // (2b) near tie: the full fp64 scan with its own certificate
         double best_e = 0.0, lo_others = INFINITY;
         for (int c = 0; c < k; ++c) {
-          const double* cc = s_c + c * D;
+          const double* cc = s_c + c;
           double t = kt::dsub(x[0], cc[0]);
           double s = kt::dmul(t, t);
 #pragma unroll
           for (int d = 1; d < DM; ++d) {
             if (d < D) {
-              t = kt::dsub(x[d], cc[d]);
+              t = kt::dsub(x[d], cc[d * k]);
               s = kt::dadd(s, kt::dmul(t, t));
             }
           }
@@ -1792,7 +1792,7 @@ struct KMeans {
   // Stream work of one assignment pass (no host synchronisation: capturable into a
   // CUDA graph), ending with the iteration's scalars copied into pinned memory.
   void enqueue_assign(const double* cent, int k, const int32_t* prev, int32_t* asg, double* dd) {
-    KT_CUDA(cudaMemsetAsync(ull, 0, 24, s()));
+    KT_CUDA(cudaMemsetAsync(ull, 0, 32, s()));  // changed, -, uncertain, empty (all read back)
     const size_t smem = sizeof(double) * (k * D) + lut_smem;
     if (use_tc && k <= kTcMaxN && k >= kTcMinK) {
       // tcgen05 screening + certified exact winner (this rank's chunk range)
@@ -2293,6 +2293,7 @@ int ktune_kmeans_run(ktune_ctx* ctx, const ktune_space* space, const void* idx, 
                      int64_t N, int k, uint64_t seed, int max_iters, int restarts,
                      ktune_kmeans_out* out, int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_kmeans_run");
     if (N == 0) kt::fail(KTUNE_ERR_CONFIG, "kmeans: empty point set");
     if (k < 1 || k > N)
       kt::fail(KTUNE_ERR_CONFIG, "kmeans: k=" + std::to_string(k) + " out of range for " + std::to_string(N) + " points");
@@ -2313,6 +2314,7 @@ int ktune_adaptive_sweep(ktune_ctx* ctx, const ktune_space* space, const void* i
                          const uint64_t* ids, int64_t N, const ktune_sampling_params* p,
                          uint64_t rng_seed, ktune_sweep_out* out, int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_adaptive_sweep");
     if (N == 0) kt::fail(KTUNE_ERR_CONFIG, "adaptive_sample: empty candidate set");
     if (p->k_min >= p->k_max_exclusive || p->k_min < 1)
       kt::fail(KTUNE_ERR_CONFIG, "adaptive_sample: need 1 <= k_min < k_max_exclusive");
@@ -2333,6 +2335,7 @@ int ktune_snap(ktune_ctx* ctx, const ktune_space* space, const double* centroids
                const void* cand_idx, int idx_bytes, const uint64_t* cand_ids, int64_t N,
                int32_t* out_idx, int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_snap");
     if (k < 0 || k > kt::kMaxK) kt::fail(KTUNE_ERR_CONFIG, "snap: 0 <= k <= 64");
     if (k == 0) return;
     if (idx_bytes != 1 && idx_bytes != 2) kt::fail(KTUNE_ERR_CONFIG, "idx_bytes must be 1 or 2");

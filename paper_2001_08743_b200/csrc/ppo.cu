@@ -412,6 +412,7 @@ int ktune_ac_forward_cache(ktune_ctx* ctx, const ktune_ac* ac, const double* sta
                            double* hp, double* hv, double* logits, double* log_probs, double* probs, double* values,
                            int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_ac_forward_cache");
     check_ac(ac);
     if (B < 0) kt::fail(KTUNE_ERR_CONFIG, "negative batch");
     if (B == 0) return;
@@ -449,6 +450,7 @@ int ktune_ac_backward(ktune_ctx* ctx, const ktune_ac* ac, const double* states, 
                       const double* hp, const double* hv, int64_t B, const double* d_logits,
                       const double* d_values, double* grad, int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_ac_backward");
     check_ac(ac);
     if (B < 0) kt::fail(KTUNE_ERR_CONFIG, "negative batch");
     const bool dev = flags & KTUNE_F_DEVICE;
@@ -579,6 +581,7 @@ int ktune_ppo_update(ktune_ctx* ctx, ktune_ac* ac, ktune_adam* adam, const ktune
                      const double* states, const int8_t* actions, const double* old_logp, const double* advantages,
                      const double* returns, uint64_t seed, double* stats, int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_ppo_update");
     check_ac(ac);
     if (!adam || !pp || adam->dim != ac->num_params) kt::fail(KTUNE_ERR_CONFIG, "ppo_update: optimizer/agent mismatch");
     if (N <= 0) kt::fail(KTUNE_ERR_CONFIG, "ppo_update: empty trajectory batch");

@@ -516,6 +516,7 @@ int ktune_debug_math(ktune_ctx* ctx, int op, const double* x, int64_t n, double*
 int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks, int32_t T,
                   int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_rollout");
     if (num_tasks < 0 || T < 0) kt::fail(KTUNE_ERR_CONFIG, "rollout: bad task count or steps");
     if (num_tasks == 0) return;
     const bool dev = flags & KTUNE_F_DEVICE;

@@ -172,6 +172,7 @@ constexpr SaKernel kSaKernels[9] = {sa_kernel<0>, sa_kernel<1>, sa_kernel<2>, sa
 extern "C" int ktune_sa_search(ktune_ctx* ctx, int num_tasks, const ktune_sa_task* tasks, int32_t T,
                                const ktune_sa_params* params, int flags) {
   return kt_guard(ctx, [&] {
+    KT_RANGE("ktune_sa_search");
     if (num_tasks < 0 || T < 0 || !params) kt::fail(KTUNE_ERR_CONFIG, "sa_search: bad task count, steps or params");
     if (!(params->initial_temperature > 0.0) || !(params->cooling_rate > 0.0) || !(params->cooling_rate < 1.0))
       kt::fail(KTUNE_ERR_CONFIG, "sa_search: temperature must be positive and 0 < cooling_rate < 1");

@@ -78,6 +78,7 @@ def test_sa_grouped_launch_equals_single_calls(O, ctx):
     dev_tasks = [SaTask(t.space, t.cost_model, torch.from_numpy(t.init_idx.view(np.int16)).cuda(), 0, t.rng_seed)
                  for t in tasks]
     on_dev = sa_search_batch(dev_tasks, p, device_out=True)
+    ctx.synchronize()  # device-pointer calls are stream-ordered on the context's stream
     for g, s1, d in zip(grouped, singles, on_dev):
         for key in ("idx", "score", "accepted"):
             assert np.array_equal(g[key], s1[key])

@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_candidates.py tests/test_gpu_rollout.py -x -q 2>&1 | tail -4
+timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -3
