@@ -95,7 +95,11 @@ __host__ __device__ inline int n3_of(int n) { return (3 * n + 15) & ~15; }
 __host__ __device__ inline uint32_t off_b3(int n) { return kOffB1 + 128u * 2 * nk_of(n) * 2; }
 __host__ __device__ inline uint32_t off_f32(int n) { return off_b3(n) + (uint32_t)n3_of(n) * 256; }
 constexpr int kNF32 = 128 + 64 + 64 + 64 + 64 + 4;  // b0 bp1 bv1 wv2 bp2 bv2
-__host__ __device__ inline uint32_t off_gbt(int n) { return (off_f32(n) + kNF32 * 4 + 15) & ~15u; }
+// D <= 8: the step's counter-RNG draws are parked in shared memory (two float4 per thread,
+// thread-contiguous) between the L2 MMA window that computes them and the L3 epilogue.
+__host__ __device__ inline uint32_t off_draw(int n) { return (off_f32(n) + kNF32 * 4 + 15) & ~15u; }
+__host__ __device__ inline uint32_t draw_bytes(int n) { return n <= 8 ? 2u * 16u * kThr : 0u; }
+__host__ __device__ inline uint32_t off_gbt(int n) { return off_draw(n) + draw_bytes(n); }
 // + fused GBT: leaves f64 [ntrees][2^depth], node words u32 [ntrees][2^depth - 1], then the
 // thread-private knob columns int32 [n][kThr] the tree walks index (conflict-free).
 __host__ __device__ inline uint32_t gbt_leaf_bytes(int ntrees, int depth) { return (uint32_t)ntrees * (8u << depth); }
@@ -145,42 +149,63 @@ __device__ __forceinline__ float lg2f(float x) {
   return y;
 }
 // S * tanh(x) from y = -2 log2(e) x (the scale is folded into the
-// pre-activation FMA): e = exp(-2x), S tanh(x) = 2S/(1 + e) - S. Two SFU ops;
-// absolute error ~4e-7 * S (x -> -inf: e = inf, 1/(1+e) = 0 -> -S).
+// pre-activation FMA): e = exp(-2x), S tanh(x) = 2S/(1 + e) - S. A PAIR of
+// units shares one reciprocal: with d = 1 + e, 1/d_a = d_b / (d_a d_b), so a
+// pair costs two ex2 and one rcp on the SFU (3 MUFU instead of 4) and the rest
+// runs as packed f32x2 FMA-pipe instructions. y is clamped at 63 so that
+// d_a d_b <= 2^126 stays finite (tanh(-21.8) = -1 to 2^-62). Absolute error
+// <= ~5e-7 * S (ex2 2^-22.7, rcp 2^-23.3, three roundings).
 constexpr float kK2L = -2.8853900817779268f;  // -2 log2(e)
-__device__ __forceinline__ float act_scaled(float y, float S) {
-  const float r = rcpf(1.0f + ex2f(y));
-  return fmaf(r, 2.f * S, -S);
+__device__ __forceinline__ float2 act2(float2 y, float S) {
+  const float ea = ex2f(fminf(y.x, 63.f)), eb = ex2f(fminf(y.y, 63.f));
+  const float2 d = __fadd2_rn(make_float2(ea, eb), make_float2(1.f, 1.f));
+  const float R = rcpf(d.x * d.y);
+  const float2 r = __fmul2_rn(make_float2(d.y, d.x), make_float2(R, R));
+  return __ffma2_rn(r, make_float2(2.f * S, 2.f * S), make_float2(-S, -S));
+}
+// Pre-activation pair: acc * sc + b (b from shared memory, 8-byte aligned).
+__device__ __forceinline__ float2 pre2(uint32_t a0, uint32_t a1, float sc, const float* b) {
+  return __ffma2_rn(make_float2(__uint_as_float(a0), __uint_as_float(a1)), make_float2(sc, sc),
+                    *reinterpret_cast<const float2*>(b));
 }
 
 __device__ __forceinline__ uint32_t h2bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// fp16 hi/lo split of a pair: hi = RN_f16(v), lo = RN_f16(v - hi) (v - hi is exact).
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 f = __half22float2(h);
+  hi = h2bits(h);
+  lo = h2bits(__float22half2_rn(__fadd2_rn(make_float2(a, b), make_float2(-f.x, -f.y))));
+}
 
 // Eight consecutive K values of row r (already scaled): hi at column k0, lo
 // at column 64 + k0 of a [128 x 128] K-major operand buffer.
 __device__ __forceinline__ void store8_split(unsigned char* Ab, int r, int k0, const float* v) {
   uint32_t hi[4], lo[4];
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const __half2 h = __floats2half2_rn(v[2 * p], v[2 * p + 1]);
-    const float2 f = __half22float2(h);
-    hi[p] = h2bits(h);
-    lo[p] = h2bits(__floats2half2_rn(__fsub_rn(v[2 * p], f.x), __fsub_rn(v[2 * p + 1], f.y)));
-  }
+  for (int p = 0; p < 4; ++p) split2(v[2 * p], v[2 * p + 1], hi[p], lo[p]);
   *reinterpret_cast<uint4*>(Ab + kt::tc::kmajor_offset(r, k0, 128)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
   *reinterpret_cast<uint4*>(Ab + kt::tc::kmajor_offset(r, 64 + k0, 128)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
 }
 
-__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
-  const __half2 h = __floats2half2_rn(a, b);
-  const float2 f = __half22float2(h);
-  hi = h2bits(h);
-  lo = h2bits(__floats2half2_rn(__fsub_rn(a, f.x), __fsub_rn(b, f.y)));
+// 16 units (TMEM columns already loaded into v) -> S*tanh -> fp16 hi/lo -> operand columns c0..c0+15.
+__device__ __forceinline__ void act_store16(unsigned char* Ab, int r, int c0, const uint32_t* v, float sc,
+                                            const float* bias) {
+  float hv[16];
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const float2 h = act2(pre2(v[j], v[j + 1], sc, bias + j), kActScale);
+    hv[j] = h.x;
+    hv[j + 1] = h.y;
+  }
+  store8_split(Ab, r, c0, hv);
+  store8_split(Ab, r, c0 + 8, hv + 8);
 }
-
-__device__ __forceinline__ void sync_slot(int slot) {
+__device__ __forceinline__ void sync_slot(int slot, int nthreads = 128) {
   kt::tc::fence_proxy_async();
   kt::tc::fence_before();
-  kt::tc::named_bar(1 + slot, 128);
+  kt::tc::named_bar(1 + slot, nthreads);
 }
 
 // Three-product split GEMM over 4 K chunks of 16: hi*hi + hi*lo + lo*hi.
@@ -229,6 +254,8 @@ __device__ __forceinline__ void store_row_idx(uint16_t* dst, const Cfg<NMAX>& c,
 
 // Exact fp64 re-decision of row `L`'s flagged knobs by the whole warp (same
 // operations and order as the exact kernel's forward_tile and the oracle).
+// cfg is each lane's own configuration (row L's is shuffled from lane L); fastp[2d],
+// fastp[2d+1] are lane L's fast p0 and c1 (or the planted draw) of knob d.
 // Returns, in lane L, the exact actions (2 bits per knob) and the sum of the
 // exact log-probabilities of the flagged knobs; check-mode statistics too.
 struct Redecided {
@@ -317,6 +344,55 @@ __device__ __noinline__ Redecided exact_redecide(const TcTask& tk, int t, int L,
   return {acts, lp_exact};
 }
 
+// Prologue shared by both kernels: the actor-critic weights -> fp16 hi/lo UMMA operands
+// (power-of-two scaled), biases (and the value head) -> fp32 in shared memory.
+__device__ __forceinline__ void stage_weights(const TcTask& tk, unsigned char* sm, const int* scard, int tid, int nthr) {
+  const int n = tk.n, nk = nk_of(n), K1 = 2 * nk, N3 = n3_of(n);
+  const double* __restrict__ P = tk.params;
+  const int ob0 = kH * n, owp1 = ob0 + kH, obp1 = owp1 + kG * kH, owp2 = obp1 + kG, obp2 = owp2 + 3 * n * kG,
+            owv1 = obp2 + 3 * n, obv1 = owv1 + kG * kH, owv2 = obv1 + kG, obv2 = owv2 + kG;
+  unsigned char* B2 = sm + kOffB2;
+  unsigned char* B1 = sm + kOffB1;
+  unsigned char* B3 = sm + off_b3(n);
+  float* f32 = reinterpret_cast<float*>(sm + off_f32(n));
+  {
+    const double s1 = ldexp(1.0, tk.e1), s2 = ldexp(1.0, tk.e2), s3 = ldexp(1.0, tk.e3);
+    for (int i = tid; i < 128 * K1; i += nthr) {
+      const int j = i / K1, k = i % K1, part = k >= nk, kk = part ? k - nk : k;
+      double v = 0.0;
+      if (kk < n && scard[kk] > 1) v = kt::dmul(kt::ddiv(P[kk * kH + j], (double)(scard[kk] - 1)), s1);
+      const __half hi = __double2half(v);
+      const __half o = part ? __double2half(kt::dsub(v, (double)__half2float(hi))) : hi;
+      *reinterpret_cast<__half*>(B1 + kt::tc::kmajor_offset(j, k, K1)) = o;
+    }
+    for (int i = tid; i < 128 * 256; i += nthr) {
+      const int u = i >> 8, k = i & 255, part = k >> 7, kk = k & 127;
+      const double wv = u < kG ? P[owp1 + kk * kG + u] : P[owv1 + kk * kG + (u - kG)];
+      const double v = kt::dmul(wv, s2);
+      const __half hi = __double2half(v);
+      const __half o = part ? __double2half(kt::dsub(v, (double)__half2float(hi))) : hi;
+      *reinterpret_cast<__half*>(B2 + kt::tc::kmajor_offset(u, k, 256)) = o;
+    }
+    for (int i = tid; i < N3 * 128; i += nthr) {
+      const int a = i >> 7, k = i & 127, part = k >> 6, kk = k & 63;
+      const double v = a < 3 * n ? kt::dmul(P[owp2 + kk * 3 * n + a], s3) : 0.0;
+      const __half hi = __double2half(v);
+      const __half o = part ? __double2half(kt::dsub(v, (double)__half2float(hi))) : hi;
+      *reinterpret_cast<__half*>(B3 + kt::tc::kmajor_offset(a, k, 128)) = o;
+    }
+    for (int i = tid; i < kNF32; i += nthr) {
+      float v = 0.f;
+      if (i < 128) v = (float)(P[ob0 + i] * (double)kK2L);  // tanh layers: bias * -2log2(e)
+      else if (i < 192) v = (float)(P[obp1 + i - 128] * (double)kK2L);
+      else if (i < 256) v = (float)(P[obv1 + i - 192] * (double)kK2L);
+      else if (i < 320) v = (float)P[owv2 + i - 256];
+      else if (i < 384) v = i - 320 < 3 * n ? (float)P[obp2 + i - 320] : 0.f;
+      else if (i == 384) v = (float)P[obv2];
+      f32[i] = v;
+    }
+  }
+}
+
 template <int NMAX>
 __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_constant__ TcLaunch L) {
   extern __shared__ __align__(1024) unsigned char sm[];
@@ -350,42 +426,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
   // ---- prologue: weights -> fp16 hi/lo operands, biases -> fp32
   if (tid < kt::kMaxKnobs) scard[tid] = tk.card[tid];
   __syncthreads();
-  {
-    const double s1 = ldexp(1.0, tk.e1), s2 = ldexp(1.0, tk.e2), s3 = ldexp(1.0, tk.e3);
-    for (int i = tid; i < 128 * K1; i += kThr) {
-      const int j = i / K1, k = i % K1, part = k >= nk, kk = part ? k - nk : k;
-      double v = 0.0;
-      if (kk < n && scard[kk] > 1) v = kt::dmul(kt::ddiv(P[kk * kH + j], (double)(scard[kk] - 1)), s1);
-      const __half hi = __double2half(v);
-      const __half o = part ? __double2half(kt::dsub(v, (double)__half2float(hi))) : hi;
-      *reinterpret_cast<__half*>(B1 + kt::tc::kmajor_offset(j, k, K1)) = o;
-    }
-    for (int i = tid; i < 128 * 256; i += kThr) {
-      const int u = i >> 8, k = i & 255, part = k >> 7, kk = k & 127;
-      const double wv = u < kG ? P[owp1 + kk * kG + u] : P[owv1 + kk * kG + (u - kG)];
-      const double v = kt::dmul(wv, s2);
-      const __half hi = __double2half(v);
-      const __half o = part ? __double2half(kt::dsub(v, (double)__half2float(hi))) : hi;
-      *reinterpret_cast<__half*>(B2 + kt::tc::kmajor_offset(u, k, 256)) = o;
-    }
-    for (int i = tid; i < N3 * 128; i += kThr) {
-      const int a = i >> 7, k = i & 127, part = k >> 6, kk = k & 63;
-      const double v = a < 3 * n ? kt::dmul(P[owp2 + kk * 3 * n + a], s3) : 0.0;
-      const __half hi = __double2half(v);
-      const __half o = part ? __double2half(kt::dsub(v, (double)__half2float(hi))) : hi;
-      *reinterpret_cast<__half*>(B3 + kt::tc::kmajor_offset(a, k, 128)) = o;
-    }
-    for (int i = tid; i < kNF32; i += kThr) {
-      float v = 0.f;
-      if (i < 128) v = (float)(P[ob0 + i] * (double)kK2L);  // tanh layers: bias * -2log2(e)
-      else if (i < 192) v = (float)(P[obp1 + i - 128] * (double)kK2L);
-      else if (i < 256) v = (float)(P[obv1 + i - 192] * (double)kK2L);
-      else if (i < 320) v = (float)P[owv2 + i - 256];
-      else if (i < 384) v = i - 320 < 3 * n ? (float)P[obp2 + i - 320] : 0.f;
-      else if (i == 384) v = (float)P[obv2];
-      f32[i] = v;
-    }
-  }
+  stage_weights(tk, sm, scard, tid, kThr);
   double* s_leaf = reinterpret_cast<double*>(sm + off_gbt(n));
   uint32_t* s_node = reinterpret_cast<uint32_t*>(sm + off_gbt(n) + (tk.gnode ? gbt_leaf_bytes(tk.ntrees, tk.depth) : 0));
   int32_t* s_col = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(s_node) +
@@ -410,7 +451,6 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
 
   const int slot = w >> 2, q = w & 3;
   const bool slot_used = 4 * slot < nw;
-  unsigned long long n_fallback = 0, n_checked = 0;
   if (slot_used) {
     const bool lw = w < nw;
     const int64_t e = row0 + 32 * w + lane;
@@ -460,10 +500,16 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
     }
     const int gh = tk.ntrees / 2;  // the walk of row t runs in two halves inside step t's MMA waits
     uint32_t ph = 0;
+#if KT_TC_TRACE
     const bool trace_cta = L.check == 2 && blockIdx.x == 0 && q == 0 && lane == 0;
+#endif
+#if KT_TC_TRACE  // phase trace (check mode 2, tools/trace_tc.py): build with -DKT_TC_TRACE=1
 #define TR(k)                                                                                  \
   if (trace_cta && (t == 200 || t == 201))                                                      \
     L.counters[4 + (slot * 2 + (t - 200)) * 16 + (k)] = (unsigned long long)clock64();
+#else
+#define TR(k)
+#endif
     for (int t = L.t_begin; t < L.t_end; ++t) {
       TR(0)
       // ---- L1 operand: [idx | idx] as fp16 (exact integers)
@@ -505,11 +551,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
           uint32_t v[16];
           kt::tc::ld_32x32b_x16(tcol + c0, v);
           kt::tc::ld_wait();
-          float hv[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) hv[j] = act_scaled(fmaf(__uint_as_float(v[j]), sc1, sb0[c0 + j]), kActScale);
-          store8_split(Ab, r, c0, hv);
-          store8_split(Ab, r, c0 + 8, hv + 8);
+          act_store16(Ab, r, c0, v, sc1, sb0 + c0);
         }
         // units 64..127: raw accumulators to registers before L2 overwrites the columns
         uint32_t* r0 = raw;
@@ -530,9 +572,8 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         // units 64..127 while the L2 MMAs run: tanh + hi/lo split in registers
 #pragma unroll
         for (int j = 0; j < 64; j += 2) {
-          const float a = act_scaled(fmaf(__uint_as_float(raw[j]), sc1, sb0[64 + j]), kActScale);
-          const float b = act_scaled(fmaf(__uint_as_float(raw[j + 1]), sc1, sb0[65 + j]), kActScale);
-          split2(a, b, raw[j], raw[j + 1]);  // raw[j] = hi pair, raw[j+1] = lo pair
+          const float2 h = act2(pre2(raw[j], raw[j + 1], sc1, sb0 + 64 + j), kActScale);
+          split2(h.x, h.y, raw[j], raw[j + 1]);  // raw[j] = hi pair, raw[j+1] = lo pair
         }
         TR(5)
         kt::tc::mbar_wait(mb, ph);
@@ -560,6 +601,12 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
           const uint64_t hsh = kt::mix64(tk.seed ^ kt::mix64((ge * (uint64_t)T + (uint64_t)t) * (uint64_t)n +
                                                              (uint64_t)d + 0x9E3779B97F4A7C15ULL));
           ufs[d] = (float)(uint32_t)(hsh >> 40) * 0x1.0p-24f;  // |uf - u| < 2^-24
+          if constexpr (NMAX > 8) asm volatile("" : "+f"(ufs[d]));  // keep the draws inside the L2 MMA window
+        }
+        if constexpr (NMAX == 8) {  // park them in shared memory across the L2 epilogue (no spills)
+          float4* sd = reinterpret_cast<float4*>(sm + off_draw(n));
+          sd[tid] = make_float4(ufs[0], ufs[1], ufs[2], ufs[3]);
+          sd[kThr + tid] = make_float4(ufs[4], ufs[5], ufs[6], ufs[7]);
         }
         if (tk.gnode) {  // fused K1, row t: second half of the walk while the L2 MMAs run
           gs = gbt_walk(gs, s_node, s_leaf, mycol, gh, tk.ntrees, tk.depth);
@@ -574,11 +621,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
           uint32_t v[16];
           kt::tc::ld_32x32b_x16(tcol + c0, v);
           kt::tc::ld_wait();
-          float hv[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) hv[j] = act_scaled(fmaf(__uint_as_float(v[j]), sc2, sbp1[c0 + j]), kActScale);
-          store8_split(Ab, r, c0, hv);
-          store8_split(Ab, r, c0 + 8, hv + 8);
+          act_store16(Ab, r, c0, v, sc2, sbp1 + c0);
         }
       }
       ph ^= 1;
@@ -591,16 +634,18 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       }
       if (lw) {
         // ---- L2 epilogue (value half), overlapping the L3 MMAs: v = wv2 . tanh(.) + bv2
-        float vs = 0.f;
+        float2 vs2 = make_float2(0.f, 0.f);
 #pragma unroll 1
         for (int c0 = 64; c0 < 128; c0 += 16) {
           uint32_t v[16];
           kt::tc::ld_32x32b_x16(tcol + c0, v);
           kt::tc::ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            vs = fmaf(swv2[c0 - 64 + j], act_scaled(fmaf(__uint_as_float(v[j]), sc2, sbv1[c0 - 64 + j]), 1.f), vs);
+          for (int j = 0; j < 16; j += 2)
+            vs2 = __ffma2_rn(*reinterpret_cast<const float2*>(swv2 + c0 - 64 + j),
+                             act2(pre2(v[j], v[j + 1], sc2, sbv1 + c0 - 64 + j), 1.f), vs2);
         }
+        const float vs = vs2.x + vs2.y;
         if (lr && L.check != 4) {
           const float v = vs + sbv2[0];
           if (tk.value) tk.value[e * T + t] = (double)v;
@@ -611,11 +656,20 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         kt::tc::fence_after();
         TR(13)
         // ---- L3 epilogue: per-knob softmax, certified inverse-CDF draw, saturating move
+        if constexpr (NMAX == 8) {
+          const float4* sd = reinterpret_cast<const float4*>(sm + off_draw(n));
+          const float4 u0 = sd[tid], u1 = sd[kThr + tid];
+          ufs[0] = u0.x; ufs[1] = u0.y; ufs[2] = u0.z; ufs[3] = u0.w;
+          ufs[4] = u1.x; ufs[5] = u1.y; ufs[6] = u1.z; ufs[7] = u1.w;
+        }
         uint64_t acts = 0;
         uint32_t cert = 0;
         float lpj = 0.f;
         const float delta = L.delta;
-        float* fastp = reinterpret_cast<float*>(Ab + 8192 * q + 2048);  // check mode: fast p0/c1 per (row, knob)
+        float* fastp = reinterpret_cast<float*>(Ab + 8192 * q + 2048);  // fast p0/c1 per (row, knob) for re-decisions
+        float fp0[NMAX], fc1[NMAX];
+        // Branch-free over all NMAX knobs (knobs >= n see zero logits and are masked), so the
+        // per-knob dependent chains (ex2 -> rcp -> lg2) of all knobs interleave.
 #pragma unroll
         for (int g = 0; g < NMAX / 8; ++g) {  // knob groups of 8: 24 logit columns
           if (8 * g < n) {
@@ -626,46 +680,54 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
 #pragma unroll
             for (int dd = 0; dd < 8; ++dd) {
               const int d = 8 * g + dd;
-              if (d < n) {
-                const float l0 = fmaf(__uint_as_float(v[3 * dd]), sc3, sbp2[3 * d]);
-                const float l1 = fmaf(__uint_as_float(v[3 * dd + 1]), sc3, sbp2[3 * d + 1]);
-                const float l2 = fmaf(__uint_as_float(v[3 * dd + 2]), sc3, sbp2[3 * d + 2]);
-                const float m = fmaxf(l0, fmaxf(l1, l2));
-                const float e0 = ex2f((l0 - m) * 1.4426950408889634f), e1 = ex2f((l1 - m) * 1.4426950408889634f),
-                            e2 = ex2f((l2 - m) * 1.4426950408889634f);
-                const float s = e0 + e1 + e2;
-                const float rs = rcpf(s);
-                const float p0 = e0 * rs, c1 = (e0 + e1) * rs;
-                float uf = ufs[d];
-                if (L.check == 5) {  // planted draw 2 delta below/above p0 or c1 (bits of the real draw)
-                  const float base = uf < 0.5f ? p0 : c1;
-                  uf = fminf(fmaxf(base + ((uf * 4.f - floorf(uf * 4.f)) < 0.5f ? -2.f : 2.f) * delta, 0.f),
-                             0x1.fffffep-1f);
-                }
-                const int a = uf < p0 ? 0 : (uf < c1 ? 1 : 2);
-                const bool ok = fabsf(uf - p0) > delta && fabsf(uf - c1) > delta;
-                acts |= (uint64_t)a << (2 * d);
-                if (L.check == 1 || L.check == 5 || !ok) {  // the re-decision compares against these
-                  fastp[(lane * NMAX + d) * 2] = p0;
-                  fastp[(lane * NMAX + d) * 2 + 1] = L.check == 5 ? uf : c1;
-                }
-                const float lpa = (a == 0 ? l0 : (a == 1 ? l1 : l2)) - m - lg2f(s) * 0.69314718055994531f;
-                cert |= ok ? 1u << d : 0u;
-                lpj += ok ? lpa : 0.f;  // branch-free; uncertain knobs add their exact log-probability later
+              const float l0 = fmaf(__uint_as_float(v[3 * dd]), sc3, sbp2[3 * d]);
+              const float l1 = fmaf(__uint_as_float(v[3 * dd + 1]), sc3, sbp2[3 * d + 1]);
+              const float l2 = fmaf(__uint_as_float(v[3 * dd + 2]), sc3, sbp2[3 * d + 2]);
+              const float m = fmaxf(l0, fmaxf(l1, l2));
+              const float e0 = ex2f((l0 - m) * 1.4426950408889634f), e1 = ex2f((l1 - m) * 1.4426950408889634f),
+                          e2 = ex2f((l2 - m) * 1.4426950408889634f);
+              const float s = e0 + e1 + e2;
+              const float rs = rcpf(s);
+              const float p0 = e0 * rs, c1 = (e0 + e1) * rs;
+              float uf = ufs[d];
+              if (L.check == 5) {  // planted draw 2 delta below/above p0 or c1 (bits of the real draw)
+                const float base = uf < 0.5f ? p0 : c1;
+                uf = fminf(fmaxf(base + ((uf * 4.f - floorf(uf * 4.f)) < 0.5f ? -2.f : 2.f) * delta, 0.f),
+                           0x1.fffffep-1f);
               }
+              const int a = uf < p0 ? 0 : (uf < c1 ? 1 : 2);
+              const bool ok = fabsf(uf - p0) > delta && fabsf(uf - c1) > delta && d < n;
+              acts |= (uint64_t)a << (2 * d);
+              fp0[d] = p0;
+              fc1[d] = L.check == 5 ? uf : c1;
+              const float lpa = (a == 0 ? l0 : (a == 1 ? l1 : l2)) - m - lg2f(s) * 0.69314718055994531f;
+              cert |= ok ? 1u << d : 0u;
+              lpj += ok ? lpa : 0.f;  // uncertain knobs add their exact log-probability later
             }
+          } else {
+#pragma unroll
+            for (int dd = 0; dd < 8; ++dd) fp0[8 * g + dd] = fc1[8 * g + dd] = 0.f;
           }
         }
         uint32_t fb;
         TR(14)
         const uint32_t allk = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
         const bool chk = L.check == 1 || L.check == 5;  // every knob re-decided exactly
-        fb = chk ? allk : (L.check == 3 ? 0u : (allk & ~cert));  // 3: timing experiment (no MMAs)
+        fb = chk ? allk : (allk & ~cert);
         if (!lr) fb = 0;
-        n_fallback += chk ? 0 : __popc(fb);
-        n_checked += chk ? __popc(fb) : 0;
+        if (fb) {  // rare: the re-decision compares against (and monitors) the fast values
+#pragma unroll
+          for (int d = 0; d < NMAX; ++d) {
+            fastp[(lane * NMAX + d) * 2] = fp0[d];
+            fastp[(lane * NMAX + d) * 2 + 1] = fc1[d];
+          }
+        }
         unsigned pend = __ballot_sync(0xffffffffu, fb != 0);
         float lpx = 0.f;
+        if (pend) {
+          const unsigned nk = __reduce_add_sync(0xffffffffu, (unsigned)__popc(fb));
+          if (lane == 0 && L.counters) atomicAdd(L.counters + (chk ? 1 : 0), (unsigned long long)nk);
+        }
         while (pend) {
           const int Lr = __ffs(pend) - 1;
           pend &= pend - 1;
@@ -686,14 +748,12 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
 #pragma unroll
         for (int i = 0; i < (NMAX + 3) / 4; ++i) apk[i] = 0;
 #pragma unroll
-        for (int d = 0; d < NMAX; ++d) {
-          if (d < n) {
-            const int a = (int)((acts >> (2 * d)) & 3u);
-            int v = cfg.get(d) + a - 1;
-            v = v < 0 ? 0 : (v > scard[d] - 1 ? scard[d] - 1 : v);
-            cfg.set(d, v);
-            apk[d >> 2] |= (uint32_t)(uint8_t)(int8_t)(a - 1) << (8 * (d & 3));
-          }
+        for (int d = 0; d < NMAX; ++d) {  // branch-free: knobs >= n have card 1, index 0, and stay 0
+          const int a = (int)((acts >> (2 * d)) & 3u);
+          int v = cfg.get(d) + a - 1;
+          v = v < 0 ? 0 : (v > scard[d] - 1 ? scard[d] - 1 : v);
+          cfg.set(d, v);
+          apk[d >> 2] |= (uint32_t)(uint8_t)(int8_t)(a - 1) << (8 * (d & 3));
         }
         if (tk.gnode) {  // the new configuration (row t+1) for the next step's fused walk
 #pragma unroll
@@ -726,15 +786,6 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
     if (tk.gnode && lr && L.t_end == T)  // row T
       tk.score[e * (int64_t)(T + 1) + T] =
           kt::dadd(tk.gbase, kt::dmul(tk.glr, gbt_walk(0.0, s_node, s_leaf, mycol, 0, tk.ntrees, tk.depth)));
-  }
-  // counters
-  for (int o = 16; o > 0; o >>= 1) {
-    n_fallback += __shfl_down_sync(0xffffffffu, n_fallback, o);
-    n_checked += __shfl_down_sync(0xffffffffu, n_checked, o);
-  }
-  if (lane == 0 && L.counters) {
-    if (n_fallback) atomicAdd(L.counters + 0, n_fallback);
-    if (n_checked) atomicAdd(L.counters + 1, n_checked);
   }
   kt::tc::fence_before();
   __syncthreads();

@@ -1,4 +1,4 @@
-"""Debug: per-phase clock64 trace of the tcgen05 rollout (CTA 0, each slot's leader, steps 200-201)."""
+"""Debug (library built with -DKT_TC_TRACE=1, e.g. KTUNE_LIB_PATH=build_ab/lib_trace.so): per-phase clock64 trace of the tcgen05 rollout (CTA 0, each slot's leader, steps 200-201)."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -9,14 +9,14 @@ from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
 from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
 from workloads.tasks import encode
 from paper_2001_08743_b200.distributed import create_context
-class A: tasks = 12; episodes = 4096; seed = 0
+class A: tasks = int(os.environ.get("TASKS", "12")); episodes = int(os.environ.get("E", "4096")); seed = 0
 ctx = create_context(0, 0, 1)
 specs = bench.build_tasks(A(), 0)
 models = [fit_gbt(encode(s.space, s.train_idx), s.train_y, seed=s.seed) for s in specs]
 spaces = [Space(s.space, ctx) for s in specs]
 gbts = [DeviceGbt(m, d) for m, d in zip(models, spaces)]
 agents = [ActorCritic(s.space.num_knobs, 128, 64, seed=s.seed, ctx=ctx) for s in specs]
-E, T = 4096, 300
+E, T = A.episodes, 300
 inits = [torch.from_numpy(s.init_idx.astype(np.uint16)).cuda() for s in specs]
 tasks = [RolloutTask(d, a, None, i, 0, s.seed) for s, d, a, g, i in zip(specs, spaces, agents, gbts, inits)]
 run_episodes_batch(tasks, T, ctx)
