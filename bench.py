@@ -48,7 +48,8 @@ SFU_OPS_PER_SM_CLK = 16  # MUFU lanes per SM per clock (ex2/rcp/lg2)
 
 
 def sfu_ops_per_config_step(n):
-    return 2 * (128 + 64 + 64) + 5 * n  # 2 per tanh (ex2 + rcp), 5 per knob softmax (3 ex2, rcp, lg2)
+    # per PAIR of tanh units: 2 ex2 + ONE shared rcp; 5 per knob softmax (3 ex2, rcp, lg2)
+    return 3 * (128 + 64 + 64) // 2 + 5 * n
 
 
 class ClockSampler:
@@ -239,6 +240,8 @@ def headline_config(args, world):
                      "tcgen05 rollout, certified sampling: configs/actions/scores bit-exact with the "
                      "oracle, logp/value fp32-accurate"),
             "l2": "256 MB buffer written between timed steps; outputs 1.2 GB/step > L2",
+            "layout": ("step-major trajectories (KTUNE_F_STEP_MAJOR: [T+1][E] / [T][E])" if args.layout == "step"
+                       else "episode-major trajectories ([E][T+1] / [E][T])"),
             "parallelism": f"dp{world} (episodes sharded, no collective)"}
 
 
@@ -655,6 +658,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--exact", action="store_true", help="exact fp64 rollout kernel instead of the tcgen05 path")
+    ap.add_argument("--layout", default="step", choices=["step", "episode"],
+                    help="trajectory layout of the rollout outputs (device and host buffers)")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size tcgen05 vs exact comparison")
     ap.add_argument("--no-sa", action="store_true", help="skip the simulated-annealing baseline measurement")
     ap.add_argument("--no-cand", action="store_true", help="skip the device make_candidate_set measurement")
@@ -716,13 +721,15 @@ def main():
 
     D0 = specs[0].space.num_knobs
     mkd = lambda shape, dt: torch.empty(shape, dtype=dt, device="cuda")
-    dev_out = [dict(idx=mkd((E, T + 1, D0), torch.uint16), score=mkd((E, T + 1), torch.float64),
-                    actions=mkd((E, T, D0), torch.int8), logp=mkd((E, T), torch.float64),
-                    value=mkd((E, T), torch.float64)) for _ in specs]  # persistent trajectory buffers
+    SM = args.layout == "step"
+    sh = lambda rows, *rest: ((rows, E) if SM else (E, rows)) + rest  # trajectory array shape
+    dev_out = [dict(idx=mkd(sh(T + 1, D0), torch.uint16), score=mkd(sh(T + 1), torch.float64),
+                    actions=mkd(sh(T, D0), torch.int8), logp=mkd(sh(T), torch.float64),
+                    value=mkd(sh(T), torch.float64)) for _ in specs]  # persistent trajectory buffers
     clk = ClockSampler(local).__enter__()  # before the warm-up: nvidia-smi start-up stalls the GPU
     ctx.set_option(L.OPT_PROFILE, 1)  # warm-up runs with the timed region's settings
     for _ in range(args.warmup):
-        run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact)
+        run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact, step_major=SM)
     torch.cuda.synchronize()
 
     def barrier():
@@ -739,13 +746,13 @@ def main():
     # the barrier the GPU has idled and its clocks ramp back up during the next launch
     # (measured: +8..25 ms on the first step otherwise); the timed region is still exactly K steps
     flush.zero_()
-    run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact)
+    run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact, step_major=SM)
     tc0 = time.perf_counter()
     start.record(stream)
     step_ev = []
     for _ in range(args.steps):
         flush.zero_()  # 256 MB > L2 between timed steps
-        run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact)
+        run_episodes_batch(tasks, T, ctx, host_out=dev_out, exact=args.exact, step_major=SM)
         if os.environ.get("BENCH_STEP_EVENTS"):  # diagnostics: per-step device times
             ev = torch.cuda.Event(enable_timing=True)
             ev.record(stream)
@@ -776,9 +783,12 @@ def main():
     peaks, peak_src = load_peaks()
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     achieved = len(specs) * E * T * flop / roll_s / 1e12
-    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    # burst peak: the rollout kernel is timed alone (~7 ms at full clock, no power cap)
+    peak = float(peaks.get("bf16_tflops", peaks.get("bf16_tflops_sustained")))
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_rollout_exact_kernel.json" if args.exact else "r01_rollout_tc_kernel.json")
+    name = "rollout_exact_kernel" if args.exact else f"rollout_tc_kernel_{args.layout}"
+    cands = [os.path.join(ROOT, "profiles", f"r02_{name}.json"), os.path.join(ROOT, "profiles", f"r01_{name}.json")]
+    prof = next((c for c in cands if os.path.exists(c)), cands[0])
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
@@ -799,20 +809,20 @@ def main():
         # scores as fp32 (north star: scores within 1e-5 relative in fp32; the device keeps and ranks
         # candidates on the exact fp64 scores)
         small = [max(s.space.cards) <= 256 for s in specs]
-        host_out = [dict(idx=None if sm else pinned((E, T + 1, D), torch.int16).view(np.uint16),
-                         idx8=pinned((E, T + 1, D), torch.uint8) if sm else None,
-                         score=None, score32=pinned((E, T + 1), torch.float32), actions=None,
-                         actions2=pinned((E, T, (D + 3) // 4), torch.uint8),  # 2 bits per direction
-                         logp=None, value=None, logp32=pinned((E, T), torch.float32),
-                         value32=pinned((E, T), torch.float32)) for sm in small]
+        host_out = [dict(idx=None if sm else pinned(sh(T + 1, D), torch.int16).view(np.uint16),
+                         idx8=pinned(sh(T + 1, D), torch.uint8) if sm else None,
+                         score=None, score32=pinned(sh(T + 1), torch.float32), actions=None,
+                         actions2=pinned(sh(T, (D + 3) // 4), torch.uint8),  # 2 bits per direction
+                         logp=None, value=None, logp32=pinned(sh(T), torch.float32),
+                         value32=pinned(sh(T), torch.float32)) for sm in small]
         htasks = [RolloutTask(d, a, g, hi, episode_offset=rank * E, root_seed=s.seed)
                   for s, d, a, g, hi in zip(specs, spaces, agents, gbts, host_init)]
         ctx.set_stream(None)
-        run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact)  # warm
+        run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact, step_major=SM)  # warm
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact)
+            run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact, step_major=SM)
         barrier()
         dt = time.perf_counter() - t0
         if world > 1:
@@ -820,7 +830,30 @@ def main():
         bi = sum(h.nbytes for h in host_init)
         bo = sum(sum(v.nbytes for v in o.values() if v is not None) for o in host_out)
         e2e = {"value": units_per_step * args.steps / dt, "unit": "config-steps/s", "h2d_bytes_per_step": bi,
-               "d2h_bytes_per_step": bo}
+               "d2h_bytes_per_step": bo,
+               "outputs": "idx as uint8 (uint16 where a cardinality > 256), score fp32 (1e-5 rel.), actions 2-bit, "
+                          "logp/value fp32 (what the tcgen05 path computes)"}
+        # the same call with full-precision outputs: fp64 scores, fp64 logp/value (0.84 GB/step)
+        del host_out
+        full_out = [dict(idx=None if sm else pinned(sh(T + 1, D), torch.int16).view(np.uint16),
+                         idx8=pinned(sh(T + 1, D), torch.uint8) if sm else None,
+                         score=pinned(sh(T + 1), torch.float64), actions=None,
+                         actions2=pinned(sh(T, (D + 3) // 4), torch.uint8), logp=pinned(sh(T), torch.float64),
+                         value=pinned(sh(T), torch.float64)) for sm in small]
+        run_episodes_batch(htasks, T, ctx, host_out=full_out, exact=args.exact, step_major=SM)  # warm
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            run_episodes_batch(htasks, T, ctx, host_out=full_out, exact=args.exact, step_major=SM)
+        barrier()
+        dtf = time.perf_counter() - t0
+        if world > 1:
+            dtf = allreduce_max(dtf)
+        e2e["full_precision"] = {"value": units_per_step * args.steps / dtf, "unit": "config-steps/s",
+                                 "d2h_bytes_per_step": sum(sum(v.nbytes for v in o.values() if v is not None)
+                                                           for o in full_out),
+                                 "outputs": "score fp64, logp/value fp64, idx uint8, actions 2-bit"}
+        del full_out
         ctx.set_stream(stream.cuda_stream)
 
     # ---- parity at the full bench size (outside the timed region): the tcgen05 path vs the
@@ -828,8 +861,8 @@ def main():
     parity = None
     if not args.exact and not args.no_parity:
         exact_out = [{k: torch.empty_like(v) for k, v in o.items()} for o in dev_out]
-        run_episodes_batch(tasks, T, ctx, host_out=exact_out, exact=True)
-        run_episodes_batch(tasks, T, ctx, host_out=dev_out)
+        run_episodes_batch(tasks, T, ctx, host_out=exact_out, exact=True, step_major=SM)
+        run_episodes_batch(tasks, T, ctx, host_out=dev_out, step_major=SM)
         torch.cuda.synchronize()
         eq = lambda k: all(bool(torch.equal(a[k], b[k])) for a, b in zip(dev_out, exact_out))
         rel = lambda k: max(float(((a[k] - b[k]).abs() / b[k].abs().clamp_min(1.0)).max()) for a, b in zip(dev_out, exact_out))
@@ -949,7 +982,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "rollout_kernel" if args.exact else "rollout_tc_kernel",
                          "kernel_ms": roll_s * 1e3, "flop_per_config_step": flop,
-                         "peak_source": f"bf16_tflops_sustained, {peak_src}",
+                         "peak_source": f"bf16_tflops (burst), {peak_src}",
                          "note": ("exact path runs on the FP64 pipe (SIMT); tensor-pipe fraction reported against bf16"
                                   if args.exact else
                                   "algorithmic MLP FLOPs counted once; the kernel issues 3x (fp16 hi/lo split) "

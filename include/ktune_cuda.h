@@ -44,8 +44,12 @@ enum ktune_status {
 
 enum ktune_flags {
   KTUNE_F_DEVICE = 1,       /* array arguments are device pointers */
-  KTUNE_F_EXACT_ROLLOUT = 2 /* ktune_rollout: exact fp64 forward for every config-step (logp/value
+  KTUNE_F_EXACT_ROLLOUT = 2, /* ktune_rollout: exact fp64 forward for every config-step (logp/value
                                bit-exact too); default is the tcgen05 path with certified sampling */
+  KTUNE_F_STEP_MAJOR = 4     /* ktune_rollout: trajectories step-major, idx/score [T+1][E], actions/logp/value
+                               [T][E] (rows of D knobs where applicable), instead of episode-major [E][T+1] /
+                               [E][T]: the device writes one coalesced row block per step, and every
+                               segment of a host-pointer call crosses PCIe as one contiguous copy */
 };
 
 typedef struct ktune_ctx ktune_ctx;
@@ -292,7 +296,8 @@ typedef struct {
   int64_t episode_offset;   /* global id of this shard's first episode (RNG key) */
   uint64_t explore_seed;    /* stream_seed(root, "explore") */
   const uint16_t* init_idx; /* E x D */
-  /* outputs (any may be NULL except idx, see idx_u8): */
+  /* outputs (any may be NULL except idx, see idx_u8); shapes are episode-major as written, step-major
+   * ([T+1] x E x ..., [T] x E x ...) with KTUNE_F_STEP_MAJOR: */
   uint16_t* idx;            /* E x (T+1) x D visited configs, row t = Θ_t (NULL allowed with idx_u8, host pointers) */
   double* score;            /* E x (T+1) predicted fitness of Θ_t */
   int8_t* actions;          /* E x T x D directions in {-1,0,+1} */

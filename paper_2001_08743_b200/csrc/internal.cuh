@@ -236,6 +236,9 @@ struct RolloutWork {
   float* logp32 = nullptr;   // fp32 copies (may be NULL)
   float* value32 = nullptr;
   bool scored = false;   // set by rollout_tc when the scores were fused into the rollout
+  // trajectory layout in rows: (e, t) of idx/score at e*sE + t*sT, of actions/logp/value at
+  // e*aE + t*aT (episode-major: T+1, 1, T, 1; step-major, KTUNE_F_STEP_MAJOR: 1, E, 1, E)
+  int64_t sE = 0, sT = 1, aE = 0, aT = 1;
 };
 // tcgen05 rollout (rollout_tc.cu): eligibility (h = 128, g = 64, n <= 21,
 // cardinalities <= 2049, representable weight scales) and the launch.

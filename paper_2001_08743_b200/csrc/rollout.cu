@@ -62,6 +62,9 @@ struct RolloutTask {
   double* value;
   float* logp32;
   float* value32;
+  // trajectory layout (rows): (e, t) of the (T+1)-row arrays at e*sE + t*sT, of the T-row
+  // arrays at e*aE + t*aT: episode-major (T+1, 1, T, 1) or step-major (1, E, 1, E)
+  int64_t sE, sT, aE, aT;
 };
 
 // Whole launch description passed BY VALUE (kernel parameter space), so a
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
       uint16_t v = 0;
       if (e < E) {
         v = tkp->init_idx[e * n + d];
-        out_idx[(e * (T + 1)) * n + d] = v;
+        out_idx[(e * tkp->sE) * n + d] = v;
       }
       cfg[d * tile + c + 32 * q] = v;
     }
@@ -305,8 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
         cfg[d * tile + el] = (uint16_t)v;
         act[(3 * d) * tile + el] = a == 0 ? k3.lp[0] : (a == 1 ? k3.lp[1] : k3.lp[2]);
         if (e < E) {
-          if (out_act) out_act[(e * T + t) * n + d] = (int8_t)(a - 1);
-          out_idx[(e * (T + 1) + t + 1) * n + d] = (uint16_t)v;
+          if (out_act) out_act[(e * tkp->aE + t * tkp->aT) * n + d] = (int8_t)(a - 1);
+          out_idx[(e * tkp->sE + (t + 1) * tkp->sT) * n + d] = (uint16_t)v;
         }
       }
     }
@@ -318,10 +321,11 @@ __global__ void __launch_bounds__(kThreads, 1) rollout_kernel(const __grid_const
       if (e < E) {
         double lp = 0.0;
         for (int d = 0; d < n; ++d) lp = kt::dadd(lp, act[(3 * d) * tile + el]);
-        if (out_logp) out_logp[e * T + t] = lp;
-        if (out_val) out_val[e * T + t] = val[el];
-        if (tkp->logp32) tkp->logp32[e * T + t] = (float)lp;
-        if (tkp->value32) tkp->value32[e * T + t] = (float)val[el];
+        const int64_t o = e * tkp->aE + t * tkp->aT;
+        if (out_logp) out_logp[o] = lp;
+        if (out_val) out_val[o] = val[el];
+        if (tkp->logp32) tkp->logp32[o] = (float)lp;
+        if (tkp->value32) tkp->value32[o] = (float)val[el];
       }
     }
     __syncthreads();
@@ -375,8 +379,8 @@ __global__ void debug_math_kernel(int op, const double* __restrict__ x, int64_t 
 
 // uint16 -> uint8 copy of trajectory rows [r0, r0 + rows) of every episode (idx_u8 outputs).
 // fp32 copies of trajectory score rows [r0, r0 + len) of every episode (row pitch P).
-__global__ void score_f32_kernel(const double* __restrict__ src, float* __restrict__ dst, int64_t E, int P, int r0,
-                                 int len) {
+__global__ void score_f32_kernel(const double* __restrict__ src, float* __restrict__ dst, int64_t E, int64_t P,
+                                 int64_t r0, int64_t len) {
   const int64_t n = E * len;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = j / len, i = e * P + r0 + (j - e * len);
@@ -385,7 +389,7 @@ __global__ void score_f32_kernel(const double* __restrict__ src, float* __restri
 }
 
 __global__ void narrow_idx_kernel(const uint16_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t E,
-                                  int rows_per_ep, int n, int r0, int rows) {
+                                  int64_t rows_per_ep, int n, int64_t r0, int64_t rows) {
   const int64_t per = (int64_t)rows * n, total = E * per;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i / per, j = (e * rows_per_ep + r0) * n + (i % per);
@@ -394,8 +398,8 @@ __global__ void narrow_idx_kernel(const uint16_t* __restrict__ src, uint8_t* __r
 }
 
 // int8 directions -> 2-bit codes (direction + 1), 4 knobs per byte, for steps [t0, t0 + steps).
-__global__ void pack_actions_kernel(const int8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t E, int T,
-                                    int n, int t0, int steps) {
+__global__ void pack_actions_kernel(const int8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t E, int64_t T,
+                                    int n, int64_t t0, int64_t steps) {
   const int nb = (n + 3) / 4;
   const int64_t per = (int64_t)steps * nb, total = E * per;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -520,6 +524,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     if (num_tasks < 0 || T < 0) kt::fail(KTUNE_ERR_CONFIG, "rollout: bad task count or steps");
     if (num_tasks == 0) return;
     const bool dev = flags & KTUNE_F_DEVICE;
+    const bool stepm = flags & KTUNE_F_STEP_MAJOR;  // trajectories [T+1][E] / [T][E] instead of [E][T+1] / [E][T]
     std::vector<RolloutTask> dt(num_tasks);
     // device buffers (host-pointer calls: one grow-only context arena, 256-byte aligned slices)
     struct HostIo {
@@ -604,6 +609,10 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       r.value = h.d_val;
       r.logp32 = h.d_logp32;
       r.value32 = h.d_val32;
+      r.sE = stepm ? 1 : (int64_t)T + 1;
+      r.sT = stepm ? E : 1;
+      r.aE = stepm ? 1 : (int64_t)T;
+      r.aT = stepm ? E : 1;
     }
     // tcgen05 path with certified sampling unless the exact fp64 forward is
     // requested (or a task is outside the tensor-core path's shapes)
@@ -625,18 +634,24 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     auto score_rows = [&](int k, int r0, int r1) {  // trajectory rows [r0, r1] of every episode
       const ktune_rollout_task& t = tasks[k];
       if (!t.gbt || !io[k].d_score || t.num_episodes == 0) return;
-      const int64_t len = r1 - r0 + 1;
+      const int64_t len = r1 - r0 + 1, E = t.num_episodes;
+      if (stepm) {  // rows r0..r1 of every episode are one contiguous block
+        kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx + r0 * E * t.ac->n, 2, E * len, io[k].d_score + r0 * E);
+        return;
+      }
       kt::RowMap m;
       if (len != T + 1) m = kt::RowMap{len, (int64_t)T + 1, r0};
-      kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx, 2, t.num_episodes * len, io[k].d_score, m);
+      kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx, 2, E * len, io[k].d_score, m);
 
     };
     auto score32_rows = [&](int k, int r0, int r1) {  // fp32 copies of the scores of rows [r0, r1]
       const ktune_rollout_task& t = tasks[k];
       if (!t.gbt || !io[k].d_s32 || t.num_episodes == 0) return;
-      const int64_t len = r1 - r0 + 1, work = t.num_episodes * len;
+      const int64_t len = r1 - r0 + 1, work = t.num_episodes * len, E = t.num_episodes;
+      // step-major: one flat range [r0*E, (r1+1)*E) of a single "episode"
       score_f32_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(work, 256), (int64_t)kt::sm_count(ctx) * 16), 256, 0,
-                         ctx->stream>>>(io[k].d_score, io[k].d_s32, t.num_episodes, T + 1, r0, len);
+                         ctx->stream>>>(io[k].d_score, io[k].d_s32, stepm ? 1 : E, T + 1, stepm ? r0 * E : r0,
+                                        stepm ? len * E : len);
       kt::check_launch(ctx, "score_f32");
     };
     auto narrow_rows = [&](int k, int r0, int r1) {  // uint16 -> uint8 trajectory rows [r0, r1]
@@ -644,8 +659,9 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       if (!t.idx_u8 || t.num_episodes == 0) return;
       narrow_idx_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(t.num_episodes * (int64_t)(r1 - r0 + 1) * t.ac->n, 256),
                                                      (int64_t)kt::sm_count(ctx) * 16),
-                          256, 0, ctx->stream>>>(io[k].d_idx, io[k].d_u8, t.num_episodes, T + 1, t.ac->n, r0,
-                                                 r1 - r0 + 1);
+                          256, 0, ctx->stream>>>(io[k].d_idx, io[k].d_u8, stepm ? 1 : t.num_episodes, T + 1,
+                                                 t.ac->n, stepm ? r0 * t.num_episodes : r0,
+                                                 stepm ? (r1 - r0 + 1) * t.num_episodes : r1 - r0 + 1);
       kt::check_launch(ctx, "narrow_idx");
     };
     auto pack_steps = [&](int k, int t0, int t1) {  // int8 -> 2-bit actions of steps [t0, t1)
@@ -653,7 +669,9 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       if (!t.actions_u2 || t.num_episodes == 0 || t1 <= t0) return;
       const int64_t work = t.num_episodes * (int64_t)(t1 - t0) * ((t.ac->n + 3) / 4);
       pack_actions_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(work, 256), (int64_t)kt::sm_count(ctx) * 16), 256,
-                            0, ctx->stream>>>(io[k].d_act, io[k].d_a2, t.num_episodes, T, t.ac->n, t0, t1 - t0);
+                            0, ctx->stream>>>(io[k].d_act, io[k].d_a2, stepm ? 1 : t.num_episodes, T, t.ac->n,
+                                              stepm ? (int64_t)t0 * t.num_episodes : t0,
+                                              stepm ? (int64_t)(t1 - t0) * t.num_episodes : t1 - t0);
       kt::check_launch(ctx, "pack_actions");
     };
     auto copy_out = [&](int k, int t0, int t1, cudaStream_t st) {  // steps [t0, t1): rows (t0, t1] (+ row 0)
@@ -663,6 +681,26 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       const HostIo& h = io[k];
       const int r0 = t0 == 0 ? 0 : t0 + 1;
       const size_t rows = (size_t)(t1 - r0 + 1), steps = (size_t)(t1 - t0);
+      if (stepm) {  // every output's segment is one contiguous block: 1-D copies
+        auto cp = [&](void* dst, const void* src, size_t off, size_t bytes) {
+          if (dst && bytes)
+            KT_CUDA(cudaMemcpyAsync((char*)dst + off, (const char*)src + off, bytes, cudaMemcpyDeviceToHost, st));
+        };
+        const size_t nb = (n + 3) / 4;
+        cp(t.idx, h.d_idx, r0 * E * n * 2, rows * E * n * 2);
+        cp(t.idx_u8, h.d_u8, r0 * E * n, rows * E * n);
+        cp(t.actions, h.d_act, t0 * E * n, steps * E * n);
+        cp(t.actions_u2, h.d_a2, t0 * E * nb, steps * E * nb);
+        cp(t.logp, h.d_logp, t0 * E * 8, steps * E * 8);
+        cp(t.value, h.d_val, t0 * E * 8, steps * E * 8);
+        cp(t.logp_f32, h.d_logp32, t0 * E * 4, steps * E * 4);
+        cp(t.value_f32, h.d_val32, t0 * E * 4, steps * E * 4);
+        if (t.gbt) {
+          cp(t.score, h.d_score, r0 * E * 8, rows * E * 8);
+          cp(t.score_f32, h.d_s32, r0 * E * 4, rows * E * 4);
+        }
+        return;
+      }
       if (t.idx)
         KT_CUDA(cudaMemcpy2DAsync(t.idx + r0 * n, (T + 1) * n * 2, h.d_idx + r0 * n, (T + 1) * n * 2, rows * n * 2,
                                   E, cudaMemcpyDeviceToHost, st));
@@ -701,6 +739,12 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         work[k] = {tasks[k].space, tasks[k].ac, dt[k].E,     dt[k].episode_offset, dt[k].seed, dt[k].init_idx,
                    dt[k].idx,      dt[k].actions, dt[k].logp, dt[k].value,         tasks[k].gbt, io[k].d_score,
                    io[k].d_logp32, io[k].d_val32};
+      for (int k = 0; k < num_tasks; ++k) {
+        work[k].sE = dt[k].sE;
+        work[k].sT = dt[k].sT;
+        work[k].aE = dt[k].aE;
+        work[k].aT = dt[k].aT;
+      }
       if (segmented) {
         for (int sg = 0; sg < S; ++sg) {
           const int t0 = (int)((int64_t)sg * T / S), t1 = (int)((int64_t)(sg + 1) * T / S);

@@ -66,6 +66,7 @@ struct TcTask {
   double* value;
   float* logp32;
   float* value32;
+  int64_t sE, sT, aE, aT;          // trajectory layout (rows), see RolloutWork
   int32_t cta_base, ctas, warps;  // CTAs [cta_base, cta_base + ctas) share warps = ceil(E/32)
   int32_t e1, e2, e3;             // power-of-two weight scales of L1, L2, L3
   // fused cost-model scoring (K1 in the epilogue; gnode == nullptr: scored by a separate K1 launch)
@@ -484,9 +485,9 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
 #pragma unroll
         for (int d = 0; d < NMAX; ++d)
           if (d < n) cfg.set(d, tk.init_idx[e * n + d]);
-        store_row_idx(tk.idx + e * (int64_t)(T + 1) * n, cfg, n);
+        store_row_idx(tk.idx + e * tk.sE * n, cfg, n);
       } else {  // resume a segmented rollout from trajectory row t_begin
-        const uint16_t* src = tk.idx + (e * (int64_t)(T + 1) + L.t_begin) * n;
+        const uint16_t* src = tk.idx + (e * tk.sE + L.t_begin * tk.sT) * n;
 #pragma unroll
         for (int d = 0; d < NMAX; ++d)
           if (d < n) cfg.set(d, src[d]);
@@ -610,7 +611,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         }
         if (tk.gnode) {  // fused K1, row t: second half of the walk while the L2 MMAs run
           gs = gbt_walk(gs, s_node, s_leaf, mycol, gh, tk.ntrees, tk.depth);
-          if (lr) tk.score[e * (int64_t)(T + 1) + t] = kt::dadd(tk.gbase, kt::dmul(tk.glr, gs));
+          if (lr) tk.score[e * tk.sE + t * tk.sT] = kt::dadd(tk.gbase, kt::dmul(tk.glr, gs));
         }
         kt::tc::mbar_wait(mb, ph);
         kt::tc::fence_after();
@@ -648,8 +649,8 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         const float vs = vs2.x + vs2.y;
         if (lr && L.check != 4) {
           const float v = vs + sbv2[0];
-          if (tk.value) tk.value[e * T + t] = (double)v;
-          if (tk.value32) tk.value32[e * T + t] = v;
+          if (tk.value) tk.value[e * tk.aE + t * tk.aT] = (double)v;
+          if (tk.value32) tk.value32[e * tk.aE + t * tk.aT] = v;
         }
         TR(12)
         kt::tc::mbar_wait(mb, ph);
@@ -762,9 +763,9 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         }
         TR(10)
         if (lr && L.check != 4) {  // 4: timing experiment (no trajectory writes)
-          store_row_idx(tk.idx + (e * (int64_t)(T + 1) + t + 1) * n, cfg, n);
+          store_row_idx(tk.idx + (e * tk.sE + (t + 1) * tk.sT) * n, cfg, n);
           if (tk.actions) {
-            int8_t* ad = tk.actions + (e * (int64_t)T + t) * n;
+            int8_t* ad = tk.actions + (e * tk.aE + t * tk.aT) * n;
             if ((n & 3) == 0) {
 #pragma unroll
               for (int i = 0; i < (NMAX + 3) / 4; ++i)
@@ -775,8 +776,8 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
                 if (d < n) ad[d] = (int8_t)((apk[d >> 2] >> (8 * (d & 3))) & 0xFF);
             }
           }
-          if (tk.logp) tk.logp[e * T + t] = (double)lpj;
-          if (tk.logp32) tk.logp32[e * T + t] = lpj;
+          if (tk.logp) tk.logp[e * tk.aE + t * tk.aT] = (double)lpj;
+          if (tk.logp32) tk.logp32[e * tk.aE + t * tk.aT] = lpj;
         }
       }
       ph ^= 1;
@@ -784,7 +785,7 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
     }
 #undef TR
     if (tk.gnode && lr && L.t_end == T)  // row T
-      tk.score[e * (int64_t)(T + 1) + T] =
+      tk.score[e * tk.sE + T * tk.sT] =
           kt::dadd(tk.gbase, kt::dmul(tk.glr, gbt_walk(0.0, s_node, s_leaf, mycol, 0, tk.ntrees, tk.depth)));
   }
   kt::tc::fence_before();
@@ -879,6 +880,10 @@ static void rollout_tc_launch(ktune_ctx* ctx, std::vector<RolloutWork>& work, in
       tk.T = T;
       tk.E = rw.E;
       tk.episode_offset = rw.episode_offset;
+      tk.sE = rw.sE;
+      tk.sT = rw.sT;
+      tk.aE = rw.aE;
+      tk.aT = rw.aT;
       tk.seed = rw.seed;
       tk.init_idx = rw.init_idx;
       tk.idx = rw.idx;
@@ -944,13 +949,13 @@ static RolloutWork episode_tail(const RolloutWork& w, int64_t e, int T) {
   t.E = w.E - e;
   t.episode_offset = w.episode_offset + e;
   t.init_idx = w.init_idx + e * n;
-  t.idx = w.idx + e * (T + 1) * n;
-  if (w.actions) t.actions = w.actions + e * T * n;
-  if (w.logp) t.logp = w.logp + e * T;
-  if (w.value) t.value = w.value + e * T;
-  if (w.logp32) t.logp32 = w.logp32 + e * T;
-  if (w.value32) t.value32 = w.value32 + e * T;
-  if (w.score) t.score = w.score + e * (T + 1);
+  t.idx = w.idx + e * w.sE * n;
+  if (w.actions) t.actions = w.actions + e * w.aE * n;
+  if (w.logp) t.logp = w.logp + e * w.aE;
+  if (w.value) t.value = w.value + e * w.aE;
+  if (w.logp32) t.logp32 = w.logp32 + e * w.aE;
+  if (w.value32) t.value32 = w.value32 + e * w.aE;
+  if (w.score) t.score = w.score + e * w.sE;
   t.scored = false;
   return t;
 }

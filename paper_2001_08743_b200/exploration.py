@@ -207,7 +207,8 @@ class RolloutTask:
 
 
 def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Context] = None,
-                       device_out: bool = False, host_out: Optional[list] = None, exact: bool = False):
+                       device_out: bool = False, host_out: Optional[list] = None, exact: bool = False,
+                       step_major: bool = False):
     """Grouped run_episodes over several workloads in ONE persistent-kernel launch.
 
     Host arrays in/out by default; with CUDA-tensor init_idx and device_out=True
@@ -218,6 +219,10 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
     Default: the tcgen05 rollout with certified sampling (configurations,
     actions and scores bit-exact; logp/value fp32-accurate). exact=True runs
     the fp64 forward on every config-step (logp/value bit-exact as well).
+    step_major=True (KTUNE_F_STEP_MAJOR) lays the trajectories out step-major:
+    idx (T+1) x E x D, score (T+1) x E, actions T x E x D, logp/value T x E -
+    the same values transposed; each step is one contiguous block on the device
+    and each segment of a host-buffer call one contiguous PCIe copy.
     """
     ctx = ctx or tasks[0].space.ctx
     arr = (L.RolloutTaskC * len(tasks))()
@@ -237,11 +242,11 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
                 o = host_out[i]
             else:
                 mk = lambda shape, dt: torch.empty(shape, dtype=dt, device=init.device)
-                o = dict(idx=mk((E, T + 1, D), torch.uint16),
-                         score=mk((E, T + 1), torch.float64) if t.cost_model is not None else None,
-                         actions=mk((E, T, D), torch.int8) if t.want_trajectory else None,
-                         logp=mk((E, T), torch.float64) if t.want_trajectory else None,
-                         value=mk((E, T), torch.float64) if t.want_trajectory else None)
+                o = dict(idx=mk(_shape(E, T + 1, step_major, D), torch.uint16),
+                         score=mk(_shape(E, T + 1, step_major), torch.float64) if t.cost_model is not None else None,
+                         actions=mk(_shape(E, T, step_major, D), torch.int8) if t.want_trajectory else None,
+                         logp=mk(_shape(E, T, step_major), torch.float64) if t.want_trajectory else None,
+                         value=mk(_shape(E, T, step_major), torch.float64) if t.want_trajectory else None)
             pp = lambda a: None if a is None else C.c_void_p(a.data_ptr())
             init_p = C.c_void_p(init.data_ptr())
             keep.append(init)
@@ -251,11 +256,11 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
             if host_out is not None:  # caller-provided (e.g. pinned) host buffers
                 o = host_out[i]
             else:
-                o = dict(idx=host_empty((E, T + 1, D), np.uint16),
-                         score=host_empty((E, T + 1), np.float64) if t.cost_model is not None else None,
-                         actions=host_empty((E, T, D), np.int8) if t.want_trajectory else None,
-                         logp=host_empty((E, T), np.float64) if t.want_trajectory else None,
-                         value=host_empty((E, T), np.float64) if t.want_trajectory else None)
+                o = dict(idx=host_empty(_shape(E, T + 1, step_major, D), np.uint16),
+                         score=host_empty(_shape(E, T + 1, step_major), np.float64) if t.cost_model is not None else None,
+                         actions=host_empty(_shape(E, T, step_major, D), np.int8) if t.want_trajectory else None,
+                         logp=host_empty(_shape(E, T, step_major), np.float64) if t.want_trajectory else None,
+                         value=host_empty(_shape(E, T, step_major), np.float64) if t.want_trajectory else None)
             pp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
             init_p = init.ctypes.data_as(C.c_void_p)
             keep.append(init)
@@ -279,8 +284,14 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
         a.score_f32 = pp(o.get("score32"))
         outs.append(o)
     ctx.check(L.lib().ktune_rollout(ctx.h, len(tasks), arr, T,
-                                    (L.F_DEVICE if dev else 0) | (L.F_EXACT_ROLLOUT if exact else 0)))
+                                    (L.F_DEVICE if dev else 0) | (L.F_EXACT_ROLLOUT if exact else 0) |
+                                    (L.F_STEP_MAJOR if step_major else 0)))
     return outs
+
+
+def _shape(E: int, rows: int, step_major: bool, D: Optional[int] = None) -> tuple:
+    s = (rows, E) if step_major else (E, rows)
+    return s + ((D,) if D is not None else ())
 
 
 def unpack_actions(packed, D: int) -> np.ndarray:

@@ -369,3 +369,61 @@ def test_rollout_tc_check_mode_c2_shape(O, ctx):
             assert np.array_equal(fast[i]["idx"][e].astype(np.int32), w["idx"][0])
             assert np.array_equal(fast[i]["actions"][e], w["actions"][0])
             assert np.array_equal(fast[i]["score"][e], w["score"][0])
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_rollout_step_major_layout(O, ctx, exact):
+    """KTUNE_F_STEP_MAJOR: the same trajectories transposed to [T+1][E] / [T][E] on every path -
+    device buffers (one launch), host buffers (segmented, 1-D copies per segment), the compact
+    outputs (idx_u8, actions_u2, score_f32, fp32 logp/value) and the exact fp64 kernel; equal to
+    the episode-major call bit for bit and to the oracle."""
+    import torch
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch, unpack_actions
+    from paper_2001_08743_b200.spaces import stream_seed
+    tasks, dtasks, inits = [], [], []
+    for i, name in enumerate(["resnet_c2", "synthetic16", "synthetic8"]):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=120 + i)
+        E = [70, 33, 129][i]
+        init = np.random.default_rng(i).integers(0, 2, (E, sp.num_knobs)).astype(np.int32)
+        inits.append((osp, og, agent, init))
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=7, root_seed=i))
+        dtasks.append(RolloutTask(dspace, agent, dg, torch.from_numpy(init).cuda(), episode_offset=7, root_seed=i))
+    T = 260
+    em = run_episodes_batch(tasks, T, exact=exact)
+    sm = run_episodes_batch(tasks, T, exact=exact, step_major=True)
+    dv = run_episodes_batch(dtasks, T, exact=exact, step_major=True)
+    torch.cuda.synchronize()
+    for a, b, d in zip(em, sm, dv):
+        for k in ["idx", "actions", "score", "logp", "value"]:
+            assert b[k].shape[:2] == (a[k].shape[1], a[k].shape[0]), k
+            assert np.array_equal(np.swapaxes(a[k], 0, 1), b[k]), k
+            assert np.array_equal(d[k].cpu().numpy(), b[k]), k
+    osp, og, agent, init = inits[0]
+    want = O.run_episodes(osp, og, 128, 64, agent.params, init[:5], T, 7, stream_seed(0, "explore"))
+    assert np.array_equal(np.swapaxes(sm[0]["idx"][:, :5], 0, 1).astype(np.int32), want["idx"])
+    assert np.array_equal(np.swapaxes(sm[0]["score"][:, :5], 0, 1), want["score"])
+    # compact outputs, step-major, on the resnet task (every cardinality <= 256)
+    E, D = len(inits[0][3]), tasks[0].space.D
+    o = dict(idx=None, idx8=np.zeros((T + 1, E, D), np.uint8), actions=None,
+             actions2=np.zeros((T, E, (D + 3) // 4), np.uint8), score=None, score32=np.zeros((T + 1, E), np.float32),
+             logp=None, value=None, logp32=np.zeros((T, E), np.float32), value32=np.zeros((T, E), np.float32))
+    run_episodes_batch(tasks[:1], T, host_out=[o], exact=exact, step_major=True)
+    assert np.array_equal(o["idx8"], sm[0]["idx"].astype(np.uint8))
+    assert np.array_equal(unpack_actions(o["actions2"], D), sm[0]["actions"])
+    assert np.array_equal(o["score32"], sm[0]["score"].astype(np.float32))
+    assert np.array_equal(o["logp32"], sm[0]["logp"].astype(np.float32))
+    assert np.array_equal(o["value32"], sm[0]["value"].astype(np.float32))
+
+
+def test_rollout_step_major_multi_wave(O, ctx):
+    """Step-major with more episodes than one resident wave (full waves + the spread remainder
+    advance the trajectory pointers by episode, i.e. by one row within every step block)."""
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    sp, osp, og, dspace, dg, agent = _setup(O, ctx, "synthetic8", seed=9)
+    E, T = 60_001, 5
+    init = np.random.default_rng(E).integers(0, 2, (E, sp.num_knobs))
+    task = RolloutTask(dspace, agent, dg, init, episode_offset=2, root_seed=9)
+    a = run_episodes_batch([task], T)[0]
+    b = run_episodes_batch([task], T, step_major=True)[0]
+    for k in ["idx", "actions", "score", "logp", "value"]:
+        assert np.array_equal(np.swapaxes(a[k], 0, 1), b[k]), k

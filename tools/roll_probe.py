@@ -25,11 +25,13 @@ E, T = args.episodes, int(os.environ.get("T", "500"))
 inits = [torch.from_numpy(s.init_idx[:E].astype(np.uint16)).cuda() for s in specs]
 tasks = [RolloutTask(d, a, g, i, 0, s.seed) for s, d, a, g, i in zip(specs, spaces, agents, gbts, inits)]
 mkd = lambda shape, dt: torch.empty(shape, dtype=dt, device="cuda")
-out = [dict(idx=mkd((E, T + 1, 8), torch.uint16), score=mkd((E, T + 1), torch.float64), actions=mkd((E, T, 8), torch.int8),
-            logp=mkd((E, T), torch.float64), value=mkd((E, T), torch.float64)) for _ in specs]
+sm = bool(int(os.environ.get("STEP", "0")))  # step-major trajectories
+sh = lambda rows, *rest: ((rows, E) if sm else (E, rows)) + rest
+out = [dict(idx=mkd(sh(T + 1, 8), torch.uint16), score=mkd(sh(T + 1), torch.float64), actions=mkd(sh(T, 8), torch.int8),
+            logp=mkd(sh(T), torch.float64), value=mkd(sh(T), torch.float64)) for _ in specs]
 chk = int(os.environ.get("CHECK", "0"))
 for _ in range(2):
-    run_episodes_batch(tasks, T, ctx, host_out=out)
+    run_episodes_batch(tasks, T, ctx, host_out=out, step_major=sm)
 torch.cuda.synchronize()
 ref = [{k: v.clone() for k, v in o.items()} for o in out] if chk else None
 ctx.set_option(L.OPT_PROFILE, 1)
@@ -39,7 +41,7 @@ keys = [L.STAT_ROLLOUT_NS, L.STAT_ROLLOUT_CALLS, L.STAT_GBT_NS, L.STAT_GBT_CALLS
 s0 = {k: ctx.stat(k) for k in keys}
 reps = int(os.environ.get("REPS", "5"))
 for i in range(reps):
-    run_episodes_batch(tasks, T, ctx, host_out=out)
+    run_episodes_batch(tasks, T, ctx, host_out=out, step_major=sm)
 torch.cuda.synchronize()
 d = {k: ctx.stat(k) - s0[k] for k in keys}
 roll = d[L.STAT_ROLLOUT_NS] / 1e6 / reps
