@@ -269,10 +269,12 @@ __device__ __noinline__ Redecided exact_redecide(const TcTask& tk, int t, int L,
                                                  const int* scard, double* sh0, double* shp, double* slg,
                                                  int64_t ge_L, uint64_t acts, const float* fastp, uint32_t fast_cert,
                                                  unsigned long long* stats, int check) {
-  float lp_exact = 0.f;
+  // Latency-bound by construction (a few dependent fp64 chains per lane), so every stage
+  // issues its global weight loads in batches ahead of the chains that consume them, and
+  // the independent chains of a lane are interleaved.
   const int lane = threadIdx.x & 31;
   const int n = tk.n;
-  const double* P = tk.params;
+  const double* __restrict__ P = tk.params;
   const int ob0 = kH * n, owp1 = ob0 + kH, obp1 = owp1 + kG * kH, owp2 = obp1 + kG, obp2 = owp2 + 3 * n * kG;
   double x[NMAX];
 #pragma unroll
@@ -280,65 +282,116 @@ __device__ __noinline__ Redecided exact_redecide(const TcTask& tk, int t, int L,
     const int c = (int)((__shfl_sync(0xffffffffu, cfg.w[d >> 1], L) >> ((d & 1) * 16)) & 0xFFFFu);
     x[d] = d < n ? tk.flut[tk.foff[d] + c] : 0.0;  // = c / (card - 1) (0 if card = 1), host-divided
   }
-  // h0 = tanh(W0 x + b0): W0 column-major (h x n)
+  // h0 = tanh(W0 x + b0): W0 column-major (h x n); units lane + 32m, four chains interleaved
+  {
+    double acc[kH / 32], bias[kH / 32];
 #pragma unroll
-  for (int m = 0; m < kH / 32; ++m) {
-    const int u = lane + 32 * m;
-    double acc = 0.0;
+    for (int m = 0; m < kH / 32; ++m) {
+      acc[m] = 0.0;
+      bias[m] = P[ob0 + lane + 32 * m];
+    }
 #pragma unroll
     for (int i = 0; i < NMAX; ++i)
-      if (i < n) acc = __fma_rn(P[i * kH + u], x[i], acc);
-    sh0[u] = kt::kt_tanh_bf(kt::dadd(acc, P[ob0 + u]));
-  }
-  __syncwarp();
-  // hp = tanh(Wp1 h0 + bp1): Wp1 column-major (g x h)
+      if (i < n) {
+        double w[kH / 32];
 #pragma unroll
-  for (int m = 0; m < kG / 32; ++m) {
-    const int u = lane + 32 * m;
-    double acc = 0.0;
-#pragma unroll 8
-    for (int i = 0; i < kH; ++i) acc = __fma_rn(P[owp1 + i * kG + u], sh0[i], acc);
-    shp[u] = kt::kt_tanh_bf(kt::dadd(acc, P[obp1 + u]));
+        for (int m = 0; m < kH / 32; ++m) w[m] = P[i * kH + lane + 32 * m];
+#pragma unroll
+        for (int m = 0; m < kH / 32; ++m) acc[m] = __fma_rn(w[m], x[i], acc[m]);
+      }
+#pragma unroll
+    for (int m = 0; m < kH / 32; ++m) sh0[lane + 32 * m] = kt::kt_tanh_bf(kt::dadd(acc[m], bias[m]));
   }
   __syncwarp();
-  // logits of the flagged knobs: item it -> (k-th flagged knob, a)
+  // hp = tanh(Wp1 h0 + bp1): Wp1 column-major (g x h); units lane, lane + 32 as two interleaved
+  // 128-long chains, weights loaded 16 rows ahead
+  {
+    constexpr int B = 8;
+    double a0 = 0.0, a1 = 0.0;
+    double w0[B], w1[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      w0[j] = P[owp1 + j * kG + lane];
+      w1[j] = P[owp1 + j * kG + lane + 32];
+    }
+#pragma unroll 1
+    for (int i0 = 0; i0 < kH; i0 += B) {
+      double n0[B], n1[B];
+      const int i1 = i0 + B < kH ? i0 + B : i0;  // next batch (reloads the last one at the end)
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        n0[j] = P[owp1 + (i1 + j) * kG + lane];
+        n1[j] = P[owp1 + (i1 + j) * kG + lane + 32];
+      }
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const double h = sh0[i0 + j];
+        a0 = __fma_rn(w0[j], h, a0);
+        a1 = __fma_rn(w1[j], h, a1);
+      }
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        w0[j] = n0[j];
+        w1[j] = n1[j];
+      }
+    }
+    const double b0v = P[obp1 + lane], b1v = P[obp1 + lane + 32];
+    shp[lane] = kt::kt_tanh_bf(kt::dadd(a0, b0v));
+    shp[lane + 32] = kt::kt_tanh_bf(kt::dadd(a1, b1v));
+  }
+  __syncwarp();
+  // logits of the flagged knobs: item it -> (k-th flagged knob, a); weights loaded up front
   const int nf = __popc(fm);
   for (int it = lane; it < 3 * nf; it += 32) {
     uint32_t mm = fm;
     for (int q = 0; q < it / 3; ++q) mm &= mm - 1;
     const int a = 3 * (__ffs(mm) - 1) + it % 3;
     double acc = 0.0;
-#pragma unroll 8
-    for (int j = 0; j < kG; ++j) acc = __fma_rn(P[owp2 + j * 3 * n + a], shp[j], acc);
+#pragma unroll
+    for (int j0 = 0; j0 < kG; j0 += 16) {
+      double w[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) w[j] = P[owp2 + (j0 + j) * 3 * n + a];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc = __fma_rn(w[j], shp[j0 + j], acc);
+    }
     slg[it] = kt::dadd(acc, P[obp2 + a]);
   }
   __syncwarp();
-  if (lane == L) {
-    int it = 0;
+  // the flagged knobs' exact softmax, draw and decision, one knob per lane, folded into lane L
+  const uint64_t acts_L = __shfl_sync(0xffffffffu, acts, L);
+  const uint32_t cert_L = __shfl_sync(0xffffffffu, fast_cert, L);
+  int ae = 0, dk = 0;
+  float lpk = 0.f;
+  if (lane < nf) {
+    uint32_t mm = fm;
+    for (int q = 0; q < lane; ++q) mm &= mm - 1;
+    dk = __ffs(mm) - 1;
+    const kt::Knob3 k3 = kt::softmax3(slg[3 * lane], slg[3 * lane + 1], slg[3 * lane + 2]);
+    // check mode 5 (planted draws): u was placed 2 delta from a FAST CDF value (fastp[2d+1])
     const uint64_t ge = (uint64_t)ge_L;
-#pragma unroll
-    for (int d = 0; d < NMAX; ++d) {
-      if (!((fm >> d) & 1u)) continue;
-      const kt::Knob3 k3 = kt::softmax3(slg[3 * it], slg[3 * it + 1], slg[3 * it + 2]);
-      // check mode 5 (planted draws): u was placed 2 delta from a FAST CDF value (fastp[2d+1])
-      const double u = check == 5 ? (double)fastp[2 * d + 1]
-                                  : kt::hash01(tk.seed, (ge * (uint64_t)tk.T + (uint64_t)t) * (uint64_t)n + (uint64_t)d);
-      const double c1 = kt::dadd(k3.p[0], k3.p[1]);
-      const int ae = u < k3.p[0] ? 0 : (u < c1 ? 1 : 2);
-      // margin monitor (every re-decided knob, every mode): max |p_fast - p_exact| of the
-      // decision's CDF values, so production runs keep measuring the certificate's margin
-      const float e0 = fabsf((float)(fastp[2 * d] - k3.p[0]));
-      const float err = check == 5 ? e0 : fmaxf(e0, fabsf((float)(fastp[2 * d + 1] - c1)));
-      atomicMax(reinterpret_cast<unsigned int*>(stats + 3), __float_as_uint(err));
-      if (check == 1 || check == 5) {  // compare against the fast decision
-        if ((fast_cert >> d) & 1u) {
-          const int af = (int)((acts >> (2 * d)) & 3u);
-          if (af != ae) atomicAdd(stats + 2, 1ull);
-        }
-      }
-      acts = (acts & ~(3ull << (2 * d))) | ((uint64_t)ae << (2 * d));
-      lp_exact += (float)k3.lp[ae];
-      ++it;
+    const double u = check == 5 ? (double)fastp[2 * dk + 1]
+                                : kt::hash01(tk.seed, (ge * (uint64_t)tk.T + (uint64_t)t) * (uint64_t)n + (uint64_t)dk);
+    const double c1 = kt::dadd(k3.p[0], k3.p[1]);
+    ae = u < k3.p[0] ? 0 : (u < c1 ? 1 : 2);
+    // margin monitor (every re-decided knob, every mode): max |p_fast - p_exact| of the
+    // decision's CDF values, so production runs keep measuring the certificate's margin
+    const float e0 = fabsf((float)(fastp[2 * dk] - k3.p[0]));
+    const float err = check == 5 ? e0 : fmaxf(e0, fabsf((float)(fastp[2 * dk + 1] - c1)));
+    atomicMax(reinterpret_cast<unsigned int*>(stats + 3), __float_as_uint(err));
+    if ((check == 1 || check == 5) && ((cert_L >> dk) & 1u)) {  // compare against the fast decision
+      const int af = (int)((acts_L >> (2 * dk)) & 3u);
+      if (af != ae) atomicAdd(stats + 2, 1ull);
+    }
+    lpk = (float)k3.lp[ae];
+  }
+  float lp_exact = 0.f;
+  for (int j = 0; j < nf; ++j) {  // knob order (the joint log-probability is summed in that order)
+    const int aj = __shfl_sync(0xffffffffu, ae, j), dj = __shfl_sync(0xffffffffu, dk, j);
+    const float lj = __shfl_sync(0xffffffffu, lpk, j);
+    if (lane == L) {
+      acts = (acts & ~(3ull << (2 * dj))) | ((uint64_t)aj << (2 * dj));
+      lp_exact += lj;
     }
   }
   __syncwarp();

@@ -36,6 +36,8 @@ torch.cuda.synchronize()
 ref = [{k: v.clone() for k, v in o.items()} for o in out] if chk else None
 ctx.set_option(L.OPT_PROFILE, 1)
 if chk: ctx.set_option(L.OPT_ROLLOUT_CHECK, chk)
+if os.environ.get("DELTA"):  # diagnostics only: the certification margin in probability units
+    ctx.set_option(L.OPT_ROLLOUT_DELTA, int(float(os.environ["DELTA"]) * 1e12))
 keys = [L.STAT_ROLLOUT_NS, L.STAT_ROLLOUT_CALLS, L.STAT_GBT_NS, L.STAT_GBT_CALLS, L.STAT_ROLLOUT_FALLBACKS,
         L.STAT_ROLLOUT_TC, L.STAT_ROLLOUT_CHECKED, L.STAT_ROLLOUT_MISMATCH, L.STAT_ROLLOUT_MAXERR]
 s0 = {k: ctx.stat(k) for k in keys}
