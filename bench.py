@@ -808,21 +808,27 @@ def main():
         # and the visited configurations as uint8 wherever every cardinality fits (the API's idx_u8);
         # scores as fp32 (north star: scores within 1e-5 relative in fp32; the device keeps and ranks
         # candidates on the exact fp64 scores)
-        small = [max(s.space.cards) <= 256 for s in specs]
-        host_out = [dict(idx=None if sm else pinned(sh(T + 1, D), torch.int16).view(np.uint16),
-                         idx8=pinned(sh(T + 1, D), torch.uint8) if sm else None,
-                         score=None, score32=pinned(sh(T + 1), torch.float32), actions=None,
-                         actions2=pinned(sh(T, (D + 3) // 4), torch.uint8),  # 2 bits per direction
-                         logp=None, value=None, logp32=pinned(sh(T), torch.float32),
-                         value32=pinned(sh(T), torch.float32)) for sm in small]
+        # grouped step-major layout (KTUNE_F_STEP_MAJOR_GROUPED): all 12 tasks' episodes side by side,
+        # one PCIe copy per output per segment; uint8 configurations for the run of tasks whose
+        # cardinalities fit, uint16 for the rest
+        from paper_2001_08743_b200.exploration import compact_grouped_outputs
+        tdt = {np.uint8: torch.uint8, np.uint16: torch.int16, np.float32: torch.float32, np.float64: torch.float64}
+        palloc = lambda shape, dt: pinned(shape, tdt[dt]).view(dt) if dt == np.uint16 else pinned(shape, tdt[dt])
         htasks = [RolloutTask(d, a, g, hi, episode_offset=rank * E, root_seed=s.seed)
                   for s, d, a, g, hi in zip(specs, spaces, agents, gbts, host_init)]
+        GRP = SM  # the grouped layout is the step-major layout over all tasks at once
+        host_out = (compact_grouped_outputs(htasks, T, palloc) if GRP else
+                    [dict(idx=None if max(s.space.cards) <= 256 else pinned(sh(T + 1, D), torch.int16).view(np.uint16),
+                          idx8=pinned(sh(T + 1, D), torch.uint8) if max(s.space.cards) <= 256 else None,
+                          score=None, score32=pinned(sh(T + 1), torch.float32), actions=None,
+                          actions2=pinned(sh(T, (D + 3) // 4), torch.uint8), logp=None, value=None,
+                          logp32=pinned(sh(T), torch.float32), value32=pinned(sh(T), torch.float32)) for s in specs])
         ctx.set_stream(None)
-        run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact, step_major=SM)  # warm
+        run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact, step_major=SM, grouped=GRP)  # warm
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact, step_major=SM)
+            run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact, step_major=SM, grouped=GRP)
         barrier()
         dt = time.perf_counter() - t0
         if world > 1:
@@ -832,19 +838,21 @@ def main():
         e2e = {"value": units_per_step * args.steps / dt, "unit": "config-steps/s", "h2d_bytes_per_step": bi,
                "d2h_bytes_per_step": bo,
                "outputs": "idx as uint8 (uint16 where a cardinality > 256), score fp32 (1e-5 rel.), actions 2-bit, "
-                          "logp/value fp32 (what the tcgen05 path computes)"}
+                          "logp/value fp32 (what the tcgen05 path computes)",
+               "layout": "grouped step-major (one array per output over all tasks)" if GRP else "per task"}
         # the same call with full-precision outputs: fp64 scores, fp64 logp/value (0.84 GB/step)
         del host_out
-        full_out = [dict(idx=None if sm else pinned(sh(T + 1, D), torch.int16).view(np.uint16),
-                         idx8=pinned(sh(T + 1, D), torch.uint8) if sm else None,
-                         score=pinned(sh(T + 1), torch.float64), actions=None,
-                         actions2=pinned(sh(T, (D + 3) // 4), torch.uint8), logp=pinned(sh(T), torch.float64),
-                         value=pinned(sh(T), torch.float64)) for sm in small]
-        run_episodes_batch(htasks, T, ctx, host_out=full_out, exact=args.exact, step_major=SM)  # warm
+        full_out = (compact_grouped_outputs(htasks, T, palloc, score64=True, logp64=True) if GRP else
+                    [dict(idx=None if max(s.space.cards) <= 256 else pinned(sh(T + 1, D), torch.int16).view(np.uint16),
+                          idx8=pinned(sh(T + 1, D), torch.uint8) if max(s.space.cards) <= 256 else None,
+                          score=pinned(sh(T + 1), torch.float64), actions=None,
+                          actions2=pinned(sh(T, (D + 3) // 4), torch.uint8), logp=pinned(sh(T), torch.float64),
+                          value=pinned(sh(T), torch.float64)) for s in specs])
+        run_episodes_batch(htasks, T, ctx, host_out=full_out, exact=args.exact, step_major=SM, grouped=GRP)  # warm
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            run_episodes_batch(htasks, T, ctx, host_out=full_out, exact=args.exact, step_major=SM)
+            run_episodes_batch(htasks, T, ctx, host_out=full_out, exact=args.exact, step_major=SM, grouped=GRP)
         barrier()
         dtf = time.perf_counter() - t0
         if world > 1:

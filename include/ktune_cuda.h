@@ -46,10 +46,14 @@ enum ktune_flags {
   KTUNE_F_DEVICE = 1,       /* array arguments are device pointers */
   KTUNE_F_EXACT_ROLLOUT = 2, /* ktune_rollout: exact fp64 forward for every config-step (logp/value
                                bit-exact too); default is the tcgen05 path with certified sampling */
-  KTUNE_F_STEP_MAJOR = 4     /* ktune_rollout: trajectories step-major, idx/score [T+1][E], actions/logp/value
+  KTUNE_F_STEP_MAJOR = 4,    /* ktune_rollout: trajectories step-major, idx/score [T+1][E], actions/logp/value
                                [T][E] (rows of D knobs where applicable), instead of episode-major [E][T+1] /
                                [E][T]: the device writes one coalesced row block per step, and every
                                segment of a host-pointer call crosses PCIe as one contiguous copy */
+  KTUNE_F_STEP_MAJOR_GROUPED = 8 /* ktune_rollout: step-major over ALL tasks' episodes at once: every output
+                               is one [T+1 or T][Etot = sum E_k] array (rows of D knobs; every task has the
+                               same D) and task k passes pointers at its episode offset sum_{j<k} E_j of task
+                               0's arrays; a segment of every task crosses PCIe as ONE copy per output */
 };
 
 typedef struct ktune_ctx ktune_ctx;

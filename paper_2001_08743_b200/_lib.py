@@ -18,6 +18,7 @@ KTUNE_OK, ERR_CONFIG, ERR_BACKEND, ERR_EXHAUSTED, ERR_LOGIC, ERR_CUDA, ERR_NOMEM
 F_DEVICE = 1
 F_EXACT_ROLLOUT = 2
 F_STEP_MAJOR = 4
+F_STEP_MAJOR_GROUPED = 8
 OPT_FORCE_EXACT, OPT_KMEANS_MODE, OPT_PROFILE, OPT_ROLLOUT_DELTA, OPT_ROLLOUT_CHECK, OPT_ROLLOUT_FUSE_GBT, \
     OPT_ROLLOUT_SEGMENTS, OPT_FORCE_SHARDED, OPT_KMEANS_BOUND_LOG2 = 1, 2, 3, 4, 5, 6, 7, 8, 9
 STAT_LAUNCHES, STAT_KPP_FALLBACKS, STAT_DECISION_FALLBACKS, STAT_ASSIGN_FALLBACKS, \

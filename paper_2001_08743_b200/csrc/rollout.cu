@@ -524,9 +524,55 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     if (num_tasks < 0 || T < 0) kt::fail(KTUNE_ERR_CONFIG, "rollout: bad task count or steps");
     if (num_tasks == 0) return;
     const bool dev = flags & KTUNE_F_DEVICE;
-    const bool stepm = flags & KTUNE_F_STEP_MAJOR;  // trajectories [T+1][E] / [T][E] instead of [E][T+1] / [E][T]
+    const bool grouped = flags & KTUNE_F_STEP_MAJOR_GROUPED;  // one step-major array over all tasks' episodes
+    const bool stepm = grouped || (flags & KTUNE_F_STEP_MAJOR);  // [T+1][E] / [T][E] instead of [E][T+1] / [E][T]
     std::vector<RolloutTask> dt(num_tasks);
-    // device buffers (host-pointer calls: one grow-only context arena, 256-byte aligned slices)
+    // grouped: task k's episodes are columns [goff[k], goff[k] + E_k) of ONE step-major array of
+    // Etot columns per output, so every step (and every segment) of all tasks is contiguous
+    std::vector<int64_t> goff(num_tasks + 1, 0);
+    for (int k = 0; k < num_tasks; ++k) goff[k + 1] = goff[k] + std::max<int64_t>(0, tasks[k].num_episodes);
+    const int64_t Etot = goff[num_tasks];
+    // per output kind (idx, score, actions, logp, value, logp32, value32, idx8, actions2, score32):
+    // the tasks that request it form one contiguous run [lo, hi] whose columns are a W-wide
+    // step-major array at the host pointer of task lo (task k at column goff[k] - goff[lo])
+    struct GKind {
+      int lo = -1, hi = -1;
+      int64_t W = 0;
+      void* host = nullptr;
+      size_t rb = 0;  // bytes per row element (per episode column)
+    };
+    std::array<GKind, 10> gk{};
+    auto kind_ptr = [&](const ktune_rollout_task& t, int q) -> void* {
+      void* const v[10] = {t.idx, t.score, t.actions, t.logp, t.value, t.logp_f32, t.value_f32, t.idx_u8, t.actions_u2,
+                           t.score_f32};
+      return v[q];
+    };
+    if (grouped) {
+      for (int k = 1; k < num_tasks; ++k)
+        if (!tasks[k].ac || !tasks[0].ac || tasks[k].ac->n != tasks[0].ac->n)
+          kt::fail(KTUNE_ERR_CONFIG, "rollout: grouped layout needs the same knob count in every task");
+      const int64_t n = tasks[0].ac ? tasks[0].ac->n : 0;
+      const size_t rbs[10] = {(size_t)(2 * n), 8, (size_t)n, 8, 8, 4, 4, (size_t)n, (size_t)((n + 3) / 4), 4};
+      for (int q = 0; q < 10; ++q) {
+        GKind& g = gk[q];
+        g.rb = rbs[q];
+        for (int k = 0; k < num_tasks; ++k) {
+          void* pk = kind_ptr(tasks[k], q);
+          if (!pk) continue;
+          if (g.lo < 0) {
+            g.lo = k;
+            g.host = pk;
+          } else if (g.hi != k - 1 || (char*)pk != (char*)g.host + (goff[k] - goff[g.lo]) * (int64_t)g.rb) {
+            kt::fail(KTUNE_ERR_CONFIG, "rollout: grouped layout needs each output's tasks contiguous, every task "
+                                       "at its episode offset of the first one's array");
+          }
+          g.hi = k;
+        }
+        if (g.lo >= 0) g.W = goff[g.hi + 1] - goff[g.lo];
+        if (dev && g.lo >= 0 && g.W != Etot)  // device pointers: the kernel writes Etot-wide rows
+          kt::fail(KTUNE_ERR_CONFIG, "rollout: grouped device outputs must be requested by every task");
+      }
+    }
     struct HostIo {
       const uint16_t* d_init;
       uint16_t* d_idx;
@@ -564,7 +610,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         for (int c : t.space->card)
           if (c > 256) kt::fail(KTUNE_ERR_CONFIG, "rollout: idx_u8 needs every knob cardinality <= 256");
       smem_params = smem_params && fits_smem(t.ac->n, t.ac->h, t.ac->g);
-      if (!dev) {
+      if (!dev && !grouped) {
         const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
         offs[k] = {slice(E * n * 2), slice(E * (T + 1) * n * 2), (t.actions || t.actions_u2) ? slice(E * T * n) : SIZE_MAX,
                    t.logp ? slice(E * T * 8) : SIZE_MAX, t.value ? slice(E * T * 8) : SIZE_MAX,
@@ -573,6 +619,15 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
                    t.actions_u2 ? slice(E * T * ((n + 3) / 4)) : SIZE_MAX,
                    t.score_f32 ? slice(E * (T + 1) * 4) : SIZE_MAX};
       }
+    }
+    if (!dev && grouped && num_tasks > 0) {  // one Etot-wide slice per output any task requests
+      const size_t E = (size_t)Etot, n = (size_t)tasks[0].ac->n;
+      auto any = [&](int q) { return gk[q].lo >= 0; };
+      offs[0] = {slice(E * n * 2), slice(E * (T + 1) * n * 2), (any(2) || any(8)) ? slice(E * T * n) : SIZE_MAX,
+                 any(3) ? slice(E * T * 8) : SIZE_MAX, any(4) ? slice(E * T * 8) : SIZE_MAX,
+                 (any(1) || any(9)) ? slice(E * (T + 1) * 8) : SIZE_MAX, any(5) ? slice(E * T * 4) : SIZE_MAX,
+                 any(6) ? slice(E * T * 4) : SIZE_MAX, any(7) ? slice(E * (T + 1) * n) : SIZE_MAX,
+                 any(8) ? slice(E * T * ((n + 3) / 4)) : SIZE_MAX, any(9) ? slice(E * (T + 1) * 4) : SIZE_MAX};
     }
     unsigned char* base = dev ? nullptr : (unsigned char*)ctx->dev(kt::WS_ROLLOUT, std::max<size_t>(arena, 256));
     auto at = [&](size_t o) { return o == SIZE_MAX ? nullptr : (void*)(base + o); };
@@ -584,6 +639,17 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       if (dev) {
         h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score, t.logp_f32, t.value_f32, t.idx_u8, t.actions_u2,
              t.score_f32};
+      } else if (grouped) {  // task 0's slices, shifted to this task's episode columns
+        const int64_t o = goff[k];
+        auto sh = [&](size_t off, int64_t per_row) -> unsigned char* {
+          return off == SIZE_MAX ? nullptr : (unsigned char*)at(off) + o * per_row;
+        };
+        h = {(const uint16_t*)sh(offs[0][0], 2 * n), (uint16_t*)sh(offs[0][1], 2 * n), (int8_t*)sh(offs[0][2], n),
+             (double*)sh(offs[0][3], 8),             (double*)sh(offs[0][4], 8),       (double*)sh(offs[0][5], 8),
+             (float*)sh(offs[0][6], 4),              (float*)sh(offs[0][7], 4),        (uint8_t*)sh(offs[0][8], n),
+             (uint8_t*)sh(offs[0][9], (n + 3) / 4),  (float*)sh(offs[0][10], 4)};
+        if (E > 0)
+          KT_CUDA(cudaMemcpyAsync((void*)h.d_init, t.init_idx, (size_t)E * n * 2, cudaMemcpyHostToDevice, ctx->stream));
       } else {
         h = {(const uint16_t*)at(offs[k][0]), (uint16_t*)at(offs[k][1]), (int8_t*)at(offs[k][2]),
              (double*)at(offs[k][3]),         (double*)at(offs[k][4]),   (double*)at(offs[k][5]),
@@ -610,9 +676,9 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       r.logp32 = h.d_logp32;
       r.value32 = h.d_val32;
       r.sE = stepm ? 1 : (int64_t)T + 1;
-      r.sT = stepm ? E : 1;
+      r.sT = stepm ? (grouped ? Etot : E) : 1;
       r.aE = stepm ? 1 : (int64_t)T;
-      r.aT = stepm ? E : 1;
+      r.aT = stepm ? (grouped ? Etot : E) : 1;
     }
     // tcgen05 path with certified sampling unless the exact fp64 forward is
     // requested (or a task is outside the tensor-core path's shapes)
@@ -635,6 +701,11 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       const ktune_rollout_task& t = tasks[k];
       if (!t.gbt || !io[k].d_score || t.num_episodes == 0) return;
       const int64_t len = r1 - r0 + 1, E = t.num_episodes;
+      if (grouped) {  // this task's columns of rows r0..r1: blocks of E every Etot
+        kt::gbt_predict_idx_device(ctx, t.gbt, io[0].d_idx, 2, E * len, io[0].d_score,
+                                   kt::RowMap{E, Etot, r0 * Etot + goff[k]});
+        return;
+      }
       if (stepm) {  // rows r0..r1 of every episode are one contiguous block
         kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx + r0 * E * t.ac->n, 2, E * len, io[k].d_score + r0 * E);
         return;
@@ -646,8 +717,12 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     };
     auto score32_rows = [&](int k, int r0, int r1) {  // fp32 copies of the scores of rows [r0, r1]
       const ktune_rollout_task& t = tasks[k];
-      if (!t.gbt || !io[k].d_s32 || t.num_episodes == 0) return;
-      const int64_t len = r1 - r0 + 1, work = t.num_episodes * len, E = t.num_episodes;
+      if (grouped) {  // one flat pass over every task's columns (task 0's pointers are the slice starts)
+        if (k > 0 || gk[9].lo < 0 || Etot == 0) return;
+      } else if (!t.gbt || !io[k].d_s32 || t.num_episodes == 0) {
+        return;
+      }
+      const int64_t len = r1 - r0 + 1, E = grouped ? Etot : t.num_episodes, work = E * len;
       // step-major: one flat range [r0*E, (r1+1)*E) of a single "episode"
       score_f32_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(work, 256), (int64_t)kt::sm_count(ctx) * 16), 256, 0,
                          ctx->stream>>>(io[k].d_score, io[k].d_s32, stepm ? 1 : E, T + 1, stepm ? r0 * E : r0,
@@ -656,26 +731,50 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     };
     auto narrow_rows = [&](int k, int r0, int r1) {  // uint16 -> uint8 trajectory rows [r0, r1]
       const ktune_rollout_task& t = tasks[k];
-      if (!t.idx_u8 || t.num_episodes == 0) return;
-      narrow_idx_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(t.num_episodes * (int64_t)(r1 - r0 + 1) * t.ac->n, 256),
+      if (grouped ? (k > 0 || gk[7].lo < 0 || Etot == 0) : (!t.idx_u8 || t.num_episodes == 0)) return;
+      const int64_t E = grouped ? Etot : t.num_episodes;
+      narrow_idx_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(E * (int64_t)(r1 - r0 + 1) * t.ac->n, 256),
                                                      (int64_t)kt::sm_count(ctx) * 16),
-                          256, 0, ctx->stream>>>(io[k].d_idx, io[k].d_u8, stepm ? 1 : t.num_episodes, T + 1,
-                                                 t.ac->n, stepm ? r0 * t.num_episodes : r0,
-                                                 stepm ? (r1 - r0 + 1) * t.num_episodes : r1 - r0 + 1);
+                          256, 0, ctx->stream>>>(io[k].d_idx, io[k].d_u8, stepm ? 1 : E, T + 1,
+                                                 t.ac->n, stepm ? r0 * E : r0,
+                                                 stepm ? (r1 - r0 + 1) * E : r1 - r0 + 1);
       kt::check_launch(ctx, "narrow_idx");
     };
     auto pack_steps = [&](int k, int t0, int t1) {  // int8 -> 2-bit actions of steps [t0, t1)
       const ktune_rollout_task& t = tasks[k];
-      if (!t.actions_u2 || t.num_episodes == 0 || t1 <= t0) return;
-      const int64_t work = t.num_episodes * (int64_t)(t1 - t0) * ((t.ac->n + 3) / 4);
+      if (t1 <= t0 || (grouped ? (k > 0 || gk[8].lo < 0 || Etot == 0) : (!t.actions_u2 || t.num_episodes == 0)))
+        return;
+      const int64_t E = grouped ? Etot : t.num_episodes;
+      const int64_t work = E * (int64_t)(t1 - t0) * ((t.ac->n + 3) / 4);
       pack_actions_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(work, 256), (int64_t)kt::sm_count(ctx) * 16), 256,
-                            0, ctx->stream>>>(io[k].d_act, io[k].d_a2, stepm ? 1 : t.num_episodes, T, t.ac->n,
-                                              stepm ? (int64_t)t0 * t.num_episodes : t0,
-                                              stepm ? (int64_t)(t1 - t0) * t.num_episodes : t1 - t0);
+                            0, ctx->stream>>>(io[k].d_act, io[k].d_a2, stepm ? 1 : E, T, t.ac->n,
+                                              stepm ? (int64_t)t0 * E : t0, stepm ? (int64_t)(t1 - t0) * E : t1 - t0);
       kt::check_launch(ctx, "pack_actions");
     };
     auto copy_out = [&](int k, int t0, int t1, cudaStream_t st) {  // steps [t0, t1): rows (t0, t1] (+ row 0)
       const ktune_rollout_task& t = tasks[k];
+      if (grouped) {  // once for every task: per output, the W columns of its task run in one copy
+        if (k > 0) return;
+        const int r0 = t0 == 0 ? 0 : t0 + 1;
+        const int64_t nr[10] = {t1 - r0 + 1, t1 - r0 + 1, t1 - t0, t1 - t0, t1 - t0, t1 - t0, t1 - t0, t1 - r0 + 1,
+                                t1 - t0, t1 - r0 + 1};
+        const int64_t first[10] = {r0, r0, t0, t0, t0, t0, t0, r0, t0, r0};
+        const void* dsrc[10] = {io[0].d_idx, io[0].d_score, io[0].d_act, io[0].d_logp, io[0].d_val,
+                                io[0].d_logp32, io[0].d_val32, io[0].d_u8, io[0].d_a2, io[0].d_s32};
+        for (int q = 0; q < 10; ++q) {
+          const GKind& g = gk[q];
+          if (g.lo < 0 || g.W == 0 || nr[q] <= 0 || !dsrc[q]) continue;
+          if ((q == 1 || q == 9) && !tasks[g.lo].gbt) continue;
+          const size_t spitch = (size_t)Etot * g.rb, dpitch = (size_t)g.W * g.rb, width = dpitch;
+          const char* src = (const char*)dsrc[q] + (size_t)first[q] * spitch + (size_t)goff[g.lo] * g.rb;
+          char* dst = (char*)g.host + (size_t)first[q] * dpitch;
+          if (spitch == dpitch)
+            KT_CUDA(cudaMemcpyAsync(dst, src, width * (size_t)nr[q], cudaMemcpyDeviceToHost, st));
+          else
+            KT_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, (size_t)nr[q], cudaMemcpyDeviceToHost, st));
+        }
+        return;
+      }
       const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
       if (E == 0) return;
       const HostIo& h = io[k];
@@ -752,8 +851,8 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
             kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
             kt::rollout_tc(ctx, work, T, t0, t1);
           }
-          for (int k = 0; k < num_tasks; ++k) {
-            score_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
+          for (int k = 0; k < num_tasks; ++k) score_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
+          for (int k = 0; k < num_tasks; ++k) {  // after every task's scores (grouped: one pass for all)
             score32_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
             narrow_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
             pack_steps(k, t0, t1);
@@ -803,8 +902,9 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       kt::check_launch(ctx, "rollout");
     }
     // cost-model scores of every visited configuration (K1 over the trajectory)
-    for (int k = 0; k < num_tasks; ++k) {
+    for (int k = 0; k < num_tasks; ++k)
       if (!scored[k]) score_rows(k, 0, T);
+    for (int k = 0; k < num_tasks; ++k) {  // after every task's scores (grouped: one pass for all)
       score32_rows(k, 0, T);
       narrow_rows(k, 0, T);
       pack_steps(k, 0, T);

@@ -206,9 +206,62 @@ class RolloutTask:
     want_trajectory: bool = True
 
 
+def grouped_outputs(tasks: Sequence[RolloutTask], T: int, alloc, fields=None) -> list:
+    """Per-task output dicts for the GROUPED step-major layout (KTUNE_F_STEP_MAJOR_GROUPED): one
+    (rows, sum E_k[, D]) array per output, task k's entries are the column views [off_k, off_k + E_k).
+    alloc(shape, name) -> array (numpy, pinned numpy or torch); fields: name -> (rows, last-dim or
+    None), default the full-precision set."""
+    D = tasks[0].space.D
+    if any(t.space.D != D for t in tasks):
+        raise ConfigError("rollout: grouped layout needs the same knob count in every task")
+    Es = [len(t.init_idx) for t in tasks]
+    Et = sum(Es)
+    fields = fields or {"idx": (T + 1, D), "score": (T + 1, None), "actions": (T, D), "logp": (T, None),
+                        "value": (T, None)}
+    big = {name: alloc((rows,) + ((Et,) if last is None else (Et, last)), name) for name, (rows, last) in fields.items()}
+    outs, off = [], 0
+    for E in Es:
+        outs.append({name: a[:, off:off + E] for name, a in big.items()})
+        off += E
+    return outs
+
+
+def compact_grouped_outputs(tasks: Sequence[RolloutTask], T: int, alloc, score64: bool = False,
+                            logp64: bool = False) -> list:
+    """Grouped step-major outputs in the compact encoding (what crosses PCIe): visited
+    configurations as uint8 for every run of consecutive tasks whose cardinalities fit (uint16
+    for the others), directions as 2-bit codes, scores fp32 (fp64 with score64) and log-probs /
+    values fp32 (fp64 with logp64; the tcgen05 path computes them in fp32). alloc(shape, dtype)
+    -> array. Every output but idx spans all tasks; idx is one array per run."""
+    D = tasks[0].space.D
+    Es = [len(t.init_idx) for t in tasks]
+    offs = np.cumsum([0] + Es)
+    Et = int(offs[-1])
+    big = {"actions2": alloc((T, Et, (D + 3) // 4), np.uint8),
+           ("score" if score64 else "score32"): alloc((T + 1, Et), np.float64 if score64 else np.float32),
+           ("logp" if logp64 else "logp32"): alloc((T, Et), np.float64 if logp64 else np.float32),
+           ("value" if logp64 else "value32"): alloc((T, Et), np.float64 if logp64 else np.float32)}
+    outs = [{k: a[:, offs[i]:offs[i + 1]] for k, a in big.items()} for i in range(len(tasks))]
+    small = [max(t.space.card) <= 256 for t in tasks]
+    i = 0
+    while i < len(tasks):  # runs of consecutive tasks with the same idx width
+        j = i
+        while j < len(tasks) and small[j] == small[i]:
+            j += 1
+        name, dt = ("idx8", np.uint8) if small[i] else ("idx", np.uint16)
+        a = alloc((T + 1, int(offs[j] - offs[i]), D), dt)
+        for q in range(i, j):
+            outs[q][name] = a[:, offs[q] - offs[i]:offs[q + 1] - offs[i]]
+        i = j
+    for o in outs:
+        for k in ("idx", "idx8", "score", "score32", "actions", "logp", "value", "logp32", "value32"):
+            o.setdefault(k, None)
+    return outs
+
+
 def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Context] = None,
                        device_out: bool = False, host_out: Optional[list] = None, exact: bool = False,
-                       step_major: bool = False):
+                       step_major: bool = False, grouped: bool = False):
     """Grouped run_episodes over several workloads in ONE persistent-kernel launch.
 
     Host arrays in/out by default; with CUDA-tensor init_idx and device_out=True
@@ -222,8 +275,31 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
     step_major=True (KTUNE_F_STEP_MAJOR) lays the trajectories out step-major:
     idx (T+1) x E x D, score (T+1) x E, actions T x E x D, logp/value T x E -
     the same values transposed; each step is one contiguous block on the device
-    and each segment of a host-buffer call one contiguous PCIe copy.
+    and each segment of a host-buffer call one contiguous PCIe copy. grouped=True
+    (KTUNE_F_STEP_MAJOR_GROUPED) lays ALL tasks' episodes side by side in one
+    step-major array per output (see grouped_outputs; host_out must come from it,
+    or is allocated that way): one copy per output per segment for every task.
     """
+    if grouped:
+        step_major = True
+        if host_out is None:
+            dev0 = hasattr(tasks[0].init_idx, "is_cuda") and tasks[0].init_idx.is_cuda
+            want = {"idx": (T + 1, tasks[0].space.D)}
+            if tasks[0].cost_model is not None:
+                want["score"] = (T + 1, None)
+            if tasks[0].want_trajectory:
+                want.update({"actions": (T, tasks[0].space.D), "logp": (T, None), "value": (T, None)})
+            dt = {"idx": np.uint16, "score": np.float64, "actions": np.int8, "logp": np.float64, "value": np.float64}
+            if dev0:
+                import torch
+                tdt = {np.uint16: torch.uint16, np.float64: torch.float64, np.int8: torch.int8}
+                alloc = lambda shape, name: torch.empty(shape, dtype=tdt[dt[name]], device=tasks[0].init_idx.device)
+            else:
+                alloc = lambda shape, name: host_empty(shape, dt[name])
+            host_out = grouped_outputs(tasks, T, alloc, want)
+            for o in host_out:
+                for k in ("idx", "score", "actions", "logp", "value"):
+                    o.setdefault(k, None)
     ctx = ctx or tasks[0].space.ctx
     arr = (L.RolloutTaskC * len(tasks))()
     outs = []
@@ -285,7 +361,8 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
         outs.append(o)
     ctx.check(L.lib().ktune_rollout(ctx.h, len(tasks), arr, T,
                                     (L.F_DEVICE if dev else 0) | (L.F_EXACT_ROLLOUT if exact else 0) |
-                                    (L.F_STEP_MAJOR if step_major else 0)))
+                                    (L.F_STEP_MAJOR if step_major else 0) |
+                                    (L.F_STEP_MAJOR_GROUPED if grouped else 0)))
     return outs
 
 

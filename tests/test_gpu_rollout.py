@@ -427,3 +427,82 @@ def test_rollout_step_major_multi_wave(O, ctx):
     b = run_episodes_batch([task], T, step_major=True)[0]
     for k in ["idx", "actions", "score", "logp", "value"]:
         assert np.array_equal(np.swapaxes(a[k], 0, 1), b[k]), k
+
+
+def test_rollout_step_major_grouped(O, ctx):
+    """KTUNE_F_STEP_MAJOR_GROUPED: all tasks' episodes side by side in one step-major array per
+    output (one PCIe copy per output per segment); every task's column block equals its own
+    step-major call, on the host (segmented) and device paths and for the compact outputs."""
+    import torch
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.exploration import RolloutTask, grouped_outputs, run_episodes_batch, unpack_actions
+    from paper_2001_08743_b200.errors import ConfigError
+    tasks, dtasks = [], []
+    for i, name in enumerate(["resnet_c2", "vgg_c4", "synthetic8"]):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=160 + i)
+        E = [70, 129, 33][i]
+        init = np.random.default_rng(i).integers(0, 2, (E, sp.num_knobs)).astype(np.int32)
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=3 * i, root_seed=i))
+        dtasks.append(RolloutTask(dspace, agent, dg, torch.from_numpy(init).cuda(), episode_offset=3 * i, root_seed=i))
+    T = 260
+    ref = run_episodes_batch(tasks, T, step_major=True)
+    grp = run_episodes_batch(tasks, T, grouped=True)
+    dgp = run_episodes_batch(dtasks, T, grouped=True)
+    torch.cuda.synchronize()
+    for a, b, d in zip(ref, grp, dgp):
+        for k in ["idx", "actions", "score", "logp", "value"]:
+            assert np.array_equal(a[k], b[k]), k
+            assert np.array_equal(a[k], d[k].cpu().numpy()), k
+    D = tasks[0].space.D
+    fields = {"idx8": (T + 1, D), "actions2": (T, (D + 3) // 4), "score32": (T + 1, None), "logp32": (T, None),
+              "value32": (T, None)}
+    dts = {"idx8": np.uint8, "actions2": np.uint8, "score32": np.float32, "logp32": np.float32, "value32": np.float32}
+    outs = grouped_outputs(tasks, T, lambda shape, name: np.zeros(shape, dts[name]), fields)
+    for o in outs:
+        o.update(idx=None, actions=None, score=None, logp=None, value=None)
+    run_episodes_batch(tasks, T, host_out=outs, grouped=True)
+    for a, o in zip(ref, outs):
+        assert np.array_equal(o["idx8"], a["idx"].astype(np.uint8))
+        assert np.array_equal(unpack_actions(o["actions2"], D), a["actions"])
+        assert np.array_equal(o["score32"], a["score"].astype(np.float32))
+        assert np.array_equal(o["logp32"], a["logp"].astype(np.float32))
+    # the bench's shape: a task whose cardinalities exceed 256 ships uint16 idx while the others ship
+    # idx_u8; each output's run of tasks is its own W-wide array (2-D copies out of the Etot-wide rows)
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt
+    from paper_2001_08743_b200.exploration import ActorCritic
+    sp = SPACES["resnet_dense_u16"]()
+    osp, og, pm = fitted(O, sp, seed=7)
+    ds = Space(sp, ctx)
+    wide = RolloutTask(ds, ActorCritic(sp.num_knobs, 128, 64, seed=7, ctx=ctx), DeviceGbt(pm, ds),
+                       np.zeros((45, sp.num_knobs), np.int32), 0, 7)
+    mixed = tasks[:2] + [wide]
+    refm = run_episodes_batch(mixed, T, step_major=True)
+    f8 = {"idx8": (T + 1, D), "score32": (T + 1, None)}
+    o8 = grouped_outputs(mixed[:2], T, lambda shape, name: np.zeros(shape, np.uint8 if name == "idx8" else np.float32), f8)
+    o16 = grouped_outputs(mixed[2:], T, lambda shape, name: np.zeros(shape, np.uint16 if name == "idx" else np.float32),
+                          {"idx": (T + 1, D), "score32": (T + 1, None)})
+    sc = np.zeros((T + 1, sum(len(t.init_idx) for t in mixed)), np.float32)  # one score32 array over all three
+    offs = np.cumsum([0] + [len(t.init_idx) for t in mixed])
+    outs_m = []
+    for i, o in enumerate(o8 + o16):
+        o = dict(o)
+        o["score32"] = sc[:, offs[i]:offs[i + 1]]
+        o.setdefault("idx", None)
+        o.setdefault("idx8", None)
+        o.update(actions=None, score=None, logp=None, value=None)
+        outs_m.append(o)
+    run_episodes_batch(mixed, T, host_out=outs_m, grouped=True)
+    for a, o in zip(refm, outs_m):
+        got = o["idx8"] if o["idx8"] is not None else o["idx"]
+        assert np.array_equal(got.astype(np.int64), a["idx"].astype(np.int64))
+        assert np.array_equal(o["score32"], a["score"].astype(np.float32))
+    # misplaced task pointers are rejected
+    bad = grouped_outputs(tasks[:2], T, lambda shape, name: np.zeros(shape, np.float64 if name != "idx" else np.uint16),
+                          {"idx": (T + 1, D), "score": (T + 1, None)})
+    bad[1]["idx"] = np.zeros((T + 1, 129, D), np.uint16)
+    for o in bad:
+        o.update(actions=None, logp=None, value=None)
+    with pytest.raises(ConfigError):
+        run_episodes_batch(tasks[:2], T, host_out=bad, grouped=True)

@@ -27,6 +27,22 @@ for h, s in zip(host_init, specs):
 htasks = [RolloutTask(d, a, g, hi, 0, s.seed) for s, d, a, g, hi in zip(specs, spaces, agents, gbts, host_init)]
 for seg in [int(x) for x in os.environ.get("SEGS", "0").split(",")]:
     ctx.set_option(L.OPT_ROLLOUT_SEGMENTS, seg)
+    for s64 in (False, True):
+        from paper_2001_08743_b200.exploration import compact_grouped_outputs
+        tdt = {np.uint8: torch.uint8, np.uint16: torch.int16, np.float32: torch.float32, np.float64: torch.float64}
+        out = compact_grouped_outputs(htasks, T, lambda shape, dt: pinned(shape, tdt[dt]).view(dt) if dt == np.uint16
+                                      else pinned(shape, tdt[dt]), score64=s64, logp64=s64)
+        run_episodes_batch(htasks, T, ctx, host_out=out, grouped=True)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            run_episodes_batch(htasks, T, ctx, host_out=out, grouped=True)
+            ts.append(time.perf_counter() - t0)
+        bo = sum(sum(v.nbytes for v in o.values() if v is not None) for o in out)
+        ms = 1e3 * np.median(ts)
+        print(f"segs {seg} grouped step-major score {'f64' if s64 else 'f32'}: {ms:.2f} ms/step, "
+              f"{12 * E * T / ms * 1e3:.3e} config-steps/s, D2H {bo / 1e9:.3f} GB ({bo / ms / 1e6:.1f} GB/s)", flush=True)
     for step_major in (False, True):
         for s64 in (False, True):
             sh = lambda rows, *rest: ((rows, E) if step_major else (E, rows)) + rest
