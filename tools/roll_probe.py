@@ -36,15 +36,20 @@ torch.cuda.synchronize()
 ref = [{k: v.clone() for k, v in o.items()} for o in out] if chk else None
 ctx.set_option(L.OPT_PROFILE, 1)
 if chk: ctx.set_option(L.OPT_ROLLOUT_CHECK, chk)
-if os.environ.get("DELTA"):  # diagnostics only: the certification margin in probability units
+if os.environ.get("DELTA"):  # the certification band in probability units
     ctx.set_option(L.OPT_ROLLOUT_DELTA, int(float(os.environ["DELTA"]) * 1e12))
+
 keys = [L.STAT_ROLLOUT_NS, L.STAT_ROLLOUT_CALLS, L.STAT_GBT_NS, L.STAT_GBT_CALLS, L.STAT_ROLLOUT_FALLBACKS,
         L.STAT_ROLLOUT_TC, L.STAT_ROLLOUT_CHECKED, L.STAT_ROLLOUT_MISMATCH, L.STAT_ROLLOUT_MAXERR]
 s0 = {k: ctx.stat(k) for k in keys}
 reps = int(os.environ.get("REPS", "5"))
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ev0.record(stream)
 for i in range(reps):
     run_episodes_batch(tasks, T, ctx, host_out=out, step_major=sm)
+ev1.record(stream)
 torch.cuda.synchronize()
+print(f"whole call (rollout + verification + K1): {ev0.elapsed_time(ev1) / reps:.3f} ms")
 d = {k: ctx.stat(k) - s0[k] for k in keys}
 roll = d[L.STAT_ROLLOUT_NS] / 1e6 / reps
 gbt = d[L.STAT_GBT_NS] / 1e6 / reps
