@@ -568,6 +568,42 @@ def kmeans_secondary(ctx, args, cpu=True):
                                        "reference's fp64 order); the certified iterations run the same kernel "
                                        "against integer-sum centroids"},
            "forced_full_sweep": full}
+    # SURVEY C4's second space: a ResNet-18 layer (uint8 indices), the same 1M-candidate protocol
+    try:
+        sp2 = S.resnet18_tasks()[1]
+        ds2 = Space(sp2, ctx)
+        idx2 = random_configs(sp2, args.kmeans_n, 123)
+        ids2 = ds2.id_of(idx2)
+        _, first2 = np.unique(ids2, return_index=True)
+        keep2 = np.sort(first2)
+        idx2, ids2 = idx2[keep2], ids2[keep2]
+        kmeans_run(ds2, idx2, 8, 11, max_iters=2, restarts=1)
+        tk = []
+        for _ in range(3):
+            t1 = time.perf_counter()
+            r2 = kmeans_run(ds2, idx2, 8, 11, restarts=1)
+            tk.append(time.perf_counter() - t1)
+        ts2 = []
+        for _ in range(3):
+            t1 = time.perf_counter()
+            sw2 = adaptive_sweep(ds2, CandidateSet(idx2, ids2, np.zeros(len(idx2))), SamplingParams(), 5)
+            ts2.append(time.perf_counter() - t1)
+        f2 = None
+        if not getattr(args, "no_full_sweep", False):
+            ctx.reset_stats()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            for kk in range(8, 64):
+                kmeans_run(ds2, idx2, kk, 1000 + kk, restarts=3)
+            torch.cuda.synchronize()
+            f2 = {"ms": 1e3 * (time.perf_counter() - t1), "lloyd_iters": ctx.stat(L.STAT_LLOYD_ITERS)}
+        out["c4_resnet18"] = {"workload": f"resnet18.t1 space (u8 idx), N={len(idx2)} candidates",
+                              "kmeans_run_k8_ms": 1e3 * float(np.median(tk)),
+                              "lloyd_iters_k8": len(r2.iteration_losses) - 1,
+                              "adaptive_sample_ms": 1e3 * float(np.median(ts2)), "sweep_k": sw2.k,
+                              "forced_full_sweep": f2}
+    except Exception as ex:  # reported, not hidden
+        out["c4_resnet18"] = {"error": repr(ex)}
     if cpu:
         try:
             from oracle import pyoracle as O
@@ -584,6 +620,50 @@ def kmeans_secondary(ctx, args, cpu=True):
         except Exception as ex:
             out["cpu_baseline"] = {"error": repr(ex)}
     return out
+
+
+def c2_total_secondary(ctx, args):
+    """SURVEY C2's other reading of "4096 configs/step": 4096 episodes IN TOTAL over the 12 ResNet-18
+    tasks (342 each), T steps, one grouped launch + scoring, device buffers (step-major)."""
+    import torch
+    from paper_2001_08743_b200.context import Space
+    from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
+    from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
+    from workloads.tasks import encode
+
+    class A:
+        tasks = args.tasks
+        episodes = -(-4096 // args.tasks)
+        seed = args.seed
+    specs = build_tasks(A, 0)
+    E, T = A.episodes, args.T
+    spaces = [Space(s.space, ctx) for s in specs]
+    gbts = [DeviceGbt(fit_gbt(encode(s.space, s.train_idx), s.train_y, seed=s.seed), d) for s, d in zip(specs, spaces)]
+    agents = [ActorCritic(s.space.num_knobs, 128, 64, seed=s.seed, ctx=ctx) for s in specs]
+    tasks = [RolloutTask(d, a, g, torch.from_numpy(s.init_idx[:E].astype(np.uint16)).cuda(), 0, s.seed)
+             for s, d, a, g in zip(specs, spaces, agents, gbts)]
+    D = specs[0].space.num_knobs
+    cs = torch.cuda.current_stream()
+    ctx.set_stream(cs.cuda_stream)  # the events below and the library on one stream
+    mk = lambda shape, dt: torch.empty(shape, dtype=dt, device="cuda")
+    out = [dict(idx=mk((T + 1, E, D), torch.uint16), score=mk((T + 1, E), torch.float64), actions=mk((T, E, D), torch.int8),
+                logp=mk((T, E), torch.float64), value=mk((T, E), torch.float64)) for _ in specs]
+    for _ in range(3):
+        run_episodes_batch(tasks, T, ctx, host_out=out, step_major=True)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cs)
+        run_episodes_batch(tasks, T, ctx, host_out=out, step_major=True)
+        b.record(cs)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    n = len(specs) * E * T
+    return {"workload": f"resnet18 {len(specs)} tasks x {E} episodes (= {len(specs) * E} configs/step in total) x "
+                        f"{T} steps, device buffers", "ms": ms, "value": n / (ms * 1e-3), "unit": "config-steps/s",
+            "note": "per SM only ~28 episodes: latency-bound (every step's chain runs at 1 slot per SM)"}
 
 
 def c5_secondary(ctx, args):
@@ -950,6 +1030,13 @@ def main():
         except Exception as ex:  # reported, not hidden
             c3 = {"error": repr(ex)}
 
+    c2t = None
+    if rank == 0 and world == 1:
+        try:
+            ctx.set_stream(stream.cuda_stream)
+            c2t = c2_total_secondary(ctx, args)
+        except Exception as ex:  # reported, not hidden
+            c2t = {"error": repr(ex)}
     kmeans = None
     if not args.no_kmeans and (world == 1 or args.kmeans_dist):
         # N > 1: the sharded k-means runs inside the C3 pipeline above; this 1M-point
@@ -1017,6 +1104,7 @@ def main():
             "sa_baseline": sa,
             "candidates": cand,
             "c1": c1,
+            "c2_total_4096": c2t,
             "ppo_update": ppo,
         }
         print(json.dumps(line), flush=True)

@@ -322,29 +322,33 @@ def test_rollout_tc_planted_draws(O, ctx):
 
 
 def test_rollout_tc_check_mode_c2_shape(O, ctx):
-    """The bench's shape (BASELINE configs[1]: 12 ResNet-18 tasks x 4096 episodes, one grouped
-    launch) at T = 64 in check mode: all 25.2M knob decisions re-decided exactly, 0
-    disagreements, the fast probabilities well inside the margin; the trajectories equal
-    the exact fp64 kernel's, and spot episodes replay on the oracle."""
+    """The bench's FULL shape (BASELINE configs[1]: 12 ResNet-18 tasks x 4096 episodes x T = 500,
+    one grouped launch) in check mode: all 196.6M knob decisions re-decided exactly, 0
+    disagreements, the fast probabilities well inside the margin; the trajectories (device
+    buffers, step-major) equal the normal run's and the exact fp64 kernel's, and spot episodes
+    replay on the oracle."""
+    import torch
     from paper_2001_08743_b200 import _lib as L
     from paper_2001_08743_b200 import spaces as S
     from paper_2001_08743_b200.context import Space
     from paper_2001_08743_b200.cost_model import DeviceGbt
     from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
     from paper_2001_08743_b200.spaces import stream_seed
-    E, T = 4096, 64
+    E, T = 4096, 500
     tasks, orc = [], []
     for i, sp in enumerate(S.resnet18_tasks()):
         osp, og, pm = fitted(O, sp, seed=200 + i)
         ds = Space(sp, ctx)
         agent = ActorCritic(sp.num_knobs, 128, 64, seed=200 + i, ctx=ctx)
         init = osp.random_valid(i, E) if O.ref_available() else np.zeros((E, sp.num_knobs), np.int32)
-        tasks.append(RolloutTask(ds, agent, DeviceGbt(pm, ds), init, episode_offset=0, root_seed=i))
+        tasks.append(RolloutTask(ds, agent, DeviceGbt(pm, ds), torch.from_numpy(init).cuda(), episode_offset=0,
+                                 root_seed=i))
         orc.append((osp, og, agent, init))
     ctx.reset_stats()
     ctx.set_option(L.OPT_ROLLOUT_CHECK, 1)
     try:
-        chk = run_episodes_batch(tasks, T)
+        chk = run_episodes_batch(tasks, T, step_major=True)
+        torch.cuda.synchronize()
     finally:
         ctx.set_option(L.OPT_ROLLOUT_CHECK, 0)
     assert ctx.stat(L.STAT_ROLLOUT_CHECKED) == 12 * E * T * 8
@@ -353,12 +357,14 @@ def test_rollout_tc_check_mode_c2_shape(O, ctx):
     print(f"C2 shape: max |p_fast - p_exact| = {maxerr:.3e} over {12 * E * T * 8} decisions")
     assert maxerr < 2 ** -18
     ctx.reset_stats()
-    fast = run_episodes_batch(tasks, T)
-    exact = run_episodes_batch(tasks, T, exact=True)
+    fast = run_episodes_batch(tasks, T, step_major=True)
+    exact = run_episodes_batch(tasks, T, exact=True, step_major=True)
+    torch.cuda.synchronize()
+    close = lambda a, b: bool(((a - b).abs() <= 1e-5 * b.abs().clamp_min(1.0)).all())
     for f, c, x in zip(fast, chk, exact):
         for k in ("idx", "actions", "score"):
-            assert np.array_equal(f[k], x[k]) and np.array_equal(c[k], x[k]), k
-        assert _close(f["logp"], x["logp"]) and _close(f["value"], x["value"])
+            assert torch.equal(f[k], x[k]) and torch.equal(c[k], x[k]), k
+        assert close(f["logp"], x["logp"]) and close(f["value"], x["value"])
     # the live margin monitor of the normal run: every fallback re-decision inside the margin
     assert ctx.stat(L.STAT_ROLLOUT_FALLBACKS) > 0 and ctx.stat(L.STAT_ROLLOUT_MAXERR) * 1e-12 < 2 ** -18
     g = np.random.default_rng(5)
@@ -366,9 +372,11 @@ def test_rollout_tc_check_mode_c2_shape(O, ctx):
         osp, og, agent, init = orc[i]
         for e in g.choice(E, 2, replace=False):
             w = O.run_episodes(osp, og, 128, 64, agent.params, init[e:e + 1], T, int(e), stream_seed(int(i), "explore"))
-            assert np.array_equal(fast[i]["idx"][e].astype(np.int32), w["idx"][0])
-            assert np.array_equal(fast[i]["actions"][e], w["actions"][0])
-            assert np.array_equal(fast[i]["score"][e], w["score"][0])
+            assert np.array_equal(fast[i]["idx"][:, e].cpu().numpy().astype(np.int32), w["idx"][0])
+            assert np.array_equal(fast[i]["actions"][:, e].cpu().numpy(), w["actions"][0])
+            assert np.array_equal(fast[i]["score"][:, e].cpu().numpy(), w["score"][0])
+    del chk, fast, exact
+    torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("exact", [False, True])
