@@ -204,10 +204,38 @@ __global__ void __launch_bounds__(256) gbt_predict_idx_kernel(
 // persistent grid over kScoreCfg*256-config chunks, trees + knob-index columns in smem.
 constexpr int kScoreThreads = 256;
 constexpr int kScoreCfg = 3;  // configurations per thread (independent walks in flight)
+// One launch scores up to kScoreJobs (model, rows) jobs: CTAs [cta_base, cta_base + ctas) serve job j
+// (every task of a grouped rollout at once: one tail instead of one per task).
+constexpr int kScoreJobs = 16;
+struct ScoreJob {
+  const void* idx;
+  int64_t B;
+  int32_t D, T;
+  const uint32_t* node;
+  const double* leaf;
+  double base, lr;
+  double* out;
+  kt::RowMap map;
+  int32_t cta_base, ctas;
+};
+struct ScoreLaunch {
+  int32_t njobs;
+  ScoreJob job[kScoreJobs];
+};
 template <class IdxT, int DEPTH>
-__global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
-    const IdxT* __restrict__ idx, int64_t B, int D, int T, const uint32_t* __restrict__ g_node,
-    const double* __restrict__ g_leaf, double base, double lr, double* __restrict__ out, kt::RowMap map) {
+__global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(const __grid_constant__ ScoreLaunch SL) {
+  int ji = 0;
+  while (ji + 1 < SL.njobs && SL.job[ji + 1].cta_base <= (int)blockIdx.x) ++ji;
+  const ScoreJob& J = SL.job[ji];
+  const IdxT* __restrict__ idx = reinterpret_cast<const IdxT*>(J.idx);
+  const int64_t B = J.B;
+  const int D = J.D, T = J.T;
+  const uint32_t* __restrict__ g_node = J.node;
+  const double* __restrict__ g_leaf = J.leaf;
+  const double base = J.base, lr = J.lr;
+  double* __restrict__ out = J.out;
+  const kt::RowMap map = J.map;
+  const int64_t cta = (int)blockIdx.x - J.cta_base, nctas = J.ctas;
   constexpr int NI = (1 << DEPTH) - 1, NL = 1 << DEPTH;
   constexpr int NIP = (NI + 3) & ~3;  // node words per tree, padded: every tree starts 16-byte aligned
   extern __shared__ __align__(16) unsigned char smem[];
@@ -232,7 +260,7 @@ __global__ void __launch_bounds__(kScoreThreads) gbt_score_kernel(
   const uint32_t col0 = (uint32_t)(reinterpret_cast<const unsigned char*>(s_idx + threadIdx.x) - sb);
   auto ld32 = [&](uint32_t a) { return *reinterpret_cast<const uint32_t*>(sb + a); };
   constexpr int NC = kScoreCfg;
-  for (int64_t c0 = (int64_t)blockIdx.x * NC * kScoreThreads; c0 < B; c0 += (int64_t)gridDim.x * NC * kScoreThreads) {
+  for (int64_t c0 = cta * NC * kScoreThreads; c0 < B; c0 += nctas * NC * kScoreThreads) {
     int64_t row[NC];
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
@@ -359,13 +387,15 @@ void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_id
     if (smem <= 200 * 1024) {
       const int per_sm = std::max(1, std::min(8, (int)((220 * 1024) / smem)));
       const int grid = (int)std::min<int64_t>(ceil_div(B, kScoreCfg * kScoreThreads), (int64_t)sm_count(ctx) * per_sm);
+      ScoreLaunch SL{};
+      SL.njobs = 1;
+      SL.job[0] = ScoreJob{d_idx, B, g->D, g->num_trees, g->d_inode_pk, g->d_leaf, g->base, g->lr, d_out, map, 0, grid};
       kt::ProfScope prof(ctx, KTUNE_STAT_GBT_NS);
 #define KT_SCORE(T_, DEP)                                                                                    \
   {                                                                                                          \
     auto kern = gbt_score_kernel<T_, DEP>;                                                                   \
     KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
-    kern<<<grid, kScoreThreads, smem, ctx->stream>>>((const T_*)d_idx, B, g->D, g->num_trees, g->d_inode_pk, \
-                                                     g->d_leaf, g->base, g->lr, d_out, map);                 \
+    kern<<<grid, kScoreThreads, smem, ctx->stream>>>(SL);                                                    \
   }
 #define KT_SCORE_D(T_)                         \
   switch (g->depth) {                          \
@@ -405,6 +435,68 @@ void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_id
                                             g->d_inode_idx, g->d_leaf, g->base, g->lr, d_out, use_smem);
   }
   check_launch(ctx, "gbt_predict_idx");
+}
+
+// Several (model, rows) jobs in ONE K1 launch when they share the tree depth and index width
+// (the rollout's tasks): CTAs split in proportion to the rows, so the launch has one tail
+// instead of one per task (each per-task launch ran ceil(rounds) of ~3 rounds of chunks).
+void gbt_predict_idx_device_multi(ktune_ctx* ctx, const std::vector<GbtJob>& jobs, int idx_bytes) {
+  std::vector<GbtJob> live;
+  for (const GbtJob& j : jobs)
+    if (j.B > 0) live.push_back(j);
+  if (live.empty()) return;
+  bool same = live.size() <= (size_t)kScoreJobs;
+  size_t smem = 0;
+  for (const GbtJob& j : live) {
+    const ktune_gbt* g = j.g;
+    same = same && g->d_inode_pk && g->has_space && g->complete && g->depth == live[0].g->depth &&
+           g->D == live[0].g->D;
+    const int ni = (1 << g->depth) - 1, nl = 1 << g->depth;
+    smem = std::max(smem, (size_t)g->num_trees * (((ni + 3) & ~3) * 4 + nl * 8) + 16 +
+                              (size_t)kScoreCfg * g->D * kScoreThreads * 4);
+  }
+  if (!same || smem > 200 * 1024) {
+    for (const GbtJob& j : live) gbt_predict_idx_device(ctx, j.g, j.idx, idx_bytes, j.B, j.out, j.map);
+    return;
+  }
+  const int per_sm = std::max(1, std::min(8, (int)((220 * 1024) / smem)));
+  const int64_t slots = (int64_t)sm_count(ctx) * per_sm;
+  int64_t rows = 0;
+  for (const GbtJob& j : live) rows += j.B;
+  ScoreLaunch SL{};
+  SL.njobs = (int)live.size();
+  int ctas = 0;
+  for (size_t q = 0; q < live.size(); ++q) {
+    const GbtJob& j = live[q];
+    const ktune_gbt* g = j.g;
+    const int64_t chunks = ceil_div(j.B, kScoreCfg * kScoreThreads);
+    const int c = (int)std::max<int64_t>(1, std::min<int64_t>(chunks, (slots * j.B + rows - 1) / rows));
+    SL.job[q] = ScoreJob{j.idx, j.B, g->D, g->num_trees, g->d_inode_pk, g->d_leaf, g->base, g->lr, j.out, j.map, ctas, c};
+    ctas += c;
+  }
+  kt::ProfScope prof(ctx, KTUNE_STAT_GBT_NS);
+#define KT_SCORE(T_, DEP)                                                                         \
+  {                                                                                               \
+    auto kern = gbt_score_kernel<T_, DEP>;                                                        \
+    KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    kern<<<ctas, kScoreThreads, smem, ctx->stream>>>(SL);                                         \
+  }
+#define KT_SCORE_D(T_)                         \
+  switch (live[0].g->depth) {                  \
+    case 0: KT_SCORE(T_, 0) break;             \
+    case 1: KT_SCORE(T_, 1) break;             \
+    case 2: KT_SCORE(T_, 2) break;             \
+    case 3: KT_SCORE(T_, 3) break;             \
+    case 4: KT_SCORE(T_, 4) break;             \
+    case 5: KT_SCORE(T_, 5) break;             \
+    case 6: KT_SCORE(T_, 6) break;             \
+    case 7: KT_SCORE(T_, 7) break;             \
+    default: KT_SCORE(T_, 8) break;            \
+  }
+  if (idx_bytes == 1) KT_SCORE_D(uint8_t) else KT_SCORE_D(uint16_t)
+#undef KT_SCORE_D
+#undef KT_SCORE
+  check_launch(ctx, "gbt_score");
 }
 
 }  // namespace kt

@@ -218,6 +218,15 @@ struct RowMap {
 };
 void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_idx, int idx_bytes, int64_t B,
                             double* d_out, RowMap map = RowMap());
+struct GbtJob {
+  const ktune_gbt* g;
+  const void* idx;
+  int64_t B;
+  double* out;
+  RowMap map;
+};
+// the jobs in one K1 launch (same depth and knob count; else one launch per job)
+void gbt_predict_idx_device_multi(ktune_ctx* ctx, const std::vector<GbtJob>& jobs, int idx_bytes);
 // One rollout workload with device pointers (shared by the exact and the
 // tcgen05 rollout kernels).
 struct RolloutWork {

@@ -697,23 +697,24 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
                                                   : (int)std::min<int64_t>(8, std::max<int64_t>(2, T / 125));
     if (segmented && !ctx->copy_stream) KT_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     std::vector<cudaEvent_t> events;
-    auto score_rows = [&](int k, int r0, int r1) {  // trajectory rows [r0, r1] of every episode
+    std::vector<kt::GbtJob> jobs;
+    auto score_rows = [&](int k, int r0, int r1) {  // queue trajectory rows [r0, r1] of every episode
       const ktune_rollout_task& t = tasks[k];
       if (!t.gbt || !io[k].d_score || t.num_episodes == 0) return;
       const int64_t len = r1 - r0 + 1, E = t.num_episodes;
       if (grouped) {  // this task's columns of rows r0..r1: blocks of E every Etot
-        kt::gbt_predict_idx_device(ctx, t.gbt, io[0].d_idx, 2, E * len, io[0].d_score,
-                                   kt::RowMap{E, Etot, r0 * Etot + goff[k]});
-        return;
+        jobs.push_back({t.gbt, io[0].d_idx, E * len, io[0].d_score, kt::RowMap{E, Etot, r0 * Etot + goff[k]}});
+      } else if (stepm) {  // rows r0..r1 of every episode are one contiguous block
+        jobs.push_back({t.gbt, io[k].d_idx + r0 * E * t.ac->n, E * len, io[k].d_score + r0 * E, kt::RowMap()});
+      } else {
+        kt::RowMap m;
+        if (len != T + 1) m = kt::RowMap{len, (int64_t)T + 1, r0};
+        jobs.push_back({t.gbt, io[k].d_idx, E * len, io[k].d_score, m});
       }
-      if (stepm) {  // rows r0..r1 of every episode are one contiguous block
-        kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx + r0 * E * t.ac->n, 2, E * len, io[k].d_score + r0 * E);
-        return;
-      }
-      kt::RowMap m;
-      if (len != T + 1) m = kt::RowMap{len, (int64_t)T + 1, r0};
-      kt::gbt_predict_idx_device(ctx, t.gbt, io[k].d_idx, 2, E * len, io[k].d_score, m);
-
+    };
+    auto flush_scores = [&]() {  // every queued task in one K1 launch
+      kt::gbt_predict_idx_device_multi(ctx, jobs, 2);
+      jobs.clear();
     };
     auto score32_rows = [&](int k, int r0, int r1) {  // fp32 copies of the scores of rows [r0, r1]
       const ktune_rollout_task& t = tasks[k];
@@ -852,6 +853,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
             kt::rollout_tc(ctx, work, T, t0, t1);
           }
           for (int k = 0; k < num_tasks; ++k) score_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
+          flush_scores();
           for (int k = 0; k < num_tasks; ++k) {  // after every task's scores (grouped: one pass for all)
             score32_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
             narrow_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
@@ -904,6 +906,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     // cost-model scores of every visited configuration (K1 over the trajectory)
     for (int k = 0; k < num_tasks; ++k)
       if (!scored[k]) score_rows(k, 0, T);
+    flush_scores();
     for (int k = 0; k < num_tasks; ++k) {  // after every task's scores (grouped: one pass for all)
       score32_rows(k, 0, T);
       narrow_rows(k, 0, T);
