@@ -773,7 +773,7 @@ def main():
         else:
             dist.init_process_group(backend)
     from paper_2001_08743_b200 import _lib as L
-    from paper_2001_08743_b200.context import Context, Space
+    from paper_2001_08743_b200.context import Space
     from paper_2001_08743_b200.cost_model import DeviceGbt, fit_gbt
     from paper_2001_08743_b200.exploration import ActorCritic, RolloutTask, run_episodes_batch
     from workloads.tasks import encode

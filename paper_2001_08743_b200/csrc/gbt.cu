@@ -374,11 +374,7 @@ void gbt_predict_idx_device(ktune_ctx* ctx, const ktune_gbt* g, const void* d_id
   if (!map.identity() && !g->d_inode_pk) fail(KTUNE_ERR_CONFIG, "cost model: strided scoring needs the K1 layout");
   if (!g->has_space) fail(KTUNE_ERR_CONFIG, "cost model: uploaded without a design space; use predict_features");
   const int threads = 256;
-  if (!g->complete) {
-    int32_t* d_lut_off = (int32_t*)ctx->dev(WS_SCRATCH2, sizeof(int32_t) * (kMaxKnobs + 1));
-    fail(KTUNE_ERR_CONFIG, "cost model: trees deeper than 8 levels are not supported on the index path");
-    (void)d_lut_off;
-  }
+  if (!g->complete) fail(KTUNE_ERR_CONFIG, "cost model: trees deeper than 8 levels are not supported on the index path");
   const int ni = (1 << g->depth) - 1, nl = 1 << g->depth;
   const size_t tree_bytes = (size_t)g->num_trees * (ni * 4 + nl * 8);
   if (g->d_inode_pk) {  // K1 fast path (node words padded to a multiple of 4 per tree)
