@@ -694,7 +694,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     if (ctx->opt_rollout_segments == 1) segmented = false;
     const int S = !segmented ? 1
                   : ctx->opt_rollout_segments > 1 ? (int)std::min<int64_t>(ctx->opt_rollout_segments, T)
-                                                  : (int)std::min<int64_t>(8, std::max<int64_t>(2, T / 125));
+                                                  : (int)std::min<int64_t>(16, std::max<int64_t>(2, T / 40));
     if (segmented && !ctx->copy_stream) KT_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     std::vector<cudaEvent_t> events;
     std::vector<kt::GbtJob> jobs;

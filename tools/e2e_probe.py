@@ -43,7 +43,7 @@ for seg in [int(x) for x in os.environ.get("SEGS", "0").split(",")]:
         ms = 1e3 * np.median(ts)
         print(f"segs {seg} grouped step-major score {'f64' if s64 else 'f32'}: {ms:.2f} ms/step, "
               f"{12 * E * T / ms * 1e3:.3e} config-steps/s, D2H {bo / 1e9:.3f} GB ({bo / ms / 1e6:.1f} GB/s)", flush=True)
-    for step_major in (False, True):
+    for step_major in (() if os.environ.get("GROUPED_ONLY") else (False, True)):
         for s64 in (False, True):
             sh = lambda rows, *rest: ((rows, E) if step_major else (E, rows)) + rest
             small = [max(s.space.cards) <= 256 for s in specs]
