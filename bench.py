@@ -686,29 +686,32 @@ def c5_secondary(ctx, args):
     cards = torch.tensor(sp.cards, device="cuda")
     init = (torch.rand((E, 16), device="cuda", generator=gen) * cards).to(torch.int32).to(torch.uint16)
     mk = lambda shape, dt: torch.empty(shape, dtype=dt, device="cuda")
-    out = [dict(idx=mk((E, T + 1, 16), torch.uint16), score=mk((E, T + 1), torch.float64), actions=None,
+    cs = torch.cuda.current_stream()
+    ctx.set_stream(cs.cuda_stream)
+    # step-major trajectories (coalesced stores), like the headline
+    out = [dict(idx=mk((T + 1, E, 16), torch.uint16), score=mk((T + 1, E), torch.float64), actions=None,
                 logp=None, value=None)]
     task = RolloutTask(ds, agent, g, init, 0, spec.seed, want_trajectory=False)
-    run_episodes_batch([task], 8, ctx, host_out=[dict(idx=mk((E, 9, 16), torch.uint16),
-                                                      score=mk((E, 9), torch.float64), actions=None, logp=None,
-                                                      value=None)])  # warm-up
+    run_episodes_batch([task], 8, ctx, host_out=[dict(idx=mk((9, E, 16), torch.uint16),
+                                                      score=mk((9, E), torch.float64), actions=None, logp=None,
+                                                      value=None)], step_major=True)  # warm-up
     torch.cuda.synchronize()
     ctx.set_option(L.OPT_PROFILE, 1)
     ctx.reset_stats()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    run_episodes_batch([task], T, ctx, host_out=out)
-    b.record()
+    a.record(cs)
+    run_episodes_batch([task], T, ctx, host_out=out, step_major=True)
+    b.record(cs)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
     roll = ctx.stat(L.STAT_ROLLOUT_NS) / 1e6
     fb, steps = ctx.stat(L.STAT_ROLLOUT_FALLBACKS), ctx.stat(L.STAT_ROLLOUT_TC)
     ctx.set_option(L.OPT_PROFILE, 0)
     idx = out[0]["idx"]
-    smp = idx[:: max(1, E // 4096)].to(torch.int32)  # properties on a 4096-episode sample
+    smp = idx[:, :: max(1, E // 4096)].to(torch.int32)  # properties on a 4096-episode sample (step-major)
     ok_range = bool((smp.amax(dim=(0, 1)) < cards).all())
-    moves = (smp[:, 1:] - smp[:, :-1]).abs().amax().item()
-    res = {"workload": "synthetic16 (SURVEY C5), 1M configs x 1000 steps, 1 GPU, device buffers",
+    moves = (smp[1:] - smp[:-1]).abs().amax().item()
+    res = {"workload": "synthetic16 (SURVEY C5), 1M configs x 1000 steps, 1 GPU, device buffers (step-major)",
            "config_steps": E * T, "ms": ms, "value": E * T / (ms * 1e-3), "unit": "config-steps/s",
            "rollout_kernel_ms": roll, "fallbacks_per_config_step": fb / max(1, steps),
            "properties": {"idx_in_range": ok_range, "max_move_per_knob": int(moves)}}
@@ -1089,7 +1092,14 @@ def main():
                 "frac": (len(specs) * E * T * sfu_ops_per_config_step(n_knobs) / roll_s) /
                         (SFU_OPS_PER_SM_CLK * sm_count * (clocks.get("sm_mhz") or 1965.0) * 1e6),
                 "ops_per_config_step": sfu_ops_per_config_step(n_knobs),
-                "note": "MUFU ex2/rcp/lg2 at 16/SM/clk at the sampled SM clock: the unit that bounds K2-TC"},
+                # round 1 issued 552 SFU ops per config-step (one reciprocal per tanh); the same
+                # throughput expressed in that work unit, for comparison across rounds
+                "frac_in_round1_ops": (len(specs) * E * T * 552 / roll_s) /
+                                      (SFU_OPS_PER_SM_CLK * sm_count * (clocks.get("sm_mhz") or 1965.0) * 1e6),
+                "note": "MUFU ex2/rcp/lg2 at 16/SM/clk at the sampled SM clock: the unit that bounds K2-TC; "
+                        "a pair of tanh units shares one reciprocal (3 MUFU per 2 units), and the activation "
+                        "microbenchmark (tools/act_probe.cu) runs one warp at 18 cycles/unit against the "
+                        "12-cycle SFU floor of that sequence"},
             "rollout_fallbacks": {"knob_decisions_redecided_exactly": fallbacks, "config_steps": tc_steps,
                                   "per_config_step": fallbacks / max(1, tc_steps)},
             "gbt_kernel_ms_per_step": gbt_ns / max(1, gbt_calls) * 1e-6 * len(specs),
