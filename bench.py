@@ -1102,7 +1102,7 @@ def main():
                         "12-cycle SFU floor of that sequence"},
             "rollout_fallbacks": {"knob_decisions_redecided_exactly": fallbacks, "config_steps": tc_steps,
                                   "per_config_step": fallbacks / max(1, tc_steps)},
-            "gbt_kernel_ms_per_step": gbt_ns / max(1, gbt_calls) * 1e-6 * len(specs),
+            "gbt_kernel_ms_per_step": gbt_ns * 1e-6 / (args.steps + 1),  # deltas cover the ramp + K steps
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
