@@ -36,6 +36,7 @@ torch.cuda.synchronize()
 ref = [{k: v.clone() for k, v in o.items()} for o in out] if chk else None
 ctx.set_option(L.OPT_PROFILE, 1)
 if chk: ctx.set_option(L.OPT_ROLLOUT_CHECK, chk)
+if os.environ.get("FUSE"): ctx.set_option(L.OPT_ROLLOUT_FUSE_GBT, int(os.environ["FUSE"]))
 if os.environ.get("DELTA"):  # the certification band in probability units
     ctx.set_option(L.OPT_ROLLOUT_DELTA, int(float(os.environ["DELTA"]) * 1e12))
 
