@@ -71,6 +71,25 @@ __device__ __forceinline__ void load_feats(const KtSpaceParams& sp, const double
   for (int d = 0; d < DM; ++d) x[d] = d < D ? feat(sp, lut_s, p, d) : 0.0;
 }
 
+// Raw 8-knob row (one 16- or 8-byte load) and its features: the split lets a loop issue the
+// next point's loads before it works on the current one (fast path of load_feats).
+template <class IdxT>
+__device__ __forceinline__ uint4 load_row8(const IdxT* p) {
+  if (sizeof(IdxT) == 2) return __ldg(reinterpret_cast<const uint4*>(p));
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+  return make_uint4(v.x, v.y, 0u, 0u);
+}
+template <class IdxT, int DM>
+__device__ __forceinline__ void feats_row8(const KtSpaceParams& sp, const double* lut_s, uint4 v, double (&x)[DM]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int d = 0; d < 8; ++d)
+    x[d] = sizeof(IdxT) == 2 ? lut_s[sp.lut_off[d] + (int)((w[d >> 1] >> (16 * (d & 1))) & 0xFFFFu)]
+                             : lut_s[sp.lut_off[d] + (int)((w[d >> 2] >> (8 * (d & 3))) & 0xFFu)];
+#pragma unroll
+  for (int d = 8; d < DM; ++d) x[d] = 0.0;
+}
+
 // Sequential squared distance.
 template <class IdxT>
 __device__ __forceinline__ double row_d2(const KtSpaceParams& sp, const double* lut, const IdxT* p,
@@ -552,15 +571,31 @@ __global__ void __launch_bounds__(kCertBT) assign_cert_kernel(
   double part = 0.0;
   int nchg = 0, nunc = 0;
   const double grow = (double)(2 * D + 4) * 0x1.0p-53;
+  // 8-knob rows: the next point's row and previous assignment are loaded one iteration ahead
+  // (their global-load latency was the kernel's top stall at small k)
+  const bool row8 = DM == 8 && D == 8;
+  uint4 raw_n = make_uint4(0u, 0u, 0u, 0u);
+  int prev_n = 0;
+  if (row8 && base + threadIdx.x < N) {
+    raw_n = load_row8<IdxT>(pts + (base + threadIdx.x) * 8);
+    if (prev) prev_n = __ldg(prev + base + threadIdx.x);
+  }
   for (int j = 0; j < kChunk / kCertBT; ++j) {
     const int64_t i = base + j * kCertBT + threadIdx.x;
     const bool live = i < N;
     int bc = 0;
+    const uint4 raw = raw_n;
+    const int prev_i = prev_n;
+    if (row8 && j + 1 < kChunk / kCertBT && i + kCertBT < N) {
+      raw_n = load_row8<IdxT>(pts + (i + kCertBT) * 8);
+      if (prev) prev_n = __ldg(prev + i + kCertBT);
+    }
     if (live) {
       // (1) fp32 screening: the winner is certified if the runner-up's interval lies
       // strictly above the winner's: s2 (1 - R) - A > s1 (1 + R) + A
       double x[DM];  // DM >= D, compile-time: the features stay in registers
-      load_feats<IdxT, DM>(sp, lut, pts + i * D, D, x);
+      if (row8) feats_row8<IdxT, DM>(sp, lut, raw, x);
+      else load_feats<IdxT, DM>(sp, lut, pts + i * D, D, x);
       float xf[DM];
 #pragma unroll
       for (int d = 0; d < DM; ++d) xf[d] = (float)x[d];  // padded knobs add 0 exactly
@@ -633,7 +668,7 @@ __global__ void __launch_bounds__(kCertBT) assign_cert_kernel(
       asg[i] = bc;
       d2[i] = best;
       part = kt::dadd(part, best);
-      const int pc = prev ? prev[i] : bc;
+      const int pc = prev ? (row8 ? prev_i : prev[i]) : bc;
       if (pc != bc) {  // move this point's indices between the clusters' integer sums
         ++nchg;
         if (g_sum) {
