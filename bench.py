@@ -887,64 +887,68 @@ def main():
             h[:] = s.init_idx
         D = n_knobs
         # logp / value as fp32: the tcgen05 path computes both in fp32, so shipping
-        # them as doubles would only add PCIe bytes
-        # and the visited configurations as uint8 wherever every cardinality fits (the API's idx_u8);
-        # scores as fp32 (north star: scores within 1e-5 relative in fp32; the device keeps and ranks
-        # candidates on the exact fp64 scores)
-        # grouped step-major layout (KTUNE_F_STEP_MAJOR_GROUPED): all 12 tasks' episodes side by side,
-        # one PCIe copy per output per segment; uint8 configurations for the run of tasks whose
-        # cardinalities fit, uint16 for the rest
+        # them as doubles would only add PCIe bytes; scores as fp32 (north star: scores within 1e-5
+        # relative in fp32; the device keeps and ranks candidates on the exact fp64 scores); grouped
+        # step-major layout (KTUNE_F_STEP_MAJOR_GROUPED): all 12 tasks' episodes side by side, one
+        # PCIe copy per output per segment; visited configurations as uint32 configuration ids (the API's ids_u32: id_of,
+        # design_space.cpp:158-167; every bench space has < 2^27 configurations), 4 bytes per
+        # configuration instead of D; the knob-index encoding is measured alongside
         from paper_2001_08743_b200.exploration import compact_grouped_outputs
-        tdt = {np.uint8: torch.uint8, np.uint16: torch.int16, np.float32: torch.float32, np.float64: torch.float64}
-        palloc = lambda shape, dt: pinned(shape, tdt[dt]).view(dt) if dt == np.uint16 else pinned(shape, tdt[dt])
+        tdt = {np.uint8: torch.uint8, np.uint16: torch.int16, np.uint32: torch.int32, np.float32: torch.float32,
+               np.float64: torch.float64}
+        palloc = lambda shape, dt: (pinned(shape, tdt[dt]).view(dt) if dt in (np.uint16, np.uint32)
+                                    else pinned(shape, tdt[dt]))
         htasks = [RolloutTask(d, a, g, hi, episode_offset=rank * E, root_seed=s.seed)
                   for s, d, a, g, hi in zip(specs, spaces, agents, gbts, host_init)]
         GRP = SM  # the grouped layout is the step-major layout over all tasks at once
-        host_out = (compact_grouped_outputs(htasks, T, palloc) if GRP else
-                    [dict(idx=None if max(s.space.cards) <= 256 else pinned(sh(T + 1, D), torch.int16).view(np.uint16),
-                          idx8=pinned(sh(T + 1, D), torch.uint8) if max(s.space.cards) <= 256 else None,
-                          score=None, score32=pinned(sh(T + 1), torch.float32), actions=None,
-                          actions2=pinned(sh(T, (D + 3) // 4), torch.uint8), logp=None, value=None,
-                          logp32=pinned(sh(T), torch.float32), value32=pinned(sh(T), torch.float32)) for s in specs])
+
+        def outputs(ids, full):
+            if GRP:
+                return compact_grouped_outputs(htasks, T, palloc, score64=full, logp64=full, ids=ids)
+            outs = []
+            for s in specs:
+                small = max(s.space.cards) <= 256 and not ids
+                o = dict(idx=None if small or ids else palloc(sh(T + 1, D), np.uint16),
+                         idx8=pinned(sh(T + 1, D), torch.uint8) if small else None,
+                         ids32=palloc(sh(T + 1), np.uint32) if ids else None,
+                         actions=None, actions2=pinned(sh(T, (D + 3) // 4), torch.uint8))
+                f = np.float64 if full else np.float32
+                o.update({("score" if full else "score32"): palloc(sh(T + 1), f),
+                          ("logp" if full else "logp32"): palloc(sh(T), f),
+                          ("value" if full else "value32"): palloc(sh(T), f)})
+                for k in ("score", "logp", "value"):
+                    o.setdefault(k, None)
+                outs.append(o)
+            return outs
+
+        def timed(host_out):
+            run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact, step_major=SM, grouped=GRP)  # warm
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact, step_major=SM, grouped=GRP)
+            barrier()
+            dt = time.perf_counter() - t0
+            if world > 1:
+                dt = allreduce_max(dt)
+            return (units_per_step * args.steps / dt,
+                    sum(sum(v.nbytes for v in o.values() if v is not None) for o in host_out))
+
         ctx.set_stream(None)
-        run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact, step_major=SM, grouped=GRP)  # warm
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            run_episodes_batch(htasks, T, ctx, host_out=host_out, exact=args.exact, step_major=SM, grouped=GRP)
-        barrier()
-        dt = time.perf_counter() - t0
-        if world > 1:
-            dt = allreduce_max(dt)
         bi = sum(h.nbytes for h in host_init)
-        bo = sum(sum(v.nbytes for v in o.values() if v is not None) for o in host_out)
-        e2e = {"value": units_per_step * args.steps / dt, "unit": "config-steps/s", "h2d_bytes_per_step": bi,
-               "d2h_bytes_per_step": bo,
-               "outputs": "idx as uint8 (uint16 where a cardinality > 256), score fp32 (1e-5 rel.), actions 2-bit, "
+        v, bo = timed(outputs(True, False))
+        e2e = {"value": v, "unit": "config-steps/s", "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+               "outputs": "configurations as uint32 ids (id_of), score fp32 (1e-5 rel.), actions 2-bit, "
                           "logp/value fp32 (what the tcgen05 path computes)",
                "layout": "grouped step-major (one array per output over all tasks)" if GRP else "per task"}
-        # the same call with full-precision outputs: fp64 scores, fp64 logp/value (0.84 GB/step)
-        del host_out
-        full_out = (compact_grouped_outputs(htasks, T, palloc, score64=True, logp64=True) if GRP else
-                    [dict(idx=None if max(s.space.cards) <= 256 else pinned(sh(T + 1, D), torch.int16).view(np.uint16),
-                          idx8=pinned(sh(T + 1, D), torch.uint8) if max(s.space.cards) <= 256 else None,
-                          score=pinned(sh(T + 1), torch.float64), actions=None,
-                          actions2=pinned(sh(T, (D + 3) // 4), torch.uint8), logp=pinned(sh(T), torch.float64),
-                          value=pinned(sh(T), torch.float64)) for s in specs])
-        run_episodes_batch(htasks, T, ctx, host_out=full_out, exact=args.exact, step_major=SM, grouped=GRP)  # warm
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            run_episodes_batch(htasks, T, ctx, host_out=full_out, exact=args.exact, step_major=SM, grouped=GRP)
-        barrier()
-        dtf = time.perf_counter() - t0
-        if world > 1:
-            dtf = allreduce_max(dtf)
-        e2e["full_precision"] = {"value": units_per_step * args.steps / dtf, "unit": "config-steps/s",
-                                 "d2h_bytes_per_step": sum(sum(v.nbytes for v in o.values() if v is not None)
-                                                           for o in full_out),
-                                 "outputs": "score fp64, logp/value fp64, idx uint8, actions 2-bit"}
-        del full_out
+        v, bo = timed(outputs(False, False))
+        e2e["knob_indices"] = {"value": v, "unit": "config-steps/s", "d2h_bytes_per_step": bo,
+                               "outputs": "configurations as knob indices: uint8 (uint16 where a cardinality > 256); "
+                                          "score, actions, logp/value as above"}
+        # full-precision outputs: fp64 scores, fp64 logp/value
+        v, bo = timed(outputs(True, True))
+        e2e["full_precision"] = {"value": v, "unit": "config-steps/s", "d2h_bytes_per_step": bo,
+                                 "outputs": "score fp64, logp/value fp64, configuration ids uint32, actions 2-bit"}
         ctx.set_stream(stream.cuda_stream)
 
     # ---- parity at the full bench size (outside the timed region): the tcgen05 path vs the

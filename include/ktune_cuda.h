@@ -108,8 +108,13 @@ enum ktune_option {
   KTUNE_OPT_FORCE_SHARDED = 8,    /* 1: run the multi-GPU k-means path (per-point state all-gathered over
                                      NCCL) even on one rank; needs a context created by
                                      ktune_ctx_create_dist with an ncclUniqueId (tests on one GPU) */
-  KTUNE_OPT_KMEANS_BOUND_LOG2 = 9  /* tests: inflate the certified k-means centroid bounds by 2^value so that
+  KTUNE_OPT_KMEANS_BOUND_LOG2 = 9, /* tests: inflate the certified k-means centroid bounds by 2^value so that
                                      speculative iterations fail and the exact rescue path runs */
+  KTUNE_OPT_ROLLOUT_STREAMED = 10  /* host-buffer rollouts on the tcgen05 path: 0 = auto (ONE rollout launch
+                                     whose slots publish their per-segment progress in device memory; the
+                                     copy stream waits on it with cuStreamWaitValue32 and copies each
+                                     finished segment while the kernel runs on; scores follow in chunks),
+                                     1 = one launch per segment (the pre-streamed path) */
 };
 int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value);
 
@@ -319,6 +324,10 @@ typedef struct {
                                calls may then pass score = NULL): within the 1e-5 relative tolerance the
                                path promises for scores, half the bytes. Candidate ranking on the device
                                always uses the exact fp64 scores. */
+  uint32_t* ids_u32;        /* E x (T+1) configuration ids id_of(Θ_t) (design_space.cpp:158-167: mixed
+                               radix, last knob fastest; config_at inverts it) (may be NULL; needs
+                               |space| <= 2^32). Host-pointer calls may then pass idx = NULL: 4 bytes per
+                               visited configuration cross PCIe instead of D (idx_u8) or 2D (idx) */
 } ktune_rollout_task;
 int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks, int32_t T,
                   int flags);

@@ -20,7 +20,7 @@ F_EXACT_ROLLOUT = 2
 F_STEP_MAJOR = 4
 F_STEP_MAJOR_GROUPED = 8
 OPT_FORCE_EXACT, OPT_KMEANS_MODE, OPT_PROFILE, OPT_ROLLOUT_DELTA, OPT_ROLLOUT_CHECK, OPT_ROLLOUT_FUSE_GBT, \
-    OPT_ROLLOUT_SEGMENTS, OPT_FORCE_SHARDED, OPT_KMEANS_BOUND_LOG2 = 1, 2, 3, 4, 5, 6, 7, 8, 9
+    OPT_ROLLOUT_SEGMENTS, OPT_FORCE_SHARDED, OPT_KMEANS_BOUND_LOG2, OPT_ROLLOUT_STREAMED = 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
 STAT_LAUNCHES, STAT_KPP_FALLBACKS, STAT_DECISION_FALLBACKS, STAT_ASSIGN_FALLBACKS, \
     STAT_SNAP_CHAINS, STAT_LLOYD_ITERS, STAT_KPP_PICKS, STAT_ROLLOUT_NS, STAT_ROLLOUT_CALLS, \
     STAT_GBT_NS, STAT_GBT_CALLS, STAT_ASSIGN_NS, STAT_ASSIGN_CALLS, STAT_XS_SEQUENTIAL, \
@@ -54,7 +54,7 @@ class RolloutTaskC(C.Structure):
     _fields_ = [("space", P), ("ac", P), ("gbt", P), ("num_episodes", i64),
                 ("episode_offset", i64), ("explore_seed", u64), ("init_idx", P), ("idx", P),
                 ("score", P), ("actions", P), ("logp", P), ("value", P), ("logp_f32", P), ("value_f32", P),
-                ("idx_u8", P), ("actions_u2", P), ("score_f32", P)]
+                ("idx_u8", P), ("actions_u2", P), ("score_f32", P), ("ids_u32", P)]
 
 
 class SaParamsC(C.Structure):

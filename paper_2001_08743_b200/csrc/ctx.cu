@@ -254,6 +254,7 @@ int ktune_ctx_destroy(ktune_ctx* ctx) {
   for (auto& b : ctx->ws) b.release();
   for (auto& b : ctx->pinned) b.release();
   if (ctx->d_counters) cudaFree(ctx->d_counters);
+  if (ctx->d_progress) cudaFree(ctx->d_progress);
   kt_nccl_destroy(ctx);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -282,6 +283,7 @@ int ktune_ctx_set_option(ktune_ctx* ctx, int option, int64_t value) {
     else if (option == KTUNE_OPT_ROLLOUT_SEGMENTS) ctx->opt_rollout_segments = value;
     else if (option == KTUNE_OPT_FORCE_SHARDED) ctx->opt_force_sharded = value;
     else if (option == KTUNE_OPT_KMEANS_BOUND_LOG2) ctx->opt_kmeans_bound_log2 = value;
+    else if (option == KTUNE_OPT_ROLLOUT_STREAMED) ctx->opt_rollout_streamed = value;
     else kt::fail(KTUNE_ERR_CONFIG, "unknown option");
   });
 }

@@ -98,6 +98,10 @@ struct ktune_ctx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // D2H of segmented rollouts, overlapping the compute
+  unsigned int* d_progress = nullptr;  // streamed rollouts: per segment, the slots that finished it
+  void* fn_wait_value = nullptr;       // cuStreamWaitValue32 (driver entry point), resolved once
+  int wait_value_state = 0;            // 0 unresolved, 1 available, -1 unavailable
+  int64_t opt_rollout_streamed = 0;    // 0 auto (streamed when available), 1 off
   std::string last_error;
   int64_t opt_force_exact = 0;
   int64_t opt_force_sharded = 0;
@@ -182,6 +186,11 @@ struct ktune_ac {
   int64_t num_params = 0;
   double* d_params = nullptr;
   std::vector<double> host_params;
+  uint64_t version = 1;  // bumped whenever host_params change (ppo_update)
+  // tcgen05 rollout: power-of-two weight scales for (version, space), computed once
+  mutable uint64_t scale_version = 0;
+  mutable const ktune_space* scale_space = nullptr;
+  mutable int scale_e[3] = {0, 0, 0};
 };
 
 namespace kt {
@@ -244,6 +253,9 @@ struct RolloutWork {
   double* score;         // E x (T+1), may be NULL
   float* logp32 = nullptr;   // fp32 copies (may be NULL)
   float* value32 = nullptr;
+  uint8_t* idx8 = nullptr;   // compact outputs written by the tcgen05 rollout (may be NULL):
+  uint32_t* ids = nullptr;   //   uint8 rows (idx layout), configuration ids (score layout),
+  uint8_t* act2 = nullptr;   //   2-bit direction codes (actions layout, ceil(n/4) bytes per step)
   bool scored = false;   // set by rollout_tc when the scores were fused into the rollout
   // trajectory layout in rows: (e, t) of idx/score at e*sE + t*sT, of actions/logp/value at
   // e*aE + t*aT (episode-major: T+1, 1, T, 1; step-major, KTUNE_F_STEP_MAJOR: 1, E, 1, E)
@@ -252,7 +264,11 @@ struct RolloutWork {
 // tcgen05 rollout (rollout_tc.cu): eligibility (h = 128, g = 64, n <= 21,
 // cardinalities <= 2049, representable weight scales) and the launch.
 bool rollout_tc_eligible(const ktune_ac* ac, const ktune_space* sp);
-void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end);
+// progress/nseg (streamed host-buffer calls): every slot adds 1 to progress[s] when it has
+// finished segment s (segment of step x = floor(x nseg / T)); segment s of the whole call is
+// complete once progress[s] reaches the returned slot count (summed over the launches).
+int64_t rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end,
+                   unsigned int* progress = nullptr, int nseg = 0);
 // Folds the device counters of the tcgen05 rollout into ctx->stats.
 void resolve_counters(ktune_ctx* ctx);
 }  // namespace kt

@@ -702,6 +702,7 @@ int ktune_ppo_update(ktune_ctx* ctx, ktune_ac* ac, ktune_adam* adam, const ktune
     KT_CUDA(cudaMemcpyAsync(htot, tot, sizeof(htot), cudaMemcpyDeviceToHost, s));
     KT_CUDA(cudaMemcpyAsync(ac->host_params.data(), ac->d_params, sizeof(double) * P, cudaMemcpyDeviceToHost, s));
     KT_CUDA(cudaStreamSynchronize(s));
+    ++ac->version;
     if (stats)
       for (int k = 0; k < 3; ++k) stats[k] = htot[k] / (double)steps;
   });

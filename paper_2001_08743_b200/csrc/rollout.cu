@@ -15,6 +15,8 @@
 //   C: logits[a][c], value[c]                 thread = (config, logit) items
 //   D: per (config, knob) log-softmax, counter-RNG draw, saturating move
 //   E: joint log-probability, trajectory writes
+#include <cuda.h>  // CUresult / CUstream for the cuStreamWaitValue32 entry point (no -lcuda)
+
 #include <algorithm>
 #include <array>
 
@@ -397,6 +399,31 @@ __global__ void narrow_idx_kernel(const uint16_t* __restrict__ src, uint8_t* __r
   }
 }
 
+// Configuration ids id_of(Θ) (design_space.cpp:158-167: mixed radix, last knob fastest) of
+// trajectory rows [r0, r0 + rows) of every episode (ids_u32 outputs; |space| <= 2^32).
+struct IdRadix {
+  int n;
+  uint32_t card[kt::kMaxKnobs];
+};
+__global__ void ids_rows_kernel(const uint16_t* __restrict__ src, uint32_t* __restrict__ dst, IdRadix rx, int64_t E,
+                                int64_t rows_per_ep, int64_t r0, int64_t rows) {
+  const int64_t total = E * rows;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / rows, r = e * rows_per_ep + r0 + (i - e * rows);
+    const uint16_t* row = src + r * rx.n;
+    uint32_t id = 0;
+    if (rx.n == 8) {  // one 16-byte load per row
+      const uint4 v = *reinterpret_cast<const uint4*>(row);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int d = 0; d < 8; ++d) id = id * rx.card[d] + ((w[d >> 1] >> (16 * (d & 1))) & 0xffffu);
+    } else {
+      for (int d = 0; d < rx.n; ++d) id = id * rx.card[d] + row[d];
+    }
+    dst[r] = id;
+  }
+}
+
 // int8 directions -> 2-bit codes (direction + 1), 4 knobs per byte, for steps [t0, t0 + steps).
 __global__ void pack_actions_kernel(const int8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t E, int64_t T,
                                     int n, int64_t t0, int64_t steps) {
@@ -414,6 +441,30 @@ __global__ void pack_actions_kernel(const int8_t* __restrict__ src, uint8_t* __r
     }
     dst[(e * T + step) * nb + b] = (uint8_t)v;
   }
+}
+
+// cuStreamWaitValue32 through the runtime's driver entry point (resolved once per context):
+// the copy stream of a streamed rollout waits until the kernel's progress counter reaches a
+// segment's count. False when the driver does not offer stream memory operations.
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+bool wait_value_available(ktune_ctx* ctx) {
+  if (ctx->wait_value_state == 0) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    int ok = 0;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn)
+      ok = 1;
+    cudaGetLastError();
+    ctx->fn_wait_value = fn;
+    ctx->wait_value_state = ok ? 1 : -1;
+  }
+  return ctx->wait_value_state == 1;
+}
+void wait_value_geq(ktune_ctx* ctx, cudaStream_t st, const unsigned int* addr, unsigned int v) {
+  const CUresult r = reinterpret_cast<WaitValueFn>(ctx->fn_wait_value)((CUstream)st, (CUdeviceptr)addr, v,
+                                                                      CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) kt::fail(KTUNE_ERR_BACKEND, "rollout: cuStreamWaitValue32 failed");
 }
 
 bool fits_smem(int n, int h, int g, int cpl = 1) { return rollout_smem_bytes(n, h, g, true, cpl) <= 227 * 1024; }
@@ -532,7 +583,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     std::vector<int64_t> goff(num_tasks + 1, 0);
     for (int k = 0; k < num_tasks; ++k) goff[k + 1] = goff[k] + std::max<int64_t>(0, tasks[k].num_episodes);
     const int64_t Etot = goff[num_tasks];
-    // per output kind (idx, score, actions, logp, value, logp32, value32, idx8, actions2, score32):
+    // per output kind (idx, score, actions, logp, value, logp32, value32, idx8, actions2, score32, ids32):
     // the tasks that request it form one contiguous run [lo, hi] whose columns are a W-wide
     // step-major array at the host pointer of task lo (task k at column goff[k] - goff[lo])
     struct GKind {
@@ -541,10 +592,11 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       void* host = nullptr;
       size_t rb = 0;  // bytes per row element (per episode column)
     };
-    std::array<GKind, 10> gk{};
+    constexpr int kKinds = 11;
+    std::array<GKind, kKinds> gk{};
     auto kind_ptr = [&](const ktune_rollout_task& t, int q) -> void* {
-      void* const v[10] = {t.idx, t.score, t.actions, t.logp, t.value, t.logp_f32, t.value_f32, t.idx_u8, t.actions_u2,
-                           t.score_f32};
+      void* const v[kKinds] = {t.idx,  t.score,    t.actions,    t.logp,      t.value,  t.logp_f32,
+                               t.value_f32, t.idx_u8, t.actions_u2, t.score_f32, t.ids_u32};
       return v[q];
     };
     if (grouped) {
@@ -552,8 +604,8 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         if (!tasks[k].ac || !tasks[0].ac || tasks[k].ac->n != tasks[0].ac->n)
           kt::fail(KTUNE_ERR_CONFIG, "rollout: grouped layout needs the same knob count in every task");
       const int64_t n = tasks[0].ac ? tasks[0].ac->n : 0;
-      const size_t rbs[10] = {(size_t)(2 * n), 8, (size_t)n, 8, 8, 4, 4, (size_t)n, (size_t)((n + 3) / 4), 4};
-      for (int q = 0; q < 10; ++q) {
+      const size_t rbs[kKinds] = {(size_t)(2 * n), 8, (size_t)n, 8, 8, 4, 4, (size_t)n, (size_t)((n + 3) / 4), 4, 4};
+      for (int q = 0; q < kKinds; ++q) {
         GKind& g = gk[q];
         g.rb = rbs[q];
         for (int k = 0; k < num_tasks; ++k) {
@@ -585,6 +637,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       uint8_t* d_u8;
       uint8_t* d_a2;
       float* d_s32;
+      uint32_t* d_ids;
     };
     std::vector<HostIo> io(num_tasks);
     bool smem_params = true;
@@ -594,13 +647,13 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       arena += (std::max<size_t>(bytes, 8) + 255) & ~(size_t)255;
       return o;
     };
-    std::vector<std::array<size_t, 11>> offs(num_tasks);
+    std::vector<std::array<size_t, 12>> offs(num_tasks);
     for (int k = 0; k < num_tasks; ++k) {
       const ktune_rollout_task& t = tasks[k];
       if (!t.space || !t.ac) kt::fail(KTUNE_ERR_CONFIG, "rollout: task needs a space and an agent");
       if (t.ac->n != t.space->D) kt::fail(KTUNE_ERR_CONFIG, "rollout: agent/space knob count mismatch");
       if (t.gbt && t.gbt->num_features != t.space->D) kt::fail(KTUNE_ERR_CONFIG, "rollout: cost model/space mismatch");
-      if (t.num_episodes < 0 || (!t.idx && (dev || !t.idx_u8)))
+      if (t.num_episodes < 0 || (!t.idx && (dev || (!t.idx_u8 && !t.ids_u32))))
         kt::fail(KTUNE_ERR_CONFIG, "rollout: bad episode count or missing idx output");
       if (t.actions_u2 && dev && !t.actions)
         kt::fail(KTUNE_ERR_CONFIG, "rollout: device-pointer calls need actions alongside actions_u2");
@@ -609,6 +662,11 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       if (t.idx_u8)
         for (int c : t.space->card)
           if (c > 256) kt::fail(KTUNE_ERR_CONFIG, "rollout: idx_u8 needs every knob cardinality <= 256");
+      if (t.ids_u32) {
+        double sz = 1;
+        for (int c : t.space->card) sz *= c;
+        if (sz > 4294967296.0) kt::fail(KTUNE_ERR_CONFIG, "rollout: ids_u32 needs a design space of at most 2^32 configurations");
+      }
       smem_params = smem_params && fits_smem(t.ac->n, t.ac->h, t.ac->g);
       if (!dev && !grouped) {
         const size_t E = (size_t)t.num_episodes, n = (size_t)t.ac->n;
@@ -617,7 +675,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
                    (t.score || t.score_f32) ? slice(E * (T + 1) * 8) : SIZE_MAX, t.logp_f32 ? slice(E * T * 4) : SIZE_MAX,
                    t.value_f32 ? slice(E * T * 4) : SIZE_MAX, t.idx_u8 ? slice(E * (T + 1) * n) : SIZE_MAX,
                    t.actions_u2 ? slice(E * T * ((n + 3) / 4)) : SIZE_MAX,
-                   t.score_f32 ? slice(E * (T + 1) * 4) : SIZE_MAX};
+                   t.score_f32 ? slice(E * (T + 1) * 4) : SIZE_MAX, t.ids_u32 ? slice(E * (T + 1) * 4) : SIZE_MAX};
       }
     }
     if (!dev && grouped && num_tasks > 0) {  // one Etot-wide slice per output any task requests
@@ -627,7 +685,8 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
                  any(3) ? slice(E * T * 8) : SIZE_MAX, any(4) ? slice(E * T * 8) : SIZE_MAX,
                  (any(1) || any(9)) ? slice(E * (T + 1) * 8) : SIZE_MAX, any(5) ? slice(E * T * 4) : SIZE_MAX,
                  any(6) ? slice(E * T * 4) : SIZE_MAX, any(7) ? slice(E * (T + 1) * n) : SIZE_MAX,
-                 any(8) ? slice(E * T * ((n + 3) / 4)) : SIZE_MAX, any(9) ? slice(E * (T + 1) * 4) : SIZE_MAX};
+                 any(8) ? slice(E * T * ((n + 3) / 4)) : SIZE_MAX, any(9) ? slice(E * (T + 1) * 4) : SIZE_MAX,
+                 any(10) ? slice(E * (T + 1) * 4) : SIZE_MAX};
     }
     unsigned char* base = dev ? nullptr : (unsigned char*)ctx->dev(kt::WS_ROLLOUT, std::max<size_t>(arena, 256));
     auto at = [&](size_t o) { return o == SIZE_MAX ? nullptr : (void*)(base + o); };
@@ -637,8 +696,8 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       const int64_t E = t.num_episodes;
       HostIo& h = io[k];
       if (dev) {
-        h = {t.init_idx, t.idx, t.actions, t.logp, t.value, t.score, t.logp_f32, t.value_f32, t.idx_u8, t.actions_u2,
-             t.score_f32};
+        h = {t.init_idx, t.idx,    t.actions,    t.logp,      t.value,  t.score,
+             t.logp_f32, t.value_f32, t.idx_u8, t.actions_u2, t.score_f32, t.ids_u32};
       } else if (grouped) {  // task 0's slices, shifted to this task's episode columns
         const int64_t o = goff[k];
         auto sh = [&](size_t off, int64_t per_row) -> unsigned char* {
@@ -647,14 +706,14 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         h = {(const uint16_t*)sh(offs[0][0], 2 * n), (uint16_t*)sh(offs[0][1], 2 * n), (int8_t*)sh(offs[0][2], n),
              (double*)sh(offs[0][3], 8),             (double*)sh(offs[0][4], 8),       (double*)sh(offs[0][5], 8),
              (float*)sh(offs[0][6], 4),              (float*)sh(offs[0][7], 4),        (uint8_t*)sh(offs[0][8], n),
-             (uint8_t*)sh(offs[0][9], (n + 3) / 4),  (float*)sh(offs[0][10], 4)};
+             (uint8_t*)sh(offs[0][9], (n + 3) / 4),  (float*)sh(offs[0][10], 4),       (uint32_t*)sh(offs[0][11], 4)};
         if (E > 0)
           KT_CUDA(cudaMemcpyAsync((void*)h.d_init, t.init_idx, (size_t)E * n * 2, cudaMemcpyHostToDevice, ctx->stream));
       } else {
         h = {(const uint16_t*)at(offs[k][0]), (uint16_t*)at(offs[k][1]), (int8_t*)at(offs[k][2]),
              (double*)at(offs[k][3]),         (double*)at(offs[k][4]),   (double*)at(offs[k][5]),
              (float*)at(offs[k][6]),          (float*)at(offs[k][7]),    (uint8_t*)at(offs[k][8]),
-             (uint8_t*)at(offs[k][9]),        (float*)at(offs[k][10])};
+             (uint8_t*)at(offs[k][9]),        (float*)at(offs[k][10]),   (uint32_t*)at(offs[k][11])};
         if (E > 0)
           KT_CUDA(cudaMemcpyAsync((void*)h.d_init, t.init_idx, (size_t)E * n * 2, cudaMemcpyHostToDevice, ctx->stream));
       }
@@ -741,6 +800,21 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
                                                  stepm ? (r1 - r0 + 1) * E : r1 - r0 + 1);
       kt::check_launch(ctx, "narrow_idx");
     };
+    auto ids_rows = [&](int k, int r0, int r1) {  // configuration ids of trajectory rows [r0, r1]
+      const ktune_rollout_task& t = tasks[k];
+      if (t.num_episodes == 0 || (grouped ? (k < gk[10].lo || k > gk[10].hi) : !t.ids_u32)) return;
+      const int64_t E = t.num_episodes, len = r1 - r0 + 1;
+      IdRadix rx{};  // per task: the radix is the task's own space
+      rx.n = t.ac->n;
+      for (int d = 0; d < rx.n; ++d) rx.card[d] = (uint32_t)t.space->card[d];
+      // (outer, inner, outer pitch, first): grouped = rows of this task's E columns every Etot;
+      // step-major = one flat block; episode-major = rows [r0, r1] of every episode
+      const int64_t outer = grouped ? len : stepm ? 1 : E, inner = grouped ? E : stepm ? len * E : len;
+      const int64_t pitch = grouped ? Etot : T + 1, first = grouped ? r0 * Etot : stepm ? r0 * E : r0;
+      ids_rows_kernel<<<(unsigned)std::min<int64_t>(kt::ceil_div(E * len, 256), (int64_t)kt::sm_count(ctx) * 16), 256,
+                        0, ctx->stream>>>(io[k].d_idx, io[k].d_ids, rx, outer, pitch, first, inner);
+      kt::check_launch(ctx, "ids_rows");
+    };
     auto pack_steps = [&](int k, int t0, int t1) {  // int8 -> 2-bit actions of steps [t0, t1)
       const ktune_rollout_task& t = tasks[k];
       if (t1 <= t0 || (grouped ? (k > 0 || gk[8].lo < 0 || Etot == 0) : (!t.actions_u2 || t.num_episodes == 0)))
@@ -752,20 +826,23 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
                                               stepm ? (int64_t)t0 * E : t0, stepm ? (int64_t)(t1 - t0) * E : t1 - t0);
       kt::check_launch(ctx, "pack_actions");
     };
-    auto copy_out = [&](int k, int t0, int t1, cudaStream_t st) {  // steps [t0, t1): rows (t0, t1] (+ row 0)
+    // steps [t0, t1): rows (t0, t1] (+ row 0); what: 1 the trajectory, 2 the scores, 3 both
+    auto copy_out = [&](int k, int t0, int t1, cudaStream_t st, int what) {
       const ktune_rollout_task& t = tasks[k];
+      const bool traj = what & 1, scores = what & 2;
       if (grouped) {  // once for every task: per output, the W columns of its task run in one copy
         if (k > 0) return;
         const int r0 = t0 == 0 ? 0 : t0 + 1;
-        const int64_t nr[10] = {t1 - r0 + 1, t1 - r0 + 1, t1 - t0, t1 - t0, t1 - t0, t1 - t0, t1 - t0, t1 - r0 + 1,
-                                t1 - t0, t1 - r0 + 1};
-        const int64_t first[10] = {r0, r0, t0, t0, t0, t0, t0, r0, t0, r0};
-        const void* dsrc[10] = {io[0].d_idx, io[0].d_score, io[0].d_act, io[0].d_logp, io[0].d_val,
-                                io[0].d_logp32, io[0].d_val32, io[0].d_u8, io[0].d_a2, io[0].d_s32};
-        for (int q = 0; q < 10; ++q) {
+        const int64_t nr[kKinds] = {t1 - r0 + 1, t1 - r0 + 1, t1 - t0,     t1 - t0, t1 - t0,     t1 - t0,
+                                    t1 - t0,     t1 - r0 + 1, t1 - t0,     t1 - r0 + 1, t1 - r0 + 1};
+        const int64_t first[kKinds] = {r0, r0, t0, t0, t0, t0, t0, r0, t0, r0, r0};
+        const void* dsrc[kKinds] = {io[0].d_idx,   io[0].d_score, io[0].d_act, io[0].d_logp, io[0].d_val, io[0].d_logp32,
+                                    io[0].d_val32, io[0].d_u8,    io[0].d_a2,  io[0].d_s32,  io[0].d_ids};
+        for (int q = 0; q < kKinds; ++q) {
           const GKind& g = gk[q];
           if (g.lo < 0 || g.W == 0 || nr[q] <= 0 || !dsrc[q]) continue;
-          if ((q == 1 || q == 9) && !tasks[g.lo].gbt) continue;
+          if ((q == 1 || q == 9) && (!tasks[g.lo].gbt || !scores)) continue;
+          if (q != 1 && q != 9 && !traj) continue;
           const size_t spitch = (size_t)Etot * g.rb, dpitch = (size_t)g.W * g.rb, width = dpitch;
           const char* src = (const char*)dsrc[q] + (size_t)first[q] * spitch + (size_t)goff[g.lo] * g.rb;
           char* dst = (char*)g.host + (size_t)first[q] * dpitch;
@@ -782,13 +859,14 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
       const int r0 = t0 == 0 ? 0 : t0 + 1;
       const size_t rows = (size_t)(t1 - r0 + 1), steps = (size_t)(t1 - t0);
       if (stepm) {  // every output's segment is one contiguous block: 1-D copies
-        auto cp = [&](void* dst, const void* src, size_t off, size_t bytes) {
-          if (dst && bytes)
+        auto cp = [&](void* dst, const void* src, size_t off, size_t bytes, bool is_score = false) {
+          if (dst && bytes && (is_score ? scores : traj))
             KT_CUDA(cudaMemcpyAsync((char*)dst + off, (const char*)src + off, bytes, cudaMemcpyDeviceToHost, st));
         };
         const size_t nb = (n + 3) / 4;
         cp(t.idx, h.d_idx, r0 * E * n * 2, rows * E * n * 2);
         cp(t.idx_u8, h.d_u8, r0 * E * n, rows * E * n);
+        cp(t.ids_u32, h.d_ids, r0 * E * 4, rows * E * 4);
         cp(t.actions, h.d_act, t0 * E * n, steps * E * n);
         cp(t.actions_u2, h.d_a2, t0 * E * nb, steps * E * nb);
         cp(t.logp, h.d_logp, t0 * E * 8, steps * E * 8);
@@ -796,39 +874,42 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         cp(t.logp_f32, h.d_logp32, t0 * E * 4, steps * E * 4);
         cp(t.value_f32, h.d_val32, t0 * E * 4, steps * E * 4);
         if (t.gbt) {
-          cp(t.score, h.d_score, r0 * E * 8, rows * E * 8);
-          cp(t.score_f32, h.d_s32, r0 * E * 4, rows * E * 4);
+          cp(t.score, h.d_score, r0 * E * 8, rows * E * 8, true);
+          cp(t.score_f32, h.d_s32, r0 * E * 4, rows * E * 4, true);
         }
         return;
       }
-      if (t.idx)
+      if (traj && t.idx)
         KT_CUDA(cudaMemcpy2DAsync(t.idx + r0 * n, (T + 1) * n * 2, h.d_idx + r0 * n, (T + 1) * n * 2, rows * n * 2,
                                   E, cudaMemcpyDeviceToHost, st));
-      if (t.idx_u8)
+      if (traj && t.idx_u8)
         KT_CUDA(cudaMemcpy2DAsync(t.idx_u8 + r0 * n, (T + 1) * n, h.d_u8 + r0 * n, (T + 1) * n, rows * n, E,
                                   cudaMemcpyDeviceToHost, st));
-      if (t.actions && steps)
+      if (traj && t.ids_u32)
+        KT_CUDA(cudaMemcpy2DAsync(t.ids_u32 + r0, (T + 1) * 4, h.d_ids + r0, (T + 1) * 4, rows * 4, E,
+                                  cudaMemcpyDeviceToHost, st));
+      if (traj && t.actions && steps)
         KT_CUDA(cudaMemcpy2DAsync(t.actions + t0 * n, T * n, h.d_act + t0 * n, T * n, steps * n, E,
                                   cudaMemcpyDeviceToHost, st));
-      if (t.actions_u2 && steps) {
+      if (traj && t.actions_u2 && steps) {
         const size_t nb = (n + 3) / 4;
         KT_CUDA(cudaMemcpy2DAsync(t.actions_u2 + t0 * nb, T * nb, h.d_a2 + t0 * nb, T * nb, steps * nb, E,
                                   cudaMemcpyDeviceToHost, st));
       }
-      if (t.logp && steps)
+      if (traj && t.logp && steps)
         KT_CUDA(cudaMemcpy2DAsync(t.logp + t0, T * 8, h.d_logp + t0, T * 8, steps * 8, E, cudaMemcpyDeviceToHost, st));
-      if (t.value && steps)
+      if (traj && t.value && steps)
         KT_CUDA(cudaMemcpy2DAsync(t.value + t0, T * 8, h.d_val + t0, T * 8, steps * 8, E, cudaMemcpyDeviceToHost, st));
-      if (t.logp_f32 && steps)
+      if (traj && t.logp_f32 && steps)
         KT_CUDA(cudaMemcpy2DAsync(t.logp_f32 + t0, T * 4, h.d_logp32 + t0, T * 4, steps * 4, E,
                                   cudaMemcpyDeviceToHost, st));
-      if (t.value_f32 && steps)
+      if (traj && t.value_f32 && steps)
         KT_CUDA(cudaMemcpy2DAsync(t.value_f32 + t0, T * 4, h.d_val32 + t0, T * 4, steps * 4, E,
                                   cudaMemcpyDeviceToHost, st));
-      if (t.score && t.gbt)
+      if (scores && t.score && t.gbt)
         KT_CUDA(cudaMemcpy2DAsync(t.score + r0, (T + 1) * 8, h.d_score + r0, (T + 1) * 8, rows * 8, E,
                                   cudaMemcpyDeviceToHost, st));
-      if (t.score_f32 && t.gbt)
+      if (scores && t.score_f32 && t.gbt)
         KT_CUDA(cudaMemcpy2DAsync(t.score_f32 + r0, (T + 1) * 4, h.d_s32 + r0, (T + 1) * 4, rows * 4, E,
                                   cudaMemcpyDeviceToHost, st));
     };
@@ -845,6 +926,71 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
         work[k].aE = dt[k].aE;
         work[k].aT = dt[k].aT;
       }
+      // Streamed (default for host buffers): ONE rollout launch; each slot publishes the segments
+      // it has finished in device memory and the copy stream waits on that counter
+      // (cuStreamWaitValue32), copying every finished segment of the trajectory (ids / idx, actions,
+      // logp, value, in the compact encodings the kernel writes itself) while the kernel runs on.
+      // The cost model then scores the whole trajectory in a few row chunks whose score copies
+      // overlap the next chunk's scoring.
+      const bool streamed = segmented && ctx->opt_rollout_streamed != 1 && !ctx->opt_rollout_fuse_gbt &&
+                            wait_value_available(ctx);
+      if (streamed) {
+        const int SS = ctx->opt_rollout_segments > 1 ? (int)std::min<int64_t>(ctx->opt_rollout_segments, T)
+                                                     : (int)std::min<int64_t>(32, std::max<int64_t>(2, T / 25));
+        auto in_run = [&](int q, int k, bool own) { return grouped ? (k >= gk[q].lo && k <= gk[q].hi) : own; };
+        for (int k = 0; k < num_tasks; ++k) {  // the kernel writes the compact encodings directly
+          const ktune_rollout_task& t = tasks[k];
+          work[k].idx8 = in_run(7, k, t.idx_u8 != nullptr) ? io[k].d_u8 : nullptr;
+          work[k].act2 = in_run(8, k, t.actions_u2 != nullptr) ? io[k].d_a2 : nullptr;
+          work[k].ids = in_run(10, k, t.ids_u32 != nullptr) ? io[k].d_ids : nullptr;
+          if (!in_run(2, k, t.actions != nullptr)) work[k].actions = nullptr;  // int8 directions not requested
+        }
+        constexpr int kMaxSegs = 64;
+        if (!ctx->d_progress) KT_CUDA(cudaMalloc(&ctx->d_progress, kMaxSegs * sizeof(unsigned int)));
+        if (SS > kMaxSegs || (int64_t)T * SS >= (1ll << 31))
+          kt::fail(KTUNE_ERR_CONFIG, "rollout: at most 64 streamed segments and T x segments < 2^31");
+        KT_CUDA(cudaMemsetAsync(ctx->d_progress, 0, SS * sizeof(unsigned int), ctx->stream));
+        auto fence = [&](cudaStream_t from, cudaStream_t to) {
+          cudaEvent_t ev;
+          KT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          events.push_back(ev);
+          KT_CUDA(cudaEventRecord(ev, from));
+          KT_CUDA(cudaStreamWaitEvent(to, ev, 0));
+        };
+        fence(ctx->stream, ctx->copy_stream);  // the counter is reset before any wait reads it
+        int64_t slots = 0;
+        {
+          kt::ProfScope prof(ctx, KTUNE_STAT_ROLLOUT_NS);
+          slots = kt::rollout_tc(ctx, work, T, 0, T, ctx->d_progress, SS);
+        }
+        // Once the rollout is done every wait is satisfied, whatever the count, so no wait can hang.
+        // The driver's GEQ test is cyclic ((int32_t)(*addr - v) >= 0): the release value 0x7F7F7F7F
+        // passes every wait value v <= 0x7F7F7F7F and no count reached before it does.
+        constexpr unsigned int kRelease = 0x7F7F7F7Fu;
+        KT_CUDA(cudaMemsetAsync(ctx->d_progress, 0x7F, SS * sizeof(unsigned int), ctx->stream));
+        if (slots >= (int64_t)kRelease) kt::fail(KTUNE_ERR_CONFIG, "rollout: too many slots");
+        for (int sg = 0; sg < SS; ++sg) {
+          const int t0 = (int)(((int64_t)sg * T + SS - 1) / SS), t1 = (int)(((int64_t)(sg + 1) * T + SS - 1) / SS);
+          if (t1 <= t0) continue;
+          // the last segment is never counted by the kernel: its copies follow the release
+          wait_value_geq(ctx, ctx->copy_stream, ctx->d_progress + sg, sg + 1 < SS ? (unsigned int)slots : kRelease);
+          for (int k = 0; k < num_tasks; ++k) copy_out(k, t0, t1, ctx->copy_stream, 1);
+        }
+        const int C = (int)std::min<int64_t>(4, T);  // score chunks
+        for (int c = 0; c < C; ++c) {
+          const int t0 = (int)((int64_t)c * T / C), t1 = (int)((int64_t)(c + 1) * T / C);
+          const int r0 = t0 == 0 ? 0 : t0 + 1;
+          for (int k = 0; k < num_tasks; ++k) score_rows(k, r0, t1);
+          flush_scores();
+          for (int k = 0; k < num_tasks; ++k) score32_rows(k, r0, t1);
+          fence(ctx->stream, ctx->copy_stream);
+          for (int k = 0; k < num_tasks; ++k) copy_out(k, t0, t1, ctx->copy_stream, 2);
+        }
+        KT_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+        for (cudaEvent_t ev : events) cudaEventDestroy(ev);
+        KT_CUDA(cudaStreamSynchronize(ctx->stream));
+        return;
+      }
       if (segmented) {
         for (int sg = 0; sg < S; ++sg) {
           const int t0 = (int)((int64_t)sg * T / S), t1 = (int)((int64_t)(sg + 1) * T / S);
@@ -857,6 +1003,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
           for (int k = 0; k < num_tasks; ++k) {  // after every task's scores (grouped: one pass for all)
             score32_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
             narrow_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
+            ids_rows(k, t0 == 0 ? 0 : t0 + 1, t1);
             pack_steps(k, t0, t1);
           }
           cudaEvent_t ev;
@@ -864,7 +1011,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
           events.push_back(ev);
           KT_CUDA(cudaEventRecord(ev, ctx->stream));
           KT_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev, 0));
-          for (int k = 0; k < num_tasks; ++k) copy_out(k, t0, t1, ctx->copy_stream);
+          for (int k = 0; k < num_tasks; ++k) copy_out(k, t0, t1, ctx->copy_stream, 3);
         }
         KT_CUDA(cudaStreamSynchronize(ctx->copy_stream));
         for (cudaEvent_t ev : events) cudaEventDestroy(ev);
@@ -910,10 +1057,11 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
     for (int k = 0; k < num_tasks; ++k) {  // after every task's scores (grouped: one pass for all)
       score32_rows(k, 0, T);
       narrow_rows(k, 0, T);
+      ids_rows(k, 0, T);
       pack_steps(k, 0, T);
     }
     if (!dev) {
-      for (int k = 0; k < num_tasks; ++k) copy_out(k, 0, T, ctx->stream);
+      for (int k = 0; k < num_tasks; ++k) copy_out(k, 0, T, ctx->stream, 3);
       KT_CUDA(cudaStreamSynchronize(ctx->stream));
     }
   });

@@ -75,6 +75,10 @@ struct TcTask {
   int32_t ntrees, depth;
   double gbase, glr;
   double* score;  // E x (T+1)
+  // compact outputs written by the rollout itself (host-buffer calls; NULL: not requested)
+  uint8_t* idx8;   // rows as uint8 knob indices (idx layout, n bytes per row)
+  uint32_t* ids;   // rows as configuration ids id_of (score layout)
+  uint8_t* act2;   // steps as 2-bit direction codes, ceil(n/4) bytes per step (actions layout)
 };
 
 struct TcLaunch {
@@ -83,6 +87,12 @@ struct TcLaunch {
   int32_t check;
   float delta;
   unsigned long long* counters;  // [fallbacks, checked, mismatches, max err (float bits)]
+  // streamed host-buffer rollouts: the episode's steps form nseg segments, segment s = steps
+  // [ceil(s T / nseg), ceil((s+1) T / nseg)); every slot adds 1 to progress[s] when its rows
+  // have finished segment s, so the copy stream can wait for progress[s] to reach the slot
+  // count (cuStreamWaitValue32) while the kernel runs on
+  unsigned int* progress;
+  int32_t nseg;
   TcTask task[kMaxTcTasks];
 };
 
@@ -234,6 +244,51 @@ struct Cfg {
     w[d >> 1] = (w[d >> 1] & ~(0xFFFFu << sh)) | ((uint32_t)v << sh);
   }
 };
+
+// Step x opens a segment of a streamed rollout (segment of step x = floor(x nseg / T)).
+// 32-bit arithmetic (x nseg < 2^31: the host caps T nseg): inline, no 64-bit division call.
+__device__ __forceinline__ bool seg_boundary(int x, int nseg, int T) {
+  return (uint32_t)(x * nseg) / (uint32_t)T != (uint32_t)((x - 1) * nseg) / (uint32_t)T;
+}
+
+// Configuration id (design_space.cpp:158-167: mixed radix, last knob fastest); knobs >= n
+// have cardinality 1 and index 0, so the Horner chain runs branch-free over NMAX.
+template <int NMAX>
+__device__ __forceinline__ uint32_t cfg_id(const Cfg<NMAX>& c, const int* card) {
+  uint32_t id = 0;
+#pragma unroll
+  for (int d = 0; d < NMAX; ++d) id = id * (uint32_t)card[d] + (uint32_t)c.get(d);
+  return id;
+}
+
+template <int NMAX>
+__device__ __forceinline__ void store_row_u8(uint8_t* dst, const Cfg<NMAX>& c, int n) {
+  if ((n & 7) == 0) {
+#pragma unroll
+    for (int q = 0; q < NMAX / 8; ++q)
+      if (8 * q < n) {
+        const uint32_t lo = __byte_perm(c.w[4 * q], c.w[4 * q + 1], 0x6420);
+        const uint32_t hi = __byte_perm(c.w[4 * q + 2], c.w[4 * q + 3], 0x6420);
+        reinterpret_cast<uint2*>(dst)[q] = make_uint2(lo, hi);
+      }
+  } else {
+#pragma unroll
+    for (int d = 0; d < NMAX; ++d)
+      if (d < n) dst[d] = (uint8_t)c.get(d);
+  }
+}
+
+// 2-bit direction codes (direction + 1) of one step: the low 2n bits of the decision word.
+__device__ __forceinline__ void store_act2(uint8_t* dst, uint64_t acts, int n) {
+  if (n == 8) {
+    *reinterpret_cast<uint16_t*>(dst) = (uint16_t)acts;
+  } else {
+    for (int b = 0; 4 * b < n; ++b) {
+      const int k = min(4, n - 4 * b);
+      dst[b] = (uint8_t)((acts >> (8 * b)) & ((1u << (2 * k)) - 1u));
+    }
+  }
+}
 
 template <int NMAX>
 __device__ __forceinline__ void store_row_idx(uint16_t* dst, const Cfg<NMAX>& c, int n) {
@@ -447,7 +502,9 @@ __device__ __forceinline__ void stage_weights(const TcTask& tk, unsigned char* s
   }
 }
 
-template <int NMAX>
+// kStream: the streamed host-buffer variant (compact encodings written here, per-segment
+// progress published); a separate instantiation so the device-buffer path keeps its registers.
+template <int NMAX, bool kStream>
 __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_constant__ TcLaunch L) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint64_t mbar[kSlots];
@@ -539,6 +596,10 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         for (int d = 0; d < NMAX; ++d)
           if (d < n) cfg.set(d, tk.init_idx[e * n + d]);
         store_row_idx(tk.idx + e * tk.sE * n, cfg, n);
+        if constexpr (kStream) {
+          if (tk.idx8) store_row_u8(tk.idx8 + e * tk.sE * n, cfg, n);
+          if (tk.ids) tk.ids[e * tk.sE] = cfg_id(cfg, scard);
+        }
       } else {  // resume a segmented rollout from trajectory row t_begin
         const uint16_t* src = tk.idx + (e * tk.sE + L.t_begin * tk.sT) * n;
 #pragma unroll
@@ -817,6 +878,11 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
         TR(10)
         if (lr && L.check != 4) {  // 4: timing experiment (no trajectory writes)
           store_row_idx(tk.idx + (e * tk.sE + (t + 1) * tk.sT) * n, cfg, n);
+          if constexpr (kStream) {
+            if (tk.idx8) store_row_u8(tk.idx8 + (e * tk.sE + (t + 1) * tk.sT) * n, cfg, n);
+            if (tk.ids) tk.ids[e * tk.sE + (t + 1) * tk.sT] = cfg_id(cfg, scard);
+            if (tk.act2) store_act2(tk.act2 + (e * tk.aE + t * tk.aT) * ((n + 3) / 4), acts, n);
+          }
           if (tk.actions) {
             int8_t* ad = tk.actions + (e * tk.aE + t * tk.aT) * n;
             if ((n & 3) == 0) {
@@ -835,6 +901,16 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       }
       ph ^= 1;
       TR(15)
+      if constexpr (kStream) {
+      if (t + 1 < L.t_end && seg_boundary(t + 1, L.nseg, T)) {
+        __threadfence();  // this row's step-t outputs are visible GPU-wide (at L2) ...
+        sync_slot(slot);  // ... for every row of the slot
+        if (leader) {
+          __threadfence_system();
+          atomicAdd(L.progress + (uint32_t)(t * L.nseg) / (uint32_t)T, 1u);  // the segment step t closes
+        }
+      }
+      }
     }
 #undef TR
     if (tk.gnode && lr && L.t_end == T)  // row T
@@ -881,8 +957,10 @@ void resolve_counters(ktune_ctx* ctx) {
       std::max<int64_t>(ctx->stats[KTUNE_STAT_ROLLOUT_MAXERR], (int64_t)std::llround((double)mx * 1e12));
 }
 
-static void rollout_tc_launch(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end,
-                              bool allow_fuse) {
+// Returns the number of episode slots launched (each adds 1 to progress[s] per segment s).
+static int64_t rollout_tc_launch(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end,
+                                 bool allow_fuse, unsigned int* progress, int nseg) {
+  int64_t total = 0;
   if (!ctx->d_counters) {
     KT_CUDA(cudaMalloc(&ctx->d_counters, (4 + 8 * 16) * sizeof(unsigned long long)));
     KT_CUDA(cudaMemsetAsync(ctx->d_counters, 0, (4 + 8 * 16) * sizeof(unsigned long long), ctx->stream));
@@ -900,6 +978,8 @@ static void rollout_tc_launch(ktune_ctx* ctx, std::vector<RolloutWork>& work, in
     L.t_end = t_end;
     L.delta = delta;
     L.counters = ctx->d_counters;
+    L.progress = progress;
+    L.nseg = nseg;
     // warps per task, then the smallest per-CTA warp count m whose CTA total fits one wave
     std::vector<int64_t> W(nt);
     int64_t wsum = 0;
@@ -919,6 +999,7 @@ static void rollout_tc_launch(ktune_ctx* ctx, std::vector<RolloutWork>& work, in
     }
     int ctas = 0;
     int nl = 0;
+    int64_t slots = 0;
     for (size_t k = 0; k < nt; ++k) {
       if (W[k] == 0) continue;
       const RolloutWork& rw = work[t0 + k];
@@ -945,22 +1026,36 @@ static void rollout_tc_launch(ktune_ctx* ctx, std::vector<RolloutWork>& work, in
       tk.value = rw.value;
       tk.logp32 = rw.logp32;
       tk.value32 = rw.value32;
+      tk.idx8 = rw.idx8;
+      tk.ids = rw.ids;
+      tk.act2 = rw.act2;
+      if (!progress && (rw.idx8 || rw.ids || rw.act2))
+        fail(KTUNE_ERR_LOGIC, "rollout: compact encodings are written by the streamed variant only");
       tk.warps = (int32_t)W[k];
       tk.ctas = (int32_t)ceil_div(W[k], m);
       tk.cta_base = ctas;
       ctas += tk.ctas;
-      // weight scales from the host copy of the parameters
+      for (int jc = 0; jc < tk.ctas; ++jc)  // the kernel's split: wbase (+1 for the first wextra CTAs) warps
+        slots += ceil_div((int64_t)(tk.warps / tk.ctas + (jc < tk.warps % tk.ctas ? 1 : 0)), 4);
+      // weight scales from the host copy of the parameters (cached per parameter version and space)
       const int n = tk.n;
-      const std::vector<double>& p = rw.ac->host_params;
-      const int ob0 = kH * n, owp1 = ob0 + kH, obp1 = owp1 + kG * kH, owp2 = obp1 + kG, obp2 = owp2 + 3 * n * kG,
-                owv1 = obp2 + 3 * n, obv1 = owv1 + kG * kH;
-      double m1 = 0, m2 = 0, m3 = 0;
-      for (int i = 0; i < n; ++i)
-        if (tk.card[i] > 1)
-          for (int j = 0; j < kH; ++j) m1 = std::max(m1, std::fabs(p[i * kH + j]) / (double)(tk.card[i] - 1));
-      for (int i = owp1; i < obp1; ++i) m2 = std::max(m2, std::fabs(p[i]));
-      for (int i = owv1; i < obv1; ++i) m2 = std::max(m2, std::fabs(p[i]));
-      for (int i = owp2; i < obp2; ++i) m3 = std::max(m3, std::fabs(p[i]));
+      if (rw.ac->scale_version != rw.ac->version || rw.ac->scale_space != rw.space) {
+        const std::vector<double>& p = rw.ac->host_params;
+        const int ob0 = kH * n, owp1 = ob0 + kH, obp1 = owp1 + kG * kH, owp2 = obp1 + kG,
+                  obp2 = owp2 + 3 * n * kG, owv1 = obp2 + 3 * n, obv1 = owv1 + kG * kH;
+        double m1 = 0, m2 = 0, m3 = 0;
+        for (int i = 0; i < n; ++i)
+          if (tk.card[i] > 1)
+            for (int j = 0; j < kH; ++j) m1 = std::max(m1, std::fabs(p[i * kH + j]) / (double)(tk.card[i] - 1));
+        for (int i = owp1; i < obp1; ++i) m2 = std::max(m2, std::fabs(p[i]));
+        for (int i = owv1; i < obv1; ++i) m2 = std::max(m2, std::fabs(p[i]));
+        for (int i = owp2; i < obp2; ++i) m3 = std::max(m3, std::fabs(p[i]));
+        rw.ac->scale_e[0] = pow2_scale(m1);
+        rw.ac->scale_e[1] = pow2_scale(m2);
+        rw.ac->scale_e[2] = pow2_scale(m3);
+        rw.ac->scale_space = rw.space;
+        rw.ac->scale_version = rw.ac->version;
+      }
       // optional fused scoring (complete-tree index layout that fits in shared memory)
       const ktune_gbt* g = rw.gbt;
       tk.gnode = nullptr;
@@ -975,9 +1070,9 @@ static void rollout_tc_launch(ktune_ctx* ctx, std::vector<RolloutWork>& work, in
         tk.score = rw.score;
         work[t0 + k].scored = true;
       }
-      tk.e1 = pow2_scale(m1);
-      tk.e2 = pow2_scale(m2);
-      tk.e3 = pow2_scale(m3);
+      tk.e1 = rw.ac->scale_e[0];
+      tk.e2 = rw.ac->scale_e[1];
+      tk.e3 = rw.ac->scale_e[2];
       if (tk.e1 > 100 || tk.e2 > 100 || tk.e3 > 100 || tk.e1 < -100 || tk.e2 < -100 || tk.e3 < -100)
         fail(KTUNE_ERR_CONFIG, "rollout: actor-critic weights out of the tensor-core path's range");
       ctx->stats[KTUNE_STAT_ROLLOUT_TC] += rw.E * (int64_t)(t_end - t_begin);
@@ -988,11 +1083,16 @@ static void rollout_tc_launch(ktune_ctx* ctx, std::vector<RolloutWork>& work, in
     for (int k = 0; k < nl; ++k)
       smem = std::max<size_t>(smem, tc_smem_bytes(L.task[k].n, L.task[k].gnode ? L.task[k].ntrees : 0,
                                                    L.task[k].depth));
-    auto kern = nmax <= 8 ? rollout_tc_kernel<8> : (nmax <= 16 ? rollout_tc_kernel<16> : rollout_tc_kernel<24>);
+    auto kern = progress ? (nmax <= 8 ? rollout_tc_kernel<8, true>
+                                      : (nmax <= 16 ? rollout_tc_kernel<16, true> : rollout_tc_kernel<24, true>))
+                         : (nmax <= 8 ? rollout_tc_kernel<8, false>
+                                      : (nmax <= 16 ? rollout_tc_kernel<16, false> : rollout_tc_kernel<24, false>));
     KT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<(unsigned)ctas, kThr, smem, ctx->stream>>>(L);
     check_launch(ctx, "rollout_tc");
+    total += slots;
   }
+  return total;
 }
 
 // Episodes [e, E) of a workload as a workload of its own (global ids, pointers advanced).
@@ -1009,30 +1109,35 @@ static RolloutWork episode_tail(const RolloutWork& w, int64_t e, int T) {
   if (w.logp32) t.logp32 = w.logp32 + e * w.aE;
   if (w.value32) t.value32 = w.value32 + e * w.aE;
   if (w.score) t.score = w.score + e * w.sE;
+  if (w.idx8) t.idx8 = w.idx8 + e * w.sE * n;
+  if (w.ids) t.ids = w.ids + e * w.sE;
+  if (w.act2) t.act2 = w.act2 + e * w.aE * ((n + 3) / 4);
   t.scored = false;
   return t;
 }
 
-void rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end) {
+int64_t rollout_tc(ktune_ctx* ctx, std::vector<RolloutWork>& work, int T, int t_begin, int t_end,
+                   unsigned int* progress, int nseg) {
   // A tile of episodes is bound to its slot for all T steps, so a workload larger than one
   // resident wave (kMaxWarps warps on every SM) would end with a part-filled wave running
   // at the full per-step latency. One workload: full waves, then the remainder spread thin
   // over every SM (e.g. 65,536 episodes = 1.15 waves).
   const int64_t cap = (int64_t)kMaxWarps * sm_count(ctx);
   if (work.size() != 1 || ceil_div(work[0].E, 32) <= cap) {
-    rollout_tc_launch(ctx, work, T, t_begin, t_end, true);
-    return;
+    return rollout_tc_launch(ctx, work, T, t_begin, t_end, true, progress, nseg);
   }
+  int64_t total = 0;
   RolloutWork rest = work[0];
   while (ceil_div(rest.E, 32) > cap) {
     std::vector<RolloutWork> wave(1, rest);
     wave[0].E = cap * 32;
-    rollout_tc_launch(ctx, wave, T, t_begin, t_end, false);
+    total += rollout_tc_launch(ctx, wave, T, t_begin, t_end, false, progress, nseg);
     rest = episode_tail(rest, cap * 32, T);
   }
   std::vector<RolloutWork> last(1, rest);
-  rollout_tc_launch(ctx, last, T, t_begin, t_end, false);
+  total += rollout_tc_launch(ctx, last, T, t_begin, t_end, false, progress, nseg);
   work[0].scored = false;
+  return total;
 }
 
 }  // namespace kt

@@ -227,12 +227,14 @@ def grouped_outputs(tasks: Sequence[RolloutTask], T: int, alloc, fields=None) ->
 
 
 def compact_grouped_outputs(tasks: Sequence[RolloutTask], T: int, alloc, score64: bool = False,
-                            logp64: bool = False) -> list:
+                            logp64: bool = False, ids: bool = False) -> list:
     """Grouped step-major outputs in the compact encoding (what crosses PCIe): visited
     configurations as uint8 for every run of consecutive tasks whose cardinalities fit (uint16
-    for the others), directions as 2-bit codes, scores fp32 (fp64 with score64) and log-probs /
-    values fp32 (fp64 with logp64; the tcgen05 path computes them in fp32). alloc(shape, dtype)
-    -> array. Every output but idx spans all tasks; idx is one array per run."""
+    for the others) - or, with ids=True, as one uint32 configuration id per visited
+    configuration (`ids32`, id_of: design_space.cpp:158-167; `configs_from_ids` inverts it) -
+    directions as 2-bit codes, scores fp32 (fp64 with score64) and log-probs / values fp32 (fp64
+    with logp64; the tcgen05 path computes them in fp32). alloc(shape, dtype) -> array. Every
+    output but idx spans all tasks; idx is one array per run."""
     D = tasks[0].space.D
     Es = [len(t.init_idx) for t in tasks]
     offs = np.cumsum([0] + Es)
@@ -241,10 +243,12 @@ def compact_grouped_outputs(tasks: Sequence[RolloutTask], T: int, alloc, score64
            ("score" if score64 else "score32"): alloc((T + 1, Et), np.float64 if score64 else np.float32),
            ("logp" if logp64 else "logp32"): alloc((T, Et), np.float64 if logp64 else np.float32),
            ("value" if logp64 else "value32"): alloc((T, Et), np.float64 if logp64 else np.float32)}
+    if ids:
+        big["ids32"] = alloc((T + 1, Et), np.uint32)
     outs = [{k: a[:, offs[i]:offs[i + 1]] for k, a in big.items()} for i in range(len(tasks))]
     small = [max(t.space.card) <= 256 for t in tasks]
     i = 0
-    while i < len(tasks):  # runs of consecutive tasks with the same idx width
+    while i < len(tasks) and not ids:  # runs of consecutive tasks with the same idx width
         j = i
         while j < len(tasks) and small[j] == small[i]:
             j += 1
@@ -254,9 +258,20 @@ def compact_grouped_outputs(tasks: Sequence[RolloutTask], T: int, alloc, score64
             outs[q][name] = a[:, offs[q] - offs[i]:offs[q + 1] - offs[i]]
         i = j
     for o in outs:
-        for k in ("idx", "idx8", "score", "score32", "actions", "logp", "value", "logp32", "value32"):
+        for k in ("idx", "idx8", "ids32", "score", "score32", "actions", "logp", "value", "logp32", "value32"):
             o.setdefault(k, None)
     return outs
+
+
+def configs_from_ids(ids, cards: Sequence[int]) -> np.ndarray:
+    """config_at (design_space.cpp:141-156) of the `ids_u32` output: ... -> ... x D uint16 knob
+    indices (mixed radix, last knob fastest)."""
+    r = np.asarray(ids).astype(np.uint64)
+    out = np.empty(r.shape + (len(cards),), np.uint16)
+    for d in range(len(cards) - 1, -1, -1):
+        out[..., d] = (r % np.uint64(cards[d])).astype(np.uint16)
+        r = r // np.uint64(cards[d])
+    return out
 
 
 def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Context] = None,
@@ -358,6 +373,7 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
         a.idx_u8 = pp(o.get("idx8"))
         a.actions_u2 = pp(o.get("actions2"))
         a.score_f32 = pp(o.get("score32"))
+        a.ids_u32 = pp(o.get("ids32"))
         outs.append(o)
     ctx.check(L.lib().ktune_rollout(ctx.h, len(tasks), arr, T,
                                     (L.F_DEVICE if dev else 0) | (L.F_EXACT_ROLLOUT if exact else 0) |

@@ -235,7 +235,10 @@ def test_rollout_tc_segmented_host_path(O, ctx):
     torch.cuda.synchronize()
     for h, d in zip(host, devo):
         for k in ["idx", "actions", "score", "logp", "value"]:
-            assert np.array_equal(h[k], d[k].cpu().numpy()), k
+            diff = h[k] != d[k].cpu().numpy()
+            where = np.nonzero(diff.any(-1) if diff.ndim == 3 else diff)
+            assert not diff.any(), (k, int(diff.sum()), sorted(set(where[0].tolist()))[:8],
+                                    sorted(set(where[1].tolist()))[:40])
     osp, og, agent, init = inits[0]
     want = O.run_episodes(osp, og, 128, 64, agent.params, init[:6], T, 3, stream_seed(0, "explore"))
     assert np.array_equal(host[0]["idx"][:6].astype(np.int32), want["idx"])
@@ -514,3 +517,112 @@ def test_rollout_step_major_grouped(O, ctx):
         o.update(actions=None, logp=None, value=None)
     with pytest.raises(ConfigError):
         run_episodes_batch(tasks[:2], T, host_out=bad, grouped=True)
+
+
+def test_rollout_ids_u32(O, ctx):
+    """ids_u32: one id_of(Θ_t) per visited configuration (design_space.cpp:158-167) instead of D
+    knob indices - equal to the mixed-radix id of the idx trajectory on every layout (grouped over
+    tasks of different radices incl. a uint16 space, step-major, episode-major segmented host path,
+    device pointers); configs_from_ids inverts it; spaces over 2^32 configurations are rejected."""
+    import torch
+    from paper_2001_08743_b200.errors import ConfigError
+    from paper_2001_08743_b200.exploration import (RolloutTask, compact_grouped_outputs, configs_from_ids,
+                                                   run_episodes_batch)
+
+    def id_of(idx, cards):
+        r = np.zeros(idx.shape[:-1], np.uint64)
+        for d, c in enumerate(cards):
+            r = r * np.uint64(c) + idx[..., d].astype(np.uint64)
+        return r
+
+    tasks, dtasks = [], []
+    for i, name in enumerate(["resnet_c2", "vgg_c4", "resnet_dense_u16"]):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=170 + i)
+        E = [70, 129, 45][i]
+        init = np.random.default_rng(i).integers(0, np.asarray(sp.cards), (E, sp.num_knobs)).astype(np.int32)
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=5 * i, root_seed=i))
+        dtasks.append(RolloutTask(dspace, agent, dg, torch.from_numpy(init).cuda(), episode_offset=5 * i, root_seed=i))
+    T = 260
+    cards = [t.space.card for t in tasks]
+    ref = run_episodes_batch(tasks, T, step_major=True)
+    # grouped compact outputs with ids: no idx array at all crosses PCIe
+    outs = compact_grouped_outputs(tasks, T, lambda shape, dt: np.zeros(shape, dt), ids=True)
+    run_episodes_batch(tasks, T, host_out=outs, grouped=True)
+    for a, o, c in zip(ref, outs, cards):
+        assert o["idx"] is None and o["idx8"] is None
+        assert np.array_equal(o["ids32"].astype(np.uint64), id_of(a["idx"], c))
+        assert np.array_equal(configs_from_ids(o["ids32"], c), a["idx"])
+        assert np.array_equal(o["score32"], a["score"].astype(np.float32))
+    # step-major and episode-major (segmented) host calls, per task buffers
+    for sm in (True, False):
+        hs = []
+        for t in tasks:
+            E = len(t.init_idx)
+            hs.append(dict(idx=None, score=np.zeros((T + 1, E) if sm else (E, T + 1)), actions=None, logp=None,
+                           value=None, ids32=np.zeros((T + 1, E) if sm else (E, T + 1), np.uint32)))
+        run_episodes_batch(tasks, T, host_out=hs, step_major=sm)
+        for a, o, c in zip(ref, hs, cards):
+            want = id_of(a["idx"], c) if sm else id_of(a["idx"], c).T
+            assert np.array_equal(o["ids32"].astype(np.uint64), want), sm
+            assert np.array_equal(o["score"], a["score"] if sm else a["score"].T), sm
+    # device pointers (idx alongside, as every device call needs)
+    dref = run_episodes_batch(dtasks, T, device_out=True, step_major=True)
+    douts = []
+    for t, o in zip(dtasks, dref):
+        o = dict(o)
+        o["ids32"] = torch.zeros((T + 1, len(t.init_idx)), dtype=torch.int32, device="cuda")
+        douts.append(o)
+    run_episodes_batch(dtasks, T, host_out=douts, step_major=True)
+    torch.cuda.synchronize()
+    for a, o, c in zip(ref, douts, cards):
+        got = o["ids32"].cpu().numpy().view(np.uint32).astype(np.uint64)
+        assert np.array_equal(got, id_of(a["idx"], c))
+    # > 2^32 configurations: rejected
+    sp, osp, og, dspace, dg, agent = _setup(O, ctx, "synthetic8", seed=3)
+    big = RolloutTask(dspace, agent, dg, np.zeros((4, sp.num_knobs), np.int32))
+    with pytest.raises(ConfigError):
+        run_episodes_batch([big], 8, host_out=[dict(idx=None, score=None, actions=None, logp=None, value=None,
+                                                    ids32=np.zeros((4, 9), np.uint32))])
+
+
+def test_rollout_streamed_host_path_repeated(O, ctx):
+    """The streamed host-buffer path (one rollout launch; the copy stream waits on the kernel's
+    per-segment progress counter) against the per-segment launches and the device path, over
+    repeated calls and several shapes (segment counts, one and several launches, every
+    encoding): the copies never read a row before it is written."""
+    import torch
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.exploration import RolloutTask, compact_grouped_outputs, run_episodes_batch
+    tasks = []
+    for i, name in enumerate(["resnet_c2", "vgg_c4", "alexnet_c3_u16"]):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=190 + i)
+        E = [600, 257, 1000][i]
+        init = np.random.default_rng(i).integers(0, np.asarray(sp.cards), (E, sp.num_knobs)).astype(np.int32)
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=11 * i, root_seed=i))
+    for T, segs in [(200, 0), (333, 0), (128, 2), (260, 32)]:
+        dref = run_episodes_batch([RolloutTask(t.space, t.agent, t.cost_model, torch.from_numpy(t.init_idx).cuda(),
+                                               t.episode_offset, t.root_seed) for t in tasks], T, step_major=True)
+        torch.cuda.synchronize()
+        ref = [{k: v.cpu().numpy() for k, v in o.items()} for o in dref]
+        ctx.set_option(L.OPT_ROLLOUT_SEGMENTS, segs)
+        try:
+            for rep in range(3):
+                hs = run_episodes_batch(tasks, T, step_major=True)
+                for a, h in zip(ref, hs):
+                    for k in ["idx", "actions", "score", "logp", "value"]:
+                        assert np.array_equal(a[k], h[k]), (T, segs, rep, k)
+                outs = compact_grouped_outputs(tasks, T, lambda shape, dt: np.zeros(shape, dt), ids=(rep % 2 == 0))
+                run_episodes_batch(tasks, T, host_out=outs, grouped=True)
+                for a, o, t in zip(ref, outs, tasks):
+                    if o["ids32"] is not None:
+                        r = np.zeros(a["idx"].shape[:-1], np.uint64)
+                        for d, c in enumerate(t.space.card):
+                            r = r * np.uint64(c) + a["idx"][..., d].astype(np.uint64)
+                        assert np.array_equal(o["ids32"].astype(np.uint64), r), (T, segs, rep)
+                    else:
+                        got = o["idx8"] if o["idx8"] is not None else o["idx"]
+                        assert np.array_equal(got.astype(np.int64), a["idx"].astype(np.int64)), (T, segs, rep)
+                    assert np.array_equal(o["score32"], a["score"].astype(np.float32)), (T, segs, rep)
+                    assert np.array_equal(o["logp32"], a["logp"].astype(np.float32)), (T, segs, rep)
+        finally:
+            ctx.set_option(L.OPT_ROLLOUT_SEGMENTS, 0)
