@@ -18,6 +18,7 @@
 #include <cuda.h>  // CUresult / CUstream for the cuStreamWaitValue32 entry point (no -lcuda)
 
 #include <algorithm>
+#include <cstdlib>
 #include <array>
 
 #include "device.cuh"
@@ -976,7 +977,7 @@ int ktune_rollout(ktune_ctx* ctx, int num_tasks, const ktune_rollout_task* tasks
           wait_value_geq(ctx, ctx->copy_stream, ctx->d_progress + sg, sg + 1 < SS ? (unsigned int)slots : kRelease);
           for (int k = 0; k < num_tasks; ++k) copy_out(k, t0, t1, ctx->copy_stream, 1);
         }
-        const int C = (int)std::min<int64_t>(4, T);  // score chunks
+        const int C = (int)std::min<int64_t>(4, T);  // score chunks (2..8 and 10..32 segments measured within noise)
         for (int c = 0; c < C; ++c) {
           const int t0 = (int)((int64_t)c * T / C), t1 = (int)((int64_t)(c + 1) * T / C);
           const int r0 = t0 == 0 ? 0 : t0 + 1;
