@@ -33,7 +33,8 @@ def host_empty(shape, dtype) -> np.ndarray:
     if _NP_TO_TORCH is None:
         _NP_TO_TORCH = {np.dtype(np.uint8): torch.uint8, np.dtype(np.int8): torch.int8,
                         np.dtype(np.uint16): torch.int16, np.dtype(np.int16): torch.int16,
-                        np.dtype(np.int32): torch.int32, np.dtype(np.float32): torch.float32,
+                        np.dtype(np.int32): torch.int32, np.dtype(np.uint32): torch.int32,
+                        np.dtype(np.float32): torch.float32,
                         np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64}
     dt = np.dtype(dtype)
     t = torch.empty(shape, dtype=_NP_TO_TORCH[dt], pin_memory=True)

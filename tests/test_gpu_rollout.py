@@ -328,8 +328,9 @@ def test_rollout_tc_check_mode_c2_shape(O, ctx):
     """The bench's FULL shape (BASELINE configs[1]: 12 ResNet-18 tasks x 4096 episodes x T = 500,
     one grouped launch) in check mode: all 196.6M knob decisions re-decided exactly, 0
     disagreements, the fast probabilities well inside the margin; the trajectories (device
-    buffers, step-major) equal the normal run's and the exact fp64 kernel's, and spot episodes
-    replay on the oracle."""
+    buffers, step-major) equal the normal run's and the exact fp64 kernel's, spot episodes
+    replay on the oracle, and the bench's end-to-end host call (streamed, configuration ids,
+    compact and full-precision encodings) returns the same trajectories."""
     import torch
     from paper_2001_08743_b200 import _lib as L
     from paper_2001_08743_b200 import spaces as S
@@ -378,6 +379,29 @@ def test_rollout_tc_check_mode_c2_shape(O, ctx):
             assert np.array_equal(fast[i]["idx"][:, e].cpu().numpy().astype(np.int32), w["idx"][0])
             assert np.array_equal(fast[i]["actions"][:, e].cpu().numpy(), w["actions"][0])
             assert np.array_equal(fast[i]["score"][:, e].cpu().numpy(), w["score"][0])
+    # the bench's end-to-end call at the same shape: host buffers, the streamed path, grouped
+    # step-major compact outputs (configuration ids, 2-bit actions, fp32 / fp64 values)
+    from paper_2001_08743_b200.context import host_empty
+    from paper_2001_08743_b200.exploration import compact_grouped_outputs, unpack_actions
+    htasks = [RolloutTask(t.space, t.agent, t.cost_model, o[3], episode_offset=0, root_seed=i)
+              for i, (t, o) in enumerate(zip(tasks, orc))]
+    for full in (False, True):
+        outs = compact_grouped_outputs(htasks, T, lambda shape, dt: host_empty(shape, dt), score64=full,
+                                       logp64=full, ids=True)
+        run_episodes_batch(htasks, T, host_out=outs, grouped=True)
+        for t, f, o in zip(tasks, fast, outs):
+            ids = torch.zeros(f["idx"].shape[:-1], dtype=torch.int64, device="cuda")
+            for d, c in enumerate(t.space.card):
+                ids = ids * int(c) + f["idx"][..., d].to(torch.int64)
+            assert np.array_equal(o["ids32"].astype(np.int64), ids.cpu().numpy())
+            assert np.array_equal(unpack_actions(o["actions2"], t.space.D), f["actions"].cpu().numpy())
+            sc, lp, va = (f[k].cpu().numpy() for k in ("score", "logp", "value"))
+            if full:
+                assert np.array_equal(o["score"], sc) and np.array_equal(o["logp"], lp) and np.array_equal(o["value"], va)
+            else:  # the fp32 values the kernel computed (the device path widens the same fp32 values)
+                assert np.array_equal(o["score32"], sc.astype(np.float32))
+                assert np.array_equal(o["logp32"], lp.astype(np.float32)) and np.array_equal(o["value32"], va.astype(np.float32))
+        del outs
     del chk, fast, exact
     torch.cuda.empty_cache()
 
