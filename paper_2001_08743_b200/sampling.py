@@ -115,28 +115,41 @@ def candidates_gather(space: Space, idx, predicted) -> CandidateSet:
 
 def _packed(space: Space, idx):
     if hasattr(idx, "is_cuda") and idx.is_cuda:
+        import torch
+        ok = (torch.uint8,) if space.index_bytes == 1 else (torch.uint16, torch.int16)
+        if idx.dtype not in ok or not idx.is_contiguous():
+            raise ConfigError(f"device points must be a contiguous tensor of {space.index_bytes}-byte knob indices "
+                              f"(got {idx.dtype})")
         return idx, True
     return np.ascontiguousarray(idx, dtype=space.idx_dtype).reshape(-1, space.D), False
 
 
 def kmeans_run(space: Space, idx, k: int, seed: int, max_iters: int = 100, restarts: int = 3) -> ClusterResult:
-    """kmeans_run (sampling.cpp:157-175) over lattice points given as knob indices."""
+    """kmeans_run (sampling.cpp:157-175) over lattice points given as knob indices.
+
+    Host arrays, or a CUDA tensor of points: then the centroids and assignments come back as
+    CUDA tensors and only the scalars (loss, per-iteration losses) cross PCIe."""
     arr, dev = _packed(space, idx)
     N = (arr.numel() if dev else arr.size) // space.D
-    cen = np.zeros((max(k, 1), space.D), np.float64)
-    asg = np.zeros(N, np.int32)
-    loss = C.c_double()
     il = np.zeros(max_iters + 1, np.float64)
     nl = C.c_int32()
-    out = L.KmeansOutC(cen.ctypes.data_as(C.c_void_p), asg.ctypes.data_as(C.c_void_p),
-                       C.cast(C.pointer(loss), C.c_void_p), il.ctypes.data_as(C.c_void_p),
-                       C.cast(C.pointer(nl), C.c_void_p))
+    if dev:
+        import torch
+        cen = torch.zeros((max(k, 1), space.D), dtype=torch.float64, device=arr.device)
+        asg = torch.zeros(N, dtype=torch.int32, device=arr.device)
+        dloss = torch.zeros(1, dtype=torch.float64, device=arr.device)
+        ptrs = [C.c_void_p(cen.data_ptr()), C.c_void_p(asg.data_ptr()), C.c_void_p(dloss.data_ptr())]
+    else:
+        cen = np.zeros((max(k, 1), space.D), np.float64)
+        asg = np.zeros(N, np.int32)
+        loss = C.c_double()
+        ptrs = [cen.ctypes.data_as(C.c_void_p), asg.ctypes.data_as(C.c_void_p), C.cast(C.pointer(loss), C.c_void_p)]
+    out = L.KmeansOutC(ptrs[0], ptrs[1], ptrs[2], il.ctypes.data_as(C.c_void_p), C.cast(C.pointer(nl), C.c_void_p))
     p = C.c_void_p(arr.data_ptr()) if dev else arr.ctypes.data_as(C.c_void_p)
-    if dev:  # device points, host outputs: stage through host result buffers
-        raise ConfigError("kmeans_run: pass host arrays (device-resident use goes through adaptive_sweep)")
     space.ctx.check(L.lib().ktune_kmeans_run(space.ctx.h, space.h, p, space.index_bytes, N, k, seed,
-                                             max_iters, restarts, C.byref(out), 0))
-    return ClusterResult(cen[:k], asg, loss.value, list(il[:nl.value]))
+                                             max_iters, restarts, C.byref(out), L.F_DEVICE if dev else 0))
+    lv = float(dloss.item()) if dev else loss.value
+    return ClusterResult(cen[:k], asg, lv, list(il[:nl.value]))
 
 
 def clusterer(space: Space, params: SamplingParams = SamplingParams()):

@@ -308,3 +308,33 @@ def test_kmeans_two_million_points_deterministic_and_exact(O, ctx, ref_ok):
     assert np.array_equal(runs[0].assignments, want["assignments"])
     assert np.array_equal(runs[0].centroids, want["centroids"])
     assert runs[0].l2_loss == want["loss"]
+
+
+@pytest.mark.parametrize("name,k", [("alexnet_c3_u16", 40), ("resnet_c2", 8)])
+def test_kmeans_run_device_points_equal_host(O, ctx, name, k):
+    """kmeans_run over a device-resident candidate set (the forced sweep's input): the same
+    centroids, assignments, loss and per-iteration losses as the host-array call."""
+    import torch
+    from paper_2001_08743_b200.sampling import kmeans_run
+    sp = SPACES[name]()
+    osp = O.OSpace(sp)
+    cidx, cids, _ = candidate_set(O, osp, 30_000, 3)
+    ds = _space(ctx, sp)
+    host = kmeans_run(ds, cidx, k, 77)
+    didx = torch.from_numpy(np.ascontiguousarray(cidx, dtype=ds.idx_dtype)).cuda()
+    dev = kmeans_run(ds, didx, k, 77)
+    assert torch.is_tensor(dev.centroids) and dev.centroids.is_cuda
+    assert np.array_equal(dev.centroids.cpu().numpy(), host.centroids)
+    assert np.array_equal(dev.assignments.cpu().numpy(), host.assignments)
+    assert dev.l2_loss == host.l2_loss and dev.iteration_losses == host.iteration_losses
+
+
+def test_kmeans_run_device_points_dtype_checked(ctx):
+    """Device points in the wrong index width are rejected, not reinterpreted."""
+    import torch
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.errors import ConfigError
+    from paper_2001_08743_b200.sampling import kmeans_run
+    ds = _space(ctx, S.synthetic_space(0, 4))
+    with pytest.raises(ConfigError, match="device points"):
+        kmeans_run(ds, torch.zeros((100, 4), dtype=torch.int64, device="cuda"), 2, 0)
