@@ -245,12 +245,6 @@ struct Cfg {
   }
 };
 
-// Step x opens a segment of a streamed rollout (segment of step x = floor(x nseg / T)).
-// 32-bit arithmetic (x nseg < 2^31: the host caps T nseg): inline, no 64-bit division call.
-__device__ __forceinline__ bool seg_boundary(int x, int nseg, int T) {
-  return (uint32_t)(x * nseg) / (uint32_t)T != (uint32_t)((x - 1) * nseg) / (uint32_t)T;
-}
-
 // Configuration id (design_space.cpp:158-167: mixed radix, last knob fastest); knobs >= n
 // have cardinality 1 and index 0, so the Horner chain runs branch-free over NMAX.
 template <int NMAX>
@@ -615,6 +609,12 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
     }
     const int gh = tk.ntrees / 2;  // the walk of row t runs in two halves inside step t's MMA waits
     uint32_t ph = 0;
+    // streamed variant: the first step of the next segment (segment of step x = floor(x nseg / T),
+    // so segment s starts at ceil(s T / nseg)); divisions only at the boundaries
+    int seg_next = 0;
+    if constexpr (kStream)
+      seg_next = (int)((((uint32_t)L.t_begin * (uint32_t)L.nseg) / (uint32_t)T + 1) * (uint32_t)T +
+                       (uint32_t)L.nseg - 1) / (uint32_t)L.nseg;
 #if KT_TC_TRACE
     const bool trace_cta = L.check == 2 && blockIdx.x == 0 && q == 0 && lane == 0;
 #endif
@@ -902,14 +902,16 @@ __global__ void __launch_bounds__(kThr, 1) rollout_tc_kernel(const __grid_consta
       ph ^= 1;
       TR(15)
       if constexpr (kStream) {
-      if (t + 1 < L.t_end && seg_boundary(t + 1, L.nseg, T)) {
-        __threadfence();  // this row's step-t outputs are visible GPU-wide (at L2) ...
-        sync_slot(slot);  // ... for every row of the slot
-        if (leader) {
-          __threadfence_system();
-          atomicAdd(L.progress + (uint32_t)(t * L.nseg) / (uint32_t)T, 1u);  // the segment step t closes
+        if (t + 1 == seg_next && t + 1 < L.t_end) {
+          __threadfence();  // this row's step-t outputs are visible GPU-wide (at L2) ...
+          sync_slot(slot);  // ... for every row of the slot
+          const uint32_t sg = (uint32_t)(t * L.nseg) / (uint32_t)T;  // the segment step t closes
+          if (leader) {
+            __threadfence_system();
+            atomicAdd(L.progress + sg, 1u);
+          }
+          seg_next = (int)(((sg + 2) * (uint32_t)T + (uint32_t)L.nseg - 1) / (uint32_t)L.nseg);
         }
-      }
       }
     }
 #undef TR

@@ -42,6 +42,12 @@ for _ in range(5):
     run_episodes_batch(htasks, T, ctx, host_out=out, grouped=True)
     ts.append(time.perf_counter() - t0)
 print(f"call wall ms (no profiler): median {1e3 * np.median(ts):.2f}  all {[round(1e3 * x, 2) for x in ts]}")
+ctx.set_option(L.OPT_PROFILE, 1)  # library-side CUDA events around the rollout / K1 launches
+ctx.reset_stats()
+for _ in range(5):
+    run_episodes_batch(htasks, T, ctx, host_out=out, grouped=True)
+print(f"event-timed: rollout {ctx.stat(L.STAT_ROLLOUT_NS) / 5e6:.3f} ms, K1 {ctx.stat(L.STAT_GBT_NS) / 5e6:.3f} ms per call")
+ctx.set_option(L.OPT_PROFILE, 0)
 from torch.profiler import profile, ProfilerActivity
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     run_episodes_batch(htasks, T, ctx, host_out=out, grouped=True)

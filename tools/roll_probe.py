@@ -45,6 +45,13 @@ keys = [L.STAT_ROLLOUT_NS, L.STAT_ROLLOUT_CALLS, L.STAT_GBT_NS, L.STAT_GBT_CALLS
 s0 = {k: ctx.stat(k) for k in keys}
 reps = int(os.environ.get("REPS", "5"))
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+if os.environ.get("DMA"):  # interference experiment: D2H copies on another stream during the rollout
+    cs = torch.cuda.Stream()
+    src = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    dst = torch.empty(64 << 20, dtype=torch.uint8, pin_memory=True)
+    with torch.cuda.stream(cs):
+        for _ in range(int(os.environ["DMA"])):
+            dst.copy_(src, non_blocking=True)
 ev0.record(stream)
 for i in range(reps):
     run_episodes_batch(tasks, T, ctx, host_out=out, step_major=sm)
