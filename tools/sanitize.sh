@@ -7,7 +7,8 @@ test_gpu_ppo.py test_gpu_sa.py::test_sa_spec_examples test_gpu_rollout.py::test_
 test_gpu_rollout.py::test_rollout_bit_exact test_gpu_kmeans.py::test_kmeans_run_matches_reference \
 test_gpu_kmeans.py::test_adaptive_sweep_and_snap_match_reference test_gpu_kmeans.py::test_snap_rule_fallback \
 test_gpu_kmeans.py::test_assign_paths_bit_exact test_gpu_kmeans.py::test_certified_lloyd_rescue \
-test_gpu_rollout.py::test_rollout_step_major_grouped"
+test_gpu_rollout.py::test_rollout_step_major_grouped test_gpu_rollout.py::test_rollout_tc_segmented_host_path \
+test_gpu_rollout.py::test_rollout_ids_u32"
 ARGS=""
 for t in $SEL; do ARGS="$ARGS tests/$t"; done
 for tool in memcheck racecheck synccheck initcheck; do
