@@ -168,6 +168,8 @@ struct KppState {
   int32_t fallbacks;   // picks decided by the exact parallel replay (kpp_x_* kernels)
   int32_t need_exact;  // set by kpp_select when the certified decision is undecided
   uint64_t rng_fb;     // generator state the exact replay starts from
+  int32_t c;           // index of the centroid the next kpp_d2 adds (advanced by kpp_select)
+  int32_t pad;
 };
 
 // d2[i] = (first ? v : min(d2[i], v)), v = |p_i - centroid c|^2, plus chunk sums.
@@ -175,8 +177,7 @@ template <class IdxT>
 __global__ void __launch_bounds__(kBT) kpp_d2_kernel(KtSpaceParams sp, int lut_total,
                                                      const IdxT* __restrict__ pts, int64_t N,
                                                      const KppState* __restrict__ st,
-                                                     double* __restrict__ cent, int c, int first,
-                                                     double* __restrict__ d2,
+                                                     double* __restrict__ cent, double* __restrict__ d2,
                                                      double* __restrict__ chunk_sum) {
   extern __shared__ double sdyn[];
   __shared__ double red[32];
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(kBT) kpp_d2_kernel(KtSpaceParams sp, int lut_t
   __syncthreads();  // the staged table is read below by other threads than those that wrote it
   const int D = sp.D;
   const int64_t pick = st->pick;
+  const int c = st->c, first = c == 0;  // the round's centroid index lives on the device (graph replay)
   if (threadIdx.x < D) {
     const double v = lut[sp.lut_off[threadIdx.x] + (int)pts[pick * D + threadIdx.x]];
     cs[threadIdx.x] = v;
@@ -227,6 +229,7 @@ __global__ void __launch_bounds__(1024) kpp_select_kernel(const double* __restri
   __shared__ int sh_bfirst, sh_bsecond;
   const int tid = threadIdx.x;
   uint64_t rng = st->rng;
+  if (mode == 1 && tid == 0) st->c += 1;  // kpp_d2 of this round has read it; the next round adds c + 1
   if (mode == 0) {
     if (tid == 0) {
       st->pick = (int64_t)kt::rng_below(rng, (uint64_t)N);
@@ -1790,30 +1793,76 @@ struct KMeans {
   cudaStream_t s() const { return ctx->stream; }
   int grid_pts() const { return (int)nchunks; }
 
+  // exact-replay workspace of kmeans++ (allocated before any capture: no cudaMalloc while capturing)
+  double* kpp_x_buffer() {
+    const int64_t S = kt::ceil_div(N, kt::xsum::kSeg);
+    return (double*)ctx->dev(kt::WS_KPP_X, (sizeof(double) + sizeof(kt::xsum::SegMap)) * kKppViews * S);
+  }
+
+  // One kmeans++ round: the distance update for centroid st->c, then (if another pick follows)
+  // the certified pick and its exact replay (a no-op unless kpp_select left the pick undecided).
+  // Nothing in it depends on the host, so it is captured once per KMeans object and replayed.
+  void kpp_round(bool pick) {
+    kpp_d2_kernel<IdxT><<<grid_pts(), kBT, lut_smem, s()>>>(sp->params, lut_total, pts, N, kst, cent_a, d2, chunk);
+    kt::check_launch(ctx, "kpp_d2");
+    if (!pick) return;
+    kpp_select_kernel<<<1, 1024, 0, s()>>>(d2, chunk, N, kst, 1, (int)ctx->opt_force_exact, scratch);
+    const int64_t S = kt::ceil_div(N, kt::xsum::kSeg);
+    double* xa = kpp_x_buffer();
+    kt::xsum::SegMap* xm = reinterpret_cast<kt::xsum::SegMap*>(xa + kKppViews * S);
+    const dim3 gv((unsigned)kt::ceil_div(S, 128), kKppViews);
+    kpp_x_partial_kernel<<<gv, 128, 0, s()>>>(d2, N, S, kst, xa);
+    kpp_x_prefix_kernel<<<1, 32 * kKppViews, 0, s()>>>(N, S, kst, xa);
+    kpp_x_map_kernel<<<gv, 128, 0, s()>>>(d2, N, S, kst, xa, xm);
+    kpp_x_pick_kernel<<<1, 128, 0, s()>>>(d2, N, S, kst, xm);
+    kt::check_launch(ctx, "kpp_select", 5);
+  }
+
+  // captured rounds, one per centroid buffer (cent_a and cent_b swap roles between restarts;
+  // every other pointer of the round is fixed for this object)
+  cudaGraphExec_t kpp_graph[2] = {nullptr, nullptr};
+  const double* kpp_graph_cent[2] = {nullptr, nullptr};
+  int64_t kpp_graph_force_exact[2] = {0, 0};
+  KMeans() = default;
+  KMeans(const KMeans&) = delete;
+  KMeans& operator=(const KMeans&) = delete;
+  ~KMeans() {
+    for (auto& g : kpp_graph)
+      if (g) cudaGraphExecDestroy(g);
+  }
+
   void kmeanspp(int k, uint64_t rng_seed) {
-    KppState h{rng_seed, 0, 0, 0, 0};
+    KppState h{rng_seed, 0, 0, 0, 0, 0, 0};
     KT_CUDA(cudaMemcpyAsync(kst, &h, sizeof(h), cudaMemcpyHostToDevice, s()));
     kpp_select_kernel<<<1, 1024, 0, s()>>>(d2, chunk, N, kst, 0, 0, scratch);
     kt::check_launch(ctx, "kpp_select");
-    const size_t smem = lut_smem;
+    // the host launch rate (6 launches per round) bounds an uncaptured kmeans++ round
+    const bool use_graph = !ctx->opt_profile && capturable(s()) && k > 2;
+    const int gi = kpp_graph_cent[0] == cent_a ? 0 : (kpp_graph_cent[1] == cent_a ? 1 : (kpp_graph[0] ? 1 : 0));
+    if (use_graph && kpp_graph[gi] &&
+        (kpp_graph_cent[gi] != cent_a || kpp_graph_force_exact[gi] != ctx->opt_force_exact)) {
+      cudaGraphExecDestroy(kpp_graph[gi]);
+      kpp_graph[gi] = nullptr;
+    }
     for (int c = 0; c < k; ++c) {
-      kpp_d2_kernel<IdxT><<<grid_pts(), kBT, smem, s()>>>(sp->params, lut_total, pts, N, kst, cent_a, c,
-                                                          c == 0 ? 1 : 0, d2, chunk);
-      kt::check_launch(ctx, "kpp_d2");
-      if (c + 1 < k) {
-        kpp_select_kernel<<<1, 1024, 0, s()>>>(d2, chunk, N, kst, 1, (int)ctx->opt_force_exact, scratch);
-        // exact replay, a no-op unless kpp_select left the pick undecided
-        const int64_t S = kt::ceil_div(N, kt::xsum::kSeg);
-        double* xa = (double*)ctx->dev(kt::WS_KPP_X, (sizeof(double) + sizeof(kt::xsum::SegMap)) * kKppViews * S);
-        kt::xsum::SegMap* xm = reinterpret_cast<kt::xsum::SegMap*>(xa + kKppViews * S);
-        const dim3 gv((unsigned)kt::ceil_div(S, 128), kKppViews);
-        kpp_x_partial_kernel<<<gv, 128, 0, s()>>>(d2, N, S, kst, xa);
-        kpp_x_prefix_kernel<<<1, 32 * kKppViews, 0, s()>>>(N, S, kst, xa);
-        kpp_x_map_kernel<<<gv, 128, 0, s()>>>(d2, N, S, kst, xa, xm);
-        kpp_x_pick_kernel<<<1, 128, 0, s()>>>(d2, N, S, kst, xm);
-        kt::check_launch(ctx, "kpp_select", 5);
-        ctx->stats[KTUNE_STAT_KPP_PICKS] += 1;
+      if (c + 1 < k && use_graph) {
+        if (!kpp_graph[gi]) {
+          kpp_x_buffer();
+          cudaGraph_t graph;
+          KT_CUDA(cudaStreamBeginCapture(s(), cudaStreamCaptureModeThreadLocal));
+          CaptureGuard cg{s()};
+          kpp_round(true);
+          cg.end(&graph);
+          KT_CUDA(cudaGraphInstantiate(&kpp_graph[gi], graph, 0));
+          cudaGraphDestroy(graph);
+          kpp_graph_cent[gi] = cent_a;
+          kpp_graph_force_exact[gi] = ctx->opt_force_exact;
+        }
+        KT_CUDA(cudaGraphLaunch(kpp_graph[gi], s()));
+      } else {
+        kpp_round(c + 1 < k);
       }
+      if (c + 1 < k) ctx->stats[KTUNE_STAT_KPP_PICKS] += 1;
     }
   }
 
