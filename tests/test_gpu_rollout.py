@@ -650,3 +650,25 @@ def test_rollout_streamed_host_path_repeated(O, ctx):
                     assert np.array_equal(o["logp32"], a["logp"].astype(np.float32)), (T, segs, rep)
         finally:
             ctx.set_option(L.OPT_ROLLOUT_SEGMENTS, 0)
+
+
+def test_rollout_streamed_more_tasks_than_one_launch(O, ctx):
+    """More tasks than one tcgen05 launch holds (several launches in stream order, every slot of
+    every launch counted per segment), host buffers: equal to the device path."""
+    import torch
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    names = ["resnet_c2", "vgg_c4", "synthetic8", "alexnet_c3_u16"]
+    tasks, dtasks = [], []
+    for i in range(20):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, names[i % 4], seed=300 + i)
+        E = 33 + 7 * i
+        init = np.random.default_rng(i).integers(0, np.asarray(sp.cards), (E, sp.num_knobs)).astype(np.int32)
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=i, root_seed=i))
+        dtasks.append(RolloutTask(dspace, agent, dg, torch.from_numpy(init).cuda(), episode_offset=i, root_seed=i))
+    T = 150
+    host = run_episodes_batch(tasks, T)
+    dev = run_episodes_batch(dtasks, T)
+    torch.cuda.synchronize()
+    for h, d in zip(host, dev):
+        for k in ["idx", "actions", "score", "logp", "value"]:
+            assert np.array_equal(h[k], d[k].cpu().numpy()), k
