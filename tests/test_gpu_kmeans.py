@@ -338,3 +338,38 @@ def test_kmeans_run_device_points_dtype_checked(ctx):
     ds = _space(ctx, S.synthetic_space(0, 4))
     with pytest.raises(ConfigError, match="device points"):
         kmeans_run(ds, torch.zeros((100, 4), dtype=torch.int64, device="cuda"), 2, 0)
+
+
+def test_kmeans_c4_scale_matches_reference(O, ctx):
+    """SURVEY C4 scale in the driver-run suite: kmeans_run over ~1M distinct AlexNet-conv2 candidates
+    (uint16 indices), k = 8, 3 restarts, equal to the REFERENCE's own kmeans_run (oracle/_ref:
+    assignments, centroids and loss bit for bit), from host arrays and from device-resident points;
+    and the whole adaptive sweep + snap equal to the reference's own adaptive_sample."""
+    import torch
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from paper_2001_08743_b200 import spaces as S
+    from paper_2001_08743_b200.sampling import kmeans_run
+    from workloads.tasks import random_configs
+    sp = S.alexnet_tasks()[1]
+    ds = _space(ctx, sp)
+    idx = random_configs(sp, 1 << 20, 123)
+    ids = ds.id_of(idx)
+    _, first = np.unique(ids, return_index=True)
+    idx = idx[np.sort(first)]
+    want = O.kmeans_run(O.OSpace(sp).encode(idx), 8, 11, restarts=3, impl="ref")
+    got = kmeans_run(ds, idx, 8, 11, restarts=3)
+    assert np.array_equal(got.assignments, want["assignments"])
+    assert np.array_equal(got.centroids, want["centroids"])
+    assert got.l2_loss == want["loss"]
+    dev = kmeans_run(ds, torch.from_numpy(np.ascontiguousarray(idx, dtype=ds.idx_dtype)).cuda(), 8, 11, restarts=3)
+    assert np.array_equal(dev.assignments.cpu().numpy(), want["assignments"])
+    assert dev.l2_loss == want["loss"]
+    from paper_2001_08743_b200.sampling import CandidateSet, SamplingParams, adaptive_sweep
+    ids = ds.id_of(idx)
+    pred = np.zeros(len(idx))
+    res = adaptive_sweep(ds, CandidateSet(idx, ids, pred), SamplingParams(), rng_seed=5)
+    ref = O.ref_adaptive_sample(O.OSpace(sp), idx, ids, pred, [], rng_seed=5)
+    assert res.k == len(ref["configs"])
+    assert np.allclose(res.k_losses, ref["k_losses"], rtol=1e-12, atol=0)
+    assert np.array_equal(res.snapped, ref["configs"])
