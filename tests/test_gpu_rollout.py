@@ -672,3 +672,29 @@ def test_rollout_streamed_more_tasks_than_one_launch(O, ctx):
     for h, d in zip(host, dev):
         for k in ["idx", "actions", "score", "logp", "value"]:
             assert np.array_equal(h[k], d[k].cpu().numpy()), k
+
+
+def test_rollout_c5_shape_equals_exact_kernel(O, ctx):
+    """SURVEY C5's shape in the driver-run suite (synthetic 16-knob space, 2^20 episodes: ~18
+    resident waves of the tcgen05 kernel), T = 48: visited configurations, actions and scores equal
+    to the exact fp64 kernel's, logp/value within 1e-5; spot episodes replay on the oracle."""
+    import torch
+    from paper_2001_08743_b200.exploration import RolloutTask, run_episodes_batch
+    from paper_2001_08743_b200.spaces import stream_seed
+    sp, osp, og, dspace, dg, agent = _setup(O, ctx, "synthetic16", seed=500)
+    E, T = 1 << 20, 48
+    init = torch.zeros((E, sp.num_knobs), dtype=torch.uint16, device="cuda")
+    task = RolloutTask(dspace, agent, dg, init, episode_offset=0, root_seed=9)
+    fast = run_episodes_batch([task], T, step_major=True)[0]
+    exact = run_episodes_batch([task], T, exact=True, step_major=True)[0]
+    torch.cuda.synchronize()
+    for k in ("idx", "actions", "score"):
+        assert torch.equal(fast[k], exact[k]), k
+    for k in ("logp", "value"):
+        assert bool(((fast[k] - exact[k]).abs() <= 1e-5 * exact[k].abs().clamp_min(1.0)).all()), k
+    for e in (0, 123_457, E - 1):
+        w = O.run_episodes(osp, og, 128, 64, agent.params, np.zeros((1, sp.num_knobs), np.int32), T, e,
+                           stream_seed(9, "explore"))
+        assert np.array_equal(fast["idx"][:, e].cpu().numpy().astype(np.int32), w["idx"][0])
+    del fast, exact
+    torch.cuda.empty_cache()
