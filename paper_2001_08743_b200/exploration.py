@@ -352,7 +352,7 @@ def run_episodes_batch(tasks: Sequence[RolloutTask], T: int, ctx: Optional[Conte
                          actions=host_empty(_shape(E, T, step_major, D), np.int8) if t.want_trajectory else None,
                          logp=host_empty(_shape(E, T, step_major), np.float64) if t.want_trajectory else None,
                          value=host_empty(_shape(E, T, step_major), np.float64) if t.want_trajectory else None)
-            pp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
+            pp = lambda a: None if a is None else a.__array_interface__["data"][0]  # int address: no ctypes objects
             init_p = init.ctypes.data_as(C.c_void_p)
             keep.append(init)
         a = arr[i]
@@ -476,7 +476,7 @@ def sa_search_batch(tasks: Sequence[SaTask], params: SaParams, ctx: Optional[Con
             init = np.ascontiguousarray(t.init_idx, np.uint16).reshape(-1, D)
             E = len(init)
             mk = lambda shape, dt: host_empty(shape, {"u16": np.uint16, "f64": np.float64, "u8": np.uint8}[dt])
-            pp = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
+            pp = lambda a: None if a is None else a.__array_interface__["data"][0]  # int address: no ctypes objects
         if host_out is not None:
             o = host_out[i]
         elif dev:

@@ -12,6 +12,7 @@ fixtures); the wrappers below build product `DesignSpace`s from it.
 """
 from __future__ import annotations
 
+import functools
 import json
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -37,6 +38,7 @@ def seed_combine(a: int, b: int) -> int:
     return mix64((a + 0x9E3779B97F4A7C15 + mix64(b)) & MASK64)
 
 
+@functools.lru_cache(maxsize=4096)
 def stream_seed(root: int, name: str) -> int:
     """FNV-1a named stream (rng.hpp:33-40)."""
     h = 0xCBF29CE484222325
