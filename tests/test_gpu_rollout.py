@@ -698,3 +698,33 @@ def test_rollout_c5_shape_equals_exact_kernel(O, ctx):
         assert np.array_equal(fast["idx"][:, e].cpu().numpy().astype(np.int32), w["idx"][0])
     del fast, exact
     torch.cuda.empty_cache()
+
+
+def test_rollout_segmented_fallback_path(O, ctx):
+    """KTUNE_OPT_ROLLOUT_STREAMED = 1 (one launch per segment: the path taken when the driver has
+    no stream memory operations) gives the same trajectories as the streamed default."""
+    from paper_2001_08743_b200 import _lib as L
+    from paper_2001_08743_b200.exploration import RolloutTask, compact_grouped_outputs, run_episodes_batch
+    tasks = []
+    for i, name in enumerate(["resnet_c2", "vgg_c4"]):
+        sp, osp, og, dspace, dg, agent = _setup(O, ctx, name, seed=400 + i)
+        E = [300, 170][i]
+        init = np.random.default_rng(i).integers(0, np.asarray(sp.cards), (E, sp.num_knobs)).astype(np.int32)
+        tasks.append(RolloutTask(dspace, agent, dg, init, episode_offset=i, root_seed=i))
+    T = 210
+    res = {}
+    for mode in (0, 1):
+        ctx.set_option(L.OPT_ROLLOUT_STREAMED, mode)
+        try:
+            plain = run_episodes_batch(tasks, T)
+            comp = compact_grouped_outputs(tasks, T, lambda shape, dt: np.zeros(shape, dt), ids=True)
+            run_episodes_batch(tasks, T, host_out=comp, grouped=True)
+        finally:
+            ctx.set_option(L.OPT_ROLLOUT_STREAMED, 0)
+        res[mode] = (plain, comp)
+    for a, b in zip(res[0][0], res[1][0]):
+        for k in ["idx", "actions", "score", "logp", "value"]:
+            assert np.array_equal(a[k], b[k]), k
+    for a, b in zip(res[0][1], res[1][1]):
+        for k in ["ids32", "actions2", "score32", "logp32", "value32"]:
+            assert np.array_equal(a[k], b[k]), k
