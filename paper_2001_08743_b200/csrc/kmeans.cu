@@ -2021,7 +2021,9 @@ struct KMeans {
   }
 
   // Exact Lloyd iterations it0 .. max_iters-1 from the exact state (asg_a, d2_a).
-  double lloyd_loop(int k, int it0, int max_iters, double loss, std::vector<double>& iter_losses) {
+  double lloyd_loop(int k, int it0, int max_iters, double loss, std::vector<double>& iter_losses,
+                    bool* converged = nullptr) {
+    if (converged) *converged = false;
     // Single-GPU iterations replay a captured CUDA graph (centroid update + assignment +
     // readback: ~20 launches): the loop is launch-bound at N = 1M. Two graphs, one per
     // parity of the a/b buffer swap.
@@ -2063,7 +2065,10 @@ struct KMeans {
       std::swap(d2_a, d2_b);
       loss = nl;
       iter_losses.push_back(nl);
-      if (changed == 0) break;
+      if (changed == 0) {
+        if (converged) *converged = true;
+        break;
+      }
     }
     return loss;
   }
@@ -2138,8 +2143,14 @@ struct KMeans {
     // previous assignment before later ones (its exact centroids reproduce the current one).
     int32_t* snap_asg = (int32_t*)ctx->dev(kt::WS_CERT_SNAP, (sizeof(int32_t) + sizeof(double)) * N);
     double* snap_d2 = reinterpret_cast<double*>(snap_asg + N);
-    auto rescue = [&](int t, double at_loss) {
+    // A rescue runs EXACT iterations from the batch start: one batch's worth, after which the
+    // integer sums are rebuilt from the exact assignment and certified batches resume (large
+    // lattice sets meet a near tie within the centroid bound now and then, not every
+    // iteration); from the third rescue of a run on, exactly to the end.
+    int rescues = 0;
+    auto rescue = [&](int t, double at_loss, bool* finished) {
       ctx->stats[KTUNE_STAT_KMEANS_ABORTS] += 1;
+      ++rescues;
       if (t == 0) {  // back to the exact initial assignment
         KT_CUDA(cudaMemcpyAsync(asg_a, snap_asg, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s()));
         KT_CUDA(cudaMemcpyAsync(d2_a, snap_d2, sizeof(double) * N, cudaMemcpyDeviceToDevice, s()));
@@ -2152,9 +2163,16 @@ struct KMeans {
         update_centroids(k, asg_b, d2_b, cent_a);
         assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);
       }
-      lloyd_loop(k, t, max_iters, at_loss, iter_losses);
+      const int limit = rescues >= 3 ? max_iters : std::min(max_iters, t + kCertBatch);
+      bool conv = false;
+      const size_t n0 = iter_losses.size();
+      const double l = lloyd_loop(k, t, limit, at_loss, iter_losses, &conv);
+      const int ran = (int)(iter_losses.size() - n0);
+      *finished = conv || t + ran >= max_iters;
+      return std::make_pair(t + ran, l);
     };
-    for (int it0 = 0; it0 < max_iters && !done; it0 += kCertBatch) {
+    while (iters < max_iters && !done) {
+      const int it0 = iters;
       const int nb = std::min(kCertBatch, max_iters - it0);
       if (iters == 0) {
         KT_CUDA(cudaMemcpyAsync(snap_asg, asg_a, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, s()));
@@ -2203,8 +2221,19 @@ struct KMeans {
           d2_a = da;
           d2_b = db;
           iter_losses.resize(nl_batch);
-          rescue(t_batch, loss_batch);
-          return true;
+          bool finished = false;
+          const auto [t_next, l_next] = rescue(t_batch, loss_batch, &finished);
+          if (finished) return true;  // exact to the end (the state lloyd_loop leaves)
+          // resume certified batches from the exact state: integer sums of asg_a, snapshot of
+          // asg_b (the previous assignment) at the next batch start
+          KT_CUDA(cudaMemsetAsync(isum[cur], 0, sizeof(unsigned long long) * words, s()));
+          cluster_sums_kernel<IdxT><<<(unsigned)nchunks, kBT, 0, s()>>>(pts, N, D, k, asg_a, isum[cur],
+                                                                        isum[cur] + (size_t)kt::kMaxK * kt::kMaxKnobs);
+          kt::check_launch(ctx, "cluster_sums");
+          if (!sharded) KT_CUDA(cudaMemsetAsync(ull, 0, 32, s()));
+          iters = t_next;
+          loss = l_next;
+          break;
         }
         ctx->stats[KTUNE_STAT_LLOYD_ITERS] += 1;
         if (h.loss > loss * (1.0 + 1e-9) + 1e-9 + loss_err(loss) + loss_err(h.loss))
