@@ -13,6 +13,7 @@
 //    outcome is not certified by the bound is re-decided by an exact
 //    sequential chain that reproduces the reference order bit-for-bit.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -2148,7 +2149,8 @@ struct KMeans {
     // lattice sets meet a near tie within the centroid bound now and then, not every
     // iteration); from the third rescue of a run on, exactly to the end.
     int rescues = 0;
-    auto rescue = [&](int t, double at_loss, bool* finished) {
+    constexpr int kMaxRescues = 3;  // caps 3, 5, 8 measured alike on C3 (<= 3 rescues per run)
+    auto rescue = [&](int t, int upto, double at_loss, bool* finished) {
       ctx->stats[KTUNE_STAT_KMEANS_ABORTS] += 1;
       ++rescues;
       if (t == 0) {  // back to the exact initial assignment
@@ -2163,7 +2165,7 @@ struct KMeans {
         update_centroids(k, asg_b, d2_b, cent_a);
         assign(cent_a, k, nullptr, asg_a, d2_a, nullptr);
       }
-      const int limit = rescues >= 3 ? max_iters : std::min(max_iters, t + kCertBatch);
+      const int limit = rescues >= kMaxRescues ? max_iters : std::min(max_iters, t + upto);
       bool conv = false;
       const size_t n0 = iter_losses.size();
       const double l = lloyd_loop(k, t, limit, at_loss, iter_losses, &conv);
@@ -2222,7 +2224,7 @@ struct KMeans {
           d2_b = db;
           iter_losses.resize(nl_batch);
           bool finished = false;
-          const auto [t_next, l_next] = rescue(t_batch, loss_batch, &finished);
+          const auto [t_next, l_next] = rescue(t_batch, kCertBatch, loss_batch, &finished);
           if (finished) return true;  // exact to the end (the state lloyd_loop leaves)
           // resume certified batches from the exact state: integer sums of asg_a, snapshot of
           // asg_b (the previous assignment) at the next batch start
