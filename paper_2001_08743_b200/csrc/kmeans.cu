@@ -139,21 +139,44 @@ __device__ double warp_exclusive_scan(double* a, int64_t n, int64_t stride) {
   return carry;
 }
 
-__device__ int warp_exclusive_scan_int(int32_t* a, int64_t n, int64_t stride) {
-  const int lane = threadIdx.x & 31;
-  int carry = 0;
-  for (int64_t i0 = 0; i0 < n; i0 += 32) {
-    const int64_t i = i0 + lane;
-    const int v = i < n ? a[i * stride] : 0;
-    int x = v;
+// Block-wide exclusive scans (blockDim.x = 1024) of a strided column, 1024 entries per round: the
+// exact-order centroid path scans ~N/1024 block counts and ~N/256 segment prefixes per (cluster,
+// knob), which one warp per column walked with a long latency chain at tens of millions of points.
+template <class T, class Add>
+__device__ T block_exclusive_scan(T* a, int64_t n, int64_t stride, Add add) {
+  __shared__ T wsum[32];
+  __shared__ T carry_sh;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_sh = T(0);
+  __syncthreads();
+  for (int64_t i0 = 0; i0 < n; i0 += 1024) {
+    const int64_t i = i0 + threadIdx.x;
+    const T v = i < n ? a[i * stride] : T(0);
+    T x = v;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffff, x, o);
-      if (lane >= o) x += y;
+      const T y = __shfl_up_sync(0xffffffff, x, o);
+      if (lane >= o) x = add(x, y);
     }
-    if (i < n) a[i * stride] = carry + x - v;
-    carry += __shfl_sync(0xffffffff, x, 31);
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      T s = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffff, s, o);
+        if (lane >= o) s = add(s, y);
+      }
+      wsum[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    const T before = add(carry_sh, w > 0 ? wsum[w - 1] : T(0));
+    if (i < n) a[i * stride] = add(before, x - v);
+    __syncthreads();
+    if (threadIdx.x == 0) carry_sh = add(carry_sh, wsum[31]);
+    __syncthreads();
   }
-  return carry;
+  return carry_sh;
 }
 
 // Load the feature LUT into shared memory.
@@ -906,29 +929,26 @@ __global__ void __launch_bounds__(kBT) hist_kernel(const int32_t* __restrict__ a
 
 // Exclusive scan over blocks per cluster; cluster totals, starts and the
 // per-cluster segment bases of the exact-sum machinery (csb[k+1]).
-__global__ void scan_counts_kernel(int32_t* __restrict__ blockcounts, int64_t nblocks, int k,
-                                   int32_t* __restrict__ counts, int32_t* __restrict__ cstart,
-                                   int32_t* __restrict__ csb) {
-  __shared__ int tot[kt::kMaxK];
-  const int w = threadIdx.x >> 5;  // warp per cluster
-  for (int c = w; c < k; c += blockDim.x >> 5) {
-    const int t = warp_exclusive_scan_int(blockcounts + c, nblocks, k);
-    if ((threadIdx.x & 31) == 0) {
-      tot[c] = t;
-      counts[c] = t;
-    }
+// One 1024-thread block per cluster: exclusive scan of its per-block counts (strided by k).
+__global__ void __launch_bounds__(1024) scan_counts_kernel(int32_t* __restrict__ blockcounts, int64_t nblocks,
+                                                           int k, int32_t* __restrict__ counts) {
+  const int c = blockIdx.x;
+  const int t = block_exclusive_scan<int32_t>(blockcounts + c, nblocks, k, [](int32_t a, int32_t b) { return a + b; });
+  if (threadIdx.x == 0) counts[c] = t;
+}
+
+// Cluster starts and segment starts from the cluster totals.
+__global__ void cluster_starts_kernel(const int32_t* __restrict__ counts, int k, int32_t* __restrict__ cstart,
+                                      int32_t* __restrict__ csb) {
+  if (threadIdx.x != 0) return;
+  int sum = 0, sb = 0;
+  for (int j = 0; j < k; ++j) {
+    cstart[j] = sum;
+    csb[j] = sb;
+    sum += counts[j];
+    sb += (counts[j] + kt::xsum::kSeg - 1) / kt::xsum::kSeg;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int sum = 0, sb = 0;
-    for (int j = 0; j < k; ++j) {
-      cstart[j] = sum;
-      csb[j] = sb;
-      sum += tot[j];
-      sb += (tot[j] + kt::xsum::kSeg - 1) / kt::xsum::kSeg;
-    }
-    csb[k] = sb;
-  }
+  csb[k] = sb;
 }
 
 // Stable scatter: warp w of the block owns points [base + w*128, base + (w+1)*128).
@@ -1009,11 +1029,13 @@ __global__ void xs_partial_kernel(KtSpaceParams sp, const IdxT* __restrict__ sor
 }
 
 // warp per (cluster c, knob d): exclusive prefix of the approximate segment sums.
-__global__ void xs_prefix_kernel(int D, const int32_t* __restrict__ csb, int k, double* __restrict__ approx) {
-  const int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (t >= k * D) return;
-  const int c = t / D, d = t % D;
-  warp_exclusive_scan(approx + (int64_t)csb[c] * D + d, csb[c + 1] - csb[c], D);
+// One 1024-thread block per (cluster, knob): the APPROXIMATE segment prefix (it only predicts the
+// binade each segment map is built for; a wrong prediction falls back to the plain chain).
+__global__ void __launch_bounds__(1024) xs_prefix_kernel(int D, const int32_t* __restrict__ csb, int k,
+                                                         double* __restrict__ approx) {
+  const int c = blockIdx.x / D, d = blockIdx.x % D;
+  block_exclusive_scan<double>(approx + (int64_t)csb[c] * D + d, csb[c + 1] - csb[c], D,
+                               [](double a, double b) { return kt::dadd(a, b); });
 }
 
 template <class IdxT>
@@ -1970,20 +1992,21 @@ struct KMeans {
   void update_centroids(int k, const int32_t* asg, const double* d2_old, double* next) {
     int32_t* cstart = counts + kt::kMaxK;
     hist_kernel<<<grid_pts(), kBT, 0, s()>>>(asg, N, k, blockcounts);
-    scan_counts_kernel<<<1, 1024, 0, s()>>>(blockcounts, nchunks, k, counts, cstart, csb);
+    scan_counts_kernel<<<k, 1024, 0, s()>>>(blockcounts, nchunks, k, counts);
+    cluster_starts_kernel<<<1, 32, 0, s()>>>(counts, k, cstart, csb);
     scatter_kernel<IdxT><<<grid_pts(), kBT, 0, s()>>>(asg, N, k, D, pts, blockcounts, cstart, members, sorted);
     // exact in-order centroid sums (exactsum.cuh)
     const int th = 256;
     const int gseg = (int)kt::ceil_div((int64_t)max_segs * D, th);
     xs_partial_kernel<IdxT><<<gseg, th, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, max_segs, xs_approx);
-    xs_prefix_kernel<<<(int)kt::ceil_div(k * D * 32, 128), 128, 0, s()>>>(D, csb, k, xs_approx);
+    xs_prefix_kernel<<<k * D, 1024, 0, s()>>>(D, csb, k, xs_approx);
     xs_map_kernel<IdxT><<<gseg, th, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, max_segs, xs_approx, xs_maps);
     xs_compose_kernel<IdxT><<<(int)kt::ceil_div(k * D * 32, 128), 128, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k,
                                                                           xs_maps, next, seqcnt);
     KT_CUDA(cudaMemsetAsync(counts + 2 * kt::kMaxK, 0, 4, s()));
     reseed_kernel<IdxT><<<1, 1024, 0, s()>>>(sp->params, pts, N, counts, k, d2_old, next,
                                              counts + 2 * kt::kMaxK);
-    kt::check_launch(ctx, "centroid update", 8);
+    kt::check_launch(ctx, "centroid update", 9);
   }
 
   // The reference's sequential loss (sampling.cpp:56-63), bit-exact, in parallel.
