@@ -1146,6 +1146,86 @@ __device__ __forceinline__ double warp_compose(At at, MapAt map_at, int nseg, in
   return s;
 }
 
+// Block-cooperative (1024 threads) version of warp_compose with bit-identical results: per round
+// of 1024 segment maps, the 32 warps compose their 32-map batches in parallel (the same scan and
+// uniform-binade test as warp_compose), then warp 0 walks the 32 batch results in order, taking
+// exactly warp_compose's per-batch decisions (identity batch, composed map, else per-segment maps
+// and sequential segments). The serial part drops from one warp scan + map load per 32 segments
+// to one apply per 32 segments.
+template <class At, class MapAt>
+__device__ double block_compose(At at, MapAt map_at, int nseg, int n, int* nseq_out) {
+  __shared__ kt::xsum::SegMap smaps[1024];
+  __shared__ kt::xsum::SegMap wmap[32];
+  __shared__ int wflag[32];  // 0: identity batch, 1: uniform (wmap valid to try), 2: per-segment
+  __shared__ double s_sh;
+  __shared__ int nseq_sh;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    s_sh = 0.0;  // MatrixXd::Zero / loss = 0.0 then += in order
+    nseq_sh = 0;
+  }
+  for (int sb0 = 0; sb0 < nseg; sb0 += 1024) {
+    {
+      const int g0 = sb0 + 32 * w;
+      const int mcount = min(32, nseg - g0);
+      kt::xsum::SegMap mine{0, 0, 0, 0};
+      if (lane < mcount) mine = map_at(g0 + lane);
+      smaps[32 * w + lane] = mine;
+      const unsigned real = __ballot_sync(0xffffffff, lane < mcount && mine.ok != 2);
+      int flag = 0;
+      if (real != 0) {
+        const int e0 = __shfl_sync(0xffffffff, mine.e, __ffs(real) - 1);
+        const bool uniform = __all_sync(0xffffffff, lane >= mcount || mine.ok == 2 || (mine.ok == 1 && mine.e == e0));
+        flag = 2;
+        if (uniform) {
+          uint64_t c0 = mine.F0, c1 = mine.F1;
+          for (int off = 1; off < 32; off <<= 1) {
+            const uint64_t p0 = __shfl_up_sync(0xffffffff, c0, off);
+            const uint64_t p1 = __shfl_up_sync(0xffffffff, c1, off);
+            if (lane >= off) {
+              const uint64_t n0 = p0 + ((p0 & 1u) ? c1 : c0);
+              const uint64_t n1 = p1 + (((1u + p1) & 1u) ? c1 : c0);
+              c0 = n0;
+              c1 = n1;
+            }
+          }
+          const uint64_t f0 = __shfl_sync(0xffffffff, c0, max(mcount, 1) - 1);
+          const uint64_t f1 = __shfl_sync(0xffffffff, c1, max(mcount, 1) - 1);
+          if (lane == 0) wmap[w] = kt::xsum::SegMap{f0, f1, e0, (f0 < (1ull << 53) && f1 < (1ull << 53)) ? 1 : 0};
+          flag = 1;
+        }
+      }
+      if (lane == 0) wflag[w] = mcount > 0 ? flag : 0;
+    }
+    __syncthreads();
+    if (w == 0) {
+      double s = s_sh;
+      int nseq = 0;
+      for (int b = 0; b < 32; ++b) {
+        const int g0 = sb0 + 32 * b;
+        if (g0 >= nseg) break;
+        const int fl = wflag[b];
+        if (fl == 0) continue;  // whole batch is identity (all-zero segments)
+        if (fl == 1 && s > 0.0 && kt::xsum::apply_map(s, wmap[b])) continue;
+        const int mcount = min(32, nseg - g0);
+        for (int q = 0; q < mcount; ++q) {
+          if (kt::xsum::apply_map(s, smaps[32 * b + q])) continue;
+          const int lo = (g0 + q) * kt::xsum::kSeg, hi = min(n, lo + kt::xsum::kSeg);
+          ++nseq;
+          s = warp_seq_segment(s, at, lo, hi);
+        }
+      }
+      if (lane == 0) {
+        s_sh = s;
+        nseq_sh += nseq;
+      }
+    }
+    __syncthreads();
+  }
+  *nseq_out = nseq_sh;
+  return s_sh;
+}
+
 // ---- kmeans++ exact replay (sampling.cpp:65-96), in parallel. Taken when the
 // certified pick is undecided (more likely at tens of millions of points, where the
 // rigorous bound of the parallel prefix grows like N u) or when forced. The reference
@@ -1323,27 +1403,26 @@ __global__ void __launch_bounds__(128) kpp_x_pick_kernel(const double* __restric
   }
 }
 
-// warp per (cluster c, knob d): compose the segment maps from s = 0 exactly;
+// 1024-thread block per (cluster c, knob d): compose the segment maps from s = 0 exactly;
 // centroid = s / count (sampling.cpp:110-121).
 template <class IdxT>
-__global__ void xs_compose_kernel(KtSpaceParams sp, const IdxT* __restrict__ sorted,
-                                  const int32_t* __restrict__ counts, const int32_t* __restrict__ cstart,
-                                  const int32_t* __restrict__ csb, int k,
-                                  const kt::xsum::SegMap* __restrict__ maps, double* __restrict__ cent,
-                                  int32_t* __restrict__ seq_segments) {
+__global__ void __launch_bounds__(1024) xs_compose_kernel(KtSpaceParams sp, const IdxT* __restrict__ sorted,
+                                                          const int32_t* __restrict__ counts,
+                                                          const int32_t* __restrict__ cstart,
+                                                          const int32_t* __restrict__ csb, int k,
+                                                          const kt::xsum::SegMap* __restrict__ maps,
+                                                          double* __restrict__ cent, int32_t* __restrict__ seq_segments) {
   const int D = sp.D;
-  const int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (t >= k * D) return;
-  const int c = t / D, d = t % D;
+  const int c = blockIdx.x / D, d = blockIdx.x % D;
   const int n = counts[c];
   if (n == 0) return;  // empty cluster: reseeded
   const double* lut = sp.lut + sp.lut_off[d];
   const IdxT* rows = sorted + (int64_t)cstart[c] * D + d;
   const int gb = csb[c], nseg = csb[c + 1] - csb[c];
   int nseq = 0;
-  const double s = warp_compose([&](int i) { return __ldg(lut + (int)rows[(int64_t)i * D]); },
-                                [&](int g) { return maps[(int64_t)(gb + g) * D + d]; }, nseg, n, &nseq);
-  if ((threadIdx.x & 31) == 0) {
+  const double s = block_compose([&](int i) { return __ldg(lut + (int)rows[(int64_t)i * D]); },
+                                 [&](int g) { return maps[(int64_t)(gb + g) * D + d]; }, nseg, n, &nseq);
+  if (threadIdx.x == 0) {
     cent[c * D + d] = kt::ddiv(s, (double)n);
     if (nseq) atomicAdd(seq_segments, nseq);
   }
@@ -1371,19 +1450,20 @@ __global__ void xs_loss_map_kernel(const double* __restrict__ x, int64_t N, cons
                             : kt::xsum::zero_segment_map(at, len);
 }
 
-__global__ void xs_loss_compose_kernel(const double* __restrict__ x, int64_t N,
-                                       const double* __restrict__ approx, double* __restrict__ prefix,
-                                       const kt::xsum::SegMap* __restrict__ maps, int phase, double* out) {
-  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+__global__ void __launch_bounds__(1024) xs_loss_compose_kernel(const double* __restrict__ x, int64_t N,
+                                                               const double* __restrict__ approx,
+                                                               double* __restrict__ prefix,
+                                                               const kt::xsum::SegMap* __restrict__ maps, int phase,
+                                                               double* out) {
   const int64_t nseg = (N + kt::xsum::kSeg - 1) / kt::xsum::kSeg;
   if (phase == 0) {  // exclusive prefix of the approximate segment sums
-    for (int64_t g = threadIdx.x; g < nseg; g += 32) prefix[g] = approx[g];
-    __syncwarp();
-    warp_exclusive_scan(prefix, nseg, 1);
+    for (int64_t g = threadIdx.x; g < nseg; g += blockDim.x) prefix[g] = approx[g];
+    __syncthreads();
+    block_exclusive_scan<double>(prefix, nseg, 1, [](double a, double b) { return kt::dadd(a, b); });
     return;
   }
   int nseq = 0;
-  const double s = warp_compose([&](int i) { return x[i]; }, [&](int g) { return maps[g]; }, (int)nseg, (int)N, &nseq);
+  const double s = block_compose([&](int i) { return x[i]; }, [&](int g) { return maps[g]; }, (int)nseg, (int)N, &nseq);
   if (threadIdx.x == 0) *out = s;
 }
 
@@ -2001,8 +2081,8 @@ struct KMeans {
     xs_partial_kernel<IdxT><<<gseg, th, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, max_segs, xs_approx);
     xs_prefix_kernel<<<k * D, 1024, 0, s()>>>(D, csb, k, xs_approx);
     xs_map_kernel<IdxT><<<gseg, th, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, max_segs, xs_approx, xs_maps);
-    xs_compose_kernel<IdxT><<<(int)kt::ceil_div(k * D * 32, 128), 128, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k,
-                                                                          xs_maps, next, seqcnt);
+    xs_compose_kernel<IdxT><<<k * D, 1024, 0, s()>>>(sp->params, sorted, counts, cstart, csb, k, xs_maps, next,
+                                                     seqcnt);
     KT_CUDA(cudaMemsetAsync(counts + 2 * kt::kMaxK, 0, 4, s()));
     reseed_kernel<IdxT><<<1, 1024, 0, s()>>>(sp->params, pts, N, counts, k, d2_old, next,
                                              counts + 2 * kt::kMaxK);
@@ -2014,9 +2094,9 @@ struct KMeans {
     const int64_t nseg = kt::ceil_div(N, kt::xsum::kSeg);
     const int g = (int)kt::ceil_div(nseg, 128);
     xs_loss_partial_kernel<<<g, 128, 0, s()>>>(dd, N, xs_approx);
-    xs_loss_compose_kernel<<<1, 32, 0, s()>>>(dd, N, xs_approx, xs_approx + nseg, xs_maps, 0, dscal + 1);
+    xs_loss_compose_kernel<<<1, 1024, 0, s()>>>(dd, N, xs_approx, xs_approx + nseg, xs_maps, 0, dscal + 1);
     xs_loss_map_kernel<<<g, 128, 0, s()>>>(dd, N, xs_approx + nseg, xs_maps);
-    xs_loss_compose_kernel<<<1, 32, 0, s()>>>(dd, N, xs_approx, xs_approx + nseg, xs_maps, 1, dscal + 1);
+    xs_loss_compose_kernel<<<1, 1024, 0, s()>>>(dd, N, xs_approx, xs_approx + nseg, xs_maps, 1, dscal + 1);
     kt::check_launch(ctx, "exact loss", 4);
     double v;
     KT_CUDA(cudaMemcpyAsync(&v, dscal + 1, 8, cudaMemcpyDeviceToHost, s()));
