@@ -490,11 +490,16 @@ __global__ void __launch_bounds__(kBT) cluster_sums_kernel(const IdxT* __restric
   for (int i = threadIdx.x; i < k * D; i += blockDim.x) s_sum[i] = 0;
   for (int i = threadIdx.x; i < k; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  for (int j = 0; j < kChunk / kBT; ++j) {
-    const int64_t i = base + j * kBT + threadIdx.x;
-    const bool live = i < N;
-    warp_cluster_sums(live, live ? asg[i] : 0, pts + (live ? i : 0) * D, D, s_sum, s_cnt);
+  // grid-stride over the chunks: a few blocks per SM, so that the k (D + 1) global atomics of the
+  // flush are paid per block, not per 1024 points (27k blocks contended on the same words at 27.7M)
+  const int64_t nch = (N + kChunk - 1) / kChunk;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    const int64_t base = ch * kChunk;
+    for (int j = 0; j < kChunk / kBT; ++j) {
+      const int64_t i = base + j * kBT + threadIdx.x;
+      const bool live = i < N;
+      warp_cluster_sums(live, live ? asg[i] : 0, pts + (live ? i : 0) * D, D, s_sum, s_cnt);
+    }
   }
   __syncthreads();
   flush_cluster_sums(k, D, s_sum, s_cnt, g_sum, g_cnt);
@@ -1894,6 +1899,12 @@ struct KMeans {
   }
 
   cudaStream_t s() const { return ctx->stream; }
+  // cluster_sums_kernel grid: a few blocks per SM, at most 1024 chunks (1M points) per block so that
+  // its int32 shared-memory sums (<= 2^20 x 2047) cannot overflow
+  unsigned sums_grid() const {
+    return (unsigned)std::max<int64_t>(std::min<int64_t>(nchunks, (int64_t)kt::sm_count(ctx) * 8),
+                                       kt::ceil_div(nchunks, 1024));
+  }
   int grid_pts() const { return (int)nchunks; }
 
   // exact-replay workspace of kmeans++ (allocated before any capture: no cudaMalloc while capturing)
@@ -2189,7 +2200,7 @@ struct KMeans {
     const size_t tsmem = cert_smem_bytes(k, D, D <= 8 ? 8 : (D <= 16 ? 16 : kt::kMaxKnobs), lut_smem);  // <= screen_smem
     int cur = 0;
     KT_CUDA(cudaMemsetAsync(isum[cur], 0, sizeof(unsigned long long) * words, s()));
-    cluster_sums_kernel<IdxT><<<(unsigned)nchunks, kBT, 0, s()>>>(pts, N, D, k, asg_a, isum[cur],
+    cluster_sums_kernel<IdxT><<<sums_grid(), kBT, 0, s()>>>(pts, N, D, k, asg_a, isum[cur],
                                                                   isum[cur] + (size_t)kt::kMaxK * kt::kMaxKnobs);
     kt::check_launch(ctx, "cluster_sums");
     // Iterations run in batches of kCertBatch replayed CUDA graphs (one per parity of the
@@ -2332,7 +2343,7 @@ struct KMeans {
           // resume certified batches from the exact state: integer sums of asg_a, snapshot of
           // asg_b (the previous assignment) at the next batch start
           KT_CUDA(cudaMemsetAsync(isum[cur], 0, sizeof(unsigned long long) * words, s()));
-          cluster_sums_kernel<IdxT><<<(unsigned)nchunks, kBT, 0, s()>>>(pts, N, D, k, asg_a, isum[cur],
+          cluster_sums_kernel<IdxT><<<sums_grid(), kBT, 0, s()>>>(pts, N, D, k, asg_a, isum[cur],
                                                                         isum[cur] + (size_t)kt::kMaxK * kt::kMaxKnobs);
           kt::check_launch(ctx, "cluster_sums");
           if (!sharded) KT_CUDA(cudaMemsetAsync(ull, 0, 32, s()));
