@@ -1206,6 +1206,7 @@ __device__ double block_compose(At at, MapAt map_at, int nseg, int n, int* nseq_
     if (w == 0) {
       double s = s_sh;
       int nseq = 0;
+      __syncwarp();  // every lane holds the round's start value before lane 0 may overwrite it
       for (int b = 0; b < 32; ++b) {
         const int g0 = sb0 + 32 * b;
         if (g0 >= nseg) break;
