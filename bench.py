@@ -358,7 +358,9 @@ def c3_pipeline(ctx, args, rank=0, world=1):
         torch.cuda.synchronize()
         roll.append(mx(time.perf_counter() - t0))
     t_roll = float(np.median(roll))
+    cidx = cids = rows = ids = sw = c = None
     for _ in range(2):  # the second pass is timed (the first sizes the workspaces)
+        cidx = cids = rows = ids = sw = c = None  # release the first pass's candidate set (allocator reuse)
         barrier()
         t1 = time.perf_counter()
         if world > 1:
