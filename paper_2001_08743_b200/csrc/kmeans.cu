@@ -997,7 +997,14 @@ __global__ void __launch_bounds__(kBT) scatter_kernel(const int32_t* __restrict_
     if (ok) {
       const int64_t pos = cstart[c] + blockoffs[(int64_t)blockIdx.x * k + c] + wcnt[w][c] + before;
       members[pos] = (int32_t)i;
-      for (int d = 0; d < D; ++d) sorted[pos * D + d] = pts[i * D + d];
+      if (D == 8) {  // the 8-knob row as one vector (8 or 16 bytes) instead of 8 scattered stores
+        if constexpr (sizeof(IdxT) == 1)
+          *reinterpret_cast<uint2*>(sorted + pos * 8) = __ldg(reinterpret_cast<const uint2*>(pts + i * 8));
+        else
+          *reinterpret_cast<uint4*>(sorted + pos * 8) = __ldg(reinterpret_cast<const uint4*>(pts + i * 8));
+      } else {
+        for (int d = 0; d < D; ++d) sorted[pos * D + d] = pts[i * D + d];
+      }
     }
     __syncwarp();
     if (ok && before == 0) wcnt[w][c] += __popc(m);
